@@ -1,0 +1,370 @@
+"""Generate golden fixtures by running the REFERENCE implementation (build container only).
+
+Usage (from the repo root, in the container that mounts /root/reference):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_goldens.py
+
+The reference package is imported read-only from /root/reference/pkg/src; nothing
+is written there.  Outputs go to tests/golden/*.npz together with the numpy /
+scipy versions that produced them (numpy PCG64/SeedSequence and scipy qhull are
+the reference's unpinned third-party dependencies).  The GPU box
+never runs this script; it only reads the committed .npz files.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import scipy
+
+REF = Path("/root/reference/pkg/src")
+REPO = Path(__file__).resolve().parents[2]
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(REPO))
+
+import volcache.renderer as vr  # noqa: E402
+import volcache.subdivision as vs  # noqa: E402
+from volcache import cache as vcache  # noqa: E402
+from volcache import formfactor as vff  # noqa: E402
+from volcache import scene as vscene  # noqa: E402
+
+from paper_1805_09258_b200 import configs  # noqa: E402
+from paper_1805_09258_b200.scene import scene_arrays, scene_to_dict  # noqa: E402
+
+VERSIONS = np.array([np.__version__, scipy.__version__])
+
+
+def ref_scene(scene):
+    return vscene.scene_from_dict(scene_to_dict(scene))
+
+
+def scene_fields(prefix, scene):
+    dim, V, E, A = scene_arrays(scene)
+    return {
+        f"{prefix}verts": V,
+        f"{prefix}emission": E,
+        f"{prefix}albedo": A,
+        f"{prefix}bmin": np.asarray(scene.bounds_min, float),
+        f"{prefix}bmax": np.asarray(scene.bounds_max, float),
+        f"{prefix}sigma": np.array([scene.medium.sigma_s, scene.medium.sigma_a]),
+    }
+
+
+# ---------------------------------------------------------------------------
+
+
+def gen_formfactors():
+    rng = np.random.default_rng(1234)
+    m = 256
+    x2 = rng.uniform(-1, 1, (m, 2))
+    y0 = rng.uniform(-1, 1, (m, 2))
+    y1 = rng.uniform(-1, 1, (m, 2))
+    y1[:8] = y0[:8] + 1e-7 * rng.normal(size=(8, 2))  # thin → degenerate γ
+    y0[8:12] = x2[8:12]  # vertex coincidence
+    ok2, v2, g2, h2 = vff.ff_segment_derivs_batch(x2, y0, y1)
+    x3 = rng.uniform(-1, 1, (m, 3))
+    t1 = rng.uniform(-1, 1, (m, 3))
+    t2 = rng.uniform(-1, 1, (m, 3))
+    t3 = rng.uniform(-1, 1, (m, 3))
+    t3[:8] = x3[:8] + 0.3 * (t1[:8] - x3[:8]) + 0.6 * (t2[:8] - x3[:8])  # coplanar with x
+    t1[8:12] = x3[8:12]
+    ok3, v3, g3, h3 = vff.ff_triangle_derivs_batch(x3, t1, t2, t3)
+    np.savez_compressed(
+        OUT / "formfactors.npz", versions=VERSIONS,
+        seg_x=x2, seg_y0=y0, seg_y1=y1, seg_ok=ok2, seg_val=v2, seg_grad=g2, seg_hess=h2,
+        tri_x=x3, tri_y1=t1, tri_y2=t2, tri_y3=t3, tri_ok=ok3, tri_val=v3, tri_grad=g3, tri_hess=h3,
+    )
+
+
+def gen_trace():
+    out = {"versions": VERSIONS}
+    rng = np.random.default_rng(99)
+    cases = {
+        "c1": configs.cfg1_scene(),
+        "c2": configs.cfg2_scene(),
+        "room": configs.cfg3_scene(n_spheres=4, level=1),
+    }
+    for name, sc in cases.items():
+        rs = ref_scene(sc)
+        d = rs.dim
+        m = 2048
+        o = rng.uniform(rs.bounds_min, rs.bounds_max, (m, d))
+        dirs = rng.normal(size=(m, d))
+        dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+        s, idx = vscene.trace_or_bounds(rs, o, dirs)
+        out.update(scene_fields(f"{name}_", sc))
+        out[f"{name}_o"] = o
+        out[f"{name}_d"] = dirs
+        out[f"{name}_s"] = s
+        out[f"{name}_idx"] = idx
+    np.savez_compressed(OUT / "trace.npz", **out)
+
+
+class Capture:
+    """Monkeypatch hooks recording the direction set and primary trace of one build."""
+
+    def __init__(self, inject=None):
+        self.inject = inject
+        self.dirs = None
+        self.s = None
+        self.idx = None
+
+    def __enter__(self):
+        self._sd = vs.stratified_directions
+        self._tb = vs.trace_or_bounds
+        cap = self
+
+        def sd(dim, n, rng_seed=None, jitter=True):
+            ds = cap._sd(dim, n, rng_seed, jitter)
+            if cap.inject is not None:
+                ds = vscene.DirectionSet(ds.dim, ds.directions, np.asarray(cap.inject), ds.stratum_measure)
+            cap.dirs = ds
+            return ds
+
+        def tb(scene, o, d):
+            s, idx = cap._tb(scene, o, d)
+            if cap.s is None:
+                cap.s, cap.idx = s, idx
+            return s, idx
+
+        vs.stratified_directions = sd
+        vs.trace_or_bounds = tb
+        return self
+
+    def __exit__(self, *a):
+        vs.stratified_directions = self._sd
+        vs.trace_or_bounds = self._tb
+
+
+def canonical_rotation(adj):
+    """Rotate each simplex so its smallest index comes first (keeps orientation)."""
+    adj = np.asarray(adj)
+    k = np.argmin(adj, axis=1)
+    return np.stack([adj[np.arange(len(adj)), (k + j) % 3] for j in range(3)], axis=1)
+
+
+def gen_records():
+    bundled = Path("/root/reference/pkg/scenes")
+    pen = vscene.load_scene(bundled / "penumbra2d.json")
+    box = vscene.load_scene(bundled / "box3d.json")
+    c1 = configs.cfg1()
+    c2 = configs.cfg2()
+    refl2d = configs.cfg1_scene()
+    refl2d = type(refl2d)(
+        tuple(
+            type(s)(vertices=s.vertices, emission=s.emission, albedo=(0.0 if s.is_emitter else 0.6))
+            for s in refl2d.surfaces
+        ),
+        refl2d.medium, refl2d.bounds_min, refl2d.bounds_max,
+    )
+    box_refl = vscene.Scene(
+        surfaces=tuple(
+            vscene.Surface(vertices=s.vertices, emission=s.emission, albedo=(0.0 if s.is_emitter else 0.5))
+            for s in box.surfaces
+        ),
+        medium=box.medium, bounds_min=box.bounds_min, bounds_max=box.bounds_max,
+    )
+    room = configs.cfg3_scene(n_spheres=4, level=1)
+    room_pts = np.random.default_rng(2).uniform(room.bounds_min, room.bounds_max, (2, 3))
+    # name: (scene, points, cfg_seed, n_angular, march_step, n_inner, n_light, inject_canonical)
+    cases = {
+        "cfg1_surf": (c1.scene, c1.points[:8], 0, 1024, 4.0, 1, 16, False),
+        "cfg1_m01": (c1.scene, c1.points[:4], 0, 1024, 0.1, 1, 16, False),
+        "pen2d": (pen, np.array([[0.15, 0.6], [0.5, 0.35], [0.3, 0.45], [0.8, 0.2]]), 7, 256, 0.05, 2, 16, False),
+        "refl2d": (refl2d, c1.points[:4], 0, 256, 0.1, 1, 16, False),
+        "cfg2_surf": (c2.scene, c2.points[:4], 1, 4096, 4.0, 1, 16, False),
+        "cfg2_m01": (c2.scene, c2.points[:3], 1, 4096, 0.1, 1, 16, False),
+        "cfg2_m01_canon": (c2.scene, c2.points[:3], 1, 4096, 0.1, 1, 16, True),
+        "box3d_refl": (box_refl, np.array([[0.5, 0.5, 0.5], [0.2, 0.7, 0.3]]), 5, 256, 0.25, 2, 4, False),
+        "room_small": (room, room_pts, 2, 1024, 0.2, 1, 16, False),
+    }
+    for name, (sc, pts, cseed, n, step, n_inner, n_light, canon) in cases.items():
+        rs = sc if isinstance(sc, vscene.Scene) else ref_scene(sc)
+        N, d = pts.shape
+        res = {k: [] for k in ("L", "grad", "hess", "stats", "dirs", "adj", "s", "idx",
+                               "rec_value", "rec_grad", "rec_axes", "rec_radii", "rec_iso_radii")}
+        for i in range(N):
+            seed = vr._seed(cseed, 401, i)
+            inject = None
+            if canon:
+                with Capture() as c0:
+                    vs.build_subdivision(rs, pts[i], n_angular=n, march_step=step,
+                                         rng_seed=vr._seed(cseed, 401, i), n_inner=n_inner,
+                                         n_light_samples=n_light)
+                inject = canonical_rotation(c0.dirs.adjacency)
+            with Capture(inject) as cap:
+                sub = vs.build_subdivision(rs, pts[i], n_angular=n, march_step=step, rng_seed=seed,
+                                           n_inner=n_inner, n_light_samples=n_light)
+            single, multiple, stats = vs.assemble_moments(sub, rs.medium)
+            res["L"].append([single.L, multiple.L])
+            res["grad"].append([single.grad, multiple.grad])
+            res["hess"].append([single.hess, multiple.hess])
+            res["stats"].append([stats["elements_evaluated"], stats["elements_dropped"], stats["star_vertices"]])
+            res["dirs"].append(cap.dirs.directions)
+            res["adj"].append(cap.dirs.adjacency)
+            res["s"].append(cap.s)
+            res["idx"].append(cap.idx)
+            rv, rg, ra, rr, ri = [], [], [], [], []
+            for mom in (single, multiple):
+                rec = vcache.make_record(pts[i], mom, 0.05, rs.scale, rs.max_emission, anisotropic=True)
+                iso = vcache.make_record(pts[i], mom, 0.05, rs.scale, rs.max_emission, anisotropic=False)
+                rv.append(rec.value)
+                rg.append(rec.grad)
+                ra.append(rec.axes)
+                rr.append(rec.radii)
+                ri.append(iso.radii)
+            res["rec_value"].append(rv)
+            res["rec_grad"].append(rg)
+            res["rec_axes"].append(ra)
+            res["rec_radii"].append(rr)
+            res["rec_iso_radii"].append(ri)
+        out = {k: np.array(v) for k, v in res.items()}
+        out.update(scene_fields("", rs))
+        out.update(
+            versions=VERSIONS, points=pts, cfg_seed=np.array(cseed),
+            params=np.array([n, step, n_inner, n_light, 1.0 if canon else 0.0]),
+        )
+        np.savez_compressed(OUT / f"rec_{name}.npz", **out)
+        print("wrote", name, flush=True)
+
+
+def gen_make_record():
+    """Eigen/radii edge cases through the reference make_record."""
+    rng = np.random.default_rng(77)
+    cases = []
+    for dim in (2, 3):
+        for kind in ("random", "zero", "rank1", "repeated", "negdef", "tiny", "diag"):
+            for _ in range(4):
+                L = rng.uniform(0.0, 3.0, 3)
+                g = rng.normal(size=(3, dim))
+                if kind == "random":
+                    H = rng.normal(size=(3, dim, dim))
+                elif kind == "zero":
+                    H = np.zeros((3, dim, dim))
+                elif kind == "rank1":
+                    v = rng.normal(size=dim)
+                    H = np.einsum("c,i,j->cij", rng.uniform(0.5, 2, 3), v, v)
+                elif kind == "repeated":
+                    H = np.broadcast_to(np.eye(dim) * rng.uniform(-2, 2), (3, dim, dim)).copy()
+                    H[:, 0, 0] += 1e-9
+                elif kind == "negdef":
+                    Q = np.linalg.qr(rng.normal(size=(dim, dim)))[0]
+                    H = np.broadcast_to(-Q @ np.diag(rng.uniform(1, 5, dim)) @ Q.T, (3, dim, dim)).copy()
+                elif kind == "tiny":
+                    H = 1e-20 * rng.normal(size=(3, dim, dim))
+                else:
+                    H = np.broadcast_to(np.diag(rng.uniform(-3, 3, dim)), (3, dim, dim)).copy()
+                H = 0.5 * (H + np.swapaxes(H, 1, 2))
+                if kind == "zero" and rng.random() < 0.5:
+                    L = np.zeros(3)
+                cases.append((dim, L, g, H))
+    out = {"versions": VERSIONS}
+    for j, (dim, L, g, H) in enumerate(cases):
+        x = rng.uniform(0, 1, dim)
+        mom = vs.Moments(L=L, grad=g, hess=H, kind="single")
+        scale = float(np.sqrt(dim))
+        for aniso in (True, False):
+            for max_em in (10.0, 0.0):
+                rec = vcache.make_record(x, mom, 0.05, scale, max_em, anisotropic=aniso)
+                key = f"c{j}_{int(aniso)}_{int(max_em)}"
+                out[key + "_axes"] = rec.axes
+                out[key + "_radii"] = rec.radii
+        out[f"c{j}_dim"] = np.array(dim)
+        out[f"c{j}_x"] = x
+        out[f"c{j}_L"] = L
+        out[f"c{j}_g"] = g
+        out[f"c{j}_H"] = H
+    out["n_cases"] = np.array(len(cases))
+    np.savez_compressed(OUT / "make_record.npz", **out)
+
+
+def _rotation(dim, rng):
+    q, r = np.linalg.qr(rng.normal(size=(dim, dim)))
+    return q * np.sign(np.diag(r))[None, :]
+
+
+def gen_interpolate():
+    out = {"versions": VERSIONS}
+    for dim in (2, 3):
+        rng = np.random.default_rng(500 + dim)
+        cache = vcache.RadianceCache(np.zeros(dim), np.ones(dim))
+        recs = []
+        for _ in range(40):
+            rec = vcache.CacheRecord(
+                position=rng.uniform(0, 1, dim), value=rng.uniform(0, 5, 3),
+                grad=rng.normal(size=(3, dim)), axes=_rotation(dim, rng),
+                radii=rng.uniform(0.02, 0.25 * np.sqrt(dim), dim),
+            )
+            cache.insert(rec)
+            recs.append(rec)
+        # power-of-two record for the exclusive-boundary case (tests/test_cache.py:586-594)
+        edge = vcache.CacheRecord(position=np.full(dim, 0.5), value=np.ones(3), grad=np.zeros((3, dim)),
+                                  axes=np.eye(dim), radii=np.full(dim, 0.125))
+        cache.insert(edge)
+        recs.append(edge)
+        q = rng.uniform(-0.2, 1.2, (400, dim))
+        q[0] = 0.5
+        q[1] = 0.5
+        q[1, 0] = 0.625
+        J = np.full((len(q), 3), np.nan)
+        cnt = np.zeros(len(q), np.int64)
+        for i, x in enumerate(q):
+            v = vcache.interpolate(cache, x)
+            cnt[i] = len(cache.query(x))
+            if v is not None:
+                J[i] = v
+        out[f"d{dim}_pos"] = np.array([r.position for r in recs])
+        out[f"d{dim}_value"] = np.array([r.value for r in recs])
+        out[f"d{dim}_grad"] = np.array([r.grad for r in recs])
+        out[f"d{dim}_axes"] = np.array([r.axes for r in recs])
+        out[f"d{dim}_radii"] = np.array([r.radii for r in recs])
+        out[f"d{dim}_q"] = q
+        out[f"d{dim}_J"] = J
+        out[f"d{dim}_count"] = cnt
+    np.savez_compressed(OUT / "interpolate.npz", **out)
+
+
+def gen_render():
+    """Tiny frozen-cache camera render of the small window room (src/renderer.py:402-484)."""
+    sc = configs.cfg3_scene(n_spheres=4, level=1)
+    rs = ref_scene(sc)
+    cam = vr.Camera(position=np.array([2.0, 1.5, 0.2]), look_at=np.array([2.0, 1.5, 4.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=60.0, width=8, height=5)
+    st = vr.RenderSettings(mode="ours-aniso", epsilon=0.5, spp=1, march_step=0.5, n_angular=256,
+                           seed=3, frozen=True, n_inner=1, n_light_samples=16)
+    cs, pop = vr.populate_cache(rs, cam, st)
+    img, stats = vr.render(rs, cam, st, cache_set=cs)
+    out = {"versions": VERSIONS, "image": img}
+    out.update(scene_fields("", sc))
+    for kind, c in (("single", cs.single), ("multiple", cs.multiple)):
+        recs = c.records
+        out[f"{kind}_pos"] = np.array([r.position for r in recs])
+        out[f"{kind}_value"] = np.array([r.value for r in recs])
+        out[f"{kind}_grad"] = np.array([r.grad for r in recs])
+        out[f"{kind}_axes"] = np.array([r.axes for r in recs])
+        out[f"{kind}_radii"] = np.array([r.radii for r in recs])
+    out["stats"] = np.array([stats["cache_hits"], stats["direct_evaluations"], pop["points_marched"]])
+    out["settings"] = np.array([st.epsilon, st.spp, st.march_step, st.n_angular, st.seed, st.n_inner,
+                                st.n_light_samples])
+    out["camera"] = np.concatenate([cam.position, cam.look_at, cam.up,
+                                    [cam.fov_degrees, cam.width, cam.height]])
+    np.savez_compressed(OUT / "render.npz", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render"]
+    if "ff" in which:
+        gen_formfactors()
+    if "trace" in which:
+        gen_trace()
+    if "records" in which:
+        gen_records()
+    if "make_record" in which:
+        gen_make_record()
+    if "interp" in which:
+        gen_interpolate()
+    if "render" in which:
+        gen_render()

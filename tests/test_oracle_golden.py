@@ -1,0 +1,113 @@
+"""Pin the CPU oracle to the reference: oracle vs golden fixtures made by the reference.
+
+CPU-only (no GPU marker).  Integer outputs (hit indices, adjacency, element counts)
+must be identical; float outputs agree to ≤1e-12 relative, since the oracle
+restates the reference's float64 arithmetic.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import REC_CASES, golden, golden_scene, rel_l2
+from oracle import volcache_oracle as O
+
+
+def test_formfactors_match_reference():
+    z = golden("formfactors")
+    ok, v, g, h = O.segment_ff(z["seg_x"], z["seg_y0"], z["seg_y1"])
+    np.testing.assert_array_equal(ok, z["seg_ok"])
+    np.testing.assert_allclose(v, z["seg_val"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(g, z["seg_grad"], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(h, z["seg_hess"], rtol=1e-11, atol=1e-300)
+    ok, v, g, h = O.triangle_ff(z["tri_x"], z["tri_y1"], z["tri_y2"], z["tri_y3"])
+    np.testing.assert_array_equal(ok, z["tri_ok"])
+    np.testing.assert_allclose(v, z["tri_val"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(g, z["tri_grad"], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(h, z["tri_hess"], rtol=1e-11, atol=1e-300)
+    assert (~z["seg_ok"]).sum() >= 8 and (~z["tri_ok"]).sum() >= 8  # degenerate cases present
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "room"])
+def test_trace_matches_reference(name):
+    z = golden("trace")
+    ps = O.pack(golden_scene(z, f"{name}_"))
+    s, idx = O.trace_or_bounds(ps, z[f"{name}_o"], z[f"{name}_d"])
+    np.testing.assert_array_equal(idx, z[f"{name}_idx"])
+    np.testing.assert_array_equal(s, z[f"{name}_s"])
+
+
+@pytest.mark.parametrize("case", REC_CASES)
+def test_records_match_reference(case):
+    z = golden(f"rec_{case}")
+    ps = O.pack(golden_scene(z))
+    n, step, n_inner, n_light, canon = z["params"]
+    seed = int(z["cfg_seed"])
+    for i, x in enumerate(z["points"]):
+        inject = z["adj"][i] if canon else None
+        rb = O.build_record(ps, x, int(n), float(step), O.seed_seq(seed, 401, i), int(n_inner),
+                            int(n_light), adjacency=inject)
+        np.testing.assert_array_equal(rb.adjacency, z["adj"][i])
+        np.testing.assert_array_equal(rb.idx, z["idx"][i])
+        np.testing.assert_array_equal(rb.s, z["s"][i])
+        np.testing.assert_array_equal(rb.dirs, z["dirs"][i])
+        st = rb.stats
+        assert [st["elements_evaluated"], st["elements_dropped"], st["star_vertices"]] == z["stats"][i].tolist()
+        for k in range(2):
+            assert rel_l2(rb.L[k], z["L"][i][k]) <= 1e-12
+            assert rel_l2(rb.grad[k], z["grad"][i][k]) <= 1e-11
+            assert rel_l2(rb.hess[k], z["hess"][i][k]) <= 1e-10
+            rec = O.make_record(x, rb.L[k], rb.grad[k], rb.hess[k], 0.05, ps.scale, ps.max_emission)
+            np.testing.assert_allclose(rec.radii, z["rec_radii"][i][k], rtol=1e-9)
+            q = rec.axes @ np.diag(rec.radii**-2.0) @ rec.axes.T
+            qz = z["rec_axes"][i][k] @ np.diag(z["rec_radii"][i][k] ** -2.0) @ z["rec_axes"][i][k].T
+            assert rel_l2(q, qz) <= 1e-8
+
+
+def test_make_record_edge_cases():
+    z = golden("make_record")
+    for j in range(int(z["n_cases"])):
+        dim = int(z[f"c{j}_dim"])
+        for aniso in (True, False):
+            for max_em in (10, 0):
+                key = f"c{j}_{int(aniso)}_{max_em}"
+                rec = O.make_record(z[f"c{j}_x"], z[f"c{j}_L"], z[f"c{j}_g"], z[f"c{j}_H"], 0.05,
+                                    float(np.sqrt(dim)), float(max_em), anisotropic=aniso)
+                np.testing.assert_allclose(rec.radii, z[key + "_radii"], rtol=1e-10)
+                q = rec.axes @ np.diag(rec.radii**-2.0) @ rec.axes.T
+                qz = z[key + "_axes"] @ np.diag(z[key + "_radii"] ** -2.0) @ z[key + "_axes"].T
+                assert rel_l2(q, qz) <= 1e-8, (j, aniso, max_em)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_interpolate_matches_reference(dim):
+    z = golden("interpolate")
+    recs = [O.Record(*a) for a in zip(z[f"d{dim}_pos"], z[f"d{dim}_value"], z[f"d{dim}_grad"],
+                                      z[f"d{dim}_axes"], z[f"d{dim}_radii"])]
+    cache = O.Cache(recs)
+    for x, J, c in zip(z[f"d{dim}_q"], z[f"d{dim}_J"], z[f"d{dim}_count"]):
+        assert len(cache.query(x)) == c
+        v = O.interpolate(cache, x)
+        if np.isnan(J[0]):
+            assert v is None
+        else:
+            np.testing.assert_allclose(v, J, rtol=1e-13)
+
+
+def test_render_matches_reference():
+    z = golden("render")
+    ps = O.pack(golden_scene(z))
+    caches = []
+    for kind in ("single", "multiple"):
+        caches.append(O.Cache([O.Record(*a) for a in zip(z[f"{kind}_pos"], z[f"{kind}_value"], z[f"{kind}_grad"],
+                                                        z[f"{kind}_axes"], z[f"{kind}_radii"])]))
+    eps, spp, step, n_ang, seed, n_inner, n_light = z["settings"]
+    c = z["camera"]
+    cam = dict(position=c[0:3], look_at=c[3:6], up=c[6:9], fov=c[9], width=int(c[10]), height=int(c[11]))
+    prm = O.RenderParams(epsilon=eps, spp=int(spp), march_step=step, n_angular=int(n_ang), seed=int(seed),
+                         n_inner=int(n_inner), n_light_samples=int(n_light))
+    img, stats = O.render_camera(ps, cam, caches[0], caches[1], prm)
+    np.testing.assert_allclose(img.reshape(z["image"].shape), z["image"], rtol=1e-12, atol=1e-14)
+    assert stats["cache_hits"] == int(z["stats"][0])
+    assert stats["direct_evaluations"] == int(z["stats"][1])
