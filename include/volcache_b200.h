@@ -1,0 +1,147 @@
+/* libvolcache_b200 — C ABI of the B200 cache-record path.
+ *
+ * Drop-in boundary for the reference's record-build / lookup / render entry points
+ * (reference = /root/reference/pkg/src/volcache, "src/" below).  The reference has no
+ * FFI of its own: its boundary is the Python functions, so each entry point cites the
+ * Python interface it replaces and the Python mirror in paper_1805_09258_b200/ binds
+ * these symbols with ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; float64 in/out (the reference's dtype); int32 indices.
+ *  - Arrays are device pointers unless VC_MEM_HOST is set in `flags`, in which case
+ *    every array argument is host memory and the library stages the copies.
+ *  - Return 0 on success, a negative VC_E* code on failure; vc_last_error() gives the
+ *    thread-local message.  VC_EINVAL / VC_EOUTSIDE mirror the reference's ValueError
+ *    cases (src/subdivision.py:155-158); the others are RuntimeErrors.
+ *  - Handles are immutable after creation apart from their internal scratch: use one
+ *    scene handle per host thread (or serialize calls) — calls on one handle are
+ *    stream-ordered on the stream they are given.
+ */
+#ifndef VOLCACHE_B200_H
+#define VOLCACHE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VC_OK 0
+#define VC_EINVAL (-1)
+#define VC_EOUTSIDE (-2)
+#define VC_ECUDA (-3)
+#define VC_ETRI (-4)
+#define VC_ENOMEM (-5)
+
+/* flags */
+#define VC_MEM_HOST 1     /* all array pointers are host memory */
+#define VC_SEED_WORDS 2   /* rng = uint32 SeedSequence entropy words, seed_words per record */
+#define VC_MAKE_RECORDS 4 /* also finalize records (make_record) into `records` */
+#define VC_ISOTROPIC 8    /* make_record(..., anisotropic=False) */
+
+typedef struct vc_scene vc_scene;
+typedef struct vc_cache vc_cache;
+
+int vc_version(void);
+const char* vc_last_error(void);
+/* Kernel launches issued by this library since load (the bench's gpu_launches claim). */
+int64_t vc_kernel_launches(void);
+
+/* Scene upload + BVH build.  Replaces Scene/_Packed2D/_Packed3D (src/scene.py:124-219).
+ * vertices: n_surfaces × dim × dim (segment endpoints or triangle corners), host memory.
+ * emission, albedo: n_surfaces × 3; bounds: dim each.  Host memory always. */
+int vc_scene_create(int dim, int n_surfaces, const double* vertices, const double* emission,
+                    const double* albedo, const double* bounds_min, const double* bounds_max,
+                    double sigma_s, double sigma_a, vc_scene** out);
+void vc_scene_destroy(vc_scene* scene);
+/* Scratch budget for one record wave (bytes, default 8 GiB). */
+int vc_scene_set_budget(vc_scene* scene, int64_t bytes);
+
+typedef struct {
+  int n_angular;       /* directions per record (estimate_moments n_angular) */
+  double march_step;   /* ring spacing (march_step) */
+  int n_inner;         /* gather directions per media sample (n_inner) */
+  int n_light_samples; /* emitter quadrature samples (n_light_samples) */
+  double epsilon;      /* make_record error budget */
+  int flags;           /* VC_* flags */
+  int seed_words;      /* entropy words per record when VC_SEED_WORDS */
+} vc_build_params;
+
+/* Batch estimate_moments (+ make_record for both kinds).
+ * Replaces subdivision.estimate_moments (src/subdivision.py:373-393) called once per
+ * point from CacheSet.compute (src/renderer.py:246-262), and cache.make_record
+ * (src/cache.py:153-189).
+ *   x          n_records × dim cache points
+ *   rng        n_records × 4 uint64 PCG64 (state_hi, state_lo, inc_hi, inc_lo), the
+ *              numpy bit_generator state of default_rng(rng_seed); or, with
+ *              VC_SEED_WORDS, n_records × seed_words uint32 SeedSequence entropy
+ *   adjacency  NULL (GPU spherical Delaunay) or n_records × (2n−4) × 3 int32 triangles
+ *              (3D; e.g. qhull's simplices, src/scene.py:388-399)
+ *   moments    n_records × 2 × (3 + 3d + 3d²): [single, multiple] × (L, grad, hess)
+ *   stats      n_records × 8 int64: elements_evaluated, elements_dropped, star_vertices,
+ *              media samples, rings, triangulation status, evaluated single, multiple
+ *   records    NULL or n_records × 2 × (d + 3 + 3d + d² + d): position, value, grad,
+ *              axes (row-major, columns = principal axes), radii
+ *   stream     cudaStream_t (NULL = legacy default stream) */
+int vc_build_records(vc_scene* scene, int n_records, const double* x, const void* rng,
+                     const int32_t* adjacency, const vc_build_params* params, double* moments,
+                     int64_t* stats, double* records, void* stream);
+
+/* One record with its per-direction internals copied to host (parity inspection).
+ * dirs n×d, s n, idx n, counts n, tris (2n−4)×3 (3D) — any may be NULL; media
+ * (media_cap × 3 float32) receives min(P, media_cap) samples, *P the count. */
+int vc_build_inspect(vc_scene* scene, const double* x, const void* rng, const int32_t* adjacency,
+                     const vc_build_params* params, double* dirs, double* s, int32_t* idx,
+                     int32_t* counts, int32_t* tris, float* media, int64_t media_cap, int64_t* P,
+                     double* moments, int64_t* stats);
+
+/* make_record for n records × {single, multiple} moments (src/cache.py:146-189).
+ * moments n × 2 × (3 + 3d + 3d²) → records n × 2 × (d + 3 + 3d + d² + d). */
+int vc_make_records(int n, int dim, const double* x, const double* moments, double epsilon,
+                    double scene_scale, double max_emission, int flags, double* records, void* stream);
+
+/* numpy SeedSequence(words) → PCG64 state (host), for n records of nw words each. */
+int vc_seed_states(int n, const uint32_t* words, int nw, uint64_t* states);
+
+/* Record cache + lookup.  Replaces RadianceCache (src/cache.py:262-334) and
+ * interpolate (src/cache.py:342-360).  records: n × (d + 3 + 3d + d² + d) float64,
+ * host memory. */
+int vc_cache_create(int dim, const double* bounds_min, const double* bounds_max, int n_records,
+                    const double* records, vc_cache** out);
+void vc_cache_destroy(vc_cache* cache);
+/* Blended J per query (NaN row when uncovered) and the covering-record count.
+ * xq m × d, J m × 3, count m (int32, may be NULL). */
+int vc_cache_interpolate(vc_cache* cache, int m, const double* xq, double* J, int32_t* count,
+                         int flags, void* stream);
+
+typedef struct {
+  double position[3], look_at[3], up[3];
+  double fov_degrees;
+  int width, height;
+  int row0, rows; /* crop: image rows [row0, row0+rows) (rows = 0 → all) */
+  int col0, cols; /* crop: columns */
+} vc_camera;
+
+typedef struct {
+  int spp;
+  double march_step;
+  int seed;
+  int n_angular;
+  int n_inner;
+  int n_light_samples;
+  double epsilon;
+} vc_render_params;
+
+/* Frozen-cache camera render (src/renderer.py:402-484, mode ours-*, frozen=True):
+ * camera march with cache lookups; steps no cache pair covers are evaluated directly
+ * through the record build with seeds (seed, 211, k, i, m).  image: height × width × 3
+ * float64 (only the crop is written); stats: cache_hits, direct_evaluations. */
+int vc_render(vc_scene* scene, vc_cache* single, vc_cache* multiple, const vc_camera* camera,
+              const vc_render_params* params, double* image, int64_t* stats, int flags,
+              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VOLCACHE_B200_H */

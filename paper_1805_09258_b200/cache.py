@@ -1,0 +1,142 @@
+"""Record cache, lookup and frozen-cache camera march on the B200 path.
+
+Mirrors src/cache.py:262-360 (RadianceCache, interpolate) and the frozen camera
+render of src/renderer.py:402-484.  Records live on the device behind a
+multi-level grid index whose covering set equals the reference tree query
+(≡ linear scan); interpolation and the march run in libvolcache_b200.so.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .records import CacheRecord, device_scene, record_size
+
+
+class RadianceCache:
+    """Records + exact point-query index (src/cache.py:262-334)."""
+
+    MAX_DEPTH = 16
+
+    def __init__(self, bounds_min, bounds_max):
+        bmin = np.asarray(bounds_min, dtype=float)
+        bmax = np.asarray(bounds_max, dtype=float)
+        if bmin.shape != bmax.shape or bmin.size not in (2, 3):
+            raise ValueError("bounds must be matching 2- or 3-vectors")
+        if np.any(bmax <= bmin):
+            raise ValueError("bounds_max must exceed bounds_min")
+        self.bounds_min = np.ascontiguousarray(bmin)
+        self.bounds_max = np.ascontiguousarray(bmax)
+        self.dim = bmin.size
+        self._records: list = []
+        self._handle = None
+        self._fin = None
+
+    def __len__(self) -> int:
+        return len(self._records)
+
+    @property
+    def records(self) -> list:
+        return list(self._records)
+
+    def insert(self, record) -> None:
+        if np.asarray(record.position).size != self.dim:
+            raise ValueError("record dimensionality does not match the cache")
+        self._records.append(record)
+        self._invalidate()
+
+    def extend_packed(self, packed: np.ndarray) -> None:
+        """Insert many records given as packed rows (N, d + 3 + 3d + d² + d)."""
+        from .records import unpack_record
+
+        for row in np.asarray(packed, float).reshape(-1, record_size(self.dim)):
+            self._records.append(unpack_record(row, self.dim))
+        self._invalidate()
+
+    def _invalidate(self):
+        if self._fin is not None:
+            self._fin()
+        self._handle = None
+        self._fin = None
+
+    def packed(self) -> np.ndarray:
+        d = self.dim
+        if not self._records:
+            return np.zeros((0, record_size(d)))
+        return np.ascontiguousarray(np.stack([np.concatenate([
+            np.asarray(r.position, float), np.asarray(r.value, float), np.asarray(r.grad, float).ravel(),
+            np.asarray(r.axes, float).ravel(), np.asarray(r.radii, float)]) for r in self._records]))
+
+    def handle(self):
+        if self._handle is None:
+            L = _lib.lib()
+            recs = self.packed()
+            h = _lib.C.c_void_p()
+            _lib.check(L.vc_cache_create(self.dim, _lib.ptr(self.bounds_min), _lib.ptr(self.bounds_max),
+                                         len(recs), _lib.ptr(recs) if len(recs) else None, _lib.C.byref(h)))
+            self._handle = h
+            self._fin = weakref.finalize(self, L.vc_cache_destroy, h)
+        return self._handle
+
+    def interpolate_many(self, X):
+        """(J (m, 3) with NaN rows where uncovered, covering-record counts (m,))."""
+        X = np.ascontiguousarray(np.asarray(X, float).reshape(-1, self.dim))
+        m = X.shape[0]
+        J = np.zeros((m, 3))
+        cnt = np.zeros(m, np.int32)
+        _lib.check(_lib.lib().vc_cache_interpolate(self.handle(), m, _lib.ptr(X), _lib.ptr(J), _lib.ptr(cnt),
+                                                   _lib.VC_MEM_HOST, None))
+        return J, cnt
+
+
+def interpolate(cache: RadianceCache, x):
+    """Cubic-weighted first-order blend of covering records, or None (src/cache.py:342-360)."""
+    J, cnt = cache.interpolate_many(np.asarray(x, float)[None])
+    if cnt[0] == 0 or np.isnan(J[0, 0]):
+        return None
+    return J[0]
+
+
+def cache_from_records(bounds_min, bounds_max, records) -> RadianceCache:
+    c = RadianceCache(bounds_min, bounds_max)
+    for r in records:
+        c._records.append(r if isinstance(r, CacheRecord) else CacheRecord(
+            np.asarray(r.position, float), np.asarray(r.value, float), np.asarray(r.grad, float),
+            np.asarray(r.axes, float), np.asarray(r.radii, float)))
+    return c
+
+
+def render_frozen(scene, camera: dict, single: RadianceCache, multiple: RadianceCache, *, spp=1,
+                  march_step=0.1, seed=0, n_angular=None, n_inner=1, n_light_samples=16, epsilon=0.05,
+                  crop=None):
+    """Frozen-cache camera image (src/renderer.py:440-484) → (image (h, w, 3), stats).
+
+    `camera` = {position, look_at, up, fov, width, height}; `crop` = (row0, rows, col0, cols)
+    restricts the march to a pixel window (other pixels stay 0).  Misses are evaluated
+    directly through the record build with seeds (seed, 211, k, i, m), as the reference.
+    """
+    ds = device_scene(scene)
+    cam = _lib.Camera()
+    for f in ("position", "look_at", "up"):
+        getattr(cam, f)[:] = [float(v) for v in np.asarray(camera[f], float)]
+    cam.fov_degrees = float(camera["fov"])
+    cam.width = int(camera["width"])
+    cam.height = int(camera["height"])
+    if crop is not None:
+        cam.row0, cam.rows, cam.col0, cam.cols = (int(v) for v in crop)
+    rp = _lib.RenderParams()
+    rp.spp = int(spp)
+    rp.march_step = float(march_step)
+    rp.seed = int(seed)
+    rp.n_angular = int(16384 if n_angular is None else n_angular)
+    rp.n_inner = int(n_inner)
+    rp.n_light_samples = int(n_light_samples)
+    rp.epsilon = float(epsilon)
+    img = np.zeros((cam.height, cam.width, 3))
+    stats = np.zeros(2, np.int64)
+    _lib.check(_lib.lib().vc_render(ds.handle, single.handle(), multiple.handle(), _lib.C.byref(cam),
+                                    _lib.C.byref(rp), _lib.ptr(img), _lib.ptr(stats), _lib.VC_MEM_HOST, None))
+    return img, {"cache_hits": int(stats[0]), "direct_evaluations": int(stats[1])}

@@ -1,0 +1,555 @@
+// C ABI of libvolcache_b200: scene upload, workspace management, wave orchestration.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/volcache_b200.h"
+#include "vc_build.h"
+#include "vc_device.cuh"
+#include "vc_api_internal.h"
+
+namespace vc {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(VC_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+void* Workspace::get(int slot, size_t bytes, cudaError_t* err) {
+  if (bytes == 0) bytes = 16;
+  if (cap[slot] < bytes) {
+    if (ptr[slot]) cudaFree(ptr[slot]);
+    ptr[slot] = nullptr;
+    cap[slot] = 0;
+    cudaError_t e = cudaMalloc(&ptr[slot], bytes);
+    if (e != cudaSuccess) {
+      *err = e;
+      return nullptr;
+    }
+    cap[slot] = bytes;
+  }
+  return ptr[slot];
+}
+
+Workspace::~Workspace() {
+  for (int i = 0; i < kSlots; ++i)
+    if (ptr[i]) cudaFree(ptr[i]);
+}
+
+// PCG64 jump tables, built once per device.
+const unsigned long long* jump_tables(cudaError_t* err) {
+  static const unsigned long long* dev_tab[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_tab[dev]) return dev_tab[dev];
+  std::vector<unsigned long long> h(3 * 1024 * 4);
+  u128 M = pcg_mult();
+  u128 bA = M, bG = 1;  // jump by 1
+  for (int lv = 0; lv < 3; ++lv) {
+    u128 A = 1, G = 0;  // jump by 0
+    for (int k = 0; k < 1024; ++k) {
+      unsigned long long* e = &h[((size_t)lv * 1024 + k) * 4];
+      e[0] = (unsigned long long)(A >> 64);
+      e[1] = (unsigned long long)A;
+      e[2] = (unsigned long long)(G >> 64);
+      e[3] = (unsigned long long)G;
+      G = bA * G + bG;  // then jump by base
+      A = bA * A;
+    }
+    // base for next level: jump by 1024^(lv+1) = current (A, G) after 1024 steps
+    bA = A;
+    bG = G;
+  }
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, h.size() * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    *err = e;
+    return nullptr;
+  }
+  dev_tab[dev] = d;
+  return d;
+}
+
+bool grid_shape_3d(int n, int* rows, int* cols) {
+  // src/scene.py:370-385
+  double target = std::sqrt(n / 2.0);
+  int best = -1;
+  int lim = (int)std::sqrt((double)n);
+  for (int r = 2; r <= lim; ++r) {
+    if (n % r) continue;
+    if (n / r < 3) continue;
+    if (best < 0 || std::fabs(r - target) < std::fabs(best - target)) best = r;
+  }
+  if (best < 0) return false;
+  *rows = best;
+  *cols = n / best;
+  return true;
+}
+
+int ensure_emitters(vc_scene* sc, int n_light) {
+  if (sc->es_nlight == n_light) return VC_OK;
+  const int D = sc->dim;
+  std::vector<double> pos, w;
+  std::vector<int> surf;
+  for (int k = 0; k < sc->K; ++k) {
+    const double* E = &sc->emission[3 * (size_t)k];
+    if (!(E[0] > 0.0 || E[1] > 0.0 || E[2] > 0.0)) continue;
+    const double* V = &sc->verts[(size_t)k * D * D];
+    if (D == 2) {  // src/transport.py:139-146
+      double e0 = V[2] - V[0], e1 = V[3] - V[1];
+      double len = std::sqrt(e0 * e0 + e1 * e1);
+      for (int j = 0; j < n_light; ++j) {
+        double u = (j + 0.5) / n_light;
+        pos.push_back(V[0] + u * e0);
+        pos.push_back(V[1] + u * e1);
+        w.push_back(len / n_light);
+        surf.push_back(k);
+      }
+    } else {  // src/transport.py:147-160
+      int m = std::max(2, (int)std::lround(std::sqrt((double)n_light)));
+      double e1[3], e2[3];
+      for (int a = 0; a < 3; ++a) {
+        e1[a] = V[3 + a] - V[a];
+        e2[a] = V[6 + a] - V[a];
+      }
+      double c0 = e1[1] * e2[2] - e1[2] * e2[1], c1 = e1[2] * e2[0] - e1[0] * e2[2],
+             c2 = e1[0] * e2[1] - e1[1] * e2[0];
+      double area = 0.5 * std::sqrt(c0 * c0 + c1 * c1 + c2 * c2);
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+          double u = (i + 0.5) / m, v = (j + 0.5) / m;
+          if (u + v > 1.0) {
+            u = 1.0 - u;
+            v = 1.0 - v;
+          }
+          for (int a = 0; a < 3; ++a) pos.push_back(V[a] + u * e1[a] + v * e2[a]);
+          w.push_back(area / (m * m));
+          surf.push_back(k);
+        }
+    }
+  }
+  cudaFree(sc->d_es_pos);
+  cudaFree(sc->d_es_w);
+  cudaFree(sc->d_es_surf);
+  sc->d_es_pos = nullptr;
+  sc->d_es_w = nullptr;
+  sc->d_es_surf = nullptr;
+  sc->n_es = (int)w.size();
+  if (sc->n_es) {
+    cudaError_t e = cudaMalloc(&sc->d_es_pos, pos.size() * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&sc->d_es_w, w.size() * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&sc->d_es_surf, surf.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(sc->d_es_pos, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(sc->d_es_w, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(sc->d_es_surf, surf.data(), surf.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "emitter upload");
+  }
+  sc->es_nlight = n_light;
+  return VC_OK;
+}
+
+DevScene dev_scene(const vc_scene* sc) {
+  DevScene S{};
+  S.dim = sc->dim;
+  S.K = sc->K;
+  S.n_nodes = sc->n_nodes;
+  S.n_es = sc->n_es;
+  S.reflective = sc->reflective;
+  for (int a = 0; a < 3; ++a) {
+    S.bmin[a] = sc->bmin[a];
+    S.bmax[a] = sc->bmax[a];
+  }
+  S.scale = sc->scale;
+  S.t_eps = 1e-6 * sc->scale;
+  S.sigma_s = sc->sigma_s;
+  S.sigma_a = sc->sigma_a;
+  S.sigma_t = sc->sigma_s + sc->sigma_a;
+  S.max_emission = sc->max_emission;
+  S.prim = sc->d_prim;
+  S.prim_id = sc->d_prim_id;
+  S.normal = sc->d_normal;
+  S.emission = sc->d_emission;
+  S.albedo = sc->d_albedo;
+  S.nodes = sc->d_nodes;
+  S.es_pos = sc->d_es_pos;
+  S.es_w = sc->d_es_w;
+  S.es_surf = sc->d_es_surf;
+  return S;
+}
+
+void count_launches(long long n) { g_launches += n; }
+
+// ---------------------------------------------------------------------------
+// The record build, in waves sized by the scratch budget.
+// ---------------------------------------------------------------------------
+
+int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int32_t* adjacency,
+               const vc_build_params* prm, double* moments, int64_t* stats, double* records,
+               cudaStream_t st, Inspect* insp) {
+  if (!sc || !prm) return fail(VC_EINVAL, "null scene or params");
+  if (N < 0) return fail(VC_EINVAL, "n_records must be non-negative");
+  if (N == 0) return VC_OK;
+  const int D = sc->dim;
+  const int n = prm->n_angular;
+  if (!(prm->march_step > 0.0)) return fail(VC_EINVAL, "march_step must be positive");
+  if (prm->n_inner < 1) return fail(VC_EINVAL, "n_inner must be >= 1");
+  if (prm->n_light_samples < 1) return fail(VC_EINVAL, "n_light_samples must be >= 1");
+  const bool host = prm->flags & VC_MEM_HOST;
+  const bool words = prm->flags & VC_SEED_WORDS;
+  BuildParams P{};
+  P.n_angular = n;
+  P.march_step = prm->march_step;
+  P.n_inner = prm->n_inner;
+  P.epsilon = prm->epsilon;
+  P.anisotropic = (prm->flags & VC_ISOTROPIC) ? 0 : 1;
+  P.make_records = (records != nullptr) || (prm->flags & VC_MAKE_RECORDS);
+  if (P.make_records && !(prm->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
+  if (D == 2) {
+    if (n < 3) return fail(VC_EINVAL, "2D stratification needs n >= 3");
+    P.rows = 1;
+    P.cols = n;
+    P.n_tris = n;
+  } else {
+    if (!grid_shape_3d(n, &P.rows, &P.cols))
+      return fail(VC_EINVAL, "n=" + std::to_string(n) + " is not expressible as rows x cols with rows >= 2 and cols >= 3");
+    P.n_tris = 2 * n - 4;
+  }
+  P.host_adjacency = (D == 3 && adjacency != nullptr) ? 1 : 0;
+  P.r_ub = (int)std::floor(sc->scale * (1.0 + 1e-9) / prm->march_step + 0.5) + 2;
+  if (host) {  // ValueError before any work (src/subdivision.py:155-158)
+    const double eps = 1e-12 * sc->scale;
+    for (int i = 0; i < N; ++i)
+      for (int a = 0; a < D; ++a) {
+        double v = x[(size_t)i * D + a];
+        if (!(v >= sc->bmin[a] - eps && v <= sc->bmax[a] + eps))
+          return fail(VC_EOUTSIDE, "subdivision center lies outside the medium bounds");
+      }
+  }
+  int rc = ensure_emitters(sc, prm->n_light_samples);
+  if (rc) return rc;
+  cudaError_t err = cudaSuccess;
+  JumpTables jt{jump_tables(&err)};
+  if (!jt.tab) return cuda_fail(err, "jump tables");
+  DevScene S = dev_scene(sc);
+
+  // per-record scratch bytes
+  const size_t MS = moment_size(D), RS = record_size(D);
+  const size_t media_per = (size_t)n * P.r_ub;
+  size_t per = (size_t)n * (D * 8 + 8 + 4 * 5 + 24) + media_per * 12 + 64 + 2 * MS * 8 + 2 * RS * 8 +
+               kStats * 8 + 32 + 8;
+  if (D == 3) per += (size_t)P.n_tris * 12 + (P.host_adjacency ? 0 : (size_t)n * 32 * 8);
+  long long B = (long long)(sc->budget / (long long)per);
+  if (B < 1) B = 1;
+  if (B > N) B = N;
+  if (B > 65535) B = 65535;
+  if (insp) B = 1;
+  Workspace& ws = sc->ws;
+  auto alloc = [&](int slot, size_t bytes) { return ws.get(slot, bytes, &err); };
+  Wave W{};
+  double* dx = (double*)alloc(0, B * D * 8);
+  uint64_t* drng = (uint64_t*)alloc(1, B * 4 * 8);
+  W.dirs = (double*)alloc(2, B * n * D * 8);
+  W.s = (double*)alloc(3, B * n * 8);
+  W.idx = (int*)alloc(4, B * n * 4);
+  W.cnt = (int*)alloc(5, B * n * 4);
+  W.pre = (int*)alloc(6, B * n * 4);
+  W.lo = (double*)alloc(7, B * n * 24);
+  W.rec_R = (int*)alloc(8, B * 4);
+  W.rec_P = (int*)alloc(9, B * 4);
+  W.rec_maxc = (int*)alloc(10, B * 4);
+  W.rec_base = (long long*)alloc(11, (B + 1) * 8);
+  W.media = (float*)alloc(12, B * media_per * 12);
+  W.media_cap = (long long)(B * media_per);
+  W.tris = (int*)alloc(13, D == 3 ? B * P.n_tris * 12 : 16);
+  W.deg = (int*)alloc(14, B * n * 4);
+  W.tri_status = (int*)alloc(15, B * 4);
+  double* dmom = (double*)alloc(16, B * 2 * MS * 8);
+  long long* dstat = (long long*)alloc(17, B * kStats * 8);
+  double* drec = (double*)alloc(18, B * 2 * RS * 8);
+  int* own = (int*)alloc(19, (D == 3 && !P.host_adjacency) ? B * n * 32 * 8 : 16);
+  int* own_cnt = (int*)alloc(20, B * n * 4);
+  uint32_t* dwords = (uint32_t*)alloc(21, words ? B * prm->seed_words * 4 + 4 : 16);
+  if (err != cudaSuccess) return cuda_fail(err, "workspace allocation");
+
+  KernelCounter kc;
+  for (long long w0 = 0; w0 < N; w0 += B) {
+    const int b = (int)std::min<long long>(B, N - w0);
+    W.B = b;
+    // inputs
+    if (host) {
+      err = cudaMemcpyAsync(dx, x + w0 * D, b * D * 8, cudaMemcpyHostToDevice, st);
+      W.x = dx;
+    } else {
+      W.x = x + w0 * D;
+    }
+    if (err != cudaSuccess) return cuda_fail(err, "x upload");
+    if (words) {
+      const uint32_t* wsrc = (const uint32_t*)rng + w0 * prm->seed_words;
+      if (host) {
+        err = cudaMemcpyAsync(dwords, wsrc, (size_t)b * prm->seed_words * 4, cudaMemcpyHostToDevice, st);
+        wsrc = dwords;
+      }
+      launch_seedseq(b, wsrc, prm->seed_words, drng, st);
+      kc.launches += 1;
+      W.rng = drng;
+    } else if (host) {
+      err = cudaMemcpyAsync(drng, (const uint64_t*)rng + w0 * 4, (size_t)b * 32, cudaMemcpyHostToDevice, st);
+      W.rng = drng;
+    } else {
+      W.rng = (const uint64_t*)rng + w0 * 4;
+    }
+    if (err != cudaSuccess) return cuda_fail(err, "rng upload");
+    if (P.host_adjacency) {
+      const size_t tb = (size_t)b * P.n_tris * 12;
+      err = cudaMemcpyAsync(W.tris, adjacency + w0 * P.n_tris * 3, tb,
+                            host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
+      if (err != cudaSuccess) return cuda_fail(err, "adjacency upload");
+    }
+    W.moments = (host || !moments) ? dmom : moments + w0 * 2 * MS;
+    W.stats = (host || !stats) ? dstat : (long long*)stats + w0 * kStats;
+    W.records = (host || !records) ? drec : records + w0 * 2 * RS;
+    launch_wave(S, P, W, jt, own, own_cnt, sc->sm_count, st, &kc);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_fail(err, "record-build launch");
+    if (host) {
+      if (moments) err = cudaMemcpyAsync(moments + w0 * 2 * MS, W.moments, b * 2 * MS * 8, cudaMemcpyDeviceToHost, st);
+      if (err == cudaSuccess && stats)
+        err = cudaMemcpyAsync(stats + w0 * kStats, W.stats, b * kStats * 8, cudaMemcpyDeviceToHost, st);
+      if (err == cudaSuccess && records)
+        err = cudaMemcpyAsync(records + w0 * 2 * RS, W.records, b * 2 * RS * 8, cudaMemcpyDeviceToHost, st);
+      if (err != cudaSuccess) return cuda_fail(err, "result download");
+    }
+    if (insp) {
+      err = cudaStreamSynchronize(st);
+      if (err != cudaSuccess) return cuda_fail(err, "inspect sync");
+      if (insp->dirs) cudaMemcpy(insp->dirs, W.dirs, (size_t)n * D * 8, cudaMemcpyDeviceToHost);
+      if (insp->s) cudaMemcpy(insp->s, W.s, (size_t)n * 8, cudaMemcpyDeviceToHost);
+      if (insp->idx) cudaMemcpy(insp->idx, W.idx, (size_t)n * 4, cudaMemcpyDeviceToHost);
+      if (insp->counts) cudaMemcpy(insp->counts, W.cnt, (size_t)n * 4, cudaMemcpyDeviceToHost);
+      if (insp->tris && D == 3) cudaMemcpy(insp->tris, W.tris, (size_t)P.n_tris * 12, cudaMemcpyDeviceToHost);
+      long long base[2];
+      cudaMemcpy(base, W.rec_base, 16, cudaMemcpyDeviceToHost);
+      long long Pn = base[1] - base[0];
+      if (insp->P) *insp->P = Pn;
+      if (insp->media && insp->media_cap > 0)
+        cudaMemcpy(insp->media, W.media, (size_t)std::min<long long>(Pn, insp->media_cap) * 12,
+                   cudaMemcpyDeviceToHost);
+      err = cudaGetLastError();
+      if (err != cudaSuccess) return cuda_fail(err, "inspect copy");
+    }
+  }
+  g_launches += kc.launches;
+  if (host) {
+    err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) return cuda_fail(err, "record build");
+    if (stats && D == 3)
+      for (int i = 0; i < N; ++i)
+        if (stats[(size_t)i * kStats + 5] != 0)
+          return fail(VC_ETRI, "spherical Delaunay triangulation failed for record " + std::to_string(i));
+  }
+  return VC_OK;
+}
+
+}  // namespace vc
+
+using namespace vc;
+
+struct vc_scene_deleter {};
+
+extern "C" {
+
+int vc_version(void) { return 1; }
+
+const char* vc_last_error(void) { return g_err.c_str(); }
+
+int64_t vc_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+int vc_scene_create(int dim, int n_surfaces, const double* vertices, const double* emission,
+                    const double* albedo, const double* bounds_min, const double* bounds_max,
+                    double sigma_s, double sigma_a, vc_scene** out) {
+  if (!out) return fail(VC_EINVAL, "null output handle");
+  *out = nullptr;
+  if (dim != 2 && dim != 3) return fail(VC_EINVAL, "dimensionality must be 2 or 3");
+  if (n_surfaces < 0) return fail(VC_EINVAL, "negative surface count");
+  if (!(sigma_s >= 0.0) || !(sigma_a >= 0.0)) return fail(VC_EINVAL, "medium coefficients must be non-negative");
+  for (int a = 0; a < dim; ++a)
+    if (!(bounds_max[a] > bounds_min[a])) return fail(VC_EINVAL, "bounds max must exceed min on every axis");
+  vc_scene* sc = new vc_scene();
+  sc->dim = dim;
+  sc->K = n_surfaces;
+  sc->verts.assign(vertices, vertices + (size_t)n_surfaces * dim * dim);
+  sc->emission.assign(emission, emission + (size_t)n_surfaces * 3);
+  sc->albedo.assign(albedo, albedo + (size_t)n_surfaces * 3);
+  double sq = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    sc->bmin[a] = a < dim ? bounds_min[a] : 0.0;
+    sc->bmax[a] = a < dim ? bounds_max[a] : 0.0;
+    if (a < dim) sq += (bounds_max[a] - bounds_min[a]) * (bounds_max[a] - bounds_min[a]);
+  }
+  sc->scale = std::sqrt(sq);
+  sc->sigma_s = sigma_s;
+  sc->sigma_a = sigma_a;
+  sc->max_emission = 0.0;
+  sc->reflective = 0;
+  for (size_t i = 0; i < sc->emission.size(); ++i) sc->max_emission = std::max(sc->max_emission, sc->emission[i]);
+  for (size_t i = 0; i < sc->albedo.size(); ++i)
+    if (sc->albedo[i] > 0.0) sc->reflective = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sc->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (sc->sm_count <= 0) sc->sm_count = 148;
+  // primitives: float64 (v0, e1, e2) or (a, e), normals (src/scene.py:124-143)
+  const int K = n_surfaces, ps = prim_stride(dim);
+  std::vector<double> prim((size_t)K * ps), normal((size_t)K * dim);
+  for (int k = 0; k < K; ++k) {
+    const double* V = &sc->verts[(size_t)k * dim * dim];
+    double* P = &prim[(size_t)k * ps];
+    if (dim == 2) {
+      P[0] = V[0];
+      P[1] = V[1];
+      P[2] = V[2] - V[0];
+      P[3] = V[3] - V[1];
+      double len = std::sqrt(P[2] * P[2] + P[3] * P[3]);
+      normal[2 * k] = -P[3] / len;
+      normal[2 * k + 1] = P[2] / len;
+    } else {
+      for (int a = 0; a < 3; ++a) {
+        P[a] = V[a];
+        P[3 + a] = V[3 + a] - V[a];
+        P[6 + a] = V[6 + a] - V[a];
+      }
+      const double* e1 = P + 3;
+      const double* e2 = P + 6;
+      double c[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+      double nn = std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+      for (int a = 0; a < 3; ++a) normal[3 * k + a] = c[a] / nn;
+    }
+  }
+  std::vector<int> order(K);
+  for (int k = 0; k < K; ++k) order[k] = k;
+  HostBVH bvh;
+  if (K > 16) {
+    build_bvh(dim, K, sc->verts.data(), 1e-5 * sc->scale, &bvh);
+    std::memcpy(order.data(), bvh.order, sizeof(int) * K);
+  }
+  std::vector<double> prim_leaf((size_t)K * ps);
+  for (int i = 0; i < K; ++i)
+    std::memcpy(&prim_leaf[(size_t)i * ps], &prim[(size_t)order[i] * ps], ps * 8);
+  cudaError_t e = cudaSuccess;
+  auto up = [&](void** dst, const void* src, size_t bytes) {
+    if (e != cudaSuccess) return;
+    if (bytes == 0) bytes = 8;
+    e = cudaMalloc(dst, bytes);
+    if (e == cudaSuccess && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  up((void**)&sc->d_prim, K ? prim_leaf.data() : nullptr, prim_leaf.size() * 8);
+  up((void**)&sc->d_prim_id, K ? order.data() : nullptr, order.size() * 4);
+  up((void**)&sc->d_normal, K ? normal.data() : nullptr, normal.size() * 8);
+  up((void**)&sc->d_emission, K ? sc->emission.data() : nullptr, sc->emission.size() * 8);
+  up((void**)&sc->d_albedo, K ? sc->albedo.data() : nullptr, sc->albedo.size() * 8);
+  if (bvh.n_nodes) {
+    up((void**)&sc->d_nodes, bvh.nodes, sizeof(float4) * 2 * bvh.n_nodes);
+    sc->n_nodes = bvh.n_nodes;
+    free_bvh(&bvh);
+  }
+  if (e != cudaSuccess) {
+    delete sc;
+    return cuda_fail(e, "scene upload");
+  }
+  *out = sc;
+  return VC_OK;
+}
+
+void vc_scene_destroy(vc_scene* sc) { delete sc; }
+
+int vc_scene_set_budget(vc_scene* sc, int64_t bytes) {
+  if (!sc || bytes <= 0) return fail(VC_EINVAL, "invalid budget");
+  sc->budget = bytes;
+  return VC_OK;
+}
+
+int vc_build_records(vc_scene* sc, int n_records, const double* x, const void* rng, const int32_t* adjacency,
+                     const vc_build_params* params, double* moments, int64_t* stats, double* records,
+                     void* stream) {
+  return build_impl(sc, n_records, x, rng, adjacency, params, moments, stats, records, (cudaStream_t)stream,
+                    nullptr);
+}
+
+int vc_build_inspect(vc_scene* sc, const double* x, const void* rng, const int32_t* adjacency,
+                     const vc_build_params* params, double* dirs, double* s, int32_t* idx, int32_t* counts,
+                     int32_t* tris, float* media, int64_t media_cap, int64_t* P, double* moments,
+                     int64_t* stats) {
+  if (!params) return fail(VC_EINVAL, "null params");
+  vc_build_params p = *params;
+  p.flags |= VC_MEM_HOST;
+  Inspect in{dirs, s, idx, counts, tris, media, media_cap, P};
+  return build_impl(sc, 1, x, rng, adjacency, &p, moments, stats, nullptr, 0, &in);
+}
+
+int vc_make_records(int n, int dim, const double* x, const double* moments, double epsilon, double scene_scale,
+                    double max_emission, int flags, double* records, void* stream) {
+  if (dim != 2 && dim != 3) return fail(VC_EINVAL, "dim must be 2 or 3");
+  if (!(epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
+  if (n <= 0) return VC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool host = flags & VC_MEM_HOST;
+  const size_t MS = moment_size(dim), RS = record_size(dim);
+  DevScene S{};
+  S.dim = dim;
+  S.scale = scene_scale;
+  S.max_emission = max_emission;
+  BuildParams P{};
+  P.epsilon = epsilon;
+  P.anisotropic = (flags & VC_ISOTROPIC) ? 0 : 1;
+  Wave W{};
+  W.B = n;
+  cudaError_t e = cudaSuccess;
+  double *dx = nullptr, *dm = nullptr, *dr = nullptr;
+  if (host) {
+    e = cudaMalloc(&dx, (size_t)n * dim * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&dm, (size_t)n * 2 * MS * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&dr, (size_t)n * 2 * RS * 8);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dx, x, (size_t)n * dim * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dm, moments, (size_t)n * 2 * MS * 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "make_records staging");
+    W.x = dx;
+    W.moments = dm;
+    W.records = dr;
+  } else {
+    W.x = x;
+    W.moments = const_cast<double*>(moments);
+    W.records = records;
+  }
+  launch_make_records(S, P, W, st);
+  count_launches(1);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "make_records launch");
+  if (host) {
+    e = cudaMemcpyAsync(records, dr, (size_t)n * 2 * RS * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dx);
+    cudaFree(dm);
+    cudaFree(dr);
+    if (e != cudaSuccess) return cuda_fail(e, "make_records download");
+  }
+  return VC_OK;
+}
+
+int vc_seed_states(int n, const uint32_t* words, int nw, uint64_t* states) {
+  if (n < 0 || nw < 1 || nw > 16) return fail(VC_EINVAL, "seed words per record must be in [1, 16]");
+  for (int i = 0; i < n; ++i) seedseq_pcg64(words + (size_t)i * nw, nw, states + (size_t)i * 4);
+  return VC_OK;
+}
+
+}  // extern "C"

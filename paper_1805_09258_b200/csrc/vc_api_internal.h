@@ -1,0 +1,80 @@
+// Host-side handle types behind the C ABI (not part of the public header).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/volcache_b200.h"
+#include "vc_internal.h"
+
+namespace vc {
+
+struct Workspace {
+  static constexpr int kSlots = 40;
+  void* ptr[kSlots] = {nullptr};
+  size_t cap[kSlots] = {0};
+  void* get(int slot, size_t bytes, cudaError_t* err);
+  ~Workspace();
+};
+
+struct Inspect {
+  double* dirs;
+  double* s;
+  int32_t* idx;
+  int32_t* counts;
+  int32_t* tris;
+  float* media;
+  int64_t media_cap;
+  int64_t* P;
+};
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+bool grid_shape_3d(int n, int* rows, int* cols);
+void count_launches(long long n);
+const unsigned long long* jump_tables(cudaError_t* err);
+
+}  // namespace vc
+
+struct vc_scene {
+  int dim = 0, K = 0;
+  std::vector<double> verts, emission, albedo;
+  double bmin[3] = {0, 0, 0}, bmax[3] = {0, 0, 0};
+  double scale = 0.0, sigma_s = 0.0, sigma_a = 0.0, max_emission = 0.0;
+  int reflective = 0;
+  int sm_count = 148;
+  double* d_prim = nullptr;
+  int* d_prim_id = nullptr;
+  double* d_normal = nullptr;
+  double* d_emission = nullptr;
+  double* d_albedo = nullptr;
+  float4* d_nodes = nullptr;
+  int n_nodes = 0;
+  int es_nlight = -1, n_es = 0;
+  double* d_es_pos = nullptr;
+  double* d_es_w = nullptr;
+  int* d_es_surf = nullptr;
+  long long budget = 8LL << 30;
+  vc::Workspace ws;
+  ~vc_scene() {
+    cudaFree(d_prim);
+    cudaFree(d_prim_id);
+    cudaFree(d_normal);
+    cudaFree(d_emission);
+    cudaFree(d_albedo);
+    cudaFree(d_nodes);
+    cudaFree(d_es_pos);
+    cudaFree(d_es_w);
+    cudaFree(d_es_surf);
+  }
+};
+
+namespace vc {
+int ensure_emitters(vc_scene* sc, int n_light);
+DevScene dev_scene(const vc_scene* sc);
+int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int32_t* adjacency,
+               const vc_build_params* prm, double* moments, int64_t* stats, double* records,
+               cudaStream_t st, Inspect* insp);
+}  // namespace vc

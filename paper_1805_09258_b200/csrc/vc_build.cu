@@ -1,0 +1,879 @@
+// Record-build kernels: one wave of B cache points → moments (+ records).
+//
+// Pipeline per wave (reference: estimate_moments, src/subdivision.py:136-393):
+//   k_primary    thread per (record, direction): PCG64 jitter → stratified direction,
+//                nearest hit (BVH, float64 decision), surface radiance (+shadow rays)
+//   k_rings      CTA per record: R = ⌊max s/step + ½⌋, live-ring counts, exclusive prefix
+//   k_wave_scan  single CTA: media-sample offsets across the wave
+//   k_gather     grid-stride over media samples: PCG64 jump to the sample's draws,
+//                gather ray, σs·mean T·L_o  (src/transport.py:288-310)
+//   k_delaunay   thread per direction (3D): spherical Voronoi cell by half-space
+//                clipping with a security radius → canonical Delaunay triangles
+//   k_tri_compact CTA per record: owned triangles in point order → triangle list
+//   k_assemble   CTA per record: ring elements with live representative vertex are
+//                queued per warp (ballot compaction) and evaluated 32 at a time;
+//                moments summed with shuffles + shared-memory tree, no atomics
+//   k_make_record thread per (record, kind): eigen + radii (src/cache.py:146-189)
+#include <cfloat>
+#include <cstdio>
+
+#include "vc_device.cuh"
+#include "vc_eigen.cuh"
+#include "vc_build.h"
+
+namespace vc {
+
+// ---------------------------------------------------------------------------
+// Directions + primary rays
+// ---------------------------------------------------------------------------
+
+template <int D>
+__device__ inline void stratum_direction(int k, const BuildParams& P, Pcg64 g0, const JumpTables& jt,
+                                         double* out) {
+  if constexpr (D == 2) {
+    // θ = (k + ξ)·2π/n  (src/scene.py:415-418)
+    Pcg64 g = g0;
+    pcg_advance(g, (unsigned long long)k, jt);
+    double xi = g.next_double();
+    double th = mul(add((double)k, xi), __ddiv_rn(2.0 * kPi, (double)P.n_angular));
+    out[0] = cos(th);
+    out[1] = sin(th);
+  } else {
+    // z = 1 − 2(r+u)/rows, φ = (c+v)·2π/cols (src/scene.py:420-431); u block then v block
+    int r = k / P.cols, c = k - r * P.cols;
+    Pcg64 g = g0;
+    pcg_advance(g, (unsigned long long)k, jt);
+    double u = g.next_double();
+    Pcg64 h = g0;
+    pcg_advance(h, (unsigned long long)P.rows * P.cols + k, jt);
+    double v = h.next_double();
+    double z = sub(1.0, __ddiv_rn(mul(2.0, add((double)r, u)), (double)P.rows));
+    double phi = mul(add((double)c, v), __ddiv_rn(2.0 * kPi, (double)P.cols));
+    double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+    out[0] = mul(sq, cos(phi));
+    out[1] = mul(sq, sin(phi));
+    out[2] = z;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+  const int n = P.n_angular;
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)W.B * n) return;
+  int rec = (int)(gid / n), k = (int)(gid - (long long)rec * n);
+  Pcg64 g0 = pcg_load(W.rng + 4 * rec);
+  double d[3], o[3];
+  stratum_direction<D>(k, P, g0, jt, d);
+#pragma unroll
+  for (int a = 0; a < D; ++a) o[a] = W.x[rec * D + a];
+  double s;
+  int id;
+  trace_or_bounds<D>(S, o, d, s, id);
+  double hit[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) hit[a] = add(o[a], mul(s, d[a]));
+  double L[3];
+  surface_radiance<D>(S, id, hit, d, L);
+  size_t base = (size_t)rec * n + k;
+#pragma unroll
+  for (int a = 0; a < D; ++a) W.dirs[base * D + a] = d[a];
+  W.s[base] = s;
+  W.idx[base] = id;
+  W.lo[base * 3 + 0] = L[0];
+  W.lo[base * 3 + 1] = L[1];
+  W.lo[base * 3 + 2] = L[2];
+}
+
+// ---------------------------------------------------------------------------
+// Ring counts (src/subdivision.py:172-176)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double ring_radius(int i, double step) {
+  // (np.arange(1, R+1) − 0.5)·step, element i (0-based)
+  return mul((double)(i + 1) - 0.5, step);
+}
+
+__device__ __forceinline__ int live_rings(double s, int R, double step) {
+  double est = floor(__ddiv_rn(s, step) + 0.5);
+  int c = (int)fmin(fmax(est, 0.0), (double)R);
+  while (c > 0 && !(ring_radius(c - 1, step) < s)) --c;
+  while (c < R && ring_radius(c, step) < s) ++c;
+  return c;
+}
+
+template <int BS>
+__device__ inline long long block_exscan(long long v, long long& total, long long* sm) {
+  // sm: BS/32 + 1 entries
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = (lane < BS / 32) ? sm[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < BS / 32) sm[lane] = w;
+  }
+  __syncthreads();
+  long long pre = (wid > 0 ? sm[wid - 1] : 0) + x - v;
+  total = sm[BS / 32 - 1];
+  __syncthreads();
+  return pre;
+}
+
+constexpr int kRingBS = 512;
+
+__global__ void __launch_bounds__(kRingBS) k_rings(BuildParams P, Wave W) {
+  __shared__ long long sm[kRingBS / 32 + 1];
+  __shared__ double smax[kRingBS / 32];
+  const int rec = blockIdx.x, n = P.n_angular;
+  const double* s = W.s + (size_t)rec * n;
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < n; k += kRingBS) mx = fmax(mx, s[k]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kRingBS / 32 ? smax[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) smax[0] = v;
+  }
+  __syncthreads();
+  const double max_s = smax[0];
+  const int R = (int)floor(__ddiv_rn(max_s, P.march_step) + 0.5);
+  long long run = 0;
+  int maxc = 0;
+  for (int base = 0; base < n; base += kRingBS) {
+    int k = base + threadIdx.x;
+    int c = (k < n) ? live_rings(s[k], R, P.march_step) : 0;
+    maxc = max(maxc, c);
+    long long tot;
+    long long pre = block_exscan<kRingBS>(c, tot, sm);
+    if (k < n) {
+      W.cnt[(size_t)rec * n + k] = c;
+      W.pre[(size_t)rec * n + k] = (int)(run + pre);
+    }
+    run += tot;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
+  __shared__ int smc[kRingBS / 32];
+  if ((threadIdx.x & 31) == 0) smc[threadIdx.x >> 5] = maxc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int w = 0; w < kRingBS / 32; ++w) m = max(m, smc[w]);
+    W.rec_R[rec] = R;
+    W.rec_P[rec] = (int)run;
+    W.rec_maxc[rec] = m;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_wave_scan(Wave W, int gather_on) {
+  __shared__ long long sm[1024 / 32 + 1];
+  long long run = 0;
+  for (int base = 0; base < W.B; base += 1024) {
+    int r = base + threadIdx.x;
+    long long v = (r < W.B && gather_on) ? W.rec_P[r] : 0;
+    long long tot;
+    long long pre = block_exscan<1024>(v, tot, sm);
+    if (r < W.B) W.rec_base[r] = run + pre;
+    run += tot;
+  }
+  if (threadIdx.x == 0) W.rec_base[W.B] = run;
+}
+
+// ---------------------------------------------------------------------------
+// Media-sample gather (src/subdivision.py:177-195, src/transport.py:288-310)
+// ---------------------------------------------------------------------------
+
+template <int D>
+__global__ void __launch_bounds__(256) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+  const long long total = W.rec_base[W.B];
+  const int n = P.n_angular;
+  const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
+  const int per = (D == 3 ? 2 : 1) * P.n_inner;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total;
+       j += (long long)gridDim.x * blockDim.x) {
+    // record: last r with base[r] ≤ j
+    int lo = 0, hi = W.B - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (W.rec_base[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    const int rec = lo;
+    const int jl = (int)(j - W.rec_base[rec]);
+    const int* pre = W.pre + (size_t)rec * n;
+    int a = 0, b = n - 1;
+    while (a < b) {
+      int mid = (a + b + 1) >> 1;
+      if (pre[mid] <= jl) a = mid; else b = mid - 1;
+    }
+    const int k = a, i = jl - pre[k];
+    const double ri = ring_radius(i, P.march_step);
+    double y[3], dk[3];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      dk[c] = W.dirs[((size_t)rec * n + k) * D + c];
+      y[c] = add(W.x[rec * D + c], mul(ri, dk[c]));
+    }
+    Pcg64 g = pcg_load(W.rng + 4 * rec);
+    pcg_advance(g, (unsigned long long)(draws0 + (long long)per * jl), jt);
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int t = 0; t < P.n_inner; ++t) {
+      double gd[3];
+      if constexpr (D == 2) {
+        double th = mul(2.0 * kPi, g.next_double());
+        gd[0] = cos(th);
+        gd[1] = sin(th);
+      } else {
+        double u0 = g.next_double(), u1 = g.next_double();
+        double z = sub(1.0, mul(2.0, u0));
+        double phi = mul(2.0 * kPi, u1);
+        double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+        gd[0] = mul(sq, cos(phi));
+        gd[1] = mul(sq, sin(phi));
+        gd[2] = z;
+      }
+      double s2;
+      int id2;
+      trace_or_bounds<D>(S, y, gd, s2, id2);
+      if (id2 >= 0) {
+        double hp[3], L[3];
+#pragma unroll
+        for (int c = 0; c < D; ++c) hp[c] = add(y[c], mul(s2, gd[c]));
+        surface_radiance<D>(S, id2, hp, gd, L);
+        double T = exp(-S.sigma_t * s2);
+        acc[0] = add(acc[0], mul(T, L[0]));
+        acc[1] = add(acc[1], mul(T, L[1]));
+        acc[2] = add(acc[2], mul(T, L[2]));
+      }
+    }
+    float* out = W.media + (size_t)(W.rec_base[rec] + jl) * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double v = mul(S.sigma_s, __ddiv_rn(acc[c], (double)P.n_inner));
+      float f = (float)v;
+      if (v > 0.0 && !(f > 0.0f)) f = FLT_TRUE_MIN;  // keep the liveness bit exact
+      out[c] = f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Spherical Delaunay (3D connectivity, src/scene.py:388-399)
+// ---------------------------------------------------------------------------
+
+constexpr int kMaxV = 32;
+
+struct Line {
+  double A, B, C;
+};
+
+__device__ __forceinline__ Line cell_line(int lab, const double* p, const double* e1, const double* e2,
+                                          const double* dirs, double L) {
+  if (lab < 0) {
+    switch (lab) {
+      case -1: return {-1.0, 0.0, L};
+      case -2: return {0.0, -1.0, L};
+      case -3: return {1.0, 0.0, L};
+      default: return {0.0, 1.0, L};
+    }
+  }
+  const double* q = dirs + 3 * (size_t)lab;
+  double d[3] = {p[0] - q[0], p[1] - q[1], p[2] - q[2]};
+  return {e1[0] * d[0] + e1[1] * d[1] + e1[2] * d[2], e2[0] * d[0] + e2[1] * d[1] + e2[2] * d[2],
+          p[0] * d[0] + p[1] * d[1] + p[2] * d[2]};
+}
+
+__device__ __forceinline__ void meet(const Line& l1, const Line& l2, double& a, double& b) {
+  double det = l1.A * l2.B - l2.A * l1.B;
+  a = (l1.B * l2.C - l2.B * l1.C) / det;
+  b = (l2.A * l1.C - l1.A * l2.C) / det;
+}
+
+// Voronoi cell of point i over candidates within angle alpha (exact if the cell radius
+// stays below alpha/2).  Returns 0 secure, 1 needs a larger alpha, 2 polygon overflow.
+__device__ int voronoi_cell(const double* dirs, int rows, int cols, int i, double alpha, int* lab,
+                            int& m) {
+  const double* p = dirs + 3 * (size_t)i;
+  double h[3] = {0.0, 0.0, 1.0};
+  if (fabs(p[2]) >= 0.9) { h[0] = 1.0; h[2] = 0.0; }
+  double e1[3] = {h[1] * p[2] - h[2] * p[1], h[2] * p[0] - h[0] * p[2], h[0] * p[1] - h[1] * p[0]};
+  double ne = sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+  e1[0] /= ne; e1[1] /= ne; e1[2] /= ne;
+  double e2[3] = {p[1] * e1[2] - p[2] * e1[1], p[2] * e1[0] - p[0] * e1[2], p[0] * e1[1] - p[1] * e1[0]};
+  const double L = tan(fmin(alpha, 1.2));
+  double va[kMaxV], vb[kMaxV];
+  int lb2[kMaxV];
+  double va2[kMaxV], vb2[kMaxV];
+  m = 4;
+  va[0] = L;  vb[0] = -L; lab[0] = -1;
+  va[1] = L;  vb[1] = L;  lab[1] = -2;
+  va[2] = -L; vb[2] = L;  lab[2] = -3;
+  va[3] = -L; vb[3] = -L; lab[3] = -4;
+  double t2R = 2.0 * L * L;
+  auto cos2R = [&]() { return t2R >= 1.0 ? -1.0 : (1.0 - t2R) / (1.0 + t2R); };
+  double cut = cos2R();
+  // candidate rows / columns from the stratum grid
+  const double zp = p[2];
+  const double th = acos(fmin(fmax(zp, -1.0), 1.0));
+  const int r0 = i / cols, c0 = i - r0 * cols;
+  auto row_of = [&](double t) {
+    double z = cos(t);
+    int r = (int)floor((1.0 - z) * rows * 0.5);
+    return min(max(r, 0), rows - 1);
+  };
+  int rlo = (th - alpha <= 0.0) ? 0 : row_of(th - alpha);
+  int rhi = (th + alpha >= kPi) ? rows - 1 : row_of(th + alpha);
+  rlo = min(rlo, r0);
+  rhi = max(rhi, r0);
+  int half;
+  if (th <= alpha || th >= kPi - alpha) {
+    half = cols;
+  } else {
+    double sphi = sin(alpha) / sin(th);
+    double dphi = sphi >= 1.0 ? kPi : asin(sphi);
+    half = (int)ceil(dphi / (2.0 * kPi / cols)) + 1;
+    if (2 * half + 1 >= cols) half = cols;
+  }
+  const int span = max(r0 - rlo, rhi - r0);
+  const int ncol_iter = (half >= cols) ? cols : 2 * half + 1;
+  for (int rr = 0; rr <= 2 * span; ++rr) {
+    // rows outward from r0 (nearest first), skipping rows outside [rlo, rhi]
+    int dr = (rr + 1) >> 1;
+    int row = (rr & 1) ? r0 - dr : r0 + dr;
+    if (row < rlo || row > rhi) continue;
+    for (int cc = 0; cc < ncol_iter; ++cc) {
+      int dc = (cc + 1) >> 1;
+      int col = (cc & 1) ? c0 - dc : c0 + dc;
+      col %= cols;
+      if (col < 0) col += cols;
+      int j = row * cols + col;
+      if (j == i) continue;
+      const double* q = dirs + 3 * (size_t)j;
+      double pq = p[0] * q[0] + p[1] * q[1] + p[2] * q[2];
+      if (!(pq > cut)) continue;
+      Line ln = cell_line(j, p, e1, e2, dirs, L);
+      double f[kMaxV];
+      bool any_out = false;
+      for (int v = 0; v < m; ++v) {
+        f[v] = ln.A * va[v] + ln.B * vb[v] + ln.C;
+        any_out |= (f[v] < 0.0);
+      }
+      if (!any_out) continue;
+      // convex: one cyclic run of outside vertices [s, e]
+      int s = -1;
+      for (int v = 0; v < m; ++v) {
+        int pv = (v + m - 1) % m;
+        if (f[v] < 0.0 && !(f[pv] < 0.0)) { s = v; break; }
+      }
+      if (s < 0) return 2;  // every vertex outside: cannot happen (p is inside)
+      int e = s;
+      while (f[(e + 1) % m] < 0.0) e = (e + 1) % m;
+      int sp = (s + m - 1) % m;  // inside vertex before the run
+      int en = (e + 1) % m;      // inside vertex after the run
+      // new polygon starting at en: en .. sp (inside run), X (edge sp ∩ ln), Y (edge e ∩ ln)
+      int mm = 0;
+      for (int v = en;; v = (v + 1) % m) {
+        if (mm >= kMaxV - 2) return 2;
+        va2[mm] = va[v]; vb2[mm] = vb[v]; lb2[mm] = lab[v]; ++mm;
+        if (v == sp) break;
+      }
+      Line lsp = cell_line(lab[sp], p, e1, e2, dirs, L);
+      Line le = cell_line(lab[e], p, e1, e2, dirs, L);
+      meet(lsp, ln, va2[mm], vb2[mm]);
+      lb2[mm] = j;  // edge X→Y lies on the new bisector
+      ++mm;
+      meet(ln, le, va2[mm], vb2[mm]);
+      lb2[mm] = lab[e];
+      ++mm;
+      m = mm;
+      t2R = 0.0;
+      for (int v = 0; v < m; ++v) {
+        va[v] = va2[v]; vb[v] = vb2[v]; lab[v] = lb2[v];
+        t2R = fmax(t2R, va[v] * va[v] + vb[v] * vb[v]);
+      }
+      cut = cos2R();
+    }
+  }
+  for (int v = 0; v < m; ++v)
+    if (lab[v] < 0) return 1;
+  double th2 = tan(0.5 * alpha);
+  return (t2R <= th2 * th2) ? 0 : 1;
+}
+
+__global__ void __launch_bounds__(128) k_delaunay(BuildParams P, Wave W, int* own /* B×n×kMaxV×2 */,
+                                                  int* own_cnt) {
+  const int n = P.n_angular;
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)W.B * n) return;
+  int rec = (int)(gid / n), i = (int)(gid - (long long)rec * n);
+  const double* dirs = W.dirs + (size_t)rec * n * 3;
+  int lab[kMaxV];
+  int m = 0;
+  double alpha = 3.5 * sqrt(4.0 * kPi / n);
+  int st = 1;
+  for (int attempt = 0; attempt < 8 && st == 1; ++attempt) {
+    st = voronoi_cell(dirs, P.rows, P.cols, i, alpha, lab, m);
+    alpha = fmin(2.0 * alpha, 1.5);
+  }
+  size_t base = ((size_t)rec * n + i);
+  W.deg[base] = (st == 0) ? m : 0;
+  int c = 0;
+  if (st == 0) {
+    for (int t = 0; t < m; ++t) {
+      int a = lab[t], b = lab[(t + 1) % m];
+      if (i < a && i < b) {
+        own[(base * kMaxV + c) * 2 + 0] = a;
+        own[(base * kMaxV + c) * 2 + 1] = b;
+        ++c;
+      }
+    }
+  } else {
+    atomicMax(W.tri_status + rec, st);
+  }
+  own_cnt[base] = c;
+}
+
+constexpr int kCompactBS = 512;
+
+__global__ void __launch_bounds__(kCompactBS) k_tri_compact(BuildParams P, Wave W, const int* own,
+                                                            const int* own_cnt) {
+  __shared__ long long sm[kCompactBS / 32 + 1];
+  const int rec = blockIdx.x, n = P.n_angular;
+  int* tris = W.tris + (size_t)rec * P.n_tris * 3;
+  long long run = 0;
+  for (int base = 0; base < n; base += kCompactBS) {
+    int i = base + threadIdx.x;
+    int c = (i < n) ? own_cnt[(size_t)rec * n + i] : 0;
+    long long tot;
+    long long pre = block_exscan<kCompactBS>(c, tot, sm);
+    if (i < n) {
+      size_t ob = ((size_t)rec * n + i) * kMaxV;
+      for (int t = 0; t < c; ++t) {
+        long long o = run + pre + t;
+        if (o < P.n_tris) {
+          tris[o * 3 + 0] = i;
+          tris[o * 3 + 1] = own[(ob + t) * 2 + 0];
+          tris[o * 3 + 2] = own[(ob + t) * 2 + 1];
+        }
+      }
+    }
+    run += tot;
+  }
+  if (threadIdx.x == 0 && run != P.n_tris) atomicMax(W.tri_status + rec, 3);
+}
+
+// Vertex valence of caller-supplied triangles (star counting).
+__global__ void k_degree(BuildParams P, Wave W) {
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long tot = (long long)W.B * P.n_tris;
+  if (gid >= tot) return;
+  int rec = (int)(gid / P.n_tris);
+  const int* t = W.tris + gid * 3;
+  for (int v = 0; v < 3; ++v) atomicAdd(W.deg + (size_t)rec * P.n_angular + t[v], 1);
+}
+
+// ---------------------------------------------------------------------------
+// Moment assembly (src/subdivision.py:287-370)
+// ---------------------------------------------------------------------------
+
+constexpr int kAsmBS = 256;
+constexpr int kQCap = 64;
+
+template <int D>
+struct ElemView {
+  int v[D];
+};
+
+template <int D>
+__device__ __forceinline__ void elem_vertices(const Wave& W, const BuildParams& P, int rec, int e, int* v) {
+  if constexpr (D == 2) {
+    v[0] = e;
+    v[1] = (e + 1 == P.n_angular) ? 0 : e + 1;
+  } else {
+    const int* t = W.tris + ((size_t)rec * P.n_tris + e) * 3;
+    v[0] = t[0];
+    v[1] = t[1];
+    v[2] = t[2];
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kAsmBS) k_assemble(DevScene S, BuildParams P, Wave W) {
+  constexpr int NQ = 1 + D + D * (D + 1) / 2;
+  constexpr int NW = kAsmBS / 32;
+  __shared__ uint2 queue[NW][kQCap];
+  __shared__ double red[NW][NQ * 3];
+  __shared__ long long redc[NW][2];
+  const int rec = blockIdx.x;
+  const int n = P.n_angular;
+  const int E = (D == 2) ? n : P.n_tris;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (D == 3 && W.tri_status[rec] != 0) {
+    // triangulation failed for this record: zero moments, report the status
+    double* M = W.moments + (size_t)rec * 2 * moment_size(D);
+    for (int t = threadIdx.x; t < 2 * moment_size(D); t += kAsmBS) M[t] = 0.0;
+    if (threadIdx.x < kStats) W.stats[(size_t)rec * kStats + threadIdx.x] = (threadIdx.x == 5) ? W.tri_status[rec] : 0;
+    return;
+  }
+  const size_t rb = (size_t)rec * n;
+  const double* dirs = W.dirs + rb * D;
+  const double* sv = W.s + rb;
+  const int* idx = W.idx + rb;
+  const int* cnt = W.cnt + rb;
+  const int* pre = W.pre + rb;
+  const double* lo = W.lo + rb * 3;
+  const float* media = W.media + (size_t)W.rec_base[rec] * 3;
+  double x[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a] = W.x[rec * D + a];
+  const double fbar = S.sigma_s / (D == 2 ? 2.0 * kPi : 4.0 * kPi);
+  const double step = P.march_step;
+  const bool media_on = S.sigma_s > 0.0;  // σs = 0: media rings carry zero radiance
+  long long n_eval = 0, n_drop = 0, ev_kind[2] = {0, 0};
+
+  for (int kind = 0; kind < 2; ++kind) {
+    const double wt = fbar * (kind == 0 ? 1.0 : step);
+    double acc[3][NQ];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[c][q] = 0.0;
+    int qn = 0;  // warp-uniform queue length
+
+    // evaluate one queued item (element e at ring `ring`, representative vertex slot rep)
+    auto evaluate = [&](uint2 it) {
+      int e = (int)it.x;
+      int ring = (int)(it.y >> 2);
+      int rep = (int)(it.y & 3u);
+      int v[D];
+      elem_vertices<D>(W, P, rec, e, v);
+      double rv[D][3];
+      double dist[D];
+      double ri = (kind == 1) ? ring_radius(ring, step) : 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        bool live = (kind == 1) && (ring < cnt[v[j]]);
+        dist[j] = live ? ri : sv[v[j]];
+#pragma unroll
+        for (int a = 0; a < D; ++a) rv[j][a] = dist[j] * dirs[(size_t)v[j] * D + a];
+      }
+      double rad[3];
+      if (kind == 0) {
+        rad[0] = lo[v[rep] * 3 + 0];
+        rad[1] = lo[v[rep] * 3 + 1];
+        rad[2] = lo[v[rep] * 3 + 2];
+      } else {
+        const float* m = media + (size_t)(pre[v[rep]] + ring) * 3;
+        rad[0] = m[0];
+        rad[1] = m[1];
+        rad[2] = m[2];
+      }
+      double F, gF[D], HF[D * (D + 1) / 2];
+      bool ok;
+      if constexpr (D == 3) ok = ff_triangle(rv[0], rv[1], rv[2], F, gF, HF);
+      else ok = ff_segment(rv[0], rv[1], F, gF, HF);
+      ++n_eval;
+      ++ev_kind[kind];
+      if (!ok) {
+        ++n_drop;
+        return;
+      }
+      double w[D], q[NQ];
+#pragma unroll
+      for (int a = 0; a < D; ++a) w[a] = -rv[rep][a];
+      element_q<D>(w, dist[rep], S.sigma_t, F, gF, HF, q);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double f = wt * rad[c];
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) acc[c][t] += f * q[t];
+      }
+    };
+
+    // lane cursor over (element, ring)
+    int e = threadIdx.x;
+    int ring = 0;
+    int vv[D];
+    int cv[D];
+    double sd[D];
+    int maxc_e = 0;
+    bool fresh = true;
+    while (true) {
+      bool has = e < E;
+      bool flag = false;
+      uint2 item = make_uint2(0, 0);
+      if (has) {
+        if (fresh) {
+          elem_vertices<D>(W, P, rec, e, vv);
+          maxc_e = 0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            cv[j] = cnt[vv[j]];
+            sd[j] = sv[vv[j]];
+            maxc_e = max(maxc_e, cv[j]);
+          }
+          fresh = false;
+        }
+        if (kind == 0) {
+          int rep = 0;
+#pragma unroll
+          for (int j = 1; j < D; ++j)
+            if (sd[j] > sd[rep]) rep = j;
+          const double* L = lo + (size_t)vv[rep] * 3;
+          flag = (L[0] > 0.0) || (L[1] > 0.0) || (L[2] > 0.0);
+          item = make_uint2((unsigned)e, (unsigned)rep);
+          e += kAsmBS;
+          fresh = true;
+        } else {
+          if (ring < maxc_e) {
+            double ri = ring_radius(ring, step);
+            int rep = 0;
+            double best = (ring < cv[0]) ? ri : sd[0];
+            bool lrep = ring < cv[0];
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+              bool lj = ring < cv[j];
+              double dj = lj ? ri : sd[j];
+              if (dj > best) {
+                best = dj;
+                rep = j;
+                lrep = lj;
+              }
+            }
+            if (lrep && media_on) {
+              const float* m = media + (size_t)(pre[vv[rep]] + ring) * 3;
+              flag = (m[0] > 0.0f) || (m[1] > 0.0f) || (m[2] > 0.0f);
+            }
+            item = make_uint2((unsigned)e, ((unsigned)ring << 2) | (unsigned)rep);
+            ++ring;
+          }
+          if (ring >= maxc_e) {
+            e += kAsmBS;
+            ring = 0;
+            fresh = true;
+          }
+        }
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, flag);
+      if (flag) queue[wid][qn + __popc(bal & ((1u << lane) - 1u))] = item;
+      qn += __popc(bal);
+      __syncwarp();
+      if (qn >= 32) {
+        evaluate(queue[wid][lane]);
+        __syncwarp();
+        int rest = qn - 32;
+        if (lane < rest) queue[wid][lane] = queue[wid][32 + lane];
+        __syncwarp();
+        qn = rest;
+      }
+      if (!__any_sync(0xffffffffu, e < E)) break;
+    }
+    if (lane < qn) evaluate(queue[wid][lane]);
+    __syncwarp();
+
+    // reduce acc over the CTA: shuffles, then a shared-memory tree across warps
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        double v = acc[c][t];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[wid][c * NQ + t] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < NQ * 3) {
+      double v = 0.0;
+      for (int w = 0; w < NW; ++w) v += red[w][threadIdx.x];
+      // scatter into the reference layout: L(3), grad(3,D), hess(3,D,D)
+      int c = threadIdx.x / NQ, t = threadIdx.x - c * NQ;
+      double* M = W.moments + ((size_t)rec * 2 + kind) * moment_size(D);
+      if (t == 0) {
+        M[c] = v;
+      } else if (t <= D) {
+        M[3 + c * D + (t - 1)] = v;
+      } else {
+        int e2 = t - 1 - D, a = 0;
+        while (e2 >= D - a) { e2 -= D - a; ++a; }
+        int b = a + e2;
+        M[3 + 3 * D + c * D * D + a * D + b] = v;
+        M[3 + 3 * D + c * D * D + b * D + a] = v;
+      }
+    }
+    __syncthreads();
+  }
+
+  // counters: evaluated / dropped / per-kind evaluated
+  long long cs[4] = {n_eval, n_drop, ev_kind[0], ev_kind[1]};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], o);
+  __shared__ long long cred[NW][4];
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) cred[wid][k] = cs[k];
+  // star vertices: Σ_k [idx_k ≥ 0] · deg_k · (maxc − cnt_k)  (src/subdivision.py:205-207)
+  const int maxc = W.rec_maxc[rec];
+  long long stars = 0;
+  for (int k = threadIdx.x; k < n; k += kAsmBS) {
+    if (idx[k] >= 0) {
+      int dg = (D == 2) ? 2 : W.deg[rb + k];
+      stars += (long long)dg * (maxc - cnt[k]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) stars += __shfl_xor_sync(0xffffffffu, stars, o);
+  if (lane == 0) redc[wid][0] = stars;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t[4] = {0, 0, 0, 0}, st = 0;
+    for (int w = 0; w < NW; ++w) {
+      for (int k = 0; k < 4; ++k) t[k] += cred[w][k];
+      st += redc[w][0];
+    }
+    long long* o = W.stats + (size_t)rec * kStats;
+    o[0] = t[0];
+    o[1] = t[1];
+    o[2] = st;
+    o[3] = W.rec_base[rec + 1] - W.rec_base[rec];
+    o[4] = W.rec_R[rec];
+    o[5] = (D == 3) ? W.tri_status[rec] : 0;
+    o[6] = t[2];
+    o[7] = t[3];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// make_record (src/cache.py:146-189)
+// ---------------------------------------------------------------------------
+
+template <int D>
+__global__ void k_make_record(DevScene S, BuildParams P, Wave W) {
+  int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= W.B * 2) return;
+  int rec = gid >> 1, kind = gid & 1;
+  const double* M = W.moments + (size_t)gid * moment_size(D);
+  double* R = W.records + (size_t)gid * record_size(D);
+  const double lw[3] = {0.2126, 0.7152, 0.0722};
+  double lum = add(add(mul(M[0], lw[0]), mul(M[1], lw[1])), mul(M[2], lw[2]));
+  double Hl[9];
+  for (int e = 0; e < D * D; ++e) {
+    double h = 0.0;
+    for (int c = 0; c < 3; ++c) h += M[3 + 3 * D + c * D * D + e] * lw[c];
+    Hl[e] = h;
+  }
+  lum = fmax(lum, 1e-6 * S.max_emission);
+  double vals[3], V[9], radii[3];
+  const double rmax = 0.25 * S.scale;
+  if (lum <= 0.0) {
+    for (int e = 0; e < D * D; ++e) V[e] = (e % (D + 1) == 0) ? 1.0 : 0.0;
+    for (int a = 0; a < D; ++a) radii[a] = rmax;
+  } else {
+    eigen_sym<D>(Hl, vals, V);
+    if (!P.anisotropic) {
+      double mx = 0.0;
+      for (int a = 0; a < D; ++a) mx = fmax(mx, fabs(vals[a]));
+      for (int a = 0; a < D; ++a) vals[a] = mx;
+    }
+    const double floor_ = 1e-12 * lum / (S.scale * S.scale);
+    for (int a = 0; a < D; ++a) {
+      double lam = fabs(vals[a]);
+      double r = rmax;
+      if (lam > floor_) {
+        r = (D == 2) ? pow(4.0 * lum * P.epsilon / (kPi * lam), 0.25)
+                     : pow(15.0 * lum * P.epsilon / (4.0 * kPi * lam), 0.2);
+      }
+      radii[a] = fmin(r, rmax);
+    }
+  }
+  int o = 0;
+  for (int a = 0; a < D; ++a) R[o++] = W.x[rec * D + a];
+  for (int c = 0; c < 3; ++c) R[o++] = M[c];
+  for (int c = 0; c < 3 * D; ++c) R[o++] = M[3 + c];
+  for (int e = 0; e < D * D; ++e) R[o++] = V[e];
+  for (int a = 0; a < D; ++a) R[o++] = radii[a];
+}
+
+// ---------------------------------------------------------------------------
+// Seeds: SeedSequence(entropy words) → PCG64 states on device
+// ---------------------------------------------------------------------------
+
+__global__ void k_seedseq(int n, const uint32_t* words, int nw, uint64_t* states) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t w[16];
+  for (int k = 0; k < nw && k < 16; ++k) w[k] = words[(size_t)i * nw + k];
+  uint64_t st[4];
+  seedseq_pcg64(w, nw < 16 ? nw : 16, st);
+  for (int k = 0; k < 4; ++k) states[(size_t)i * 4 + k] = st[k];
+}
+
+// ---------------------------------------------------------------------------
+// Host launch sequence for one wave
+// ---------------------------------------------------------------------------
+
+static int grid_for(long long threads, int bs) { return (int)((threads + bs - 1) / bs); }
+
+template <int D>
+static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt,
+                          int* own, int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
+  const long long nt = (long long)W.B * P.n_angular;
+  k_primary<D><<<grid_for(nt, 256), 256, 0, st>>>(S, P, W, jt);
+  k_rings<<<W.B, kRingBS, 0, st>>>(P, W);
+  k_wave_scan<<<1, 1024, 0, st>>>(W, S.sigma_s > 0.0 ? 1 : 0);
+  int nl = 3;
+  if (S.sigma_s > 0.0) {
+    k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
+    ++nl;
+  }
+  if constexpr (D == 3) {
+    cudaMemsetAsync(W.tri_status, 0, sizeof(int) * W.B, st);
+    if (!P.host_adjacency) {
+      k_delaunay<<<grid_for(nt, 128), 128, 0, st>>>(P, W, own, own_cnt);
+      k_tri_compact<<<W.B, kCompactBS, 0, st>>>(P, W, own, own_cnt);
+      nl += 2;
+    } else {
+      cudaMemsetAsync(W.deg, 0, sizeof(int) * nt, st);
+      k_degree<<<grid_for((long long)W.B * P.n_tris, 256), 256, 0, st>>>(P, W);
+      ++nl;
+    }
+  }
+  k_assemble<D><<<W.B, kAsmBS, 0, st>>>(S, P, W);
+  ++nl;
+  if (P.make_records) {
+    k_make_record<D><<<grid_for(2LL * W.B, 128), 128, 0, st>>>(S, P, W);
+    ++nl;
+  }
+  if (kc) kc->launches += nl;
+}
+
+void launch_wave(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt, int* own,
+                 int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
+  if (S.dim == 2) launch_wave_t<2>(S, P, W, jt, own, own_cnt, sm_count, st, kc);
+  else launch_wave_t<3>(S, P, W, jt, own, own_cnt, sm_count, st, kc);
+}
+
+void launch_make_records(const DevScene& S, const BuildParams& P, const Wave& W, cudaStream_t st) {
+  if (S.dim == 2) k_make_record<2><<<grid_for(2LL * W.B, 128), 128, 0, st>>>(S, P, W);
+  else k_make_record<3><<<grid_for(2LL * W.B, 128), 128, 0, st>>>(S, P, W);
+}
+
+void launch_seedseq(int n, const uint32_t* words, int nw, uint64_t* states, cudaStream_t st) {
+  k_seedseq<<<grid_for(n, 128), 128, 0, st>>>(n, words, nw, states);
+}
+
+}  // namespace vc

@@ -1,0 +1,30 @@
+// Host-side declarations of the record-build launchers and runtime helpers.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vc_internal.h"
+
+namespace vc {
+
+struct KernelCounter {
+  long long launches = 0;
+};
+
+void launch_wave(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt, int* own,
+                 int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc);
+void launch_make_records(const DevScene& S, const BuildParams& P, const Wave& W, cudaStream_t st);
+void launch_seedseq(int n, const uint32_t* words, int nw, uint64_t* states, cudaStream_t st);
+
+// Host BVH build (binned SAH) over primitive bounds; returns nodes (2 float4 each)
+// and the leaf order of primitives.
+struct HostBVH {
+  int n_nodes = 0;
+  float4* nodes = nullptr;  // host array, 2*n_nodes
+  int* order = nullptr;     // leaf order → original primitive
+};
+void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out);
+void free_bvh(HostBVH* b);
+
+}  // namespace vc

@@ -1,0 +1,191 @@
+// Host BVH builder: binned SAH over primitive boxes, built once per scene.
+//
+// The reference traces by brute force over every primitive (src/scene.py:227-268);
+// the BVH only culls, so the nearest hit (float64 decision, lowest-index tie break)
+// is unchanged.  Boxes are float32 rounded outward and padded by `pad`, which keeps
+// float32 slab culling conservative for float64 rays.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "vc_build.h"
+
+namespace vc {
+
+namespace {
+
+struct Box {
+  float lo[3], hi[3];
+  void reset() {
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = FLT_MAX;
+      hi[a] = -FLT_MAX;
+    }
+  }
+  void grow(const Box& b) {
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], b.lo[a]);
+      hi[a] = std::max(hi[a], b.hi[a]);
+    }
+  }
+  float area() const {
+    float d[3];
+    for (int a = 0; a < 3; ++a) d[a] = std::max(0.0f, hi[a] - lo[a]);
+    return 2.0f * (d[0] * d[1] + d[1] * d[2] + d[0] * d[2]);
+  }
+};
+
+struct Node {
+  Box b;
+  int first, count;  // interior: first = left child, count = 0
+};
+
+constexpr int kBins = 16;
+constexpr int kLeafMax = 4;
+
+}  // namespace
+
+void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out) {
+  std::vector<Box> pb(K);
+  std::vector<float> cen(3 * (size_t)K);
+  const int nv = dim;  // vertices per primitive
+  for (int k = 0; k < K; ++k) {
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) {
+      lo[a] = hi[a] = verts[((size_t)k * nv) * dim + a];
+      for (int v = 1; v < nv; ++v) {
+        double x = verts[((size_t)k * nv + v) * dim + a];
+        lo[a] = std::min(lo[a], x);
+        hi[a] = std::max(hi[a], x);
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      float fl = std::nextafter((float)(lo[a] - pad), -FLT_MAX);
+      float fh = std::nextafter((float)(hi[a] + pad), FLT_MAX);
+      pb[k].lo[a] = fl;
+      pb[k].hi[a] = fh;
+      cen[3 * (size_t)k + a] = 0.5f * (fl + fh);
+    }
+  }
+  std::vector<int> order(K);
+  for (int k = 0; k < K; ++k) order[k] = k;
+  std::vector<Node> nodes;
+  nodes.reserve(2 * (size_t)K + 1);
+  nodes.push_back(Node{});
+  struct Task {
+    int node, begin, end;
+  };
+  std::vector<Task> stack;
+  stack.push_back({0, 0, K});
+  while (!stack.empty()) {
+    Task t = stack.back();
+    stack.pop_back();
+    Box nb, cb;
+    nb.reset();
+    cb.reset();
+    for (int i = t.begin; i < t.end; ++i) {
+      int k = order[i];
+      nb.grow(pb[k]);
+      Box c;
+      for (int a = 0; a < 3; ++a) c.lo[a] = c.hi[a] = cen[3 * (size_t)k + a];
+      cb.grow(c);
+    }
+    const int cnt = t.end - t.begin;
+    nodes[t.node].b = nb;
+    if (cnt <= kLeafMax) {
+      nodes[t.node].first = t.begin;
+      nodes[t.node].count = cnt;
+      continue;
+    }
+    // binned SAH over all axes
+    float best_cost = FLT_MAX;
+    int best_axis = -1, best_split = -1;
+    for (int a = 0; a < dim; ++a) {
+      float ext = cb.hi[a] - cb.lo[a];
+      if (!(ext > 0.0f)) continue;
+      Box bb[kBins];
+      int bc[kBins] = {0};
+      for (int i = 0; i < kBins; ++i) bb[i].reset();
+      for (int i = t.begin; i < t.end; ++i) {
+        int k = order[i];
+        int bi = (int)((cen[3 * (size_t)k + a] - cb.lo[a]) / ext * kBins);
+        bi = std::min(std::max(bi, 0), kBins - 1);
+        bc[bi]++;
+        bb[bi].grow(pb[k]);
+      }
+      float la[kBins], ra[kBins];
+      int lc[kBins], rc[kBins];
+      Box acc;
+      acc.reset();
+      int c = 0;
+      for (int i = 0; i < kBins; ++i) {
+        acc.grow(bb[i]);
+        c += bc[i];
+        la[i] = acc.area();
+        lc[i] = c;
+      }
+      acc.reset();
+      c = 0;
+      for (int i = kBins - 1; i >= 0; --i) {
+        acc.grow(bb[i]);
+        c += bc[i];
+        ra[i] = acc.area();
+        rc[i] = c;
+      }
+      for (int s = 0; s < kBins - 1; ++s) {
+        if (lc[s] == 0 || rc[s + 1] == 0) continue;
+        float cost = la[s] * lc[s] + ra[s + 1] * rc[s + 1];
+        if (cost < best_cost) {
+          best_cost = cost;
+          best_axis = a;
+          best_split = s;
+        }
+      }
+    }
+    int mid;
+    if (best_axis >= 0) {
+      float ext = cb.hi[best_axis] - cb.lo[best_axis];
+      auto it = std::partition(order.begin() + t.begin, order.begin() + t.end, [&](int k) {
+        int bi = (int)((cen[3 * (size_t)k + best_axis] - cb.lo[best_axis]) / ext * kBins);
+        bi = std::min(std::max(bi, 0), kBins - 1);
+        return bi <= best_split;
+      });
+      mid = (int)(it - order.begin());
+      if (mid == t.begin || mid == t.end) mid = (t.begin + t.end) / 2;
+    } else {
+      mid = (t.begin + t.end) / 2;  // coincident centroids: split by index
+    }
+    int left = (int)nodes.size();
+    nodes.push_back(Node{});
+    nodes.push_back(Node{});
+    nodes[t.node].first = left;
+    nodes[t.node].count = 0;
+    stack.push_back({left + 1, mid, t.end});
+    stack.push_back({left, t.begin, mid});
+  }
+  out->n_nodes = (int)nodes.size();
+  out->nodes = (float4*)malloc(sizeof(float4) * 2 * nodes.size());
+  out->order = (int*)malloc(sizeof(int) * (size_t)std::max(K, 1));
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    const Node& n = nodes[i];
+    float fi, fc;
+    std::memcpy(&fi, &n.first, 4);
+    std::memcpy(&fc, &n.count, 4);
+    out->nodes[2 * i] = make_float4(n.b.lo[0], n.b.lo[1], n.b.lo[2], fi);
+    out->nodes[2 * i + 1] = make_float4(n.b.hi[0], n.b.hi[1], n.b.hi[2], fc);
+  }
+  std::memcpy(out->order, order.data(), sizeof(int) * K);
+}
+
+void free_bvh(HostBVH* b) {
+  free(b->nodes);
+  free(b->order);
+  b->nodes = nullptr;
+  b->order = nullptr;
+  b->n_nodes = 0;
+}
+
+}  // namespace vc

@@ -1,0 +1,563 @@
+// Device building blocks of the cache-record path.
+//
+// Exactness rules (SURVEY.md §7 hard parts 3-4, Appendix A):
+//  * PCG64 streams are bit-exact with numpy (128-bit LCG, XSL-RR, double = (x>>11)·2⁻⁵³).
+//  * Ray–primitive tests run in float64 in the reference's operation order with FMA
+//    contraction disabled (__d*_rn), nearest hit with first-min (lowest index) tie break.
+//  * BVH boxes are float32, padded so culling is conservative; hits are decided in float64.
+#pragma once
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "vc_internal.h"
+
+namespace vc {
+
+typedef unsigned __int128 u128;
+
+// ---------------------------------------------------------------------------
+// PCG64 (numpy's default bit generator) — src/renderer.py:278-279 seeds it via SeedSequence
+// ---------------------------------------------------------------------------
+
+__host__ __device__ inline u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
+}
+
+struct Pcg64 {
+  u128 s, inc;
+  __device__ inline uint64_t next64() {
+    s = s * pcg_mult() + inc;
+    uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    uint64_t x = hi ^ lo;
+    unsigned rot = (unsigned)(s >> 122);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  __device__ inline double next_double() {
+    return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
+  }
+};
+
+__device__ inline u128 ld128(const unsigned long long* p) {
+  return ((u128)p[0] << 64) | (u128)p[1];
+}
+
+// Advance by delta draws with the precomputed 3-level table (delta < 2^30),
+// falling back to square-and-multiply beyond it.
+__device__ inline void pcg_advance(Pcg64& g, unsigned long long delta, const JumpTables& jt) {
+  if (delta < (1ULL << 30)) {
+#pragma unroll
+    for (int lv = 0; lv < 3; ++lv) {
+      unsigned k = (unsigned)(delta >> (10 * lv)) & 1023u;
+      if (k) {
+        const unsigned long long* e = jt.tab + ((size_t)lv * 1024 + k) * 4;
+        u128 A = ld128(e), G = ld128(e + 2);
+        g.s = A * g.s + G * g.inc;
+      }
+    }
+    return;
+  }
+  u128 am = 1, ap = 0, cm = pcg_mult(), cp = g.inc;
+  while (delta) {
+    if (delta & 1) {
+      am *= cm;
+      ap = ap * cm + cp;
+    }
+    cp = (cm + 1) * cp;
+    cm *= cm;
+    delta >>= 1;
+  }
+  g.s = am * g.s + ap;
+}
+
+__device__ inline Pcg64 pcg_load(const uint64_t* st) {
+  Pcg64 g;
+  g.s = ((u128)st[0] << 64) | (u128)st[1];
+  g.inc = ((u128)st[2] << 64) | (u128)st[3];
+  return g;
+}
+
+// numpy SeedSequence(entropy words) → PCG64 (state, inc).  Pool size 4, 32-bit hashes.
+__host__ __device__ inline void seedseq_pcg64(const uint32_t* w, int nw, uint64_t out[4]) {
+  const uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u, INIT_B = 0x8b51f9ddu,
+                 MULT_B = 0x58f38dedu, MIX_L = 0xca01f9ddu, MIX_R = 0x4973f715u;
+  uint32_t pool[4];
+  uint32_t hc = INIT_A;
+  auto hashmix = [&](uint32_t v) {
+    v ^= hc;
+    hc *= MULT_A;
+    v *= hc;
+    v ^= v >> 16;
+    return v;
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    uint32_t r = MIX_L * x - MIX_R * y;
+    r ^= r >> 16;
+    return r;
+  };
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < nw ? w[i] : 0u);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s]));
+  for (int s = 4; s < nw; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(w[s]));
+  uint32_t st[8];
+  uint32_t hb = INIT_B;
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i & 3];
+    v ^= hb;
+    hb *= MULT_B;
+    v *= hb;
+    v ^= v >> 16;
+    st[i] = v;
+  }
+  uint64_t q[4];
+  for (int i = 0; i < 4; ++i) q[i] = (uint64_t)st[2 * i] | ((uint64_t)st[2 * i + 1] << 32);
+  u128 seed = ((u128)q[0] << 64) | q[1];
+  u128 inc = ((((u128)q[2] << 64) | q[3]) << 1) | 1;
+  u128 s = 0;
+  s = s * pcg_mult() + inc;
+  s += seed;
+  s = s * pcg_mult() + inc;
+  out[0] = (uint64_t)(s >> 64);
+  out[1] = (uint64_t)s;
+  out[2] = (uint64_t)(inc >> 64);
+  out[3] = (uint64_t)inc;
+}
+
+// ---------------------------------------------------------------------------
+// numpy-faithful float64 helpers (no FMA contraction)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+  return add(add(mul(a[0], b[0]), mul(a[1], b[1])), mul(a[2], b[2]));
+}
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
+  c[0] = sub(mul(a[1], b[2]), mul(a[2], b[1]));
+  c[1] = sub(mul(a[2], b[0]), mul(a[0], b[2]));
+  c[2] = sub(mul(a[0], b[1]), mul(a[1], b[0]));
+}
+// np.maximum / np.minimum propagate NaN
+__device__ __forceinline__ double np_max(double a, double b) {
+  return (isnan(a) || isnan(b)) ? __longlong_as_double(0x7ff8000000000000LL) : (a >= b ? a : b);
+}
+__device__ __forceinline__ double np_min(double a, double b) {
+  return (isnan(a) || isnan(b)) ? __longlong_as_double(0x7ff8000000000000LL) : (a <= b ? a : b);
+}
+
+// ---------------------------------------------------------------------------
+// Ray–primitive tests (src/scene.py:227-268)
+// ---------------------------------------------------------------------------
+
+// 3D Möller–Trumbore on (v0, e1, e2); returns t or +inf when invalid.
+__device__ inline double hit_tri(const double* P, const double* o, const double* d, double t_eps) {
+  const double* v0 = P;
+  const double* e1 = P + 3;
+  const double* e2 = P + 6;
+  double pv[3], tv[3], qv[3];
+  cross3(d, e2, pv);
+  double det = dot3(e1, pv);
+  tv[0] = sub(o[0], v0[0]);
+  tv[1] = sub(o[1], v0[1]);
+  tv[2] = sub(o[2], v0[2]);
+  double inv = __ddiv_rn(1.0, det);
+  double u = mul(dot3(tv, pv), inv);
+  cross3(tv, e1, qv);
+  double v = mul(dot3(d, qv), inv);
+  double t = mul(dot3(e2, qv), inv);
+  bool ok = isfinite(t) && (fabs(det) > 0.0) && (u >= 0.0) && (v >= 0.0) && (add(u, v) <= 1.0) &&
+            (t > t_eps);
+  return ok ? t : INFINITY;
+}
+
+// 2D segment (a, e) cross-product test; returns t or +inf.
+__device__ inline double hit_seg(const double* P, const double* o, const double* d, double t_eps) {
+  double ax = sub(P[0], o[0]), ay = sub(P[1], o[1]);
+  double ex = P[2], ey = P[3];
+  double den = sub(mul(d[0], ey), mul(d[1], ex));
+  double t = __ddiv_rn(sub(mul(ax, ey), mul(ay, ex)), den);
+  double u = __ddiv_rn(sub(mul(ax, d[1]), mul(ay, d[0])), den);
+  bool ok = (fabs(den) > 0.0) && (u >= 0.0) && (u <= 1.0) && (t > t_eps);
+  return ok ? t : INFINITY;
+}
+
+template <int D>
+__device__ __forceinline__ double hit_prim(const double* P, const double* o, const double* d, double t_eps) {
+  if constexpr (D == 3) return hit_tri(P, o, d, t_eps);
+  else return hit_seg(P, o, d, t_eps);
+}
+
+// Conservative float32 slab test against a padded node box.
+template <int D>
+__device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, const float* of,
+                                        const float* inv, float t_best, float& t_near) {
+  float t0 = (lo.x - of[0]) * inv[0], t1 = (hi.x - of[0]) * inv[0];
+  float tn = fminf(t0, t1), tf = fmaxf(t0, t1);
+  t0 = (lo.y - of[1]) * inv[1];
+  t1 = (hi.y - of[1]) * inv[1];
+  tn = fmaxf(tn, fminf(t0, t1));
+  tf = fminf(tf, fmaxf(t0, t1));
+  if constexpr (D == 3) {
+    t0 = (lo.z - of[2]) * inv[2];
+    t1 = (hi.z - of[2]) * inv[2];
+    tn = fmaxf(tn, fminf(t0, t1));
+    tf = fminf(tf, fmaxf(t0, t1));
+  }
+  t_near = tn;
+  return tn <= tf && tf >= 0.0f && tn <= t_best;
+}
+
+// Nearest hit (src/scene.py:271-292).  `t_best` in/out (init +inf), `id_best` original index.
+template <int D>
+__device__ void trace_closest(const DevScene& S, const double* o, const double* d, double& t_best,
+                              int& id_best) {
+  const int ps = prim_stride(D);
+  t_best = INFINITY;
+  id_best = -1;
+  if (S.K == 0) return;
+  if (S.n_nodes == 0) {
+    for (int k = 0; k < S.K; ++k) {
+      double t = hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps);
+      int id = S.prim_id[k];
+      if (t < t_best || (t == t_best && t != INFINITY && id < id_best)) {
+        t_best = t;
+        id_best = id;
+      }
+    }
+    return;
+  }
+  float of[3], inv[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    of[a] = (float)o[a];
+    inv[a] = 1.0f / (float)d[a];
+  }
+  int stack[64];
+  int sp = 0;
+  int node = 0;
+  float tbf = INFINITY;
+  while (true) {
+    float4 lo = __ldg(S.nodes + 2 * node), hi = __ldg(S.nodes + 2 * node + 1);
+    float tn;
+    if (box_hit<D>(lo, hi, of, inv, tbf, tn)) {
+      int cnt = __float_as_int(hi.w);
+      int first = __float_as_int(lo.w);
+      if (cnt > 0) {
+        for (int k = first; k < first + cnt; ++k) {
+          double t = hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps);
+          if (t <= t_best && t != INFINITY) {
+            int id = S.prim_id[k];
+            if (t < t_best || id < id_best) {
+              t_best = t;
+              id_best = id;
+              // round up and widen slightly: ties at t_best must still enter boxes
+              tbf = __double2float_ru(t_best) * 1.0000005f + 1e-30f;
+            }
+          }
+        }
+      } else {
+        if (sp < 62) {
+          stack[sp++] = first + 1;
+          node = first;
+          continue;
+        }
+      }
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+}
+
+// Any valid hit with t < thr (shadow rays: visible iff nearest t ≥ thr, src/transport.py:213-214).
+template <int D>
+__device__ bool occluded(const DevScene& S, const double* o, const double* d, double thr) {
+  const int ps = prim_stride(D);
+  if (S.K == 0) return false;
+  if (S.n_nodes == 0) {
+    for (int k = 0; k < S.K; ++k)
+      if (hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps) < thr) return true;
+    return false;
+  }
+  float of[3], inv[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    of[a] = (float)o[a];
+    inv[a] = 1.0f / (float)d[a];
+  }
+  float tbf = __double2float_ru(thr) * 1.0000005f + 1e-30f;
+  int stack[64];
+  int sp = 0;
+  int node = 0;
+  while (true) {
+    float4 lo = __ldg(S.nodes + 2 * node), hi = __ldg(S.nodes + 2 * node + 1);
+    float tn;
+    if (box_hit<D>(lo, hi, of, inv, tbf, tn)) {
+      int cnt = __float_as_int(hi.w);
+      int first = __float_as_int(lo.w);
+      if (cnt > 0) {
+        for (int k = first; k < first + cnt; ++k)
+          if (hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps) < thr) return true;
+      } else if (sp < 62) {
+        stack[sp++] = first + 1;
+        node = first;
+        continue;
+      }
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+  return false;
+}
+
+// Distance to the bounds box exit (src/scene.py:295-303), NaN semantics of numpy.
+template <int D>
+__device__ inline double bounds_exit(const DevScene& S, const double* o, const double* d) {
+  double res = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double t1 = __ddiv_rn(sub(S.bmin[a], o[a]), d[a]);
+    double t2 = __ddiv_rn(sub(S.bmax[a], o[a]), d[a]);
+    double far = isnan(t1) ? INFINITY : np_max(t1, t2);
+    res = (a == 0) ? far : np_min(res, far);
+  }
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// Surface shading (src/transport.py:127-254)
+// ---------------------------------------------------------------------------
+
+template <int D>
+__device__ void direct_light(const DevScene& S, const double* p, const double* n, double acc[3]) {
+  acc[0] = acc[1] = acc[2] = 0.0;
+  const double off = 1e-6 * S.scale;
+  double org[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) org[a] = add(p[a], mul(off, n[a]));
+  for (int j = 0; j < S.n_es; ++j) {
+    const double* P = S.es_pos + (size_t)j * D;
+    double to[3], dd[3] = {0.0, 0.0, 0.0};
+    double r2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      to[a] = sub(P[a], org[a]);
+      r2 = add(r2, mul(to[a], to[a]));
+    }
+    double r = sqrt(r2);
+    bool ok = r > off;
+    if (!ok) continue;
+#pragma unroll
+    for (int a = 0; a < D; ++a) dd[a] = __ddiv_rn(to[a], r);
+    int e = S.es_surf[j];
+    const double* N = S.normal + (size_t)e * D;
+    double cp = 0.0, cq = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      cp = add(cp, mul(n[a], dd[a]));
+      cq = add(cq, mul(dd[a], N[a]));
+    }
+    cp = fmax(cp, 0.0);
+    cq = fabs(cq);
+    if (!(cp > 0.0 && cq > 0.0)) continue;
+    if (occluded<D>(S, org, dd, mul(r, 1.0 - 1e-6))) continue;
+    double rm = fmax(r, off);
+    double g = __ddiv_rn(mul(cp, cq), D == 3 ? mul(rm, rm) : rm);
+    g = mul(mul(g, exp(-S.sigma_t * r)), S.es_w[j]);
+    const double* E = S.emission + (size_t)e * 3;
+    acc[0] = add(acc[0], mul(g, E[0]));
+    acc[1] = add(acc[1], mul(g, E[1]));
+    acc[2] = add(acc[2], mul(g, E[2]));
+  }
+  const double norm = (D == 3) ? 3.141592653589793 : 2.0;
+  acc[0] = __ddiv_rn(acc[0], norm);
+  acc[1] = __ddiv_rn(acc[1], norm);
+  acc[2] = __ddiv_rn(acc[2], norm);
+}
+
+// Outgoing radiance at a hit: emission + albedo·direct; idx < 0 → 0.
+template <int D>
+__device__ void surface_radiance(const DevScene& S, int idx, const double* hit, const double* dir,
+                                 double out[3]) {
+  out[0] = out[1] = out[2] = 0.0;
+  if (idx < 0) return;
+  const double* E = S.emission + (size_t)idx * 3;
+  out[0] = E[0];
+  out[1] = E[1];
+  out[2] = E[2];
+  if (!S.reflective) return;
+  const double* A = S.albedo + (size_t)idx * 3;
+  if (!(A[0] > 0.0 || A[1] > 0.0 || A[2] > 0.0)) return;
+  const double* nn = S.normal + (size_t)idx * D;
+  double sd = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) sd = add(sd, mul(nn[a], dir[a]));
+  double sg = sd > 0.0 ? 1.0 : (sd < 0.0 ? -1.0 : 1.0);
+  double no[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) no[a] = -(nn[a] * sg);
+  double dl[3];
+  direct_light<D>(S, hit, no, dl);
+  out[0] = add(out[0], mul(A[0], dl[0]));
+  out[1] = add(out[1], mul(A[1], dl[1]));
+  out[2] = add(out[2], mul(A[2], dl[2]));
+}
+
+// trace_or_bounds (src/scene.py:306-315)
+template <int D>
+__device__ __forceinline__ void trace_or_bounds(const DevScene& S, const double* o, const double* d,
+                                                double& s, int& idx) {
+  double t;
+  trace_closest<D>(S, o, d, t, idx);
+  s = isfinite(t) ? t : bounds_exit<D>(S, o, d);
+}
+
+// ---------------------------------------------------------------------------
+// Form factors with derivatives (src/formfactor.py:85-343), float64 scalar form.
+// H is returned symmetrized, packed as xx, xy, (xz), yy, (yz), (zz).
+// ---------------------------------------------------------------------------
+
+constexpr double kPi = 3.141592653589793;
+
+__device__ inline bool ff_triangle(const double* r1v, const double* r2v, const double* r3v, double& F,
+                                   double g[3], double H[6]) {
+  const double* R[3] = {r1v, r2v, r3v};
+  double r[3];
+  for (int i = 0; i < 3; ++i) r[i] = sqrt(R[i][0] * R[i][0] + R[i][1] * R[i][1] + R[i][2] * R[i][2]);
+  if (!(r[0] > 0.0 && r[1] > 0.0 && r[2] > 0.0)) return false;
+  double c23[3], c12[3], c31[3];
+  cross3(R[1], R[2], c23);
+  cross3(R[0], R[1], c12);
+  cross3(R[2], R[0], c31);
+  double A = R[0][0] * c23[0] + R[0][1] * c23[1] + R[0][2] * c23[2];
+  double d12 = R[0][0] * R[1][0] + R[0][1] * R[1][1] + R[0][2] * R[1][2];
+  double d23 = R[1][0] * R[2][0] + R[1][1] * R[2][1] + R[1][2] * R[2][2];
+  double d13 = R[0][0] * R[2][0] + R[0][1] * R[2][1] + R[0][2] * R[2][2];
+  double B = r[0] * r[1] * r[2] + d12 * r[2] + d23 * r[0] + d13 * r[1];
+  double aA = fabs(A);
+  if (!(aA >= 1e-12 * r[0] * r[1] * r[2])) return false;
+  F = 2.0 * atan2(aA, B) / (4.0 * kPi);
+  double gA[3], gr[3][3], gB[3];
+  for (int c = 0; c < 3; ++c) {
+    gA[c] = -(c12[c] + c23[c] + c31[c]);
+    for (int i = 0; i < 3; ++i) gr[i][c] = -R[i][c] / r[i];
+  }
+  for (int c = 0; c < 3; ++c) {
+    gB[c] = (r[1] * r[2]) * gr[0][c] + (r[0] * r[2]) * gr[1][c] + (r[0] * r[1]) * gr[2][c] +
+            d12 * gr[2][c] - r[2] * (R[0][c] + R[1][c]) + d23 * gr[0][c] - r[0] * (R[1][c] + R[2][c]) +
+            d13 * gr[1][c] - r[1] * (R[0][c] + R[2][c]);
+  }
+  // HB (symmetric part only is needed downstream)
+  const double w3[3] = {r[1] * r[2], r[0] * r[2], r[0] * r[1]};
+  double g23[3], g13[3], g12[3], s12[3], s23[3], s13[3];
+  for (int c = 0; c < 3; ++c) {
+    g12[c] = r[1] * gr[0][c] + r[0] * gr[1][c];
+    g23[c] = r[2] * gr[1][c] + r[1] * gr[2][c];
+    g13[c] = r[2] * gr[0][c] + r[0] * gr[2][c];
+    s12[c] = R[0][c] + R[1][c];
+    s23[c] = R[1][c] + R[2][c];
+    s13[c] = R[0][c] + R[2][c];
+  }
+  const double dk[3] = {d23, d13, d12};  // coefficient of Jr_k in the j_dot terms (k = 0, 1, 2)
+  const int pij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  double HB[6];
+  for (int e = 0; e < 6; ++e) {
+    int a = pij[e][0], b = pij[e][1];
+    double I = (a == b) ? 1.0 : 0.0;
+    double h = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      double Jr = (I - R[i][a] * R[i][b] / (r[i] * r[i])) / r[i];
+      h += (w3[i] + dk[i]) * Jr + 2.0 * r[i] * I;
+    }
+    // outer(gr_i, g_jk) terms, symmetrized
+    h += 0.5 * (gr[0][a] * g23[b] + gr[0][b] * g23[a]) + 0.5 * (gr[1][a] * g13[b] + gr[1][b] * g13[a]) +
+         0.5 * (gr[2][a] * g12[b] + gr[2][b] * g12[a]);
+    // −outer(gr_k, p+q) − outer(p+q, gr_k) for (k=2, s12), (k=0, s23), (k=1, s13)
+    h -= gr[2][a] * s12[b] + s12[a] * gr[2][b];
+    h -= gr[0][a] * s23[b] + s23[a] * gr[0][b];
+    h -= gr[1][a] * s13[b] + s13[a] * gr[1][b];
+    HB[e] = h;
+  }
+  double sg = A >= 0.0 ? 1.0 : -1.0;
+  double gU[3], num[3], gD[3];
+  double den = A * A + B * B;
+  for (int c = 0; c < 3; ++c) {
+    gU[c] = sg * gA[c];
+    num[c] = B * gU[c] - aA * gB[c];
+    gD[c] = 2.0 * aA * gU[c] + 2.0 * B * gB[c];
+    g[c] = num[c] / den / (2.0 * kPi);
+  }
+  for (int e = 0; e < 6; ++e) {
+    int a = pij[e][0], b = pij[e][1];
+    double h = (-aA * HB[e]) / den - 0.5 * (num[a] * gD[b] + num[b] * gD[a]) / (den * den);
+    H[e] = h / (2.0 * kPi);
+  }
+  return true;
+}
+
+__device__ inline bool ff_segment(const double* u, const double* v, double& F, double g[2], double H[3]) {
+  double r0 = sqrt(u[0] * u[0] + u[1] * u[1]);
+  double r1 = sqrt(v[0] * v[0] + v[1] * v[1]);
+  if (!(r0 > 0.0 && r1 > 0.0)) return false;
+  double dt = u[0] * v[0] + u[1] * v[1];
+  double cr = u[0] * v[1] - u[1] * v[0];
+  double gam = atan2(fabs(cr), dt);
+  if (!(gam > 1e-5 && gam < kPi - 1e-5)) return false;
+  F = gam / (2.0 * kPi);
+  double ab = r0 * r1;
+  double c = fmin(fmax(dt / ab, -1.0), 1.0);
+  double sn = fabs(cr) / ab;
+  double a2 = r0 * r0, b2 = r1 * r1;
+  double gc[2];
+  for (int k = 0; k < 2; ++k) gc[k] = (c / a2) * u[k] + (c / b2) * v[k] - (u[k] + v[k]) / ab;
+  for (int k = 0; k < 2; ++k) g[k] = -(gc[k] / sn) / (2.0 * kPi);
+  const int pij[3][2] = {{0, 0}, {0, 1}, {1, 1}};
+  double w0[2], s[2];
+  for (int k = 0; k < 2; ++k) {
+    w0[k] = u[k] / (a2 * r0 * r1) + v[k] / (r0 * b2 * r1);
+    s[k] = u[k] + v[k];
+  }
+  for (int e = 0; e < 3; ++e) {
+    int a = pij[e][0], b = pij[e][1];
+    double I = (a == b) ? 1.0 : 0.0;
+    double jc = 0.5 * (u[a] * gc[b] + u[b] * gc[a]) / a2 + 2.0 * (c / (a2 * a2)) * u[a] * u[b] -
+                (c / a2) * I + 0.5 * (v[a] * gc[b] + v[b] * gc[a]) / b2 +
+                2.0 * (c / (b2 * b2)) * v[a] * v[b] - (c / b2) * I + 2.0 * I / ab -
+                0.5 * (s[a] * w0[b] + s[b] * w0[a]);
+    H[e] = -(jc / sn + (c / (sn * sn * sn)) * gc[a] * gc[b]) / (2.0 * kPi);
+  }
+  return true;
+}
+
+// Element contribution q = (T·F, ∇(T·F), H(T·F)) for representative offset w = x − y_rep
+// at stored distance dr (src/subdivision.py:320-340, src/transport.py:108-119).
+template <int D>
+__device__ inline void element_q(const double* w, double dr, double sigma_t, double F, const double* gF,
+                                 const double* HF, double* q /* 1 + D + D(D+1)/2 */) {
+  constexpr int NH = D * (D + 1) / 2;
+  double T = exp(-sigma_t * dr);
+  double gT[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) gT[a] = (-sigma_t * w[a]) / dr * T;
+  q[0] = T * F;
+#pragma unroll
+  for (int a = 0; a < D; ++a) q[1 + a] = T * gF[a] + gT[a] * F;
+  int e = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+#pragma unroll
+    for (int b = a; b < D; ++b) {
+      double ww = w[a] * w[b];
+      double I = (a == b) ? 1.0 : 0.0;
+      double HT = -sigma_t * (I / dr - ww / (dr * dr * dr) - sigma_t * ww / (dr * dr)) * T;
+      q[1 + D + e] = T * HF[e] + gT[a] * gF[b] + gF[a] * gT[b] + HT * F;
+      ++e;
+    }
+  }
+  (void)NH;
+}
+
+}  // namespace vc

@@ -1,0 +1,93 @@
+// Internal types shared by the host runtime and the device kernels of libvolcache_b200.
+//
+// Layout in HBM (all device arrays are structure-of-arrays unless noted):
+//   scene   : primitives in BVH-leaf order as float64 (3D: v0,e1,e2 = 9 doubles;
+//             2D: a,e = 4 doubles), original-order normals/emission/albedo, fp32
+//             BVH nodes (2×float4 each), emitter quadrature samples (float64).
+//   wave    : per-record scratch for B records processed together — directions,
+//             primary hits, ring counts/prefixes, surface radiance (float64),
+//             media-sample radiance (float32×3, one entry per live (dir, ring)),
+//             canonical spherical-Delaunay triangles (int32×3).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vc {
+
+constexpr int kMaxDim = 3;
+
+// Scene as seen by kernels (passed by value).
+struct DevScene {
+  int dim;
+  int K;                 // primitives
+  int n_nodes;           // BVH nodes (0 → brute force over K)
+  int n_es;              // emitter quadrature samples (all emitters)
+  int reflective;        // any albedo > 0
+  double bmin[3], bmax[3];
+  double scale, t_eps;   // bounds diagonal; 1e-6·scale self-hit guard (src/scene.py:22)
+  double sigma_s, sigma_a, sigma_t;
+  double max_emission;
+  const double* prim;    // leaf order, stride kPrimStride(dim)
+  const int* prim_id;    // leaf order → original surface index
+  const double* normal;  // original order, dim doubles each
+  const double* emission;// original order, 3 doubles
+  const double* albedo;  // original order, 3 doubles
+  const float4* nodes;   // 2 float4 per node: (lo.xyz, child/first), (hi.xyz, count)
+  const double* es_pos;  // n_es × dim
+  const double* es_w;    // n_es
+  const int* es_surf;    // n_es → original surface index of the emitter
+};
+
+__host__ __device__ constexpr int prim_stride(int dim) { return dim == 3 ? 9 : 4; }
+
+// Per-call record-build parameters (mirrors estimate_moments' arguments).
+struct BuildParams {
+  int n_angular;
+  double march_step;
+  int n_inner;
+  int rows, cols;        // 3D stratum grid (src/scene.py:370-385); 2D: rows = 1, cols = n
+  int n_tris;            // elements per ring: n (2D) or 2n-4 (3D)
+  int r_ub;              // upper bound on rings per record (allocation)
+  int host_adjacency;    // 1 → triangles supplied by the caller
+  double epsilon;        // record error budget (make_record)
+  int anisotropic;
+  int make_records;
+};
+
+// Per-record scratch for one wave (device pointers).
+struct Wave {
+  int B;                 // records in this wave
+  const double* x;       // B × dim
+  const uint64_t* rng;   // B × 4: state_hi, state_lo, inc_hi, inc_lo (PCG64, numpy layout)
+  double* dirs;          // B × n × dim
+  double* s;             // B × n primary hit distance (or bounds exit)
+  int* idx;              // B × n primary hit surface (−1: bounds)
+  int* cnt;              // B × n live rings per direction (after clamp to R)
+  int* pre;              // B × n exclusive prefix of cnt within the record
+  double* lo;            // B × n × 3 surface radiance
+  int* rec_R;            // B rings per record
+  int* rec_P;            // B live media samples per record
+  int* rec_maxc;         // B max cnt (rings that carry any live sample)
+  long long* rec_base;   // B+1 exclusive prefix of rec_P across the wave (+ total)
+  float* media;          // Σ P × 3 media radiance (positive values floored at FLT_TRUE_MIN)
+  long long media_cap;   // capacity in samples
+  int* tris;             // B × n_tris × 3 (3D) canonical or injected triangles
+  int* deg;              // B × n vertex valence (3D)
+  int* tri_status;       // B: 0 ok, else triangulation failure code
+  double* moments;       // B × 2 × M (M = 3 + 3d + 3d²)
+  long long* stats;      // B × kStats
+  double* records;       // B × 2 × RecordSize(d) (optional)
+};
+
+constexpr int kStats = 8;  // evaluated, dropped, stars, P, R, tri_status, eval_single, eval_multiple
+
+__host__ __device__ constexpr int moment_size(int d) { return 3 + 3 * d + 3 * d * d; }
+__host__ __device__ constexpr int record_size(int d) { return d + 3 + 3 * d + d * d + d; }
+
+// PCG64 jump tables (3 levels × 1024 entries): A = MULT^delta, G = Σ_{j<delta} MULT^j.
+struct JumpTables {
+  const unsigned long long* tab;  // [level][1024][4]: A_hi, A_lo, G_hi, G_lo
+};
+
+}  // namespace vc

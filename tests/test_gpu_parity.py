@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA record build / lookup / march against the reference goldens and the
+CPU oracle (tests/golden/* were produced by the reference itself, tests/golden/make_goldens.py).
+
+Tolerances (BASELINE.json north_star): radiance L ≤ 1e-4 relative, gradient and Hessian
+≤ 1e-3 relative L2 per record; hit indices, triangle sets and element counts bit-exact.
+The achieved errors are also written to gpurun_out/parity_errors.json for the record.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import REC_CASES, ROOT, golden, golden_scene, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL_L, TOL_G, TOL_H = 1e-4, 1e-3, 1e-3
+ERRORS: dict = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    prev = {}
+    p = out / "parity_errors.json"
+    if p.exists():
+        try:
+            prev = json.loads(p.read_text())
+        except Exception:
+            prev = {}
+    prev.update(ERRORS)
+    p.write_text(json.dumps(prev, indent=1, sort_keys=True))
+
+
+def _err(key, **v):
+    ERRORS[key] = {k: float(x) for k, x in v.items()}
+
+
+def _check_moments(tag, L, g, h, zL, zg, zh):
+    eL = max(rel_l2(L[k], zL[k], floor=1e-300) if np.linalg.norm(zL[k]) > 0 else float(np.abs(L[k]).max())
+             for k in range(2))
+    eg = max(rel_l2(g[k], zg[k], floor=1e-300) if np.linalg.norm(zg[k]) > 0 else float(np.abs(g[k]).max())
+             for k in range(2))
+    eh = max(rel_l2(h[k], zh[k], floor=1e-300) if np.linalg.norm(zh[k]) > 0 else float(np.abs(h[k]).max())
+             for k in range(2))
+    _err(tag, L=eL, grad=eg, hess=eh)
+    assert eL <= TOL_L, (tag, eL)
+    assert eg <= TOL_G, (tag, eg)
+    assert eh <= TOL_H, (tag, eh)
+
+
+def _quadform(axes, radii):
+    return axes @ np.diag(np.asarray(radii) ** -2.0) @ axes.T
+
+
+@pytest.mark.parametrize("case", REC_CASES)
+def test_records_vs_reference_goldens(case):
+    """GPU with the reference's own connectivity injected ≡ reference estimate_moments + make_record."""
+    from paper_1805_09258_b200 import estimate_moments_batch, inspect_record
+    from paper_1805_09258_b200.records import unpack_record
+
+    z = golden(f"rec_{case}")
+    sc = golden_scene(z)
+    n, step, n_inner, n_light, _ = z["params"]
+    seed = int(z["cfg_seed"])
+    N, d = z["points"].shape
+    words = np.array([[seed, 401, i] for i in range(N)], np.uint32)
+    adj = z["adj"].astype(np.int32) if d == 3 else None
+    r = estimate_moments_batch(sc, z["points"], seeds=words, n_angular=int(n), march_step=float(step),
+                               n_inner=int(n_inner), n_light_samples=int(n_light), adjacency=adj, epsilon=0.05)
+    for i in range(N):
+        _check_moments(f"{case}[{i}]", r.L[i], r.grad[i], r.hess[i], z["L"][i], z["grad"][i], z["hess"][i])
+        assert r.stats[i, 0] == z["stats"][i][0], "elements_evaluated"
+        assert r.stats[i, 1] == z["stats"][i][1], "elements_dropped"
+        assert r.stats[i, 2] == z["stats"][i][2], "star_vertices"
+        for k in range(2):
+            rec = unpack_record(r.records[i, k], d)
+            np.testing.assert_allclose(rec.value, z["rec_value"][i][k], rtol=1e-4, atol=1e-300)
+            q = _quadform(rec.axes, rec.radii)
+            qz = _quadform(z["rec_axes"][i][k], z["rec_radii"][i][k])
+            assert rel_l2(q, qz) <= 1e-3, (case, i, k)
+        ins = inspect_record(sc, z["points"][i], rng_seed=np.random.SeedSequence([seed, 401, i]),
+                             n_angular=int(n), march_step=float(step), n_inner=int(n_inner),
+                             n_light_samples=int(n_light), adjacency=adj[i] if adj is not None else None)
+        np.testing.assert_array_equal(ins["idx"], z["idx"][i])  # hit indices bit-exact
+        np.testing.assert_allclose(ins["dirs"], z["dirs"][i], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(ins["s"], z["s"][i], rtol=1e-13)
+
+
+def _tri_set(t):
+    return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
+
+
+@pytest.mark.parametrize("case", [c for c in REC_CASES if c.startswith(("cfg2", "box3d", "room"))])
+def test_gpu_delaunay_equals_qhull(case):
+    """The GPU spherical Delaunay reproduces qhull's hull triangle set exactly."""
+    from paper_1805_09258_b200 import inspect_record
+
+    z = golden(f"rec_{case}")
+    sc = golden_scene(z)
+    n, step, n_inner, n_light, _ = z["params"]
+    seed = int(z["cfg_seed"])
+    for i, x in enumerate(z["points"]):
+        ins = inspect_record(sc, x, rng_seed=np.random.SeedSequence([seed, 401, i]), n_angular=int(n),
+                             march_step=float(step), n_inner=int(n_inner), n_light_samples=int(n_light))
+        assert ins["stats"][5] == 0
+        assert _tri_set(ins["tris"]) == _tri_set(z["adj"][i])
+        assert len(ins["tris"]) == 2 * int(n) - 4
+
+
+@pytest.mark.parametrize("case", [c for c in REC_CASES if c.startswith(("cfg2_m01", "room", "box3d"))])
+def test_gpu_connectivity_vs_oracle(case):
+    """Default path (GPU triangulation) ≡ oracle re-run with the GPU's triangles injected."""
+    from paper_1805_09258_b200 import estimate_moments_batch, inspect_record
+    from oracle import volcache_oracle as O
+
+    z = golden(f"rec_{case}")
+    sc = golden_scene(z)
+    ps = O.pack(sc)
+    n, step, n_inner, n_light, _ = z["params"]
+    seed = int(z["cfg_seed"])
+    N = len(z["points"])
+    words = np.array([[seed, 401, i] for i in range(N)], np.uint32)
+    r = estimate_moments_batch(sc, z["points"], seeds=words, n_angular=int(n), march_step=float(step),
+                               n_inner=int(n_inner), n_light_samples=int(n_light))
+    for i, x in enumerate(z["points"]):
+        ins = inspect_record(sc, x, rng_seed=np.random.SeedSequence([seed, 401, i]), n_angular=int(n),
+                             march_step=float(step), n_inner=int(n_inner), n_light_samples=int(n_light))
+        ob = O.build_record(ps, x, int(n), float(step), O.seed_seq(seed, 401, i), int(n_inner), int(n_light),
+                            adjacency=ins["tris"])
+        _check_moments(f"{case}-gpuadj[{i}]", r.L[i], r.grad[i], r.hess[i], ob.L, ob.grad, ob.hess)
+        assert r.stats[i, 0] == ob.stats["elements_evaluated"]
+        assert r.stats[i, 2] == ob.stats["star_vertices"]
+        np.testing.assert_array_equal(ins["counts"], ob.counts)
+        if ob.media_radiance.size:
+            np.testing.assert_allclose(ins["media"], ob.media_radiance, rtol=1e-6, atol=0)
+
+
+def test_cfg1_batch_vs_oracle():
+    """Config 1 (2D flatland, n = 1024, surface ring): 64 records vs the oracle."""
+    from paper_1805_09258_b200 import configs, estimate_moments_batch, seed_words
+    from oracle import volcache_oracle as O
+
+    w = configs.cfg1()
+    ps = O.pack(w.scene)
+    idx = np.arange(64)
+    r = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=w.n_angular,
+                               march_step=w.march_step, epsilon=w.epsilon)
+    for i in idx:
+        ob = O.build_record(ps, w.points[i], w.n_angular, w.march_step, O.seed_seq(w.seed, 401, i))
+        _check_moments(f"cfg1[{i}]", r.L[i], r.grad[i], r.hess[i], ob.L, ob.grad, ob.hess)
+        assert r.stats[i, 0] == ob.stats["elements_evaluated"]
+
+
+def test_cfg2_full_size_properties():
+    """Config 2 at n = 4096: watertight 2n−4 triangulation per record, determinism, batch ≡ single,
+    and wave-splitting (sharding) invariance."""
+    from paper_1805_09258_b200 import configs, device_scene, estimate_moments_batch, inspect_record, seed_words
+
+    w = configs.cfg2()
+    idx = np.arange(48)
+    a = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=w.n_angular,
+                               march_step=0.1)
+    b = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=w.n_angular,
+                               march_step=0.1)
+    np.testing.assert_array_equal(a.moments, b.moments)  # bit-identical reruns
+    ds = device_scene(w.scene)
+    ds.set_budget(64 << 20)  # force several waves
+    c = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=w.n_angular,
+                               march_step=0.1)
+    ds.set_budget(8 << 30)
+    np.testing.assert_array_equal(a.moments, c.moments)
+    assert np.all(a.stats[:, 5] == 0)
+    ins = inspect_record(w.scene, w.points[7], rng_seed=np.random.SeedSequence([w.seed, 401, 7]),
+                         n_angular=w.n_angular, march_step=0.1)
+    np.testing.assert_array_equal(ins["moments"], a.moments[7])
+    t = ins["tris"]
+    edges = {}
+    for tri in t:
+        for u, v in ((tri[0], tri[1]), (tri[1], tri[2]), (tri[2], tri[0])):
+            edges[(min(u, v), max(u, v))] = edges.get((min(u, v), max(u, v)), 0) + 1
+    assert all(c == 2 for c in edges.values())  # closed 2-manifold
+    assert len(edges) == 3 * w.n_angular - 6  # Euler: E = 3n − 6
+
+
+def test_full_size_16k_directions_triangulation():
+    """n = 16384 (the metric's direction count): watertight, Euler-consistent, qhull-equal."""
+    from paper_1805_09258_b200 import configs, inspect_record
+    from oracle import volcache_oracle as O
+
+    sc = configs.cfg3_scene(n_spheres=4, level=1)
+    x = np.array([2.0, 1.5, 2.0])
+    ins = inspect_record(sc, x, rng_seed=np.random.SeedSequence([2, 401, 0]), n_angular=16384, march_step=0.5)
+    assert ins["stats"][5] == 0
+    rng = np.random.default_rng(np.random.SeedSequence([2, 401, 0]))
+    d, adj = O.directions(3, 16384, rng)
+    np.testing.assert_allclose(ins["dirs"], d, atol=1e-15, rtol=0)
+    assert _tri_set(ins["tris"]) == _tri_set(adj)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_interpolate_vs_reference(dim):
+    from paper_1805_09258_b200.cache import RadianceCache
+    from paper_1805_09258_b200.records import CacheRecord
+
+    z = golden("interpolate")
+    c = RadianceCache(np.zeros(dim), np.ones(dim))
+    for a in zip(z[f"d{dim}_pos"], z[f"d{dim}_value"], z[f"d{dim}_grad"], z[f"d{dim}_axes"], z[f"d{dim}_radii"]):
+        c.insert(CacheRecord(*a))
+    J, cnt = c.interpolate_many(z[f"d{dim}_q"])
+    np.testing.assert_array_equal(cnt, z[f"d{dim}_count"])  # covering sets ≡ reference tree query
+    zJ = z[f"d{dim}_J"]
+    np.testing.assert_array_equal(np.isnan(J[:, 0]), np.isnan(zJ[:, 0]))
+    ok = ~np.isnan(zJ[:, 0])
+    np.testing.assert_allclose(J[ok], zJ[ok], rtol=1e-12, atol=1e-14)
+    assert cnt[1] == 0  # exclusive support boundary (tests/test_cache.py:586-594)
+
+
+def test_render_vs_reference():
+    from paper_1805_09258_b200.cache import RadianceCache, render_frozen
+    from paper_1805_09258_b200.records import CacheRecord
+
+    z = golden("render")
+    sc = golden_scene(z)
+    caches = []
+    for kind in ("single", "multiple"):
+        c = RadianceCache(sc.bounds_min, sc.bounds_max)
+        for a in zip(z[f"{kind}_pos"], z[f"{kind}_value"], z[f"{kind}_grad"], z[f"{kind}_axes"], z[f"{kind}_radii"]):
+            c.insert(CacheRecord(*a))
+        caches.append(c)
+    eps, spp, step, n_ang, seed, n_inner, n_light = z["settings"]
+    cam = z["camera"]
+    camera = dict(position=cam[0:3], look_at=cam[3:6], up=cam[6:9], fov=cam[9], width=int(cam[10]),
+                  height=int(cam[11]))
+    img, st = render_frozen(sc, camera, caches[0], caches[1], spp=int(spp), march_step=float(step), seed=int(seed),
+                            n_angular=int(n_ang), n_inner=int(n_inner), n_light_samples=int(n_light), epsilon=eps)
+    np.testing.assert_allclose(img, z["image"], rtol=1e-9, atol=1e-12)
+    assert st["cache_hits"] == int(z["stats"][0])
+    assert st["direct_evaluations"] == int(z["stats"][1])
+
+
+def test_render_misses_vs_oracle():
+    """Frozen render with an empty cache: every march step is a direct evaluation (record build)."""
+    from paper_1805_09258_b200 import configs
+    from paper_1805_09258_b200.cache import RadianceCache, render_frozen
+    from oracle import volcache_oracle as O
+
+    sc = configs.cfg3_scene(n_spheres=3, level=1)
+    camera = dict(position=np.array([2.0, 1.5, 0.2]), look_at=np.array([2.0, 1.5, 4.0]),
+                  up=np.array([0.0, 1.0, 0.0]), fov=60.0, width=6, height=4)
+    empty = RadianceCache(sc.bounds_min, sc.bounds_max)
+    kw = dict(spp=2, march_step=1.0, seed=5, n_angular=256, n_inner=1, n_light_samples=16)
+    img, st = render_frozen(sc, camera, empty, empty, crop=(1, 2, 2, 3), **kw)
+    ps = O.pack(sc)
+    prm = O.RenderParams(epsilon=0.05, spp=2, march_step=1.0, n_angular=256, seed=5)
+    pix = [r * 6 + c for r in range(1, 3) for c in range(2, 5)]
+    center = 0.5 * (sc.bounds_min + sc.bounds_max)
+
+    def gpu_adjacency(seed):  # the triangulation depends only on the record's stream
+        from paper_1805_09258_b200 import inspect_record
+
+        return inspect_record(sc, center, rng_seed=seed, n_angular=256, march_step=1.0)["tris"]
+
+    ref, rst = O.render_camera(ps, dict(camera), O.Cache(), O.Cache(), prm, pixels=pix,
+                               adjacency_fn=gpu_adjacency)
+    got = img.reshape(-1, 3)[pix]
+    want = ref[pix]
+    _err("render_misses", image=rel_l2(got, want))
+    assert rel_l2(got, want) <= 1e-5
+    assert st["direct_evaluations"] == rst["direct_evaluations"]
+    assert np.all(img.reshape(-1, 3)[[i for i in range(24) if i not in pix]] == 0.0)  # crop only
+
+
+def test_errors_and_edge_cases():
+    from paper_1805_09258_b200 import configs, estimate_moments, estimate_moments_batch, seed_words
+    from paper_1805_09258_b200.scene import Medium, Scene
+
+    sc = configs.cfg1_scene()
+    with pytest.raises(ValueError):
+        estimate_moments(sc, np.array([1.5, 0.5]))
+    with pytest.raises(ValueError):
+        estimate_moments(sc, np.array([0.5, 0.5]), march_step=0.0)
+    sc3 = configs.cfg2_scene()
+    with pytest.raises(ValueError):
+        estimate_moments(sc3, np.array([0.5, 0.5, 0.5]), n_angular=7)  # no rows×cols grid
+    # empty scene: bounds terminations only → zero moments, no elements
+    empty = Scene((), Medium(0.5, 0.1), np.zeros(3), np.ones(3))
+    s, m = estimate_moments(empty, np.array([0.5, 0.5, 0.5]), n_angular=256, rng_seed=1)
+    assert np.all(s.L == 0) and np.all(m.L == 0)
+    # σs = 0: no media radiance; x on the bounds face is inside (±1e-12·scale)
+    dark = Scene(sc3.surfaces, Medium(0.0, 0.3), np.zeros(3), np.ones(3))
+    s, m = estimate_moments(dark, np.array([0.5, 0.0, 0.5]), n_angular=256, rng_seed=2)
+    assert np.all(m.L == 0)
+    # empty batch
+    r = estimate_moments_batch(sc, np.zeros((0, 2)), seeds=seed_words(0, 401, []), n_angular=64)
+    assert r.moments.shape == (0, 2, 21)
+
+
+def test_generator_advanced_like_reference():
+    """A Generator passed as rng_seed is advanced by exactly the draws the build consumed."""
+    from paper_1805_09258_b200 import configs, estimate_moments
+    from oracle import volcache_oracle as O
+
+    sc = configs.cfg1_scene()
+    g1 = np.random.default_rng(42)
+    g2 = np.random.default_rng(42)
+    estimate_moments(sc, np.array([0.3, 0.3]), n_angular=128, march_step=0.1, rng_seed=g1)
+    O.build_record(O.pack(sc), np.array([0.3, 0.3]), 128, 0.1, g2)
+    assert g1.random() == g2.random()
+
+
+def test_device_tensor_path():
+    """CUDA tensors in/out (async on the current stream), same numbers as the host path."""
+    import torch
+
+    from paper_1805_09258_b200 import configs, estimate_moments_batch, seed_words
+
+    w = configs.cfg2()
+    idx = np.arange(16)
+    h = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=1024,
+                               march_step=0.2, epsilon=0.05)
+    X = torch.tensor(w.points[idx], device="cuda")
+    S = torch.tensor(seed_words(w.seed, 401, idx).astype(np.int32), device="cuda")
+    d = estimate_moments_batch(w.scene, X, seeds=S, n_angular=1024, march_step=0.2, epsilon=0.05)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d.moments.cpu().numpy(), h.moments)
+    np.testing.assert_array_equal(d.records.cpu().numpy(), h.records)
