@@ -1,0 +1,375 @@
+"""Benchmark: cache records/sec (radiance + grad + Hessian, 16k dirs/record) on B200.
+
+Workload (BASELINE.json configs[2], parity variant — SURVEY.md §8d): the 4×3×4 window
+room with 40 seeded level-3 icospheres (51,300 triangles), σs = 0.27, σa = 0.03,
+19,000 cache points (seed 2), n = 16384 stratified directions per record,
+march_step 0.1, one gather direction per media sample, records finalised with ε = 0.05.
+A step builds `records_per_step` records per rank (points cycle through the config in
+order, per-record PCG64 streams SeedSequence([2, 401, i])).
+
+One process per GPU (torchrun for N > 1): ranks take disjoint record shards with no
+data-path collective ("weak" scaling); timing is CUDA events on each rank's stream,
+max over ranks.  `--impl reference` times the CPU oracle (numpy restatement of the
+reference, brute-force trace in C over all host threads) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "cache records/sec (radiance+grad+Hessian, 16k dirs/record); % of FP32 roofline"
+UNIT = "records/s"
+MEASURED = ROOT / "MEASURED_PEAKS.json"
+
+# Algorithmic flop model: divides/sqrt/exp/atan2 count 1.
+F_DIR3, F_REC, F_X3, F_LVL3, F_BOX3, F_ELEM3 = 20, 150, 45, 24, 12, 640
+F_TRI_POINT = 300  # spherical-Delaunay cell per direction (added: SURVEY's W omits qhull)
+
+
+def f_ray(K: int) -> int:
+    lg = int(np.ceil(np.log2(max(K, 2))))
+    return min(F_X3 * K, F_X3 + F_LVL3 * lg) + F_BOX3
+
+
+def peaks():
+    pk = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback"}
+    if MEASURED.exists():
+        d = json.loads(MEASURED.read_text())
+        pk.update(hbm_gbs=float(d.get("hbm_gbs", 6650.0)), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
+                  source="measured")
+    # FP32 vector peak: SMs × 128 lanes × 2 flop × f_max
+    pk["fp32_tflops"] = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+    return pk
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons, sampled during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.period = period
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, b in names.items():
+                    if r & b and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def workload(args):
+    from paper_1805_09258_b200 import configs
+
+    if args.config == "cfg3":
+        return configs.cfg3()
+    if args.config == "cfg2":
+        return configs.cfg2(march_step=args.march_step or 4.0)
+    if args.config == "cfg1":
+        return configs.cfg1(march_step=args.march_step or 4.0)
+    raise SystemExit(f"unknown config {args.config}")
+
+
+def step_indices(s: int, rank: int, world: int, B: int, N: int):
+    start = (s * world + rank) * B
+    return (start + np.arange(B)) % N
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline
+# ---------------------------------------------------------------------------
+
+
+def cpu_sample(w, n_records: int, start: int = 0):
+    """Oracle records (reference algorithm; brute-force trace over all host threads)."""
+    from oracle import volcache_oracle as O
+
+    threads = len(os.sched_getaffinity(0))
+    O.use_c_trace(threads)
+    ps = O.pack(w.scene)
+    t0 = time.perf_counter()
+    for i in range(start, start + n_records):
+        rb = O.build_record(ps, w.points[i % len(w.points)], w.n_angular, w.march_step,
+                            O.seed_seq(w.seed, 401, i % len(w.points)), w.n_inner, w.n_light_samples)
+        for k in range(2):
+            O.make_record(w.points[i % len(w.points)], rb.L[k], rb.grad[k], rb.hess[k], w.epsilon, ps.scale,
+                          ps.max_emission)
+    dt = time.perf_counter() - t0
+    return dt, threads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    w = workload(args)
+    per = max(1, args.cpu_records)
+    for s in range(args.warmup):
+        cpu_sample(w, per, start=s * per)
+    tot = 0.0
+    threads = 1
+    for s in range(args.steps):
+        dt, threads = cpu_sample(w, per, start=(args.warmup + s) * per)
+        tot += dt
+    value = args.steps * per / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded parity-variant scene, see DESIGN.md)",
+        "config": {"workload": w.name, "records_per_step": per, "n_angular": w.n_angular,
+                   "march_step": w.march_step, "triangles": len(w.scene.surfaces)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per} record(s) per step of {w.name}: oracle/volcache_oracle.py "
+                                   f"(numpy restatement) with the brute-force trace in oracle/trace_c.c "
+                                   f"on {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--march-step", type=float, default=None)
+    ap.add_argument("--records-per-step", type=int, default=2048)
+    ap.add_argument("--cpu-records", type=int, default=1, help="oracle records per CPU sample/step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_09258_b200 import _lib, device_scene, estimate_moments_batch, seed_words
+    from paper_1805_09258_b200.records import moment_size, record_size
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args)
+    N = len(w.points)
+    B = args.records_per_step
+    ds = device_scene(w.scene)
+    kw = dict(n_angular=w.n_angular, march_step=w.march_step, n_inner=w.n_inner,
+              n_light_samples=w.n_light_samples, epsilon=w.epsilon)
+    total_steps = args.warmup + args.steps
+    # inputs resident in HBM before timing
+    Xs, Ss = [], []
+    for s in range(total_steps):
+        idx = step_indices(s, rank, world, B, N)
+        Xs.append(torch.tensor(w.points[idx], device="cuda"))
+        Ss.append(torch.tensor(seed_words(w.seed, 401, idx).astype(np.int32), device="cuda"))
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    res = None
+    for s in range(args.warmup):
+        res = estimate_moments_batch(w.scene, Xs[s], seeds=Ss[s], **kw)
+    torch.cuda.synchronize()
+    L = _lib.lib()
+    L.vc_profile(1)
+    launches0 = L.vc_kernel_launches()
+    stats_acc = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for s in range(args.warmup, total_steps):
+            res = estimate_moments_batch(w.scene, Xs[s], seeds=Ss[s], **kw)
+            stats_acc.append(res.stats)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = L.vc_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    kms = np.zeros(12)
+    kcnt = np.zeros(12, np.int64)
+    L.vc_profile_read(_lib.ptr(kms), _lib.ptr(kcnt), 12)
+    L.vc_profile(0)
+    st = torch.cat(stats_acc).cpu().numpy()
+    tri_fail = int((st[:, 5] != 0).sum())
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    records = B * args.steps * world
+    value = records / (ms_max / 1e3)
+
+    # ---- e2e: public API with pinned host buffers, H2D + D2H inside the timed region ----
+    e2e_steps = max(1, args.e2e_steps)
+    Xh = [torch.tensor(w.points[step_indices(s, rank, world, B, N)]).pin_memory().numpy() for s in range(e2e_steps)]
+    Sh = [torch.tensor(seed_words(w.seed, 401, step_indices(s, rank, world, B, N)).astype(np.int32))
+          .pin_memory().numpy().view(np.uint32) for s in range(e2e_steps)]
+    d = ds.dim
+    MS, RS = moment_size(d), record_size(d)
+    mom_h = torch.empty((B, 2, MS), dtype=torch.float64).pin_memory().numpy()
+    rec_h = torch.empty((B, 2, RS), dtype=torch.float64).pin_memory().numpy()
+    st_h = torch.empty((B, 8), dtype=torch.int64).pin_memory().numpy()
+    prm = _lib.BuildParams()
+    prm.n_angular, prm.march_step, prm.n_inner = w.n_angular, w.march_step, w.n_inner
+    prm.n_light_samples, prm.epsilon = w.n_light_samples, w.epsilon
+    prm.flags = _lib.VC_MEM_HOST | _lib.VC_SEED_WORDS | _lib.VC_MAKE_RECORDS
+    prm.seed_words = 3
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        _lib.check(L.vc_build_records(ds.handle, B, _lib.ptr(Xh[s]), _lib.ptr(Sh[s]), None, _lib.C.byref(prm),
+                                      _lib.ptr(mom_h), _lib.ptr(st_h), _lib.ptr(rec_h), None))
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = B * e2e_steps * world / e2e_s
+    h2d = B * (d * 8 + 3 * 4)
+    d2h = B * (2 * MS * 8 + 8 * 8 + 2 * RS * 8)
+
+    # ---- roofline of the dominant kernel (CUDA events on the launching stream) ----
+    pk = peaks()
+    K = len(w.scene.surfaces)
+    n = w.n_angular
+    P_sum = float(st[:, 3].sum())
+    E_sum = float(st[:, 0].sum())
+    nrec = float(len(st))
+    work = {  # algorithmic flops over the timed region, per kernel class
+        "gather": P_sum * (6 + w.n_inner * (f_ray(K) + 10)),
+        "primary": nrec * n * (F_DIR3 + f_ray(K)),
+        "assemble": E_sum * F_ELEM3,
+        "delaunay": nrec * n * F_TRI_POINT,
+        "make_record": nrec * 2 * F_REC,
+    }
+    names = _lib.KERNEL_CLASSES
+    shares = {names[i]: float(kms[i]) for i in range(12) if kcnt[i] > 0}
+    dom = max(shares, key=shares.get)
+    dom_i = names.index(dom)
+    launches_dom = int(kcnt[dom_i])
+    avg_ms = float(kms[dom_i]) / max(launches_dom, 1)
+    flops_per_launch = work.get(dom, 0.0) / max(launches_dom, 1)
+    achieved = flops_per_launch / (avg_ms / 1e3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["fp32_tflops"], "traffic": traffic,
+                "peak_source": f"148 SMs x 128 FP32 lanes x 2 x sm_max_mhz ({pk['source']} clocks)",
+                "kernel_ms_share": {k: round(v / sum(shares.values()), 4) for k, v in shares.items()},
+                "algorithmic_flops_per_launch": flops_per_launch}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded parity-variant scene; no public dataset)",
+        "config": {"workload": w.name, "records_per_step": B * world, "records_per_rank_step": B,
+                   "n_angular": n, "march_step": w.march_step, "n_inner": w.n_inner, "epsilon": w.epsilon,
+                   "triangles": K, "cache_points": N, "parallelism": f"records sharded over {world} GPU(s)",
+                   "l2": "no flush: per-step scratch (media samples, directions) is GBs, far above the 126 MB L2",
+                   "samples_per_s": value * n, "mean_media_samples_per_record": P_sum / nrec,
+                   "mean_elements_evaluated": E_sum / nrec, "triangulation_failures": tri_fail},
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h * world},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, threads = cpu_sample(w, max(1, args.cpu_records))
+        line["cpu_baseline"] = {
+            "value": max(1, args.cpu_records) / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{max(1, args.cpu_records)} record(s) of {w.name} through oracle/volcache_oracle.py "
+                      f"(numpy restatement of the reference) with the brute-force trace in oracle/trace_c.c "
+                      f"on {threads} host threads",
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

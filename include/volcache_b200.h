@@ -38,6 +38,7 @@ extern "C" {
 #define VC_SEED_WORDS 2   /* rng = uint32 SeedSequence entropy words, seed_words per record */
 #define VC_MAKE_RECORDS 4 /* also finalize records (make_record) into `records` */
 #define VC_ISOTROPIC 8    /* make_record(..., anisotropic=False) */
+#define VC_TRACE_BOUNDS 16 /* vc_trace: trace_or_bounds semantics */
 
 typedef struct vc_scene vc_scene;
 typedef struct vc_cache vc_cache;
@@ -46,6 +47,13 @@ int vc_version(void);
 const char* vc_last_error(void);
 /* Kernel launches issued by this library since load (the bench's gpu_launches claim). */
 int64_t vc_kernel_launches(void);
+/* Per-kernel CUDA-event profile (events recorded on the launching stream while on).
+ * vc_profile(1) clears and enables; vc_profile_read fills per-class milliseconds and
+ * launch counts for up to max_classes classes, in the order: primary, rings, wave_scan,
+ * gather, delaunay, tri_compact, degree, assemble, make_record, seedseq, interpolate,
+ * march; returns the number of classes. */
+int vc_profile(int on);
+int vc_profile_read(double* ms, int64_t* launches, int max_classes);
 
 /* Scene upload + BVH build.  Replaces Scene/_Packed2D/_Packed3D (src/scene.py:124-219).
  * vertices: n_surfaces × dim × dim (segment endpoints or triangle corners), host memory.
@@ -99,6 +107,12 @@ int vc_build_inspect(vc_scene* scene, const double* x, const void* rng, const in
  * moments n × 2 × (3 + 3d + 3d²) → records n × 2 × (d + 3 + 3d + d² + d). */
 int vc_make_records(int n, int dim, const double* x, const double* moments, double epsilon,
                     double scene_scale, double max_emission, int flags, double* records, void* stream);
+
+/* Nearest hit per ray: trace (src/scene.py:271-292; misses t = inf, idx = −1) or, with
+ * VC_TRACE_BOUNDS, trace_or_bounds (src/scene.py:306-315; misses t = bounds exit).
+ * o, d: m × dim float64; t: m float64; idx: m int32 (original surface index). */
+int vc_trace(vc_scene* scene, int m, const double* o, const double* d, double* t, int32_t* idx, int flags,
+             void* stream);
 
 /* numpy SeedSequence(words) → PCG64 state (host), for n records of nw words each. */
 int vc_seed_states(int n, const uint32_t* words, int nw, uint64_t* states);

@@ -59,7 +59,8 @@ class PackedScene:
     bmax: np.ndarray
     sigma_s: float
     sigma_a: float
-    # derived
+    # derived (+ cached flat primitive array for the C helper)
+    _prim: np.ndarray = field(init=False, default=None, repr=False)
     a: np.ndarray = field(init=False)
     e1: np.ndarray = field(init=False)
     e2: np.ndarray = field(init=False)
@@ -173,6 +174,46 @@ def _hits_3d(ps, o, d, t_eps):
     return np.where(ok, t, np.inf)
 
 
+_C_TRACE = {"lib": None, "threads": 0}
+
+
+def use_c_trace(n_threads: int | None = None) -> bool:
+    """Route `trace` through oracle/trace_c.c (same brute-force algorithm, OpenMP over rays).
+
+    n_threads=0 switches back to numpy.  Returns whether the C helper is active.
+    """
+    import ctypes
+    import os
+    from pathlib import Path
+
+    if n_threads == 0:
+        _C_TRACE["threads"] = 0
+        return False
+    so = Path(__file__).resolve().parent / "_build" / "liboracle_trace.so"
+    if not so.exists():
+        from . import build_oracle
+
+        build_oracle.build()
+    if _C_TRACE["lib"] is None:
+        L = ctypes.CDLL(str(so))
+        L.oracle_trace.restype = None
+        L.oracle_trace.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_int]
+        _C_TRACE["lib"] = L
+    _C_TRACE["threads"] = int(n_threads or len(os.sched_getaffinity(0)))
+    return True
+
+
+def _prim_array(ps: PackedScene) -> np.ndarray:
+    if getattr(ps, "_prim", None) is None:
+        if ps.dim == 3:
+            ps._prim = np.ascontiguousarray(np.concatenate([ps.a, ps.e1, ps.e2], axis=1))
+        else:
+            ps._prim = np.ascontiguousarray(np.concatenate([ps.a, ps.e1], axis=1))
+    return ps._prim
+
+
 def trace(ps: PackedScene, origins, dirs, chunk: int = 4096):
     """Nearest hit per ray → (t, idx); misses (inf, −1).  src/scene.py:271-292.
 
@@ -187,6 +228,13 @@ def trace(ps: PackedScene, origins, dirs, chunk: int = 4096):
     if ps.K == 0 or m == 0:
         return t_out, i_out
     t_eps = T_EPS_REL * ps.scale
+    if _C_TRACE["threads"]:
+        P = _prim_array(ps)
+        oc = np.ascontiguousarray(o)
+        dc = np.ascontiguousarray(d)
+        _C_TRACE["lib"].oracle_trace(ps.dim, ps.K, P.ctypes.data, m, oc.ctypes.data, dc.ctypes.data,
+                                     t_eps, t_out.ctypes.data, i_out.ctypes.data, _C_TRACE["threads"])
+        return t_out, i_out
     step = max(1, min(chunk, (1 << 22) // max(ps.K, 1)))
     kern = _hits_2d if ps.dim == 2 else _hits_3d
     for lo in range(0, m, step):

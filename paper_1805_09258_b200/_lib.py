@@ -23,6 +23,7 @@ VC_MEM_HOST = 1
 VC_SEED_WORDS = 2
 VC_MAKE_RECORDS = 4
 VC_ISOTROPIC = 8
+VC_TRACE_BOUNDS = 16
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -73,6 +74,8 @@ _SIGS = {
     "vc_version": (C.c_int, []),
     "vc_last_error": (C.c_char_p, []),
     "vc_kernel_launches": (C.c_int64, []),
+    "vc_profile": (C.c_int, [C.c_int]),
+    "vc_profile_read": (C.c_int, [_vp, _vp, C.c_int]),
     "vc_scene_create": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double,
                                   C.POINTER(_vp)]),
     "vc_scene_destroy": (None, [_vp]),
@@ -82,6 +85,7 @@ _SIGS = {
                                    C.c_int64, _vp, _vp, _vp]),
     "vc_make_records": (C.c_int, [C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, C.c_double, C.c_int,
                                   _vp, _vp]),
+    "vc_trace": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "vc_seed_states": (C.c_int, [C.c_int, _vp, C.c_int, _vp]),
     "vc_cache_create": (C.c_int, [C.c_int, _vp, _vp, C.c_int, _vp, C.POINTER(_vp)]),
     "vc_cache_destroy": (None, [_vp]),
@@ -90,6 +94,9 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS)
+
+KERNEL_CLASSES = ("primary", "rings", "wave_scan", "gather", "delaunay", "tri_compact", "degree",
+                  "assemble", "make_record", "seedseq", "interpolate", "march")
 
 _lib = None
 

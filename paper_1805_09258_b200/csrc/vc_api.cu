@@ -1,4 +1,5 @@
 // C ABI of libvolcache_b200: scene upload, workspace management, wave orchestration.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -182,6 +183,9 @@ DevScene dev_scene(const vc_scene* sc) {
   S.emission = sc->d_emission;
   S.albedo = sc->d_albedo;
   S.nodes = sc->d_nodes;
+  S.n_em = sc->n_em;
+  S.em_prim = sc->d_em_prim;
+  S.em_id = sc->d_em_id;
   S.es_pos = sc->d_es_pos;
   S.es_w = sc->d_es_w;
   S.es_surf = sc->d_es_surf;
@@ -189,6 +193,48 @@ DevScene dev_scene(const vc_scene* sc) {
 }
 
 void count_launches(long long n) { g_launches += n; }
+
+// Optional per-kernel CUDA-event profile: events are recorded on the launching stream
+// around every kernel while enabled; vc_profile_read sums elapsed time per class.
+namespace {
+struct ProfRec {
+  int kc;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  int open_kc = -1;
+  cudaEvent_t open_ev = nullptr;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Profiler g_prof;
+}  // namespace
+
+void prof_begin(int kc, cudaStream_t st) {
+  if (!g_prof.on) return;
+  g_prof.open_kc = kc;
+  g_prof.open_ev = g_prof.get();
+  cudaEventRecord(g_prof.open_ev, st);
+}
+
+void prof_end(cudaStream_t st) {
+  if (!g_prof.on || g_prof.open_kc < 0) return;
+  cudaEvent_t b = g_prof.get();
+  cudaEventRecord(b, st);
+  g_prof.recs.push_back({g_prof.open_kc, g_prof.open_ev, b});
+  g_prof.open_kc = -1;
+}
 
 // ---------------------------------------------------------------------------
 // The record build, in waves sized by the scratch budget.
@@ -375,6 +421,35 @@ const char* vc_last_error(void) { return g_err.c_str(); }
 
 int64_t vc_kernel_launches(void) { return (int64_t)g_launches.load(); }
 
+int vc_profile(int on) {
+  for (auto& r : g_prof.recs) {
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.recs.clear();
+  g_prof.on = on != 0;
+  return VC_OK;
+}
+
+int vc_profile_read(double* ms, int64_t* launches, int max_classes) {
+  const int n = std::min<int>(max_classes, KC_COUNT);
+  for (int k = 0; k < n; ++k) {
+    ms[k] = 0.0;
+    launches[k] = 0;
+  }
+  for (auto& r : g_prof.recs) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_fail(e, "profile sync");
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.kc < n) {
+      ms[r.kc] += t;
+      launches[r.kc] += 1;
+    }
+  }
+  return KC_COUNT;
+}
+
 int vc_scene_create(int dim, int n_surfaces, const double* vertices, const double* emission,
                     const double* albedo, const double* bounds_min, const double* bounds_max,
                     double sigma_s, double sigma_a, vc_scene** out) {
@@ -458,6 +533,19 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
   up((void**)&sc->d_normal, K ? normal.data() : nullptr, normal.size() * 8);
   up((void**)&sc->d_emission, K ? sc->emission.data() : nullptr, sc->emission.size() * 8);
   up((void**)&sc->d_albedo, K ? sc->albedo.data() : nullptr, sc->albedo.size() * 8);
+  // emitter primitives in original order (emitter-first gather queries)
+  std::vector<double> em_prim;
+  std::vector<int> em_id;
+  for (int k = 0; k < K; ++k) {
+    const double* E = &sc->emission[3 * (size_t)k];
+    if (E[0] > 0.0 || E[1] > 0.0 || E[2] > 0.0) {
+      em_prim.insert(em_prim.end(), &prim[(size_t)k * ps], &prim[(size_t)k * ps] + ps);
+      em_id.push_back(k);
+    }
+  }
+  sc->n_em = (int)em_id.size();
+  up((void**)&sc->d_em_prim, em_prim.empty() ? nullptr : em_prim.data(), em_prim.size() * 8);
+  up((void**)&sc->d_em_id, em_id.empty() ? nullptr : em_id.data(), em_id.size() * 4);
   if (bvh.n_nodes) {
     up((void**)&sc->d_nodes, bvh.nodes, sizeof(float4) * 2 * bvh.n_nodes);
     sc->n_nodes = bvh.n_nodes;
@@ -542,6 +630,45 @@ int vc_make_records(int n, int dim, const double* x, const double* moments, doub
     cudaFree(dm);
     cudaFree(dr);
     if (e != cudaSuccess) return cuda_fail(e, "make_records download");
+  }
+  return VC_OK;
+}
+
+int vc_trace(vc_scene* sc, int m, const double* o, const double* d, double* t, int32_t* idx, int flags,
+             void* stream) {
+  if (!sc) return fail(VC_EINVAL, "null scene");
+  if (m <= 0) return VC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool host = flags & VC_MEM_HOST;
+  const int D = sc->dim;
+  const double* dO = o;
+  const double* dD = d;
+  double* dt = t;
+  int* di = idx;
+  void* buf = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (host) {
+    e = cudaMalloc(&buf, (size_t)m * (2 * D * 8 + 12));
+    if (e != cudaSuccess) return cuda_fail(e, "trace staging");
+    double* b = (double*)buf;
+    dO = b;
+    dD = b + (size_t)m * D;
+    dt = b + (size_t)2 * m * D;
+    di = (int*)(b + (size_t)2 * m * D + m);
+    e = cudaMemcpyAsync((void*)dO, o, (size_t)m * D * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((void*)dD, d, (size_t)m * D * 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "trace upload");
+  }
+  launch_trace(dev_scene(sc), m, dO, dD, dt, di, (flags & VC_TRACE_BOUNDS) ? 1 : 0, st);
+  g_launches += 1;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "trace launch");
+  if (host) {
+    e = cudaMemcpyAsync(t, dt, (size_t)m * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(idx, di, (size_t)m * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(buf);
+    if (e != cudaSuccess) return cuda_fail(e, "trace download");
   }
   return VC_OK;
 }

@@ -52,6 +52,9 @@ struct vc_scene {
   double* d_albedo = nullptr;
   float4* d_nodes = nullptr;
   int n_nodes = 0;
+  int n_em = 0;
+  double* d_em_prim = nullptr;
+  int* d_em_id = nullptr;
   int es_nlight = -1, n_es = 0;
   double* d_es_pos = nullptr;
   double* d_es_w = nullptr;
@@ -65,6 +68,8 @@ struct vc_scene {
     cudaFree(d_emission);
     cudaFree(d_albedo);
     cudaFree(d_nodes);
+    cudaFree(d_em_prim);
+    cudaFree(d_em_id);
     cudaFree(d_es_pos);
     cudaFree(d_es_w);
     cudaFree(d_es_surf);

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(256) k_gather(DevScene S, BuildParams P, Wave 
   const int n = P.n_angular;
   const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
   const int per = (D == 3 ? 2 : 1) * P.n_inner;
+  const bool emitter_first = !S.reflective && S.n_em <= 64;
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total;
        j += (long long)gridDim.x * blockDim.x) {
     // record: last r with base[r] ≤ j
@@ -248,7 +249,16 @@ __global__ void __launch_bounds__(256) k_gather(DevScene S, BuildParams P, Wave 
       }
       double s2;
       int id2;
-      trace_or_bounds<D>(S, y, gd, s2, id2);
+      if (emitter_first) {
+        // Non-reflective scene: L_o(hit) = emission, so only a nearest hit on an emitter
+        // carries radiance.  Find the nearest emitter, then ask the BVH whether any
+        // primitive precedes it in (t, index) order — same (s2, idx2) decision as the
+        // full nearest-hit search whenever the result can be non-zero.
+        nearest_emitter<D>(S, y, gd, s2, id2);
+        if (id2 >= 0 && occluded<D>(S, y, gd, s2, id2)) id2 = -1;
+      } else {
+        trace_or_bounds<D>(S, y, gd, s2, id2);
+      }
       if (id2 >= 0) {
         double hp[3], L[3];
 #pragma unroll
@@ -822,6 +832,33 @@ __global__ void k_seedseq(int n, const uint32_t* words, int nw, uint64_t* states
   for (int k = 0; k < 4; ++k) states[(size_t)i * 4 + k] = st[k];
 }
 
+// Raw nearest-hit queries (src/scene.py:271-315): trace (misses → inf, −1) or
+// trace_or_bounds (misses → bounds exit distance).
+template <int D>
+__global__ void k_trace(DevScene S, int m, const double* org, const double* dir, double* t_out, int* idx_out,
+                        int with_bounds) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double o[3], d[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    o[a] = org[(size_t)i * D + a];
+    d[a] = dir[(size_t)i * D + a];
+  }
+  double t;
+  int id;
+  if (with_bounds) trace_or_bounds<D>(S, o, d, t, id);
+  else trace_closest<D>(S, o, d, t, id);
+  t_out[i] = t;
+  idx_out[i] = id;
+}
+
+void launch_trace(const DevScene& S, int m, const double* o, const double* d, double* t, int* idx, int with_bounds,
+                  cudaStream_t st) {
+  if (S.dim == 2) k_trace<2><<<grid_for(m, 128), 128, 0, st>>>(S, m, o, d, t, idx, with_bounds);
+  else k_trace<3><<<grid_for(m, 128), 128, 0, st>>>(S, m, o, d, t, idx, with_bounds);
+}
+
 // ---------------------------------------------------------------------------
 // Host launch sequence for one wave
 // ---------------------------------------------------------------------------
@@ -832,30 +869,48 @@ template <int D>
 static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt,
                           int* own, int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
   const long long nt = (long long)W.B * P.n_angular;
+  prof_begin(KC_PRIMARY, st);
   k_primary<D><<<grid_for(nt, 256), 256, 0, st>>>(S, P, W, jt);
+  prof_end(st);
+  prof_begin(KC_RINGS, st);
   k_rings<<<W.B, kRingBS, 0, st>>>(P, W);
+  prof_end(st);
+  prof_begin(KC_WAVESCAN, st);
   k_wave_scan<<<1, 1024, 0, st>>>(W, S.sigma_s > 0.0 ? 1 : 0);
+  prof_end(st);
   int nl = 3;
   if (S.sigma_s > 0.0) {
-    k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
+    prof_begin(KC_GATHER, st);
+  k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
+  prof_end(st);
     ++nl;
   }
   if constexpr (D == 3) {
     cudaMemsetAsync(W.tri_status, 0, sizeof(int) * W.B, st);
     if (!P.host_adjacency) {
-      k_delaunay<<<grid_for(nt, 128), 128, 0, st>>>(P, W, own, own_cnt);
-      k_tri_compact<<<W.B, kCompactBS, 0, st>>>(P, W, own, own_cnt);
+      prof_begin(KC_DELAUNAY, st);
+  k_delaunay<<<grid_for(nt, 128), 128, 0, st>>>(P, W, own, own_cnt);
+  prof_end(st);
+      prof_begin(KC_COMPACT, st);
+  k_tri_compact<<<W.B, kCompactBS, 0, st>>>(P, W, own, own_cnt);
+  prof_end(st);
       nl += 2;
     } else {
       cudaMemsetAsync(W.deg, 0, sizeof(int) * nt, st);
-      k_degree<<<grid_for((long long)W.B * P.n_tris, 256), 256, 0, st>>>(P, W);
+      prof_begin(KC_DEGREE, st);
+  k_degree<<<grid_for((long long)W.B * P.n_tris, 256), 256, 0, st>>>(P, W);
+  prof_end(st);
       ++nl;
     }
   }
+  prof_begin(KC_ASSEMBLE, st);
   k_assemble<D><<<W.B, kAsmBS, 0, st>>>(S, P, W);
+  prof_end(st);
   ++nl;
   if (P.make_records) {
+    prof_begin(KC_RECORD, st);
     k_make_record<D><<<grid_for(2LL * W.B, 128), 128, 0, st>>>(S, P, W);
+    prof_end(st);
     ++nl;
   }
   if (kc) kc->launches += nl;
@@ -873,7 +928,9 @@ void launch_make_records(const DevScene& S, const BuildParams& P, const Wave& W,
 }
 
 void launch_seedseq(int n, const uint32_t* words, int nw, uint64_t* states, cudaStream_t st) {
+  prof_begin(KC_SEED, st);
   k_seedseq<<<grid_for(n, 128), 128, 0, st>>>(n, words, nw, states);
+  prof_end(st);
 }
 
 }  // namespace vc

@@ -12,8 +12,18 @@ struct KernelCounter {
   long long launches = 0;
 };
 
+// Kernel classes for the optional per-kernel CUDA-event profile (vc_profile_*).
+enum KernelClass {
+  KC_PRIMARY, KC_RINGS, KC_WAVESCAN, KC_GATHER, KC_DELAUNAY, KC_COMPACT, KC_DEGREE, KC_ASSEMBLE,
+  KC_RECORD, KC_SEED, KC_INTERP, KC_MARCH, KC_COUNT
+};
+void prof_begin(int kc, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
 void launch_wave(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt, int* own,
                  int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc);
+void launch_trace(const DevScene& S, int m, const double* o, const double* d, double* t, int* idx, int with_bounds,
+                  cudaStream_t st);
 void launch_make_records(const DevScene& S, const BuildParams& P, const Wave& W, cudaStream_t st);
 void launch_seedseq(int n, const uint32_t* words, int nw, uint64_t* states, cudaStream_t st);
 

@@ -74,7 +74,8 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out) {
   for (int k = 0; k < K; ++k) order[k] = k;
   std::vector<Node> nodes;
   nodes.reserve(2 * (size_t)K + 1);
-  nodes.push_back(Node{});
+  nodes.push_back(Node{});  // root
+  nodes.push_back(Node{});  // pad: child pairs start at even indices → 64-byte aligned
   struct Task {
     int node, begin, end;
   };

@@ -211,106 +211,137 @@ __device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, cons
   return tn <= tf && tf >= 0.0f && tn <= t_best;
 }
 
-// Nearest hit (src/scene.py:271-292).  `t_best` in/out (init +inf), `id_best` original index.
+// Visit one primitive of a leaf (float64 decision, src/scene.py:242-268).
+template <int D>
+__device__ __forceinline__ double leaf_hit(const DevScene& S, int k, const double* o, const double* d) {
+  return hit_prim<D>(S.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+}
+
+// Ordered BVH traversal.  mode 0: nearest hit (t_best/id_best out).  mode 1: any hit
+// that precedes (thr, id_thr) in (t, index) order — returns true on the first one.
+template <int D, int MODE>
+__device__ bool bvh_query(const DevScene& S, const double* o, const double* d, double& t_best, int& id_best) {
+  float of[3] = {0.f, 0.f, 0.f}, inv[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    of[a] = (float)o[a];
+    inv[a] = 1.0f / (float)d[a];
+  }
+  // slack: float32 t limit strictly above the float64 one
+  auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + 1e-5f * (float)S.scale : INFINITY; };
+  float tbf = tlim(t_best);
+  int stack[64];
+  float stn[64];
+  int sp = 0;
+  int node = 0;
+  {
+    float tn;
+    if (!box_hit<D>(__ldg(S.nodes), __ldg(S.nodes + 1), of, inv, tbf, tn)) return false;
+  }
+  while (true) {
+    const float4 meta = __ldg(S.nodes + 2 * node);
+    const float4 mh = __ldg(S.nodes + 2 * node + 1);
+    int cnt = __float_as_int(mh.w);
+    int first = __float_as_int(meta.w);
+    if (cnt > 0) {
+      for (int k = first; k < first + cnt; ++k) {
+        double t = leaf_hit<D>(S, k, o, d);
+        if (t == INFINITY) continue;
+        int id = S.prim_id[k];
+        if (MODE == 0) {
+          if (t < t_best || (t == t_best && id < id_best)) {
+            t_best = t;
+            id_best = id;
+            tbf = tlim(t_best);
+          }
+        } else {
+          if (t < t_best || (t == t_best && id < id_best)) return true;
+        }
+      }
+    } else {
+      const float4 l0 = __ldg(S.nodes + 2 * first), l1 = __ldg(S.nodes + 2 * first + 1);
+      const float4 r0 = __ldg(S.nodes + 2 * first + 2), r1 = __ldg(S.nodes + 2 * first + 3);
+      float tl, tr;
+      bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
+      bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
+      if (hl && hr) {
+        int nearc = (tl <= tr) ? first : first + 1;
+        if (sp < 64) {
+          stack[sp] = (tl <= tr) ? first + 1 : first;
+          stn[sp] = fmaxf(tl, tr);
+          ++sp;
+        }
+        node = nearc;
+        continue;
+      }
+      if (hl) { node = first; continue; }
+      if (hr) { node = first + 1; continue; }
+    }
+    // pop, skipping entries whose entry distance is beyond the current best
+    bool found = false;
+    while (sp > 0) {
+      --sp;
+      if (stn[sp] <= tbf) {
+        node = stack[sp];
+        found = true;
+        break;
+      }
+    }
+    if (!found) break;
+  }
+  return false;
+}
+
+// Nearest hit (src/scene.py:271-292).  `id_best` is the original surface index.
 template <int D>
 __device__ void trace_closest(const DevScene& S, const double* o, const double* d, double& t_best,
                               int& id_best) {
-  const int ps = prim_stride(D);
   t_best = INFINITY;
   id_best = -1;
   if (S.K == 0) return;
   if (S.n_nodes == 0) {
     for (int k = 0; k < S.K; ++k) {
-      double t = hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps);
-      int id = S.prim_id[k];
-      if (t < t_best || (t == t_best && t != INFINITY && id < id_best)) {
+      double t = hit_prim<D>(S.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+      if (t < t_best) {  // primitives in original order: strict < keeps the first minimum
         t_best = t;
-        id_best = id;
+        id_best = S.prim_id[k];
       }
     }
     return;
   }
-  float of[3], inv[3];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    of[a] = (float)o[a];
-    inv[a] = 1.0f / (float)d[a];
-  }
-  int stack[64];
-  int sp = 0;
-  int node = 0;
-  float tbf = INFINITY;
-  while (true) {
-    float4 lo = __ldg(S.nodes + 2 * node), hi = __ldg(S.nodes + 2 * node + 1);
-    float tn;
-    if (box_hit<D>(lo, hi, of, inv, tbf, tn)) {
-      int cnt = __float_as_int(hi.w);
-      int first = __float_as_int(lo.w);
-      if (cnt > 0) {
-        for (int k = first; k < first + cnt; ++k) {
-          double t = hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps);
-          if (t <= t_best && t != INFINITY) {
-            int id = S.prim_id[k];
-            if (t < t_best || id < id_best) {
-              t_best = t;
-              id_best = id;
-              // round up and widen slightly: ties at t_best must still enter boxes
-              tbf = __double2float_ru(t_best) * 1.0000005f + 1e-30f;
-            }
-          }
-        }
-      } else {
-        if (sp < 62) {
-          stack[sp++] = first + 1;
-          node = first;
-          continue;
-        }
-      }
-    }
-    if (sp == 0) break;
-    node = stack[--sp];
-  }
+  bvh_query<D, 0>(S, o, d, t_best, id_best);
 }
 
-// Any valid hit with t < thr (shadow rays: visible iff nearest t ≥ thr, src/transport.py:213-214).
+// Is there a valid hit preceding (thr, id_thr) in (t, index) order?  Shadow rays use
+// id_thr = −1 (visible iff nearest t ≥ thr, src/transport.py:213-214).
 template <int D>
-__device__ bool occluded(const DevScene& S, const double* o, const double* d, double thr) {
-  const int ps = prim_stride(D);
+__device__ bool occluded(const DevScene& S, const double* o, const double* d, double thr, int id_thr = -1) {
   if (S.K == 0) return false;
   if (S.n_nodes == 0) {
-    for (int k = 0; k < S.K; ++k)
-      if (hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps) < thr) return true;
+    for (int k = 0; k < S.K; ++k) {
+      double t = hit_prim<D>(S.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+      if (t < thr || (t == thr && S.prim_id[k] < id_thr)) return true;
+    }
     return false;
   }
-  float of[3], inv[3];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    of[a] = (float)o[a];
-    inv[a] = 1.0f / (float)d[a];
-  }
-  float tbf = __double2float_ru(thr) * 1.0000005f + 1e-30f;
-  int stack[64];
-  int sp = 0;
-  int node = 0;
-  while (true) {
-    float4 lo = __ldg(S.nodes + 2 * node), hi = __ldg(S.nodes + 2 * node + 1);
-    float tn;
-    if (box_hit<D>(lo, hi, of, inv, tbf, tn)) {
-      int cnt = __float_as_int(hi.w);
-      int first = __float_as_int(lo.w);
-      if (cnt > 0) {
-        for (int k = first; k < first + cnt; ++k)
-          if (hit_prim<D>(S.prim + (size_t)k * ps, o, d, S.t_eps) < thr) return true;
-      } else if (sp < 62) {
-        stack[sp++] = first + 1;
-        node = first;
-        continue;
-      }
+  double t = thr;
+  int id = id_thr;
+  return bvh_query<D, 1>(S, o, d, t, id);
+}
+
+// Nearest emitter hit (emitters in original order; lowest index wins ties).
+template <int D>
+__device__ __forceinline__ void nearest_emitter(const DevScene& S, const double* o, const double* d, double& te,
+                                                int& ie) {
+  te = INFINITY;
+  ie = -1;
+  for (int j = 0; j < S.n_em; ++j) {
+    double t = hit_prim<D>(S.em_prim + (size_t)j * prim_stride(D), o, d, S.t_eps);
+    if (t < te) {
+      te = t;
+      ie = S.em_id[j];
     }
-    if (sp == 0) break;
-    node = stack[--sp];
   }
-  return false;
 }
 
 // Distance to the bounds box exit (src/scene.py:295-303), NaN semantics of numpy.

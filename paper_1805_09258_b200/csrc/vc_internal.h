@@ -34,6 +34,9 @@ struct DevScene {
   const double* emission;// original order, 3 doubles
   const double* albedo;  // original order, 3 doubles
   const float4* nodes;   // 2 float4 per node: (lo.xyz, child/first), (hi.xyz, count)
+  int n_em;              // emitter primitives (emitter-first gather when !reflective)
+  const double* em_prim; // n_em primitives in original order (prim_stride doubles each)
+  const int* em_id;      // n_em original surface indices
   const double* es_pos;  // n_es × dim
   const double* es_w;    // n_es
   const int* es_surf;    // n_es → original surface index of the emitter

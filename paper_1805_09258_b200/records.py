@@ -339,6 +339,19 @@ def make_record(x, moments, epsilon, scene_scale, max_emission, anisotropic=True
     return unpack_record(rec[0, 0], d)
 
 
+def trace(scene, origins, dirs, with_bounds=False):
+    """Nearest hit per ray → (t, idx): trace / trace_or_bounds (src/scene.py:271-315)."""
+    ds = device_scene(scene)
+    o = np.ascontiguousarray(np.asarray(origins, float).reshape(-1, ds.dim))
+    d = np.ascontiguousarray(np.asarray(dirs, float).reshape(-1, ds.dim))
+    m = o.shape[0]
+    t = np.zeros(m)
+    idx = np.zeros(m, np.int32)
+    flags = _lib.VC_MEM_HOST | (_lib.VC_TRACE_BOUNDS if with_bounds else 0)
+    _lib.check(_lib.lib().vc_trace(ds.handle, m, _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), _lib.ptr(idx), flags, None))
+    return t, idx.astype(np.int64)
+
+
 def seed_words(cfg_seed: int, purpose: int, idx) -> np.ndarray:
     """(cfg_seed, purpose, i) rows as uint32 entropy words (src/renderer.py:278-279)."""
     idx = np.asarray(idx, dtype=np.int64)
