@@ -832,6 +832,8 @@ __global__ void k_seedseq(int n, const uint32_t* words, int nw, uint64_t* states
   for (int k = 0; k < 4; ++k) states[(size_t)i * 4 + k] = st[k];
 }
 
+static int grid_for(long long threads, int bs) { return (int)((threads + bs - 1) / bs); }
+
 // Raw nearest-hit queries (src/scene.py:271-315): trace (misses → inf, −1) or
 // trace_or_bounds (misses → bounds exit distance).
 template <int D>
@@ -862,8 +864,6 @@ void launch_trace(const DevScene& S, int m, const double* o, const double* d, do
 // ---------------------------------------------------------------------------
 // Host launch sequence for one wave
 // ---------------------------------------------------------------------------
-
-static int grid_for(long long threads, int bs) { return (int)((threads + bs - 1) / bs); }
 
 template <int D>
 static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt,
