@@ -292,7 +292,7 @@ def test_trace_vs_reference_goldens(name):
     sc = golden_scene(z, f"{name}_")
     s, idx = trace(sc, z[f"{name}_o"], z[f"{name}_d"], with_bounds=True)
     np.testing.assert_array_equal(idx, z[f"{name}_idx"])
-    np.testing.assert_allclose(s, z[f"{name}_s"], rtol=4e-16, atol=0)
+    np.testing.assert_allclose(s, z[f"{name}_s"], rtol=2e-15, atol=0)
 
 
 def test_trace_full_cfg3_vs_oracle():
@@ -317,7 +317,7 @@ def test_trace_full_cfg3_vs_oracle():
     _err("trace_cfg3_200k", mismatches=mism)
     assert mism == 0
     hit = i_ref >= 0
-    np.testing.assert_allclose(t[hit], t_ref[hit], rtol=4e-16, atol=0)
+    np.testing.assert_allclose(t[hit], t_ref[hit], rtol=2e-15, atol=0)
     assert np.all(np.isinf(t[~hit]))
 
 
