@@ -164,7 +164,8 @@ DevScene dev_scene(const vc_scene* sc) {
   DevScene S{};
   S.dim = sc->dim;
   S.K = sc->K;
-  S.n_nodes = sc->n_nodes;
+  S.geo = sc->geo.dev();
+  S.emit = sc->emit.dev();
   S.n_es = sc->n_es;
   S.reflective = sc->reflective;
   for (int a = 0; a < 3; ++a) {
@@ -177,15 +178,9 @@ DevScene dev_scene(const vc_scene* sc) {
   S.sigma_a = sc->sigma_a;
   S.sigma_t = sc->sigma_s + sc->sigma_a;
   S.max_emission = sc->max_emission;
-  S.prim = sc->d_prim;
-  S.prim_id = sc->d_prim_id;
   S.normal = sc->d_normal;
   S.emission = sc->d_emission;
   S.albedo = sc->d_albedo;
-  S.nodes = sc->d_nodes;
-  S.n_em = sc->n_em;
-  S.em_prim = sc->d_em_prim;
-  S.em_id = sc->d_em_id;
   S.es_pos = sc->d_es_pos;
   S.es_w = sc->d_es_w;
   S.es_surf = sc->d_es_surf;
@@ -511,16 +506,6 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
       for (int a = 0; a < 3; ++a) normal[3 * k + a] = c[a] / nn;
     }
   }
-  std::vector<int> order(K);
-  for (int k = 0; k < K; ++k) order[k] = k;
-  HostBVH bvh;
-  if (K > 16) {
-    build_bvh(dim, K, sc->verts.data(), 1e-5 * sc->scale, &bvh);
-    std::memcpy(order.data(), bvh.order, sizeof(int) * K);
-  }
-  std::vector<double> prim_leaf((size_t)K * ps);
-  for (int i = 0; i < K; ++i)
-    std::memcpy(&prim_leaf[(size_t)i * ps], &prim[(size_t)order[i] * ps], ps * 8);
   cudaError_t e = cudaSuccess;
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (e != cudaSuccess) return;
@@ -528,29 +513,40 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     e = cudaMalloc(dst, bytes);
     if (e == cudaSuccess && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
   };
-  up((void**)&sc->d_prim, K ? prim_leaf.data() : nullptr, prim_leaf.size() * 8);
-  up((void**)&sc->d_prim_id, K ? order.data() : nullptr, order.size() * 4);
+  // a primitive subset (original ids `ids`) → BVH (when large enough) + leaf-order prims
+  auto make_set = [&](const std::vector<int>& ids, int bvh_min, GpuBvh& g) {
+    const int Ks = (int)ids.size();
+    g.K = Ks;
+    std::vector<int> order(ids);
+    HostBVH bvh;
+    if (Ks > bvh_min) {
+      std::vector<double> vs((size_t)Ks * dim * dim);
+      for (int i = 0; i < Ks; ++i)
+        std::memcpy(&vs[(size_t)i * dim * dim], &sc->verts[(size_t)ids[i] * dim * dim], dim * dim * 8);
+      build_bvh(dim, Ks, vs.data(), 1e-5 * sc->scale, &bvh);
+      for (int i = 0; i < Ks; ++i) order[i] = ids[bvh.order[i]];
+    }
+    std::vector<double> leaf((size_t)Ks * ps);
+    for (int i = 0; i < Ks; ++i) std::memcpy(&leaf[(size_t)i * ps], &prim[(size_t)order[i] * ps], ps * 8);
+    up((void**)&g.prim, Ks ? leaf.data() : nullptr, leaf.size() * 8);
+    up((void**)&g.prim_id, Ks ? order.data() : nullptr, order.size() * 4);
+    if (bvh.n_nodes) {
+      up((void**)&g.nodes, bvh.nodes, sizeof(float4) * 2 * bvh.n_nodes);
+      g.n_nodes = bvh.n_nodes;
+      free_bvh(&bvh);
+    }
+  };
+  std::vector<int> all(K), em;
+  for (int k = 0; k < K; ++k) {
+    all[k] = k;
+    const double* E = &sc->emission[3 * (size_t)k];
+    if (E[0] > 0.0 || E[1] > 0.0 || E[2] > 0.0) em.push_back(k);
+  }
+  make_set(all, 16, sc->geo);
+  make_set(em, 4, sc->emit);
   up((void**)&sc->d_normal, K ? normal.data() : nullptr, normal.size() * 8);
   up((void**)&sc->d_emission, K ? sc->emission.data() : nullptr, sc->emission.size() * 8);
   up((void**)&sc->d_albedo, K ? sc->albedo.data() : nullptr, sc->albedo.size() * 8);
-  // emitter primitives in original order (emitter-first gather queries)
-  std::vector<double> em_prim;
-  std::vector<int> em_id;
-  for (int k = 0; k < K; ++k) {
-    const double* E = &sc->emission[3 * (size_t)k];
-    if (E[0] > 0.0 || E[1] > 0.0 || E[2] > 0.0) {
-      em_prim.insert(em_prim.end(), &prim[(size_t)k * ps], &prim[(size_t)k * ps] + ps);
-      em_id.push_back(k);
-    }
-  }
-  sc->n_em = (int)em_id.size();
-  up((void**)&sc->d_em_prim, em_prim.empty() ? nullptr : em_prim.data(), em_prim.size() * 8);
-  up((void**)&sc->d_em_id, em_id.empty() ? nullptr : em_id.data(), em_id.size() * 4);
-  if (bvh.n_nodes) {
-    up((void**)&sc->d_nodes, bvh.nodes, sizeof(float4) * 2 * bvh.n_nodes);
-    sc->n_nodes = bvh.n_nodes;
-    free_bvh(&bvh);
-  }
   if (e != cudaSuccess) {
     delete sc;
     return cuda_fail(e, "scene upload");

@@ -38,6 +38,20 @@ const unsigned long long* jump_tables(cudaError_t* err);
 
 }  // namespace vc
 
+// Device copy of one primitive set (all surfaces, or the emitters) with its BVH.
+struct GpuBvh {
+  int K = 0, n_nodes = 0;
+  double* prim = nullptr;
+  int* prim_id = nullptr;
+  float4* nodes = nullptr;
+  vc::DevBvh dev() const { return vc::DevBvh{K, n_nodes, nodes, prim, prim_id}; }
+  ~GpuBvh() {
+    cudaFree(prim);
+    cudaFree(prim_id);
+    cudaFree(nodes);
+  }
+};
+
 struct vc_scene {
   int dim = 0, K = 0;
   std::vector<double> verts, emission, albedo;
@@ -45,16 +59,10 @@ struct vc_scene {
   double scale = 0.0, sigma_s = 0.0, sigma_a = 0.0, max_emission = 0.0;
   int reflective = 0;
   int sm_count = 148;
-  double* d_prim = nullptr;
-  int* d_prim_id = nullptr;
+  GpuBvh geo, emit;
   double* d_normal = nullptr;
   double* d_emission = nullptr;
   double* d_albedo = nullptr;
-  float4* d_nodes = nullptr;
-  int n_nodes = 0;
-  int n_em = 0;
-  double* d_em_prim = nullptr;
-  int* d_em_id = nullptr;
   int es_nlight = -1, n_es = 0;
   double* d_es_pos = nullptr;
   double* d_es_w = nullptr;
@@ -62,14 +70,9 @@ struct vc_scene {
   long long budget = 8LL << 30;
   vc::Workspace ws;
   ~vc_scene() {
-    cudaFree(d_prim);
-    cudaFree(d_prim_id);
     cudaFree(d_normal);
     cudaFree(d_emission);
     cudaFree(d_albedo);
-    cudaFree(d_nodes);
-    cudaFree(d_em_prim);
-    cudaFree(d_em_id);
     cudaFree(d_es_pos);
     cudaFree(d_es_w);
     cudaFree(d_es_surf);

@@ -57,7 +57,7 @@ __device__ inline void stratum_direction(int k, const BuildParams& P, Pcg64 g0, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+__global__ void __launch_bounds__(256, 3) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)W.B * n) return;
@@ -199,12 +199,12 @@ __global__ void __launch_bounds__(1024) k_wave_scan(Wave W, int gather_on) {
 // ---------------------------------------------------------------------------
 
 template <int D>
-__global__ void __launch_bounds__(256) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+__global__ void __launch_bounds__(256, 3) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const long long total = W.rec_base[W.B];
   const int n = P.n_angular;
   const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
   const int per = (D == 3 ? 2 : 1) * P.n_inner;
-  const bool emitter_first = !S.reflective && S.n_em <= 64;
+  const bool emitter_first = !S.reflective && 2 * S.emit.K <= S.geo.K;
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total;
        j += (long long)gridDim.x * blockDim.x) {
     // record: last r with base[r] ≤ j
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) k_gather(DevScene S, BuildParams P, Wave 
 // Spherical Delaunay (3D connectivity, src/scene.py:388-399)
 // ---------------------------------------------------------------------------
 
-constexpr int kMaxV = 32;
+constexpr int kMaxV = 24;
 
 struct Line {
   double A, B, C;
@@ -521,12 +521,28 @@ __device__ __forceinline__ void elem_vertices(const Wave& W, const BuildParams& 
   }
 }
 
+// Warp transpose-reduction: every lane holds 32 values v[0..31]; afterwards lane l holds
+// Σ_lanes v[l] in v[0] (31 double shuffles; no per-lane persistent accumulators).
+__device__ __forceinline__ void warp_transpose_sum(double (&v)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      double send = up ? v[k] : v[k + h];
+      double keep = up ? v[k + h] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+}
+
 template <int D>
-__global__ void __launch_bounds__(kAsmBS) k_assemble(DevScene S, BuildParams P, Wave W) {
+__global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams P, Wave W) {
   constexpr int NQ = 1 + D + D * (D + 1) / 2;
   constexpr int NW = kAsmBS / 32;
+  static_assert(3 * NQ <= 32, "contribution vector must fit one warp");
   __shared__ uint2 queue[NW][kQCap];
-  __shared__ double red[NW][NQ * 3];
+  __shared__ double red[NW][32];
   __shared__ long long redc[NW][2];
   const int rec = blockIdx.x;
   const int n = P.n_angular;
@@ -557,15 +573,11 @@ __global__ void __launch_bounds__(kAsmBS) k_assemble(DevScene S, BuildParams P, 
 
   for (int kind = 0; kind < 2; ++kind) {
     const double wt = fbar * (kind == 0 ? 1.0 : step);
-    double acc[3][NQ];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) acc[c][q] = 0.0;
-    int qn = 0;  // warp-uniform queue length
+    double acc = 0.0;  // lane l accumulates contribution component l (c·NQ + t)
+    int qn = 0;        // warp-uniform queue length
 
-    // evaluate one queued item (element e at ring `ring`, representative vertex slot rep)
-    auto evaluate = [&](uint2 it) {
+    // contribution of one queued item (element e at ring `ring`, representative slot rep)
+    auto eval_item = [&](uint2 it, double (&cvec)[32]) {
       int e = (int)it.x;
       int ring = (int)(it.y >> 2);
       int rep = (int)(it.y & 3u);
@@ -610,8 +622,18 @@ __global__ void __launch_bounds__(kAsmBS) k_assemble(DevScene S, BuildParams P, 
       for (int c = 0; c < 3; ++c) {
         double f = wt * rad[c];
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) acc[c][t] += f * q[t];
+        for (int t = 0; t < NQ; ++t) cvec[c * NQ + t] = f * q[t];
       }
+    };
+    // evaluate one item per lane (all lanes take part) and fold the 3·NQ components:
+    // lane l accumulates component l, no per-lane 3·NQ accumulator array
+    auto evaluate = [&](uint2 it, bool valid) {
+      double cvec[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) cvec[t] = 0.0;
+      if (valid) eval_item(it, cvec);
+      warp_transpose_sum(cvec, lane);
+      acc += cvec[0];
     };
 
     // lane cursor over (element, ring)
@@ -683,7 +705,7 @@ __global__ void __launch_bounds__(kAsmBS) k_assemble(DevScene S, BuildParams P, 
       qn += __popc(bal);
       __syncwarp();
       if (qn >= 32) {
-        evaluate(queue[wid][lane]);
+        evaluate(queue[wid][lane], true);
         __syncwarp();
         int rest = qn - 32;
         if (lane < rest) queue[wid][lane] = queue[wid][32 + lane];
@@ -692,19 +714,11 @@ __global__ void __launch_bounds__(kAsmBS) k_assemble(DevScene S, BuildParams P, 
       }
       if (!__any_sync(0xffffffffu, e < E)) break;
     }
-    if (lane < qn) evaluate(queue[wid][lane]);
+    if (qn > 0) evaluate(queue[wid][lane], lane < qn);
     __syncwarp();
 
-    // reduce acc over the CTA: shuffles, then a shared-memory tree across warps
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        double v = acc[c][t];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[wid][c * NQ + t] = v;
-      }
+    // lane l of every warp holds component l: shared-memory tree across warps
+    red[wid][lane] = acc;
     __syncthreads();
     if (threadIdx.x < NQ * 3) {
       double v = 0.0;

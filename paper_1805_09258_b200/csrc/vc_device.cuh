@@ -213,14 +213,15 @@ __device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, cons
 
 // Visit one primitive of a leaf (float64 decision, src/scene.py:242-268).
 template <int D>
-__device__ __forceinline__ double leaf_hit(const DevScene& S, int k, const double* o, const double* d) {
-  return hit_prim<D>(S.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+__device__ __forceinline__ double leaf_hit(const DevBvh& H, int k, const double* o, const double* d, double t_eps) {
+  return hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, t_eps);
 }
 
 // Ordered BVH traversal.  mode 0: nearest hit (t_best/id_best out).  mode 1: any hit
 // that precedes (thr, id_thr) in (t, index) order — returns true on the first one.
 template <int D, int MODE>
-__device__ bool bvh_query(const DevScene& S, const double* o, const double* d, double& t_best, int& id_best) {
+__device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const double* o, const double* d,
+                          double& t_best, int& id_best) {
   float of[3] = {0.f, 0.f, 0.f}, inv[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -228,7 +229,7 @@ __device__ bool bvh_query(const DevScene& S, const double* o, const double* d, d
     inv[a] = 1.0f / (float)d[a];
   }
   // slack: float32 t limit strictly above the float64 one
-  auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + 1e-5f * (float)S.scale : INFINITY; };
+  auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + slack : INFINITY; };
   float tbf = tlim(t_best);
   int stack[64];
   float stn[64];
@@ -236,18 +237,18 @@ __device__ bool bvh_query(const DevScene& S, const double* o, const double* d, d
   int node = 0;
   {
     float tn;
-    if (!box_hit<D>(__ldg(S.nodes), __ldg(S.nodes + 1), of, inv, tbf, tn)) return false;
+    if (!box_hit<D>(__ldg(H.nodes), __ldg(H.nodes + 1), of, inv, tbf, tn)) return false;
   }
   while (true) {
-    const float4 meta = __ldg(S.nodes + 2 * node);
-    const float4 mh = __ldg(S.nodes + 2 * node + 1);
+    const float4 meta = __ldg(H.nodes + 2 * node);
+    const float4 mh = __ldg(H.nodes + 2 * node + 1);
     int cnt = __float_as_int(mh.w);
     int first = __float_as_int(meta.w);
     if (cnt > 0) {
       for (int k = first; k < first + cnt; ++k) {
-        double t = leaf_hit<D>(S, k, o, d);
+        double t = leaf_hit<D>(H, k, o, d, t_eps);
         if (t == INFINITY) continue;
-        int id = S.prim_id[k];
+        int id = H.prim_id[k];
         if (MODE == 0) {
           if (t < t_best || (t == t_best && id < id_best)) {
             t_best = t;
@@ -259,8 +260,8 @@ __device__ bool bvh_query(const DevScene& S, const double* o, const double* d, d
         }
       }
     } else {
-      const float4 l0 = __ldg(S.nodes + 2 * first), l1 = __ldg(S.nodes + 2 * first + 1);
-      const float4 r0 = __ldg(S.nodes + 2 * first + 2), r1 = __ldg(S.nodes + 2 * first + 3);
+      const float4 l0 = __ldg(H.nodes + 2 * first), l1 = __ldg(H.nodes + 2 * first + 1);
+      const float4 r0 = __ldg(H.nodes + 2 * first + 2), r1 = __ldg(H.nodes + 2 * first + 3);
       float tl, tr;
       bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
       bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
@@ -292,56 +293,56 @@ __device__ bool bvh_query(const DevScene& S, const double* o, const double* d, d
   return false;
 }
 
-// Nearest hit (src/scene.py:271-292).  `id_best` is the original surface index.
+// Nearest hit in a primitive set; `id_best` is the original surface index.
 template <int D>
-__device__ void trace_closest(const DevScene& S, const double* o, const double* d, double& t_best,
-                              int& id_best) {
+__device__ void bvh_closest(const DevBvh& H, double t_eps, float slack, const double* o, const double* d,
+                            double& t_best, int& id_best) {
   t_best = INFINITY;
   id_best = -1;
-  if (S.K == 0) return;
-  if (S.n_nodes == 0) {
-    for (int k = 0; k < S.K; ++k) {
-      double t = hit_prim<D>(S.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+  if (H.K == 0) return;
+  if (H.n_nodes == 0) {
+    for (int k = 0; k < H.K; ++k) {
+      double t = hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, t_eps);
       if (t < t_best) {  // primitives in original order: strict < keeps the first minimum
         t_best = t;
-        id_best = S.prim_id[k];
+        id_best = H.prim_id[k];
       }
     }
     return;
   }
-  bvh_query<D, 0>(S, o, d, t_best, id_best);
+  bvh_query<D, 0>(H, t_eps, slack, o, d, t_best, id_best);
+}
+
+// Nearest hit over the scene (src/scene.py:271-292).
+template <int D>
+__device__ __forceinline__ void trace_closest(const DevScene& S, const double* o, const double* d, double& t_best,
+                                              int& id_best) {
+  bvh_closest<D>(S.geo, S.t_eps, 1e-5f * (float)S.scale, o, d, t_best, id_best);
 }
 
 // Is there a valid hit preceding (thr, id_thr) in (t, index) order?  Shadow rays use
 // id_thr = −1 (visible iff nearest t ≥ thr, src/transport.py:213-214).
 template <int D>
 __device__ bool occluded(const DevScene& S, const double* o, const double* d, double thr, int id_thr = -1) {
-  if (S.K == 0) return false;
-  if (S.n_nodes == 0) {
-    for (int k = 0; k < S.K; ++k) {
-      double t = hit_prim<D>(S.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
-      if (t < thr || (t == thr && S.prim_id[k] < id_thr)) return true;
+  const DevBvh& H = S.geo;
+  if (H.K == 0) return false;
+  if (H.n_nodes == 0) {
+    for (int k = 0; k < H.K; ++k) {
+      double t = hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+      if (t < thr || (t == thr && H.prim_id[k] < id_thr)) return true;
     }
     return false;
   }
   double t = thr;
   int id = id_thr;
-  return bvh_query<D, 1>(S, o, d, t, id);
+  return bvh_query<D, 1>(H, S.t_eps, 1e-5f * (float)S.scale, o, d, t, id);
 }
 
-// Nearest emitter hit (emitters in original order; lowest index wins ties).
+// Nearest emitter hit (lowest original index wins ties), through the emitter BVH.
 template <int D>
 __device__ __forceinline__ void nearest_emitter(const DevScene& S, const double* o, const double* d, double& te,
                                                 int& ie) {
-  te = INFINITY;
-  ie = -1;
-  for (int j = 0; j < S.n_em; ++j) {
-    double t = hit_prim<D>(S.em_prim + (size_t)j * prim_stride(D), o, d, S.t_eps);
-    if (t < te) {
-      te = t;
-      ie = S.em_id[j];
-    }
-  }
+  bvh_closest<D>(S.emit, S.t_eps, 1e-5f * (float)S.scale, o, d, te, ie);
 }
 
 // Distance to the bounds box exit (src/scene.py:295-303), NaN semantics of numpy.
@@ -471,60 +472,51 @@ __device__ inline bool ff_triangle(const double* r1v, const double* r2v, const d
   double aA = fabs(A);
   if (!(aA >= 1e-12 * r[0] * r[1] * r[2])) return false;
   F = 2.0 * atan2(aA, B) / (4.0 * kPi);
-  double gA[3], gr[3][3], gB[3];
-  for (int c = 0; c < 3; ++c) {
-    gA[c] = -(c12[c] + c23[c] + c31[c]);
-    for (int i = 0; i < 3; ++i) gr[i][c] = -R[i][c] / r[i];
+  // Closed forms of the reference's term-by-term chain (src/formfactor.py:199-251) with
+  // unit vectors n_i = R_i/r_i, σ₂ = r₀r₁ + r₀r₂ + r₁r₂, ρ = r₀ + r₁ + r₂, m = Σn_i,
+  // d = (d23, d13, d12):  ∇B = −Σ (σ₂ + d_i) n_i
+  //   HB = (Σ c_i/r_i + 2ρ) I − Σ (c_i/r_i + ρ) n_i n_iᵀ + ρ m mᵀ,  c_i = Π_{j≠i} r_j + d_i
+  // (the outer(∇r, ·) terms of j_rrr and j_dot_term sum to ρ·(m mᵀ − Σ n_i n_iᵀ)).
+  const double sg = A >= 0.0 ? 1.0 : -1.0;
+  const double s2 = r[0] * r[1] + r[0] * r[2] + r[1] * r[2];
+  const double rho = r[0] + r[1] + r[2];
+  const double dk[3] = {d23, d13, d12};
+  double n[3][3], cr[3], gU[3], gB[3], m[3];
+  double diag = 2.0 * rho;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double inv = 1.0 / r[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) n[i][c] = R[i][c] * inv;
+    cr[i] = (r[(i + 1) % 3] * r[(i + 2) % 3] + dk[i]) * inv;  // c_i / r_i
+    diag += cr[i];
   }
+#pragma unroll
   for (int c = 0; c < 3; ++c) {
-    gB[c] = (r[1] * r[2]) * gr[0][c] + (r[0] * r[2]) * gr[1][c] + (r[0] * r[1]) * gr[2][c] +
-            d12 * gr[2][c] - r[2] * (R[0][c] + R[1][c]) + d23 * gr[0][c] - r[0] * (R[1][c] + R[2][c]) +
-            d13 * gr[1][c] - r[1] * (R[0][c] + R[2][c]);
+    gU[c] = -sg * (c12[c] + c23[c] + c31[c]);
+    gB[c] = -((s2 + dk[0]) * n[0][c] + (s2 + dk[1]) * n[1][c] + (s2 + dk[2]) * n[2][c]);
+    m[c] = n[0][c] + n[1][c] + n[2][c];
   }
-  // HB (symmetric part only is needed downstream)
-  const double w3[3] = {r[1] * r[2], r[0] * r[2], r[0] * r[1]};
-  double g23[3], g13[3], g12[3], s12[3], s23[3], s13[3];
+  const double den = A * A + B * B;
+  const double k2pi = 1.0 / (2.0 * kPi);
+  double num[3], gD[3];
+#pragma unroll
   for (int c = 0; c < 3; ++c) {
-    g12[c] = r[1] * gr[0][c] + r[0] * gr[1][c];
-    g23[c] = r[2] * gr[1][c] + r[1] * gr[2][c];
-    g13[c] = r[2] * gr[0][c] + r[0] * gr[2][c];
-    s12[c] = R[0][c] + R[1][c];
-    s23[c] = R[1][c] + R[2][c];
-    s13[c] = R[0][c] + R[2][c];
-  }
-  const double dk[3] = {d23, d13, d12};  // coefficient of Jr_k in the j_dot terms (k = 0, 1, 2)
-  const int pij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
-  double HB[6];
-  for (int e = 0; e < 6; ++e) {
-    int a = pij[e][0], b = pij[e][1];
-    double I = (a == b) ? 1.0 : 0.0;
-    double h = 0.0;
-    for (int i = 0; i < 3; ++i) {
-      double Jr = (I - R[i][a] * R[i][b] / (r[i] * r[i])) / r[i];
-      h += (w3[i] + dk[i]) * Jr + 2.0 * r[i] * I;
-    }
-    // outer(gr_i, g_jk) terms, symmetrized
-    h += 0.5 * (gr[0][a] * g23[b] + gr[0][b] * g23[a]) + 0.5 * (gr[1][a] * g13[b] + gr[1][b] * g13[a]) +
-         0.5 * (gr[2][a] * g12[b] + gr[2][b] * g12[a]);
-    // −outer(gr_k, p+q) − outer(p+q, gr_k) for (k=2, s12), (k=0, s23), (k=1, s13)
-    h -= gr[2][a] * s12[b] + s12[a] * gr[2][b];
-    h -= gr[0][a] * s23[b] + s23[a] * gr[0][b];
-    h -= gr[1][a] * s13[b] + s13[a] * gr[1][b];
-    HB[e] = h;
-  }
-  double sg = A >= 0.0 ? 1.0 : -1.0;
-  double gU[3], num[3], gD[3];
-  double den = A * A + B * B;
-  for (int c = 0; c < 3; ++c) {
-    gU[c] = sg * gA[c];
     num[c] = B * gU[c] - aA * gB[c];
     gD[c] = 2.0 * aA * gU[c] + 2.0 * B * gB[c];
-    g[c] = num[c] / den / (2.0 * kPi);
+    g[c] = num[c] / den * k2pi;
   }
-  for (int e = 0; e < 6; ++e) {
-    int a = pij[e][0], b = pij[e][1];
-    double h = (-aA * HB[e]) / den - 0.5 * (num[a] * gD[b] + num[b] * gD[a]) / (den * den);
-    H[e] = h / (2.0 * kPi);
+  const double ia = -aA / den, id2 = -0.5 / (den * den);
+  int e = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      double hb = (a == b ? diag : 0.0) + rho * m[a] * m[b];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) hb -= (cr[i] + rho) * n[i][a] * n[i][b];
+      H[e++] = (ia * hb + id2 * (num[a] * gD[b] + num[b] * gD[a])) * k2pi;
+    }
   }
   return true;
 }

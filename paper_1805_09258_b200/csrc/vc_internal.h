@@ -17,26 +17,30 @@ namespace vc {
 
 constexpr int kMaxDim = 3;
 
+// A BVH over a primitive set: float32 nodes, float64 primitives in leaf order.
+struct DevBvh {
+  int K;                 // primitives
+  int n_nodes;           // nodes (0 → brute force over K in original order)
+  const float4* nodes;   // 2 float4 per node: (lo.xyz, child/first), (hi.xyz, count)
+  const double* prim;    // leaf order, prim_stride(dim) doubles each
+  const int* prim_id;    // leaf order → original surface index
+};
+
 // Scene as seen by kernels (passed by value).
 struct DevScene {
   int dim;
   int K;                 // primitives
-  int n_nodes;           // BVH nodes (0 → brute force over K)
   int n_es;              // emitter quadrature samples (all emitters)
   int reflective;        // any albedo > 0
   double bmin[3], bmax[3];
   double scale, t_eps;   // bounds diagonal; 1e-6·scale self-hit guard (src/scene.py:22)
   double sigma_s, sigma_a, sigma_t;
   double max_emission;
-  const double* prim;    // leaf order, stride kPrimStride(dim)
-  const int* prim_id;    // leaf order → original surface index
+  DevBvh geo;            // every surface
+  DevBvh emit;           // emitting surfaces only (emitter-first gather when !reflective)
   const double* normal;  // original order, dim doubles each
   const double* emission;// original order, 3 doubles
   const double* albedo;  // original order, 3 doubles
-  const float4* nodes;   // 2 float4 per node: (lo.xyz, child/first), (hi.xyz, count)
-  int n_em;              // emitter primitives (emitter-first gather when !reflective)
-  const double* em_prim; // n_em primitives in original order (prim_stride doubles each)
-  const int* em_id;      // n_em original surface indices
   const double* es_pos;  // n_es × dim
   const double* es_w;    // n_es
   const int* es_surf;    // n_es → original surface index of the emitter

@@ -247,6 +247,9 @@ def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None
     if not anisotropic:
         flags |= _lib.VC_ISOTROPIC
     N = int(X.shape[0])
+    if N == 0:
+        return BatchResult(d, np.zeros((0, 2, moment_size(d))), np.zeros((0, 8), np.int64),
+                           np.zeros((0, 2, record_size(d))) if epsilon else None)
     if on_dev:
         import torch
 
