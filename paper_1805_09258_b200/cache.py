@@ -92,8 +92,26 @@ class RadianceCache:
         return J, cnt
 
 
-def interpolate(cache: RadianceCache, x):
+_MIRRORS: dict = {}
+
+
+def _as_device_cache(cache) -> RadianceCache:
+    """Accept a reference RadianceCache too: mirror its records on the device (re-mirrored
+    when its record count changes, i.e. after inserts)."""
+    if isinstance(cache, RadianceCache):
+        return cache
+    key = id(cache)
+    hit = _MIRRORS.get(key)
+    if hit is not None and hit[0] is cache and hit[1] == len(cache):
+        return hit[2]
+    dc = cache_from_records(cache.bounds_min, cache.bounds_max, cache.records)
+    _MIRRORS[key] = (cache, len(cache), dc)
+    return dc
+
+
+def interpolate(cache, x):
     """Cubic-weighted first-order blend of covering records, or None (src/cache.py:342-360)."""
+    cache = _as_device_cache(cache)
     J, cnt = cache.interpolate_many(np.asarray(x, float)[None])
     if cnt[0] == 0 or np.isnan(J[0, 0]):
         return None

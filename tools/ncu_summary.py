@@ -1,0 +1,71 @@
+"""Summarise an ncu --set full report into profiles/ (markdown + traffic JSON).
+
+usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r1_ncu_full.md [profiles/ncu_traffic.json]
+"""
+import csv, io, json, subprocess, sys
+from collections import defaultdict
+
+METRICS = [
+    "gpu__time_duration.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed.avg.per_cycle_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "lts__t_bytes.sum", "l1tex__t_bytes.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "local_load_bytes", "smsp__sass_inst_executed_op_local_ld.sum",
+]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    return hdr, units, rows[2:]
+
+
+def to_bytes(v, unit):
+    f = float(v.replace(",", ""))
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+
+
+def main():
+    rep, md = sys.argv[1], sys.argv[2]
+    traffic_out = sys.argv[3] if len(sys.argv) > 3 else None
+    hdr, units, rows = raw(rep)
+    col = {h: i for i, h in enumerate(hdr)}
+    lines = [f"# ncu --set full summary: `{rep}`", "", "| kernel | metric | value | unit |", "|---|---|---|---|"]
+    traffic = {}
+    stalls = {}
+    for row in rows:
+        name = row[col["Kernel Name"]]
+        short = name.split("(")[0].replace("void ", "")
+        for m in METRICS:
+            if m in col and row[col[m]] not in ("", "n/a"):
+                lines.append(f"| {short} | {m} | {row[col[m]]} | {units[col[m]]} |")
+        rb = to_bytes(row[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
+        wb = to_bytes(row[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
+        key = short.replace("vc::", "").replace("k_", "").split("<")[0]
+        traffic[key] = rb + wb
+        st = []
+        for h, i in col.items():
+            if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
+                try:
+                    st.append((float(row[i].replace(",", "")), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in st) or 1.0
+        stalls[short] = [(n, round(v / tot, 3)) for v, n in sorted(st, reverse=True)[:6]]
+    lines += ["", "## Warp stall reasons (pc sampling share)", ""]
+    for k, v in stalls.items():
+        lines.append(f"- {k}: " + ", ".join(f"{n} {s:.1%}" for n, s in v))
+    lines += ["", "## DRAM traffic per launch (read + write bytes)", ""]
+    for k, v in traffic.items():
+        lines.append(f"- {k}: {v:.4g} B")
+    open(md, "w").write("\n".join(lines) + "\n")
+    if traffic_out:
+        json.dump(traffic, open(traffic_out, "w"), indent=1)
+    print(open(md).read())
+
+
+if __name__ == "__main__":
+    main()
