@@ -43,23 +43,26 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile the library; `out`/`defines` build an experiment variant (e.g. -DVC_LB_TRACE=2)."""
+    lib = Path(out) if out else LIB
+    if not force and out is None and up_to_date():
         return LIB
-    OBJ.mkdir(exist_ok=True)
-    LIBDIR.mkdir(exist_ok=True)
+    obj = OBJ if out is None else OBJ / lib.stem
+    obj.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     cuda_inc = str(Path(nvcc).resolve().parent.parent / "include")
     jobs = []
     for s in CU_SOURCES:
-        jobs.append([nvcc, *NVCC_FLAGS, "-c", str(CSRC / s), "-o", str(OBJ / (s + ".o"))])
+        jobs.append([nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(CSRC / s), "-o", str(obj / (s + ".o"))])
     for s in CPP_SOURCES:
         jobs.append(["g++", "-O3", "-std=c++17", "-fPIC", "-I", cuda_inc, "-c", str(CSRC / s),
-                     "-o", str(OBJ / (s + ".o"))])
+                     "-o", str(obj / (s + ".o"))])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log = OBJ / (Path(cmd[-1]).name + ".log")
+        log = obj / (Path(cmd[-1]).name + ".log")
         log.write_text(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}{r.stderr}")
@@ -67,16 +70,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
-    objs = [str(OBJ / (s + ".o")) for s in CU_SOURCES + CPP_SOURCES]
-    tmp = LIB.with_suffix(".so.tmp")
+    objs = [str(obj / (s + ".o")) for s in CU_SOURCES + CPP_SOURCES]
+    tmp = lib.with_suffix(".so.tmp")
     link = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":

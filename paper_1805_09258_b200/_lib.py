@@ -8,9 +8,10 @@ VC_EINVAL / VC_EOUTSIDE → ValueError (src/subdivision.py:155-158), others → 
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvolcache_b200.so"
+LIB_PATH = Path(os.environ.get("VOLCACHE_B200_LIB", Path(__file__).resolve().parent / "lib" / "libvolcache_b200.so"))
 
 VC_OK = 0
 VC_EINVAL = -1

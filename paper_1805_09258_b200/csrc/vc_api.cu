@@ -321,6 +321,11 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   int* own = (int*)alloc(19, (D == 3 && !P.host_adjacency) ? B * n * 32 * 8 : 16);
   int* own_cnt = (int*)alloc(20, B * n * 4);
   uint32_t* dwords = (uint32_t*)alloc(21, words ? B * prm->seed_words * 4 + 4 : 16);
+  // two-pass gather queue (emitter hits; overflow falls back to in-place resolution)
+  W.gather_q_cap = std::min<long long>(W.media_cap, 1LL << 24);
+  if (const char* e = getenv("VOLCACHE_GATHER_QCAP")) W.gather_q_cap = std::min<long long>(W.gather_q_cap, atoll(e));
+  W.gather_q = alloc(32, (size_t)W.gather_q_cap * 72);
+  W.gather_q_count = (unsigned long long*)alloc(33, 8);
   if (err != cudaSuccess) return cuda_fail(err, "workspace allocation");
 
   KernelCounter kc;

@@ -57,7 +57,14 @@ __device__ inline void stratum_direction(int k, const BuildParams& P, Pcg64 g0, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 3) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+#ifndef VC_LB_TRACE
+#define VC_LB_TRACE 3  // min resident 256-thread CTAs per SM for the ray kernels
+#endif
+#ifndef VC_LB_DEL
+#define VC_LB_DEL 4  // min resident 128-thread CTAs per SM for the triangulation
+#endif
+
+__global__ void __launch_bounds__(256, VC_LB_TRACE) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)W.B * n) return;
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(1024) k_wave_scan(Wave W, int gather_on) {
 // ---------------------------------------------------------------------------
 
 template <int D>
-__global__ void __launch_bounds__(256, 3) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+__global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const long long total = W.rec_base[W.B];
   const int n = P.n_angular;
   const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
@@ -281,6 +288,136 @@ __global__ void __launch_bounds__(256, 3) k_gather(DevScene S, BuildParams P, Wa
   }
 }
 
+// Two-pass gather for non-reflective scenes with one gather direction per sample.
+// Pass 1 (k_gather_emit): CTA rows = records, each thread walks a run of consecutive
+// samples (direction found once by binary search, then advanced; PCG64 jumped once and
+// stepped), tests the gather ray against the emitter BVH only, writes zero radiance
+// for misses and queues emitter hits.  Pass 2 (k_gather_occl): one thread per queued
+// ray runs the any-hit occlusion query on the full BVH in (t, index) order — full warps
+// for the divergent traversal, and the same (s, idx) decision as a nearest-hit search.
+struct GatherItem {
+  double y[3], d[3], te;
+  long long slot;  // media row
+  int ie, pad;
+};
+
+static_assert(sizeof(GatherItem) == 72, "queue entry layout (workspace sizing)");
+
+constexpr int kGatherRun = 4;  // consecutive samples per thread in pass 1
+
+__device__ __forceinline__ void store_media(float* out, const double* v) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float f = (float)v[c];
+    if (v[c] > 0.0 && !(f > 0.0f)) f = FLT_TRUE_MIN;  // keep the liveness bit exact
+    out[c] = f;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
+                                                               GatherItem* q, unsigned long long* q_count,
+                                                               long long q_cap) {
+  const int rec = blockIdx.y;
+  const long long base = W.rec_base[rec];
+  const int Pr = (int)(W.rec_base[rec + 1] - base);
+  const int n = P.n_angular;
+  const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
+  const int* pre = W.pre + (size_t)rec * n;
+  const int* cnt = W.cnt + (size_t)rec * n;
+  double x[3];
+#pragma unroll
+  for (int c = 0; c < D; ++c) x[c] = W.x[rec * D + c];
+  const uint64_t* st = W.rng + 4 * rec;
+  for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * kGatherRun; j0 < Pr;
+       j0 += gridDim.x * blockDim.x * kGatherRun) {
+    // direction of the first sample: last k with pre[k] ≤ j0
+    int a = 0, b = n - 1;
+    while (a < b) {
+      int mid = (a + b + 1) >> 1;
+      if (pre[mid] <= j0) a = mid; else b = mid - 1;
+    }
+    int k = a, i = j0 - pre[k];
+    Pcg64 g = pcg_load(st);
+    pcg_advance(g, (unsigned long long)(draws0 + (long long)(D == 3 ? 2 : 1) * j0), jt);
+    const int jend = min(j0 + kGatherRun, Pr);
+    for (int j = j0; j < jend; ++j) {
+      while (i >= cnt[k]) {  // next direction with live rings
+        ++k;
+        i = 0;
+      }
+      const double ri = ring_radius(i, P.march_step);
+      double y[3], gd[3];
+#pragma unroll
+      for (int c = 0; c < D; ++c) y[c] = add(x[c], mul(ri, W.dirs[((size_t)rec * n + k) * D + c]));
+      if constexpr (D == 2) {
+        double th = mul(2.0 * kPi, g.next_double());
+        gd[0] = cos(th);
+        gd[1] = sin(th);
+      } else {
+        double u0 = g.next_double(), u1 = g.next_double();
+        double z = sub(1.0, mul(2.0, u0));
+        double phi = mul(2.0 * kPi, u1);
+        double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+        gd[0] = mul(sq, cos(phi));
+        gd[1] = mul(sq, sin(phi));
+        gd[2] = z;
+      }
+      double te;
+      int ie;
+      nearest_emitter<D>(S, y, gd, te, ie);
+      float* out = W.media + (size_t)(base + j) * 3;
+      double zero[3] = {0.0, 0.0, 0.0};
+      if (ie < 0) {
+        store_media(out, zero);
+      } else {
+        unsigned long long slot = atomicAdd(q_count, 1ULL);
+        if ((long long)slot < q_cap) {
+          GatherItem& it = q[slot];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            it.y[c] = c < D ? y[c] : 0.0;
+            it.d[c] = c < D ? gd[c] : 0.0;
+          }
+          it.te = te;
+          it.ie = ie;
+          it.slot = base + j;
+        } else {  // queue full: resolve in place (same result, less coherent)
+          double v[3] = {0.0, 0.0, 0.0};
+          if (!occluded<D>(S, y, gd, te, ie)) {
+            const double* E = S.emission + (size_t)ie * 3;
+            double T = exp(-S.sigma_t * te);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
+          }
+          store_media(out, v);
+        }
+      }
+      ++i;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_occl(DevScene S, const GatherItem* q,
+                                                               const unsigned long long* q_count, long long q_cap,
+                                                               float* media) {
+  const long long nq = min((long long)*q_count, q_cap);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nq;
+       t += (long long)gridDim.x * blockDim.x) {
+    const GatherItem it = q[t];
+    double v[3] = {0.0, 0.0, 0.0};
+    if (!occluded<D>(S, it.y, it.d, it.te, it.ie)) {
+      // L_o = emission (non-reflective scene); σs · T · L_o / n_inner with n_inner = 1
+      const double* E = S.emission + (size_t)it.ie * 3;
+      double T = exp(-S.sigma_t * it.te);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
+    }
+    store_media(media + (size_t)it.slot * 3, v);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Spherical Delaunay (3D connectivity, src/scene.py:388-399)
 // ---------------------------------------------------------------------------
@@ -324,10 +461,10 @@ __device__ int voronoi_cell(const double* dirs, int rows, int cols, int i, doubl
   double ne = sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
   e1[0] /= ne; e1[1] /= ne; e1[2] /= ne;
   double e2[3] = {p[1] * e1[2] - p[2] * e1[1], p[2] * e1[0] - p[0] * e1[2], p[0] * e1[1] - p[1] * e1[0]};
-  const double L = tan(fmin(alpha, 1.2));
+  // initial square of half-size tan(α/2): a cell reaching beyond it fails the security
+  // test (2·R_cell ≤ α) anyway, and the tighter start shrinks the candidate cut early
+  const double L = tan(0.5 * fmin(alpha, 1.5)) * 1.001;
   double va[kMaxV], vb[kMaxV];
-  int lb2[kMaxV];
-  double va2[kMaxV], vb2[kMaxV];
   m = 4;
   va[0] = L;  vb[0] = -L; lab[0] = -1;
   va[1] = L;  vb[1] = L;  lab[1] = -2;
@@ -376,45 +513,51 @@ __device__ int voronoi_cell(const double* dirs, int rows, int cols, int i, doubl
       double pq = p[0] * q[0] + p[1] * q[1] + p[2] * q[2];
       if (!(pq > cut)) continue;
       Line ln = cell_line(j, p, e1, e2, dirs, L);
-      double f[kMaxV];
-      bool any_out = false;
-      for (int v = 0; v < m; ++v) {
-        f[v] = ln.A * va[v] + ln.B * vb[v] + ln.C;
-        any_out |= (f[v] < 0.0);
+      unsigned out = 0;
+      for (int v = 0; v < m; ++v) out |= (ln.A * va[v] + ln.B * vb[v] + ln.C < 0.0 ? 1u : 0u) << v;
+      if (!out) continue;
+      const unsigned full = (m == 32) ? 0xffffffffu : ((1u << m) - 1u);
+      if (out == full) return 2;  // cannot happen: p (the origin) is inside every bisector
+      // convex polygon: the outside vertices form one cyclic run [s, e]
+      const unsigned prev = ((out << 1) | (out >> (m - 1))) & full;  // bit v: out[v−1]
+      const unsigned next = ((out >> 1) | (out << (m - 1))) & full;  // bit v: out[v+1]
+      const int s = __ffs(out & ~prev) - 1;
+      const int e = __ffs(out & ~next) - 1;
+      const int sp = (s + m - 1) % m;  // inside vertex before the run
+      const int L_out = __popc(out);
+      const int m_new = m - L_out + 2;
+      if (m_new > kMaxV) return 2;
+      // X = edge(sp) ∩ bisector, Y = bisector ∩ edge(e); cyclic order … sp, X, Y, e+1 …
+      const int lab_e = lab[e];
+      double xa, xb, ya, yb;
+      meet(cell_line(lab[sp], p, e1, e2, dirs, L), ln, xa, xb);
+      meet(ln, cell_line(lab_e, p, e1, e2, dirs, L), ya, yb);
+      if (s <= e) {
+        // run inside the array: [0, s) X Y [e+1, m) — shift the tail by 2 − L_out in place
+        const int shift = 2 - L_out;
+        if (shift < 0) {
+          for (int v = e + 1; v < m; ++v) {
+            va[v + shift] = va[v]; vb[v + shift] = vb[v]; lab[v + shift] = lab[v];
+          }
+        } else if (shift > 0) {
+          for (int v = m - 1; v > e; --v) {
+            va[v + shift] = va[v]; vb[v + shift] = vb[v]; lab[v + shift] = lab[v];
+          }
+        }
+        va[s] = xa; vb[s] = xb; lab[s] = j;
+        va[s + 1] = ya; vb[s + 1] = yb; lab[s + 1] = lab_e;
+      } else {
+        // run wraps: keep [e+1, s) moved to the front, then X Y
+        const int K = s - e - 1;
+        for (int v = 0; v < K; ++v) {
+          va[v] = va[e + 1 + v]; vb[v] = vb[e + 1 + v]; lab[v] = lab[e + 1 + v];
+        }
+        va[K] = xa; vb[K] = xb; lab[K] = j;
+        va[K + 1] = ya; vb[K + 1] = yb; lab[K + 1] = lab_e;
       }
-      if (!any_out) continue;
-      // convex: one cyclic run of outside vertices [s, e]
-      int s = -1;
-      for (int v = 0; v < m; ++v) {
-        int pv = (v + m - 1) % m;
-        if (f[v] < 0.0 && !(f[pv] < 0.0)) { s = v; break; }
-      }
-      if (s < 0) return 2;  // every vertex outside: cannot happen (p is inside)
-      int e = s;
-      while (f[(e + 1) % m] < 0.0) e = (e + 1) % m;
-      int sp = (s + m - 1) % m;  // inside vertex before the run
-      int en = (e + 1) % m;      // inside vertex after the run
-      // new polygon starting at en: en .. sp (inside run), X (edge sp ∩ ln), Y (edge e ∩ ln)
-      int mm = 0;
-      for (int v = en;; v = (v + 1) % m) {
-        if (mm >= kMaxV - 2) return 2;
-        va2[mm] = va[v]; vb2[mm] = vb[v]; lb2[mm] = lab[v]; ++mm;
-        if (v == sp) break;
-      }
-      Line lsp = cell_line(lab[sp], p, e1, e2, dirs, L);
-      Line le = cell_line(lab[e], p, e1, e2, dirs, L);
-      meet(lsp, ln, va2[mm], vb2[mm]);
-      lb2[mm] = j;  // edge X→Y lies on the new bisector
-      ++mm;
-      meet(ln, le, va2[mm], vb2[mm]);
-      lb2[mm] = lab[e];
-      ++mm;
-      m = mm;
+      m = m_new;
       t2R = 0.0;
-      for (int v = 0; v < m; ++v) {
-        va[v] = va2[v]; vb[v] = vb2[v]; lab[v] = lb2[v];
-        t2R = fmax(t2R, va[v] * va[v] + vb[v] * vb[v]);
-      }
+      for (int v = 0; v < m; ++v) t2R = fmax(t2R, va[v] * va[v] + vb[v] * vb[v]);
       cut = cos2R();
     }
   }
@@ -424,7 +567,7 @@ __device__ int voronoi_cell(const double* dirs, int rows, int cols, int i, doubl
   return (t2R <= th2 * th2) ? 0 : 1;
 }
 
-__global__ void __launch_bounds__(128) k_delaunay(BuildParams P, Wave W, int* own /* B×n×kMaxV×2 */,
+__global__ void __launch_bounds__(128, VC_LB_DEL) k_delaunay(BuildParams P, Wave W, int* own /* B×n×kMaxV×2 */,
                                                   int* own_cnt) {
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -894,10 +1037,21 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   prof_end(st);
   int nl = 3;
   if (S.sigma_s > 0.0) {
+    const bool two_pass =
+        !S.reflective && 2 * S.emit.K <= S.geo.K && P.n_inner == 1 && W.gather_q_cap > 0;
     prof_begin(KC_GATHER, st);
-  k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
-  prof_end(st);
-    ++nl;
+    if (two_pass) {
+      cudaMemsetAsync(W.gather_q_count, 0, sizeof(unsigned long long), st);
+      k_gather_emit<D><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+                                                      W.gather_q_cap);
+      k_gather_occl<D><<<sm_count * 8, 256, 0, st>>>(S, (const GatherItem*)W.gather_q, W.gather_q_count,
+                                                     W.gather_q_cap, W.media);
+      nl += 2;
+    } else {
+      k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
+      ++nl;
+    }
+    prof_end(st);
   }
   if constexpr (D == 3) {
     cudaMemsetAsync(W.tri_status, 0, sizeof(int) * W.B, st);

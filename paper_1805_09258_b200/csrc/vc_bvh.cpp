@@ -77,10 +77,10 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out) {
   nodes.push_back(Node{});  // root
   nodes.push_back(Node{});  // pad: child pairs start at even indices → 64-byte aligned
   struct Task {
-    int node, begin, end;
+    int node, begin, end, depth;
   };
   std::vector<Task> stack;
-  stack.push_back({0, 0, K});
+  stack.push_back({0, 0, K, 0});
   while (!stack.empty()) {
     Task t = stack.back();
     stack.pop_back();
@@ -96,7 +96,8 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out) {
     }
     const int cnt = t.end - t.begin;
     nodes[t.node].b = nb;
-    if (cnt <= kLeafMax) {
+    // the device traversal stack holds kBvhMaxDepth entries: cap the depth with a large leaf
+    if (cnt <= kLeafMax || t.depth >= kBvhMaxDepth - 1) {
       nodes[t.node].first = t.begin;
       nodes[t.node].count = cnt;
       continue;
@@ -164,8 +165,8 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out) {
     nodes.push_back(Node{});
     nodes[t.node].first = left;
     nodes[t.node].count = 0;
-    stack.push_back({left + 1, mid, t.end});
-    stack.push_back({left, t.begin, mid});
+    stack.push_back({left + 1, mid, t.end, t.depth + 1});
+    stack.push_back({left, t.begin, mid, t.depth + 1});
   }
   out->n_nodes = (int)nodes.size();
   out->nodes = (float4*)malloc(sizeof(float4) * 2 * nodes.size());

@@ -231,8 +231,8 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
   // slack: float32 t limit strictly above the float64 one
   auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + slack : INFINITY; };
   float tbf = tlim(t_best);
-  int stack[64];
-  float stn[64];
+  int stack[kBvhMaxDepth];  // the builder caps the depth, so pushes never overflow
+  float stn[kBvhMaxDepth];
   int sp = 0;
   int node = 0;
   {
@@ -267,11 +267,9 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
       bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
       if (hl && hr) {
         int nearc = (tl <= tr) ? first : first + 1;
-        if (sp < 64) {
-          stack[sp] = (tl <= tr) ? first + 1 : first;
-          stn[sp] = fmaxf(tl, tr);
-          ++sp;
-        }
+        stack[sp] = (tl <= tr) ? first + 1 : first;
+        stn[sp] = fmaxf(tl, tr);
+        ++sp;
         node = nearc;
         continue;
       }

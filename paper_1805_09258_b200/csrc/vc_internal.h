@@ -16,6 +16,7 @@
 namespace vc {
 
 constexpr int kMaxDim = 3;
+constexpr int kBvhMaxDepth = 32;  // BVH depth cap = device traversal stack size
 
 // A BVH over a primitive set: float32 nodes, float64 primitives in leaf order.
 struct DevBvh {
@@ -85,6 +86,9 @@ struct Wave {
   double* moments;       // B × 2 × M (M = 3 + 3d + 3d²)
   long long* stats;      // B × kStats
   double* records;       // B × 2 × RecordSize(d) (optional)
+  void* gather_q;        // two-pass gather: queued emitter-hit rays (GatherItem)
+  unsigned long long* gather_q_count;
+  long long gather_q_cap;
 };
 
 constexpr int kStats = 8;  // evaluated, dropped, stars, P, R, tri_status, eval_single, eval_multiple

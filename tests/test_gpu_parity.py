@@ -321,6 +321,27 @@ def test_trace_full_cfg3_vs_oracle():
     assert np.all(np.isinf(t[~hit]))
 
 
+def test_gather_queue_overflow_same_result():
+    """Two-pass gather with a tiny queue (overflow → in-place resolution) is bit-identical."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1805_09258_b200 import configs, estimate_moments_batch, seed_words;"
+        "sc = configs.cfg3_scene(n_spheres=4, level=1); X = np.random.default_rng(5).uniform(sc.bounds_min, sc.bounds_max, (6, 3));"
+        "r = estimate_moments_batch(sc, X, seeds=seed_words(2, 401, range(6)), n_angular=1024, march_step=0.1);"
+        "np.save(sys.argv[1], r.moments)"
+    )
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    env = dict(os.environ)
+    subprocess.run([sys.executable, "-c", code, str(out / "q_full.npy")], check=True, cwd=ROOT, env=env)
+    env["VOLCACHE_GATHER_QCAP"] = "7"
+    subprocess.run([sys.executable, "-c", code, str(out / "q_tiny.npy")], check=True, cwd=ROOT, env=env)
+    np.testing.assert_array_equal(np.load(out / "q_full.npy"), np.load(out / "q_tiny.npy"))
+
+
 def test_errors_and_edge_cases():
     from paper_1805_09258_b200 import configs, estimate_moments, estimate_moments_batch, seed_words
     from paper_1805_09258_b200.scene import Medium, Scene
