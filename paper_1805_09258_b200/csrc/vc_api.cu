@@ -290,6 +290,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   size_t per = (size_t)n * (D * 8 + 8 + 4 * 5 + 24) + media_per * 12 + 64 + 2 * MS * 8 + 2 * RS * 8 +
                kStats * 8 + 32 + 8;
   if (D == 3) per += (size_t)P.n_tris * 12 + (P.host_adjacency ? 0 : (size_t)n * 32 * 8);
+  per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
+  per += (size_t)n * 16;                          // float32 directions
   long long B = (long long)(sc->budget / (long long)per);
   if (B < 1) B = 1;
   if (B > N) B = N;
@@ -321,6 +323,9 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   int* own = (int*)alloc(19, (D == 3 && !P.host_adjacency) ? B * n * 32 * 8 : 16);
   int* own_cnt = (int*)alloc(20, B * n * 4);
   uint32_t* dwords = (uint32_t*)alloc(21, words ? B * prm->seed_words * 4 + 4 : 16);
+  W.dirs32 = (float4*)alloc(35, D == 3 ? B * n * 16 : 16);
+  W.live_words = (P.r_ub + 63) / 64;
+  W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);
   // two-pass gather queue (emitter hits; overflow falls back to in-place resolution)
   W.gather_q_cap = std::min<long long>(W.media_cap, 1LL << 24);
   if (const char* e = getenv("VOLCACHE_GATHER_QCAP")) W.gather_q_cap = std::min<long long>(W.gather_q_cap, atoll(e));

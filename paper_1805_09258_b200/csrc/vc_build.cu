@@ -50,8 +50,10 @@ __device__ inline void stratum_direction(int k, const BuildParams& P, Pcg64 g0, 
     double z = sub(1.0, __ddiv_rn(mul(2.0, add((double)r, u)), (double)P.rows));
     double phi = mul(add((double)c, v), __ddiv_rn(2.0 * kPi, (double)P.cols));
     double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
-    out[0] = mul(sq, cos(phi));
-    out[1] = mul(sq, sin(phi));
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    out[0] = mul(sq, cp);
+    out[1] = mul(sq, sp);
     out[2] = z;
   }
 }
@@ -85,6 +87,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_primary(DevScene S, BuildP
   size_t base = (size_t)rec * n + k;
 #pragma unroll
   for (int a = 0; a < D; ++a) W.dirs[base * D + a] = d[a];
+  if constexpr (D == 3) W.dirs32[base] = make_float4((float)d[0], (float)d[1], (float)d[2], 0.0f);
   W.s[base] = s;
   W.idx[base] = id;
   W.lo[base * 3 + 0] = L[0];
@@ -303,7 +306,7 @@ struct GatherItem {
 
 static_assert(sizeof(GatherItem) == 72, "queue entry layout (workspace sizing)");
 
-constexpr int kGatherRun = 4;  // consecutive samples per thread in pass 1
+constexpr int kGatherRun = 8;  // consecutive samples per thread in pass 1
 
 __device__ __forceinline__ void store_media(float* out, const double* v) {
 #pragma unroll
@@ -359,8 +362,10 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
         double z = sub(1.0, mul(2.0, u0));
         double phi = mul(2.0 * kPi, u1);
         double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
-        gd[0] = mul(sq, cos(phi));
-        gd[1] = mul(sq, sin(phi));
+        double sp, cp;
+        sincos(phi, &sp, &cp);
+        gd[0] = mul(sq, cp);
+        gd[1] = mul(sq, sp);
         gd[2] = z;
       }
       double te;
@@ -368,10 +373,17 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
       nearest_emitter<D>(S, y, gd, te, ie);
       float* out = W.media + (size_t)(base + j) * 3;
       double zero[3] = {0.0, 0.0, 0.0};
+      // warp-aggregated queue append (one atomic per warp and step)
+      const unsigned act = __activemask();
+      const unsigned hits = __ballot_sync(act, ie >= 0);
+      const int leader = __ffs(act) - 1;
+      unsigned long long wbase = 0;
+      if ((threadIdx.x & 31) == leader && hits) wbase = atomicAdd(q_count, (unsigned long long)__popc(hits));
+      wbase = __shfl_sync(act, wbase, leader);
       if (ie < 0) {
         store_media(out, zero);
       } else {
-        unsigned long long slot = atomicAdd(q_count, 1ULL);
+        unsigned long long slot = wbase + __popc(hits & ((1u << (threadIdx.x & 31)) - 1u));
         if ((long long)slot < q_cap) {
           GatherItem& it = q[slot];
 #pragma unroll
@@ -449,6 +461,186 @@ __device__ __forceinline__ void meet(const Line& l1, const Line& l2, double& a, 
   a = (l1.B * l2.C - l2.B * l1.C) / det;
   b = (l2.A * l1.C - l1.A * l2.C) / det;
 }
+
+// Cell polygon held in shared memory, [vertex][thread] layout (bank-conflict free): the
+// per-thread working set of the clipping loop would otherwise live in local memory and,
+// at full occupancy, overflow L1 into L2.
+constexpr int kDelBS = 128;
+constexpr int kPolyV = 20;  // polygon capacity (final Delaunay degree ≤ ~12 on these grids)
+
+struct Poly {
+  double* a;
+  double* b;
+  int* lab;
+  __device__ __forceinline__ double& A(int v) { return a[v * kDelBS]; }
+  __device__ __forceinline__ double& B(int v) { return b[v * kDelBS]; }
+  __device__ __forceinline__ int& L(int v) { return lab[v * kDelBS]; }
+};
+
+// Voronoi cell of point i over candidates within angle alpha (exact if the cell radius
+// stays below alpha/2).  Returns 0 secure, 1 needs a larger alpha, 2 polygon overflow.
+__device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* __restrict__ dirs32, int rows,
+                                 int cols, int i, double alpha, Poly poly, int& m) {
+  const double* p = dirs + 3 * (size_t)i;
+  const double px = p[0], py = p[1], pz = p[2];
+  const float4 p32 = dirs32[i];
+  double h[3] = {0.0, 0.0, 1.0};
+  if (fabs(pz) >= 0.9) { h[0] = 1.0; h[2] = 0.0; }
+  double e1[3] = {h[1] * pz - h[2] * py, h[2] * px - h[0] * pz, h[0] * py - h[1] * px};
+  const double ne = rsqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+  e1[0] *= ne; e1[1] *= ne; e1[2] *= ne;
+  const double e2[3] = {py * e1[2] - pz * e1[1], pz * e1[0] - px * e1[2], px * e1[1] - py * e1[0]};
+  const double pp[3] = {px, py, pz};
+  // initial square of half-size tan(α/2): a cell reaching beyond it fails the security
+  // test (2·R_cell ≤ α) anyway, and the tighter start shrinks the candidate cut early
+  const double L = tan(0.5 * fmin(alpha, 1.5)) * 1.001;
+  m = 4;
+  poly.A(0) = L;  poly.B(0) = -L; poly.L(0) = -1;
+  poly.A(1) = L;  poly.B(1) = L;  poly.L(1) = -2;
+  poly.A(2) = -L; poly.B(2) = L;  poly.L(2) = -3;
+  poly.A(3) = -L; poly.B(3) = -L; poly.L(3) = -4;
+  double t2R = 2.0 * L * L;
+  auto cos2R = [&]() { return t2R >= 1.0 ? -1.0 : (1.0 - t2R) / (1.0 + t2R); };
+  double cut = cos2R();
+  float cutf = (float)cut - 2e-6f;
+  // candidate rows: bands meeting z ∈ [cos(θ+α), cos(θ−α)]; columns: azimuth half-width
+  // asin(sin α / sin θ) ≤ (π/2)·sin α / sin θ (conservative, no transcendental per point)
+  const double sa = sin(alpha), ca = cos(alpha);
+  const double st = sqrt(fmax(0.0, 1.0 - pz * pz));
+  const double z_hi = pz * ca + st * sa;  // cos(θ − α) (pole cap when θ ≤ α)
+  const double z_lo = pz * ca - st * sa;  // cos(θ + α)
+  const bool cap_n = st <= sa && pz > 0.0, cap_s = st <= sa && pz < 0.0;
+  const int r0 = i / cols, c0 = i - r0 * cols;
+  auto row_of = [&](double z) {
+    int r = (int)floor((1.0 - z) * rows * 0.5);
+    return min(max(r, 0), rows - 1);
+  };
+  const int rlo = cap_n ? 0 : min(row_of(z_hi), r0);
+  const int rhi = cap_s ? rows - 1 : max(row_of(z_lo), r0);
+  int half = cols;
+  if (!cap_n && !cap_s) {
+    const double dphi = asin(fmin(sa / st, 1.0));
+    half = (int)ceil(dphi * cols / (2.0 * kPi)) + 1;
+    if (2 * half + 1 >= cols) half = cols;
+  }
+  const int span = max(r0 - rlo, rhi - r0);
+  const int ncol_iter = (half >= cols) ? cols : 2 * half + 1;
+  for (int rr = 0; rr <= 2 * span; ++rr) {
+    // rows outward from r0 (nearest first), skipping rows outside [rlo, rhi]
+    int dr = (rr + 1) >> 1;
+    int row = (rr & 1) ? r0 - dr : r0 + dr;
+    if (row < rlo || row > rhi) continue;
+    for (int cc = 0; cc < ncol_iter; ++cc) {
+      int dc = (cc + 1) >> 1;
+      int col = (cc & 1) ? c0 - dc : c0 + dc;
+      if (col < 0) col += cols;
+      else if (col >= cols) col -= cols;
+      const int j = row * cols + col;
+      if (j == i) continue;
+      // float32 pre-test (one 16-byte load); its margin 2e-6 ≫ the float32 rounding error
+      const float4 q4 = __ldg(dirs32 + j);
+      if (!(p32.x * q4.x + p32.y * q4.y + p32.z * q4.z > cutf)) continue;
+      const double* q = dirs + 3 * (size_t)j;
+      const double qx = q[0], qy = q[1], qz = q[2];
+      if (!(px * qx + py * qy + pz * qz > cut)) continue;
+      const double d0 = px - qx, d1 = py - qy, d2 = pz - qz;
+      const Line ln = {e1[0] * d0 + e1[1] * d1 + e1[2] * d2, e2[0] * d0 + e2[1] * d1 + e2[2] * d2,
+                       px * d0 + py * d1 + pz * d2};
+      unsigned out = 0;
+      for (int v = 0; v < m; ++v) out |= (ln.A * poly.A(v) + ln.B * poly.B(v) + ln.C < 0.0 ? 1u : 0u) << v;
+      if (!out) continue;
+      const unsigned full = (1u << m) - 1u;
+      if (out == full) return 2;  // cannot happen: p (the origin) is inside every bisector
+      // convex polygon: the outside vertices form one cyclic run [s, e]
+      const unsigned prev = ((out << 1) | (out >> (m - 1))) & full;  // bit v: out[v−1]
+      const unsigned next = ((out >> 1) | (out << (m - 1))) & full;  // bit v: out[v+1]
+      const int s = __ffs(out & ~prev) - 1;
+      const int e = __ffs(out & ~next) - 1;
+      const int sp = (s + m - 1) % m;  // inside vertex before the run
+      const int L_out = __popc(out);
+      const int m_new = m - L_out + 2;
+      if (m_new > kPolyV) return 2;
+      // X = edge(sp) ∩ bisector, Y = bisector ∩ edge(e); cyclic order … sp, X, Y, e+1 …
+      const int lab_e = poly.L(e);
+      double xa, xb, ya, yb;
+      meet(cell_line(poly.L(sp), pp, e1, e2, dirs, L), ln, xa, xb);
+      meet(ln, cell_line(lab_e, pp, e1, e2, dirs, L), ya, yb);
+      if (s <= e) {
+        // run inside the array: [0, s) X Y [e+1, m) — shift the tail by 2 − L_out in place
+        const int shift = 2 - L_out;
+        if (shift < 0) {
+          for (int v = e + 1; v < m; ++v) {
+            poly.A(v + shift) = poly.A(v); poly.B(v + shift) = poly.B(v); poly.L(v + shift) = poly.L(v);
+          }
+        } else if (shift > 0) {
+          for (int v = m - 1; v > e; --v) {
+            poly.A(v + shift) = poly.A(v); poly.B(v + shift) = poly.B(v); poly.L(v + shift) = poly.L(v);
+          }
+        }
+        poly.A(s) = xa; poly.B(s) = xb; poly.L(s) = j;
+        poly.A(s + 1) = ya; poly.B(s + 1) = yb; poly.L(s + 1) = lab_e;
+      } else {
+        // run wraps: keep [e+1, s) moved to the front, then X Y
+        const int K = s - e - 1;
+        for (int v = 0; v < K; ++v) {
+          poly.A(v) = poly.A(e + 1 + v); poly.B(v) = poly.B(e + 1 + v); poly.L(v) = poly.L(e + 1 + v);
+        }
+        poly.A(K) = xa; poly.B(K) = xb; poly.L(K) = j;
+        poly.A(K + 1) = ya; poly.B(K + 1) = yb; poly.L(K + 1) = lab_e;
+      }
+      m = m_new;
+      t2R = 0.0;
+      for (int v = 0; v < m; ++v) t2R = fmax(t2R, poly.A(v) * poly.A(v) + poly.B(v) * poly.B(v));
+      cut = cos2R();
+      cutf = (float)cut - 2e-6f;
+    }
+  }
+  for (int v = 0; v < m; ++v)
+    if (poly.L(v) < 0) return 1;
+  const double th2 = tan(0.5 * alpha);
+  return (t2R <= th2 * th2) ? 0 : 1;
+}
+
+__global__ void __launch_bounds__(kDelBS, 4) k_delaunay_smem(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ unsigned char dsm[];
+  double* sa = (double*)dsm;
+  double* sb = sa + kPolyV * kDelBS;
+  int* sl = (int*)(sb + kPolyV * kDelBS);
+  const int n = P.n_angular;
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)W.B * n) return;
+  int rec = (int)(gid / n), i = (int)(gid - (long long)rec * n);
+  const double* dirs = W.dirs + (size_t)rec * n * 3;
+  Poly poly{sa + threadIdx.x, sb + threadIdx.x, sl + threadIdx.x};
+  int m = 0;
+  // search radius α = 2.8 × mean spacing: the security test needs α ≥ 2·R_cell, and on the
+  // jittered stratum grid R_cell ≤ 1.4 spacing for > 99.8% of directions (max ≈ 1.6);
+  // the rest retry with 1.5α
+  double alpha = 2.8 * sqrt(4.0 * kPi / n);
+  int st = 1;
+  for (int attempt = 0; attempt < 10 && st == 1; ++attempt) {
+    st = voronoi_cell_poly(dirs, W.dirs32 + (size_t)rec * n, P.rows, P.cols, i, alpha, poly, m);
+    alpha = fmin(1.5 * alpha, 1.5);
+  }
+  size_t base = ((size_t)rec * n + i);
+  W.deg[base] = (st == 0) ? m : 0;
+  int c = 0;
+  if (st == 0) {
+    for (int t = 0; t < m; ++t) {
+      int a = poly.L(t), b = poly.L(t + 1 == m ? 0 : t + 1);
+      if (i < a && i < b) {
+        own[(base * kMaxV + c) * 2 + 0] = a;
+        own[(base * kMaxV + c) * 2 + 1] = b;
+        ++c;
+      }
+    }
+  } else {
+    atomicMax(W.tri_status + rec, st);
+  }
+  own_cnt[base] = c;
+}
+
+constexpr size_t kDelSmem = (size_t)kPolyV * kDelBS * (8 + 8 + 4);
 
 // Voronoi cell of point i over candidates within angle alpha (exact if the cell radius
 // stays below alpha/2).  Returns 0 secure, 1 needs a larger alpha, 2 polygon overflow.
@@ -629,6 +821,29 @@ __global__ void __launch_bounds__(kCompactBS) k_tri_compact(BuildParams P, Wave 
   if (threadIdx.x == 0 && run != P.n_tris) atomicMax(W.tri_status + rec, 3);
 }
 
+// Per-direction bit masks of live media samples (rad > 0 in any channel): word w of
+// direction k holds samples (k, 64w … 64w+63).  Read by the assembly's candidate scan.
+__global__ void k_live_masks(BuildParams P, Wave W, int media_on) {
+  const int n = P.n_angular;
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)W.B * n) return;
+  const int rec = (int)(gid / n), k = (int)(gid - (long long)rec * n);
+  const int c = W.cnt[gid];
+  const float* m = W.media + (size_t)(W.rec_base[rec] + W.pre[gid]) * 3;
+  unsigned long long* out = W.live + (size_t)rec * W.live_words * n + k;
+  for (int w = 0; w < W.live_words; ++w) {
+    unsigned long long word = 0;
+    if (media_on) {
+      const int hi = min(c - 64 * w, 64);
+      for (int b = 0; b < hi; ++b) {
+        const float* r = m + (size_t)(64 * w + b) * 3;
+        if (r[0] > 0.0f || r[1] > 0.0f || r[2] > 0.0f) word |= 1ULL << b;
+      }
+    }
+    out[(size_t)w * n] = word;
+  }
+}
+
 // Vertex valence of caller-supplied triangles (star counting).
 __global__ void k_degree(BuildParams P, Wave W) {
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -779,12 +994,16 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
       acc += cvec[0];
     };
 
-    // lane cursor over (element, ring)
+    // lane cursor over (element, ring); liveness of media samples comes from the per-direction
+    // bit masks, so the scan itself touches memory once per element (and per 64 rings)
+    const unsigned long long* live = W.live + (size_t)rec * W.live_words * n;
     int e = threadIdx.x;
     int ring = 0;
     int vv[D];
     int cv[D];
     double sd[D];
+    unsigned long long mk[D];
+    int word = -1;
     int maxc_e = 0;
     bool fresh = true;
     while (true) {
@@ -802,6 +1021,7 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
             maxc_e = max(maxc_e, cv[j]);
           }
           fresh = false;
+          word = -1;
         }
         if (kind == 0) {
           int rep = 0;
@@ -830,8 +1050,12 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
               }
             }
             if (lrep && media_on) {
-              const float* m = media + (size_t)(pre[vv[rep]] + ring) * 3;
-              flag = (m[0] > 0.0f) || (m[1] > 0.0f) || (m[2] > 0.0f);
+              if ((ring >> 6) != word) {
+                word = ring >> 6;
+#pragma unroll
+                for (int jj = 0; jj < D; ++jj) mk[jj] = live[(size_t)word * n + vv[jj]];
+              }
+              flag = (mk[rep] >> (ring & 63)) & 1ULL;
             }
             item = make_uint2((unsigned)e, ((unsigned)ring << 2) | (unsigned)rep);
             ++ring;
@@ -1056,9 +1280,14 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   if constexpr (D == 3) {
     cudaMemsetAsync(W.tri_status, 0, sizeof(int) * W.B, st);
     if (!P.host_adjacency) {
+      static bool smem_attr = false;
+      if (!smem_attr) {
+        cudaFuncSetAttribute(k_delaunay_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
+        smem_attr = true;
+      }
       prof_begin(KC_DELAUNAY, st);
-  k_delaunay<<<grid_for(nt, 128), 128, 0, st>>>(P, W, own, own_cnt);
-  prof_end(st);
+      k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
+      prof_end(st);
       prof_begin(KC_COMPACT, st);
   k_tri_compact<<<W.B, kCompactBS, 0, st>>>(P, W, own, own_cnt);
   prof_end(st);
@@ -1072,6 +1301,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
     }
   }
   prof_begin(KC_ASSEMBLE, st);
+  k_live_masks<<<grid_for(nt, 256), 256, 0, st>>>(P, W, S.sigma_s > 0.0 ? 1 : 0);
+  ++nl;
   k_assemble<D><<<W.B, kAsmBS, 0, st>>>(S, P, W);
   prof_end(st);
   ++nl;

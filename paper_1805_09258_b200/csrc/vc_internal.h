@@ -69,6 +69,7 @@ struct Wave {
   const double* x;       // B × dim
   const uint64_t* rng;   // B × 4: state_hi, state_lo, inc_hi, inc_lo (PCG64, numpy layout)
   double* dirs;          // B × n × dim
+  float4* dirs32;        // B × n float32 copy (3D triangulation pre-tests)
   double* s;             // B × n primary hit distance (or bounds exit)
   int* idx;              // B × n primary hit surface (−1: bounds)
   int* cnt;              // B × n live rings per direction (after clamp to R)
@@ -86,6 +87,8 @@ struct Wave {
   double* moments;       // B × 2 × M (M = 3 + 3d + 3d²)
   long long* stats;      // B × kStats
   double* records;       // B × 2 × RecordSize(d) (optional)
+  unsigned long long* live;  // B × live_words × n: bit i of word w = media sample (k, 64w+i) has rad > 0
+  int live_words;            // ⌈r_ub / 64⌉
   void* gather_q;        // two-pass gather: queued emitter-hit rays (GatherItem)
   unsigned long long* gather_q_count;
   long long gather_q_cap;
