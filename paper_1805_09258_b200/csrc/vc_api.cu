@@ -292,6 +292,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   if (D == 3) per += (size_t)P.n_tris * 12 + (P.host_adjacency ? 0 : (size_t)n * 32 * 8);
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
+  per += (size_t)n * 16 + kAsmSplit * 96 * 8;     // DirInfo + assembly partials
   long long B = (long long)(sc->budget / (long long)per);
   if (B < 1) B = 1;
   if (B > N) B = N;
@@ -324,6 +325,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   int* own_cnt = (int*)alloc(20, B * n * 4);
   uint32_t* dwords = (uint32_t*)alloc(21, words ? B * prm->seed_words * 4 + 4 : 16);
   W.dirs32 = (float4*)alloc(35, D == 3 ? B * n * 16 : 16);
+  W.info = (DirInfo*)alloc(36, B * n * sizeof(DirInfo));
+  W.partial = (double*)alloc(37, B * kAsmSplit * 64 * 8 + B * kAsmSplit * 5 * 8);  // sums + 5 counters
   W.live_words = (P.r_ub + 63) / 64;
   W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);
   // two-pass gather queue (emitter hits; overflow falls back to in-place resolution)

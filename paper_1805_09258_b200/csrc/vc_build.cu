@@ -171,8 +171,15 @@ __global__ void __launch_bounds__(kRingBS) k_rings(BuildParams P, Wave W) {
     long long tot;
     long long pre = block_exscan<kRingBS>(c, tot, sm);
     if (k < n) {
-      W.cnt[(size_t)rec * n + k] = c;
-      W.pre[(size_t)rec * n + k] = (int)(run + pre);
+      const size_t g = (size_t)rec * n + k;
+      W.cnt[g] = c;
+      W.pre[g] = (int)(run + pre);
+      const double* lo = W.lo + g * 3;
+      DirInfo di;
+      di.s = s[k];
+      di.cnt = c;
+      di.surf_live = (lo[0] > 0.0 || lo[1] > 0.0 || lo[2] > 0.0) ? 1 : 0;
+      W.info[g] = di;
     }
     run += tot;
   }
@@ -902,17 +909,14 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
   __shared__ uint2 queue[NW][kQCap];
   __shared__ double red[NW][32];
   __shared__ long long redc[NW][2];
-  const int rec = blockIdx.x;
+  const int rec = blockIdx.y, part = blockIdx.x;  // kAsmSplit CTAs share one record
   const int n = P.n_angular;
   const int E = (D == 2) ? n : P.n_tris;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (D == 3 && W.tri_status[rec] != 0) {
-    // triangulation failed for this record: zero moments, report the status
-    double* M = W.moments + (size_t)rec * 2 * moment_size(D);
-    for (int t = threadIdx.x; t < 2 * moment_size(D); t += kAsmBS) M[t] = 0.0;
-    if (threadIdx.x < kStats) W.stats[(size_t)rec * kStats + threadIdx.x] = (threadIdx.x == 5) ? W.tri_status[rec] : 0;
-    return;
-  }
+  double* out_part = W.partial + ((size_t)rec * kAsmSplit + part) * 64;
+  long long* out_cnt = (long long*)(W.partial + (size_t)W.B * kAsmSplit * 64) + ((size_t)rec * kAsmSplit + part) * 5;
+  if (D == 3 && W.tri_status[rec] != 0) return;  // k_asm_final reports the failure
+  const DirInfo* info = W.info + (size_t)rec * n;
   const size_t rb = (size_t)rec * n;
   const double* dirs = W.dirs + rb * D;
   const double* sv = W.s + rb;
@@ -997,11 +1001,13 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
     // lane cursor over (element, ring); liveness of media samples comes from the per-direction
     // bit masks, so the scan itself touches memory once per element (and per 64 rings)
     const unsigned long long* live = W.live + (size_t)rec * W.live_words * n;
-    int e = threadIdx.x;
+    constexpr int kStride = kAsmBS * kAsmSplit;  // elements interleaved across the record's CTAs
+    int e = part * kAsmBS + threadIdx.x;
     int ring = 0;
     int vv[D];
     int cv[D];
     double sd[D];
+    int sl[D];
     unsigned long long mk[D];
     int word = -1;
     int maxc_e = 0;
@@ -1016,8 +1022,10 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
           maxc_e = 0;
 #pragma unroll
           for (int j = 0; j < D; ++j) {
-            cv[j] = cnt[vv[j]];
-            sd[j] = sv[vv[j]];
+            const DirInfo di = info[vv[j]];
+            cv[j] = di.cnt;
+            sd[j] = di.s;
+            sl[j] = di.surf_live;
             maxc_e = max(maxc_e, cv[j]);
           }
           fresh = false;
@@ -1028,10 +1036,9 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
 #pragma unroll
           for (int j = 1; j < D; ++j)
             if (sd[j] > sd[rep]) rep = j;
-          const double* L = lo + (size_t)vv[rep] * 3;
-          flag = (L[0] > 0.0) || (L[1] > 0.0) || (L[2] > 0.0);
+          flag = sl[rep] != 0;
           item = make_uint2((unsigned)e, (unsigned)rep);
-          e += kAsmBS;
+          e += kStride;
           fresh = true;
         } else {
           if (ring < maxc_e) {
@@ -1061,7 +1068,7 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
             ++ring;
           }
           if (ring >= maxc_e) {
-            e += kAsmBS;
+            e += kStride;
             ring = 0;
             fresh = true;
           }
@@ -1087,23 +1094,10 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
     // lane l of every warp holds component l: shared-memory tree across warps
     red[wid][lane] = acc;
     __syncthreads();
-    if (threadIdx.x < NQ * 3) {
+    if (threadIdx.x < 32) {  // this CTA's partial sums, component order c·NQ + t
       double v = 0.0;
       for (int w = 0; w < NW; ++w) v += red[w][threadIdx.x];
-      // scatter into the reference layout: L(3), grad(3,D), hess(3,D,D)
-      int c = threadIdx.x / NQ, t = threadIdx.x - c * NQ;
-      double* M = W.moments + ((size_t)rec * 2 + kind) * moment_size(D);
-      if (t == 0) {
-        M[c] = v;
-      } else if (t <= D) {
-        M[3 + c * D + (t - 1)] = v;
-      } else {
-        int e2 = t - 1 - D, a = 0;
-        while (e2 >= D - a) { e2 -= D - a; ++a; }
-        int b = a + e2;
-        M[3 + 3 * D + c * D * D + a * D + b] = v;
-        M[3 + 3 * D + c * D * D + b * D + a] = v;
-      }
+      out_part[kind * 32 + threadIdx.x] = v;
     }
     __syncthreads();
   }
@@ -1120,7 +1114,7 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
   // star vertices: Σ_k [idx_k ≥ 0] · deg_k · (maxc − cnt_k)  (src/subdivision.py:205-207)
   const int maxc = W.rec_maxc[rec];
   long long stars = 0;
-  for (int k = threadIdx.x; k < n; k += kAsmBS) {
+  for (int k = part * kAsmBS + threadIdx.x; k < n; k += kAsmBS * kAsmSplit) {
     if (idx[k] >= 0) {
       int dg = (D == 2) ? 2 : W.deg[rb + k];
       stars += (long long)dg * (maxc - cnt[k]);
@@ -1136,15 +1130,54 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
       for (int k = 0; k < 4; ++k) t[k] += cred[w][k];
       st += redc[w][0];
     }
+    for (int k = 0; k < 4; ++k) out_cnt[k] = t[k];
+    out_cnt[4] = st;
+  }
+}
+
+// Fixed-order sum of the kAsmSplit partials per record (deterministic), scattered into
+// the reference layout L(3), grad(3, D), hess(3, D, D); stats.
+template <int D>
+__global__ void k_asm_final(BuildParams P, Wave W) {
+  constexpr int NQ = 1 + D + D * (D + 1) / 2;
+  const int rec = blockIdx.x;
+  const int tid = threadIdx.x;  // 64 threads: kind · 32 + component
+  const bool failed = (D == 3) && W.tri_status[rec] != 0;
+  const int kind = tid >> 5, comp = tid & 31;
+  if (comp < 3 * NQ) {
+    double v = 0.0;
+    if (!failed)
+      for (int p = 0; p < kAsmSplit; ++p) v += W.partial[((size_t)rec * kAsmSplit + p) * 64 + kind * 32 + comp];
+    const int c = comp / NQ, t = comp - c * NQ;
+    double* M = W.moments + ((size_t)rec * 2 + kind) * moment_size(D);
+    if (t == 0) {
+      M[c] = v;
+    } else if (t <= D) {
+      M[3 + c * D + (t - 1)] = v;
+    } else {
+      int e2 = t - 1 - D, a = 0;
+      while (e2 >= D - a) { e2 -= D - a; ++a; }
+      const int b = a + e2;
+      M[3 + 3 * D + c * D * D + a * D + b] = v;
+      M[3 + 3 * D + c * D * D + b * D + a] = v;
+    }
+  }
+  if (tid == 0) {
+    const long long* cnt = (const long long*)(W.partial + (size_t)W.B * kAsmSplit * 64);
+    long long t[5] = {0, 0, 0, 0, 0};
+    if (!failed)
+      for (int p = 0; p < kAsmSplit; ++p)
+        for (int k = 0; k < 5; ++k) t[k] += cnt[((size_t)rec * kAsmSplit + p) * 5 + k];
     long long* o = W.stats + (size_t)rec * kStats;
     o[0] = t[0];
     o[1] = t[1];
-    o[2] = st;
+    o[2] = t[4];
     o[3] = W.rec_base[rec + 1] - W.rec_base[rec];
     o[4] = W.rec_R[rec];
     o[5] = (D == 3) ? W.tri_status[rec] : 0;
     o[6] = t[2];
     o[7] = t[3];
+    (void)P;
   }
 }
 
@@ -1303,7 +1336,9 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   prof_begin(KC_ASSEMBLE, st);
   k_live_masks<<<grid_for(nt, 256), 256, 0, st>>>(P, W, S.sigma_s > 0.0 ? 1 : 0);
   ++nl;
-  k_assemble<D><<<W.B, kAsmBS, 0, st>>>(S, P, W);
+  k_assemble<D><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
+  k_asm_final<D><<<W.B, 64, 0, st>>>(P, W);
+  ++nl;
   prof_end(st);
   ++nl;
   if (P.make_records) {

@@ -17,6 +17,7 @@ namespace vc {
 
 constexpr int kMaxDim = 3;
 constexpr int kBvhMaxDepth = 32;  // BVH depth cap = device traversal stack size
+constexpr int kAsmSplit = 4;      // CTAs per record in the moment assembly
 
 // A BVH over a primitive set: float32 nodes, float64 primitives in leaf order.
 struct DevBvh {
@@ -63,8 +64,17 @@ struct BuildParams {
   int make_records;
 };
 
+// Per-direction data read by the assembly scan, one 16-byte load per vertex.
+struct alignas(16) DirInfo {
+  double s;        // primary hit distance (or bounds exit)
+  int cnt;         // live rings
+  int surf_live;   // surface radiance > 0 in any channel
+};
+
 // Per-record scratch for one wave (device pointers).
 struct Wave {
+  DirInfo* info;         // B × n
+  double* partial;       // B × kAsmSplit × 2 × 32 assembly partial sums
   int B;                 // records in this wave
   const double* x;       // B × dim
   const uint64_t* rng;   // B × 4: state_hi, state_lo, inc_hi, inc_lo (PCG64, numpy layout)
