@@ -290,9 +290,16 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   size_t per = (size_t)n * (D * 8 + 8 + 4 * 5 + 24) + media_per * 12 + 64 + 2 * MS * 8 + 2 * RS * 8 +
                kStats * 8 + 32 + 8;
   if (D == 3) per += (size_t)P.n_tris * 12 + (P.host_adjacency ? 0 : (size_t)n * 32 * 8);
+  per += media_per / 10 * 72;                     // two-pass gather queue
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
   per += (size_t)n * 16 + kAsmSplit * 96 * 8;     // DirInfo + assembly partials
+  if (sc->budget <= 0) {  // default scratch budget: 1/4 of HBM (B200: 45 GB), ≤ 48 GiB
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    sc->budget = std::min<long long>((long long)(tot / 4), 48LL << 30);
+    if (sc->budget < (1LL << 30)) sc->budget = 1LL << 30;
+  }
   long long B = (long long)(sc->budget / (long long)per);
   if (B < 1) B = 1;
   if (B > N) B = N;
@@ -330,7 +337,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.live_words = (P.r_ub + 63) / 64;
   W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);
   // two-pass gather queue (emitter hits; overflow falls back to in-place resolution)
-  W.gather_q_cap = std::min<long long>(W.media_cap, 1LL << 24);
+  // ~5% of cfg3 gather rays hit a window: room for ≥ 10% of the wave's media capacity
+  W.gather_q_cap = std::min<long long>(W.media_cap, std::max<long long>(1LL << 24, W.media_cap / 10));
   if (const char* e = getenv("VOLCACHE_GATHER_QCAP")) W.gather_q_cap = std::min<long long>(W.gather_q_cap, atoll(e));
   W.gather_q = alloc(32, (size_t)W.gather_q_cap * 72);
   W.gather_q_count = (unsigned long long*)alloc(33, 8);

@@ -180,7 +180,7 @@ def test_cfg2_full_size_properties():
     ds.set_budget(64 << 20)  # force several waves
     c = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=w.n_angular,
                                march_step=0.1)
-    ds.set_budget(8 << 30)
+    ds.set_budget(16 << 30)
     np.testing.assert_array_equal(a.moments, c.moments)
     assert np.all(a.stats[:, 5] == 0)
     ins = inspect_record(w.scene, w.points[7], rng_seed=np.random.SeedSequence([w.seed, 401, 7]),
