@@ -333,6 +333,10 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   uint32_t* dwords = (uint32_t*)alloc(21, words ? B * prm->seed_words * 4 + 4 : 16);
   W.dirs32 = (float4*)alloc(35, D == 3 ? B * n * 16 : 16);
   W.info = (DirInfo*)alloc(36, B * n * sizeof(DirInfo));
+  W.del_retry_cap = (int)std::min<long long>(B * n, 1LL << 16);
+  W.del_retry = (int*)alloc(38, (size_t)W.del_retry_cap * 4);
+  W.del_retry_count = (unsigned int*)alloc(39, 8);
+  W.del_scratch = (double*)alloc(40, D == 3 ? (size_t)W.del_retry_cap * 48 * 3 * 8 : 16);
   W.partial = (double*)alloc(37, B * kAsmSplit * 64 * 8 + B * kAsmSplit * 5 * 8);  // sums + 5 counters
   W.live_words = (P.r_ub + 63) / 64;
   W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);

@@ -12,7 +12,7 @@
 namespace vc {
 
 struct Workspace {
-  static constexpr int kSlots = 40;
+  static constexpr int kSlots = 48;
   void* ptr[kSlots] = {nullptr};
   size_t cap[kSlots] = {0};
   void* get(int slot, size_t bytes, cudaError_t* err);

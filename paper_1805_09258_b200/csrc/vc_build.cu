@@ -62,9 +62,6 @@ template <int D>
 #ifndef VC_LB_TRACE
 #define VC_LB_TRACE 3  // min resident 256-thread CTAs per SM for the ray kernels
 #endif
-#ifndef VC_LB_DEL
-#define VC_LB_DEL 4  // min resident 128-thread CTAs per SM for the triangulation
-#endif
 
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const int n = P.n_angular;
@@ -473,19 +470,31 @@ __device__ __forceinline__ void meet(const Line& l1, const Line& l2, double& a, 
 // per-thread working set of the clipping loop would otherwise live in local memory and,
 // at full occupancy, overflow L1 into L2.
 constexpr int kDelBS = 128;
-constexpr int kPolyV = 20;  // polygon capacity (final Delaunay degree ≤ ~12 on these grids)
+// Polygon capacity in shared memory.  On the stratum grids the largest polygon met while
+// clipping has 11 vertices (n = 16384, measured); a cell that outgrows the capacity is
+// recomputed by k_delaunay_retry with a 48-vertex polygon in global memory.
+#ifndef VC_POLYV
+#define VC_POLYV 14
+#endif
+constexpr int kPolyV = VC_POLYV;
+constexpr int kRetryV = 48;
 
-struct Poly {
+template <int STRIDE, int CAP>
+struct PolyT {
+  static constexpr int kCap = CAP;
   double* a;
   double* b;
   int* lab;
-  __device__ __forceinline__ double& A(int v) { return a[v * kDelBS]; }
-  __device__ __forceinline__ double& B(int v) { return b[v * kDelBS]; }
-  __device__ __forceinline__ int& L(int v) { return lab[v * kDelBS]; }
+  __device__ __forceinline__ double& A(int v) { return a[v * STRIDE]; }
+  __device__ __forceinline__ double& B(int v) { return b[v * STRIDE]; }
+  __device__ __forceinline__ int& L(int v) { return lab[v * STRIDE]; }
 };
+using Poly = PolyT<kDelBS, kPolyV>;
+using PolyRetry = PolyT<1, kRetryV>;
 
 // Voronoi cell of point i over candidates within angle alpha (exact if the cell radius
 // stays below alpha/2).  Returns 0 secure, 1 needs a larger alpha, 2 polygon overflow.
+template <class Poly>
 __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* __restrict__ dirs32, int rows,
                                  int cols, int i, double alpha, Poly poly, int& m) {
   const double* p = dirs + 3 * (size_t)i;
@@ -566,7 +575,7 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
       const int sp = (s + m - 1) % m;  // inside vertex before the run
       const int L_out = __popc(out);
       const int m_new = m - L_out + 2;
-      if (m_new > kPolyV) return 2;
+      if (m_new > Poly::kCap) return 2;
       // X = edge(sp) ∩ bisector, Y = bisector ∩ edge(e); cyclic order … sp, X, Y, e+1 …
       const int lab_e = poly.L(e);
       double xa, xb, ya, yb;
@@ -608,17 +617,14 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
   return (t2R <= th2 * th2) ? 0 : 1;
 }
 
-__global__ void __launch_bounds__(kDelBS, 4) k_delaunay_smem(BuildParams P, Wave W, int* own, int* own_cnt) {
-  extern __shared__ unsigned char dsm[];
-  double* sa = (double*)dsm;
-  double* sb = sa + kPolyV * kDelBS;
-  int* sl = (int*)(sb + kPolyV * kDelBS);
+// One direction's cell → valence and owned canonical triangles (i < both neighbours).
+// Returns 0 ok, 2 polygon overflow (nothing written); 1 (not closed after every retry)
+// marks the record as failed.
+template <class PolyType>
+__device__ int delaunay_point(const BuildParams& P, const Wave& W, int rec, int i, PolyType poly, int* own,
+                              int* own_cnt) {
   const int n = P.n_angular;
-  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)W.B * n) return;
-  int rec = (int)(gid / n), i = (int)(gid - (long long)rec * n);
   const double* dirs = W.dirs + (size_t)rec * n * 3;
-  Poly poly{sa + threadIdx.x, sb + threadIdx.x, sl + threadIdx.x};
   int m = 0;
   // search radius α = 2.8 × mean spacing: the security test needs α ≥ 2·R_cell, and on the
   // jittered stratum grid R_cell ≤ 1.4 spacing for > 99.8% of directions (max ≈ 1.6);
@@ -629,13 +635,18 @@ __global__ void __launch_bounds__(kDelBS, 4) k_delaunay_smem(BuildParams P, Wave
     st = voronoi_cell_poly(dirs, W.dirs32 + (size_t)rec * n, P.rows, P.cols, i, alpha, poly, m);
     alpha = fmin(1.5 * alpha, 1.5);
   }
-  size_t base = ((size_t)rec * n + i);
+  if (st == 2) return 2;
+  const size_t base = ((size_t)rec * n + i);
   W.deg[base] = (st == 0) ? m : 0;
   int c = 0;
   if (st == 0) {
     for (int t = 0; t < m; ++t) {
       int a = poly.L(t), b = poly.L(t + 1 == m ? 0 : t + 1);
       if (i < a && i < b) {
+        if (c == kMaxV) {
+          atomicMax(W.tri_status + rec, 2);
+          break;
+        }
         own[(base * kMaxV + c) * 2 + 0] = a;
         own[(base * kMaxV + c) * 2 + 1] = b;
         ++c;
@@ -645,159 +656,46 @@ __global__ void __launch_bounds__(kDelBS, 4) k_delaunay_smem(BuildParams P, Wave
     atomicMax(W.tri_status + rec, st);
   }
   own_cnt[base] = c;
+  return 0;
 }
 
-constexpr size_t kDelSmem = (size_t)kPolyV * kDelBS * (8 + 8 + 4);
+#ifndef VC_LB_DEL2
+#define VC_LB_DEL2 5
+#endif
 
-// Voronoi cell of point i over candidates within angle alpha (exact if the cell radius
-// stays below alpha/2).  Returns 0 secure, 1 needs a larger alpha, 2 polygon overflow.
-__device__ int voronoi_cell(const double* dirs, int rows, int cols, int i, double alpha, int* lab,
-                            int& m) {
-  const double* p = dirs + 3 * (size_t)i;
-  double h[3] = {0.0, 0.0, 1.0};
-  if (fabs(p[2]) >= 0.9) { h[0] = 1.0; h[2] = 0.0; }
-  double e1[3] = {h[1] * p[2] - h[2] * p[1], h[2] * p[0] - h[0] * p[2], h[0] * p[1] - h[1] * p[0]};
-  double ne = sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
-  e1[0] /= ne; e1[1] /= ne; e1[2] /= ne;
-  double e2[3] = {p[1] * e1[2] - p[2] * e1[1], p[2] * e1[0] - p[0] * e1[2], p[0] * e1[1] - p[1] * e1[0]};
-  // initial square of half-size tan(α/2): a cell reaching beyond it fails the security
-  // test (2·R_cell ≤ α) anyway, and the tighter start shrinks the candidate cut early
-  const double L = tan(0.5 * fmin(alpha, 1.5)) * 1.001;
-  double va[kMaxV], vb[kMaxV];
-  m = 4;
-  va[0] = L;  vb[0] = -L; lab[0] = -1;
-  va[1] = L;  vb[1] = L;  lab[1] = -2;
-  va[2] = -L; vb[2] = L;  lab[2] = -3;
-  va[3] = -L; vb[3] = -L; lab[3] = -4;
-  double t2R = 2.0 * L * L;
-  auto cos2R = [&]() { return t2R >= 1.0 ? -1.0 : (1.0 - t2R) / (1.0 + t2R); };
-  double cut = cos2R();
-  // candidate rows / columns from the stratum grid
-  const double zp = p[2];
-  const double th = acos(fmin(fmax(zp, -1.0), 1.0));
-  const int r0 = i / cols, c0 = i - r0 * cols;
-  auto row_of = [&](double t) {
-    double z = cos(t);
-    int r = (int)floor((1.0 - z) * rows * 0.5);
-    return min(max(r, 0), rows - 1);
-  };
-  int rlo = (th - alpha <= 0.0) ? 0 : row_of(th - alpha);
-  int rhi = (th + alpha >= kPi) ? rows - 1 : row_of(th + alpha);
-  rlo = min(rlo, r0);
-  rhi = max(rhi, r0);
-  int half;
-  if (th <= alpha || th >= kPi - alpha) {
-    half = cols;
-  } else {
-    double sphi = sin(alpha) / sin(th);
-    double dphi = sphi >= 1.0 ? kPi : asin(sphi);
-    half = (int)ceil(dphi / (2.0 * kPi / cols)) + 1;
-    if (2 * half + 1 >= cols) half = cols;
-  }
-  const int span = max(r0 - rlo, rhi - r0);
-  const int ncol_iter = (half >= cols) ? cols : 2 * half + 1;
-  for (int rr = 0; rr <= 2 * span; ++rr) {
-    // rows outward from r0 (nearest first), skipping rows outside [rlo, rhi]
-    int dr = (rr + 1) >> 1;
-    int row = (rr & 1) ? r0 - dr : r0 + dr;
-    if (row < rlo || row > rhi) continue;
-    for (int cc = 0; cc < ncol_iter; ++cc) {
-      int dc = (cc + 1) >> 1;
-      int col = (cc & 1) ? c0 - dc : c0 + dc;
-      col %= cols;
-      if (col < 0) col += cols;
-      int j = row * cols + col;
-      if (j == i) continue;
-      const double* q = dirs + 3 * (size_t)j;
-      double pq = p[0] * q[0] + p[1] * q[1] + p[2] * q[2];
-      if (!(pq > cut)) continue;
-      Line ln = cell_line(j, p, e1, e2, dirs, L);
-      unsigned out = 0;
-      for (int v = 0; v < m; ++v) out |= (ln.A * va[v] + ln.B * vb[v] + ln.C < 0.0 ? 1u : 0u) << v;
-      if (!out) continue;
-      const unsigned full = (m == 32) ? 0xffffffffu : ((1u << m) - 1u);
-      if (out == full) return 2;  // cannot happen: p (the origin) is inside every bisector
-      // convex polygon: the outside vertices form one cyclic run [s, e]
-      const unsigned prev = ((out << 1) | (out >> (m - 1))) & full;  // bit v: out[v−1]
-      const unsigned next = ((out >> 1) | (out << (m - 1))) & full;  // bit v: out[v+1]
-      const int s = __ffs(out & ~prev) - 1;
-      const int e = __ffs(out & ~next) - 1;
-      const int sp = (s + m - 1) % m;  // inside vertex before the run
-      const int L_out = __popc(out);
-      const int m_new = m - L_out + 2;
-      if (m_new > kMaxV) return 2;
-      // X = edge(sp) ∩ bisector, Y = bisector ∩ edge(e); cyclic order … sp, X, Y, e+1 …
-      const int lab_e = lab[e];
-      double xa, xb, ya, yb;
-      meet(cell_line(lab[sp], p, e1, e2, dirs, L), ln, xa, xb);
-      meet(ln, cell_line(lab_e, p, e1, e2, dirs, L), ya, yb);
-      if (s <= e) {
-        // run inside the array: [0, s) X Y [e+1, m) — shift the tail by 2 − L_out in place
-        const int shift = 2 - L_out;
-        if (shift < 0) {
-          for (int v = e + 1; v < m; ++v) {
-            va[v + shift] = va[v]; vb[v + shift] = vb[v]; lab[v + shift] = lab[v];
-          }
-        } else if (shift > 0) {
-          for (int v = m - 1; v > e; --v) {
-            va[v + shift] = va[v]; vb[v + shift] = vb[v]; lab[v + shift] = lab[v];
-          }
-        }
-        va[s] = xa; vb[s] = xb; lab[s] = j;
-        va[s + 1] = ya; vb[s + 1] = yb; lab[s + 1] = lab_e;
-      } else {
-        // run wraps: keep [e+1, s) moved to the front, then X Y
-        const int K = s - e - 1;
-        for (int v = 0; v < K; ++v) {
-          va[v] = va[e + 1 + v]; vb[v] = vb[e + 1 + v]; lab[v] = lab[e + 1 + v];
-        }
-        va[K] = xa; vb[K] = xb; lab[K] = j;
-        va[K + 1] = ya; vb[K + 1] = yb; lab[K + 1] = lab_e;
-      }
-      m = m_new;
-      t2R = 0.0;
-      for (int v = 0; v < m; ++v) t2R = fmax(t2R, va[v] * va[v] + vb[v] * vb[v]);
-      cut = cos2R();
-    }
-  }
-  for (int v = 0; v < m; ++v)
-    if (lab[v] < 0) return 1;
-  double th2 = tan(0.5 * alpha);
-  return (t2R <= th2 * th2) ? 0 : 1;
-}
-
-__global__ void __launch_bounds__(128, VC_LB_DEL) k_delaunay(BuildParams P, Wave W, int* own /* B×n×kMaxV×2 */,
-                                                  int* own_cnt) {
+__global__ void __launch_bounds__(kDelBS, VC_LB_DEL2) k_delaunay_smem(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ unsigned char dsm[];
+  double* sa = (double*)dsm;
+  double* sb = sa + kPolyV * kDelBS;
+  int* sl = (int*)(sb + kPolyV * kDelBS);
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)W.B * n) return;
   int rec = (int)(gid / n), i = (int)(gid - (long long)rec * n);
-  const double* dirs = W.dirs + (size_t)rec * n * 3;
-  int lab[kMaxV];
-  int m = 0;
-  double alpha = 3.5 * sqrt(4.0 * kPi / n);
-  int st = 1;
-  for (int attempt = 0; attempt < 8 && st == 1; ++attempt) {
-    st = voronoi_cell(dirs, P.rows, P.cols, i, alpha, lab, m);
-    alpha = fmin(2.0 * alpha, 1.5);
+  Poly poly{sa + threadIdx.x, sb + threadIdx.x, sl + threadIdx.x};
+  const int st = delaunay_point(P, W, rec, i, poly, own, own_cnt);
+  if (st == 2) {  // polygon outgrew shared memory: queue for k_delaunay_retry
+    const unsigned slot = atomicAdd(W.del_retry_count, 1u);
+    if ((int)slot < W.del_retry_cap) W.del_retry[slot] = (int)gid;
+    else atomicMax(W.tri_status + rec, 2);
   }
-  size_t base = ((size_t)rec * n + i);
-  W.deg[base] = (st == 0) ? m : 0;
-  int c = 0;
-  if (st == 0) {
-    for (int t = 0; t < m; ++t) {
-      int a = lab[t], b = lab[(t + 1) % m];
-      if (i < a && i < b) {
-        own[(base * kMaxV + c) * 2 + 0] = a;
-        own[(base * kMaxV + c) * 2 + 1] = b;
-        ++c;
-      }
-    }
-  } else {
-    atomicMax(W.tri_status + rec, st);
-  }
-  own_cnt[base] = c;
 }
+
+// Cells that outgrew the shared-memory polygon, recomputed with a 48-vertex polygon in
+// global memory (one slot per queued cell).
+__global__ void __launch_bounds__(128) k_delaunay_retry(BuildParams P, Wave W, int* own, int* own_cnt,
+                                                        double* scratch) {
+  const unsigned nr = min(*W.del_retry_count, (unsigned)W.del_retry_cap);
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += gridDim.x * blockDim.x) {
+    const int gid = W.del_retry[t];
+    const int rec = gid / P.n_angular, i = gid - rec * P.n_angular;
+    double* a = scratch + (size_t)t * kRetryV * 3;
+    PolyRetry poly{a, a + kRetryV, (int*)(a + 2 * kRetryV)};
+    if (delaunay_point(P, W, rec, i, poly, own, own_cnt) != 0) atomicMax(W.tri_status + rec, 2);
+  }
+}
+
+constexpr size_t kDelSmem = (size_t)kPolyV * kDelBS * (8 + 8 + 4);
 
 constexpr int kCompactBS = 512;
 
@@ -1319,7 +1217,10 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         smem_attr = true;
       }
       prof_begin(KC_DELAUNAY, st);
+      cudaMemsetAsync(W.del_retry_count, 0, sizeof(unsigned int), st);
       k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
+      k_delaunay_retry<<<sm_count * 2, 128, 0, st>>>(P, W, own, own_cnt, W.del_scratch);
+      ++nl;
       prof_end(st);
       prof_begin(KC_COMPACT, st);
   k_tri_compact<<<W.B, kCompactBS, 0, st>>>(P, W, own, own_cnt);

@@ -99,6 +99,10 @@ struct Wave {
   double* records;       // B × 2 × RecordSize(d) (optional)
   unsigned long long* live;  // B × live_words × n: bit i of word w = media sample (k, 64w+i) has rad > 0
   int live_words;            // ⌈r_ub / 64⌉
+  int* del_retry;        // triangulation cells that outgrew the shared-memory polygon
+  unsigned int* del_retry_count;
+  int del_retry_cap;
+  double* del_scratch;   // del_retry_cap × 48 × 3 doubles of global-memory polygons
   void* gather_q;        // two-pass gather: queued emitter-hit rays (GatherItem)
   unsigned long long* gather_q_count;
   long long gather_q_cap;
