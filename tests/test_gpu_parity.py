@@ -210,6 +210,41 @@ def test_full_size_16k_directions_triangulation():
     assert _tri_set(ins["tris"]) == _tri_set(adj)
 
 
+def test_cfg3_full_scale_records_vs_oracle():
+    """The benchmark workload itself: cfg3 records (51,300 triangles, n = 16384, march 0.1,
+    ~64 rings, ~200k gather rays each) vs the oracle re-run with the GPU's triangles
+    (brute-force C trace over all host threads) — moments, counts, ring counts, media."""
+    from paper_1805_09258_b200 import configs, estimate_moments_batch, inspect_record, seed_words
+    from oracle import volcache_oracle as O
+
+    w = configs.cfg3(n_points=64)
+    ps = O.pack(w.scene)
+    O.use_c_trace(None)
+    idx = np.array([3, 17])
+    r = estimate_moments_batch(w.scene, w.points[idx], seeds=seed_words(w.seed, 401, idx), n_angular=w.n_angular,
+                               march_step=w.march_step, epsilon=w.epsilon)
+    try:
+        for k, i in enumerate(idx):
+            ins = inspect_record(w.scene, w.points[i], rng_seed=np.random.SeedSequence([w.seed, 401, int(i)]),
+                                 n_angular=w.n_angular, march_step=w.march_step)
+            ob = O.build_record(ps, w.points[i], w.n_angular, w.march_step, O.seed_seq(w.seed, 401, int(i)),
+                                adjacency=ins["tris"])
+            _check_moments(f"cfg3_full[{i}]", r.L[k], r.grad[k], r.hess[k], ob.L, ob.grad, ob.hess)
+            np.testing.assert_array_equal(ins["idx"], ob.idx)
+            np.testing.assert_array_equal(ins["counts"], ob.counts)
+            assert r.stats[k, 0] == ob.stats["elements_evaluated"]
+            assert r.stats[k, 1] == ob.stats["elements_dropped"]
+            assert r.stats[k, 2] == ob.stats["star_vertices"]
+            np.testing.assert_allclose(ins["media"], ob.media_radiance, rtol=1e-6, atol=0)
+            rec = O.make_record(w.points[i], ob.L[0], ob.grad[0], ob.hess[0], w.epsilon, ps.scale, ps.max_emission)
+            from paper_1805_09258_b200.records import unpack_record
+
+            g = unpack_record(r.records[k, 0], 3)
+            assert rel_l2(_quadform(g.axes, g.radii), _quadform(rec.axes, rec.radii)) <= 1e-3
+    finally:
+        O.use_c_trace(0)
+
+
 @pytest.mark.parametrize("dim", [2, 3])
 def test_interpolate_vs_reference(dim):
     from paper_1805_09258_b200.cache import RadianceCache
