@@ -333,11 +333,22 @@ def main():
             traffic = json.loads(tf.read_text()).get(dom)
         except Exception:
             traffic = None
+    # every modelled kernel's fraction, and the whole path: W per record over the step time
+    per_kernel = {}
+    for k, w_k in work.items():
+        if k in shares and shares[k] > 0:
+            a = w_k / (shares[k] / 1e3) / 1e12
+            per_kernel[k] = {"achieved_tflops": a, "frac": a / pk["fp32_tflops"], "ms": shares[k]}
+    w_path = sum(work.values())
+    path_achieved = w_path / (ms / 1e3) / 1e12
     roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["fp32_tflops"], "traffic": traffic,
                 "peak_source": f"148 SMs x 128 FP32 lanes x 2 x sm_max_mhz ({pk['source']} clocks)",
                 "kernel_ms_share": {k: round(v / sum(shares.values()), 4) for k, v in shares.items()},
-                "algorithmic_flops_per_launch": flops_per_launch}
+                "algorithmic_flops_per_launch": flops_per_launch,
+                "per_kernel": per_kernel,
+                "path": {"algorithmic_flops_per_record": w_path / nrec, "achieved": path_achieved,
+                         "frac": path_achieved / pk["fp32_tflops"]}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

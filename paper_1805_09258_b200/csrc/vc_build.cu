@@ -58,16 +58,29 @@ __device__ inline void stratum_direction(int k, const BuildParams& P, Pcg64 g0, 
   }
 }
 
-template <int D>
 #ifndef VC_LB_TRACE
 #define VC_LB_TRACE 3  // min resident 256-thread CTAs per SM for the ray kernels
 #endif
 
+// Thread → direction map: each warp takes a 4-row × 8-column tile of the stratum grid
+// (≈7°×11° at the equator) instead of 32 columns of one row (≈2°×45°), so the lanes'
+// rays and cells are spatially coherent.  Falls back to row-major when the grid does
+// not tile.
+__device__ __forceinline__ int tiled_direction(int t, const BuildParams& P) {
+  if ((P.rows & 3) || (P.cols & 7) || P.rows == 1) return t;
+  const int tile = t >> 5, lane = t & 31;
+  const int tiles_per_row = P.cols >> 3;
+  const int tr = tile / tiles_per_row, tc = tile - tr * tiles_per_row;
+  return ((tr << 2) + (lane >> 3)) * P.cols + (tc << 3) + (lane & 7);
+}
+
+template <int D>
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)W.B * n) return;
-  int rec = (int)(gid / n), k = (int)(gid - (long long)rec * n);
+  int rec = (int)(gid / n);
+  int k = tiled_direction((int)(gid - (long long)rec * n), P);
   Pcg64 g0 = pcg_load(W.rng + 4 * rec);
   double d[3], o[3];
   stratum_direction<D>(k, P, g0, jt, d);
@@ -671,12 +684,13 @@ __global__ void __launch_bounds__(kDelBS, VC_LB_DEL2) k_delaunay_smem(BuildParam
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)W.B * n) return;
-  int rec = (int)(gid / n), i = (int)(gid - (long long)rec * n);
+  const int rec = (int)(gid / n);
+  const int i = (int)(gid - (long long)rec * n);  // row-major: a warp shares one row's window shape
   Poly poly{sa + threadIdx.x, sb + threadIdx.x, sl + threadIdx.x};
   const int st = delaunay_point(P, W, rec, i, poly, own, own_cnt);
   if (st == 2) {  // polygon outgrew shared memory: queue for k_delaunay_retry
     const unsigned slot = atomicAdd(W.del_retry_count, 1u);
-    if ((int)slot < W.del_retry_cap) W.del_retry[slot] = (int)gid;
+    if ((int)slot < W.del_retry_cap) W.del_retry[slot] = rec * n + i;
     else atomicMax(W.tri_status + rec, 2);
   }
 }
