@@ -268,6 +268,13 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   }
   P.host_adjacency = (D == 3 && adjacency != nullptr) ? 1 : 0;
   P.r_ub = (int)std::floor(sc->scale * (1.0 + 1e-9) / prm->march_step + 0.5) + 2;
+  {  // triangulation search radii: α₀ = 2.8 × mean direction spacing, ×1.5 per retry, ≤ 1.5
+    double a = 2.8 * std::sqrt(4.0 * 3.141592653589793 / n);
+    for (int k = 0; k < kDelLevels; ++k) {
+      P.del[k] = DelAngle{a, std::sin(a), std::cos(a), std::tan(0.5 * a)};
+      a = std::min(1.5 * a, 1.5);
+    }
+  }
   if (host) {  // ValueError before any work (src/subdivision.py:155-158)
     const double eps = 1e-12 * sc->scale;
     for (int i = 0; i < N; ++i)

@@ -509,7 +509,8 @@ using PolyRetry = PolyT<1, kRetryV>;
 // stays below alpha/2).  Returns 0 secure, 1 needs a larger alpha, 2 polygon overflow.
 template <class Poly>
 __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* __restrict__ dirs32, int rows,
-                                 int cols, int i, double alpha, Poly poly, int& m) {
+                                 int cols, int i, const DelAngle& ang, Poly poly, int& m) {
+  const double alpha = ang.alpha;
   const double* p = dirs + 3 * (size_t)i;
   const double px = p[0], py = p[1], pz = p[2];
   const float4 p32 = dirs32[i];
@@ -522,7 +523,7 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
   const double pp[3] = {px, py, pz};
   // initial square of half-size tan(α/2): a cell reaching beyond it fails the security
   // test (2·R_cell ≤ α) anyway, and the tighter start shrinks the candidate cut early
-  const double L = tan(0.5 * fmin(alpha, 1.5)) * 1.001;
+  const double L = ang.tan_half * 1.001;
   m = 4;
   poly.A(0) = L;  poly.B(0) = -L; poly.L(0) = -1;
   poly.A(1) = L;  poly.B(1) = L;  poly.L(1) = -2;
@@ -533,8 +534,8 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
   double cut = cos2R();
   float cutf = (float)cut - 2e-6f;
   // candidate rows: bands meeting z ∈ [cos(θ+α), cos(θ−α)]; columns: azimuth half-width
-  // asin(sin α / sin θ) ≤ (π/2)·sin α / sin θ (conservative, no transcendental per point)
-  const double sa = sin(alpha), ca = cos(alpha);
+  // asin(sin α / sin θ)
+  const double sa = ang.sin_a, ca = ang.cos_a;
   const double st = sqrt(fmax(0.0, 1.0 - pz * pz));
   const double z_hi = pz * ca + st * sa;  // cos(θ − α) (pole cap when θ ≤ α)
   const double z_lo = pz * ca - st * sa;  // cos(θ + α)
@@ -626,7 +627,7 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
   }
   for (int v = 0; v < m; ++v)
     if (poly.L(v) < 0) return 1;
-  const double th2 = tan(0.5 * alpha);
+  const double th2 = ang.tan_half;
   return (t2R <= th2 * th2) ? 0 : 1;
 }
 
@@ -642,12 +643,9 @@ __device__ int delaunay_point(const BuildParams& P, const Wave& W, int rec, int 
   // search radius α = 2.8 × mean spacing: the security test needs α ≥ 2·R_cell, and on the
   // jittered stratum grid R_cell ≤ 1.4 spacing for > 99.8% of directions (max ≈ 1.6);
   // the rest retry with 1.5α
-  double alpha = 2.8 * sqrt(4.0 * kPi / n);
   int st = 1;
-  for (int attempt = 0; attempt < 10 && st == 1; ++attempt) {
-    st = voronoi_cell_poly(dirs, W.dirs32 + (size_t)rec * n, P.rows, P.cols, i, alpha, poly, m);
-    alpha = fmin(1.5 * alpha, 1.5);
-  }
+  for (int attempt = 0; attempt < kDelLevels && st == 1; ++attempt)
+    st = voronoi_cell_poly(dirs, W.dirs32 + (size_t)rec * n, P.rows, P.cols, i, P.del[attempt], poly, m);
   if (st == 2) return 2;
   const size_t base = ((size_t)rec * n + i);
   W.deg[base] = (st == 0) ? m : 0;

@@ -50,8 +50,15 @@ struct DevScene {
 
 __host__ __device__ constexpr int prim_stride(int dim) { return dim == 3 ? 9 : 4; }
 
+// Triangulation search radius α and its trigonometry, per retry level (host-computed).
+struct DelAngle {
+  double alpha, sin_a, cos_a, tan_half;
+};
+constexpr int kDelLevels = 10;
+
 // Per-call record-build parameters (mirrors estimate_moments' arguments).
 struct BuildParams {
+  DelAngle del[kDelLevels];  // α_k = min(2.8 · spacing · 1.5^k, 1.5)
   int n_angular;
   double march_step;
   int n_inner;
