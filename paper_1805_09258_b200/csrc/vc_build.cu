@@ -921,6 +921,11 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
     unsigned long long mk[D];
     int word = -1;
     int maxc_e = 0;
+    // rings [0, minc_e) have every vertex live: the representative is vertex 0 (equal
+    // distances, first argmax) and the element is live exactly on vertex 0's mask bits,
+    // which are popped directly; rings [minc_e, maxc_e) are resolved one by one
+    int minc_e = 0, bw = 0;
+    unsigned long long bits = 0;
     bool fresh = true;
     while (true) {
       bool has = e < E;
@@ -930,6 +935,7 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
         if (fresh) {
           elem_vertices<D>(W, P, rec, e, vv);
           maxc_e = 0;
+          minc_e = 1 << 30;
 #pragma unroll
           for (int j = 0; j < D; ++j) {
             const DirInfo di = info[vv[j]];
@@ -937,9 +943,24 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
             sd[j] = di.s;
             sl[j] = di.surf_live;
             maxc_e = max(maxc_e, cv[j]);
+            minc_e = min(minc_e, cv[j]);
           }
           fresh = false;
           word = -1;
+          if (kind == 1) {
+            bw = 0;
+            bits = 0;
+            if (!media_on) {
+              minc_e = 0;
+              ring = maxc_e;  // media rings carry no radiance
+            } else {
+              ring = minc_e;
+              if (minc_e > 0) {
+                const unsigned long long m0 = live[vv[0]];
+                bits = (minc_e >= 64) ? m0 : (m0 & ((1ULL << minc_e) - 1ULL));
+              }
+            }
+          }
         }
         if (kind == 0) {
           int rep = 0;
@@ -950,6 +971,20 @@ __global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams 
           item = make_uint2((unsigned)e, (unsigned)rep);
           e += kStride;
           fresh = true;
+        } else if (bits) {
+          const int b = __ffsll((long long)bits) - 1;
+          bits &= bits - 1ULL;
+          flag = true;
+          item = make_uint2((unsigned)e, ((unsigned)(bw * 64 + b) << 2));
+          if (!bits && !((bw + 1) * 64 < minc_e) && ring >= maxc_e) {
+            e += kStride;
+            fresh = true;
+          }
+        } else if ((bw + 1) * 64 < minc_e) {
+          ++bw;
+          const int hi = minc_e - bw * 64;
+          const unsigned long long m0 = live[(size_t)bw * n + vv[0]];
+          bits = (hi >= 64) ? m0 : (m0 & ((1ULL << hi) - 1ULL));
         } else {
           if (ring < maxc_e) {
             double ri = ring_radius(ring, step);
