@@ -154,6 +154,46 @@ int vc_render(vc_scene* scene, vc_cache* single, vc_cache* multiple, const vc_ca
               const vc_render_params* params, double* image, int64_t* stats, int flags,
               void* stream);
 
+/* Record rows and creation tags (march-point ordinal, −1 for records given to
+ * vc_cache_create) of a cache, in insertion order.  records: n × record size float64,
+ * tags: n int64 (either may be NULL); host memory with VC_MEM_HOST, else device. */
+int64_t vc_cache_size(const vc_cache* cache);
+int vc_cache_records(const vc_cache* cache, double* records, int64_t* tags, int flags, void* stream);
+
+#define VC_TARGET_FIELD 1  /* FieldGrid: 2D cell centers, scanline order (src/renderer.py:88-131) */
+#define VC_TARGET_CAMERA 2 /* Camera: pixel-center rays marched at march_step (src/renderer.py:134-193) */
+
+typedef struct {
+  int target;                 /* VC_TARGET_FIELD or VC_TARGET_CAMERA */
+  vc_camera camera;           /* camera target (crop fields ignored) */
+  int field_nx, field_ny;     /* field target: cells */
+  double field_min[2], field_max[2]; /* field target: FieldGrid bounds */
+  double march_step;          /* RenderSettings.march_step (camera march and ring spacing) */
+  int seed;                   /* RenderSettings.seed: record seeds (seed, 401, i) */
+  int n_angular, n_inner, n_light_samples;
+  double epsilon;
+  int isotropic;              /* mode "ours-iso" */
+  int window;                 /* record builds per speculative window (0: 2048, max 2048) */
+  int64_t lookahead;          /* initial lookahead in march points (0: 65536) */
+} vc_populate_params;
+
+/* populate_cache (src/renderer.py:302-327) for the cache modes ours-aniso / ours-iso:
+ * march the target's points in scanline order and insert a (single, multiple) record
+ * pair, per-cache masked, wherever a cache lacks coverage.  The result equals the
+ * sequential loop's caches record for record (speculative windows, exact resolution).
+ * Returns two new caches; stats (may be NULL) = points_marched, records_single,
+ * records_multiple, windows, builds, discarded_builds, early_stops, 0. */
+int vc_populate(vc_scene* scene, const vc_populate_params* params, vc_cache** single, vc_cache** multiple,
+                int64_t* stats, void* stream);
+
+/* FieldGrid render (src/renderer.py:425-437) for the cache modes: S(x) = full_angle(2) ·
+ * (J_single + J_multiple) at the cell centers, image ny × nx × 3 float64.  Cells no cache
+ * pair covers are evaluated directly with seeds (seed, 307, iy, ix); with frozen = 0 they
+ * also insert their records into the caches in scanline order (sequentially exact, as
+ * vc_populate) and read the blended value back.  stats: cache_hits, direct_evaluations. */
+int vc_render_field(vc_scene* scene, vc_cache* single, vc_cache* multiple, const vc_populate_params* params,
+                    int frozen, double* image, int64_t* stats, int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -958,3 +958,90 @@ def render_camera(ps, cam: dict, single: Cache, multiple: Cache, prm: RenderPara
                 acc += np.exp(-sig * max(0.0, t_end[q] - t_in[q])) * lo[q]
             img[i] += acc
     return img / prm.spp, stats
+
+
+# ---------------------------------------------------------------------------
+# Cache population and field render (src/renderer.py:282-327, :335-368, :425-437)
+# ---------------------------------------------------------------------------
+
+
+def march_points(ps, target: dict, march_step: float):
+    """Scanline march points (src/renderer.py:282-299).
+
+    `target` = {"kind": "field", nx, ny, bmin, bmax} or {"kind": "camera", position,
+    look_at, up, fov, width, height}.
+    """
+    if target["kind"] == "field":
+        nx, ny = target["nx"], target["ny"]
+        lo, hi = np.asarray(target["bmin"], float), np.asarray(target["bmax"], float)
+        dx = (hi[0] - lo[0]) / nx
+        dy = (hi[1] - lo[1]) / ny
+        for iy in range(ny):
+            for ix in range(nx):
+                yield np.array([lo[0] + (ix + 0.5) * dx, hi[1] - (iy + 0.5) * dy])
+        return
+    h, w = target["height"], target["width"]
+    o, d = camera_rays(target["position"], target["look_at"], target["up"], target["fov"], w, h,
+                       np.full((h, w, 2), 0.5))
+    t_s, _ = trace(ps, o, d)
+    t_in, t_out, valid = bounds_span(ps, o, d)
+    t_end = np.minimum(t_s, t_out)
+    for i in range(o.shape[0]):
+        if not valid[i]:
+            continue
+        n_steps = int(np.floor((t_end[i] - t_in[i]) / march_step + 0.5))
+        for k in range(1, n_steps + 1):
+            yield o[i] + (t_in[i] + (k - 0.5) * march_step) * d[i]
+
+
+def compute_pair(ps, x, prm: RenderParams, seed, adjacency_fn=None):
+    """CacheSet.compute (src/renderer.py:231-262) for the ours-* modes → (J, (rec_s, rec_m))."""
+    rb = build_record(ps, x, n_angular=prm.n_angular, march_step=prm.march_step, rng_seed=seed,
+                      n_inner=prm.n_inner, n_light_samples=prm.n_light_samples,
+                      adjacency=None if adjacency_fn is None else adjacency_fn(seed))
+    recs = tuple(make_record(x, rb.L[k], rb.grad[k], rb.hess[k], prm.epsilon, ps.scale, ps.max_emission,
+                             anisotropic=prm.anisotropic) for k in (0, 1))
+    return rb.L[0] + rb.L[1], recs
+
+
+def populate_cache(ps, target: dict, prm: RenderParams, adjacency_fn=None):
+    """Sequential greedy insertion (src/renderer.py:302-327) → (single, multiple, points)."""
+    single, multiple = Cache(), Cache()
+    n = 0
+    for i, x in enumerate(march_points(ps, target, prm.march_step)):
+        n += 1
+        s, m = interpolate(single, x), interpolate(multiple, x)
+        if s is None or m is None:
+            _, (rs, rm) = compute_pair(ps, x, prm, seed_seq(prm.seed, 401, i), adjacency_fn)
+            if s is None:
+                single.records.append(rs)
+            if m is None:
+                multiple.records.append(rm)
+    return single, multiple, n
+
+
+def render_field(ps, target: dict, single: Cache, multiple: Cache, prm: RenderParams, frozen=True):
+    """FieldGrid render (src/renderer.py:425-437 with _point_value :335-368) → (image, stats)."""
+    nx, ny = target["nx"], target["ny"]
+    img = np.zeros((ny, nx, 3))
+    stats = {"cache_hits": 0, "direct_evaluations": 0}
+    pts = list(march_points(ps, target, prm.march_step))
+    for j, x in enumerate(pts):
+        iy, ix = divmod(j, nx)
+        s, m = interpolate(single, x), interpolate(multiple, x)
+        if s is not None and m is not None:
+            stats["cache_hits"] += 1
+            val = s + m
+        else:
+            stats["direct_evaluations"] += 1
+            val, (rs, rm) = compute_pair(ps, x, prm, seed_seq(prm.seed, 307, iy, ix))
+            if not frozen:
+                if s is None:
+                    single.records.append(rs)
+                if m is None:
+                    multiple.records.append(rm)
+                a, b = interpolate(single, x), interpolate(multiple, x)
+                if a is not None and b is not None:
+                    val = a + b
+        img[iy, ix] = 2.0 * np.pi * val
+    return img, stats

@@ -71,6 +71,30 @@ class RenderParams(C.Structure):
     ]
 
 
+VC_TARGET_FIELD = 1
+VC_TARGET_CAMERA = 2
+
+
+class PopulateParams(C.Structure):
+    _fields_ = [
+        ("target", C.c_int),
+        ("camera", Camera),
+        ("field_nx", C.c_int),
+        ("field_ny", C.c_int),
+        ("field_min", C.c_double * 2),
+        ("field_max", C.c_double * 2),
+        ("march_step", C.c_double),
+        ("seed", C.c_int),
+        ("n_angular", C.c_int),
+        ("n_inner", C.c_int),
+        ("n_light_samples", C.c_int),
+        ("epsilon", C.c_double),
+        ("isotropic", C.c_int),
+        ("window", C.c_int),
+        ("lookahead", C.c_int64),
+    ]
+
+
 _SIGS = {
     "vc_version": (C.c_int, []),
     "vc_last_error": (C.c_char_p, []),
@@ -92,6 +116,10 @@ _SIGS = {
     "vc_cache_destroy": (None, [_vp]),
     "vc_cache_interpolate": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
     "vc_render": (C.c_int, [_vp, _vp, _vp, C.POINTER(Camera), C.POINTER(RenderParams), _vp, _vp, C.c_int, _vp]),
+    "vc_cache_size": (C.c_int64, [_vp]),
+    "vc_cache_records": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "vc_populate": (C.c_int, [_vp, C.POINTER(PopulateParams), C.POINTER(_vp), C.POINTER(_vp), _vp, _vp]),
+    "vc_render_field": (C.c_int, [_vp, _vp, _vp, C.POINTER(PopulateParams), C.c_int, _vp, _vp, C.c_int, _vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -35,25 +35,53 @@ class RadianceCache:
         self._handle = None
         self._fin = None
 
+    @classmethod
+    def _adopt(cls, bounds_min, bounds_max, handle) -> "RadianceCache":
+        """Wrap a device cache built by the library (vc_populate); records download lazily."""
+        c = cls(bounds_min, bounds_max)
+        c._records = None
+        c._handle = handle
+        c._fin = weakref.finalize(c, _lib.lib().vc_cache_destroy, handle)
+        return c
+
+    def _device_changed(self) -> None:
+        """The device cache grew in place (render with frozen=False): re-read lazily."""
+        self._records = None
+
+    def _host_records(self) -> list:
+        if self._records is None:
+            L = _lib.lib()
+            n = int(L.vc_cache_size(self._handle))
+            rows = np.zeros((n, record_size(self.dim)))
+            if n:
+                _lib.check(L.vc_cache_records(self._handle, _lib.ptr(rows), None, _lib.VC_MEM_HOST, None))
+            from .records import unpack_record
+
+            self._records = [unpack_record(r, self.dim) for r in rows]
+        return self._records
+
     def __len__(self) -> int:
+        if self._records is None:
+            return int(_lib.lib().vc_cache_size(self._handle))
         return len(self._records)
 
     @property
     def records(self) -> list:
-        return list(self._records)
+        return list(self._host_records())
 
     def insert(self, record) -> None:
         if np.asarray(record.position).size != self.dim:
             raise ValueError("record dimensionality does not match the cache")
-        self._records.append(record)
+        self._host_records().append(record)
         self._invalidate()
 
     def extend_packed(self, packed: np.ndarray) -> None:
         """Insert many records given as packed rows (N, d + 3 + 3d + d² + d)."""
         from .records import unpack_record
 
+        recs = self._host_records()
         for row in np.asarray(packed, float).reshape(-1, record_size(self.dim)):
-            self._records.append(unpack_record(row, self.dim))
+            recs.append(unpack_record(row, self.dim))
         self._invalidate()
 
     def _invalidate(self):
@@ -64,11 +92,12 @@ class RadianceCache:
 
     def packed(self) -> np.ndarray:
         d = self.dim
-        if not self._records:
+        recs = self._host_records()
+        if not recs:
             return np.zeros((0, record_size(d)))
         return np.ascontiguousarray(np.stack([np.concatenate([
             np.asarray(r.position, float), np.asarray(r.value, float), np.asarray(r.grad, float).ravel(),
-            np.asarray(r.axes, float).ravel(), np.asarray(r.radii, float)]) for r in self._records]))
+            np.asarray(r.axes, float).ravel(), np.asarray(r.radii, float)]) for r in recs]))
 
     def handle(self):
         if self._handle is None:

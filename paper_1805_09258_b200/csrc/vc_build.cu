@@ -775,7 +775,10 @@ __global__ void k_degree(BuildParams P, Wave W) {
 // Moment assembly (src/subdivision.py:287-370)
 // ---------------------------------------------------------------------------
 
-constexpr int kAsmBS = 256;
+#ifndef VC_ASM_BS
+#define VC_ASM_BS 128
+#endif
+constexpr int kAsmBS = VC_ASM_BS;
 constexpr int kQCap = 64;
 
 template <int D>
@@ -812,7 +815,7 @@ __device__ __forceinline__ void warp_transpose_sum(double (&v)[32], int lane) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kAsmBS, 2) k_assemble(DevScene S, BuildParams P, Wave W) {
+__global__ void __launch_bounds__(kAsmBS, 512 / kAsmBS) k_assemble(DevScene S, BuildParams P, Wave W) {
   constexpr int NQ = 1 + D + D * (D + 1) / 2;
   constexpr int NW = kAsmBS / 32;
   static_assert(3 * NQ <= 32, "contribution vector must fit one warp");

@@ -1,139 +1,319 @@
-// Record cache on device: multi-level grid index, interpolation, frozen-cache camera march.
-//
-// Index: the reference keeps records in an MX-CIF tree whose point query returns
-// exactly the records with support > 0 (src/cache.py:262-334, ≡ linear scan).  Here a
-// record of bounding radius r lives on the coarsest-needed level ℓ of a pyramid of
-// dense grids over the same padded root cube (cell size h_ℓ ≥ 2r, so its box touches
-// ≤ 2^d cells); a query visits one cell per level plus the overflow list of records
-// whose box leaves the root cube, and applies the reference's strict support test —
-// the covering set is identical to the linear scan.
+// Record cache on device: index build, interpolation, frozen-cache camera march.
+// (Index layout and the tag rule: vc_cache.cuh.)
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
 
-#include "vc_api_internal.h"
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
 #include "vc_build.h"
-#include "vc_device.cuh"
+#include "vc_cache.cuh"
 
 namespace vc {
 
-struct DevCache {
-  int dim, n, L0, n_overflow;
-  double origin[3];
-  double size;
-  const long long* level_off;  // L0+2 entries: first cell index of each level
-  const int* cell_start;       // per cell start into items (+1 sentinel)
-  const int* items;
-  const int* overflow;
-  const double* rec;           // n × record_size(dim), reference layout
+// ---------------------------------------------------------------------------
+// Index build on the device
+// ---------------------------------------------------------------------------
+
+struct IdxGeom {
+  int dim, L0;
+  double origin[3], size;
+  const long long* level_off;
 };
 
-}  // namespace vc
-
-struct vc_cache {
-  int dim = 0, n = 0, L0 = 0;
-  double origin[3] = {0, 0, 0}, size = 0.0;
-  long long n_cells = 0;
-  std::vector<long long> level_off;
-  long long* d_level_off = nullptr;
-  int* d_cell_start = nullptr;
-  int* d_items = nullptr;
-  int* d_overflow = nullptr;
-  int n_overflow = 0;
-  double* d_rec = nullptr;
-  vc::DevCache dev() const {
-    vc::DevCache c{};
-    c.dim = dim;
-    c.n = n;
-    c.L0 = L0;
-    c.n_overflow = n_overflow;
-    for (int a = 0; a < 3; ++a) c.origin[a] = origin[a];
-    c.size = size;
-    c.level_off = d_level_off;
-    c.cell_start = d_cell_start;
-    c.items = d_items;
-    c.overflow = d_overflow;
-    c.rec = d_rec;
-    return c;
+// Level and cell box of record R; false → overflow list (box leaves the root cube).
+__device__ inline bool record_cells(const IdxGeom& G, const double* R, int& lv, long long clo[3], long long chi[3]) {
+  const int d = G.dim;
+  const double* rad = R + d + 3 + 3 * d + d * d;
+  double br = 0.0;
+  for (int a = 0; a < d; ++a) br = fmax(br, rad[a]);
+  br = br * (1.0 + 1e-9) + 1e-12 * G.size;
+  bool fits = isfinite(br);
+  double lo[3], hi[3];
+  for (int a = 0; a < d; ++a) {
+    lo[a] = R[a] - br;
+    hi[a] = R[a] + br;
+    if (!(lo[a] >= G.origin[a] && hi[a] <= G.origin[a] + G.size)) fits = false;
   }
-  ~vc_cache() {
-    cudaFree(d_level_off);
-    cudaFree(d_cell_start);
-    cudaFree(d_items);
-    cudaFree(d_overflow);
-    cudaFree(d_rec);
+  if (!fits) return false;
+  lv = 0;
+  while (lv < G.L0 && G.size / (double)(1LL << (G.L0 - lv)) < 2.0 * br) ++lv;
+  const long long N = 1LL << (G.L0 - lv);
+  const double h = G.size / (double)N;
+  for (int a = 0; a < 3; ++a) clo[a] = chi[a] = 0;
+  for (int a = 0; a < d; ++a) {
+    clo[a] = min(max((long long)floor((lo[a] - G.origin[a]) / h), 0LL), N - 1);
+    chi[a] = min(max((long long)floor((hi[a] - G.origin[a]) / h), 0LL), N - 1);
   }
-};
-
-namespace vc {
-
-// support coordinate, first-order estimate, cubic weight (src/cache.py:49-56, :112-121)
-template <int D>
-__device__ __forceinline__ void blend_record(const double* R, const double* x, double num[3], double& den,
-                                             int& hits) {
-  const double* pos = R;
-  const double* val = R + D;
-  const double* grd = R + D + 3;
-  const double* ax = R + D + 3 + 3 * D;
-  const double* rad = R + D + 3 + 3 * D + D * D;
-  double dl[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) dl[a] = sub(x[a], pos[a]);
-  double q = 0.0;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    double al = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) al = add(al, mul(dl[i], ax[i * D + j]));
-    double t = __ddiv_rn(al, rad[j]);
-    q = add(q, mul(t, t));
-  }
-  double sup = sub(1.0, sqrt(q));
-  if (!(sup > 0.0)) return;
-  ++hits;
-  double d = fmin(fmax(sup, 0.0), 1.0);
-  double w = sub(mul(mul(3.0, d), d), mul(mul(mul(2.0, d), d), d));
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    double e = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) e = add(e, mul(grd[c * D + i], dl[i]));
-    e = add(val[c], e);
-    e = fmax(e, 0.0);
-    num[c] = add(num[c], mul(w, e));
-  }
-  den = add(den, w);
+  return true;
 }
 
-template <int D>
-__device__ inline bool cache_interpolate(const DevCache& C, const double* x, double J[3], int* count) {
-  double num[3] = {0.0, 0.0, 0.0}, den = 0.0;
-  int hits = 0;
-  const int RS = record_size(D);
-  for (int lv = C.L0; lv >= 0; --lv) {  // coarse → fine (tree order: root first)
-    const int N = 1 << (C.L0 - lv);
-    const double h = C.size / N;
-    long long cell = 0;
-    bool inside = true;
-#pragma unroll
-    for (int a = D - 1; a >= 0; --a) {
-      double f = floor((x[a] - C.origin[a]) / h);
-      if (!(f >= 0.0 && f < (double)N)) inside = false;
-      cell = cell * N + (inside ? (long long)f : 0);
-    }
-    if (!inside) continue;
-    long long ci = C.level_off[lv] + cell;
-    int b = C.cell_start[ci], e = C.cell_start[ci + 1];
-    for (int t = b; t < e; ++t) blend_record<D>(C.rec + (size_t)C.items[t] * RS, x, num, den, hits);
+__global__ void k_idx_count(IdxGeom G, const double* rec, int n, int* cnt, int* ovf) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int lv;
+  long long clo[3], chi[3];
+  bool fits = record_cells(G, rec + (size_t)r * record_size(G.dim), lv, clo, chi);
+  long long c = 0;
+  if (fits) c = (chi[0] - clo[0] + 1) * (chi[1] - clo[1] + 1) * (chi[2] - clo[2] + 1);
+  cnt[r] = (int)c;
+  ovf[r] = fits ? 0 : 1;
+}
+
+__global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, unsigned* keys, int* vals) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int lv;
+  long long clo[3], chi[3];
+  if (!record_cells(G, rec + (size_t)r * record_size(G.dim), lv, clo, chi)) return;
+  const long long N = 1LL << (G.L0 - lv);
+  int o = off[r];
+  for (long long z = clo[2]; z <= chi[2]; ++z)
+    for (long long y = clo[1]; y <= chi[1]; ++y)
+      for (long long x = clo[0]; x <= chi[0]; ++x) {
+        long long cell = (G.dim == 3) ? (z * N + y) * N + x : y * N + x;
+        keys[o] = (unsigned)(G.level_off[lv] + cell);
+        vals[o] = r;
+        ++o;
+      }
+}
+
+// cell_start[c] = first sorted entry with key ≥ c, for c in [0, n_cells]
+__global__ void k_idx_starts(const unsigned* keys, int T, long long n_cells, int* start) {
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n_cells) return;
+  int lo = 0, hi = T;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((long long)keys[mid] < c) lo = mid + 1;
+    else hi = mid;
   }
-  for (int t = 0; t < C.n_overflow; ++t) blend_record<D>(C.rec + (size_t)C.overflow[t] * RS, x, num, den, hits);
-  if (count) *count = hits;
-  if (hits == 0 || !(den > 0.0)) return false;
-  J[0] = __ddiv_rn(num[0], den);
-  J[1] = __ddiv_rn(num[1], den);
-  J[2] = __ddiv_rn(num[2], den);
-  return true;
+  start[c] = lo;
+}
+
+__global__ void k_cache_gather(const double* src, size_t stride, const int* sel, const long long* tags, int k, int RS,
+                               double* dst, long long* dtag) {
+  int j = blockIdx.y;
+  if (j >= k) return;
+  const double* s = src + (size_t)sel[j] * stride;
+  for (int t = threadIdx.x; t < RS; t += blockDim.x) dst[(size_t)j * RS + t] = s[t];
+  if (threadIdx.x == 0) dtag[j] = tags ? tags[j] : -1;
+}
+
+__global__ void k_iota(int* v, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+__global__ void k_fill_tags(long long* tag, int n, long long v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tag[i] = v;
+}
+
+int make_dev_camera(const vc_camera& C0, DevCamera* out) {
+  DevCamera cam{};
+  // camera frame (src/renderer.py:158-170)
+  double f[3], r[3], u[3];
+  double fn = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    f[a] = C0.look_at[a] - C0.position[a];
+    fn += f[a] * f[a];
+  }
+  fn = std::sqrt(fn);
+  if (fn == 0.0) return fail(VC_EINVAL, "camera look_at must differ from position");
+  for (int a = 0; a < 3; ++a) f[a] /= fn;
+  r[0] = f[1] * C0.up[2] - f[2] * C0.up[1];
+  r[1] = f[2] * C0.up[0] - f[0] * C0.up[2];
+  r[2] = f[0] * C0.up[1] - f[1] * C0.up[0];
+  double rn = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  if (rn < 1e-9) return fail(VC_EINVAL, "camera up must not be parallel to the view direction");
+  for (int a = 0; a < 3; ++a) r[a] /= rn;
+  u[0] = r[1] * f[2] - r[2] * f[1];
+  u[1] = r[2] * f[0] - r[0] * f[2];
+  u[2] = r[0] * f[1] - r[1] * f[0];
+  for (int a = 0; a < 3; ++a) {
+    cam.pos[a] = C0.position[a];
+    cam.fwd[a] = f[a];
+    cam.right[a] = r[a];
+    cam.up[a] = u[a];
+  }
+  cam.tan_half = std::tan(C0.fov_degrees * (3.141592653589793 / 180.0) * 0.5);
+  cam.aspect = (double)C0.width / (double)C0.height;
+  cam.w = C0.width;
+  cam.h = C0.height;
+  cam.row0 = C0.row0;
+  cam.rows = C0.rows > 0 ? C0.rows : C0.height - C0.row0;
+  cam.col0 = C0.col0;
+  cam.cols = C0.cols > 0 ? C0.cols : C0.width - C0.col0;
+  if (cam.w < 1 || cam.h < 1) return fail(VC_EINVAL, "camera resolution must be positive");
+  if (cam.row0 < 0 || cam.col0 < 0 || cam.row0 + cam.rows > cam.h || cam.col0 + cam.cols > cam.w)
+    return fail(VC_EINVAL, "crop outside the image");
+  *out = cam;
+  return VC_OK;
+}
+
+int cache_init(vc_cache* c, int dim, const double* bmin, const double* bmax) {
+  c->dim = dim;
+  c->n = 0;
+  // root cube of the reference tree (src/cache.py:284-288)
+  double diag = 0.0, mx = 0.0;
+  for (int a = 0; a < dim; ++a) {
+    diag += (bmax[a] - bmin[a]) * (bmax[a] - bmin[a]);
+    mx = std::max(mx, bmax[a] - bmin[a]);
+  }
+  diag = std::sqrt(diag);
+  double half = 0.5 * mx + 0.25 * diag;
+  for (int a = 0; a < dim; ++a) c->origin[a] = 0.5 * (bmin[a] + bmax[a]) - half;
+  c->size = 2.0 * half;
+  c->L0 = dim == 3 ? 7 : 10;
+  // levels: N_ℓ = 2^(L0−ℓ) cells per axis
+  c->level_off.assign(c->L0 + 2, 0);
+  long long tot = 0;
+  for (int lv = 0; lv <= c->L0; ++lv) {
+    c->level_off[lv] = tot;
+    long long N = 1LL << (c->L0 - lv);
+    tot += (dim == 3) ? N * N * N : N * N;
+  }
+  c->level_off[c->L0 + 1] = tot;
+  c->n_cells = tot;
+  cudaError_t e = cudaMalloc(&c->d_level_off, c->level_off.size() * 8);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->d_level_off, c->level_off.data(), c->level_off.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_cell_start, (size_t)(tot + 1) * 4);
+  if (e == cudaSuccess) e = cudaMemset(c->d_cell_start, 0, (size_t)(tot + 1) * 4);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index allocation");
+  return VC_OK;
+}
+
+int cache_reserve(vc_cache* c, size_t n_records, cudaStream_t st) {
+  if (n_records <= c->rec_cap) return VC_OK;
+  size_t cap = std::max<size_t>(n_records, std::max<size_t>(1024, c->rec_cap * 2));
+  const size_t RS = record_size(c->dim);
+  double* r = nullptr;
+  long long* t = nullptr;
+  cudaError_t e = cudaMalloc(&r, cap * RS * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&t, cap * 8);
+  if (e == cudaSuccess && c->n) e = cudaMemcpyAsync(r, c->d_rec, (size_t)c->n * RS * 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && c->n) e = cudaMemcpyAsync(t, c->d_tag, (size_t)c->n * 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(r);
+    cudaFree(t);
+    return cuda_fail(e, "cache growth");
+  }
+  cudaFree(c->d_rec);
+  cudaFree(c->d_tag);
+  c->d_rec = r;
+  c->d_tag = t;
+  c->rec_cap = cap;
+  return VC_OK;
+}
+
+int cache_append(vc_cache* c, const double* src, size_t stride, const int* d_sel, const long long* d_tags, int k,
+                 cudaStream_t st) {
+  if (k <= 0) return VC_OK;
+  int rc = cache_reserve(c, (size_t)c->n + k, st);
+  if (rc) return rc;
+  const int RS = record_size(c->dim);
+  k_cache_gather<<<dim3(1, k), 32, 0, st>>>(src, stride, d_sel, d_tags, k, RS, c->d_rec + (size_t)c->n * RS,
+                                            c->d_tag + c->n);
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "cache append");
+  c->n += k;
+  return VC_OK;
+}
+
+int cache_truncate(vc_cache* c, int n, cudaStream_t st) {
+  (void)st;
+  if (n < c->n) c->n = n;
+  return VC_OK;
+}
+
+int cache_rebuild(vc_cache* c, cudaStream_t st) {
+  const int n = c->n;
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](int slot, size_t bytes) { return c->ws.get(slot, bytes, &e); };
+  if (n == 0) {
+    c->n_overflow = 0;
+    e = cudaMemsetAsync(c->d_cell_start, 0, (size_t)(c->n_cells + 1) * 4, st);
+    if (e == cudaSuccess && !c->d_items) e = cudaMalloc(&c->d_items, 16);
+    if (e == cudaSuccess && !c->d_overflow) e = cudaMalloc(&c->d_overflow, 16);
+    return e == cudaSuccess ? VC_OK : cuda_fail(e, "cache index reset");
+  }
+  IdxGeom G{};
+  G.dim = c->dim;
+  G.L0 = c->L0;
+  for (int a = 0; a < 3; ++a) G.origin[a] = c->origin[a];
+  G.size = c->size;
+  G.level_off = c->d_level_off;
+  int* cnt = (int*)alloc(0, (size_t)n * 4);
+  int* ovf = (int*)alloc(1, (size_t)n * 4);
+  int* off = (int*)alloc(2, ((size_t)n + 1) * 4);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
+  const int nb = (n + 127) / 128;
+  k_idx_count<<<nb, 128, 0, st>>>(G, c->d_rec, n, cnt, ovf);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, st);
+  // scan n+1 entries: the last input is read past cnt[n-1]; give it a zero slot
+  int* cnt1 = (int*)alloc(3, ((size_t)n + 1) * 4);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
+  e = cudaMemcpyAsync(cnt1, cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt1 + n, 0, 4, st);
+  void* tmp = alloc(4, tb);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index scan");
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt1, off, n + 1, st);
+  // overflow list (record order) and its count
+  int* ovf_list = (int*)alloc(5, (size_t)n * 4);
+  int* n_sel = (int*)alloc(6, 16);
+  size_t sb = 0;
+  int* iota = (int*)alloc(12, (size_t)n * 4);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
+  k_iota<<<nb, 128, 0, st>>>(iota, n);
+  cub::DeviceSelect::Flagged(nullptr, sb, iota, ovf, ovf_list, n_sel, n, st);
+  void* stmp = alloc(7, sb);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index select");
+  cub::DeviceSelect::Flagged(stmp, sb, iota, ovf, ovf_list, n_sel, n, st);
+  int hv[2] = {0, 0};
+  e = cudaMemcpyAsync(&hv[0], off + n, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[1], n_sel, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index sizes");
+  const int T = hv[0];
+  c->n_overflow = hv[1];
+  unsigned* keys = (unsigned*)alloc(8, (size_t)T * 4 + 4);
+  int* vals = (int*)alloc(9, (size_t)T * 4 + 4);
+  unsigned* keys2 = (unsigned*)alloc(10, (size_t)T * 4 + 4);
+  if (c->items_cap < (size_t)T + 1) {
+    cudaFree(c->d_items);
+    c->d_items = nullptr;
+    size_t cap = std::max<size_t>((size_t)T + 1, c->items_cap * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_items, cap * 4);
+    c->items_cap = e == cudaSuccess ? cap : 0;
+  }
+  cudaFree(c->d_overflow);
+  c->d_overflow = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_overflow, (size_t)c->n_overflow * 4 + 4);
+  if (e == cudaSuccess && c->n_overflow)
+    e = cudaMemcpyAsync(c->d_overflow, ovf_list, (size_t)c->n_overflow * 4, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index buffers");
+  k_idx_emit<<<nb, 128, 0, st>>>(G, c->d_rec, n, off, keys, vals);
+  // stable sort by cell keeps records in insertion order within a cell
+  int end_bit = 1;
+  while (end_bit < 32 && (1LL << end_bit) <= c->n_cells) ++end_bit;
+  size_t rb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
+  void* rtmp = alloc(11, rb);
+  if (e != cudaSuccess) return cuda_fail(e, "cache index sort scratch");
+  if (T > 0) cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
+  k_idx_starts<<<(int)((c->n_cells + 1 + 255) / 256), 256, 0, st>>>(keys2, T, c->n_cells, c->d_cell_start);
+  count_launches(7);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "cache index build");
+  return VC_OK;
 }
 
 template <int D>
@@ -157,12 +337,6 @@ __global__ void k_interpolate(DevCache C, int m, const double* xq, double* J, in
 // Camera march (src/renderer.py:133-193, :382-394, :440-484)
 // ---------------------------------------------------------------------------
 
-struct DevCamera {
-  double pos[3], fwd[3], right[3], up[3];
-  double tan_half, aspect;
-  int w, h, row0, rows, col0, cols;
-};
-
 struct MarchOut {
   double* image;          // h × w × 3
   long long* miss_cnt;    // per crop pixel (pass 1)
@@ -172,45 +346,6 @@ struct MarchOut {
   const double* miss_J;   // direct-evaluation results (pass 2)
   long long* hits;        // per crop pixel cache hits
 };
-
-__device__ inline void camera_ray(const DevCamera& cam, int px, int py, double jx, double jy, double* o, double* d) {
-  double u = __ddiv_rn(add((double)px, jx), (double)cam.w);
-  double v = __ddiv_rn(add((double)py, jy), (double)cam.h);
-  double xn = mul(mul(sub(mul(2.0, u), 1.0), cam.tan_half), cam.aspect);
-  double yn = mul(sub(1.0, mul(2.0, v)), cam.tan_half);
-  double nn = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    d[a] = add(add(cam.fwd[a], mul(xn, cam.right[a])), mul(yn, cam.up[a]));
-    nn = add(nn, mul(d[a], d[a]));
-  }
-  nn = sqrt(nn);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    d[a] = __ddiv_rn(d[a], nn);
-    o[a] = cam.pos[a];
-  }
-}
-
-__device__ inline void bounds_span(const DevScene& S, const double* o, const double* d, double& t_in,
-                                   double& t_out, bool& valid) {
-  const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  double nr = 0.0, fr = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double t1 = __ddiv_rn(sub(S.bmin[a], o[a]), d[a]);
-    double t2 = __ddiv_rn(sub(S.bmax[a], o[a]), d[a]);
-    double near = np_min(t1, t2), far = np_max(t1, t2);
-    near = isnan(near) ? -INFINITY : near;
-    far = isnan(far) ? INFINITY : far;
-    nr = (a == 0) ? near : np_max(nr, near);
-    fr = (a == 0) ? far : np_min(fr, far);
-  }
-  (void)nan;
-  t_in = fmax(nr, 0.0);
-  t_out = fr;
-  valid = t_out > t_in;
-}
 
 // mode 0: count misses; mode 1: write miss points + seeds; mode 2: final accumulation
 __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
@@ -338,89 +473,22 @@ int vc_cache_create(int dim, const double* bmin, const double* bmax, int n, cons
     if (!(bmax[a] > bmin[a])) return fail(VC_EINVAL, "bounds_max must exceed bounds_min");
   if (n < 0) return fail(VC_EINVAL, "negative record count");
   vc_cache* c = new vc_cache();
-  c->dim = dim;
-  c->n = n;
-  // root cube of the reference tree (src/cache.py:284-288)
-  double diag = 0.0, mx = 0.0;
-  for (int a = 0; a < dim; ++a) {
-    diag += (bmax[a] - bmin[a]) * (bmax[a] - bmin[a]);
-    mx = std::max(mx, bmax[a] - bmin[a]);
+  int rc = cache_init(c, dim, bmin, bmax);
+  if (!rc) rc = cache_reserve(c, (size_t)std::max(n, 1), 0);
+  if (!rc && n > 0) {
+    cudaError_t e = cudaMemcpy(c->d_rec, records, (size_t)n * record_size(dim) * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cache upload");
+    k_fill_tags<<<(n + 255) / 256, 256>>>(c->d_tag, n, -1LL);
+    c->n = n;
   }
-  diag = std::sqrt(diag);
-  double half = 0.5 * mx + 0.25 * diag;
-  for (int a = 0; a < dim; ++a) c->origin[a] = 0.5 * (bmin[a] + bmax[a]) - half;
-  c->size = 2.0 * half;
-  c->L0 = dim == 3 ? 7 : 10;
-  const int RS = record_size(dim);
-  // levels: N_ℓ = 2^(L0−ℓ) cells per axis
-  c->level_off.assign(c->L0 + 2, 0);
-  long long tot = 0;
-  for (int lv = 0; lv <= c->L0; ++lv) {
-    c->level_off[lv] = tot;
-    long long N = 1LL << (c->L0 - lv);
-    tot += (dim == 3) ? N * N * N : N * N;
+  if (!rc) rc = cache_rebuild(c, 0);
+  if (!rc) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = cuda_fail(e, "cache build");
   }
-  c->level_off[c->L0 + 1] = tot;
-  c->n_cells = tot;
-  std::vector<int> cnt(tot + 1, 0);
-  std::vector<std::pair<long long, int>> ins;  // (cell, record)
-  std::vector<int> overflow;
-  ins.reserve((size_t)n * (1 << dim));
-  for (int r = 0; r < n; ++r) {
-    const double* R = records + (size_t)r * RS;
-    const double* rad = R + dim + 3 + 3 * dim + dim * dim;
-    double br = 0.0;
-    for (int a = 0; a < dim; ++a) br = std::max(br, rad[a]);
-    br = br * (1.0 + 1e-9) + 1e-12 * c->size;
-    bool fits = std::isfinite(br);
-    double lo[3], hi[3];
-    for (int a = 0; a < dim; ++a) {
-      lo[a] = R[a] - br;
-      hi[a] = R[a] + br;
-      if (!(lo[a] >= c->origin[a] && hi[a] <= c->origin[a] + c->size)) fits = false;
-    }
-    if (!fits) {
-      overflow.push_back(r);
-      continue;
-    }
-    int lv = 0;
-    while (lv < c->L0 && c->size / (double)(1LL << (c->L0 - lv)) < 2.0 * br) ++lv;
-    long long N = 1LL << (c->L0 - lv);
-    double h = c->size / (double)N;
-    long long clo[3] = {0, 0, 0}, chi[3] = {0, 0, 0};
-    for (int a = 0; a < dim; ++a) {
-      clo[a] = std::min(std::max((long long)std::floor((lo[a] - c->origin[a]) / h), 0LL), N - 1);
-      chi[a] = std::min(std::max((long long)std::floor((hi[a] - c->origin[a]) / h), 0LL), N - 1);
-    }
-    for (long long z = (dim == 3 ? clo[2] : 0); z <= (dim == 3 ? chi[2] : 0); ++z)
-      for (long long y = clo[1]; y <= chi[1]; ++y)
-        for (long long x = clo[0]; x <= chi[0]; ++x) {
-          long long cell = (dim == 3) ? (z * N + y) * N + x : y * N + x;
-          ins.push_back({c->level_off[lv] + cell, r});
-          cnt[c->level_off[lv] + cell]++;
-        }
-  }
-  std::vector<int> start(tot + 1, 0);
-  for (long long i = 0; i < tot; ++i) start[i + 1] = start[i] + cnt[i];
-  std::vector<int> items(ins.size() + 1);
-  std::vector<int> fillp(start.begin(), start.end() - 1);
-  for (auto& p : ins) items[fillp[p.first]++] = p.second;  // records stay in insertion order
-  c->n_overflow = (int)overflow.size();
-  cudaError_t e = cudaSuccess;
-  auto up = [&](void** dst, const void* src, size_t bytes) {
-    if (e != cudaSuccess) return;
-    if (bytes == 0) bytes = 8;
-    e = cudaMalloc(dst, bytes);
-    if (e == cudaSuccess && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
-  };
-  up((void**)&c->d_level_off, c->level_off.data(), c->level_off.size() * 8);
-  up((void**)&c->d_cell_start, start.data(), start.size() * 4);
-  up((void**)&c->d_items, items.data(), items.size() * 4);
-  up((void**)&c->d_overflow, overflow.empty() ? nullptr : overflow.data(), overflow.size() * 4);
-  up((void**)&c->d_rec, n ? records : nullptr, (size_t)n * RS * 8);
-  if (e != cudaSuccess) {
+  if (rc) {
     delete c;
-    return cuda_fail(e, "cache upload");
+    return rc;
   }
   *out = c;
   return VC_OK;
@@ -479,43 +547,10 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
   cudaStream_t st = (cudaStream_t)stream;
   const vc_camera& C0 = *camp;
   DevCamera cam{};
-  // camera frame (src/renderer.py:158-170)
-  double f[3], r[3], u[3];
-  double fn = 0.0;
-  for (int a = 0; a < 3; ++a) {
-    f[a] = C0.look_at[a] - C0.position[a];
-    fn += f[a] * f[a];
-  }
-  fn = std::sqrt(fn);
-  if (fn == 0.0) return fail(VC_EINVAL, "camera look_at must differ from position");
-  for (int a = 0; a < 3; ++a) f[a] /= fn;
-  r[0] = f[1] * C0.up[2] - f[2] * C0.up[1];
-  r[1] = f[2] * C0.up[0] - f[0] * C0.up[2];
-  r[2] = f[0] * C0.up[1] - f[1] * C0.up[0];
-  double rn = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-  if (rn < 1e-9) return fail(VC_EINVAL, "camera up must not be parallel to the view direction");
-  for (int a = 0; a < 3; ++a) r[a] /= rn;
-  u[0] = r[1] * f[2] - r[2] * f[1];
-  u[1] = r[2] * f[0] - r[0] * f[2];
-  u[2] = r[0] * f[1] - r[1] * f[0];
-  for (int a = 0; a < 3; ++a) {
-    cam.pos[a] = C0.position[a];
-    cam.fwd[a] = f[a];
-    cam.right[a] = r[a];
-    cam.up[a] = u[a];
-  }
-  cam.tan_half = std::tan(C0.fov_degrees * (3.141592653589793 / 180.0) * 0.5);
-  cam.aspect = (double)C0.width / (double)C0.height;
-  cam.w = C0.width;
-  cam.h = C0.height;
-  cam.row0 = C0.row0;
-  cam.rows = C0.rows > 0 ? C0.rows : C0.height - C0.row0;
-  cam.col0 = C0.col0;
-  cam.cols = C0.cols > 0 ? C0.cols : C0.width - C0.col0;
-  if (cam.row0 < 0 || cam.col0 < 0 || cam.row0 + cam.rows > cam.h || cam.col0 + cam.cols > cam.w)
-    return fail(VC_EINVAL, "crop outside the image");
+  int rc = make_dev_camera(*camp, &cam);
+  if (rc) return rc;
   const int npx = cam.rows * cam.cols;
-  int rc = ensure_emitters(sc, rp->n_light_samples);
+  rc = ensure_emitters(sc, rp->n_light_samples);
   if (rc) return rc;
   DevScene S = dev_scene(sc);
   cudaError_t e = cudaSuccess;

@@ -1,0 +1,252 @@
+// Record cache on device: handle type, device view and the support / blend routines
+// shared by the lookup, the camera march and the populate engine.
+//
+// Index: the reference keeps records in an MX-CIF tree whose point query returns
+// exactly the records with support > 0 (src/cache.py:262-334, ≡ linear scan).  Here a
+// record of bounding radius r lives on the coarsest-needed level ℓ of a pyramid of
+// dense grids over the same padded root cube (cell size h_ℓ ≥ 2r, so its box touches
+// ≤ 2^d cells); a query visits one cell per level plus the overflow list of records
+// whose box leaves the root cube, and applies the reference's strict support test —
+// the covering set is identical to the linear scan.  The index is rebuilt on the
+// device (counting pass → scan → stable radix sort by cell) after every insert batch.
+//
+// Every record carries a tag (the ordinal of the march point that created it, or −1):
+// a query with limit t sees only records with tag < t, which is how the populate
+// engine evaluates "the cache as it was when point t was reached" after records of
+// later points have been appended speculatively.
+#pragma once
+
+#include <climits>
+#include <vector>
+
+#include "vc_api_internal.h"
+#include "vc_device.cuh"
+
+namespace vc {
+
+struct DevCache {
+  int dim, n, L0, n_overflow;
+  double origin[3];
+  double size;
+  const long long* level_off;  // L0+2 entries: first cell index of each level
+  const int* cell_start;       // per cell start into items (+1 sentinel)
+  const int* items;
+  const int* overflow;
+  const double* rec;           // n × record_size(dim), reference layout
+  const long long* tag;        // n creation ordinals
+};
+
+}  // namespace vc
+
+struct vc_cache {
+  int dim = 0, n = 0, L0 = 0;
+  double origin[3] = {0, 0, 0}, size = 0.0;
+  long long n_cells = 0;
+  std::vector<long long> level_off;
+  long long* d_level_off = nullptr;
+  int* d_cell_start = nullptr;
+  int* d_items = nullptr;
+  size_t items_cap = 0;
+  int* d_overflow = nullptr;
+  int n_overflow = 0;
+  double* d_rec = nullptr;
+  long long* d_tag = nullptr;
+  size_t rec_cap = 0;  // records
+  vc::Workspace ws;    // index-build scratch
+  vc::DevCache dev() const {
+    vc::DevCache c{};
+    c.dim = dim;
+    c.n = n;
+    c.L0 = L0;
+    c.n_overflow = n_overflow;
+    for (int a = 0; a < 3; ++a) c.origin[a] = origin[a];
+    c.size = size;
+    c.level_off = d_level_off;
+    c.cell_start = d_cell_start;
+    c.items = d_items;
+    c.overflow = d_overflow;
+    c.rec = d_rec;
+    c.tag = d_tag;
+    return c;
+  }
+  ~vc_cache() {
+    cudaFree(d_level_off);
+    cudaFree(d_cell_start);
+    cudaFree(d_items);
+    cudaFree(d_overflow);
+    cudaFree(d_rec);
+    cudaFree(d_tag);
+  }
+};
+
+namespace vc {
+
+// ---------------------------------------------------------------------------
+// Camera rays and medium span (src/renderer.py:133-193, :382-394)
+// ---------------------------------------------------------------------------
+
+struct DevCamera {
+  double pos[3], fwd[3], right[3], up[3];
+  double tan_half, aspect;
+  int w, h, row0, rows, col0, cols;
+};
+
+__device__ inline void camera_ray(const DevCamera& cam, int px, int py, double jx, double jy, double* o, double* d) {
+  double u = __ddiv_rn(add((double)px, jx), (double)cam.w);
+  double v = __ddiv_rn(add((double)py, jy), (double)cam.h);
+  double xn = mul(mul(sub(mul(2.0, u), 1.0), cam.tan_half), cam.aspect);
+  double yn = mul(sub(1.0, mul(2.0, v)), cam.tan_half);
+  double nn = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    d[a] = add(add(cam.fwd[a], mul(xn, cam.right[a])), mul(yn, cam.up[a]));
+    nn = add(nn, mul(d[a], d[a]));
+  }
+  nn = sqrt(nn);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    d[a] = __ddiv_rn(d[a], nn);
+    o[a] = cam.pos[a];
+  }
+}
+
+__device__ inline void bounds_span(const DevScene& S, const double* o, const double* d, double& t_in,
+                                   double& t_out, bool& valid) {
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  double nr = 0.0, fr = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double t1 = __ddiv_rn(sub(S.bmin[a], o[a]), d[a]);
+    double t2 = __ddiv_rn(sub(S.bmax[a], o[a]), d[a]);
+    double near = np_min(t1, t2), far = np_max(t1, t2);
+    near = isnan(near) ? -INFINITY : near;
+    far = isnan(far) ? INFINITY : far;
+    nr = (a == 0) ? near : np_max(nr, near);
+    fr = (a == 0) ? far : np_min(fr, far);
+  }
+  (void)nan;
+  t_in = fmax(nr, 0.0);
+  t_out = fr;
+  valid = t_out > t_in;
+}
+
+// Host-side cache management (vc_cache.cu).
+int make_dev_camera(const vc_camera& cam, DevCamera* out);
+int cache_init(vc_cache* c, int dim, const double* bmin, const double* bmax);
+int cache_reserve(vc_cache* c, size_t n_records, cudaStream_t st);
+// Append k record rows gathered from src (row j = src + sel[j]·stride doubles) with tags.
+int cache_append(vc_cache* c, const double* src, size_t stride, const int* d_sel, const long long* d_tags,
+                 int k, cudaStream_t st);
+int cache_truncate(vc_cache* c, int n, cudaStream_t st);
+int cache_rebuild(vc_cache* c, cudaStream_t st);
+
+// support coordinate 1 − ‖(Δ·A)/r‖ (src/cache.py:112-116)
+template <int D>
+__device__ __forceinline__ double record_support(const double* R, const double* x, double* dl) {
+  const double* pos = R;
+  const double* ax = R + D + 3 + 3 * D;
+  const double* rad = R + D + 3 + 3 * D + D * D;
+#pragma unroll
+  for (int a = 0; a < D; ++a) dl[a] = sub(x[a], pos[a]);
+  double q = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double al = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) al = add(al, mul(dl[i], ax[i * D + j]));
+    double t = __ddiv_rn(al, rad[j]);
+    q = add(q, mul(t, t));
+  }
+  return sub(1.0, sqrt(q));
+}
+
+// Cubic weight of a support coordinate (src/cache.py:49-56).
+__device__ __forceinline__ double support_weight(double sup) {
+  double d = fmin(fmax(sup, 0.0), 1.0);
+  return sub(mul(mul(3.0, d), d), mul(mul(mul(2.0, d), d), d));
+}
+
+// support coordinate, first-order estimate, cubic weight (src/cache.py:49-56, :112-121)
+template <int D>
+__device__ __forceinline__ void blend_record(const double* R, const double* x, double num[3], double& den,
+                                             int& hits) {
+  const double* val = R + D;
+  const double* grd = R + D + 3;
+  double dl[D];
+  double sup = record_support<D>(R, x, dl);
+  if (!(sup > 0.0)) return;
+  ++hits;
+  double w = support_weight(sup);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double e = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) e = add(e, mul(grd[c * D + i], dl[i]));
+    e = add(val[c], e);
+    e = fmax(e, 0.0);
+    num[c] = add(num[c], mul(w, e));
+  }
+  den = add(den, w);
+}
+
+// Visit the candidate records of x in tree order (root level first, then the overflow
+// list); f(record_index) returns true to stop early.
+template <int D, typename F>
+__device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, F&& f) {
+  for (int lv = C.L0; lv >= 0; --lv) {  // coarse → fine (tree order: root first)
+    const int N = 1 << (C.L0 - lv);
+    const double h = C.size / N;
+    long long cell = 0;
+    bool inside = true;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      double fl = floor((x[a] - C.origin[a]) / h);
+      if (!(fl >= 0.0 && fl < (double)N)) inside = false;
+      cell = cell * N + (inside ? (long long)fl : 0);
+    }
+    if (!inside) continue;
+    long long ci = C.level_off[lv] + cell;
+    int b = C.cell_start[ci], e = C.cell_start[ci + 1];
+    for (int t = b; t < e; ++t)
+      if (f(C.items[t])) return;
+  }
+  for (int t = 0; t < C.n_overflow; ++t)
+    if (f(C.overflow[t])) return;
+}
+
+// Blended J over records with tag < limit; false when none covers x (src/cache.py:342-360).
+template <int D>
+__device__ inline bool cache_interpolate(const DevCache& C, const double* x, double J[3], int* count,
+                                         long long limit = LLONG_MAX) {
+  double num[3] = {0.0, 0.0, 0.0}, den = 0.0;
+  int hits = 0;
+  const int RS = record_size(D);
+  cache_visit<D>(C, x, [&](int r) {
+    if (C.tag[r] < limit) blend_record<D>(C.rec + (size_t)r * RS, x, num, den, hits);
+    return false;
+  });
+  if (count) *count = hits;
+  if (hits == 0 || !(den > 0.0)) return false;
+  J[0] = __ddiv_rn(num[0], den);
+  J[1] = __ddiv_rn(num[1], den);
+  J[2] = __ddiv_rn(num[2], den);
+  return true;
+}
+
+// interpolate(cache, x) is not None ⇔ some record with tag < limit has support > 0 and
+// a positive weight (the blend denominator is a sum of non-negative weights).
+template <int D>
+__device__ inline bool cache_covers(const DevCache& C, const double* x, long long limit) {
+  const int RS = record_size(D);
+  bool hit = false;
+  cache_visit<D>(C, x, [&](int r) {
+    if (C.tag[r] >= limit) return false;
+    double dl[D];
+    double sup = record_support<D>(C.rec + (size_t)r * RS, x, dl);
+    hit = sup > 0.0 && support_weight(sup) > 0.0;
+    return hit;
+  });
+  return hit;
+}
+
+}  // namespace vc

@@ -17,7 +17,10 @@ namespace vc {
 
 constexpr int kMaxDim = 3;
 constexpr int kBvhMaxDepth = 32;  // BVH depth cap = device traversal stack size
-constexpr int kAsmSplit = 4;      // CTAs per record in the moment assembly
+#ifndef VC_ASM_SPLIT
+#define VC_ASM_SPLIT 8
+#endif
+constexpr int kAsmSplit = VC_ASM_SPLIT;  // CTAs per record in the moment assembly
 
 // A BVH over a primitive set: float32 nodes, float64 primitives in leaf order.
 struct DevBvh {

@@ -1,0 +1,875 @@
+// Cache pre-population on the device: populate_cache (src/renderer.py:282-327).
+//
+// The reference marches view points in scanline order and, at each point whose
+// single or multiple cache lacks coverage, builds a record pair and inserts it
+// (which = per-cache miss).  That greedy loop is sequential: whether point t needs a
+// record depends on every record inserted before t.  This engine reproduces it
+// exactly with speculative windows:
+//
+//   1. cover   — the next L points (the lookahead) are tested against the committed
+//                caches; the uncovered ones form U (ordered).
+//   2. select  — a speculative build set: the first point of U, every point that
+//                already has a pooled build, and the first point of U in each cell of
+//                a grid of predicted record size (first C by ordinal).
+//   3. build   — record pairs for the new selections (one record-build wave).
+//   4. resolve — the sequential rule among the built points, by one warp over C×C
+//                coverage bitsets: built point e takes a record in cache c iff it was
+//                uncovered in c and no earlier accepted record of c covers it.
+//   5. stop    — accepted records are appended (tag = ordinal) and indexed; the first
+//                point of U that was not built but is still uncovered by records of
+//                smaller ordinal is the stop point.  Decisions before it are final;
+//                records with larger tags are rolled back and their builds pooled.
+//
+// Every decision uses the reference's coverage predicate on the exact record set the
+// sequential loop would have seen, so the committed caches equal the reference's
+// (record for record, in insertion order).  Misprediction costs only time: a stop
+// ends the window early, an unneeded speculative build is discarded.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "vc_build.h"
+#include "vc_cache.cuh"
+
+namespace vc {
+
+// Ordered march-point stream (src/renderer.py:282-299).
+struct MarchStream {
+  int kind;  // 0: FieldGrid cell centers, 1: camera march
+  int nx, ny;
+  double fmin[2], fmax[2];
+  double pos[3];             // camera origin
+  const double* ray;         // per pixel: d.xyz, t_in
+  const long long* first;    // per pixel: first point ordinal (n_rays + 1 entries)
+  int n_rays;
+  double step;
+};
+
+template <int D>
+__device__ inline void stream_point(const MarchStream& S, long long ord, double* x) {
+  if (S.kind == 0) {  // FieldGrid.cell_center (src/renderer.py:112-121)
+    const int iy = (int)(ord / S.nx), ix = (int)(ord % S.nx);
+    const double dx = __ddiv_rn(sub(S.fmax[0], S.fmin[0]), (double)S.nx);
+    const double dy = __ddiv_rn(sub(S.fmax[1], S.fmin[1]), (double)S.ny);
+    x[0] = add(S.fmin[0], mul(add((double)ix, 0.5), dx));
+    x[1] = sub(S.fmax[1], mul(add((double)iy, 0.5), dy));
+    return;
+  }
+  int lo = 0, hi = S.n_rays;  // first[lo] ≤ ord < first[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (S.first[mid] <= ord) lo = mid;
+    else hi = mid;
+  }
+  const double* R = S.ray + (size_t)lo * 4;
+  const long long k = ord - S.first[lo] + 1;
+  const double t = add(R[3], mul((double)k - 0.5, S.step));
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a] = add(S.pos[a], mul(t, R[a]));
+}
+
+// Pixel-center rays, first hit and medium span → march steps (src/renderer.py:290-299).
+__global__ void k_pop_rays(DevScene S, DevCamera cam, double step, double* ray, long long* steps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cam.w * cam.h) return;
+  const int py = i / cam.w, px = i % cam.w;
+  double o[3], d[3];
+  camera_ray(cam, px, py, 0.5, 0.5, o, d);
+  double ts;
+  int id;
+  trace_closest<3>(S, o, d, ts, id);
+  double t_in, t_out;
+  bool valid;
+  bounds_span(S, o, d, t_in, t_out, valid);
+  long long n = 0;
+  if (valid) {
+    double t_end = fmin(ts, t_out);
+    if (isnan(ts)) t_end = ts;
+    double f = floor(__ddiv_rn(sub(t_end, t_in), step) + 0.5);
+    if (f > 0.0) n = (long long)f;
+  }
+  ray[(size_t)i * 4 + 0] = d[0];
+  ray[(size_t)i * 4 + 1] = d[1];
+  ray[(size_t)i * 4 + 2] = d[2];
+  ray[(size_t)i * 4 + 3] = t_in;
+  steps[i] = n;
+}
+
+// 1. points [pos, pos+L) and their per-cache miss bits against records of smaller tag
+template <int D>
+__global__ void k_pop_cover(MarchStream M, DevCache Cs, DevCache Cm, long long pos, int L, double* X,
+                            unsigned char* need) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= L) return;
+  const long long ord = pos + j;
+  double x[3];
+  stream_point<D>(M, ord, x);
+#pragma unroll
+  for (int a = 0; a < D; ++a) X[(size_t)j * D + a] = x[a];
+  const bool cs = cache_covers<D>(Cs, x, ord);
+  const bool cm = cache_covers<D>(Cm, x, ord);
+  need[j] = (unsigned char)((cs ? 0 : 1) | (cm ? 0 : 2));
+}
+
+__global__ void k_pop_iota(int* v, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+// 2. selection: cell key per uncovered point
+template <int D>
+__global__ void k_pop_keys(const double* X, const int* U, int nu, double o0, double o1, double o2, double inv_h,
+                           unsigned long long* keys, int* vals) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nu) return;
+  const double* x = X + (size_t)U[p] * D;
+  const double o[3] = {o0, o1, o2};
+  unsigned long long k = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double f = floor((x[a] - o[a]) * inv_h);
+    long long c = (long long)fmin(fmax(f, 0.0), 2097151.0);
+    k |= (unsigned long long)c << (21 * a);
+  }
+  keys[p] = k;
+  vals[p] = p;
+}
+
+__global__ void k_pop_first(const unsigned long long* keys, const int* vals, int nu, unsigned char* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nu) return;
+  if (i == 0 || keys[i] != keys[i - 1]) flag[vals[i]] = 1;
+}
+
+// pooled builds (sorted ordinals) are always selected while uncovered
+__global__ void k_pop_pooled(const int* U, int nu, long long pos, const long long* pool, int np,
+                             unsigned char* flag) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nu) return;
+  if (p == 0) flag[0] = 1;
+  if (np == 0) return;
+  const long long ord = pos + U[p];
+  int lo = 0, hi = np;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (pool[mid] < ord) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < np && pool[lo] == ord) flag[p] = 1;
+}
+
+// selected U positions → lookahead indices j
+__global__ void k_pop_sel_j(const int* sel_p, const int* U, int E, int* sel_j, unsigned char* built) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  sel_j[e] = U[sel_p[e]];
+  built[sel_p[e]] = 1;
+}
+
+template <int D>
+__global__ void k_pop_gather_x(const double* X, const int* js, int n, double* out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+#pragma unroll
+  for (int a = 0; a < D; ++a) out[(size_t)e * D + a] = X[(size_t)js[e] * D + a];
+}
+
+// new record pairs (2·RS doubles each) → window slots
+__global__ void k_pop_scatter(const double* src, int n, const int* slot, int RS2, double* WR) {
+  const int e = blockIdx.y;
+  if (e >= n) return;
+  for (int t = threadIdx.x; t < RS2; t += blockDim.x) WR[(size_t)slot[e] * RS2 + t] = src[(size_t)e * RS2 + t];
+}
+
+// 4a. coverage bits: bit b of word (c, e, w) = record c of built point b (b < e) covers x_e
+template <int D>
+__global__ void k_pop_bits(const double* WR, const int* slot, const int* sel_j, const double* X, int E, int W,
+                           unsigned long long* bits) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2LL * E * W) return;
+  const int c = (int)(t / ((long long)E * W));
+  const int rem = (int)(t % ((long long)E * W));
+  const int e = rem / W, w = rem % W;
+  const int RS = record_size(D);
+  double x[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a] = X[(size_t)sel_j[e] * D + a];
+  unsigned long long word = 0;
+  const int b1 = min(w * 64 + 64, e);
+  for (int b = w * 64; b < b1; ++b) {
+    const double* R = WR + (size_t)slot[b] * 2 * RS + (size_t)c * RS;
+    double dl[D];
+    double sup = record_support<D>(R, x, dl);
+    if (sup > 0.0 && support_weight(sup) > 0.0) word |= 1ULL << (b - w * 64);
+  }
+  bits[((size_t)c * E + e) * W + w] = word;
+}
+
+// 4b. sequential acceptance among the built points (one warp; E ≤ 2048)
+__global__ void k_pop_resolve(const unsigned long long* bits, const unsigned char* need, const int* sel_j, int E,
+                              int W, unsigned char* acc) {
+  const int lane = threadIdx.x;
+  unsigned long long as = 0, am = 0;
+  for (int e = 0; e < E; ++e) {
+    unsigned long long bs = 0, bm = 0;
+    if (lane < W) {
+      bs = bits[(size_t)e * W + lane] & as;
+      bm = bits[((size_t)E + e) * W + lane] & am;
+    }
+    const bool cov_s = __any_sync(0xffffffffu, bs != 0);
+    const bool cov_m = __any_sync(0xffffffffu, bm != 0);
+    const int nd = need[sel_j[e]];
+    const bool a_s = (nd & 1) && !cov_s;
+    const bool a_m = (nd & 2) && !cov_m;
+    if (lane == (e >> 6)) {
+      if (a_s) as |= 1ULL << (e & 63);
+      if (a_m) am |= 1ULL << (e & 63);
+    }
+    if (lane == 0) acc[e] = (unsigned char)((a_s ? 1 : 0) | (a_m ? 2 : 0));
+  }
+}
+
+// 5. first uncovered point of U that was not built, against records of smaller tag
+template <int D>
+__global__ void k_pop_stop(MarchStream M, DevCache Cs, DevCache Cm, const double* X, const int* U, int nu,
+                           const unsigned char* need, const unsigned char* built, long long pos,
+                           unsigned long long* stop) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nu || built[p]) return;
+  const int j = U[p];
+  const long long ord = pos + j;
+  if ((unsigned long long)ord >= *stop) return;
+  double x[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a] = X[(size_t)j * D + a];
+  const int nd = need[j];
+  const bool ms = (nd & 1) && !cache_covers<D>(Cs, x, ord);
+  const bool mm = !ms && (nd & 2) && !cache_covers<D>(Cm, x, ord);
+  if (ms || mm) atomicMin(stop, (unsigned long long)ord);
+}
+
+struct PopBuffers {
+  Workspace ws;
+};
+
+}  // namespace vc
+
+using namespace vc;
+
+namespace {
+
+struct Engine {
+  vc_scene* sc;
+  vc_cache* cs;
+  vc_cache* cm;
+  MarchStream M{};
+  long long N = 0;
+  int D = 0;
+  vc_build_params bp{};
+  uint32_t seed = 0;
+  int seed_kind = 0;  // 0: populate (seed, 401, i); 1: field render (seed, 307, iy, ix)
+  cudaStream_t st = nullptr;
+  Workspace ws;
+  int C = 2048;
+  long long L = 65536, Lmax = 1LL << 24;
+  double kappa = 1.0, h_sel = INFINITY;
+  int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaError_t e = cudaSuccess;
+
+  void* get(int slot, size_t bytes) { return ws.get(slot, bytes, &e); }
+
+  int run();
+};
+
+int Engine::run() {
+  const int RS = record_size(D);
+  const int RS2 = 2 * RS;
+  // window record slots: ≤ C selections + ≤ C pooled builds
+  const int n_slots = 2 * C;
+  double* WR = (double*)get(0, (size_t)n_slots * RS2 * 8);
+  std::vector<int> free_slots;
+  for (int s = n_slots - 1; s >= 0; --s) free_slots.push_back(s);
+  std::map<long long, int> pool;  // ordinal → slot (built, not yet resolved)
+  long long pos = 0;
+  std::vector<double> hrec;
+  while (pos < N) {
+    const int Lw = (int)std::min<long long>(L, N - pos);
+    double* X = (double*)get(1, (size_t)Lw * D * 8);
+    unsigned char* need = (unsigned char*)get(2, (size_t)Lw);
+    int* iota = (int*)get(3, (size_t)Lw * 4);
+    int* U = (int*)get(4, (size_t)Lw * 4);
+    int* cnt = (int*)get(5, 64);
+    if (e != cudaSuccess) return cuda_fail(e, "populate lookahead buffers");
+    const DevCache Cs = cs->dev(), Cm = cm->dev();
+    const int nb = (Lw + 127) / 128;
+    if (D == 2) k_pop_cover<2><<<nb, 128, 0, st>>>(M, Cs, Cm, pos, Lw, X, need);
+    else k_pop_cover<3><<<nb, 128, 0, st>>>(M, Cs, Cm, pos, Lw, X, need);
+    k_pop_iota<<<nb, 128, 0, st>>>(iota, Lw);
+    size_t tb = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb, iota, need, U, cnt, Lw, st);
+    void* tmp = get(6, tb);
+    if (e != cudaSuccess) return cuda_fail(e, "populate select scratch");
+    cub::DeviceSelect::Flagged(tmp, tb, iota, need, U, cnt, Lw, st);
+    int nu = 0;
+    e = cudaMemcpyAsync(&nu, cnt, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "populate cover");
+    count_launches(4);
+    stats[3] += 1;
+    if (nu == 0) {  // lookahead fully covered
+      for (auto it = pool.begin(); it != pool.end() && it->first < pos + Lw;) {
+        free_slots.push_back(it->second);
+        it = pool.erase(it);
+      }
+      pos += Lw;
+      L = std::min(Lmax, L * 2);
+      continue;
+    }
+    // 2. selection
+    unsigned char* flag = (unsigned char*)get(7, (size_t)nu);
+    unsigned char* built = (unsigned char*)get(8, (size_t)nu);
+    long long* dpool = (long long*)get(9, (pool.size() + 1) * 8);
+    if (e != cudaSuccess) return cuda_fail(e, "populate selection buffers");
+    e = cudaMemsetAsync(flag, 0, nu, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(built, 0, nu, st);
+    std::vector<long long> hpool;
+    for (auto& kv : pool) hpool.push_back(kv.first);
+    if (e == cudaSuccess && !hpool.empty())
+      e = cudaMemcpyAsync(dpool, hpool.data(), hpool.size() * 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "populate selection");
+    const int nbu = (nu + 127) / 128;
+    if (std::isfinite(h_sel) && h_sel > 0.0) {
+      unsigned long long* keys = (unsigned long long*)get(10, (size_t)nu * 8);
+      unsigned long long* keys2 = (unsigned long long*)get(11, (size_t)nu * 8);
+      int* vals = (int*)get(12, (size_t)nu * 4);
+      int* vals2 = (int*)get(13, (size_t)nu * 4);
+      if (e != cudaSuccess) return cuda_fail(e, "populate key buffers");
+      const double inv_h = 1.0 / h_sel;
+      if (D == 2) k_pop_keys<2><<<nbu, 128, 0, st>>>(X, U, nu, sc->bmin[0], sc->bmin[1], 0.0, inv_h, keys, vals);
+      else k_pop_keys<3><<<nbu, 128, 0, st>>>(X, U, nu, sc->bmin[0], sc->bmin[1], sc->bmin[2], inv_h, keys, vals);
+      size_t rb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, vals2, nu, 0, 21 * D, st);
+      void* rtmp = get(14, rb);
+      if (e != cudaSuccess) return cuda_fail(e, "populate sort scratch");
+      cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, vals2, nu, 0, 21 * D, st);
+      k_pop_first<<<nbu, 128, 0, st>>>(keys2, vals2, nu, flag);
+      count_launches(3);
+    }
+    k_pop_pooled<<<nbu, 128, 0, st>>>(U, nu, pos, dpool, (int)hpool.size(), flag);
+    int* iota_u = (int*)get(15, (size_t)nu * 4);
+    int* sel_p = (int*)get(16, (size_t)nu * 4);
+    if (e != cudaSuccess) return cuda_fail(e, "populate selection buffers");
+    k_pop_iota<<<nbu, 128, 0, st>>>(iota_u, nu);
+    size_t tb2 = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb2, iota_u, flag, sel_p, cnt + 1, nu, st);
+    void* tmp2 = get(17, tb2);
+    if (e != cudaSuccess) return cuda_fail(e, "populate select scratch");
+    cub::DeviceSelect::Flagged(tmp2, tb2, iota_u, flag, sel_p, cnt + 1, nu, st);
+    int ns = 0;
+    e = cudaMemcpyAsync(&ns, cnt + 1, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "populate selection count");
+    count_launches(3);
+    const int E = std::min(ns, C);
+    int* sel_j = (int*)get(18, (size_t)E * 4);
+    if (e != cudaSuccess) return cuda_fail(e, "populate selection list");
+    k_pop_sel_j<<<(E + 127) / 128, 128, 0, st>>>(sel_p, U, E, sel_j, built);
+    std::vector<int> hj(E);
+    e = cudaMemcpyAsync(hj.data(), sel_j, (size_t)E * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "populate selection download");
+    count_launches(1);
+    // 3. build the new selections
+    std::vector<int> slot(E), new_e, new_slot;
+    std::vector<long long> sel_ords(E);
+    for (int q = 0; q < E; ++q) sel_ords[q] = pos + hj[q];  // ascending
+    for (int q = 0; q < E; ++q) {
+      const long long ord = sel_ords[q];
+      auto it = pool.find(ord);
+      if (it != pool.end()) {
+        slot[q] = it->second;
+      } else {
+        if (free_slots.empty()) {  // evict the furthest pooled build not selected here
+          auto victim = pool.end();
+          for (auto r = pool.rbegin(); r != pool.rend(); ++r)
+            if (!std::binary_search(sel_ords.begin(), sel_ords.end(), r->first)) {
+              victim = std::next(r).base();
+              break;
+            }
+          if (victim == pool.end()) return fail(VC_ENOMEM, "populate window slots exhausted");
+          free_slots.push_back(victim->second);
+          pool.erase(victim);
+        }
+        slot[q] = free_slots.back();
+        free_slots.pop_back();
+        new_e.push_back(q);
+        new_slot.push_back(slot[q]);
+      }
+    }
+    const int nn = (int)new_e.size();
+    int* dslot = (int*)get(19, (size_t)E * 4);
+    if (e != cudaSuccess) return cuda_fail(e, "populate slots");
+    e = cudaMemcpyAsync(dslot, slot.data(), (size_t)E * 4, cudaMemcpyHostToDevice, st);
+    if (nn > 0) {
+      std::vector<int> js(nn);
+      const int nw = bp.seed_words;
+      std::vector<uint32_t> words((size_t)nn * nw);
+      for (int i = 0; i < nn; ++i) {
+        js[i] = hj[new_e[i]];
+        const long long ord = pos + js[i];
+        uint32_t* w = words.data() + (size_t)i * nw;
+        w[0] = seed;
+        if (seed_kind == 0) {  // SeedSequence([seed, 401, i]) (src/renderer.py:317)
+          w[1] = 401u;
+          w[2] = (uint32_t)(ord & 0xffffffffLL);
+        } else {  // SeedSequence([seed, 307, iy, ix]) (src/renderer.py:432-434)
+          w[1] = 307u;
+          w[2] = (uint32_t)(ord / M.nx);
+          w[3] = (uint32_t)(ord % M.nx);
+        }
+      }
+      int* djs = (int*)get(20, (size_t)nn * 4);
+      int* dns = (int*)get(21, (size_t)nn * 4);
+      double* xb = (double*)get(22, (size_t)nn * D * 8);
+      uint32_t* dw = (uint32_t*)get(23, (size_t)nn * 16);
+      double* rec = (double*)get(24, (size_t)nn * RS2 * 8);
+      double* mom = (double*)get(25, (size_t)nn * 2 * moment_size(D) * 8);
+      long long* bst = (long long*)get(26, (size_t)nn * kStats * 8);
+      if (e != cudaSuccess) return cuda_fail(e, "populate build buffers");
+      e = cudaMemcpyAsync(djs, js.data(), (size_t)nn * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dns, new_slot.data(), (size_t)nn * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dw, words.data(), words.size() * 4, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate build upload");
+      if (D == 2) k_pop_gather_x<2><<<(nn + 127) / 128, 128, 0, st>>>(X, djs, nn, xb);
+      else k_pop_gather_x<3><<<(nn + 127) / 128, 128, 0, st>>>(X, djs, nn, xb);
+      count_launches(1);
+      int rc = build_impl(sc, nn, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
+      if (rc) return rc;
+      k_pop_scatter<<<dim3(1, nn), 64, 0, st>>>(rec, nn, dns, RS2, WR);
+      count_launches(1);
+      if (D == 3) {
+        std::vector<long long> hs((size_t)nn * kStats);
+        e = cudaMemcpyAsync(hs.data(), bst, hs.size() * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "populate build");
+        for (int i = 0; i < nn; ++i)
+          if (hs[(size_t)i * kStats + 5] != 0)
+            return fail(VC_ETRI, "spherical Delaunay triangulation failed at march point " +
+                                     std::to_string(pos + js[i]));
+      }
+      stats[4] += nn;
+    }
+    // 4. sequential acceptance among the built points
+    const int W = (E + 63) / 64;
+    unsigned long long* bits = (unsigned long long*)get(27, (size_t)2 * E * W * 8);
+    unsigned char* acc = (unsigned char*)get(28, (size_t)E);
+    if (e != cudaSuccess) return cuda_fail(e, "populate resolve buffers");
+    {
+      const long long nt = 2LL * E * W;
+      if (D == 2) k_pop_bits<2><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, sel_j, X, E, W, bits);
+      else k_pop_bits<3><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, sel_j, X, E, W, bits);
+    }
+    k_pop_resolve<<<1, 32, 0, st>>>(bits, need, sel_j, E, W, acc);
+    count_launches(2);
+    std::vector<unsigned char> hacc(E);
+    e = cudaMemcpyAsync(hacc.data(), acc, E, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "populate resolve");
+    // tentative commit: accepted rows (row = 2·slot + cache) with tag = ordinal
+    const int n0s = cs->n, n0m = cm->n;
+    std::vector<int> rows_s, rows_m;
+    std::vector<long long> tags_s, tags_m;
+    for (int q = 0; q < E; ++q) {
+      const long long ord = pos + hj[q];
+      if (hacc[q] & 1) {
+        rows_s.push_back(2 * slot[q]);
+        tags_s.push_back(ord);
+      }
+      if (hacc[q] & 2) {
+        rows_m.push_back(2 * slot[q] + 1);
+        tags_m.push_back(ord);
+      }
+    }
+    auto append = [&](vc_cache* c, const std::vector<int>& rows, const std::vector<long long>& tags, int s0) -> int {
+      if (rows.empty()) return VC_OK;
+      int* dr = (int*)get(s0, rows.size() * 4);
+      long long* dt = (long long*)get(s0 + 1, tags.size() * 8);
+      if (e != cudaSuccess) return cuda_fail(e, "populate append buffers");
+      e = cudaMemcpyAsync(dr, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dt, tags.data(), tags.size() * 8, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate append upload");
+      int rc = cache_append(c, WR, RS, dr, dt, (int)rows.size(), st);
+      if (rc) return rc;
+      return cache_rebuild(c, st);
+    };
+    int rc = append(cs, rows_s, tags_s, 29);
+    if (!rc) rc = append(cm, rows_m, tags_m, 31);
+    if (rc) return rc;
+    // 5. stop point
+    unsigned long long* dstop = (unsigned long long*)get(33, 8);
+    if (e != cudaSuccess) return cuda_fail(e, "populate stop buffer");
+    unsigned long long hstop = (unsigned long long)(pos + Lw);
+    e = cudaMemcpyAsync(dstop, &hstop, 8, cudaMemcpyHostToDevice, st);
+    {
+      const DevCache Cs2 = cs->dev(), Cm2 = cm->dev();
+      if (D == 2) k_pop_stop<2><<<nbu, 128, 0, st>>>(M, Cs2, Cm2, X, U, nu, need, built, pos, dstop);
+      else k_pop_stop<3><<<nbu, 128, 0, st>>>(M, Cs2, Cm2, X, U, nu, need, built, pos, dstop);
+    }
+    count_launches(1);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hstop, dstop, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "populate stop");
+    const long long stop = (long long)hstop;
+    // roll back records of ordinal > stop; pool their builds
+    int keep_s = 0, keep_m = 0, committed = 0, covered = 0;
+    bool beyond = false;
+    for (int q = 0; q < E; ++q) {
+      const long long ord = pos + hj[q];
+      if (ord < stop) {
+        keep_s += (hacc[q] & 1) ? 1 : 0;
+        keep_m += (hacc[q] & 2) ? 1 : 0;
+        if (hacc[q]) {
+          ++committed;
+          ++stats[7];
+        }
+        else ++covered;
+      } else {
+        beyond = true;
+      }
+    }
+    if (keep_s < (int)rows_s.size()) {
+      cache_truncate(cs, n0s + keep_s, st);
+      rc = cache_rebuild(cs, st);
+      if (rc) return rc;
+    }
+    if (keep_m < (int)rows_m.size()) {
+      cache_truncate(cm, n0m + keep_m, st);
+      rc = cache_rebuild(cm, st);
+      if (rc) return rc;
+    }
+    // radii of the committed records → next selection cell size
+    hrec.resize((size_t)n_slots * RS2);
+    std::vector<double> rmin;
+    {
+      std::vector<int> need_rows;
+      for (int q = 0; q < E; ++q)
+        if (pos + hj[q] < stop && hacc[q]) need_rows.push_back(q);
+      e = cudaMemcpyAsync(hrec.data(), WR, hrec.size() * 8, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate radii");
+      for (int q : need_rows)
+        for (int c = 0; c < 2; ++c) {
+          if (!(hacc[q] & (1 << c))) continue;
+          const double* rad = hrec.data() + (size_t)slot[q] * RS2 + (size_t)c * RS + D + 3 + 3 * D + D * D;
+          double r = rad[0];
+          for (int a = 1; a < D; ++a) r = std::min(r, rad[a]);
+          if (std::isfinite(r) && r > 0.0) rmin.push_back(r);
+        }
+    }
+    // pool bookkeeping: resolved ordinals free their slots
+    for (int q = 0; q < E; ++q) {
+      const long long ord = pos + hj[q];
+      if (ord < stop) {
+        auto it = pool.find(ord);
+        if (it != pool.end()) pool.erase(it);
+        free_slots.push_back(slot[q]);
+      } else {
+        pool[ord] = slot[q];
+      }
+    }
+    for (auto it = pool.begin(); it != pool.end() && it->first < stop;) {
+      free_slots.push_back(it->second);
+      it = pool.erase(it);
+    }
+    stats[5] += covered;
+    if (stop < pos + Lw) stats[6] += 1;
+    // adapt: early stop → finer speculation; mostly-covered builds → coarser
+    if (!rmin.empty()) {
+      std::nth_element(rmin.begin(), rmin.begin() + rmin.size() / 2, rmin.end());
+      const double med = rmin[rmin.size() / 2];
+      if (stop < pos + Lw && beyond) kappa *= 0.75;
+      else if (covered > committed) kappa *= 1.25;
+      kappa = std::min(4.0, std::max(0.05, kappa));
+      h_sel = kappa * med;
+    }
+    if (stop >= pos + Lw && E < C) L = std::min(Lmax, L * 2);
+    pos = stop;
+  }
+  stats[0] = N;
+  stats[1] = cs->n;
+  stats[2] = cm->n;
+  return VC_OK;
+}
+
+}  // namespace
+
+// Stream setup + engine run on existing caches (records with tag −1 pre-exist).
+int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
+                 int64_t* stats, cudaStream_t st) {
+  if (!(pp->march_step > 0.0)) return fail(VC_EINVAL, "march_step must be positive");
+  if (!(pp->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
+  Engine g;
+  g.sc = sc;
+  g.D = sc->dim;
+  g.st = st;
+  g.seed = (uint32_t)pp->seed;
+  g.seed_kind = seed_kind;
+  g.bp.n_angular = pp->n_angular;
+  g.bp.march_step = pp->march_step;
+  g.bp.n_inner = pp->n_inner;
+  g.bp.n_light_samples = pp->n_light_samples;
+  g.bp.epsilon = pp->epsilon;
+  g.bp.flags = VC_SEED_WORDS | VC_MAKE_RECORDS | (pp->isotropic ? VC_ISOTROPIC : 0);
+  g.bp.seed_words = seed_kind == 0 ? 3 : 4;
+  if (pp->window > 0) g.C = std::min(pp->window, 2048);
+  if (pp->lookahead > 0) g.L = pp->lookahead;
+  MarchStream& M = g.M;
+  M.step = pp->march_step;
+  struct Bufs {
+    double* ray = nullptr;
+    long long* first = nullptr;
+    long long* steps = nullptr;
+    void* tmp = nullptr;
+    ~Bufs() {
+      cudaFree(ray);
+      cudaFree(first);
+      cudaFree(steps);
+      cudaFree(tmp);
+    }
+  } bf;
+  if (pp->target == VC_TARGET_FIELD) {
+    if (sc->dim != 2) return fail(VC_EINVAL, "FieldGrid rendering requires a 2D scene");
+    if (pp->field_nx < 1 || pp->field_ny < 1) return fail(VC_EINVAL, "FieldGrid resolution must be positive");
+    for (int a = 0; a < 2; ++a)
+      if (!(pp->field_max[a] > pp->field_min[a])) return fail(VC_EINVAL, "FieldGrid bounds must have positive extent");
+    M.kind = 0;
+    M.nx = pp->field_nx;
+    M.ny = pp->field_ny;
+    for (int a = 0; a < 2; ++a) {
+      M.fmin[a] = pp->field_min[a];
+      M.fmax[a] = pp->field_max[a];
+    }
+    g.N = (long long)M.nx * M.ny;
+  } else if (pp->target == VC_TARGET_CAMERA) {
+    if (sc->dim != 3) return fail(VC_EINVAL, "Camera rendering requires a 3D scene");
+    if (seed_kind != 0) return fail(VC_EINVAL, "camera render insertion is not a populate stream");
+    DevCamera cam{};
+    vc_camera c0 = pp->camera;
+    c0.row0 = c0.col0 = 0;
+    c0.rows = c0.cols = 0;
+    int rc = make_dev_camera(c0, &cam);
+    if (rc) return rc;
+    const int npx = cam.w * cam.h;
+    cudaError_t e = cudaMalloc(&bf.ray, (size_t)npx * 32);
+    if (e == cudaSuccess) e = cudaMalloc(&bf.steps, ((size_t)npx + 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&bf.first, ((size_t)npx + 1) * 8);
+    if (e != cudaSuccess) return cuda_fail(e, "populate ray buffers");
+    rc = ensure_emitters(sc, pp->n_light_samples);
+    if (rc) return rc;
+    DevScene S = dev_scene(sc);
+    k_pop_rays<<<(npx + 127) / 128, 128, 0, st>>>(S, cam, pp->march_step, bf.ray, bf.steps);
+    e = cudaMemsetAsync(bf.steps + npx, 0, 8, st);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, bf.steps, bf.first, npx + 1, st);
+    if (e == cudaSuccess) e = cudaMalloc(&bf.tmp, tb + 16);
+    if (e == cudaSuccess) cub::DeviceScan::ExclusiveSum(bf.tmp, tb, bf.steps, bf.first, npx + 1, st);
+    long long total = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, bf.first + npx, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    count_launches(2);
+    if (e != cudaSuccess) return cuda_fail(e, "populate rays");
+    M.kind = 1;
+    for (int a = 0; a < 3; ++a) M.pos[a] = cam.pos[a];
+    M.ray = bf.ray;
+    M.first = bf.first;
+    M.n_rays = npx;
+    g.N = total;
+  } else {
+    return fail(VC_EINVAL, "target must be VC_TARGET_FIELD or VC_TARGET_CAMERA");
+  }
+  g.cs = cs;
+  g.cm = cm;
+  int rc = g.run();
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "populate");
+  }
+  if (!rc && stats)
+    for (int k = 0; k < 8; ++k) stats[k] = g.stats[k];
+  return rc;
+}
+
+__global__ void k_field_values(MarchStream M, DevCache Cs, DevCache Cm, int n, int tagged, double* J,
+                               unsigned char* miss) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double x[2];
+  stream_point<2>(M, j, x);
+  const long long lim = tagged ? (long long)j + 1 : LLONG_MAX;
+  double Js[3], Jm[3];
+  const bool cs = cache_interpolate<2>(Cs, x, Js, nullptr, lim);
+  const bool cm = cache_interpolate<2>(Cm, x, Jm, nullptr, lim);
+  const bool hit = cs && cm;
+  for (int c = 0; c < 3; ++c) J[(size_t)j * 3 + c] = hit ? add(Js[c], Jm[c]) : 0.0;
+  miss[j] = hit ? 0 : 1;
+}
+
+__global__ void k_field_points(MarchStream M, const int* cells, int n, double* x, uint32_t* words, uint32_t seed) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int j = cells[e];
+  stream_point<2>(M, j, x + (size_t)e * 2);
+  uint32_t* w = words + (size_t)e * 4;
+  w[0] = seed;
+  w[1] = 307u;
+  w[2] = (uint32_t)(j / M.nx);
+  w[3] = (uint32_t)(j % M.nx);
+}
+
+__global__ void k_field_direct(const double* mom, int MS, const int* cells, int n, double* J) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double* m = mom + (size_t)e * 2 * MS;
+  for (int c = 0; c < 3; ++c) J[(size_t)cells[e] * 3 + c] = add(m[c], m[MS + c]);
+}
+
+extern "C" {
+
+int vc_populate(vc_scene* sc, const vc_populate_params* pp, vc_cache** single, vc_cache** multiple, int64_t* stats,
+                void* stream) {
+  if (!sc || !pp || !single || !multiple) return fail(VC_EINVAL, "null argument");
+  *single = *multiple = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  double bmin[3], bmax[3];
+  for (int a = 0; a < 3; ++a) {
+    bmin[a] = sc->bmin[a];
+    bmax[a] = sc->bmax[a];
+  }
+  vc_cache* cs = new vc_cache();
+  vc_cache* cm = new vc_cache();
+  int rc = cache_init(cs, sc->dim, bmin, bmax);
+  if (!rc) rc = cache_init(cm, sc->dim, bmin, bmax);
+  if (!rc) rc = cache_reserve(cs, 1024, st);
+  if (!rc) rc = cache_reserve(cm, 1024, st);
+  if (!rc) rc = cache_rebuild(cs, st);
+  if (!rc) rc = cache_rebuild(cm, st);
+  if (!rc) rc = populate_run(sc, pp, 0, cs, cm, stats, st);
+  if (rc) {
+    delete cs;
+    delete cm;
+    return rc;
+  }
+  *single = cs;
+  *multiple = cm;
+  return VC_OK;
+}
+
+int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_params* pp, int frozen,
+                    double* image, int64_t* stats, int flags, void* stream) {
+  if (!sc || !cs || !cm || !pp || !image) return fail(VC_EINVAL, "null argument");
+  if (sc->dim != 2 || cs->dim != 2 || cm->dim != 2) return fail(VC_EINVAL, "FieldGrid rendering requires a 2D scene");
+  if (pp->target != VC_TARGET_FIELD) return fail(VC_EINVAL, "vc_render_field needs a VC_TARGET_FIELD target");
+  if (pp->field_nx < 1 || pp->field_ny < 1) return fail(VC_EINVAL, "FieldGrid resolution must be positive");
+  if (!(pp->march_step > 0.0)) return fail(VC_EINVAL, "march_step must be positive");
+  if (!(pp->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = pp->field_nx * pp->field_ny;
+  MarchStream M{};
+  M.kind = 0;
+  M.nx = pp->field_nx;
+  M.ny = pp->field_ny;
+  for (int a = 0; a < 2; ++a) {
+    M.fmin[a] = pp->field_min[a];
+    M.fmax[a] = pp->field_max[a];
+  }
+  int64_t pst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (!frozen) {  // misses insert as the render proceeds (src/renderer.py:361-368)
+    int rc = populate_run(sc, pp, 1, cs, cm, pst, st);
+    if (rc) return rc;
+  }
+  Workspace ws;
+  cudaError_t e = cudaSuccess;
+  double* J = (double*)ws.get(0, (size_t)n * 24, &e);
+  unsigned char* miss = (unsigned char*)ws.get(1, (size_t)n, &e);
+  if (e != cudaSuccess) return cuda_fail(e, "field buffers");
+  k_field_values<<<(n + 127) / 128, 128, 0, st>>>(M, cs->dev(), cm->dev(), n, frozen ? 0 : 1, J, miss);
+  count_launches(1);
+  std::vector<unsigned char> hm(n);
+  e = cudaMemcpyAsync(hm.data(), miss, n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "field lookup");
+  long long direct = 0;
+  if (frozen) {  // direct evaluation, no insertion
+    std::vector<int> cells;
+    for (int j = 0; j < n; ++j)
+      if (hm[j]) cells.push_back(j);
+    const int nm = (int)cells.size();
+    direct = nm;
+    if (nm > 0) {
+      const int MS = moment_size(2);
+      int* dc = (int*)ws.get(2, (size_t)nm * 4, &e);
+      double* x = (double*)ws.get(3, (size_t)nm * 16, &e);
+      uint32_t* w = (uint32_t*)ws.get(4, (size_t)nm * 16, &e);
+      double* mom = (double*)ws.get(5, (size_t)nm * 2 * MS * 8, &e);
+      long long* bst = (long long*)ws.get(6, (size_t)nm * kStats * 8, &e);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dc, cells.data(), (size_t)nm * 4, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "field miss buffers");
+      k_field_points<<<(nm + 127) / 128, 128, 0, st>>>(M, dc, nm, x, w, (uint32_t)pp->seed);
+      vc_build_params bp{};
+      bp.n_angular = pp->n_angular;
+      bp.march_step = pp->march_step;
+      bp.n_inner = pp->n_inner;
+      bp.n_light_samples = pp->n_light_samples;
+      bp.epsilon = pp->epsilon;
+      bp.flags = VC_SEED_WORDS;
+      bp.seed_words = 4;
+      int rc = build_impl(sc, nm, x, w, nullptr, &bp, mom, (int64_t*)bst, nullptr, st, nullptr);
+      if (rc) return rc;
+      k_field_direct<<<(nm + 127) / 128, 128, 0, st>>>(mom, MS, dc, nm, J);
+      count_launches(2);
+    }
+  } else {
+    direct = pst[7];
+  }
+  // image = full_angle(2) · J (src/renderer.py:428-436)
+  std::vector<double> hJ((size_t)n * 3);
+  e = cudaMemcpyAsync(hJ.data(), J, (size_t)n * 24, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "field download");
+  const double scale = 2.0 * 3.141592653589793;
+  std::vector<double> out((size_t)n * 3);
+  for (size_t i = 0; i < out.size(); ++i) out[i] = scale * hJ[i];
+  if (flags & VC_MEM_HOST) {
+    std::copy(out.begin(), out.end(), image);
+  } else {
+    e = cudaMemcpyAsync(image, out.data(), out.size() * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "field upload");
+  }
+  if (stats) {
+    stats[0] = n - direct;
+    stats[1] = direct;
+  }
+  return VC_OK;
+}
+
+int64_t vc_cache_size(const vc_cache* c) { return c ? (int64_t)c->n : -1; }
+
+int vc_cache_records(const vc_cache* c, double* records, int64_t* tags, int flags, void* stream) {
+  if (!c) return fail(VC_EINVAL, "null cache");
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaMemcpyKind k = (flags & VC_MEM_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  cudaError_t e = cudaSuccess;
+  if (c->n > 0 && records) e = cudaMemcpyAsync(records, c->d_rec, (size_t)c->n * record_size(c->dim) * 8, k, st);
+  if (e == cudaSuccess && c->n > 0 && tags) e = cudaMemcpyAsync(tags, c->d_tag, (size_t)c->n * 8, k, st);
+  if (e == cudaSuccess && (flags & VC_MEM_HOST)) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "cache download");
+  return VC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,320 @@
+"""Render orchestration on the B200 path: settings, targets, CacheSet, populate_cache, render.
+
+Mirrors src/renderer.py:45-131 (RenderSettings, FieldGrid), :134-193 (Camera),
+:201-275 (CacheSet), :282-327 (populate_cache) and :402-484 (render) for the cache
+modes "ours-aniso" / "ours-iso" — same names, argument meaning, return values and
+ValueError / TypeError cases.  The march, the sequential-exact cache population and
+every record build, lookup and image accumulation run in libvolcache_b200.so
+(vc_populate, vc_render_field, vc_render); this module only validates and packs.
+
+Out of scope here: the reference's correctness-oracle modes "path"
+and "quadrature" and the occlusion-unaware "baseline" estimator, which raise
+NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .cache import RadianceCache, interpolate
+from .records import DEFAULT_N_ANGULAR, device_scene, estimate_moments, make_record
+
+MODES = ("ours-aniso", "ours-iso", "baseline", "path", "quadrature")
+CACHE_MODES = ("ours-aniso", "ours-iso", "baseline")
+DEVICE_MODES = ("ours-aniso", "ours-iso")
+
+
+def _unsupported(mode: str):
+    return NotImplementedError(
+        f"mode {mode!r} is outside the B200 hot path (DESIGN.md §6); use the reference for it")
+
+
+@dataclass(frozen=True)
+class RenderSettings:
+    """Knobs shared by populate/render (src/renderer.py:50-85)."""
+
+    mode: str = "ours-aniso"
+    epsilon: float = 0.05
+    spp: int = 16
+    march_step: float = 0.1
+    n_angular: int | None = None
+    seed: int = 0
+    frozen: bool = True
+    max_media_bounces: int = 2
+    n_light_samples: int = 16
+    n_inner: int = 1
+    baseline_alpha: float = 1.0
+    path_samples_per_point: int = 256
+    quad_gather_grid: int = 96
+    quad_n_secondary: int = 256
+    quad_n_angular: int = 512
+    quad_n_dist: int = 24
+    quad3d_n_angular: int = 256
+    quad3d_n_dist: int = 12
+    quad3d_n_secondary: int = 64
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.epsilon <= 0.0:
+            raise ValueError("epsilon must be positive")
+        if self.march_step <= 0.0:
+            raise ValueError("march_step must be positive")
+        if self.spp < 1:
+            raise ValueError("spp must be at least 1")
+
+
+@dataclass(frozen=True)
+class FieldGrid:
+    """2D cell-center evaluation grid in display orientation, row 0 = top (src/renderer.py:88-131)."""
+
+    bounds_min: np.ndarray
+    bounds_max: np.ndarray
+    nx: int
+    ny: int
+
+    def __post_init__(self):
+        object.__setattr__(self, "bounds_min", np.asarray(self.bounds_min, dtype=float))
+        object.__setattr__(self, "bounds_max", np.asarray(self.bounds_max, dtype=float))
+        if self.bounds_min.shape != (2,) or self.bounds_max.shape != (2,):
+            raise ValueError("FieldGrid bounds must be 2-vectors")
+        if np.any(self.bounds_max <= self.bounds_min):
+            raise ValueError("FieldGrid bounds must have positive extent")
+        if self.nx < 1 or self.ny < 1:
+            raise ValueError("FieldGrid resolution must be positive")
+
+    @classmethod
+    def for_scene(cls, scene, nx: int, ny: int) -> "FieldGrid":
+        if scene.dim != 2:
+            raise ValueError("FieldGrid targets require a 2D scene")
+        return cls(scene.bounds_min, scene.bounds_max, nx, ny)
+
+    def cell_center(self, iy: int, ix: int) -> np.ndarray:
+        dx = (self.bounds_max[0] - self.bounds_min[0]) / self.nx
+        dy = (self.bounds_max[1] - self.bounds_min[1]) / self.ny
+        return np.array([self.bounds_min[0] + (ix + 0.5) * dx, self.bounds_max[1] - (iy + 0.5) * dy])
+
+    @property
+    def centers(self) -> np.ndarray:
+        dx = (self.bounds_max[0] - self.bounds_min[0]) / self.nx
+        dy = (self.bounds_max[1] - self.bounds_min[1]) / self.ny
+        xs = self.bounds_min[0] + (np.arange(self.nx) + 0.5) * dx
+        ys = self.bounds_max[1] - (np.arange(self.ny) + 0.5) * dy
+        gx, gy = np.meshgrid(xs, ys)
+        return np.stack([gx, gy], axis=-1)
+
+
+@dataclass(frozen=True)
+class Camera:
+    """Pinhole camera for 3D scenes; fov_degrees is the vertical field of view (src/renderer.py:134-170)."""
+
+    position: np.ndarray
+    look_at: np.ndarray
+    up: np.ndarray
+    fov_degrees: float
+    width: int
+    height: int
+
+    def __post_init__(self):
+        vals = {}
+        for name in ("position", "look_at", "up"):
+            v = np.asarray(getattr(self, name), dtype=float)
+            if v.shape != (3,):
+                raise ValueError(f"camera {name} must be a 3-vector")
+            vals[name] = v
+            object.__setattr__(self, name, v)
+        if not 0.0 < self.fov_degrees < 180.0:
+            raise ValueError("fov_degrees must lie in (0, 180)")
+        if self.width < 1 or self.height < 1:
+            raise ValueError("camera resolution must be positive")
+        forward = vals["look_at"] - vals["position"]
+        if np.linalg.norm(forward) == 0.0:
+            raise ValueError("camera look_at must differ from position")
+        if np.linalg.norm(np.cross(forward / np.linalg.norm(forward), vals["up"])) < 1e-9:
+            raise ValueError("camera up must not be parallel to the view direction")
+
+    def _c(self) -> "_lib.Camera":
+        cam = _lib.Camera()
+        cam.position[:] = [float(v) for v in self.position]
+        cam.look_at[:] = [float(v) for v in self.look_at]
+        cam.up[:] = [float(v) for v in self.up]
+        cam.fov_degrees = float(self.fov_degrees)
+        cam.width = int(self.width)
+        cam.height = int(self.height)
+        return cam
+
+
+def _check_target(scene, target) -> None:
+    """src/renderer.py:371-379."""
+    if isinstance(target, FieldGrid):
+        if scene.dim != 2:
+            raise ValueError("FieldGrid rendering requires a 2D scene")
+    elif isinstance(target, Camera):
+        if scene.dim != 3:
+            raise ValueError("Camera rendering requires a 3D scene")
+    else:
+        raise TypeError("target must be a FieldGrid or a Camera")
+
+
+def _n_angular(scene, settings) -> int:
+    return int(settings.n_angular if settings.n_angular is not None else DEFAULT_N_ANGULAR[scene.dim])
+
+
+def _params(scene, target, settings) -> "_lib.PopulateParams":
+    p = _lib.PopulateParams()
+    if isinstance(target, FieldGrid):
+        p.target = _lib.VC_TARGET_FIELD
+        p.field_nx, p.field_ny = int(target.nx), int(target.ny)
+        p.field_min[:] = [float(v) for v in target.bounds_min]
+        p.field_max[:] = [float(v) for v in target.bounds_max]
+    else:
+        p.target = _lib.VC_TARGET_CAMERA
+        p.camera = target._c()
+    p.march_step = float(settings.march_step)
+    p.seed = int(settings.seed) & 0xFFFFFFFF  # _seed masks every part to 32 bits (src/renderer.py:278-279)
+    p.n_angular = _n_angular(scene, settings)
+    p.n_inner = int(settings.n_inner)
+    p.n_light_samples = int(settings.n_light_samples)
+    p.epsilon = float(settings.epsilon)
+    p.isotropic = 1 if settings.mode == "ours-iso" else 0
+    return p
+
+
+class CacheSet:
+    """Paired single/multiple-scattering caches built by one estimator mode (src/renderer.py:201-275)."""
+
+    def __init__(self, scene, mode: str, *, _single=None, _multiple=None):
+        if mode not in CACHE_MODES:
+            raise ValueError(f"cache modes are {CACHE_MODES}, got {mode!r}")
+        if mode not in DEVICE_MODES:
+            raise _unsupported(mode)
+        self.mode = mode
+        self.scene = scene
+        self.single = _single if _single is not None else RadianceCache(scene.bounds_min, scene.bounds_max)
+        self.multiple = _multiple if _multiple is not None else RadianceCache(scene.bounds_min, scene.bounds_max)
+
+    @property
+    def record_count(self) -> int:
+        return len(self.single) + len(self.multiple)
+
+    def lookup_parts(self, x):
+        return interpolate(self.single, x), interpolate(self.multiple, x)
+
+    def lookup(self, x):
+        s, m = self.lookup_parts(x)
+        if s is None or m is None:
+            return None
+        return s + m
+
+    def compute(self, x, settings: RenderSettings, rng_seed):
+        """Fresh estimates at x → (total J, (record_single, record_multiple))."""
+        scene = self.scene
+        mom_s, mom_m = estimate_moments(scene, x, n_angular=settings.n_angular, march_step=settings.march_step,
+                                        rng_seed=rng_seed, n_inner=settings.n_inner,
+                                        n_light_samples=settings.n_light_samples)
+        aniso = self.mode == "ours-aniso"
+        rec_s = make_record(x, mom_s, settings.epsilon, scene.scale, scene.max_emission, anisotropic=aniso)
+        rec_m = make_record(x, mom_m, settings.epsilon, scene.scale, scene.max_emission, anisotropic=aniso)
+        return mom_s.L + mom_m.L, (rec_s, rec_m)
+
+    def insert(self, records, which=(True, True)) -> None:
+        rec_s, rec_m = records
+        if which[0]:
+            self.single.insert(rec_s)
+        if which[1]:
+            self.multiple.insert(rec_m)
+
+
+def populate_cache(scene, target, settings: RenderSettings, *, window: int = 0, lookahead: int = 0):
+    """March view points in scanline order, inserting records where coverage lacks.
+
+    Returns (CacheSet, stats) equal to the reference's sequential loop
+    (src/renderer.py:302-327), computed by the speculative-window engine (vc_populate).
+    `window` / `lookahead` bound the speculative builds per window and the initial
+    lookahead (0 = library defaults); the result does not depend on them.
+    """
+    if settings.mode not in CACHE_MODES:
+        raise ValueError(f"populate_cache requires a cache mode, got {settings.mode!r}")
+    _check_target(scene, target)
+    if settings.mode not in DEVICE_MODES:
+        raise _unsupported(settings.mode)
+    start = time.perf_counter()
+    ds = device_scene(scene)
+    p = _params(scene, target, settings)
+    p.window = int(window)
+    p.lookahead = int(lookahead)
+    hs, hm = _lib.C.c_void_p(), _lib.C.c_void_p()
+    st = np.zeros(8, np.int64)
+    _lib.check(_lib.lib().vc_populate(ds.handle, _lib.C.byref(p), _lib.C.byref(hs), _lib.C.byref(hm),
+                                      _lib.ptr(st), None))
+    single = RadianceCache._adopt(scene.bounds_min, scene.bounds_max, hs)
+    multiple = RadianceCache._adopt(scene.bounds_min, scene.bounds_max, hm)
+    cs = CacheSet(scene, settings.mode, _single=single, _multiple=multiple)
+    stats = {
+        "mode": settings.mode,
+        "points_marched": int(st[0]),
+        "records": int(st[1] + st[2]),
+        "records_single": int(st[1]),
+        "records_multiple": int(st[2]),
+        "seconds": time.perf_counter() - start,
+        "windows": int(st[3]),
+        "builds": int(st[4]),
+        "discarded_builds": int(st[5]),
+        "early_stops": int(st[6]),
+    }
+    return cs, stats
+
+
+def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
+    """Render the target; returns (image, stats) (src/renderer.py:402-422).
+
+    Cache modes populate a fresh cache first unless one is passed in.  Field images hold
+    the in-scatter source density; camera images hold radiance.
+    """
+    _check_target(scene, target)
+    if settings.mode not in DEVICE_MODES:
+        raise _unsupported(settings.mode)
+    start = time.perf_counter()
+    stats = {"mode": settings.mode, "cache_hits": 0, "direct_evaluations": 0}
+    if cache_set is None:
+        cache_set, pop_stats = populate_cache(scene, target, settings)
+        stats["populate"] = pop_stats
+    stats["records"] = cache_set.record_count
+    ds = device_scene(scene)
+    out = np.zeros(2, np.int64)
+    if isinstance(target, FieldGrid):
+        p = _params(scene, target, settings)
+        image = np.zeros((target.ny, target.nx, 3))
+        _lib.check(_lib.lib().vc_render_field(ds.handle, cache_set.single.handle(), cache_set.multiple.handle(),
+                                              _lib.C.byref(p), 1 if settings.frozen else 0, _lib.ptr(image),
+                                              _lib.ptr(out), _lib.VC_MEM_HOST, None))
+        if not settings.frozen:
+            cache_set.single._device_changed()
+            cache_set.multiple._device_changed()
+    else:
+        if not settings.frozen:
+            raise NotImplementedError("camera render with frozen=False (insertion during the march) is not on "
+                                      "the B200 path; populate first or render frozen")
+        cam = target._c()
+        rp = _lib.RenderParams()
+        rp.spp = int(settings.spp)
+        rp.march_step = float(settings.march_step)
+        rp.seed = int(settings.seed) & 0xFFFFFFFF
+        rp.n_angular = _n_angular(scene, settings)
+        rp.n_inner = int(settings.n_inner)
+        rp.n_light_samples = int(settings.n_light_samples)
+        rp.epsilon = float(settings.epsilon)
+        image = np.zeros((target.height, target.width, 3))
+        _lib.check(_lib.lib().vc_render(ds.handle, cache_set.single.handle(), cache_set.multiple.handle(),
+                                        _lib.C.byref(cam), _lib.C.byref(rp), _lib.ptr(image), _lib.ptr(out),
+                                        _lib.VC_MEM_HOST, None))
+    stats["cache_hits"] = int(out[0])
+    stats["direct_evaluations"] = int(out[1])
+    if not settings.frozen:
+        stats["records"] = cache_set.record_count
+    stats["seconds"] = time.perf_counter() - start
+    return image, stats

@@ -354,8 +354,97 @@ def gen_render():
     np.savez_compressed(OUT / "render.npz", **out)
 
 
+def _records_fields(prefix, cache):
+    recs = cache.records
+    d = cache.bounds_min.size
+    rows = [np.concatenate([r.position, r.value, r.grad.ravel(), r.axes.ravel(), r.radii]) for r in recs]
+    return {prefix: np.array(rows).reshape(len(rows), d + 3 + 3 * d + d * d + d)}
+
+
+def gen_populate():
+    """populate_cache / field render / camera render through the reference (src/renderer.py:282-484)."""
+    bundled = Path("/root/reference/pkg/scenes")
+    pen = vscene.load_scene(bundled / "penumbra2d.json")
+    box = vscene.load_scene(bundled / "box3d.json")
+    simple = vscene.Scene(
+        surfaces=(vscene.Surface(vertices=np.array([[0.2, 0.8], [0.8, 0.8]]), emission=np.array([5.0, 4.0, 3.0])),),
+        medium=vscene.Medium(sigma_s=0.5, sigma_a=0.25), bounds_min=np.zeros(2), bounds_max=np.ones(2))
+    cheap = dict(mode="ours-aniso", epsilon=0.05, march_step=0.1, n_angular=64, n_light_samples=4, seed=3)
+    cam3d = dict(mode="ours-aniso", epsilon=0.2, march_step=0.25, n_angular=512, n_light_samples=4, spp=1, seed=5)
+    out = {"versions": VERSIONS}
+    out.update(scene_fields("simple_", simple))
+    out.update(scene_fields("pen_", pen))
+    out.update(scene_fields("box_", box))
+
+    def settings_vec(st):
+        return np.array([st.epsilon, st.march_step, st.n_angular, st.n_light_samples, st.seed, st.n_inner, st.spp,
+                         1.0 if st.frozen else 0.0, 1.0 if st.mode == "ours-iso" else 0.0])
+
+    def pop(name, scene, target, st):
+        cs, stats = vr.populate_cache(scene, target, st)
+        out.update(_records_fields(f"{name}_single", cs.single))
+        out.update(_records_fields(f"{name}_multiple", cs.multiple))
+        out[f"{name}_stats"] = np.array([stats["points_marched"], stats["records_single"], stats["records_multiple"]])
+        out[f"{name}_settings"] = settings_vec(st)
+        print("populate", name, stats, flush=True)
+        return cs
+
+    def field(nx, ny, scene):
+        return vr.FieldGrid.for_scene(scene, nx, ny)
+
+    # populate: FieldGrid targets
+    pop("simple6", simple, field(6, 6, simple), vr.RenderSettings(**cheap))
+    pop("pen8_tight", pen, field(8, 8, pen), vr.RenderSettings(**{**cheap, "epsilon": 0.005}))
+    pop("pen8_loose", pen, field(8, 8, pen), vr.RenderSettings(**{**cheap, "epsilon": 0.5}))
+    pop("pen16_iso", pen, field(16, 12, pen), vr.RenderSettings(**{**cheap, "mode": "ours-iso", "seed": 8}))
+    # field renders: default (populate then frozen lookups), frozen with an empty cache, growing cache
+    st = vr.RenderSettings(**{**cheap, "seed": 11})
+    img, stats = vr.render(pen, field(6, 5, pen), st)
+    out["render_pen65_image"] = img
+    out["render_pen65_stats"] = np.array([stats["cache_hits"], stats["direct_evaluations"], stats["records"]])
+    out["render_pen65_settings"] = settings_vec(st)
+    st = vr.RenderSettings(**{**cheap, "frozen": True})
+    empty = vr.CacheSet(simple, "ours-aniso")
+    img, stats = vr.render(simple, field(3, 3, simple), st, cache_set=empty)
+    out["render_frozen_image"] = img
+    out["render_frozen_stats"] = np.array([stats["cache_hits"], stats["direct_evaluations"], empty.record_count])
+    out["render_frozen_settings"] = settings_vec(st)
+    st = vr.RenderSettings(**{**cheap, "frozen": False})
+    growing = vr.CacheSet(simple, "ours-aniso")
+    img, stats = vr.render(simple, field(6, 6, simple), st, cache_set=growing)
+    out["render_grow_image"] = img
+    out["render_grow_stats"] = np.array([stats["cache_hits"], stats["direct_evaluations"], growing.record_count])
+    out["render_grow_settings"] = settings_vec(st)
+    out.update(_records_fields("render_grow_single", growing.single))
+    out.update(_records_fields("render_grow_multiple", growing.multiple))
+    # camera targets over box3d
+    cam = vr.Camera(position=np.array([0.5, 0.5, 0.5]), look_at=np.array([0.5, 0.5, 1.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=60.0, width=3, height=2)
+    st = vr.RenderSettings(**cam3d)
+    cs = pop("box32", box, cam, st)
+    img, stats = vr.render(box, cam, st, cache_set=cs)
+    out["box32_image"] = img
+    out["box32_camera"] = np.concatenate([cam.position, cam.look_at, cam.up, [cam.fov_degrees, cam.width,
+                                                                                cam.height]])
+    cam = vr.Camera(position=np.array([0.5, 0.3, 0.05]), look_at=np.array([0.5, 0.5, 1.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=70.0, width=10, height=8)
+    st = vr.RenderSettings(**{**cam3d, "march_step": 0.1, "n_angular": 128, "epsilon": 0.1, "seed": 9})
+    pop("box108", box, cam, st)
+    out["box108_camera"] = np.concatenate([cam.position, cam.look_at, cam.up, [cam.fov_degrees, cam.width,
+                                                                                 cam.height]])
+    # larger targets: many speculative windows on the device
+    pop("pen64", pen, field(64, 48, pen), vr.RenderSettings(**{**cheap, "epsilon": 0.01, "seed": 21}))
+    cam = vr.Camera(position=np.array([0.1, 0.2, 0.05]), look_at=np.array([0.6, 0.5, 1.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=75.0, width=32, height=24)
+    st = vr.RenderSettings(**{**cam3d, "march_step": 0.05, "n_angular": 256, "epsilon": 0.05, "seed": 13})
+    pop("box3224", box, cam, st)
+    out["box3224_camera"] = np.concatenate([cam.position, cam.look_at, cam.up, [cam.fov_degrees, cam.width,
+                                                                                  cam.height]])
+    np.savez_compressed(OUT / "populate.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render"]
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate"]
     if "ff" in which:
         gen_formfactors()
     if "trace" in which:
@@ -368,3 +457,5 @@ if __name__ == "__main__":
         gen_interpolate()
     if "render" in which:
         gen_render()
+    if "populate" in which:
+        gen_populate()

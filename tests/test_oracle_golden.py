@@ -111,3 +111,74 @@ def test_render_matches_reference():
     np.testing.assert_allclose(img.reshape(z["image"].shape), z["image"], rtol=1e-12, atol=1e-14)
     assert stats["cache_hits"] == int(z["stats"][0])
     assert stats["direct_evaluations"] == int(z["stats"][1])
+
+
+def _prm(v):
+    eps, step, n, nl, seed, n_inner, spp, frozen, iso = v
+    return O.RenderParams(epsilon=float(eps), spp=int(spp), march_step=float(step), n_angular=int(n),
+                          seed=int(seed), n_light_samples=int(nl), n_inner=int(n_inner), anisotropic=not iso)
+
+
+def _field(z, prefix, nx, ny):
+    return {"kind": "field", "nx": nx, "ny": ny, "bmin": z[prefix + "bmin"], "bmax": z[prefix + "bmax"]}
+
+
+def _camera_target(v):
+    return {"kind": "camera", "position": v[0:3], "look_at": v[3:6], "up": v[6:9], "fov": float(v[9]),
+            "width": int(v[10]), "height": int(v[11])}
+
+
+def _rows(cache):
+    return np.array([np.concatenate([r.position, r.value, r.grad.ravel(), r.axes.ravel(), r.radii])
+                     for r in cache.records]).reshape(len(cache.records), -1)
+
+
+def _assert_rows(got, want, d):
+    assert got.shape == want.shape
+    np.testing.assert_array_equal(got[:, :d], want[:, :d])
+    assert rel_l2(got[:, d:], want[:, d:]) <= 1e-9
+
+
+@pytest.mark.parametrize("name,prefix,nx,ny", [("simple6", "simple_", 6, 6), ("pen8_tight", "pen_", 8, 8),
+                                               ("pen16_iso", "pen_", 16, 12)])
+def test_populate_field_matches_reference(name, prefix, nx, ny):
+    z = golden("populate")
+    ps = O.pack(golden_scene(z, prefix))
+    s, m, n = O.populate_cache(ps, _field(z, prefix, nx, ny), _prm(z[f"{name}_settings"]))
+    assert [n, len(s.records), len(m.records)] == z[f"{name}_stats"].tolist()
+    _assert_rows(_rows(s), z[f"{name}_single"], 2)
+    _assert_rows(_rows(m), z[f"{name}_multiple"], 2)
+
+
+@pytest.mark.parametrize("name", ["box32", "box108"])
+def test_populate_camera_matches_reference(name):
+    z = golden("populate")
+    ps = O.pack(golden_scene(z, "box_"))
+    s, m, n = O.populate_cache(ps, _camera_target(z[f"{name}_camera"]), _prm(z[f"{name}_settings"]))
+    assert [n, len(s.records), len(m.records)] == z[f"{name}_stats"].tolist()
+    _assert_rows(_rows(s), z[f"{name}_single"], 3)
+    _assert_rows(_rows(m), z[f"{name}_multiple"], 3)
+
+
+def test_render_field_matches_reference():
+    z = golden("populate")
+    ps = O.pack(golden_scene(z, "pen_"))
+    prm = _prm(z["render_pen65_settings"])
+    tgt = _field(z, "pen_", 6, 5)
+    s, m, _ = O.populate_cache(ps, tgt, prm)
+    img, st = O.render_field(ps, tgt, s, m, prm)
+    assert [st["cache_hits"], st["direct_evaluations"], len(s.records) + len(m.records)] == \
+        z["render_pen65_stats"].tolist()
+    np.testing.assert_allclose(img, z["render_pen65_image"], rtol=1e-11)
+    ps = O.pack(golden_scene(z, "simple_"))
+    prm = _prm(z["render_frozen_settings"])
+    s, m = O.Cache(), O.Cache()
+    img, st = O.render_field(ps, _field(z, "simple_", 3, 3), s, m, prm, frozen=True)
+    assert [st["cache_hits"], st["direct_evaluations"], 0] == z["render_frozen_stats"].tolist()
+    np.testing.assert_allclose(img, z["render_frozen_image"], rtol=1e-11)
+    prm = _prm(z["render_grow_settings"])
+    img, st = O.render_field(ps, _field(z, "simple_", 6, 6), s, m, prm, frozen=False)
+    assert [st["cache_hits"], st["direct_evaluations"], len(s.records) + len(m.records)] == \
+        z["render_grow_stats"].tolist()
+    np.testing.assert_allclose(img, z["render_grow_image"], rtol=1e-11)
+    _assert_rows(_rows(s), z["render_grow_single"], 2)
