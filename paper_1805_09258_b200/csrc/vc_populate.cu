@@ -121,54 +121,10 @@ __global__ void k_pop_iota(int* v, int n) {
   if (i < n) v[i] = i;
 }
 
-// 2. selection: cell key per uncovered point
-template <int D>
-__global__ void k_pop_keys(const double* X, const int* U, int nu, double o0, double o1, double o2, double inv_h,
-                           unsigned long long* keys, int* vals) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nu) return;
-  const double* x = X + (size_t)U[p] * D;
-  const double o[3] = {o0, o1, o2};
-  unsigned long long k = 0;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double f = floor((x[a] - o[a]) * inv_h);
-    long long c = (long long)fmin(fmax(f, 0.0), 2097151.0);
-    k |= (unsigned long long)c << (21 * a);
-  }
-  keys[p] = k;
-  vals[p] = p;
-}
-
 __global__ void k_pop_first(const unsigned long long* keys, const int* vals, int nu, unsigned char* flag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nu) return;
   if (i == 0 || keys[i] != keys[i - 1]) flag[vals[i]] = 1;
-}
-
-// pooled builds (sorted ordinals) are always selected while uncovered
-__global__ void k_pop_pooled(const int* U, int nu, long long pos, const long long* pool, int np,
-                             unsigned char* flag) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nu) return;
-  if (p == 0) flag[0] = 1;
-  if (np == 0) return;
-  const long long ord = pos + U[p];
-  int lo = 0, hi = np;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (pool[mid] < ord) lo = mid + 1;
-    else hi = mid;
-  }
-  if (lo < np && pool[lo] == ord) flag[p] = 1;
-}
-
-// selected U positions → lookahead indices j
-__global__ void k_pop_sel_j(const int* sel_p, const int* U, int E, int* sel_j, unsigned char* built) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  sel_j[e] = U[sel_p[e]];
-  built[sel_p[e]] = 1;
 }
 
 template <int D>
@@ -186,19 +142,28 @@ __global__ void k_pop_scatter(const double* src, int n, const int* slot, int RS2
   for (int t = threadIdx.x; t < RS2; t += blockDim.x) WR[(size_t)slot[e] * RS2 + t] = src[(size_t)e * RS2 + t];
 }
 
-// 4a. coverage bits: bit b of word (c, e, w) = record c of built point b (b < e) covers x_e
+// need bits of pooled builds against the committed caches (records of tag < pos ≤ ord)
 template <int D>
-__global__ void k_pop_bits(const double* WR, const int* slot, const int* sel_j, const double* X, int E, int W,
-                           unsigned long long* bits) {
+__global__ void k_pool_need(const double* WR, const int* slot, const long long* ords, int E, DevCache Cs,
+                            DevCache Cm, unsigned char* needP) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const double* x = WR + (size_t)slot[e] * 2 * record_size(D);  // record position = march point
+  const bool cs = cache_covers<D>(Cs, x, ords[e]);
+  const bool cm = cache_covers<D>(Cm, x, ords[e]);
+  needP[e] = (unsigned char)((cs ? 0 : 1) | (cm ? 0 : 2));
+}
+
+// coverage bits: bit b of word (c, e, w) = record c of pooled build b (b < e) covers x_e
+template <int D>
+__global__ void k_pop_bits(const double* WR, const int* slot, int E, int W, unsigned long long* bits) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 2LL * E * W) return;
   const int c = (int)(t / ((long long)E * W));
   const int rem = (int)(t % ((long long)E * W));
   const int e = rem / W, w = rem % W;
   const int RS = record_size(D);
-  double x[3];
-#pragma unroll
-  for (int a = 0; a < D; ++a) x[a] = X[(size_t)sel_j[e] * D + a];
+  const double* x = WR + (size_t)slot[e] * 2 * RS;
   unsigned long long word = 0;
   const int b1 = min(w * 64 + 64, e);
   for (int b = w * 64; b < b1; ++b) {
@@ -210,52 +175,90 @@ __global__ void k_pop_bits(const double* WR, const int* slot, const int* sel_j, 
   bits[((size_t)c * E + e) * W + w] = word;
 }
 
-// 4b. sequential acceptance among the built points (one warp; E ≤ 2048)
-__global__ void k_pop_resolve(const unsigned long long* bits, const unsigned char* need, const int* sel_j, int E,
-                              int W, unsigned char* acc) {
+// sequential acceptance among the pooled builds, in ordinal order (one warp; E ≤ 4096)
+__global__ void k_pop_resolve(const unsigned long long* bits, const unsigned char* needP, int E, int W,
+                              unsigned char* acc) {
   const int lane = threadIdx.x;
-  unsigned long long as = 0, am = 0;
+  unsigned long long as[2] = {0, 0}, am[2] = {0, 0};
   for (int e = 0; e < E; ++e) {
-    unsigned long long bs = 0, bm = 0;
-    if (lane < W) {
-      bs = bits[(size_t)e * W + lane] & as;
-      bm = bits[((size_t)E + e) * W + lane] & am;
+    bool hs = false, hm = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int w = lane + 32 * k;
+      if (w < W) {
+        hs |= (bits[(size_t)e * W + w] & as[k]) != 0;
+        hm |= (bits[((size_t)E + e) * W + w] & am[k]) != 0;
+      }
     }
-    const bool cov_s = __any_sync(0xffffffffu, bs != 0);
-    const bool cov_m = __any_sync(0xffffffffu, bm != 0);
-    const int nd = need[sel_j[e]];
+    const bool cov_s = __any_sync(0xffffffffu, hs);
+    const bool cov_m = __any_sync(0xffffffffu, hm);
+    const int nd = needP[e];
     const bool a_s = (nd & 1) && !cov_s;
     const bool a_m = (nd & 2) && !cov_m;
-    if (lane == (e >> 6)) {
-      if (a_s) as |= 1ULL << (e & 63);
-      if (a_m) am |= 1ULL << (e & 63);
+    const int w = e >> 6;
+    if ((w & 31) == lane) {
+      if (a_s) as[w >> 5] |= 1ULL << (e & 63);
+      if (a_m) am[w >> 5] |= 1ULL << (e & 63);
     }
     if (lane == 0) acc[e] = (unsigned char)((a_s ? 1 : 0) | (a_m ? 2 : 0));
   }
 }
 
-// 5. first uncovered point of U that was not built, against records of smaller tag
+// Uncovered lookahead points that have no build, against every record of smaller tag
+// (committed + tentatively accepted pooled builds): need2 flags and the stop ordinal.
 template <int D>
-__global__ void k_pop_stop(MarchStream M, DevCache Cs, DevCache Cm, const double* X, const int* U, int nu,
-                           const unsigned char* need, const unsigned char* built, long long pos,
-                           unsigned long long* stop) {
+__global__ void k_pop_need2(const double* X, const int* U, int nu, const unsigned char* need, long long pos,
+                            const long long* pool, int np, DevCache Cs, DevCache Cm, unsigned char* need2,
+                            unsigned long long* stop) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nu || built[p]) return;
+  if (p >= nu) return;
   const int j = U[p];
   const long long ord = pos + j;
-  if ((unsigned long long)ord >= *stop) return;
+  int lo = 0, hi = np;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (pool[mid] < ord) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < np && pool[lo] == ord) {
+    need2[p] = 0;
+    return;
+  }
   double x[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) x[a] = X[(size_t)j * D + a];
   const int nd = need[j];
   const bool ms = (nd & 1) && !cache_covers<D>(Cs, x, ord);
   const bool mm = !ms && (nd & 2) && !cache_covers<D>(Cm, x, ord);
+  need2[p] = (ms || mm) ? 1 : 0;
   if (ms || mm) atomicMin(stop, (unsigned long long)ord);
 }
 
-struct PopBuffers {
-  Workspace ws;
-};
+// cell key per need2 candidate (V = positions in U)
+template <int D>
+__global__ void k_pop_keys(const double* X, const int* U, const int* V, int nv, double o0, double o1, double o2,
+                           double inv_h, unsigned long long* keys, int* vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const double* x = X + (size_t)U[V[i]] * D;
+  const double o[3] = {o0, o1, o2};
+  unsigned long long k = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double f = floor((x[a] - o[a]) * inv_h);
+    long long c = (long long)fmin(fmax(f, 0.0), 2097151.0);
+    k |= (unsigned long long)c << (21 * a);
+  }
+  keys[i] = k;
+  vals[i] = i;
+}
+
+// selected V entries → lookahead indices j
+__global__ void k_pop_sel_j(const int* sel, const int* V, const int* U, int E, int* sel_j) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  sel_j[e] = U[V[sel[e]]];
+}
 
 }  // namespace vc
 
@@ -289,26 +292,26 @@ struct Engine {
 int Engine::run() {
   const int RS = record_size(D);
   const int RS2 = 2 * RS;
-  // window record slots: ≤ C selections + ≤ C pooled builds
-  const int n_slots = 2 * C;
+  const int n_slots = 2 * C;  // pooled builds (built, not yet resolved)
   double* WR = (double*)get(0, (size_t)n_slots * RS2 * 8);
+  if (e != cudaSuccess) return cuda_fail(e, "populate pool");
   std::vector<int> free_slots;
   for (int s = n_slots - 1; s >= 0; --s) free_slots.push_back(s);
-  std::map<long long, int> pool;  // ordinal → slot (built, not yet resolved)
+  std::map<long long, int> pool;  // ordinal → slot
+  std::vector<double> hrec((size_t)n_slots * RS2);
   long long pos = 0;
-  std::vector<double> hrec;
   while (pos < N) {
     const int Lw = (int)std::min<long long>(L, N - pos);
+    // 1. lookahead points and their misses against the committed caches
     double* X = (double*)get(1, (size_t)Lw * D * 8);
     unsigned char* need = (unsigned char*)get(2, (size_t)Lw);
     int* iota = (int*)get(3, (size_t)Lw * 4);
     int* U = (int*)get(4, (size_t)Lw * 4);
     int* cnt = (int*)get(5, 64);
     if (e != cudaSuccess) return cuda_fail(e, "populate lookahead buffers");
-    const DevCache Cs = cs->dev(), Cm = cm->dev();
     const int nb = (Lw + 127) / 128;
-    if (D == 2) k_pop_cover<2><<<nb, 128, 0, st>>>(M, Cs, Cm, pos, Lw, X, need);
-    else k_pop_cover<3><<<nb, 128, 0, st>>>(M, Cs, Cm, pos, Lw, X, need);
+    if (D == 2) k_pop_cover<2><<<nb, 128, 0, st>>>(M, cs->dev(), cm->dev(), pos, Lw, X, need);
+    else k_pop_cover<3><<<nb, 128, 0, st>>>(M, cs->dev(), cm->dev(), pos, Lw, X, need);
     k_pop_iota<<<nb, 128, 0, st>>>(iota, Lw);
     size_t tb = 0;
     cub::DeviceSelect::Flagged(nullptr, tb, iota, need, U, cnt, Lw, st);
@@ -321,178 +324,54 @@ int Engine::run() {
     if (e != cudaSuccess) return cuda_fail(e, "populate cover");
     count_launches(4);
     stats[3] += 1;
-    if (nu == 0) {  // lookahead fully covered
-      for (auto it = pool.begin(); it != pool.end() && it->first < pos + Lw;) {
-        free_slots.push_back(it->second);
-        it = pool.erase(it);
-      }
-      pos += Lw;
-      L = std::min(Lmax, L * 2);
-      continue;
+    // 2. sequential acceptance among the pooled builds inside the lookahead
+    std::vector<long long> pords;
+    std::vector<int> pslots;
+    for (auto& kv : pool) {
+      if (kv.first >= pos + Lw) break;
+      pords.push_back(kv.first);
+      pslots.push_back(kv.second);
     }
-    // 2. selection
-    unsigned char* flag = (unsigned char*)get(7, (size_t)nu);
-    unsigned char* built = (unsigned char*)get(8, (size_t)nu);
-    long long* dpool = (long long*)get(9, (pool.size() + 1) * 8);
-    if (e != cudaSuccess) return cuda_fail(e, "populate selection buffers");
-    e = cudaMemsetAsync(flag, 0, nu, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(built, 0, nu, st);
-    std::vector<long long> hpool;
-    for (auto& kv : pool) hpool.push_back(kv.first);
-    if (e == cudaSuccess && !hpool.empty())
-      e = cudaMemcpyAsync(dpool, hpool.data(), hpool.size() * 8, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "populate selection");
-    const int nbu = (nu + 127) / 128;
-    if (std::isfinite(h_sel) && h_sel > 0.0) {
-      unsigned long long* keys = (unsigned long long*)get(10, (size_t)nu * 8);
-      unsigned long long* keys2 = (unsigned long long*)get(11, (size_t)nu * 8);
-      int* vals = (int*)get(12, (size_t)nu * 4);
-      int* vals2 = (int*)get(13, (size_t)nu * 4);
-      if (e != cudaSuccess) return cuda_fail(e, "populate key buffers");
-      const double inv_h = 1.0 / h_sel;
-      if (D == 2) k_pop_keys<2><<<nbu, 128, 0, st>>>(X, U, nu, sc->bmin[0], sc->bmin[1], 0.0, inv_h, keys, vals);
-      else k_pop_keys<3><<<nbu, 128, 0, st>>>(X, U, nu, sc->bmin[0], sc->bmin[1], sc->bmin[2], inv_h, keys, vals);
-      size_t rb = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, vals2, nu, 0, 21 * D, st);
-      void* rtmp = get(14, rb);
-      if (e != cudaSuccess) return cuda_fail(e, "populate sort scratch");
-      cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, vals2, nu, 0, 21 * D, st);
-      k_pop_first<<<nbu, 128, 0, st>>>(keys2, vals2, nu, flag);
-      count_launches(3);
-    }
-    k_pop_pooled<<<nbu, 128, 0, st>>>(U, nu, pos, dpool, (int)hpool.size(), flag);
-    int* iota_u = (int*)get(15, (size_t)nu * 4);
-    int* sel_p = (int*)get(16, (size_t)nu * 4);
-    if (e != cudaSuccess) return cuda_fail(e, "populate selection buffers");
-    k_pop_iota<<<nbu, 128, 0, st>>>(iota_u, nu);
-    size_t tb2 = 0;
-    cub::DeviceSelect::Flagged(nullptr, tb2, iota_u, flag, sel_p, cnt + 1, nu, st);
-    void* tmp2 = get(17, tb2);
-    if (e != cudaSuccess) return cuda_fail(e, "populate select scratch");
-    cub::DeviceSelect::Flagged(tmp2, tb2, iota_u, flag, sel_p, cnt + 1, nu, st);
-    int ns = 0;
-    e = cudaMemcpyAsync(&ns, cnt + 1, 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "populate selection count");
-    count_launches(3);
-    const int E = std::min(ns, C);
-    int* sel_j = (int*)get(18, (size_t)E * 4);
-    if (e != cudaSuccess) return cuda_fail(e, "populate selection list");
-    k_pop_sel_j<<<(E + 127) / 128, 128, 0, st>>>(sel_p, U, E, sel_j, built);
-    std::vector<int> hj(E);
-    e = cudaMemcpyAsync(hj.data(), sel_j, (size_t)E * 4, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "populate selection download");
-    count_launches(1);
-    // 3. build the new selections
-    std::vector<int> slot(E), new_e, new_slot;
-    std::vector<long long> sel_ords(E);
-    for (int q = 0; q < E; ++q) sel_ords[q] = pos + hj[q];  // ascending
-    for (int q = 0; q < E; ++q) {
-      const long long ord = sel_ords[q];
-      auto it = pool.find(ord);
-      if (it != pool.end()) {
-        slot[q] = it->second;
-      } else {
-        if (free_slots.empty()) {  // evict the furthest pooled build not selected here
-          auto victim = pool.end();
-          for (auto r = pool.rbegin(); r != pool.rend(); ++r)
-            if (!std::binary_search(sel_ords.begin(), sel_ords.end(), r->first)) {
-              victim = std::next(r).base();
-              break;
-            }
-          if (victim == pool.end()) return fail(VC_ENOMEM, "populate window slots exhausted");
-          free_slots.push_back(victim->second);
-          pool.erase(victim);
-        }
-        slot[q] = free_slots.back();
-        free_slots.pop_back();
-        new_e.push_back(q);
-        new_slot.push_back(slot[q]);
-      }
-    }
-    const int nn = (int)new_e.size();
-    int* dslot = (int*)get(19, (size_t)E * 4);
-    if (e != cudaSuccess) return cuda_fail(e, "populate slots");
-    e = cudaMemcpyAsync(dslot, slot.data(), (size_t)E * 4, cudaMemcpyHostToDevice, st);
-    if (nn > 0) {
-      std::vector<int> js(nn);
-      const int nw = bp.seed_words;
-      std::vector<uint32_t> words((size_t)nn * nw);
-      for (int i = 0; i < nn; ++i) {
-        js[i] = hj[new_e[i]];
-        const long long ord = pos + js[i];
-        uint32_t* w = words.data() + (size_t)i * nw;
-        w[0] = seed;
-        if (seed_kind == 0) {  // SeedSequence([seed, 401, i]) (src/renderer.py:317)
-          w[1] = 401u;
-          w[2] = (uint32_t)(ord & 0xffffffffLL);
-        } else {  // SeedSequence([seed, 307, iy, ix]) (src/renderer.py:432-434)
-          w[1] = 307u;
-          w[2] = (uint32_t)(ord / M.nx);
-          w[3] = (uint32_t)(ord % M.nx);
-        }
-      }
-      int* djs = (int*)get(20, (size_t)nn * 4);
-      int* dns = (int*)get(21, (size_t)nn * 4);
-      double* xb = (double*)get(22, (size_t)nn * D * 8);
-      uint32_t* dw = (uint32_t*)get(23, (size_t)nn * 16);
-      double* rec = (double*)get(24, (size_t)nn * RS2 * 8);
-      double* mom = (double*)get(25, (size_t)nn * 2 * moment_size(D) * 8);
-      long long* bst = (long long*)get(26, (size_t)nn * kStats * 8);
-      if (e != cudaSuccess) return cuda_fail(e, "populate build buffers");
-      e = cudaMemcpyAsync(djs, js.data(), (size_t)nn * 4, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(dns, new_slot.data(), (size_t)nn * 4, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(dw, words.data(), words.size() * 4, cudaMemcpyHostToDevice, st);
-      if (e != cudaSuccess) return cuda_fail(e, "populate build upload");
-      if (D == 2) k_pop_gather_x<2><<<(nn + 127) / 128, 128, 0, st>>>(X, djs, nn, xb);
-      else k_pop_gather_x<3><<<(nn + 127) / 128, 128, 0, st>>>(X, djs, nn, xb);
-      count_launches(1);
-      int rc = build_impl(sc, nn, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
-      if (rc) return rc;
-      k_pop_scatter<<<dim3(1, nn), 64, 0, st>>>(rec, nn, dns, RS2, WR);
-      count_launches(1);
-      if (D == 3) {
-        std::vector<long long> hs((size_t)nn * kStats);
-        e = cudaMemcpyAsync(hs.data(), bst, hs.size() * 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return cuda_fail(e, "populate build");
-        for (int i = 0; i < nn; ++i)
-          if (hs[(size_t)i * kStats + 5] != 0)
-            return fail(VC_ETRI, "spherical Delaunay triangulation failed at march point " +
-                                     std::to_string(pos + js[i]));
-      }
-      stats[4] += nn;
-    }
-    // 4. sequential acceptance among the built points
-    const int W = (E + 63) / 64;
-    unsigned long long* bits = (unsigned long long*)get(27, (size_t)2 * E * W * 8);
-    unsigned char* acc = (unsigned char*)get(28, (size_t)E);
-    if (e != cudaSuccess) return cuda_fail(e, "populate resolve buffers");
-    {
+    const int E = (int)pords.size();
+    long long* dords = (long long*)get(9, (size_t)(E + 1) * 8);
+    int* dslot = (int*)get(19, (size_t)(E + 1) * 4);
+    unsigned char* acc = (unsigned char*)get(28, (size_t)E + 1);
+    if (e != cudaSuccess) return cuda_fail(e, "populate pool buffers");
+    std::vector<unsigned char> hacc(E, 0);
+    if (E > 0) {
+      unsigned char* needP = (unsigned char*)get(10, (size_t)E);
+      const int W = (E + 63) / 64;
+      unsigned long long* bits = (unsigned long long*)get(27, (size_t)2 * E * W * 8);
+      if (e != cudaSuccess) return cuda_fail(e, "populate resolve buffers");
+      e = cudaMemcpyAsync(dords, pords.data(), (size_t)E * 8, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dslot, pslots.data(), (size_t)E * 4, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate pool upload");
       const long long nt = 2LL * E * W;
-      if (D == 2) k_pop_bits<2><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, sel_j, X, E, W, bits);
-      else k_pop_bits<3><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, sel_j, X, E, W, bits);
+      if (D == 2) {
+        k_pool_need<2><<<(E + 127) / 128, 128, 0, st>>>(WR, dslot, dords, E, cs->dev(), cm->dev(), needP);
+        k_pop_bits<2><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, E, W, bits);
+      } else {
+        k_pool_need<3><<<(E + 127) / 128, 128, 0, st>>>(WR, dslot, dords, E, cs->dev(), cm->dev(), needP);
+        k_pop_bits<3><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, E, W, bits);
+      }
+      k_pop_resolve<<<1, 32, 0, st>>>(bits, needP, E, W, acc);
+      count_launches(3);
+      e = cudaMemcpyAsync(hacc.data(), acc, E, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate resolve");
     }
-    k_pop_resolve<<<1, 32, 0, st>>>(bits, need, sel_j, E, W, acc);
-    count_launches(2);
-    std::vector<unsigned char> hacc(E);
-    e = cudaMemcpyAsync(hacc.data(), acc, E, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "populate resolve");
-    // tentative commit: accepted rows (row = 2·slot + cache) with tag = ordinal
+    // 3. tentative insertion of the accepted builds (tag = ordinal)
     const int n0s = cs->n, n0m = cm->n;
     std::vector<int> rows_s, rows_m;
     std::vector<long long> tags_s, tags_m;
     for (int q = 0; q < E; ++q) {
-      const long long ord = pos + hj[q];
       if (hacc[q] & 1) {
-        rows_s.push_back(2 * slot[q]);
-        tags_s.push_back(ord);
+        rows_s.push_back(2 * pslots[q]);
+        tags_s.push_back(pords[q]);
       }
       if (hacc[q] & 2) {
-        rows_m.push_back(2 * slot[q] + 1);
-        tags_m.push_back(ord);
+        rows_m.push_back(2 * pslots[q] + 1);
+        tags_m.push_back(pords[q]);
       }
     }
     auto append = [&](vc_cache* c, const std::vector<int>& rows, const std::vector<long long>& tags, int s0) -> int {
@@ -510,38 +389,98 @@ int Engine::run() {
     int rc = append(cs, rows_s, tags_s, 29);
     if (!rc) rc = append(cm, rows_m, tags_m, 31);
     if (rc) return rc;
-    // 5. stop point
+    // 4. unbuilt points still uncovered by every record of smaller tag; the first is the stop
+    unsigned char* need2 = (unsigned char*)get(7, (size_t)nu + 1);
     unsigned long long* dstop = (unsigned long long*)get(33, 8);
-    if (e != cudaSuccess) return cuda_fail(e, "populate stop buffer");
+    if (e != cudaSuccess) return cuda_fail(e, "populate stop buffers");
     unsigned long long hstop = (unsigned long long)(pos + Lw);
     e = cudaMemcpyAsync(dstop, &hstop, 8, cudaMemcpyHostToDevice, st);
-    {
-      const DevCache Cs2 = cs->dev(), Cm2 = cm->dev();
-      if (D == 2) k_pop_stop<2><<<nbu, 128, 0, st>>>(M, Cs2, Cm2, X, U, nu, need, built, pos, dstop);
-      else k_pop_stop<3><<<nbu, 128, 0, st>>>(M, Cs2, Cm2, X, U, nu, need, built, pos, dstop);
+    const int nbu = (nu + 127) / 128;
+    if (nu > 0) {
+      if (D == 2) k_pop_need2<2><<<nbu, 128, 0, st>>>(X, U, nu, need, pos, dords, E, cs->dev(), cm->dev(), need2, dstop);
+      else k_pop_need2<3><<<nbu, 128, 0, st>>>(X, U, nu, need, pos, dords, E, cs->dev(), cm->dev(), need2, dstop);
+      count_launches(1);
     }
-    count_launches(1);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&hstop, dstop, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "populate stop");
-    const long long stop = (long long)hstop;
-    // roll back records of ordinal > stop; pool their builds
-    int keep_s = 0, keep_m = 0, committed = 0, covered = 0;
-    bool beyond = false;
-    for (int q = 0; q < E; ++q) {
-      const long long ord = pos + hj[q];
-      if (ord < stop) {
-        keep_s += (hacc[q] & 1) ? 1 : 0;
-        keep_m += (hacc[q] & 2) ? 1 : 0;
-        if (hacc[q]) {
-          ++committed;
-          ++stats[7];
-        }
-        else ++covered;
+    const long long stop = std::min<long long>((long long)hstop, pos + Lw);
+    // 5. next speculative builds: need2 points thinned to one per cell of the predicted size
+    std::vector<int> hj;
+    if (stop < pos + Lw) {
+      int* iota_u = (int*)get(15, (size_t)nu * 4);
+      int* V = (int*)get(16, (size_t)nu * 4);
+      if (e != cudaSuccess) return cuda_fail(e, "populate selection buffers");
+      k_pop_iota<<<nbu, 128, 0, st>>>(iota_u, nu);
+      size_t tb2 = 0;
+      cub::DeviceSelect::Flagged(nullptr, tb2, iota_u, need2, V, cnt + 1, nu, st);
+      void* tmp2 = get(17, tb2);
+      if (e != cudaSuccess) return cuda_fail(e, "populate select scratch");
+      cub::DeviceSelect::Flagged(tmp2, tb2, iota_u, need2, V, cnt + 1, nu, st);
+      int nv = 0;
+      e = cudaMemcpyAsync(&nv, cnt + 1, 4, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate candidates");
+      count_launches(3);
+      int* sel = (int*)get(18, (size_t)nv * 4 + 4);
+      int ns = 1;
+      if (std::isfinite(h_sel) && h_sel > 0.0 && nv > 1) {
+        unsigned long long* keys = (unsigned long long*)get(11, (size_t)nv * 8);
+        unsigned long long* keys2 = (unsigned long long*)get(12, (size_t)nv * 8);
+        int* vals = (int*)get(13, (size_t)nv * 4);
+        int* vals2 = (int*)get(14, (size_t)nv * 4);
+        unsigned char* flagv = (unsigned char*)get(8, (size_t)nv);
+        int* iota_v = (int*)get(20, (size_t)nv * 4);
+        if (e != cudaSuccess) return cuda_fail(e, "populate key buffers");
+        const double inv_h = 1.0 / h_sel;
+        const int nbv = (nv + 127) / 128;
+        if (D == 2)
+          k_pop_keys<2><<<nbv, 128, 0, st>>>(X, U, V, nv, sc->bmin[0], sc->bmin[1], 0.0, inv_h, keys, vals);
+        else
+          k_pop_keys<3><<<nbv, 128, 0, st>>>(X, U, V, nv, sc->bmin[0], sc->bmin[1], sc->bmin[2], inv_h, keys, vals);
+        size_t rb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, vals2, nv, 0, 21 * D, st);
+        void* rtmp = get(21, rb);
+        if (e != cudaSuccess) return cuda_fail(e, "populate sort scratch");
+        cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, vals2, nv, 0, 21 * D, st);
+        e = cudaMemsetAsync(flagv, 0, nv, st);
+        k_pop_first<<<nbv, 128, 0, st>>>(keys2, vals2, nv, flagv);
+        k_pop_iota<<<nbv, 128, 0, st>>>(iota_v, nv);
+        size_t tb3 = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb3, iota_v, flagv, sel, cnt + 2, nv, st);
+        void* tmp3 = get(22, tb3);
+        if (e != cudaSuccess) return cuda_fail(e, "populate thinning scratch");
+        cub::DeviceSelect::Flagged(tmp3, tb3, iota_v, flagv, sel, cnt + 2, nv, st);
+        e = cudaMemcpyAsync(&ns, cnt + 2, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "populate thinning");
+        count_launches(6);
       } else {
-        beyond = true;
+        const int zero = 0;
+        e = cudaMemcpyAsync(sel, &zero, 4, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "populate selection");
       }
+      const int Es = std::min(ns, C);
+      int* sel_j = (int*)get(23, (size_t)Es * 4);
+      if (e != cudaSuccess) return cuda_fail(e, "populate selection list");
+      k_pop_sel_j<<<(Es + 127) / 128, 128, 0, st>>>(sel, V, U, Es, sel_j);
+      count_launches(1);
+      hj.resize(Es);
+      e = cudaMemcpyAsync(hj.data(), sel_j, (size_t)Es * 4, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate selection download");
     }
+    // 6. decisions before the stop are final: keep them, roll back the rest
+    int keep_s = 0, keep_m = 0, committed = 0, covered = 0;
+    for (int q = 0; q < E; ++q) {
+      if (pords[q] >= stop) break;
+      keep_s += (hacc[q] & 1) ? 1 : 0;
+      keep_m += (hacc[q] & 2) ? 1 : 0;
+      if (hacc[q]) ++committed;
+      else ++covered;
+    }
+    stats[5] += covered;
+    stats[7] += committed;
     if (keep_s < (int)rows_s.size()) {
       cache_truncate(cs, n0s + keep_s, st);
       rc = cache_rebuild(cs, st);
@@ -552,53 +491,103 @@ int Engine::run() {
       rc = cache_rebuild(cm, st);
       if (rc) return rc;
     }
-    // radii of the committed records → next selection cell size
-    hrec.resize((size_t)n_slots * RS2);
-    std::vector<double> rmin;
-    {
-      std::vector<int> need_rows;
-      for (int q = 0; q < E; ++q)
-        if (pos + hj[q] < stop && hacc[q]) need_rows.push_back(q);
+    if (committed > 0) {  // committed radii → next cell size
       e = cudaMemcpyAsync(hrec.data(), WR, hrec.size() * 8, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return cuda_fail(e, "populate radii");
-      for (int q : need_rows)
+      std::vector<double> rmin;
+      for (int q = 0; q < E && pords[q] < stop; ++q)
         for (int c = 0; c < 2; ++c) {
           if (!(hacc[q] & (1 << c))) continue;
-          const double* rad = hrec.data() + (size_t)slot[q] * RS2 + (size_t)c * RS + D + 3 + 3 * D + D * D;
+          const double* rad = hrec.data() + (size_t)pslots[q] * RS2 + (size_t)c * RS + D + 3 + 3 * D + D * D;
           double r = rad[0];
           for (int a = 1; a < D; ++a) r = std::min(r, rad[a]);
           if (std::isfinite(r) && r > 0.0) rmin.push_back(r);
         }
-    }
-    // pool bookkeeping: resolved ordinals free their slots
-    for (int q = 0; q < E; ++q) {
-      const long long ord = pos + hj[q];
-      if (ord < stop) {
-        auto it = pool.find(ord);
-        if (it != pool.end()) pool.erase(it);
-        free_slots.push_back(slot[q]);
-      } else {
-        pool[ord] = slot[q];
+      if (!rmin.empty()) {
+        std::nth_element(rmin.begin(), rmin.begin() + rmin.size() / 2, rmin.end());
+        if (covered > committed) kappa *= 1.25;
+        else kappa *= 0.9;
+        kappa = std::min(8.0, std::max(0.1, kappa));
+        h_sel = kappa * rmin[rmin.size() / 2];
       }
     }
-    for (auto it = pool.begin(); it != pool.end() && it->first < stop;) {
-      free_slots.push_back(it->second);
-      it = pool.erase(it);
+    for (int q = 0; q < E && pords[q] < stop; ++q) {
+      pool.erase(pords[q]);
+      free_slots.push_back(pslots[q]);
     }
-    stats[5] += covered;
-    if (stop < pos + Lw) stats[6] += 1;
-    // adapt: early stop → finer speculation; mostly-covered builds → coarser
-    if (!rmin.empty()) {
-      std::nth_element(rmin.begin(), rmin.begin() + rmin.size() / 2, rmin.end());
-      const double med = rmin[rmin.size() / 2];
-      if (stop < pos + Lw && beyond) kappa *= 0.75;
-      else if (covered > committed) kappa *= 1.25;
-      kappa = std::min(4.0, std::max(0.05, kappa));
-      h_sel = kappa * med;
+    // 7. build the new selections into the pool
+    const int nn = (int)hj.size();
+    if (nn > 0) {
+      std::vector<int> new_slot;
+      std::vector<int> js;
+      for (int q = 0; q < nn; ++q) {
+        if (free_slots.empty()) {  // evict the furthest pooled build
+          if (pool.empty()) break;
+          auto last = std::prev(pool.end());
+          free_slots.push_back(last->second);
+          pool.erase(last);
+        }
+        new_slot.push_back(free_slots.back());
+        free_slots.pop_back();
+        js.push_back(hj[q]);
+      }
+      const int nb2 = (int)js.size();
+      const int nw = bp.seed_words;
+      std::vector<uint32_t> words((size_t)nb2 * nw);
+      for (int i = 0; i < nb2; ++i) {
+        const long long ord = pos + js[i];
+        uint32_t* w = words.data() + (size_t)i * nw;
+        w[0] = seed;
+        if (seed_kind == 0) {  // SeedSequence([seed, 401, i]) (src/renderer.py:317)
+          w[1] = 401u;
+          w[2] = (uint32_t)(ord & 0xffffffffLL);
+        } else {  // SeedSequence([seed, 307, iy, ix]) (src/renderer.py:432-434)
+          w[1] = 307u;
+          w[2] = (uint32_t)(ord / M.nx);
+          w[3] = (uint32_t)(ord % M.nx);
+        }
+      }
+      int* djs = (int*)get(24, (size_t)nb2 * 4);
+      int* dns = (int*)get(25, (size_t)nb2 * 4);
+      double* xb = (double*)get(26, (size_t)nb2 * D * 8);
+      uint32_t* dw = (uint32_t*)get(34, (size_t)nb2 * 16);
+      double* rec = (double*)get(35, (size_t)nb2 * RS2 * 8);
+      double* mom = (double*)get(36, (size_t)nb2 * 2 * moment_size(D) * 8);
+      long long* bst = (long long*)get(37, (size_t)nb2 * kStats * 8);
+      if (e != cudaSuccess) return cuda_fail(e, "populate build buffers");
+      e = cudaMemcpyAsync(djs, js.data(), (size_t)nb2 * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dns, new_slot.data(), (size_t)nb2 * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(dw, words.data(), words.size() * 4, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate build upload");
+      if (D == 2) k_pop_gather_x<2><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
+      else k_pop_gather_x<3><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
+      count_launches(1);
+      rc = build_impl(sc, nb2, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
+      if (rc) return rc;
+      k_pop_scatter<<<dim3(1, nb2), 64, 0, st>>>(rec, nb2, dns, RS2, WR);
+      count_launches(1);
+      if (D == 3) {
+        std::vector<long long> hs((size_t)nb2 * kStats);
+        e = cudaMemcpyAsync(hs.data(), bst, hs.size() * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "populate build");
+        for (int i = 0; i < nb2; ++i)
+          if (hs[(size_t)i * kStats + 5] != 0)
+            return fail(VC_ETRI, "spherical Delaunay triangulation failed at march point " +
+                                     std::to_string(pos + js[i]));
+      }
+      for (int i = 0; i < nb2; ++i) pool[pos + js[i]] = new_slot[i];
+      stats[4] += nb2;
     }
-    if (stop >= pos + Lw && E < C) L = std::min(Lmax, L * 2);
-    pos = stop;
+    // 8. advance
+    if (stop >= pos + Lw) {
+      pos += Lw;
+      L = std::min(Lmax, L * 2);
+    } else {
+      if (stop > pos) stats[6] += 1;
+      pos = stop;
+    }
   }
   stats[0] = N;
   stats[1] = cs->n;
