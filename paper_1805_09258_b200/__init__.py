@@ -1,7 +1,8 @@
 """volcache on B200: the cache-record build and lookup path of arXiv 1805.09258.
 
 Public API mirrors the reference `volcache` entry points for this path
-(estimate_moments, make_record, RadianceCache, interpolate, frozen camera render),
+(estimate_moments, make_record, RadianceCache, interpolate, populate_cache, render,
+save_cache / load_cache, PFM I/O),
 backed by hand-written sm_100a kernels in libvolcache_b200.so (C ABI:
 include/volcache_b200.h).  There is no CPU fallback.
 """
@@ -21,9 +22,15 @@ from .records import (
     make_records,
     seed_words,
 )
+from .io import (CACHE_FORMAT, CACHE_VERSION, BaselineRecord, CacheFormatError, load_cache, load_cache_npz, read_pfm,
+                 save_cache, save_cache_npz, write_pfm, write_ppm)
+from .renderer import (CACHE_MODES, MODES, CacheSet, Camera, FieldGrid, RenderSettings, populate_cache, render)
 from .scene import Medium, Scene, Surface, load_scene, save_scene
 
 __all__ = [
+    "CACHE_FORMAT", "CACHE_MODES", "CACHE_VERSION", "MODES", "BaselineRecord", "CacheFormatError", "CacheSet",
+    "Camera", "FieldGrid", "RenderSettings", "load_cache", "load_cache_npz", "populate_cache", "read_pfm", "render",
+    "save_cache", "save_cache_npz", "write_pfm", "write_ppm",
     "DEFAULT_N_ANGULAR", "BatchResult", "CacheRecord", "DeviceScene", "Moments", "RadianceCache",
     "Medium", "Scene", "Surface", "cache_from_records", "device_scene", "estimate_moments",
     "estimate_moments_batch", "inspect_record", "interpolate", "load_scene", "make_record",

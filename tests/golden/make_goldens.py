@@ -443,8 +443,23 @@ def gen_populate():
     np.savez_compressed(OUT / "populate.npz", **out)
 
 
+def gen_io():
+    """A cache document and a PFM written by the reference's own writers (src/cache.py:441-457,
+    src/renderer.py:689-699)."""
+    cache = vcache.RadianceCache(np.array([0.0, -1.0]), np.array([2.0, 3.0]))
+    c, s_ = np.cos(0.4), np.sin(0.4)
+    cache.insert(vcache.CacheRecord(position=np.array([0.5, 0.5]), value=np.array([1.0, 0.5, 0.25]),
+                                    grad=np.arange(6.0).reshape(3, 2) / 7.0, axes=np.array([[c, -s_], [s_, c]]),
+                                    radii=np.array([0.2, 0.1])))
+    cache.insert(vcache.BaselineRecord(position=np.array([1.0, 2.0]), value=np.array([0.5, 0.25, 0.125]),
+                                       grad=np.ones((3, 2)), radius=0.15))
+    vcache.save_cache(cache, OUT / "ref_cache.json", metadata={"mode": "test", "epsilon": 0.01})
+    img = np.random.default_rng(0).uniform(0.0, 10.0, size=(5, 7, 3)).astype(np.float32)
+    vr.write_pfm(OUT / "ref_image.pfm", img)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate"]
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io"]
     if "ff" in which:
         gen_formfactors()
     if "trace" in which:
@@ -459,3 +474,5 @@ if __name__ == "__main__":
         gen_render()
     if "populate" in which:
         gen_populate()
+    if "io" in which:
+        gen_io()
