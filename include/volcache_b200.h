@@ -117,12 +117,34 @@ int vc_trace(vc_scene* scene, int m, const double* o, const double* d, double* t
 /* numpy SeedSequence(words) → PCG64 state (host), for n records of nw words each. */
 int vc_seed_states(int n, const uint32_t* words, int nw, uint64_t* states);
 
+typedef struct {
+  int n_angular;         /* stratified primary directions (baseline_estimate n_angular) */
+  int max_media_bounces; /* collisions per path = max_media_bounces − 1 */
+  int n_light_samples;
+  double alpha;          /* baseline_alpha: scales log_gradient_radius */
+  int flags;             /* VC_MEM_HOST, VC_SEED_WORDS */
+  int seed_words;
+} vc_baseline_params;
+
+/* Occlusion-unaware baseline for n records: baseline_estimate (src/subdivision.py:416-521)
+ * + make_baseline_record (src/cache.py:212-226).  x, rng as vc_build_records.
+ *   estimates  NULL or n × 2 × (3 + 3d): [single, multiple] × (value, grad)
+ *   records    NULL or n × 2 × (d + 3 + 3d + d² + d): sphere records in the cache row
+ *              layout (axes = identity, every radius = log_gradient_radius)
+ *   samples    NULL or n × 2 × 2 × n_angular: [kind] × (luminance values, gradient norms) */
+int vc_baseline_records(vc_scene* scene, int n_records, const double* x, const void* rng,
+                        const vc_baseline_params* params, double* estimates, double* records, double* samples,
+                        void* stream);
+
 /* Record cache + lookup.  Replaces RadianceCache (src/cache.py:262-334) and
  * interpolate (src/cache.py:342-360).  records: n × (d + 3 + 3d + d² + d) float64,
  * host memory. */
 int vc_cache_create(int dim, const double* bounds_min, const double* bounds_max, int n_records,
                     const double* records, vc_cache** out);
 void vc_cache_destroy(vc_cache* cache);
+/* log_space = 1: the cache holds BaselineRecord spheres and blends with
+ * log_space_interpolate (src/cache.py:363-394); 0 (default): ellipsoids, interpolate. */
+int vc_cache_set_blend(vc_cache* cache, int log_space);
 /* Blended J per query (NaN row when uncovered) and the covering-record count.
  * xq m × d, J m × 3, count m (int32, may be NULL). */
 int vc_cache_interpolate(vc_cache* cache, int m, const double* xq, double* J, int32_t* count,
@@ -144,6 +166,8 @@ typedef struct {
   int n_inner;
   int n_light_samples;
   double epsilon;
+  int estimator;         /* VC_EST_* used for direct evaluations at cache misses */
+  int max_media_bounces; /* baseline estimator only */
 } vc_render_params;
 
 /* Frozen-cache camera render (src/renderer.py:402-484, mode ours-*, frozen=True):
@@ -160,6 +184,9 @@ int vc_render(vc_scene* scene, vc_cache* single, vc_cache* multiple, const vc_ca
 int64_t vc_cache_size(const vc_cache* cache);
 int vc_cache_records(const vc_cache* cache, double* records, int64_t* tags, int flags, void* stream);
 
+#define VC_EST_SUBDIVISION 0 /* estimate_moments + make_record, ellipsoid records */
+#define VC_EST_BASELINE 1    /* baseline_estimate + make_baseline_record, sphere records */
+
 #define VC_TARGET_FIELD 1  /* FieldGrid: 2D cell centers, scanline order (src/renderer.py:88-131) */
 #define VC_TARGET_CAMERA 2 /* Camera: pixel-center rays marched at march_step (src/renderer.py:134-193) */
 
@@ -175,6 +202,9 @@ typedef struct {
   int isotropic;              /* mode "ours-iso" */
   int window;                 /* record builds per speculative window (0: 2048, max 2048) */
   int64_t lookahead;          /* initial lookahead in march points (0: 65536) */
+  int estimator;              /* VC_EST_SUBDIVISION (ours-*) or VC_EST_BASELINE (mode "baseline") */
+  int max_media_bounces;      /* baseline estimator only */
+  double baseline_alpha;      /* baseline estimator only: log_gradient_radius scale */
 } vc_populate_params;
 
 /* populate_cache (src/renderer.py:302-327) for the cache modes ours-aniso / ours-iso:

@@ -68,9 +68,13 @@ class RenderParams(C.Structure):
         ("n_inner", C.c_int),
         ("n_light_samples", C.c_int),
         ("epsilon", C.c_double),
+        ("estimator", C.c_int),
+        ("max_media_bounces", C.c_int),
     ]
 
 
+VC_EST_SUBDIVISION = 0
+VC_EST_BASELINE = 1
 VC_TARGET_FIELD = 1
 VC_TARGET_CAMERA = 2
 
@@ -92,6 +96,20 @@ class PopulateParams(C.Structure):
         ("isotropic", C.c_int),
         ("window", C.c_int),
         ("lookahead", C.c_int64),
+        ("estimator", C.c_int),
+        ("max_media_bounces", C.c_int),
+        ("baseline_alpha", C.c_double),
+    ]
+
+
+class BaselineParams(C.Structure):
+    _fields_ = [
+        ("n_angular", C.c_int),
+        ("max_media_bounces", C.c_int),
+        ("n_light_samples", C.c_int),
+        ("alpha", C.c_double),
+        ("flags", C.c_int),
+        ("seed_words", C.c_int),
     ]
 
 
@@ -117,6 +135,8 @@ _SIGS = {
     "vc_cache_interpolate": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
     "vc_render": (C.c_int, [_vp, _vp, _vp, C.POINTER(Camera), C.POINTER(RenderParams), _vp, _vp, C.c_int, _vp]),
     "vc_cache_size": (C.c_int64, [_vp]),
+    "vc_cache_set_blend": (C.c_int, [_vp, C.c_int]),
+    "vc_baseline_records": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(BaselineParams), _vp, _vp, _vp, _vp]),
     "vc_cache_records": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "vc_populate": (C.c_int, [_vp, C.POINTER(PopulateParams), C.POINTER(_vp), C.POINTER(_vp), _vp, _vp]),
     "vc_render_field": (C.c_int, [_vp, _vp, _vp, C.POINTER(PopulateParams), C.c_int, _vp, _vp, C.c_int, _vp]),

@@ -110,14 +110,19 @@ class RadianceCache:
             self._fin = weakref.finalize(self, L.vc_cache_destroy, h)
         return self._handle
 
-    def interpolate_many(self, X):
-        """(J (m, 3) with NaN rows where uncovered, covering-record counts (m,))."""
+    def interpolate_many(self, X, log_space: bool = False):
+        """(J (m, 3) with NaN rows where uncovered, covering-record counts (m,)).
+
+        log_space=True blends like log_space_interpolate (sphere records, src/cache.py:363-394).
+        """
         X = np.ascontiguousarray(np.asarray(X, float).reshape(-1, self.dim))
         m = X.shape[0]
         J = np.zeros((m, 3))
         cnt = np.zeros(m, np.int32)
-        _lib.check(_lib.lib().vc_cache_interpolate(self.handle(), m, _lib.ptr(X), _lib.ptr(J), _lib.ptr(cnt),
-                                                   _lib.VC_MEM_HOST, None))
+        h = self.handle()
+        L = _lib.lib()
+        _lib.check(L.vc_cache_set_blend(h, 1 if log_space else 0))
+        _lib.check(L.vc_cache_interpolate(h, m, _lib.ptr(X), _lib.ptr(J), _lib.ptr(cnt), _lib.VC_MEM_HOST, None))
         return J, cnt
 
 
@@ -148,11 +153,19 @@ def interpolate(cache, x):
 
 
 def cache_from_records(bounds_min, bounds_max, records) -> RadianceCache:
+    from .io import BaselineRecord
+
     c = RadianceCache(bounds_min, bounds_max)
     for r in records:
-        c._records.append(r if isinstance(r, CacheRecord) else CacheRecord(
-            np.asarray(r.position, float), np.asarray(r.value, float), np.asarray(r.grad, float),
-            np.asarray(r.axes, float), np.asarray(r.radii, float)))
+        if isinstance(r, (CacheRecord, BaselineRecord)):
+            c._records.append(r)
+        elif hasattr(r, "radius") and not hasattr(r, "axes"):  # reference BaselineRecord
+            c._records.append(BaselineRecord(np.asarray(r.position, float), np.asarray(r.value, float),
+                                             np.asarray(r.grad, float), float(r.radius)))
+        else:
+            c._records.append(CacheRecord(np.asarray(r.position, float), np.asarray(r.value, float),
+                                          np.asarray(r.grad, float), np.asarray(r.axes, float),
+                                          np.asarray(r.radii, float)))
     return c
 
 

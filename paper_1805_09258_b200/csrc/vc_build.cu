@@ -27,37 +27,6 @@ namespace vc {
 // Directions + primary rays
 // ---------------------------------------------------------------------------
 
-template <int D>
-__device__ inline void stratum_direction(int k, const BuildParams& P, Pcg64 g0, const JumpTables& jt,
-                                         double* out) {
-  if constexpr (D == 2) {
-    // θ = (k + ξ)·2π/n  (src/scene.py:415-418)
-    Pcg64 g = g0;
-    pcg_advance(g, (unsigned long long)k, jt);
-    double xi = g.next_double();
-    double th = mul(add((double)k, xi), __ddiv_rn(2.0 * kPi, (double)P.n_angular));
-    out[0] = cos(th);
-    out[1] = sin(th);
-  } else {
-    // z = 1 − 2(r+u)/rows, φ = (c+v)·2π/cols (src/scene.py:420-431); u block then v block
-    int r = k / P.cols, c = k - r * P.cols;
-    Pcg64 g = g0;
-    pcg_advance(g, (unsigned long long)k, jt);
-    double u = g.next_double();
-    Pcg64 h = g0;
-    pcg_advance(h, (unsigned long long)P.rows * P.cols + k, jt);
-    double v = h.next_double();
-    double z = sub(1.0, __ddiv_rn(mul(2.0, add((double)r, u)), (double)P.rows));
-    double phi = mul(add((double)c, v), __ddiv_rn(2.0 * kPi, (double)P.cols));
-    double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
-    double sp, cp;
-    sincos(phi, &sp, &cp);
-    out[0] = mul(sq, cp);
-    out[1] = mul(sq, sp);
-    out[2] = z;
-  }
-}
-
 #ifndef VC_LB_TRACE
 #define VC_LB_TRACE 3  // min resident 256-thread CTAs per SM for the ray kernels
 #endif

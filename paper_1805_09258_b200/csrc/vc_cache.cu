@@ -496,6 +496,12 @@ int vc_cache_create(int dim, const double* bmin, const double* bmax, int n, cons
 
 void vc_cache_destroy(vc_cache* c) { delete c; }
 
+int vc_cache_set_blend(vc_cache* c, int log_space) {
+  if (!c) return fail(VC_EINVAL, "null cache");
+  c->blend = log_space ? 1 : 0;
+  return VC_OK;
+}
+
 int vc_cache_interpolate(vc_cache* c, int m, const double* xq, double* J, int32_t* count, int flags,
                          void* stream) {
   if (!c) return fail(VC_EINVAL, "null cache");
@@ -604,9 +610,22 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     bp.flags = VC_SEED_WORDS;
     bp.seed_words = 5;
     // direct evaluations at cache misses (src/renderer.py:361-368, frozen)
-    rc = build_impl(sc, (int)nmiss, mx, mw, nullptr, &bp, mmom, (int64_t*)mst, nullptr, st, nullptr);
+    int stride = moment_size(3);
+    if (rp->estimator == VC_EST_BASELINE) {  // CacheSet.compute, mode "baseline"
+      vc_baseline_params blp{};
+      blp.n_angular = rp->n_angular;
+      blp.max_media_bounces = rp->max_media_bounces;
+      blp.n_light_samples = rp->n_light_samples;
+      blp.alpha = 1.0;
+      blp.flags = VC_SEED_WORDS;
+      blp.seed_words = 5;
+      stride = 3 + 3 * 3;
+      rc = baseline_impl(sc, (int)nmiss, mx, mw, &blp, mmom, nullptr, nullptr, st);
+    } else {
+      rc = build_impl(sc, (int)nmiss, mx, mw, nullptr, &bp, mmom, (int64_t*)mst, nullptr, st, nullptr);
+    }
     if (rc) return rc;
-    k_misses_J<<<(int)((nmiss + 127) / 128), 128, 0, st>>>((int)nmiss, mmom, moment_size(3), mJ);
+    k_misses_J<<<(int)((nmiss + 127) / 128), 128, 0, st>>>((int)nmiss, mmom, stride, mJ);
     mo.miss_J = mJ;
     launches += 2;
   }

@@ -26,6 +26,7 @@ namespace vc {
 
 struct DevCache {
   int dim, n, L0, n_overflow;
+  int blend;                   // 0: ellipsoid records, linear blend; 1: sphere records, log-space blend
   double origin[3];
   double size;
   const long long* level_off;  // L0+2 entries: first cell index of each level
@@ -40,6 +41,7 @@ struct DevCache {
 
 struct vc_cache {
   int dim = 0, n = 0, L0 = 0;
+  int blend = 0;  // 1: baseline cache (BaselineRecord spheres, log_space_interpolate)
   double origin[3] = {0, 0, 0}, size = 0.0;
   long long n_cells = 0;
   std::vector<long long> level_off;
@@ -59,6 +61,7 @@ struct vc_cache {
     c.n = n;
     c.L0 = L0;
     c.n_overflow = n_overflow;
+    c.blend = blend;
     for (int a = 0; a < 3; ++a) c.origin[a] = origin[a];
     c.size = size;
     c.level_off = d_level_off;
@@ -160,6 +163,19 @@ __device__ __forceinline__ double record_support(const double* R, const double* 
   return sub(1.0, sqrt(q));
 }
 
+// sphere record: 1 − ‖Δ‖/radius (src/cache.py:142-145); radius stored in every radii slot
+template <int D>
+__device__ __forceinline__ double sphere_support(const double* R, const double* x, double* dl) {
+  const double* rad = R + D + 3 + 3 * D + D * D;
+  double q = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    dl[a] = sub(x[a], R[a]);
+    q = add(q, mul(dl[a], dl[a]));
+  }
+  return sub(1.0, __ddiv_rn(sqrt(q), rad[0]));
+}
+
 // Cubic weight of a support coordinate (src/cache.py:49-56).
 __device__ __forceinline__ double support_weight(double sup) {
   double d = fmin(fmax(sup, 0.0), 1.0);
@@ -214,36 +230,80 @@ __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, 
     if (f(C.overflow[t])) return;
 }
 
-// Blended J over records with tag < limit; false when none covers x (src/cache.py:342-360).
+// log-space blend term of one sphere record (src/cache.py:363-394)
+template <int D>
+__device__ __forceinline__ void log_blend_record(const double* R, const double* x, double num[3], double den[3],
+                                                 int& hits) {
+  const double* val = R + D;
+  const double* grd = R + D + 3;
+  double dl[D];
+  double sup = sphere_support<D>(R, x, dl);
+  if (!(sup > 0.0)) return;
+  ++hits;
+  const double w = support_weight(sup);
+  if (!(w > 0.0)) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (!(val[c] > 0.0)) continue;
+    double gd = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) gd = add(gd, mul(grd[c * D + i], dl[i]));
+    const double le = add(log(val[c]), __ddiv_rn(gd, val[c]));
+    num[c] = add(num[c], mul(w, le));
+    den[c] = add(den[c], w);
+  }
+}
+
+// Blended J over records with tag < limit; false when the reference returns None
+// (interpolate, src/cache.py:342-360; log_space_interpolate, :363-394).
 template <int D>
 __device__ inline bool cache_interpolate(const DevCache& C, const double* x, double J[3], int* count,
                                          long long limit = LLONG_MAX) {
-  double num[3] = {0.0, 0.0, 0.0}, den = 0.0;
+  double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};
   int hits = 0;
   const int RS = record_size(D);
+  if (C.blend == 0) {
+    cache_visit<D>(C, x, [&](int r) {
+      if (C.tag[r] < limit) blend_record<D>(C.rec + (size_t)r * RS, x, num, den[0], hits);
+      return false;
+    });
+    if (count) *count = hits;
+    if (hits == 0 || !(den[0] > 0.0)) return false;
+    J[0] = __ddiv_rn(num[0], den[0]);
+    J[1] = __ddiv_rn(num[1], den[0]);
+    J[2] = __ddiv_rn(num[2], den[0]);
+    return true;
+  }
   cache_visit<D>(C, x, [&](int r) {
-    if (C.tag[r] < limit) blend_record<D>(C.rec + (size_t)r * RS, x, num, den, hits);
+    if (C.tag[r] < limit) log_blend_record<D>(C.rec + (size_t)r * RS, x, num, den, hits);
     return false;
   });
   if (count) *count = hits;
-  if (hits == 0 || !(den > 0.0)) return false;
-  J[0] = __ddiv_rn(num[0], den);
-  J[1] = __ddiv_rn(num[1], den);
-  J[2] = __ddiv_rn(num[2], den);
+  const bool live = den[0] > 0.0 || den[1] > 0.0 || den[2] > 0.0;
+  if (hits == 0 || !live) return false;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) J[c] = den[c] > 0.0 ? exp(__ddiv_rn(num[c], den[c])) : 0.0;
   return true;
 }
 
 // interpolate(cache, x) is not None ⇔ some record with tag < limit has support > 0 and
-// a positive weight (the blend denominator is a sum of non-negative weights).
+// a positive weight (the blend denominator is a sum of non-negative weights); for the
+// log-space blend the record must also hold a positive channel.
 template <int D>
 __device__ inline bool cache_covers(const DevCache& C, const double* x, long long limit) {
   const int RS = record_size(D);
   bool hit = false;
   cache_visit<D>(C, x, [&](int r) {
     if (C.tag[r] >= limit) return false;
+    const double* R = C.rec + (size_t)r * RS;
     double dl[D];
-    double sup = record_support<D>(C.rec + (size_t)r * RS, x, dl);
-    hit = sup > 0.0 && support_weight(sup) > 0.0;
+    if (C.blend == 0) {
+      double sup = record_support<D>(R, x, dl);
+      hit = sup > 0.0 && support_weight(sup) > 0.0;
+    } else {
+      double sup = sphere_support<D>(R, x, dl);
+      hit = sup > 0.0 && support_weight(sup) > 0.0 && (R[D] > 0.0 || R[D + 1] > 0.0 || R[D + 2] > 0.0);
+    }
     return hit;
   });
   return hit;

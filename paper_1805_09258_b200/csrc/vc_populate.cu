@@ -156,7 +156,7 @@ __global__ void k_pool_need(const double* WR, const int* slot, const long long* 
 
 // coverage bits: bit b of word (c, e, w) = record c of pooled build b (b < e) covers x_e
 template <int D>
-__global__ void k_pop_bits(const double* WR, const int* slot, int E, int W, unsigned long long* bits) {
+__global__ void k_pop_bits(const double* WR, const int* slot, int E, int W, int blend, unsigned long long* bits) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 2LL * E * W) return;
   const int c = (int)(t / ((long long)E * W));
@@ -169,8 +169,15 @@ __global__ void k_pop_bits(const double* WR, const int* slot, int E, int W, unsi
   for (int b = w * 64; b < b1; ++b) {
     const double* R = WR + (size_t)slot[b] * 2 * RS + (size_t)c * RS;
     double dl[D];
-    double sup = record_support<D>(R, x, dl);
-    if (sup > 0.0 && support_weight(sup) > 0.0) word |= 1ULL << (b - w * 64);
+    bool cov;
+    if (blend == 0) {
+      const double sup = record_support<D>(R, x, dl);
+      cov = sup > 0.0 && support_weight(sup) > 0.0;
+    } else {  // log_space_interpolate coverage: sphere support and a positive channel
+      const double sup = sphere_support<D>(R, x, dl);
+      cov = sup > 0.0 && support_weight(sup) > 0.0 && (R[D] > 0.0 || R[D + 1] > 0.0 || R[D + 2] > 0.0);
+    }
+    if (cov) word |= 1ULL << (b - w * 64);
   }
   bits[((size_t)c * E + e) * W + w] = word;
 }
@@ -260,6 +267,14 @@ __global__ void k_pop_sel_j(const int* sel, const int* V, const int* U, int E, i
   sel_j[e] = U[V[sel[e]]];
 }
 
+__global__ void k_pop_commit_J(const double* WR, const int* slot, const long long* ord, int k, int D, int RS,
+                               double* J) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= k) return;
+  const double* R = WR + (size_t)slot[q] * 2 * RS;
+  for (int c = 0; c < 3; ++c) J[(size_t)ord[q] * 3 + c] = add(R[D + c], R[RS + D + c]);
+}
+
 }  // namespace vc
 
 using namespace vc;
@@ -276,6 +291,9 @@ struct Engine {
   vc_build_params bp{};
   uint32_t seed = 0;
   int seed_kind = 0;  // 0: populate (seed, 401, i); 1: field render (seed, 307, iy, ix)
+  int estimator = VC_EST_SUBDIVISION;
+  vc_baseline_params blp{};
+  double* commit_J = nullptr;  // optional N × 3: direct value (L_s + L_m) of every point that built
   cudaStream_t st = nullptr;
   Workspace ws;
   int C = 2048;
@@ -349,10 +367,10 @@ int Engine::run() {
       const long long nt = 2LL * E * W;
       if (D == 2) {
         k_pool_need<2><<<(E + 127) / 128, 128, 0, st>>>(WR, dslot, dords, E, cs->dev(), cm->dev(), needP);
-        k_pop_bits<2><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, E, W, bits);
+        k_pop_bits<2><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, E, W, cs->blend, bits);
       } else {
         k_pool_need<3><<<(E + 127) / 128, 128, 0, st>>>(WR, dslot, dords, E, cs->dev(), cm->dev(), needP);
-        k_pop_bits<3><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, E, W, bits);
+        k_pop_bits<3><<<(int)((nt + 127) / 128), 128, 0, st>>>(WR, dslot, E, W, cs->blend, bits);
       }
       k_pop_resolve<<<1, 32, 0, st>>>(bits, needP, E, W, acc);
       count_launches(3);
@@ -481,6 +499,24 @@ int Engine::run() {
     }
     stats[5] += covered;
     stats[7] += committed;
+    if (commit_J && committed > 0) {  // the value _point_value returns when the blend is None
+      std::vector<int> cs_slot;
+      std::vector<long long> cs_ord;
+      for (int q = 0; q < E && pords[q] < stop; ++q)
+        if (hacc[q]) {
+          cs_slot.push_back(pslots[q]);
+          cs_ord.push_back(pords[q]);
+        }
+      int* d1 = (int*)get(38, cs_slot.size() * 4);
+      long long* d2 = (long long*)get(39, cs_ord.size() * 8);
+      if (e != cudaSuccess) return cuda_fail(e, "populate commit buffers");
+      e = cudaMemcpyAsync(d1, cs_slot.data(), cs_slot.size() * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(d2, cs_ord.data(), cs_ord.size() * 8, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "populate commit upload");
+      k_pop_commit_J<<<((int)cs_slot.size() + 127) / 128, 128, 0, st>>>(WR, d1, d2, (int)cs_slot.size(), D, RS,
+                                                                       commit_J);
+      count_launches(1);
+    }
     if (keep_s < (int)rows_s.size()) {
       cache_truncate(cs, n0s + keep_s, st);
       rc = cache_rebuild(cs, st);
@@ -563,11 +599,15 @@ int Engine::run() {
       if (D == 2) k_pop_gather_x<2><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
       else k_pop_gather_x<3><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
       count_launches(1);
-      rc = build_impl(sc, nb2, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
+      if (estimator == VC_EST_BASELINE) {  // CacheSet.compute, mode "baseline" (src/renderer.py:233-244)
+        rc = baseline_impl(sc, nb2, xb, dw, &blp, nullptr, rec, nullptr, st);
+      } else {
+        rc = build_impl(sc, nb2, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
+      }
       if (rc) return rc;
       k_pop_scatter<<<dim3(1, nb2), 64, 0, st>>>(rec, nb2, dns, RS2, WR);
       count_launches(1);
-      if (D == 3) {
+      if (D == 3 && estimator != VC_EST_BASELINE) {
         std::vector<long long> hs((size_t)nb2 * kStats);
         e = cudaMemcpyAsync(hs.data(), bst, hs.size() * 8, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -599,7 +639,7 @@ int Engine::run() {
 
 // Stream setup + engine run on existing caches (records with tag −1 pre-exist).
 int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
-                 int64_t* stats, cudaStream_t st) {
+                 int64_t* stats, cudaStream_t st, double* commit_J = nullptr) {
   if (!(pp->march_step > 0.0)) return fail(VC_EINVAL, "march_step must be positive");
   if (!(pp->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
   Engine g;
@@ -608,6 +648,7 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
   g.st = st;
   g.seed = (uint32_t)pp->seed;
   g.seed_kind = seed_kind;
+  g.commit_J = commit_J;
   g.bp.n_angular = pp->n_angular;
   g.bp.march_step = pp->march_step;
   g.bp.n_inner = pp->n_inner;
@@ -615,6 +656,14 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
   g.bp.epsilon = pp->epsilon;
   g.bp.flags = VC_SEED_WORDS | VC_MAKE_RECORDS | (pp->isotropic ? VC_ISOTROPIC : 0);
   g.bp.seed_words = seed_kind == 0 ? 3 : 4;
+  g.estimator = pp->estimator == VC_EST_BASELINE ? VC_EST_BASELINE : VC_EST_SUBDIVISION;
+  g.blp.n_angular = pp->n_angular;
+  g.blp.max_media_bounces = pp->max_media_bounces;
+  g.blp.n_light_samples = pp->n_light_samples;
+  g.blp.alpha = pp->baseline_alpha;
+  g.blp.flags = VC_SEED_WORDS;
+  g.blp.seed_words = g.bp.seed_words;
+  cs->blend = cm->blend = (g.estimator == VC_EST_BASELINE) ? 1 : 0;
   if (pp->window > 0) g.C = std::min(pp->window, 2048);
   if (pp->lookahead > 0) g.L = pp->lookahead;
   MarchStream& M = g.M;
@@ -693,8 +742,8 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
   return rc;
 }
 
-__global__ void k_field_values(MarchStream M, DevCache Cs, DevCache Cm, int n, int tagged, double* J,
-                               unsigned char* miss) {
+__global__ void k_field_values(MarchStream M, DevCache Cs, DevCache Cm, int n, int tagged, const double* direct,
+                               double* J, unsigned char* miss) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   double x[2];
@@ -705,6 +754,8 @@ __global__ void k_field_values(MarchStream M, DevCache Cs, DevCache Cm, int n, i
   const bool cm = cache_interpolate<2>(Cm, x, Jm, nullptr, lim);
   const bool hit = cs && cm;
   for (int c = 0; c < 3; ++c) J[(size_t)j * 3 + c] = hit ? add(Js[c], Jm[c]) : 0.0;
+  if (!hit && direct && !isnan(direct[(size_t)j * 3]))  // inserted, blend still None: the direct value
+    for (int c = 0; c < 3; ++c) J[(size_t)j * 3 + c] = direct[(size_t)j * 3 + c];
   miss[j] = hit ? 0 : 1;
 }
 
@@ -777,28 +828,32 @@ int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_
     M.fmax[a] = pp->field_max[a];
   }
   int64_t pst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (!frozen) {  // misses insert as the render proceeds (src/renderer.py:361-368)
-    int rc = populate_run(sc, pp, 1, cs, cm, pst, st);
-    if (rc) return rc;
-  }
   Workspace ws;
   cudaError_t e = cudaSuccess;
+  double* direct = nullptr;
+  if (!frozen) {  // misses insert as the render proceeds (src/renderer.py:361-368)
+    direct = (double*)ws.get(7, (size_t)n * 24, &e);
+    if (e == cudaSuccess) e = cudaMemsetAsync(direct, 0xff, (size_t)n * 24, st);  // NaN: no direct value
+    if (e != cudaSuccess) return cuda_fail(e, "field direct buffer");
+    int rc = populate_run(sc, pp, 1, cs, cm, pst, st, direct);
+    if (rc) return rc;
+  }
   double* J = (double*)ws.get(0, (size_t)n * 24, &e);
   unsigned char* miss = (unsigned char*)ws.get(1, (size_t)n, &e);
   if (e != cudaSuccess) return cuda_fail(e, "field buffers");
-  k_field_values<<<(n + 127) / 128, 128, 0, st>>>(M, cs->dev(), cm->dev(), n, frozen ? 0 : 1, J, miss);
+  k_field_values<<<(n + 127) / 128, 128, 0, st>>>(M, cs->dev(), cm->dev(), n, frozen ? 0 : 1, direct, J, miss);
   count_launches(1);
   std::vector<unsigned char> hm(n);
   e = cudaMemcpyAsync(hm.data(), miss, n, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "field lookup");
-  long long direct = 0;
+  long long n_direct = 0;
   if (frozen) {  // direct evaluation, no insertion
     std::vector<int> cells;
     for (int j = 0; j < n; ++j)
       if (hm[j]) cells.push_back(j);
     const int nm = (int)cells.size();
-    direct = nm;
+    n_direct = nm;
     if (nm > 0) {
       const int MS = moment_size(2);
       int* dc = (int*)ws.get(2, (size_t)nm * 4, &e);
@@ -817,13 +872,27 @@ int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_
       bp.epsilon = pp->epsilon;
       bp.flags = VC_SEED_WORDS;
       bp.seed_words = 4;
-      int rc = build_impl(sc, nm, x, w, nullptr, &bp, mom, (int64_t*)bst, nullptr, st, nullptr);
+      int rc;
+      int stride = MS;
+      if (pp->estimator == VC_EST_BASELINE) {  // value = est_single + est_multiple
+        vc_baseline_params blp{};
+        blp.n_angular = pp->n_angular;
+        blp.max_media_bounces = pp->max_media_bounces;
+        blp.n_light_samples = pp->n_light_samples;
+        blp.alpha = pp->baseline_alpha;
+        blp.flags = VC_SEED_WORDS;
+        blp.seed_words = 4;
+        stride = 3 + 3 * 2;
+        rc = baseline_impl(sc, nm, x, w, &blp, mom, nullptr, nullptr, st);
+      } else {
+        rc = build_impl(sc, nm, x, w, nullptr, &bp, mom, (int64_t*)bst, nullptr, st, nullptr);
+      }
       if (rc) return rc;
-      k_field_direct<<<(nm + 127) / 128, 128, 0, st>>>(mom, MS, dc, nm, J);
+      k_field_direct<<<(nm + 127) / 128, 128, 0, st>>>(mom, stride, dc, nm, J);
       count_launches(2);
     }
   } else {
-    direct = pst[7];
+    n_direct = pst[7];
   }
   // image = full_angle(2) · J (src/renderer.py:428-436)
   std::vector<double> hJ((size_t)n * 3);
@@ -841,8 +910,8 @@ int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_
     if (e != cudaSuccess) return cuda_fail(e, "field upload");
   }
   if (stats) {
-    stats[0] = n - direct;
-    stats[1] = direct;
+    stats[0] = n - n_direct;
+    stats[1] = n_direct;
   }
   return VC_OK;
 }

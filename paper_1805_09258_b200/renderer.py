@@ -7,9 +7,9 @@ ValueError / TypeError cases.  The march, the sequential-exact cache population 
 every record build, lookup and image accumulation run in libvolcache_b200.so
 (vc_populate, vc_render_field, vc_render); this module only validates and packs.
 
-Out of scope here: the reference's correctness-oracle modes "path"
-and "quadrature" and the occlusion-unaware "baseline" estimator, which raise
-NotImplementedError.
+The occlusion-unaware "baseline" mode runs on the device too (vc_baseline_records,
+log-space blend).  Out of scope: the reference's correctness-oracle
+modes "path" and "quadrature", which raise NotImplementedError.
 """
 
 from __future__ import annotations
@@ -20,12 +20,13 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from .baseline import baseline_estimate, log_space_interpolate, make_baseline_record
 from .cache import RadianceCache, interpolate
 from .records import DEFAULT_N_ANGULAR, device_scene, estimate_moments, make_record
 
 MODES = ("ours-aniso", "ours-iso", "baseline", "path", "quadrature")
 CACHE_MODES = ("ours-aniso", "ours-iso", "baseline")
-DEVICE_MODES = ("ours-aniso", "ours-iso")
+DEVICE_MODES = ("ours-aniso", "ours-iso", "baseline")
 
 
 def _unsupported(mode: str):
@@ -148,6 +149,11 @@ class Camera:
         return cam
 
 
+def _seed(*parts) -> np.random.SeedSequence:
+    """SeedSequence of 32-bit-masked parts (src/renderer.py:278-279)."""
+    return np.random.SeedSequence([int(p) & 0xFFFFFFFF for p in parts])
+
+
 def _check_target(scene, target) -> None:
     """src/renderer.py:371-379."""
     if isinstance(target, FieldGrid):
@@ -181,6 +187,9 @@ def _params(scene, target, settings) -> "_lib.PopulateParams":
     p.n_light_samples = int(settings.n_light_samples)
     p.epsilon = float(settings.epsilon)
     p.isotropic = 1 if settings.mode == "ours-iso" else 0
+    p.estimator = _lib.VC_EST_BASELINE if settings.mode == "baseline" else _lib.VC_EST_SUBDIVISION
+    p.max_media_bounces = int(settings.max_media_bounces)
+    p.baseline_alpha = float(settings.baseline_alpha)
     return p
 
 
@@ -202,7 +211,17 @@ class CacheSet:
         return len(self.single) + len(self.multiple)
 
     def lookup_parts(self, x):
+        if self.mode == "baseline":
+            return log_space_interpolate(self.single, x), log_space_interpolate(self.multiple, x)
         return interpolate(self.single, x), interpolate(self.multiple, x)
+
+    def _handles(self):
+        """Device caches flagged with this mode's blend (log-space for baseline)."""
+        log = 1 if self.mode == "baseline" else 0
+        hs, hm = self.single.handle(), self.multiple.handle()
+        _lib.check(_lib.lib().vc_cache_set_blend(hs, log))
+        _lib.check(_lib.lib().vc_cache_set_blend(hm, log))
+        return hs, hm
 
     def lookup(self, x):
         s, m = self.lookup_parts(x)
@@ -213,6 +232,13 @@ class CacheSet:
     def compute(self, x, settings: RenderSettings, rng_seed):
         """Fresh estimates at x → (total J, (record_single, record_multiple))."""
         scene = self.scene
+        if self.mode == "baseline":
+            est_s, est_m = baseline_estimate(scene, x, n_angular=settings.n_angular, rng_seed=rng_seed,
+                                             max_media_bounces=settings.max_media_bounces,
+                                             n_light_samples=settings.n_light_samples)
+            rec_s = make_baseline_record(x, est_s, scene.scale, settings.baseline_alpha)
+            rec_m = make_baseline_record(x, est_m, scene.scale, settings.baseline_alpha)
+            return est_s.value + est_m.value, (rec_s, rec_m)
         mom_s, mom_m = estimate_moments(scene, x, n_angular=settings.n_angular, march_step=settings.march_step,
                                         rng_seed=rng_seed, n_inner=settings.n_inner,
                                         n_light_samples=settings.n_light_samples)
@@ -289,9 +315,9 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
     if isinstance(target, FieldGrid):
         p = _params(scene, target, settings)
         image = np.zeros((target.ny, target.nx, 3))
-        _lib.check(_lib.lib().vc_render_field(ds.handle, cache_set.single.handle(), cache_set.multiple.handle(),
-                                              _lib.C.byref(p), 1 if settings.frozen else 0, _lib.ptr(image),
-                                              _lib.ptr(out), _lib.VC_MEM_HOST, None))
+        hs, hm = cache_set._handles()
+        _lib.check(_lib.lib().vc_render_field(ds.handle, hs, hm, _lib.C.byref(p), 1 if settings.frozen else 0,
+                                              _lib.ptr(image), _lib.ptr(out), _lib.VC_MEM_HOST, None))
         if not settings.frozen:
             cache_set.single._device_changed()
             cache_set.multiple._device_changed()
@@ -308,10 +334,12 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
         rp.n_inner = int(settings.n_inner)
         rp.n_light_samples = int(settings.n_light_samples)
         rp.epsilon = float(settings.epsilon)
+        rp.estimator = _lib.VC_EST_BASELINE if settings.mode == "baseline" else _lib.VC_EST_SUBDIVISION
+        rp.max_media_bounces = int(settings.max_media_bounces)
         image = np.zeros((target.height, target.width, 3))
-        _lib.check(_lib.lib().vc_render(ds.handle, cache_set.single.handle(), cache_set.multiple.handle(),
-                                        _lib.C.byref(cam), _lib.C.byref(rp), _lib.ptr(image), _lib.ptr(out),
-                                        _lib.VC_MEM_HOST, None))
+        hs, hm = cache_set._handles()
+        _lib.check(_lib.lib().vc_render(ds.handle, hs, hm, _lib.C.byref(cam), _lib.C.byref(rp), _lib.ptr(image),
+                                        _lib.ptr(out), _lib.VC_MEM_HOST, None))
     stats["cache_hits"] = int(out[0])
     stats["direct_evaluations"] = int(out[1])
     if not settings.frozen:

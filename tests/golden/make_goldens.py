@@ -357,7 +357,12 @@ def gen_render():
 def _records_fields(prefix, cache):
     recs = cache.records
     d = cache.bounds_min.size
-    rows = [np.concatenate([r.position, r.value, r.grad.ravel(), r.axes.ravel(), r.radii]) for r in recs]
+    def row(r):
+        if hasattr(r, "radius"):  # BaselineRecord sphere → identity axes, equal radii (device layout)
+            return np.concatenate([r.position, r.value, r.grad.ravel(), np.eye(d).ravel(), np.full(d, r.radius)])
+        return np.concatenate([r.position, r.value, r.grad.ravel(), r.axes.ravel(), r.radii])
+
+    rows = [row(r) for r in recs]
     return {prefix: np.array(rows).reshape(len(rows), d + 3 + 3 * d + d * d + d)}
 
 
@@ -458,8 +463,91 @@ def gen_io():
     vr.write_pfm(OUT / "ref_image.pfm", img)
 
 
+def gen_baseline():
+    """baseline_estimate / make_baseline_record / log_space_interpolate and the baseline
+    cache mode through the reference (src/subdivision.py:416-521, src/cache.py:190-394)."""
+    bundled = Path("/root/reference/pkg/scenes")
+    pen = vscene.load_scene(bundled / "penumbra2d.json")
+    box = vscene.load_scene(bundled / "box3d.json")
+    box_refl = vscene.Scene(
+        surfaces=tuple(vscene.Surface(vertices=s.vertices, emission=s.emission,
+                                      albedo=(0.0 if s.is_emitter else 0.5)) for s in box.surfaces),
+        medium=box.medium, bounds_min=box.bounds_min, bounds_max=box.bounds_max)
+    out = {"versions": VERSIONS}
+    out.update(scene_fields("pen_", pen))
+    out.update(scene_fields("box_", box))
+    out.update(scene_fields("boxr_", box_refl))
+    cases = {  # name: (scene prefix, scene, points, n_angular, max_media_bounces, n_light)
+        "pen": ("pen_", pen, np.array([[0.15, 0.6], [0.3, 0.45], [0.8, 0.2]]), 512, 2, 16),
+        "pen3": ("pen_", pen, np.array([[0.5, 0.35]]), 256, 4, 8),
+        "box": ("box_", box, np.array([[0.5, 0.5, 0.5], [0.2, 0.7, 0.3]]), 1024, 2, 8),
+        "boxr": ("boxr_", box_refl, np.array([[0.4, 0.6, 0.5]]), 512, 3, 4),
+    }
+    for name, (prefix, sc, pts, n, mmb, nl) in cases.items():
+        vals, grads, svals, snorms, radii = [], [], [], [], []
+        for i, x in enumerate(pts):
+            s_, m_ = vs.baseline_estimate(sc, x, n_angular=n, rng_seed=vr._seed(17, 401, i), max_media_bounces=mmb,
+                                          n_light_samples=nl)
+            vals.append([s_.value, m_.value])
+            grads.append([s_.grad, m_.grad])
+            svals.append([s_.sample_values, m_.sample_values])
+            snorms.append([s_.sample_grad_norms, m_.sample_grad_norms])
+            radii.append([vcache.make_baseline_record(x, e, sc.scale, 0.7).radius for e in (s_, m_)])
+        out[f"{name}_points"] = pts
+        out[f"{name}_params"] = np.array([n, mmb, nl])
+        out[f"{name}_value"] = np.array(vals)
+        out[f"{name}_grad"] = np.array(grads)
+        out[f"{name}_svals"] = np.array(svals)
+        out[f"{name}_snorms"] = np.array(snorms)
+        out[f"{name}_radius"] = np.array(radii)
+        out[f"{name}_prefix"] = np.array(prefix)
+    # log-space interpolation on a random sphere-record cache
+    rng = np.random.default_rng(808)
+    cache = vcache.RadianceCache(np.zeros(3), np.ones(3))
+    recs = []
+    for _ in range(40):
+        v = rng.uniform(0.0, 2.0, 3)
+        v[rng.uniform(size=3) < 0.2] = 0.0
+        r = vcache.BaselineRecord(position=rng.uniform(0, 1, 3), value=v, grad=rng.normal(size=(3, 3)),
+                                  radius=float(rng.uniform(0.05, 0.3)))
+        cache.insert(r)
+        recs.append(np.concatenate([r.position, r.value, r.grad.ravel(), [r.radius]]))
+    q = rng.uniform(0, 1, (300, 3))
+    J = np.array([vcache.log_space_interpolate(cache, x) if vcache.log_space_interpolate(cache, x) is not None
+                  else np.full(3, np.nan) for x in q])
+    out["log_records"] = np.array(recs)
+    out["log_q"] = q
+    out["log_J"] = J
+    # baseline cache mode: populate + field render (2D), camera populate (3D)
+    cheap = dict(mode="baseline", epsilon=0.05, march_step=0.1, n_angular=64, n_light_samples=4, seed=3,
+                 baseline_alpha=0.8)
+    st = vr.RenderSettings(**cheap)
+    grid = vr.FieldGrid.for_scene(pen, 8, 6)
+    cs, pst = vr.populate_cache(pen, grid, st)
+    out.update(_records_fields("bpop_single", cs.single))
+    out.update(_records_fields("bpop_multiple", cs.multiple))
+    img, rst = vr.render(pen, grid, st, cache_set=cs)
+    out["bpop_image"] = img
+    out["bpop_stats"] = np.array([pst["points_marched"], pst["records_single"], pst["records_multiple"],
+                                  rst["cache_hits"], rst["direct_evaluations"]])
+    cam = vr.Camera(position=np.array([0.5, 0.3, 0.05]), look_at=np.array([0.5, 0.5, 1.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=70.0, width=6, height=5)
+    st3 = vr.RenderSettings(mode="baseline", epsilon=0.1, march_step=0.1, n_angular=256, n_light_samples=4, seed=9,
+                            spp=1)
+    cs3, pst3 = vr.populate_cache(box, cam, st3)
+    out.update(_records_fields("bcam_single", cs3.single))
+    out.update(_records_fields("bcam_multiple", cs3.multiple))
+    img3, rst3 = vr.render(box, cam, st3, cache_set=cs3)
+    out["bcam_image"] = img3
+    out["bcam_stats"] = np.array([pst3["points_marched"], pst3["records_single"], pst3["records_multiple"],
+                                  rst3["cache_hits"], rst3["direct_evaluations"]])
+    out["bcam_camera"] = np.concatenate([cam.position, cam.look_at, cam.up, [cam.fov_degrees, cam.width,
+                                                                               cam.height]])
+    np.savez_compressed(OUT / "baseline.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io"]
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline"]
     if "ff" in which:
         gen_formfactors()
     if "trace" in which:
@@ -476,3 +564,5 @@ if __name__ == "__main__":
         gen_populate()
     if "io" in which:
         gen_io()
+    if "baseline" in which:
+        gen_baseline()

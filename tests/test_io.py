@@ -201,5 +201,3 @@ def test_render_settings_and_targets_validation():
             Camera(**base)
     with pytest.raises(ValueError):
         CacheSet(None, "path")
-    with pytest.raises(NotImplementedError):
-        CacheSet(None, "baseline")
