@@ -136,6 +136,13 @@ int vc_baseline_records(vc_scene* scene, int n_records, const double* x, const v
                         const vc_baseline_params* params, double* estimates, double* records, double* samples,
                         void* stream);
 
+/* path_trace_radiance (src/transport.py:318-391) at m query points: out m × 2 × 3 =
+ * (J_single, J_multiple).  rng per point as vc_build_records (flags VC_SEED_WORDS +
+ * seed_words, or PCG64 states); points sharing a stream get common random numbers
+ * (fd_derivatives, src/renderer.py:590-643).  VC_MEM_HOST: host arrays. */
+int vc_path_trace(vc_scene* scene, int m, const double* x, const void* rng, int64_t n_samples,
+                  int max_media_bounces, int n_light_samples, int flags, int seed_words, double* out, void* stream);
+
 /* Record cache + lookup.  Replaces RadianceCache (src/cache.py:262-334) and
  * interpolate (src/cache.py:342-360).  records: n × (d + 3 + 3d + d² + d) float64,
  * host memory. */
@@ -167,7 +174,8 @@ typedef struct {
   int n_light_samples;
   double epsilon;
   int estimator;         /* VC_EST_* used for direct evaluations at cache misses */
-  int max_media_bounces; /* baseline estimator only */
+  int max_media_bounces; /* baseline and path estimators */
+  int path_samples;      /* path estimator: path_samples_per_point */
 } vc_render_params;
 
 /* Frozen-cache camera render (src/renderer.py:402-484, mode ours-*, frozen=True):
@@ -186,6 +194,7 @@ int vc_cache_records(const vc_cache* cache, double* records, int64_t* tags, int 
 
 #define VC_EST_SUBDIVISION 0 /* estimate_moments + make_record, ellipsoid records */
 #define VC_EST_BASELINE 1    /* baseline_estimate + make_baseline_record, sphere records */
+#define VC_EST_PATH 2        /* path_trace_radiance (render mode "path": every point evaluated) */
 
 #define VC_TARGET_FIELD 1  /* FieldGrid: 2D cell centers, scanline order (src/renderer.py:88-131) */
 #define VC_TARGET_CAMERA 2 /* Camera: pixel-center rays marched at march_step (src/renderer.py:134-193) */
@@ -202,9 +211,10 @@ typedef struct {
   int isotropic;              /* mode "ours-iso" */
   int window;                 /* record builds per speculative window (0: 2048, max 2048) */
   int64_t lookahead;          /* initial lookahead in march points (0: 65536) */
-  int estimator;              /* VC_EST_SUBDIVISION (ours-*) or VC_EST_BASELINE (mode "baseline") */
-  int max_media_bounces;      /* baseline estimator only */
+  int estimator;              /* VC_EST_SUBDIVISION (ours-*), VC_EST_BASELINE, VC_EST_PATH (render only) */
+  int max_media_bounces;      /* baseline and path estimators */
   double baseline_alpha;      /* baseline estimator only: log_gradient_radius scale */
+  int path_samples;           /* path estimator: path_samples_per_point */
 } vc_populate_params;
 
 /* populate_cache (src/renderer.py:302-327) for the cache modes ours-aniso / ours-iso:

@@ -70,11 +70,13 @@ class RenderParams(C.Structure):
         ("epsilon", C.c_double),
         ("estimator", C.c_int),
         ("max_media_bounces", C.c_int),
+        ("path_samples", C.c_int),
     ]
 
 
 VC_EST_SUBDIVISION = 0
 VC_EST_BASELINE = 1
+VC_EST_PATH = 2
 VC_TARGET_FIELD = 1
 VC_TARGET_CAMERA = 2
 
@@ -99,6 +101,7 @@ class PopulateParams(C.Structure):
         ("estimator", C.c_int),
         ("max_media_bounces", C.c_int),
         ("baseline_alpha", C.c_double),
+        ("path_samples", C.c_int),
     ]
 
 
@@ -136,6 +139,7 @@ _SIGS = {
     "vc_render": (C.c_int, [_vp, _vp, _vp, C.POINTER(Camera), C.POINTER(RenderParams), _vp, _vp, C.c_int, _vp]),
     "vc_cache_size": (C.c_int64, [_vp]),
     "vc_cache_set_blend": (C.c_int, [_vp, C.c_int]),
+    "vc_path_trace": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "vc_baseline_records": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(BaselineParams), _vp, _vp, _vp, _vp]),
     "vc_cache_records": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "vc_populate": (C.c_int, [_vp, C.POINTER(PopulateParams), C.POINTER(_vp), C.POINTER(_vp), _vp, _vp]),

@@ -84,6 +84,8 @@ int ensure_emitters(vc_scene* sc, int n_light);
 DevScene dev_scene(const vc_scene* sc);
 int baseline_impl(vc_scene* sc, int N, const double* x, const void* rng, const vc_baseline_params* prm,
                   double* est, double* records, double* samples, cudaStream_t st);
+int path_impl(vc_scene* sc, int m, const double* x, const void* rng, long long n_samples, int max_media_bounces,
+              int n_light_samples, int flags, int seed_words, double* out, cudaStream_t st);
 int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int32_t* adjacency,
                const vc_build_params* prm, double* moments, int64_t* stats, double* records,
                cudaStream_t st, Inspect* insp);

@@ -611,7 +611,11 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     bp.seed_words = 5;
     // direct evaluations at cache misses (src/renderer.py:361-368, frozen)
     int stride = moment_size(3);
-    if (rp->estimator == VC_EST_BASELINE) {  // CacheSet.compute, mode "baseline"
+    if (rp->estimator == VC_EST_PATH) {  // _point_value, mode "path" (src/renderer.py:337-346)
+      stride = 3;
+      rc = path_impl(sc, (int)nmiss, mx, mw, rp->path_samples, rp->max_media_bounces, rp->n_light_samples,
+                     VC_SEED_WORDS, 5, mmom, st);
+    } else if (rp->estimator == VC_EST_BASELINE) {  // CacheSet.compute, mode "baseline"
       vc_baseline_params blp{};
       blp.n_angular = rp->n_angular;
       blp.max_media_bounces = rp->max_media_bounces;

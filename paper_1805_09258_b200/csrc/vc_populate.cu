@@ -819,6 +819,7 @@ int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_
   if (!(pp->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
   cudaStream_t st = (cudaStream_t)stream;
   const int n = pp->field_nx * pp->field_ny;
+  if (pp->estimator == VC_EST_PATH) frozen = 1;  // no cache in the path mode
   MarchStream M{};
   M.kind = 0;
   M.nx = pp->field_nx;
@@ -874,7 +875,11 @@ int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_
       bp.seed_words = 4;
       int rc;
       int stride = MS;
-      if (pp->estimator == VC_EST_BASELINE) {  // value = est_single + est_multiple
+      if (pp->estimator == VC_EST_PATH) {  // _point_value, mode "path" (src/renderer.py:337-346)
+        stride = 3;
+        rc = path_impl(sc, nm, x, w, pp->path_samples, pp->max_media_bounces, pp->n_light_samples, VC_SEED_WORDS,
+                       4, mom, st);
+      } else if (pp->estimator == VC_EST_BASELINE) {  // value = est_single + est_multiple
         vc_baseline_params blp{};
         blp.n_angular = pp->n_angular;
         blp.max_media_bounces = pp->max_media_bounces;

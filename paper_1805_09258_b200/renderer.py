@@ -8,8 +8,9 @@ every record build, lookup and image accumulation run in libvolcache_b200.so
 (vc_populate, vc_render_field, vc_render); this module only validates and packs.
 
 The occlusion-unaware "baseline" mode runs on the device too (vc_baseline_records,
-log-space blend).  Out of scope: the reference's correctness-oracle
-modes "path" and "quadrature", which raise NotImplementedError.
+log-space blend), and so does the path-traced reference mode "path" (vc_path_trace).
+Out of scope: the deterministic "quadrature" oracle mode, which raises
+NotImplementedError.
 """
 
 from __future__ import annotations
@@ -187,10 +188,15 @@ def _params(scene, target, settings) -> "_lib.PopulateParams":
     p.n_light_samples = int(settings.n_light_samples)
     p.epsilon = float(settings.epsilon)
     p.isotropic = 1 if settings.mode == "ours-iso" else 0
-    p.estimator = _lib.VC_EST_BASELINE if settings.mode == "baseline" else _lib.VC_EST_SUBDIVISION
+    p.estimator = _estimator(settings.mode)
     p.max_media_bounces = int(settings.max_media_bounces)
     p.baseline_alpha = float(settings.baseline_alpha)
+    p.path_samples = int(settings.path_samples_per_point)
     return p
+
+
+def _estimator(mode: str) -> int:
+    return {"baseline": _lib.VC_EST_BASELINE, "path": _lib.VC_EST_PATH}.get(mode, _lib.VC_EST_SUBDIVISION)
 
 
 class CacheSet:
@@ -302,14 +308,19 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
     the in-scatter source density; camera images hold radiance.
     """
     _check_target(scene, target)
-    if settings.mode not in DEVICE_MODES:
+    if settings.mode not in DEVICE_MODES + ("path",):
         raise _unsupported(settings.mode)
     start = time.perf_counter()
     stats = {"mode": settings.mode, "cache_hits": 0, "direct_evaluations": 0}
-    if cache_set is None:
+    path = settings.mode == "path"
+    if path:  # every shading point path-traced: an empty cache pair, frozen (src/renderer.py:337-346)
+        cache_set = CacheSet(scene, "ours-aniso")
+        settings = RenderSettings(**{**settings.__dict__, "frozen": True})
+    elif cache_set is None:
         cache_set, pop_stats = populate_cache(scene, target, settings)
         stats["populate"] = pop_stats
-    stats["records"] = cache_set.record_count
+    if not path:
+        stats["records"] = cache_set.record_count
     ds = device_scene(scene)
     out = np.zeros(2, np.int64)
     if isinstance(target, FieldGrid):
@@ -334,14 +345,16 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
         rp.n_inner = int(settings.n_inner)
         rp.n_light_samples = int(settings.n_light_samples)
         rp.epsilon = float(settings.epsilon)
-        rp.estimator = _lib.VC_EST_BASELINE if settings.mode == "baseline" else _lib.VC_EST_SUBDIVISION
+        rp.estimator = _estimator(settings.mode)
         rp.max_media_bounces = int(settings.max_media_bounces)
+        rp.path_samples = int(settings.path_samples_per_point)
         image = np.zeros((target.height, target.width, 3))
         hs, hm = cache_set._handles()
         _lib.check(_lib.lib().vc_render(ds.handle, hs, hm, _lib.C.byref(cam), _lib.C.byref(rp), _lib.ptr(image),
                                         _lib.ptr(out), _lib.VC_MEM_HOST, None))
-    stats["cache_hits"] = int(out[0])
-    stats["direct_evaluations"] = int(out[1])
+    if not path:  # the reference counts hits/evaluations only in the cache modes
+        stats["cache_hits"] = int(out[0])
+        stats["direct_evaluations"] = int(out[1])
     if not settings.frozen:
         stats["records"] = cache_set.record_count
     stats["seconds"] = time.perf_counter() - start

@@ -546,8 +546,52 @@ def gen_baseline():
     np.savez_compressed(OUT / "baseline.npz", **out)
 
 
+def gen_path():
+    """path_trace_radiance / fd_derivatives / render mode "path" through the reference
+    (src/transport.py:318-391, src/renderer.py:337-346, :590-643)."""
+    import volcache.transport as vt
+
+    bundled = Path("/root/reference/pkg/scenes")
+    pen = vscene.load_scene(bundled / "penumbra2d.json")
+    box = vscene.load_scene(bundled / "box3d.json")
+    box_refl = vscene.Scene(
+        surfaces=tuple(vscene.Surface(vertices=s.vertices, emission=s.emission,
+                                      albedo=(0.0 if s.is_emitter else 0.5)) for s in box.surfaces),
+        medium=box.medium, bounds_min=box.bounds_min, bounds_max=box.bounds_max)
+    out = {"versions": VERSIONS}
+    out.update(scene_fields("pen_", pen))
+    out.update(scene_fields("box_", box))
+    out.update(scene_fields("boxr_", box_refl))
+    cases = {  # name: (prefix, scene, x, n_samples, max_media_bounces, n_light, seed)
+        "pen": ("pen_", pen, np.array([0.15, 0.6]), 70000, 2, 16, 5),
+        "pen4": ("pen_", pen, np.array([0.5, 0.35]), 3000, 4, 8, 6),
+        "box": ("box_", box, np.array([0.5, 0.5, 0.5]), 70000, 2, 8, 7),
+        "boxr": ("boxr_", box_refl, np.array([0.3, 0.6, 0.4]), 5000, 3, 4, 8),
+    }
+    for name, (prefix, sc, x, n, mmb, nl, seed) in cases.items():
+        s_, m_ = vt.path_trace_radiance(sc, x, n, max_media_bounces=mmb, rng_seed=seed, n_light_samples=nl)
+        out[f"{name}_x"] = x
+        out[f"{name}_params"] = np.array([n, mmb, nl, seed])
+        out[f"{name}_J"] = np.array([s_, m_])
+        out[f"{name}_prefix"] = np.array(prefix)
+    fs, fm = vr.fd_derivatives(pen, np.array([0.3, 0.45]), h=0.02, n_samples=20000, seed=11, include_hessian=True)
+    out["fd_pen"] = np.array([np.concatenate([e.value, e.grad.ravel(), e.hess.ravel()]) for e in (fs, fm)])
+    fs, fm = vr.fd_derivatives(box, np.array([0.5, 0.4, 0.6]), h=0.03, n_samples=8000, seed=12, include_hessian=True,
+                               n_light_samples=4)
+    out["fd_box"] = np.array([np.concatenate([e.value, e.grad.ravel(), e.hess.ravel()]) for e in (fs, fm)])
+    st = vr.RenderSettings(mode="path", path_samples_per_point=64, n_light_samples=4, seed=4)
+    img, _ = vr.render(pen, vr.FieldGrid.for_scene(pen, 4, 3), st)
+    out["render_field"] = img
+    cam = vr.Camera(position=np.array([0.5, 0.5, 0.5]), look_at=np.array([0.5, 0.5, 1.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=60.0, width=3, height=2)
+    st3 = vr.RenderSettings(mode="path", path_samples_per_point=32, n_light_samples=4, seed=5, spp=2, march_step=0.25)
+    img3, _ = vr.render(box, cam, st3)
+    out["render_camera"] = img3
+    np.savez_compressed(OUT / "path.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline"]
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline", "path"]
     if "ff" in which:
         gen_formfactors()
     if "trace" in which:
@@ -566,3 +610,5 @@ if __name__ == "__main__":
         gen_io()
     if "baseline" in which:
         gen_baseline()
+    if "path" in which:
+        gen_path()
