@@ -26,11 +26,17 @@ from .io import (CACHE_FORMAT, CACHE_VERSION, BaselineRecord, CacheFormatError, 
                  save_cache, save_cache_npz, write_pfm, write_ppm)
 from .renderer import (CACHE_MODES, MODES, CacheSet, Camera, FieldGrid, RenderSettings, populate_cache, render)
 from .scene import Medium, Scene, Surface, load_scene, save_scene
+from . import baseline, path  # noqa: E402  (submodules: b200.baseline.*, b200.path.*)
+from .baseline import (BaselineEstimate, baseline_estimate, log_gradient_radius, log_space_interpolate,
+                       make_baseline_record, occlusion_unaware_gradient)
+from .path import TransportDerivativeEstimate, fd_derivatives, path_trace_radiance
 
 __all__ = [
     "CACHE_FORMAT", "CACHE_MODES", "CACHE_VERSION", "MODES", "BaselineRecord", "CacheFormatError", "CacheSet",
     "Camera", "FieldGrid", "RenderSettings", "load_cache", "load_cache_npz", "populate_cache", "read_pfm", "render",
     "save_cache", "save_cache_npz", "write_pfm", "write_ppm",
+    "BaselineEstimate", "TransportDerivativeEstimate", "baseline_estimate", "fd_derivatives", "log_gradient_radius",
+    "log_space_interpolate", "make_baseline_record", "occlusion_unaware_gradient", "path_trace_radiance",
     "DEFAULT_N_ANGULAR", "BatchResult", "CacheRecord", "DeviceScene", "Moments", "RadianceCache",
     "Medium", "Scene", "Surface", "cache_from_records", "device_scene", "estimate_moments",
     "estimate_moments_batch", "inspect_record", "interpolate", "load_scene", "make_record",
