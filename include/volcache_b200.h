@@ -176,10 +176,13 @@ typedef struct {
   int estimator;         /* VC_EST_* used for direct evaluations at cache misses */
   int max_media_bounces; /* baseline and path estimators */
   int path_samples;      /* path estimator: path_samples_per_point */
+  int grow;              /* 1: frozen = False — misses insert their records (full image only) */
+  int isotropic;         /* grow + subdivision: mode "ours-iso" */
+  double baseline_alpha; /* grow + baseline */
 } vc_render_params;
 
-/* Frozen-cache camera render (src/renderer.py:402-484, mode ours-*, frozen=True):
- * camera march with cache lookups; steps no cache pair covers are evaluated directly
+/* Camera render (src/renderer.py:402-484): camera march with cache lookups.  Frozen
+ * (grow = 0): steps no cache pair covers are evaluated directly
  * through the record build with seeds (seed, 211, k, i, m).  image: height × width × 3
  * float64 (only the crop is written); stats: cache_hits, direct_evaluations. */
 int vc_render(vc_scene* scene, vc_cache* single, vc_cache* multiple, const vc_camera* camera,

@@ -906,14 +906,23 @@ class RenderParams:
     anisotropic: bool = True
 
 
-def point_value(ps, y, single: Cache, multiple: Cache, prm: RenderParams, seed, stats, adjacency_fn=None):
-    """Frozen-cache shading value at a march point (src/renderer.py:335-368)."""
+def point_value(ps, y, single: Cache, multiple: Cache, prm: RenderParams, seed, stats, adjacency_fn=None,
+                frozen=True):
+    """Shading value at a march point (src/renderer.py:335-368); frozen=False inserts."""
     a = interpolate(single, y)
     b = interpolate(multiple, y)
     if a is not None and b is not None:
         stats["cache_hits"] += 1
         return a + b
     stats["direct_evaluations"] += 1
+    if not frozen:
+        value, (rs, rm) = compute_pair(ps, y, prm, seed, adjacency_fn)
+        if a is None:
+            single.records.append(rs)
+        if b is None:
+            multiple.records.append(rm)
+        a2, b2 = interpolate(single, y), interpolate(multiple, y)
+        return a2 + b2 if (a2 is not None and b2 is not None) else value
     rb = build_record(
         ps, y, n_angular=prm.n_angular, march_step=prm.march_step, rng_seed=seed,
         n_inner=prm.n_inner, n_light_samples=prm.n_light_samples,
@@ -923,7 +932,7 @@ def point_value(ps, y, single: Cache, multiple: Cache, prm: RenderParams, seed, 
 
 
 def render_camera(ps, cam: dict, single: Cache, multiple: Cache, prm: RenderParams,
-                  pixels=None, adjacency_fn=None):
+                  pixels=None, adjacency_fn=None, frozen=True):
     """Frozen-cache camera image (src/renderer.py:440-484); `pixels` restricts to a crop.
 
     `cam` = {position, look_at, up, fov, width, height}.  Returns (image (h·w, 3), stats).
@@ -952,7 +961,8 @@ def render_camera(ps, cam: dict, single: Cache, multiple: Cache, prm: RenderPara
             for m in range(1, steps + 1):
                 tk = t_in[q] + (m - 0.5) * prm.march_step
                 y = o[i] + tk * d[i]
-                J = point_value(ps, y, single, multiple, prm, seed_seq(prm.seed, 211, k, i, m), stats, adjacency_fn)
+                J = point_value(ps, y, single, multiple, prm, seed_seq(prm.seed, 211, k, i, m), stats, adjacency_fn,
+                                frozen)
                 acc += np.exp(-sig * (tk - t_in[q])) * (4.0 * np.pi) * J * prm.march_step
             if idx[q] >= 0:
                 acc += np.exp(-sig * max(0.0, t_end[q] - t_in[q])) * lo[q]

@@ -71,6 +71,9 @@ class RenderParams(C.Structure):
         ("estimator", C.c_int),
         ("max_media_bounces", C.c_int),
         ("path_samples", C.c_int),
+        ("grow", C.c_int),
+        ("isotropic", C.c_int),
+        ("baseline_alpha", C.c_double),
     ]
 
 

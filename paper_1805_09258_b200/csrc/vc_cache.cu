@@ -345,9 +345,15 @@ struct MarchOut {
   uint32_t* miss_words;   // miss seeds (seed, 211, k, i, m)
   const double* miss_J;   // direct-evaluation results (pass 2)
   long long* hits;        // per crop pixel cache hits
+  const long long* first; // mode 3: first march-point ordinal per (pass, pixel)
+  const long long* c_ord; // mode 3: ordinals of the points that inserted records (sorted)
+  const double* c_val;    // mode 3: their direct values
+  long long c_n;
 };
 
-// mode 0: count misses; mode 1: write miss points + seeds; mode 2: final accumulation
+// mode 0: count misses; mode 1: write miss points + seeds; mode 2: final accumulation;
+// mode 3: final accumulation after insertion (frozen=False): each point reads the caches
+// as they were when it was reached (records of tag ≤ its ordinal), src/renderer.py:361-368
 __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
                                                double step, int seed, const uint64_t* jit_state, JumpTables jt,
                                                int n_light_dummy, MarchOut out, int mode) {
@@ -377,13 +383,13 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
     double tt = isfinite(ts) ? ts : 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) hp[a] = add(o[a], mul(tt, d[a]));
-    if (mode == 2) surface_radiance<3>(S, id, hp, d, lo);
+    if (mode >= 2) surface_radiance<3>(S, id, hp, d, lo);
     double t_in, t_out;
     bool valid;
     bounds_span(S, o, d, t_in, t_out, valid);
     double acc[3] = {0.0, 0.0, 0.0};
     if (!valid) {
-      if (mode == 2 && id >= 0) {
+      if (mode >= 2 && id >= 0) {
         img[0] += lo[0];
         img[1] += lo[1];
         img[2] += lo[2];
@@ -399,14 +405,26 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
 #pragma unroll
       for (int a = 0; a < 3; ++a) y[a] = add(o[a], mul(tk, d[a]));
       double Js[3], Jm[3];
-      bool cs = cache_interpolate<3>(Cs, y, Js, nullptr);
-      bool cm = cs && cache_interpolate<3>(Cm, y, Jm, nullptr);
+      long long lim = LLONG_MAX;
+      if (mode == 3) lim = out.first[(long long)k * cam.w * cam.h + i] + m;
+      bool cs = cache_interpolate<3>(Cs, y, Js, nullptr, lim);
+      bool cm = cs && cache_interpolate<3>(Cm, y, Jm, nullptr, lim);
       double J[3];
       if (cs && cm) {
         ++hits;
         J[0] = add(Js[0], Jm[0]);
         J[1] = add(Js[1], Jm[1]);
         J[2] = add(Js[2], Jm[2]);
+      } else if (mode == 3) {  // inserted, blend still None: the direct value
+        const long long ord = lim - 1;
+        long long lo = 0, hi = out.c_n;
+        while (lo < hi) {
+          long long mid = (lo + hi) >> 1;
+          if (out.c_ord[mid] < ord) lo = mid + 1;
+          else hi = mid;
+        }
+        const bool f = lo < out.c_n && out.c_ord[lo] == ord;
+        for (int c = 0; c < 3; ++c) J[c] = f ? out.c_val[lo * 3 + c] : 0.0;
       } else {
         if (mode == 1) {
           for (int a = 0; a < 3; ++a) out.miss_x[slot * 3 + a] = y[a];
@@ -425,13 +443,13 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
         ++slot;
         ++nm;
       }
-      if (mode == 2) {
+      if (mode >= 2) {
         double f = mul(mul(exp(-S.sigma_t * sub(tk, t_in)), four_pi), 1.0);
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[c] = add(acc[c], mul(mul(f, J[c]), step));
       }
     }
-    if (mode == 2) {
+    if (mode >= 2) {
       if (id >= 0) {
         double T = exp(-S.sigma_t * fmax(0.0, sub(t_end, t_in)));
 #pragma unroll
@@ -443,7 +461,7 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
     }
   }
   if (mode == 0) out.miss_cnt[t] = nm;
-  if (mode == 2) {
+  if (mode >= 2) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) out.image[i * 3 + c] = __ddiv_rn(img[c], (double)spp);
     out.hits[t] = hits;
@@ -580,8 +598,47 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
   mo.miss_cnt = mcnt;
   mo.miss_off = moff;
   mo.hits = hits;
-  DevCache Cs = cs->dev(), Cm = cm->dev();
   const int grid = (npx + 127) / 128;
+  if (rp->grow) {  // frozen = False: misses insert in (pass, pixel, step) order (src/renderer.py:361-368)
+    if (rp->estimator == VC_EST_PATH) return fail(VC_EINVAL, "the path mode has no cache to grow");
+    if (cam.rows != cam.h || cam.cols != cam.w) return fail(VC_EINVAL, "frozen=False renders the full image (no crop)");
+    vc_populate_params pp{};
+    pp.target = VC_TARGET_CAMERA;
+    pp.camera = C0;
+    pp.march_step = rp->march_step;
+    pp.seed = rp->seed;
+    pp.n_angular = rp->n_angular;
+    pp.n_inner = rp->n_inner;
+    pp.n_light_samples = rp->n_light_samples;
+    pp.epsilon = rp->epsilon > 0 ? rp->epsilon : 0.05;
+    pp.isotropic = rp->isotropic;
+    pp.estimator = rp->estimator;
+    pp.max_media_bounces = rp->max_media_bounces;
+    pp.baseline_alpha = rp->baseline_alpha;
+    RenderStream rs;
+    int64_t pst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    rc = populate_run(sc, &pp, 2, cs, cm, pst, st, nullptr, rp->spp, &rs);
+    if (rc) return rc;
+    mo.first = rs.first;
+    mo.c_ord = rs.c_ord;
+    mo.c_val = rs.c_val;
+    mo.c_n = rs.c_n;
+    k_march<<<grid, 128, 0, st>>>(S, cs->dev(), cm->dev(), cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo,
+                                  3);
+    count_launches(1);
+    e = cudaGetLastError();
+    for (int y = 0; y < cam.h && e == cudaSuccess; ++y)
+      e = cudaMemcpyAsync(image + (size_t)y * cam.w * 3, dimg + (size_t)y * cam.w * 3, (size_t)cam.w * 24,
+                          (flags & VC_MEM_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "render download");
+    if (stats) {
+      stats[0] = rs.total - pst[7];
+      stats[1] = pst[7];
+    }
+    return VC_OK;
+  }
+  DevCache Cs = cs->dev(), Cm = cm->dev();
   k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 0);
   std::vector<long long> hc(npx), ho(npx + 1, 0);
   e = cudaMemcpyAsync(hc.data(), mcnt, (size_t)npx * 8, cudaMemcpyDeviceToHost, st);

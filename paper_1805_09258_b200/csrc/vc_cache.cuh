@@ -133,6 +133,22 @@ __device__ inline void bounds_span(const DevScene& S, const double* o, const dou
   valid = t_out > t_in;
 }
 
+// Camera render with insertion: ray prefix over (pass, pixel) and the direct values of
+// the points that built records, in ordinal order (vc_populate.cu → vc_render).
+struct RenderStream {
+  long long* first = nullptr;
+  long long* c_ord = nullptr;
+  double* c_val = nullptr;
+  long long c_n = 0, total = 0;
+  ~RenderStream() {
+    cudaFree(first);
+    cudaFree(c_ord);
+    cudaFree(c_val);
+  }
+};
+int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
+                 int64_t* stats, cudaStream_t st, double* commit_J, int spp, RenderStream* rs);
+
 // Host-side cache management (vc_cache.cu).
 int make_dev_camera(const vc_camera& cam, DevCamera* out);
 int cache_init(vc_cache* c, int dim, const double* bmin, const double* bmax);

@@ -74,12 +74,25 @@ __device__ inline void stream_point(const MarchStream& S, long long ord, double*
 }
 
 // Pixel-center rays, first hit and medium span → march steps (src/renderer.py:290-299).
-__global__ void k_pop_rays(DevScene S, DevCamera cam, double step, double* ray, long long* steps) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cam.w * cam.h) return;
-  const int py = i / cam.w, px = i % cam.w;
+// Pass k of a render with spp > 1 jitters pixel i by rng.random((h, w, 2)) of the stream
+// SeedSequence(seed, 101) (src/renderer.py:446-450): draws k·h·w·2 + 2i, +1.
+__global__ void k_pop_rays(DevScene S, DevCamera cam, double step, int spp, const uint64_t* jit_state,
+                           JumpTables jt, double* ray, long long* steps) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long npx = (long long)cam.w * cam.h;
+  if (r >= npx * spp) return;
+  const int k = (int)(r / npx);
+  const long long i = r - (long long)k * npx;
+  const int py = (int)(i / cam.w), px = (int)(i % cam.w);
+  double jx = 0.5, jy = 0.5;
+  if (spp > 1) {
+    Pcg64 g = pcg_load(jit_state);
+    pcg_advance(g, (unsigned long long)((long long)k * npx * 2 + i * 2), jt);
+    jx = g.next_double();
+    jy = g.next_double();
+  }
   double o[3], d[3];
-  camera_ray(cam, px, py, 0.5, 0.5, o, d);
+  camera_ray(cam, px, py, jx, jy, o, d);
   double ts;
   int id;
   trace_closest<3>(S, o, d, ts, id);
@@ -93,11 +106,11 @@ __global__ void k_pop_rays(DevScene S, DevCamera cam, double step, double* ray, 
     double f = floor(__ddiv_rn(sub(t_end, t_in), step) + 0.5);
     if (f > 0.0) n = (long long)f;
   }
-  ray[(size_t)i * 4 + 0] = d[0];
-  ray[(size_t)i * 4 + 1] = d[1];
-  ray[(size_t)i * 4 + 2] = d[2];
-  ray[(size_t)i * 4 + 3] = t_in;
-  steps[i] = n;
+  ray[(size_t)r * 4 + 0] = d[0];
+  ray[(size_t)r * 4 + 1] = d[1];
+  ray[(size_t)r * 4 + 2] = d[2];
+  ray[(size_t)r * 4 + 3] = t_in;
+  steps[r] = n;
 }
 
 // 1. points [pos, pos+L) and their per-cache miss bits against records of smaller tag
@@ -125,6 +138,47 @@ __global__ void k_pop_first(const unsigned long long* keys, const int* vals, int
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nu) return;
   if (i == 0 || keys[i] != keys[i - 1]) flag[vals[i]] = 1;
+}
+
+// SeedSequence entropy of a march point: populate (seed, 401, i) (src/renderer.py:317),
+// field render (seed, 307, iy, ix) (:432-434), camera render (seed, 211, k, i, m) (:471)
+__global__ void k_pop_words(MarchStream M, long long pos, const int* js, int n, uint32_t seed, int kind, int npx,
+                            uint32_t* words) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const long long ord = pos + js[e];
+  const int nw = kind == 0 ? 3 : (kind == 1 ? 4 : 5);
+  uint32_t* w = words + (size_t)e * nw;
+  w[0] = seed;
+  if (kind == 0) {
+    w[1] = 401u;
+    w[2] = (uint32_t)(ord & 0xffffffffLL);
+  } else if (kind == 1) {
+    w[1] = 307u;
+    w[2] = (uint32_t)(ord / M.nx);
+    w[3] = (uint32_t)(ord % M.nx);
+  } else {
+    int lo = 0, hi = M.n_rays;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (M.first[mid] <= ord) lo = mid;
+      else hi = mid;
+    }
+    w[1] = 211u;
+    w[2] = (uint32_t)(lo / npx);
+    w[3] = (uint32_t)(lo % npx);
+    w[4] = (uint32_t)(ord - M.first[lo] + 1);
+  }
+}
+
+// committed builds of a camera render: (ordinal, L_s + L_m), appended in ordinal order
+__global__ void k_pop_commit_list(const double* WR, const int* slot, const long long* ord, int k, int D, int RS,
+                                  long long* c_ord, double* c_val) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= k) return;
+  const double* R = WR + (size_t)slot[q] * 2 * RS;
+  c_ord[q] = ord[q];
+  for (int c = 0; c < 3; ++c) c_val[(size_t)q * 3 + c] = add(R[D + c], R[RS + D + c]);
 }
 
 template <int D>
@@ -290,10 +344,19 @@ struct Engine {
   int D = 0;
   vc_build_params bp{};
   uint32_t seed = 0;
-  int seed_kind = 0;  // 0: populate (seed, 401, i); 1: field render (seed, 307, iy, ix)
+  int seed_kind = 0;  // 0: populate (seed, 401, i); 1: field render (seed, 307, iy, ix); 2: camera render
+  int npx = 1;        // camera pixels (seed kind 2)
   int estimator = VC_EST_SUBDIVISION;
   vc_baseline_params blp{};
   double* commit_J = nullptr;  // optional N × 3: direct value (L_s + L_m) of every point that built
+  bool commit_list = false;    // camera render: (ordinal, value) of every point that built
+  long long* c_ord = nullptr;
+  double* c_val = nullptr;
+  long long c_n = 0, c_cap = 0;
+  ~Engine() {
+    cudaFree(c_ord);
+    cudaFree(c_val);
+  }
   cudaStream_t st = nullptr;
   Workspace ws;
   int C = 2048;
@@ -517,6 +580,46 @@ int Engine::run() {
                                                                        commit_J);
       count_launches(1);
     }
+    if (commit_list && committed > 0) {
+      std::vector<int> cs_slot;
+      std::vector<long long> cs_ord;
+      for (int q = 0; q < E && pords[q] < stop; ++q)
+        if (hacc[q]) {
+          cs_slot.push_back(pslots[q]);
+          cs_ord.push_back(pords[q]);
+        }
+      const long long k = (long long)cs_slot.size();
+      if (c_n + k > c_cap) {  // grow (ordinals arrive sorted)
+        const long long cap = std::max<long long>(c_n + k, std::max<long long>(4096, 2 * c_cap));
+        long long* no = nullptr;
+        double* nv = nullptr;
+        e = cudaMalloc(&no, cap * 8);
+        if (e == cudaSuccess) e = cudaMalloc(&nv, cap * 24);
+        if (e == cudaSuccess && c_n) e = cudaMemcpyAsync(no, c_ord, c_n * 8, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess && c_n) e = cudaMemcpyAsync(nv, c_val, c_n * 24, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+          cudaFree(no);
+          cudaFree(nv);
+          return cuda_fail(e, "render commit list");
+        }
+        cudaFree(c_ord);
+        cudaFree(c_val);
+        c_ord = no;
+        c_val = nv;
+        c_cap = cap;
+      }
+      int* d1 = (int*)get(38, cs_slot.size() * 4);
+      long long* d2 = (long long*)get(39, cs_ord.size() * 8);
+      if (e != cudaSuccess) return cuda_fail(e, "render commit buffers");
+      e = cudaMemcpyAsync(d1, cs_slot.data(), cs_slot.size() * 4, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(d2, cs_ord.data(), cs_ord.size() * 8, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "render commit upload");
+      k_pop_commit_list<<<(int)((k + 127) / 128), 128, 0, st>>>(WR, d1, d2, (int)k, D, RS, c_ord + c_n,
+                                                                c_val + (size_t)c_n * 3);
+      count_launches(1);
+      c_n += k;
+    }
     if (keep_s < (int)rows_s.size()) {
       cache_truncate(cs, n0s + keep_s, st);
       rc = cache_rebuild(cs, st);
@@ -569,33 +672,18 @@ int Engine::run() {
         js.push_back(hj[q]);
       }
       const int nb2 = (int)js.size();
-      const int nw = bp.seed_words;
-      std::vector<uint32_t> words((size_t)nb2 * nw);
-      for (int i = 0; i < nb2; ++i) {
-        const long long ord = pos + js[i];
-        uint32_t* w = words.data() + (size_t)i * nw;
-        w[0] = seed;
-        if (seed_kind == 0) {  // SeedSequence([seed, 401, i]) (src/renderer.py:317)
-          w[1] = 401u;
-          w[2] = (uint32_t)(ord & 0xffffffffLL);
-        } else {  // SeedSequence([seed, 307, iy, ix]) (src/renderer.py:432-434)
-          w[1] = 307u;
-          w[2] = (uint32_t)(ord / M.nx);
-          w[3] = (uint32_t)(ord % M.nx);
-        }
-      }
       int* djs = (int*)get(24, (size_t)nb2 * 4);
       int* dns = (int*)get(25, (size_t)nb2 * 4);
       double* xb = (double*)get(26, (size_t)nb2 * D * 8);
-      uint32_t* dw = (uint32_t*)get(34, (size_t)nb2 * 16);
+      uint32_t* dw = (uint32_t*)get(34, (size_t)nb2 * 20);
       double* rec = (double*)get(35, (size_t)nb2 * RS2 * 8);
       double* mom = (double*)get(36, (size_t)nb2 * 2 * moment_size(D) * 8);
       long long* bst = (long long*)get(37, (size_t)nb2 * kStats * 8);
       if (e != cudaSuccess) return cuda_fail(e, "populate build buffers");
       e = cudaMemcpyAsync(djs, js.data(), (size_t)nb2 * 4, cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(dns, new_slot.data(), (size_t)nb2 * 4, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(dw, words.data(), words.size() * 4, cudaMemcpyHostToDevice, st);
       if (e != cudaSuccess) return cuda_fail(e, "populate build upload");
+      k_pop_words<<<(nb2 + 127) / 128, 128, 0, st>>>(M, pos, djs, nb2, seed, seed_kind, npx, dw);
       if (D == 2) k_pop_gather_x<2><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
       else k_pop_gather_x<3><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
       count_launches(1);
@@ -638,8 +726,10 @@ int Engine::run() {
 }  // namespace
 
 // Stream setup + engine run on existing caches (records with tag −1 pre-exist).
-int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
-                 int64_t* stats, cudaStream_t st, double* commit_J = nullptr) {
+// seed_kind 2 (camera render with insertion) marches spp jittered passes and hands the
+// ray prefix and the committed direct values to the caller through `rs`.
+int vc::populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
+                     int64_t* stats, cudaStream_t st, double* commit_J, int spp, RenderStream* rs) {
   if (!(pp->march_step > 0.0)) return fail(VC_EINVAL, "march_step must be positive");
   if (!(pp->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
   Engine g;
@@ -655,7 +745,8 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
   g.bp.n_light_samples = pp->n_light_samples;
   g.bp.epsilon = pp->epsilon;
   g.bp.flags = VC_SEED_WORDS | VC_MAKE_RECORDS | (pp->isotropic ? VC_ISOTROPIC : 0);
-  g.bp.seed_words = seed_kind == 0 ? 3 : 4;
+  g.bp.seed_words = seed_kind == 0 ? 3 : (seed_kind == 1 ? 4 : 5);
+  g.commit_list = rs != nullptr;
   g.estimator = pp->estimator == VC_EST_BASELINE ? VC_EST_BASELINE : VC_EST_SUBDIVISION;
   g.blp.n_angular = pp->n_angular;
   g.blp.max_media_bounces = pp->max_media_bounces;
@@ -695,7 +786,8 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
     g.N = (long long)M.nx * M.ny;
   } else if (pp->target == VC_TARGET_CAMERA) {
     if (sc->dim != 3) return fail(VC_EINVAL, "Camera rendering requires a 3D scene");
-    if (seed_kind != 0) return fail(VC_EINVAL, "camera render insertion is not a populate stream");
+    if (seed_kind == 1) return fail(VC_EINVAL, "field seeds on a camera target");
+    if (seed_kind == 0) spp = 1;
     DevCamera cam{};
     vc_camera c0 = pp->camera;
     c0.row0 = c0.col0 = 0;
@@ -703,21 +795,39 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
     int rc = make_dev_camera(c0, &cam);
     if (rc) return rc;
     const int npx = cam.w * cam.h;
-    cudaError_t e = cudaMalloc(&bf.ray, (size_t)npx * 32);
-    if (e == cudaSuccess) e = cudaMalloc(&bf.steps, ((size_t)npx + 1) * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&bf.first, ((size_t)npx + 1) * 8);
+    const long long nr = (long long)npx * spp;
+    if (nr > (1LL << 31) - 2) return fail(VC_EINVAL, "too many camera rays");
+    cudaError_t e = cudaMalloc(&bf.ray, (size_t)nr * 32);
+    if (e == cudaSuccess) e = cudaMalloc(&bf.steps, ((size_t)nr + 1) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&bf.first, ((size_t)nr + 1) * 8);
     if (e != cudaSuccess) return cuda_fail(e, "populate ray buffers");
     rc = ensure_emitters(sc, pp->n_light_samples);
     if (rc) return rc;
     DevScene S = dev_scene(sc);
-    k_pop_rays<<<(npx + 127) / 128, 128, 0, st>>>(S, cam, pp->march_step, bf.ray, bf.steps);
-    e = cudaMemsetAsync(bf.steps + npx, 0, 8, st);
+    uint64_t* djit = nullptr;
+    JumpTables jt{jump_tables(&e)};
+    if (!jt.tab) return cuda_fail(e, "jump tables");
+    if (spp > 1) {  // jitter stream default_rng(SeedSequence([seed, 101])) (src/renderer.py:446)
+      uint32_t jw[2] = {(uint32_t)pp->seed, 101u};
+      uint64_t jst[4];
+      seedseq_pcg64(jw, 2, jst);
+      e = cudaMalloc(&djit, 32);
+      if (e == cudaSuccess) e = cudaMemcpy(djit, jst, 32, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) {
+        cudaFree(djit);
+        return cuda_fail(e, "jitter state");
+      }
+    }
+    k_pop_rays<<<(int)((nr + 127) / 128), 128, 0, st>>>(S, cam, pp->march_step, spp, djit, jt, bf.ray, bf.steps);
+    e = cudaMemsetAsync(bf.steps + nr, 0, 8, st);
     size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, bf.steps, bf.first, npx + 1, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, bf.steps, bf.first, nr + 1, st);
     if (e == cudaSuccess) e = cudaMalloc(&bf.tmp, tb + 16);
-    if (e == cudaSuccess) cub::DeviceScan::ExclusiveSum(bf.tmp, tb, bf.steps, bf.first, npx + 1, st);
+    if (e == cudaSuccess) cub::DeviceScan::ExclusiveSum(bf.tmp, tb, bf.steps, bf.first, nr + 1, st);
     long long total = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, bf.first + npx, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, bf.first + nr, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(djit);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     count_launches(2);
     if (e != cudaSuccess) return cuda_fail(e, "populate rays");
@@ -725,7 +835,8 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
     for (int a = 0; a < 3; ++a) M.pos[a] = cam.pos[a];
     M.ray = bf.ray;
     M.first = bf.first;
-    M.n_rays = npx;
+    M.n_rays = (int)nr;
+    g.npx = npx;
     g.N = total;
   } else {
     return fail(VC_EINVAL, "target must be VC_TARGET_FIELD or VC_TARGET_CAMERA");
@@ -739,6 +850,16 @@ int populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_c
   }
   if (!rc && stats)
     for (int k = 0; k < 8; ++k) stats[k] = g.stats[k];
+  if (!rc && rs) {  // hand over the ray prefix and the committed direct values
+    rs->first = bf.first;
+    bf.first = nullptr;
+    rs->c_ord = g.c_ord;
+    rs->c_val = g.c_val;
+    rs->c_n = g.c_n;
+    g.c_ord = nullptr;
+    g.c_val = nullptr;
+    rs->total = g.N;
+  }
   return rc;
 }
 
@@ -798,7 +919,7 @@ int vc_populate(vc_scene* sc, const vc_populate_params* pp, vc_cache** single, v
   if (!rc) rc = cache_reserve(cm, 1024, st);
   if (!rc) rc = cache_rebuild(cs, st);
   if (!rc) rc = cache_rebuild(cm, st);
-  if (!rc) rc = populate_run(sc, pp, 0, cs, cm, stats, st);
+  if (!rc) rc = populate_run(sc, pp, 0, cs, cm, stats, st, nullptr, 1, nullptr);
   if (rc) {
     delete cs;
     delete cm;
@@ -836,7 +957,7 @@ int vc_render_field(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_populate_
     direct = (double*)ws.get(7, (size_t)n * 24, &e);
     if (e == cudaSuccess) e = cudaMemsetAsync(direct, 0xff, (size_t)n * 24, st);  // NaN: no direct value
     if (e != cudaSuccess) return cuda_fail(e, "field direct buffer");
-    int rc = populate_run(sc, pp, 1, cs, cm, pst, st, direct);
+    int rc = populate_run(sc, pp, 1, cs, cm, pst, st, direct, 1, nullptr);
     if (rc) return rc;
   }
   double* J = (double*)ws.get(0, (size_t)n * 24, &e);

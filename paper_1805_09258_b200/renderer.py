@@ -333,9 +333,6 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
             cache_set.single._device_changed()
             cache_set.multiple._device_changed()
     else:
-        if not settings.frozen:
-            raise NotImplementedError("camera render with frozen=False (insertion during the march) is not on "
-                                      "the B200 path; populate first or render frozen")
         cam = target._c()
         rp = _lib.RenderParams()
         rp.spp = int(settings.spp)
@@ -348,10 +345,16 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
         rp.estimator = _estimator(settings.mode)
         rp.max_media_bounces = int(settings.max_media_bounces)
         rp.path_samples = int(settings.path_samples_per_point)
+        rp.grow = 0 if settings.frozen else 1
+        rp.isotropic = 1 if settings.mode == "ours-iso" else 0
+        rp.baseline_alpha = float(settings.baseline_alpha)
         image = np.zeros((target.height, target.width, 3))
         hs, hm = cache_set._handles()
         _lib.check(_lib.lib().vc_render(ds.handle, hs, hm, _lib.C.byref(cam), _lib.C.byref(rp), _lib.ptr(image),
                                         _lib.ptr(out), _lib.VC_MEM_HOST, None))
+        if not settings.frozen:
+            cache_set.single._device_changed()
+            cache_set.multiple._device_changed()
     if not path:  # the reference counts hits/evaluations only in the cache modes
         stats["cache_hits"] = int(out[0])
         stats["direct_evaluations"] = int(out[1])

@@ -590,8 +590,31 @@ def gen_path():
     np.savez_compressed(OUT / "path.npz", **out)
 
 
+def gen_grow():
+    """Camera render with frozen=False (insertion during the march, src/renderer.py:361-368)."""
+    bundled = Path("/root/reference/pkg/scenes")
+    box = vscene.load_scene(bundled / "box3d.json")
+    out = {"versions": VERSIONS}
+    out.update(scene_fields("box_", box))
+    cam = vr.Camera(position=np.array([0.5, 0.3, 0.05]), look_at=np.array([0.5, 0.5, 1.0]),
+                    up=np.array([0.0, 1.0, 0.0]), fov_degrees=70.0, width=4, height=3)
+    out["camera"] = np.concatenate([cam.position, cam.look_at, cam.up, [cam.fov_degrees, cam.width, cam.height]])
+    for mode in ("baseline", "ours-aniso"):
+        st = vr.RenderSettings(mode=mode, epsilon=0.1, march_step=0.2, n_angular=128, n_light_samples=4, seed=21,
+                               spp=2, frozen=False)
+        cs = vr.CacheSet(box, mode)
+        img, stats = vr.render(box, cam, st, cache_set=cs)
+        key = mode.replace("-", "_")
+        out[f"{key}_image"] = img
+        out[f"{key}_stats"] = np.array([stats["cache_hits"], stats["direct_evaluations"], len(cs.single),
+                                        len(cs.multiple)])
+        out.update(_records_fields(f"{key}_single", cs.single))
+        out.update(_records_fields(f"{key}_multiple", cs.multiple))
+    np.savez_compressed(OUT / "grow.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline", "path"]
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline", "path", "grow"]
     if "ff" in which:
         gen_formfactors()
     if "trace" in which:
@@ -612,3 +635,5 @@ if __name__ == "__main__":
         gen_baseline()
     if "path" in which:
         gen_path()
+    if "grow" in which:
+        gen_grow()

@@ -182,3 +182,18 @@ def test_render_field_matches_reference():
         z["render_grow_stats"].tolist()
     np.testing.assert_allclose(img, z["render_grow_image"], rtol=1e-11)
     _assert_rows(_rows(s), z["render_grow_single"], 2)
+
+
+def test_render_camera_growing_matches_reference():
+    """frozen=False camera render (insertion during the march) vs the reference's run."""
+    z = golden("grow")
+    ps = O.pack(golden_scene(z, "box_"))
+    v = z["camera"]
+    cam = dict(position=v[0:3], look_at=v[3:6], up=v[6:9], fov=float(v[9]), width=int(v[10]), height=int(v[11]))
+    prm = O.RenderParams(epsilon=0.1, spp=2, march_step=0.2, n_angular=128, seed=21, n_light_samples=4)
+    s, m = O.Cache(), O.Cache()
+    img, st = O.render_camera(ps, cam, s, m, prm, frozen=False)
+    assert [st["cache_hits"], st["direct_evaluations"], len(s.records), len(m.records)] == \
+        z["ours_aniso_stats"].tolist()
+    np.testing.assert_allclose(img.reshape(z["ours_aniso_image"].shape), z["ours_aniso_image"], rtol=1e-11)
+    _assert_rows(_rows(s), z["ours_aniso_single"], 3)

@@ -223,3 +223,50 @@ def test_populate_validation():
         render(sc2, "not a target", RenderSettings())
     with pytest.raises(ValueError):
         CacheSet(sc2, "path")
+
+
+def test_render_camera_growing_baseline_matches_reference():
+    """frozen=False camera render in baseline mode (no triangulation): equal to the reference."""
+    from paper_1805_09258_b200.renderer import CacheSet, RenderSettings, render
+
+    z = golden("grow")
+    sc = golden_scene(z, "box_")
+    cam = _camera(z["camera"])
+    st = RenderSettings(mode="baseline", epsilon=0.1, march_step=0.2, n_angular=128, n_light_samples=4, seed=21,
+                        spp=2, frozen=False)
+    cs = CacheSet(sc, "baseline")
+    img, stats = render(sc, cam, st, cache_set=cs)
+    assert [stats["cache_hits"], stats["direct_evaluations"], len(cs.single), len(cs.multiple)] == \
+        z["baseline_stats"].tolist()
+    np.testing.assert_array_equal(cs.single.packed()[:, :3], z["baseline_single"][:, :3])
+    assert rel_l2(cs.multiple.packed(), z["baseline_multiple"]) <= 1e-9
+    assert rel_l2(img, z["baseline_image"]) <= 1e-9
+
+
+def test_render_camera_growing_matches_oracle():
+    """frozen=False camera render, subdivision records: vs the oracle with the GPU triangulations."""
+    from oracle import volcache_oracle as O
+    from paper_1805_09258_b200 import inspect_record
+    from paper_1805_09258_b200.renderer import CacheSet, RenderSettings, render
+
+    z = golden("grow")
+    sc = golden_scene(z, "box_")
+    cam = _camera(z["camera"])
+    st = RenderSettings(mode="ours-aniso", epsilon=0.1, march_step=0.2, n_angular=128, n_light_samples=4, seed=21,
+                        spp=2, frozen=False)
+    cs = CacheSet(sc, "ours-aniso")
+    img, stats = render(sc, cam, st, cache_set=cs)
+    center = 0.5 * (sc.bounds_min + sc.bounds_max)
+
+    def gpu_adjacency(seed):
+        return inspect_record(sc, center, rng_seed=seed, n_angular=128, march_step=0.2)["tris"]
+
+    v = z["camera"]
+    ocam = dict(position=v[0:3], look_at=v[3:6], up=v[6:9], fov=float(v[9]), width=int(v[10]), height=int(v[11]))
+    prm = O.RenderParams(epsilon=0.1, spp=2, march_step=0.2, n_angular=128, seed=21, n_light_samples=4)
+    s, m = O.Cache(), O.Cache()
+    oimg, ost = O.render_camera(O.pack(sc), ocam, s, m, prm, adjacency_fn=gpu_adjacency, frozen=False)
+    assert (stats["cache_hits"], stats["direct_evaluations"]) == (ost["cache_hits"], ost["direct_evaluations"])
+    _same_records(cs.single.packed(), _oracle_rows(s), 3)
+    _same_records(cs.multiple.packed(), _oracle_rows(m), 3)
+    assert rel_l2(img, oimg.reshape(img.shape)) <= 1e-4
