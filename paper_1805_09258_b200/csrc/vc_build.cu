@@ -443,9 +443,10 @@ __device__ __forceinline__ Line cell_line(int lab, const double* p, const double
 }
 
 __device__ __forceinline__ void meet(const Line& l1, const Line& l2, double& a, double& b) {
-  double det = l1.A * l2.B - l2.A * l1.B;
-  a = (l1.B * l2.C - l2.B * l1.C) / det;
-  b = (l2.A * l1.C - l1.A * l2.C) / det;
+  const double det = l1.A * l2.B - l2.A * l1.B;
+  const double inv = 1.0 / det;
+  a = (l1.B * l2.C - l2.B * l1.C) * inv;
+  b = (l2.A * l1.C - l1.A * l2.C) * inv;
 }
 
 // Cell polygon held in shared memory, [vertex][thread] layout (bank-conflict free): the
@@ -499,9 +500,14 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
   poly.A(2) = -L; poly.B(2) = L;  poly.L(2) = -3;
   poly.A(3) = -L; poly.B(3) = -L; poly.L(3) = -4;
   double t2R = 2.0 * L * L;
-  auto cos2R = [&]() { return t2R >= 1.0 ? -1.0 : (1.0 - t2R) / (1.0 + t2R); };
-  double cut = cos2R();
-  float cutf = (float)cut - 2e-6f;
+  // a candidate q can cut the cell only if ∠(p, q) < 2·R_cell, i.e. p·q > cos 2R =
+  // (1 − tan²R)/(1 + tan²R); tested in float32 with a margin (2e-6) far above the
+  // rounding of the float32 directions, dot and bound — a looser cut only costs time
+  auto cutf_of = [](double t) {
+    const float tf = (float)t;
+    return __fdividef(1.0f - tf, 1.0f + tf) - 2e-6f;
+  };
+  float cutf = cutf_of(t2R);
   // candidate rows: bands meeting z ∈ [cos(θ+α), cos(θ−α)]; columns: azimuth half-width
   // asin(sin α / sin θ)
   const double sa = ang.sin_a, ca = ang.cos_a;
@@ -541,7 +547,6 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
       if (!(p32.x * q4.x + p32.y * q4.y + p32.z * q4.z > cutf)) continue;
       const double* q = dirs + 3 * (size_t)j;
       const double qx = q[0], qy = q[1], qz = q[2];
-      if (!(px * qx + py * qy + pz * qz > cut)) continue;
       const double d0 = px - qx, d1 = py - qy, d2 = pz - qz;
       const Line ln = {e1[0] * d0 + e1[1] * d1 + e1[2] * d2, e2[0] * d0 + e2[1] * d1 + e2[2] * d2,
                        px * d0 + py * d1 + pz * d2};
@@ -580,18 +585,17 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
         poly.A(s + 1) = ya; poly.B(s + 1) = yb; poly.L(s + 1) = lab_e;
       } else {
         // run wraps: keep [e+1, s) moved to the front, then X Y
-        const int K = s - e - 1;
-        for (int v = 0; v < K; ++v) {
+        const int nk = s - e - 1;
+        for (int v = 0; v < nk; ++v) {
           poly.A(v) = poly.A(e + 1 + v); poly.B(v) = poly.B(e + 1 + v); poly.L(v) = poly.L(e + 1 + v);
         }
-        poly.A(K) = xa; poly.B(K) = xb; poly.L(K) = j;
-        poly.A(K + 1) = ya; poly.B(K + 1) = yb; poly.L(K + 1) = lab_e;
+        poly.A(nk) = xa; poly.B(nk) = xb; poly.L(nk) = j;
+        poly.A(nk + 1) = ya; poly.B(nk + 1) = yb; poly.L(nk + 1) = lab_e;
       }
       m = m_new;
       t2R = 0.0;
       for (int v = 0; v < m; ++v) t2R = fmax(t2R, poly.A(v) * poly.A(v) + poly.B(v) * poly.B(v));
-      cut = cos2R();
-      cutf = (float)cut - 2e-6f;
+      cutf = cutf_of(t2R);
     }
   }
   for (int v = 0; v < m; ++v)
