@@ -546,7 +546,7 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     if (e == cudaSuccess && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
   };
   // a primitive subset (original ids `ids`) → BVH (when large enough) + leaf-order prims
-  auto make_set = [&](const std::vector<int>& ids, int bvh_min, GpuBvh& g) {
+  auto make_set = [&](const std::vector<int>& ids, int bvh_min, GpuBvh& g, int leaf_max) {
     const int Ks = (int)ids.size();
     g.K = Ks;
     std::vector<int> order(ids);
@@ -555,7 +555,7 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
       std::vector<double> vs((size_t)Ks * dim * dim);
       for (int i = 0; i < Ks; ++i)
         std::memcpy(&vs[(size_t)i * dim * dim], &sc->verts[(size_t)ids[i] * dim * dim], dim * dim * 8);
-      build_bvh(dim, Ks, vs.data(), 1e-5 * sc->scale, &bvh);
+      build_bvh(dim, Ks, vs.data(), 1e-5 * sc->scale, &bvh, leaf_max);
       for (int i = 0; i < Ks; ++i) order[i] = ids[bvh.order[i]];
     }
     std::vector<double> leaf((size_t)Ks * ps);
@@ -574,8 +574,12 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     const double* E = &sc->emission[3 * (size_t)k];
     if (E[0] > 0.0 || E[1] > 0.0 || E[2] > 0.0) em.push_back(k);
   }
-  make_set(all, 16, sc->geo);
-  make_set(em, 4, sc->emit);
+  auto leaf_env = [](const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+  };
+  make_set(all, 16, sc->geo, leaf_env("VOLCACHE_LEAF_GEO", 2));  // leaf ≤ 2: fewer float64 tests
+  make_set(em, 4, sc->emit, leaf_env("VOLCACHE_LEAF_EMIT", 2));
   up((void**)&sc->d_normal, K ? normal.data() : nullptr, normal.size() * 8);
   up((void**)&sc->d_emission, K ? sc->emission.data() : nullptr, sc->emission.size() * 8);
   up((void**)&sc->d_albedo, K ? sc->albedo.data() : nullptr, sc->albedo.size() * 8);

@@ -34,7 +34,7 @@ struct HostBVH {
   float4* nodes = nullptr;  // host array, 2*n_nodes
   int* order = nullptr;     // leaf order → original primitive
 };
-void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out);
+void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, int leaf_max = 0);
 void free_bvh(HostBVH* b);
 
 }  // namespace vc

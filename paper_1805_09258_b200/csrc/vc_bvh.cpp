@@ -44,11 +44,12 @@ struct Node {
 };
 
 constexpr int kBins = 16;
-constexpr int kLeafMax = 4;
+constexpr int kLeafDefault = 4;
 
 }  // namespace
 
-void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out) {
+void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, int leaf_max) {
+  const int kLeafMax = leaf_max > 0 ? leaf_max : kLeafDefault;
   std::vector<Box> pb(K);
   std::vector<float> cen(3 * (size_t)K);
   const int nv = dim;  // vertices per primitive
