@@ -530,6 +530,80 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
   }
   const int span = max(r0 - rlo, rhi - r0);
   const int ncol_iter = (half >= cols) ? cols : 2 * half + 1;
+  // clip the cell by the bisector of (p, q_j); 2 = polygon overflow
+  auto consider = [&](const int j) -> int {
+    // float32 pre-test (one 16-byte load); its margin 2e-6 ≫ the float32 rounding error
+    const float4 q4 = __ldg(dirs32 + j);
+    if (!(p32.x * q4.x + p32.y * q4.y + p32.z * q4.z > cutf)) return 0;
+    const double* q = dirs + 3 * (size_t)j;
+    const double qx = q[0], qy = q[1], qz = q[2];
+    const double d0 = px - qx, d1 = py - qy, d2 = pz - qz;
+    const Line ln = {e1[0] * d0 + e1[1] * d1 + e1[2] * d2, e2[0] * d0 + e2[1] * d1 + e2[2] * d2,
+                     px * d0 + py * d1 + pz * d2};
+    unsigned out = 0;
+    for (int v = 0; v < m; ++v) out |= (ln.A * poly.A(v) + ln.B * poly.B(v) + ln.C < 0.0 ? 1u : 0u) << v;
+    if (!out) return 0;
+    const unsigned full = (1u << m) - 1u;
+    if (out == full) return 2;  // cannot happen: p (the origin) is inside every bisector
+    // convex polygon: the outside vertices form one cyclic run [s, e]
+    const unsigned prev = ((out << 1) | (out >> (m - 1))) & full;  // bit v: out[v−1]
+    const unsigned next = ((out >> 1) | (out << (m - 1))) & full;  // bit v: out[v+1]
+    const int s = __ffs(out & ~prev) - 1;
+    const int e = __ffs(out & ~next) - 1;
+    const int sp = (s + m - 1) % m;  // inside vertex before the run
+    const int L_out = __popc(out);
+    const int m_new = m - L_out + 2;
+    if (m_new > Poly::kCap) return 2;
+    // X = edge(sp) ∩ bisector, Y = bisector ∩ edge(e); cyclic order … sp, X, Y, e+1 …
+    const int lab_e = poly.L(e);
+    double xa, xb, ya, yb;
+    meet(cell_line(poly.L(sp), pp, e1, e2, dirs, L), ln, xa, xb);
+    meet(ln, cell_line(lab_e, pp, e1, e2, dirs, L), ya, yb);
+    if (s <= e) {
+      // run inside the array: [0, s) X Y [e+1, m) — shift the tail by 2 − L_out in place
+      const int shift = 2 - L_out;
+      if (shift < 0) {
+        for (int v = e + 1; v < m; ++v) {
+          poly.A(v + shift) = poly.A(v); poly.B(v + shift) = poly.B(v); poly.L(v + shift) = poly.L(v);
+        }
+      } else if (shift > 0) {
+        for (int v = m - 1; v > e; --v) {
+          poly.A(v + shift) = poly.A(v); poly.B(v + shift) = poly.B(v); poly.L(v + shift) = poly.L(v);
+        }
+      }
+      poly.A(s) = xa; poly.B(s) = xb; poly.L(s) = j;
+      poly.A(s + 1) = ya; poly.B(s + 1) = yb; poly.L(s + 1) = lab_e;
+    } else {
+      // run wraps: keep [e+1, s) moved to the front, then X Y
+      const int nk = s - e - 1;
+      for (int v = 0; v < nk; ++v) {
+        poly.A(v) = poly.A(e + 1 + v); poly.B(v) = poly.B(e + 1 + v); poly.L(v) = poly.L(e + 1 + v);
+      }
+      poly.A(nk) = xa; poly.B(nk) = xb; poly.L(nk) = j;
+      poly.A(nk + 1) = ya; poly.B(nk + 1) = yb; poly.L(nk + 1) = lab_e;
+    }
+    m = m_new;
+    t2R = 0.0;
+    for (int v = 0; v < m; ++v) t2R = fmax(t2R, poly.A(v) * poly.A(v) + poly.B(v) * poly.B(v));
+    cutf = cutf_of(t2R);
+    return 0;
+  };
+  // regular cells first take their 8 stratum neighbours, which are nearly always Delaunay
+  // neighbours: the lanes of a warp (adjacent cells of one row) then clip together, and
+  // the later, farther candidates mostly fail the cut pre-test
+  const bool pro = half < cols;
+  if (pro) {
+    for (int t = 0; t < 8; ++t) {
+      const int dr = (t < 2) ? 0 : ((t < 4) ? ((t & 1) ? 1 : -1) : ((t < 6) ? -1 : 1));
+      const int dc = (t < 2) ? ((t & 1) ? 1 : -1) : ((t < 4) ? 0 : ((t & 1) ? 1 : -1));
+      const int row = r0 + dr;
+      if (row < rlo || row > rhi) continue;
+      int col = c0 + dc;
+      if (col < 0) col += cols;
+      else if (col >= cols) col -= cols;
+      if (consider(row * cols + col) == 2) return 2;
+    }
+  }
   for (int rr = 0; rr <= 2 * span; ++rr) {
     // rows outward from r0 (nearest first), skipping rows outside [rlo, rhi]
     int dr = (rr + 1) >> 1;
@@ -537,65 +611,13 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
     if (row < rlo || row > rhi) continue;
     for (int cc = 0; cc < ncol_iter; ++cc) {
       int dc = (cc + 1) >> 1;
+      if (pro && dr <= 1 && dc <= 1) continue;  // taken above
       int col = (cc & 1) ? c0 - dc : c0 + dc;
       if (col < 0) col += cols;
       else if (col >= cols) col -= cols;
       const int j = row * cols + col;
       if (j == i) continue;
-      // float32 pre-test (one 16-byte load); its margin 2e-6 ≫ the float32 rounding error
-      const float4 q4 = __ldg(dirs32 + j);
-      if (!(p32.x * q4.x + p32.y * q4.y + p32.z * q4.z > cutf)) continue;
-      const double* q = dirs + 3 * (size_t)j;
-      const double qx = q[0], qy = q[1], qz = q[2];
-      const double d0 = px - qx, d1 = py - qy, d2 = pz - qz;
-      const Line ln = {e1[0] * d0 + e1[1] * d1 + e1[2] * d2, e2[0] * d0 + e2[1] * d1 + e2[2] * d2,
-                       px * d0 + py * d1 + pz * d2};
-      unsigned out = 0;
-      for (int v = 0; v < m; ++v) out |= (ln.A * poly.A(v) + ln.B * poly.B(v) + ln.C < 0.0 ? 1u : 0u) << v;
-      if (!out) continue;
-      const unsigned full = (1u << m) - 1u;
-      if (out == full) return 2;  // cannot happen: p (the origin) is inside every bisector
-      // convex polygon: the outside vertices form one cyclic run [s, e]
-      const unsigned prev = ((out << 1) | (out >> (m - 1))) & full;  // bit v: out[v−1]
-      const unsigned next = ((out >> 1) | (out << (m - 1))) & full;  // bit v: out[v+1]
-      const int s = __ffs(out & ~prev) - 1;
-      const int e = __ffs(out & ~next) - 1;
-      const int sp = (s + m - 1) % m;  // inside vertex before the run
-      const int L_out = __popc(out);
-      const int m_new = m - L_out + 2;
-      if (m_new > Poly::kCap) return 2;
-      // X = edge(sp) ∩ bisector, Y = bisector ∩ edge(e); cyclic order … sp, X, Y, e+1 …
-      const int lab_e = poly.L(e);
-      double xa, xb, ya, yb;
-      meet(cell_line(poly.L(sp), pp, e1, e2, dirs, L), ln, xa, xb);
-      meet(ln, cell_line(lab_e, pp, e1, e2, dirs, L), ya, yb);
-      if (s <= e) {
-        // run inside the array: [0, s) X Y [e+1, m) — shift the tail by 2 − L_out in place
-        const int shift = 2 - L_out;
-        if (shift < 0) {
-          for (int v = e + 1; v < m; ++v) {
-            poly.A(v + shift) = poly.A(v); poly.B(v + shift) = poly.B(v); poly.L(v + shift) = poly.L(v);
-          }
-        } else if (shift > 0) {
-          for (int v = m - 1; v > e; --v) {
-            poly.A(v + shift) = poly.A(v); poly.B(v + shift) = poly.B(v); poly.L(v + shift) = poly.L(v);
-          }
-        }
-        poly.A(s) = xa; poly.B(s) = xb; poly.L(s) = j;
-        poly.A(s + 1) = ya; poly.B(s + 1) = yb; poly.L(s + 1) = lab_e;
-      } else {
-        // run wraps: keep [e+1, s) moved to the front, then X Y
-        const int nk = s - e - 1;
-        for (int v = 0; v < nk; ++v) {
-          poly.A(v) = poly.A(e + 1 + v); poly.B(v) = poly.B(e + 1 + v); poly.L(v) = poly.L(e + 1 + v);
-        }
-        poly.A(nk) = xa; poly.B(nk) = xb; poly.L(nk) = j;
-        poly.A(nk + 1) = ya; poly.B(nk + 1) = yb; poly.L(nk + 1) = lab_e;
-      }
-      m = m_new;
-      t2R = 0.0;
-      for (int v = 0; v < m; ++v) t2R = fmax(t2R, poly.A(v) * poly.A(v) + poly.B(v) * poly.B(v));
-      cutf = cutf_of(t2R);
+      if (consider(j) == 2) return 2;
     }
   }
   for (int v = 0; v < m; ++v)
