@@ -300,7 +300,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   per += media_per / 10 * 72;                     // two-pass gather queue
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
-  per += (size_t)n * 16 + kAsmSplit * 96 * 8;     // DirInfo + assembly partials
+  per += (size_t)n * 16 + kAsmParts * 96 * 8;     // DirInfo + assembly partials
   if (sc->budget <= 0) {  // default scratch budget: 1/4 of HBM (B200: 45 GB), ≤ 48 GiB
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -344,7 +344,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.del_retry = (int*)alloc(38, (size_t)W.del_retry_cap * 4);
   W.del_retry_count = (unsigned int*)alloc(39, 8);
   W.del_scratch = (double*)alloc(40, D == 3 ? (size_t)W.del_retry_cap * 48 * 3 * 8 : 16);
-  W.partial = (double*)alloc(37, B * kAsmSplit * 64 * 8 + B * kAsmSplit * 5 * 8);  // sums + 5 counters
+  W.partial = (double*)alloc(37, B * kAsmParts * 64 * 8 + B * kAsmParts * 5 * 8);  // sums + 5 counters
   W.live_words = (P.r_ub + 63) / 64;
   W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);
   // two-pass gather queue (emitter hits; overflow falls back to in-place resolution)

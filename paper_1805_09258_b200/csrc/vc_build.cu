@@ -770,10 +770,6 @@ __global__ void k_degree(BuildParams P, Wave W) {
 // Moment assembly (src/subdivision.py:287-370)
 // ---------------------------------------------------------------------------
 
-#ifndef VC_ASM_BS
-#define VC_ASM_BS 128
-#endif
-constexpr int kAsmBS = VC_ASM_BS;
 constexpr int kQCap = 64;
 
 template <int D>
@@ -815,14 +811,14 @@ __global__ void __launch_bounds__(kAsmBS, 512 / kAsmBS) k_assemble(DevScene S, B
   constexpr int NW = kAsmBS / 32;
   static_assert(3 * NQ <= 32, "contribution vector must fit one warp");
   __shared__ uint2 queue[NW][kQCap];
-  __shared__ double red[NW][32];
-  __shared__ long long redc[NW][2];
   const int rec = blockIdx.y, part = blockIdx.x;  // kAsmSplit CTAs share one record
   const int n = P.n_angular;
   const int E = (D == 2) ? n : P.n_tris;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* out_part = W.partial + ((size_t)rec * kAsmSplit + part) * 64;
-  long long* out_cnt = (long long*)(W.partial + (size_t)W.B * kAsmSplit * 64) + ((size_t)rec * kAsmSplit + part) * 5;
+  // every warp writes its own partial sums (no block barrier: warps finish independently)
+  const size_t slot = (size_t)rec * kAsmParts + (size_t)part * NW + wid;
+  double* out_part = W.partial + slot * 64;
+  long long* out_cnt = (long long*)(W.partial + (size_t)W.B * kAsmParts * 64) + slot * 5;
   if (D == 3 && W.tri_status[rec] != 0) return;  // k_asm_final reports the failure
   const DirInfo* info = W.info + (size_t)rec * n;
   const size_t rb = (size_t)rec * n;
@@ -1034,26 +1030,11 @@ __global__ void __launch_bounds__(kAsmBS, 512 / kAsmBS) k_assemble(DevScene S, B
     if (qn > 0) evaluate(queue[wid][lane], lane < qn);
     __syncwarp();
 
-    // lane l of every warp holds component l: shared-memory tree across warps
-    red[wid][lane] = acc;
-    __syncthreads();
-    if (threadIdx.x < 32) {  // this CTA's partial sums, component order c·NQ + t
-      double v = 0.0;
-      for (int w = 0; w < NW; ++w) v += red[w][threadIdx.x];
-      out_part[kind * 32 + threadIdx.x] = v;
-    }
-    __syncthreads();
+    // lane l holds component l (order c·NQ + t) of this warp's sum
+    out_part[kind * 32 + lane] = acc;
   }
 
   // counters: evaluated / dropped / per-kind evaluated
-  long long cs[4] = {n_eval, n_drop, ev_kind[0], ev_kind[1]};
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], o);
-  __shared__ long long cred[NW][4];
-  if (lane == 0)
-    for (int k = 0; k < 4; ++k) cred[wid][k] = cs[k];
   // star vertices: Σ_k [idx_k ≥ 0] · deg_k · (maxc − cnt_k)  (src/subdivision.py:205-207)
   const int maxc = W.rec_maxc[rec];
   long long stars = 0;
@@ -1063,19 +1044,14 @@ __global__ void __launch_bounds__(kAsmBS, 512 / kAsmBS) k_assemble(DevScene S, B
       stars += (long long)dg * (maxc - cnt[k]);
     }
   }
+  // counters: evaluated / dropped / per-kind evaluated / stars
+  long long cs[5] = {n_eval, n_drop, ev_kind[0], ev_kind[1], stars};
 #pragma unroll
-  for (int o = 16; o; o >>= 1) stars += __shfl_xor_sync(0xffffffffu, stars, o);
-  if (lane == 0) redc[wid][0] = stars;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long t[4] = {0, 0, 0, 0}, st = 0;
-    for (int w = 0; w < NW; ++w) {
-      for (int k = 0; k < 4; ++k) t[k] += cred[w][k];
-      st += redc[w][0];
-    }
-    for (int k = 0; k < 4; ++k) out_cnt[k] = t[k];
-    out_cnt[4] = st;
-  }
+  for (int k = 0; k < 5; ++k)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], o);
+  if (lane == 0)
+    for (int k = 0; k < 5; ++k) out_cnt[k] = cs[k];
 }
 
 // Fixed-order sum of the kAsmSplit partials per record (deterministic), scattered into
@@ -1090,7 +1066,7 @@ __global__ void k_asm_final(BuildParams P, Wave W) {
   if (comp < 3 * NQ) {
     double v = 0.0;
     if (!failed)
-      for (int p = 0; p < kAsmSplit; ++p) v += W.partial[((size_t)rec * kAsmSplit + p) * 64 + kind * 32 + comp];
+      for (int p = 0; p < kAsmParts; ++p) v += W.partial[((size_t)rec * kAsmParts + p) * 64 + kind * 32 + comp];
     const int c = comp / NQ, t = comp - c * NQ;
     double* M = W.moments + ((size_t)rec * 2 + kind) * moment_size(D);
     if (t == 0) {
@@ -1106,11 +1082,11 @@ __global__ void k_asm_final(BuildParams P, Wave W) {
     }
   }
   if (tid == 0) {
-    const long long* cnt = (const long long*)(W.partial + (size_t)W.B * kAsmSplit * 64);
+    const long long* cnt = (const long long*)(W.partial + (size_t)W.B * kAsmParts * 64);
     long long t[5] = {0, 0, 0, 0, 0};
     if (!failed)
-      for (int p = 0; p < kAsmSplit; ++p)
-        for (int k = 0; k < 5; ++k) t[k] += cnt[((size_t)rec * kAsmSplit + p) * 5 + k];
+      for (int p = 0; p < kAsmParts; ++p)
+        for (int k = 0; k < 5; ++k) t[k] += cnt[((size_t)rec * kAsmParts + p) * 5 + k];
     long long* o = W.stats + (size_t)rec * kStats;
     o[0] = t[0];
     o[1] = t[1];

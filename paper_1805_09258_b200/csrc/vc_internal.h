@@ -18,9 +18,14 @@ namespace vc {
 constexpr int kMaxDim = 3;
 constexpr int kBvhMaxDepth = 32;  // BVH depth cap = device traversal stack size
 #ifndef VC_ASM_SPLIT
-#define VC_ASM_SPLIT 8
+#define VC_ASM_SPLIT 16
+#endif
+#ifndef VC_ASM_BS
+#define VC_ASM_BS 64
 #endif
 constexpr int kAsmSplit = VC_ASM_SPLIT;  // CTAs per record in the moment assembly
+constexpr int kAsmBS = VC_ASM_BS;        // threads per assembly CTA
+constexpr int kAsmParts = kAsmSplit * (kAsmBS / 32);  // per-warp partial sums per record
 
 // A BVH over a primitive set: float32 nodes, float64 primitives in leaf order.
 struct DevBvh {
@@ -84,7 +89,7 @@ struct alignas(16) DirInfo {
 // Per-record scratch for one wave (device pointers).
 struct Wave {
   DirInfo* info;         // B × n
-  double* partial;       // B × kAsmSplit × 2 × 32 assembly partial sums
+  double* partial;       // B × kAsmParts × 2 × 32 assembly partial sums (+ counters)
   int B;                 // records in this wave
   const double* x;       // B × dim
   const uint64_t* rng;   // B × 4: state_hi, state_lo, inc_hi, inc_lo (PCG64, numpy layout)
