@@ -330,7 +330,8 @@ def main():
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(dom)
+            tj = json.loads(tf.read_text())
+            traffic = tj.get("per_class", tj).get(dom)
         except Exception:
             traffic = None
     # every modelled kernel's fraction, and the whole path: W per record over the step time

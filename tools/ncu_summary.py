@@ -28,6 +28,13 @@ def to_bytes(v, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
 
 
+# kernel → bench.py kernel class (vc_profile classes)
+CLASS = {"primary": "primary", "rings": "rings", "wave_scan": "wave_scan", "gather": "gather",
+         "gather_emit": "gather", "gather_occl": "gather", "delaunay_smem": "delaunay", "delaunay_retry": "delaunay",
+         "tri_compact": "tri_compact", "degree": "degree", "live_masks": "assemble", "assemble": "assemble",
+         "asm_final": "assemble", "make_record": "make_record", "seedseq": "seedseq"}
+
+
 def main():
     rep, md = sys.argv[1], sys.argv[2]
     traffic_out = sys.argv[3] if len(sys.argv) > 3 else None
@@ -63,7 +70,12 @@ def main():
         lines.append(f"- {k}: {v:.4g} B")
     open(md, "w").write("\n".join(lines) + "\n")
     if traffic_out:
-        json.dump(traffic, open(traffic_out, "w"), indent=1)
+        per_class = {}
+        for k, v in traffic.items():
+            c = CLASS.get(k)
+            if c:
+                per_class[c] = per_class.get(c, 0.0) + v
+        json.dump({"report": rep, "per_kernel": traffic, "per_class": per_class}, open(traffic_out, "w"), indent=1)
     print(open(md).read())
 
 
