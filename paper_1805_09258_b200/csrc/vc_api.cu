@@ -563,7 +563,7 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     up((void**)&g.prim, Ks ? leaf.data() : nullptr, leaf.size() * 8);
     up((void**)&g.prim_id, Ks ? order.data() : nullptr, order.size() * 4);
     if (bvh.n_nodes) {
-      up((void**)&g.nodes, bvh.nodes, sizeof(float4) * 2 * bvh.n_nodes);
+      up((void**)&g.nodes, bvh.nodes, sizeof(float4) * 4 * bvh.n_nodes);
       g.n_nodes = bvh.n_nodes;
       free_bvh(&bvh);
     }

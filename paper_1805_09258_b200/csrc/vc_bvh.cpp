@@ -169,16 +169,38 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, in
     stack.push_back({left + 1, mid, t.end, t.depth + 1});
     stack.push_back({left, t.begin, mid, t.depth + 1});
   }
-  out->n_nodes = (int)nodes.size();
-  out->nodes = (float4*)malloc(sizeof(float4) * 2 * nodes.size());
+  // Device layout: one 64-byte record per interior node holding its two children's boxes
+  // and references — (lo.xyz, ref), (hi.xyz, count) per child, ref = first primitive of a
+  // leaf (count > 0) or the child's interior-node index (count = 0).  A visit loads one
+  // cache line and tests both children; leaves need no node of their own.
+  std::vector<int> inner(nodes.size(), -1);
+  int n_inner = 0;
+  for (size_t i = 0; i < nodes.size(); ++i)
+    if (i != 1 && nodes[i].count == 0) inner[i] = n_inner++;
+  const bool root_leaf = nodes[0].count > 0;
+  if (root_leaf) n_inner = 1;  // a single leaf: wrap it
+  out->n_nodes = n_inner;
+  out->nodes = (float4*)malloc(sizeof(float4) * 4 * (size_t)n_inner);
   out->order = (int*)malloc(sizeof(int) * (size_t)std::max(K, 1));
-  for (size_t i = 0; i < nodes.size(); ++i) {
-    const Node& n = nodes[i];
-    float fi, fc;
-    std::memcpy(&fi, &n.first, 4);
+  auto entry = [&](float4* dst, int c) {
+    const Node& n = nodes[c];
+    const int ref = n.count > 0 ? n.first : inner[c];
+    float fr, fc;
+    std::memcpy(&fr, &ref, 4);
     std::memcpy(&fc, &n.count, 4);
-    out->nodes[2 * i] = make_float4(n.b.lo[0], n.b.lo[1], n.b.lo[2], fi);
-    out->nodes[2 * i + 1] = make_float4(n.b.hi[0], n.b.hi[1], n.b.hi[2], fc);
+    dst[0] = make_float4(n.b.lo[0], n.b.lo[1], n.b.lo[2], fr);
+    dst[1] = make_float4(n.b.hi[0], n.b.hi[1], n.b.hi[2], fc);
+  };
+  if (root_leaf) {  // both children the same leaf (tested twice: same result)
+    entry(out->nodes, 0);
+    entry(out->nodes + 2, 0);
+  } else {
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      if (inner[i] < 0) continue;
+      float4* dst = out->nodes + 4 * (size_t)inner[i];
+      entry(dst, nodes[i].first);
+      entry(dst + 2, nodes[i].first + 1);
+    }
   }
   std::memcpy(out->order, order.data(), sizeof(int) * K);
 }

@@ -219,6 +219,7 @@ __device__ __forceinline__ double leaf_hit(const DevBvh& H, int k, const double*
 
 // Ordered BVH traversal.  mode 0: nearest hit (t_best/id_best out).  mode 1: any hit
 // that precedes (thr, id_thr) in (t, index) order — returns true on the first one.
+// Node layout (vc_bvh.cpp): per interior node the two children's boxes and references.
 template <int D, int MODE>
 __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const double* o, const double* d,
                           double& t_best, int& id_best) {
@@ -231,21 +232,13 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
   // slack: float32 t limit strictly above the float64 one
   auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + slack : INFINITY; };
   float tbf = tlim(t_best);
-  int stack[kBvhMaxDepth];  // the builder caps the depth, so pushes never overflow
+  int sref[kBvhMaxDepth], scnt[kBvhMaxDepth];  // the builder caps the depth: pushes never overflow
   float stn[kBvhMaxDepth];
   int sp = 0;
-  int node = 0;
-  {
-    float tn;
-    if (!box_hit<D>(__ldg(H.nodes), __ldg(H.nodes + 1), of, inv, tbf, tn)) return false;
-  }
+  int ref = 0, cnt = 0;  // current entry: interior node `ref` (cnt = 0) or leaf [ref, ref+cnt)
   while (true) {
-    const float4 meta = __ldg(H.nodes + 2 * node);
-    const float4 mh = __ldg(H.nodes + 2 * node + 1);
-    int cnt = __float_as_int(mh.w);
-    int first = __float_as_int(meta.w);
     if (cnt > 0) {
-      for (int k = first; k < first + cnt; ++k) {
+      for (int k = ref; k < ref + cnt; ++k) {
         double t = leaf_hit<D>(H, k, o, d, t_eps);
         if (t == INFINITY) continue;
         int id = H.prim_id[k];
@@ -260,28 +253,39 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
         }
       }
     } else {
-      const float4 l0 = __ldg(H.nodes + 2 * first), l1 = __ldg(H.nodes + 2 * first + 1);
-      const float4 r0 = __ldg(H.nodes + 2 * first + 2), r1 = __ldg(H.nodes + 2 * first + 3);
+      const float4* N = H.nodes + 4 * (size_t)ref;
+      const float4 l0 = __ldg(N), l1 = __ldg(N + 1), r0 = __ldg(N + 2), r1 = __ldg(N + 3);
       float tl, tr;
-      bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
-      bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
+      const bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
+      const bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
       if (hl && hr) {
-        int nearc = (tl <= tr) ? first : first + 1;
-        stack[sp] = (tl <= tr) ? first + 1 : first;
-        stn[sp] = fmaxf(tl, tr);
+        const bool lf = tl <= tr;
+        sref[sp] = __float_as_int(lf ? r0.w : l0.w);
+        scnt[sp] = __float_as_int(lf ? r1.w : l1.w);
+        stn[sp] = lf ? tr : tl;
         ++sp;
-        node = nearc;
+        ref = __float_as_int(lf ? l0.w : r0.w);
+        cnt = __float_as_int(lf ? l1.w : r1.w);
         continue;
       }
-      if (hl) { node = first; continue; }
-      if (hr) { node = first + 1; continue; }
+      if (hl) {
+        ref = __float_as_int(l0.w);
+        cnt = __float_as_int(l1.w);
+        continue;
+      }
+      if (hr) {
+        ref = __float_as_int(r0.w);
+        cnt = __float_as_int(r1.w);
+        continue;
+      }
     }
     // pop, skipping entries whose entry distance is beyond the current best
     bool found = false;
     while (sp > 0) {
       --sp;
       if (stn[sp] <= tbf) {
-        node = stack[sp];
+        ref = sref[sp];
+        cnt = scnt[sp];
         found = true;
         break;
       }
