@@ -270,3 +270,23 @@ def test_render_camera_growing_matches_oracle():
     _same_records(cs.single.packed(), _oracle_rows(s), 3)
     _same_records(cs.multiple.packed(), _oracle_rows(m), 3)
     assert rel_l2(img, oimg.reshape(img.shape)) <= 1e-4
+
+
+def test_populate_edge_cases():
+    """Empty marches (camera looking away from the medium), a 1×1 field, a zero-step camera."""
+    from paper_1805_09258_b200.renderer import Camera, FieldGrid, RenderSettings, populate_cache, render
+
+    z = golden("populate")
+    box = golden_scene(z, "box_")
+    st = RenderSettings(mode="ours-aniso", epsilon=0.2, march_step=0.25, n_angular=128, n_light_samples=4, spp=1)
+    away = Camera(position=np.array([0.5, 0.5, -2.0]), look_at=np.array([0.5, 0.5, -3.0]),
+                  up=np.array([0.0, 1.0, 0.0]), fov_degrees=30.0, width=4, height=3)
+    cs, stats = populate_cache(box, away, st)
+    assert stats["points_marched"] == 0 and cs.record_count == 0
+    img, rst = render(box, away, st, cache_set=cs)
+    assert np.all(img == 0.0) and rst["direct_evaluations"] == 0
+    sc2 = golden_scene(z, "simple_")
+    st2 = RenderSettings(mode="ours-aniso", epsilon=0.05, march_step=0.1, n_angular=64, n_light_samples=4, seed=3)
+    cs, stats = populate_cache(sc2, FieldGrid.for_scene(sc2, 1, 1), st2)
+    assert stats["points_marched"] == 1 and stats["records_single"] == 1 and stats["records_multiple"] == 1
+    np.testing.assert_array_equal(cs.single.packed()[0, :2], [0.5, 0.5])
