@@ -541,7 +541,12 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
     const Line ln = {e1[0] * d0 + e1[1] * d1 + e1[2] * d2, e2[0] * d0 + e2[1] * d1 + e2[2] * d2,
                      px * d0 + py * d1 + pz * d2};
     unsigned out = 0;
-    for (int v = 0; v < m; ++v) out |= (ln.A * poly.A(v) + ln.B * poly.B(v) + ln.C < 0.0 ? 1u : 0u) << v;
+    double kept = 0.0;  // largest squared radius among the vertices the cut keeps
+    for (int v = 0; v < m; ++v) {
+      const double va = poly.A(v), vb = poly.B(v);
+      if (ln.A * va + ln.B * vb + ln.C < 0.0) out |= 1u << v;
+      else kept = fmax(kept, va * va + vb * vb);
+    }
     if (!out) return 0;
     const unsigned full = (1u << m) - 1u;
     if (out == full) return 2;  // cannot happen: p (the origin) is inside every bisector
@@ -583,8 +588,8 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
       poly.A(nk + 1) = ya; poly.B(nk + 1) = yb; poly.L(nk + 1) = lab_e;
     }
     m = m_new;
-    t2R = 0.0;
-    for (int v = 0; v < m; ++v) t2R = fmax(t2R, poly.A(v) * poly.A(v) + poly.B(v) * poly.B(v));
+    // the new polygon = kept vertices + X + Y: its radius without another pass
+    t2R = fmax(kept, fmax(xa * xa + xb * xb, ya * ya + yb * yb));
     cutf = cutf_of(t2R);
     return 0;
   };
