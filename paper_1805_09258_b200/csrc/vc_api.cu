@@ -297,7 +297,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   size_t per = (size_t)n * (D * 8 + 8 + 4 * 5 + 24) + media_per * 12 + 64 + 2 * MS * 8 + 2 * RS * 8 +
                kStats * 8 + 32 + 8;
   if (D == 3) per += (size_t)P.n_tris * 12 + (P.host_adjacency ? 0 : (size_t)n * 32 * 8);
-  per += media_per / 10 * 72;                     // two-pass gather queue
+  per += media_per / 10 * 80;                     // two-pass gather queue
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
   per += (size_t)n * 16 + kAsmParts * 96 * 8;     // DirInfo + assembly partials
@@ -351,7 +351,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   // ~5% of cfg3 gather rays hit a window: room for ≥ 10% of the wave's media capacity
   W.gather_q_cap = std::min<long long>(W.media_cap, std::max<long long>(1LL << 24, W.media_cap / 10));
   if (const char* e = getenv("VOLCACHE_GATHER_QCAP")) W.gather_q_cap = std::min<long long>(W.gather_q_cap, atoll(e));
-  W.gather_q = alloc(32, (size_t)W.gather_q_cap * 72);
+  W.gather_q = alloc(32, (size_t)W.gather_q_cap * 80);
   W.gather_q_count = (unsigned long long*)alloc(33, 8);
   if (err != cudaSuccess) return cuda_fail(err, "workspace allocation");
 

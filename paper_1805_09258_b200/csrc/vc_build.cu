@@ -194,6 +194,13 @@ __global__ void __launch_bounds__(1024) k_wave_scan(Wave W, int gather_on) {
 // Media-sample gather (src/subdivision.py:177-195, src/transport.py:288-310)
 // ---------------------------------------------------------------------------
 
+// Live-sample bit of media sample (k, ring) of record rec (read by the assembly scan);
+// set by whoever computes a positive radiance, on masks zeroed before the gather.
+__device__ __forceinline__ void mark_live(const Wave& W, int n, int rec, int k, int ring) {
+  unsigned long long* w = W.live + ((size_t)rec * W.live_words + (ring >> 6)) * n + k;
+  atomicOr(w, 1ULL << (ring & 63));
+}
+
 template <int D>
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const long long total = W.rec_base[W.B];
@@ -267,13 +274,16 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
       }
     }
     float* out = W.media + (size_t)(W.rec_base[rec] + jl) * 3;
+    bool pos = false;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       double v = mul(S.sigma_s, __ddiv_rn(acc[c], (double)P.n_inner));
       float f = (float)v;
       if (v > 0.0 && !(f > 0.0f)) f = FLT_TRUE_MIN;  // keep the liveness bit exact
       out[c] = f;
+      pos |= f > 0.0f;
     }
+    if (pos) mark_live(W, n, rec, k, i);
   }
 }
 
@@ -287,10 +297,12 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
 struct GatherItem {
   double y[3], d[3], te;
   long long slot;  // media row
-  int ie, pad;
+  int ie, rec, k, ring;
 };
 
-static_assert(sizeof(GatherItem) == 72, "queue entry layout (workspace sizing)");
+static_assert(sizeof(GatherItem) == 80, "queue entry layout (workspace sizing)");
+
+
 
 constexpr int kGatherRun = 8;  // consecutive samples per thread in pass 1
 
@@ -380,6 +392,9 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
           it.te = te;
           it.ie = ie;
           it.slot = base + j;
+          it.rec = rec;
+          it.k = k;
+          it.ring = i;
         } else {  // queue full: resolve in place (same result, less coherent)
           double v[3] = {0.0, 0.0, 0.0};
           if (!occluded<D>(S, y, gd, te, ie)) {
@@ -389,6 +404,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
             for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
           }
           store_media(out, v);
+          if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, rec, k, i);
         }
       }
       ++i;
@@ -397,7 +413,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_occl(DevScene S, const GatherItem* q,
+__global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_occl(DevScene S, Wave W, int n, const GatherItem* q,
                                                                const unsigned long long* q_count, long long q_cap,
                                                                float* media) {
   const long long nq = min((long long)*q_count, q_cap);
@@ -413,6 +429,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_occl(DevScene S, co
       for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
     }
     store_media(media + (size_t)it.slot * 3, v);
+    if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, it.rec, it.k, it.ring);
   }
 }
 
@@ -736,29 +753,6 @@ __global__ void __launch_bounds__(kCompactBS) k_tri_compact(BuildParams P, Wave 
     run += tot;
   }
   if (threadIdx.x == 0 && run != P.n_tris) atomicMax(W.tri_status + rec, 3);
-}
-
-// Per-direction bit masks of live media samples (rad > 0 in any channel): word w of
-// direction k holds samples (k, 64w … 64w+63).  Read by the assembly's candidate scan.
-__global__ void k_live_masks(BuildParams P, Wave W, int media_on) {
-  const int n = P.n_angular;
-  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)W.B * n) return;
-  const int rec = (int)(gid / n), k = (int)(gid - (long long)rec * n);
-  const int c = W.cnt[gid];
-  const float* m = W.media + (size_t)(W.rec_base[rec] + W.pre[gid]) * 3;
-  unsigned long long* out = W.live + (size_t)rec * W.live_words * n + k;
-  for (int w = 0; w < W.live_words; ++w) {
-    unsigned long long word = 0;
-    if (media_on) {
-      const int hi = min(c - 64 * w, 64);
-      for (int b = 0; b < hi; ++b) {
-        const float* r = m + (size_t)(64 * w + b) * 3;
-        if (r[0] > 0.0f || r[1] > 0.0f || r[2] > 0.0f) word |= 1ULL << b;
-      }
-    }
-    out[(size_t)w * n] = word;
-  }
 }
 
 // Vertex valence of caller-supplied triangles (star counting).
@@ -1217,6 +1211,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   k_wave_scan<<<1, 1024, 0, st>>>(W, S.sigma_s > 0.0 ? 1 : 0);
   prof_end(st);
   int nl = 3;
+  // live-sample masks are set by the gather itself (mark_live)
+  cudaMemsetAsync(W.live, 0, sizeof(unsigned long long) * (size_t)W.live_words * nt, st);
   if (S.sigma_s > 0.0) {
     const bool two_pass =
         !S.reflective && 2 * S.emit.K <= S.geo.K && P.n_inner == 1 && W.gather_q_cap > 0;
@@ -1225,7 +1221,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       cudaMemsetAsync(W.gather_q_count, 0, sizeof(unsigned long long), st);
       k_gather_emit<D><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                       W.gather_q_cap);
-      k_gather_occl<D><<<sm_count * 8, 256, 0, st>>>(S, (const GatherItem*)W.gather_q, W.gather_q_count,
+      k_gather_occl<D><<<sm_count * 8, 256, 0, st>>>(S, W, P.n_angular, (const GatherItem*)W.gather_q,
+                                                     W.gather_q_count,
                                                      W.gather_q_cap, W.media);
       nl += 2;
     } else {
@@ -1261,8 +1258,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
     }
   }
   prof_begin(KC_ASSEMBLE, st);
-  k_live_masks<<<grid_for(nt, 256), 256, 0, st>>>(P, W, S.sigma_s > 0.0 ? 1 : 0);
-  ++nl;
+
   k_assemble<D><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
   k_asm_final<D><<<W.B, 64, 0, st>>>(P, W);
   ++nl;
