@@ -346,6 +346,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.del_scratch = (double*)alloc(40, D == 3 ? (size_t)W.del_retry_cap * 48 * 3 * 8 : 16);
   W.partial = (double*)alloc(37, B * kAsmParts * 64 * 8 + B * kAsmParts * 5 * 8);  // sums + 5 counters
   W.live_words = (P.r_ub + 63) / 64;
+  W.dense_media = insp ? 1 : 0;
   W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);
   // two-pass gather queue (emitter hits; overflow falls back to in-place resolution)
   // ~5% of cfg3 gather rays hit a window: room for ≥ 10% of the wave's media capacity

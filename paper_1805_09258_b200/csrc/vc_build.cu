@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
       if ((threadIdx.x & 31) == leader && hits) wbase = atomicAdd(q_count, (unsigned long long)__popc(hits));
       wbase = __shfl_sync(act, wbase, leader);
       if (ie < 0) {
-        store_media(out, zero);
+        // dead samples are never read by the assembly (live masks); written only for inspection
+        if (W.dense_media) store_media(out, zero);
       } else {
         unsigned long long slot = wbase + __popc(hits & ((1u << (threadIdx.x & 31)) - 1u));
         if ((long long)slot < q_cap) {

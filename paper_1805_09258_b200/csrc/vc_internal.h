@@ -114,6 +114,7 @@ struct Wave {
   double* records;       // B × 2 × RecordSize(d) (optional)
   unsigned long long* live;  // B × live_words × n: bit i of word w = media sample (k, 64w+i) has rad > 0
   int live_words;            // ⌈r_ub / 64⌉
+  int dense_media;           // 1: write zero radiance for dead samples too (inspection)
   int* del_retry;        // triangulation cells that outgrew the shared-memory polygon
   unsigned int* del_retry_count;
   int del_retry_cap;
