@@ -304,7 +304,10 @@ static_assert(sizeof(GatherItem) == 80, "queue entry layout (workspace sizing)")
 
 
 
-constexpr int kGatherRun = 8;  // consecutive samples per thread in pass 1
+#ifndef VC_GATHER_RUN
+#define VC_GATHER_RUN 16
+#endif
+constexpr int kGatherRun = VC_GATHER_RUN;  // consecutive samples per thread in pass 1
 
 __device__ __forceinline__ void store_media(float* out, const double* v) {
 #pragma unroll
