@@ -774,6 +774,9 @@ __global__ void k_degree(BuildParams P, Wave W) {
 // ---------------------------------------------------------------------------
 
 constexpr int kQCap = 64;
+#ifndef VC_ASM_MINB
+#define VC_ASM_MINB (512 / VC_ASM_BS)  // resident CTAs per SM → ≤ 128 registers
+#endif
 
 template <int D>
 struct ElemView {
@@ -809,7 +812,7 @@ __device__ __forceinline__ void warp_transpose_sum(double (&v)[32], int lane) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kAsmBS, 512 / kAsmBS) k_assemble(DevScene S, BuildParams P, Wave W) {
+__global__ void __launch_bounds__(kAsmBS, VC_ASM_MINB) k_assemble(DevScene S, BuildParams P, Wave W) {
   constexpr int NQ = 1 + D + D * (D + 1) / 2;
   constexpr int NW = kAsmBS / 32;
   static_assert(3 * NQ <= 32, "contribution vector must fit one warp");
