@@ -62,7 +62,7 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
                     const double* albedo, const double* bounds_min, const double* bounds_max,
                     double sigma_s, double sigma_a, vc_scene** out);
 void vc_scene_destroy(vc_scene* scene);
-/* Scratch budget for one record wave (bytes; default a quarter of device memory, ≤ 48 GiB). */
+/* Scratch budget for one record wave (bytes; default a third of device memory, ≤ 64 GiB). */
 int vc_scene_set_budget(vc_scene* scene, int64_t bytes);
 
 typedef struct {

@@ -301,10 +301,10 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
   per += (size_t)n * 16 + kAsmParts * 96 * 8;     // DirInfo + assembly partials
-  if (sc->budget <= 0) {  // default scratch budget: 1/4 of HBM (B200: 45 GB), ≤ 48 GiB
+  if (sc->budget <= 0) {  // default scratch budget: 1/3 of HBM (B200: 60 GB), ≤ 64 GiB
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    sc->budget = std::min<long long>((long long)(tot / 4), 48LL << 30);
+    sc->budget = std::min<long long>((long long)(tot / 3), 64LL << 30);
     if (sc->budget < (1LL << 30)) sc->budget = 1LL << 30;
   }
   long long B = (long long)(sc->budget / (long long)per);

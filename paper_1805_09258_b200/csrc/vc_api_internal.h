@@ -67,7 +67,7 @@ struct vc_scene {
   double* d_es_pos = nullptr;
   double* d_es_w = nullptr;
   int* d_es_surf = nullptr;
-  long long budget = 0;  // 0: a quarter of the device memory, capped at 48 GiB
+  long long budget = 0;  // 0: a third of the device memory, capped at 64 GiB
   vc::Workspace ws;
   ~vc_scene() {
     cudaFree(d_normal);
