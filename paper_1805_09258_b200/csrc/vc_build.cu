@@ -318,6 +318,12 @@ __device__ __forceinline__ void store_media(float* out, const double* v) {
   }
 }
 
+#ifndef VC_QCHUNK
+#define VC_QCHUNK 32
+#endif
+constexpr int kQChunk = VC_QCHUNK;  // queue slots a warp reserves with one atomic
+static_assert(kQChunk >= 32, "a step's hits (≤ 32) must fit one fresh chunk");
+
 template <int D>
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
                                                                GatherItem* q, unsigned long long* q_count,
@@ -329,91 +335,115 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
   const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
   const int* pre = W.pre + (size_t)rec * n;
   const int* cnt = W.cnt + (size_t)rec * n;
+  const int lane = threadIdx.x & 31;
   double x[3];
 #pragma unroll
   for (int c = 0; c < D; ++c) x[c] = W.x[rec * D + c];
   const uint64_t* st = W.rng + 4 * rec;
-  for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * kGatherRun; j0 < Pr;
-       j0 += gridDim.x * blockDim.x * kGatherRun) {
-    // direction of the first sample: last k with pre[k] ≤ j0
-    int a = 0, b = n - 1;
-    while (a < b) {
-      int mid = (a + b + 1) >> 1;
-      if (pre[mid] <= j0) a = mid; else b = mid - 1;
+  // the warp appends emitter hits into queue chunks it reserves kQChunk slots at a time
+  // (one atomic per chunk instead of one per step); unused slots are marked empty
+  long long cbase = 0;
+  int cused = kQChunk;  // warp-uniform
+  auto seal = [&]() {   // mark the rest of the current chunk empty
+    for (int t = cused + lane; t < kQChunk; t += 32)
+      if (cbase + t < q_cap) q[cbase + t].slot = -1;
+  };
+  const int stride = gridDim.x * blockDim.x * kGatherRun;
+  // warp-uniform loop: lane runs [j0, j0 + kGatherRun) of the record's samples
+  for (int j0w = (blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * kGatherRun; j0w < Pr; j0w += stride) {
+    const int j0 = j0w + lane * kGatherRun;
+    int k = 0, i = 0;
+    Pcg64 g;
+    if (j0 < Pr) {
+      // direction of the first sample: last k with pre[k] ≤ j0
+      int a = 0, b = n - 1;
+      while (a < b) {
+        int mid = (a + b + 1) >> 1;
+        if (pre[mid] <= j0) a = mid; else b = mid - 1;
+      }
+      k = a;
+      i = j0 - pre[k];
+      g = pcg_load(st);
+      pcg_advance(g, (unsigned long long)(draws0 + (long long)(D == 3 ? 2 : 1) * j0), jt);
     }
-    int k = a, i = j0 - pre[k];
-    Pcg64 g = pcg_load(st);
-    pcg_advance(g, (unsigned long long)(draws0 + (long long)(D == 3 ? 2 : 1) * j0), jt);
-    const int jend = min(j0 + kGatherRun, Pr);
-    for (int j = j0; j < jend; ++j) {
-      while (i >= cnt[k]) {  // next direction with live rings
-        ++k;
-        i = 0;
-      }
-      const double ri = ring_radius(i, P.march_step);
-      double y[3], gd[3];
+    for (int step = 0; step < kGatherRun; ++step) {
+      const int j = j0 + step;
+      const bool active = j < Pr;
+      double y[3], gd[3], te = 0.0;
+      int ie = -1;
+      if (active) {
+        while (i >= cnt[k]) {  // next direction with live rings
+          ++k;
+          i = 0;
+        }
+        const double ri = ring_radius(i, P.march_step);
 #pragma unroll
-      for (int c = 0; c < D; ++c) y[c] = add(x[c], mul(ri, W.dirs[((size_t)rec * n + k) * D + c]));
-      if constexpr (D == 2) {
-        double th = mul(2.0 * kPi, g.next_double());
-        gd[0] = cos(th);
-        gd[1] = sin(th);
-      } else {
-        double u0 = g.next_double(), u1 = g.next_double();
-        double z = sub(1.0, mul(2.0, u0));
-        double phi = mul(2.0 * kPi, u1);
-        double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
-        double sp, cp;
-        sincos(phi, &sp, &cp);
-        gd[0] = mul(sq, cp);
-        gd[1] = mul(sq, sp);
-        gd[2] = z;
-      }
-      double te;
-      int ie;
-      nearest_emitter<D>(S, y, gd, te, ie);
-      float* out = W.media + (size_t)(base + j) * 3;
-      double zero[3] = {0.0, 0.0, 0.0};
-      // warp-aggregated queue append (one atomic per warp and step)
-      const unsigned act = __activemask();
-      const unsigned hits = __ballot_sync(act, ie >= 0);
-      const int leader = __ffs(act) - 1;
-      unsigned long long wbase = 0;
-      if ((threadIdx.x & 31) == leader && hits) wbase = atomicAdd(q_count, (unsigned long long)__popc(hits));
-      wbase = __shfl_sync(act, wbase, leader);
-      if (ie < 0) {
-        // dead samples are never read by the assembly (live masks); written only for inspection
-        if (W.dense_media) store_media(out, zero);
-      } else {
-        unsigned long long slot = wbase + __popc(hits & ((1u << (threadIdx.x & 31)) - 1u));
-        if ((long long)slot < q_cap) {
-          GatherItem& it = q[slot];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            it.y[c] = c < D ? y[c] : 0.0;
-            it.d[c] = c < D ? gd[c] : 0.0;
-          }
-          it.te = te;
-          it.ie = ie;
-          it.slot = base + j;
-          it.rec = rec;
-          it.k = k;
-          it.ring = i;
-        } else {  // queue full: resolve in place (same result, less coherent)
-          double v[3] = {0.0, 0.0, 0.0};
-          if (!occluded<D>(S, y, gd, te, ie)) {
-            const double* E = S.emission + (size_t)ie * 3;
-            double T = exp(-S.sigma_t * te);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
-          }
-          store_media(out, v);
-          if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, rec, k, i);
+        for (int c = 0; c < D; ++c) y[c] = add(x[c], mul(ri, W.dirs[((size_t)rec * n + k) * D + c]));
+        if constexpr (D == 2) {
+          double th = mul(2.0 * kPi, g.next_double());
+          gd[0] = cos(th);
+          gd[1] = sin(th);
+        } else {
+          double u0 = g.next_double(), u1 = g.next_double();
+          double z = sub(1.0, mul(2.0, u0));
+          double phi = mul(2.0 * kPi, u1);
+          double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+          double sp, cp;
+          sincos(phi, &sp, &cp);
+          gd[0] = mul(sq, cp);
+          gd[1] = mul(sq, sp);
+          gd[2] = z;
+        }
+        nearest_emitter<D>(S, y, gd, te, ie);
+        if (ie < 0 && W.dense_media) {  // dead samples are read only by inspection
+          const double zero[3] = {0.0, 0.0, 0.0};
+          store_media(W.media + (size_t)(base + j) * 3, zero);
         }
       }
-      ++i;
+      const bool hit = active && ie >= 0;
+      const unsigned hits = __ballot_sync(0xffffffffu, hit);
+      if (hits) {
+        const int nh = __popc(hits);
+        if (cused + nh > kQChunk) {  // new chunk
+          seal();
+          unsigned long long nb = 0;
+          if (lane == 0) nb = atomicAdd(q_count, (unsigned long long)kQChunk);
+          cbase = (long long)__shfl_sync(0xffffffffu, nb, 0);
+          cused = 0;
+        }
+        if (hit) {
+          const long long slot = cbase + cused + __popc(hits & ((1u << lane) - 1u));
+          if (slot < q_cap) {
+            GatherItem& it = q[slot];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              it.y[c] = c < D ? y[c] : 0.0;
+              it.d[c] = c < D ? gd[c] : 0.0;
+            }
+            it.te = te;
+            it.ie = ie;
+            it.slot = base + j;
+            it.rec = rec;
+            it.k = k;
+            it.ring = i;
+          } else {  // queue full: resolve in place (same result, less coherent)
+            double v[3] = {0.0, 0.0, 0.0};
+            if (!occluded<D>(S, y, gd, te, ie)) {
+              const double* E = S.emission + (size_t)ie * 3;
+              double T = exp(-S.sigma_t * te);
+#pragma unroll
+              for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
+            }
+            store_media(W.media + (size_t)(base + j) * 3, v);
+            if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, rec, k, i);
+          }
+        }
+        cused += nh;
+      }
+      if (active) ++i;
     }
   }
+  seal();
 }
 
 template <int D>
@@ -423,6 +453,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_occl(DevScene S, Wa
   const long long nq = min((long long)*q_count, q_cap);
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nq;
        t += (long long)gridDim.x * blockDim.x) {
+    if (q[t].slot < 0) continue;  // unused tail of a warp's chunk
     const GatherItem it = q[t];
     double v[3] = {0.0, 0.0, 0.0};
     if (!occluded<D>(S, it.y, it.d, it.te, it.ie)) {

@@ -227,7 +227,13 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     of[a] = (float)o[a];
+#ifndef VC_EXACT_RCP
+    // approximate reciprocal (≤ 1 ulp; ±0 → ±inf): the slab error it adds is far inside
+    // the 1e-5·scale box padding
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv[a]) : "f"((float)d[a]));
+#else
     inv[a] = 1.0f / (float)d[a];
+#endif
   }
   // slack: float32 t limit strictly above the float64 one
   auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + slack : INFINITY; };
