@@ -661,12 +661,30 @@ __device__ int voronoi_cell_poly(const double* __restrict__ dirs, const float4* 
       if (consider(row * cols + col) == 2) return 2;
     }
   }
-  for (int rr = 0; rr <= 2 * span; ++rr) {
-    // rows outward from r0 (nearest first), skipping rows outside [rlo, rhi]
+  // after the neighbours the cell is usually well inside half the search radius: sweep
+  // only the window of its current 2·R_cell (same bounds as for α; R only shrinks, so a
+  // point outside it can never cut)
+  int rlo2 = rlo, rhi2 = rhi, ncol2 = ncol_iter, span2 = span;
+  if (pro) {
+    const double t = t2R;
+    const double c2 = (1.0 - t) / (1.0 + t) - 1e-12, s2 = 2.0 * sqrt(t) / (1.0 + t) + 1e-12;
+    if (c2 > ca && s2 < sa) {
+      const bool capn2 = st <= s2 && pz > 0.0, caps2 = st <= s2 && pz < 0.0;
+      rlo2 = max(rlo, capn2 ? 0 : min(row_of(pz * c2 + st * s2), r0));
+      rhi2 = min(rhi, caps2 ? rows - 1 : max(row_of(pz * c2 - st * s2), r0));
+      if (!capn2 && !caps2) {
+        const int h2 = (int)ceil(asin(fmin(s2 / st, 1.0)) * cols / (2.0 * kPi)) + 1;
+        if (2 * h2 + 1 < ncol2) ncol2 = 2 * h2 + 1;
+      }
+      span2 = max(r0 - rlo2, rhi2 - r0);
+    }
+  }
+  for (int rr = 0; rr <= 2 * span2; ++rr) {
+    // rows outward from r0 (nearest first), skipping rows outside [rlo2, rhi2]
     int dr = (rr + 1) >> 1;
     int row = (rr & 1) ? r0 - dr : r0 + dr;
-    if (row < rlo || row > rhi) continue;
-    for (int cc = 0; cc < ncol_iter; ++cc) {
+    if (row < rlo2 || row > rhi2) continue;
+    for (int cc = 0; cc < ncol2; ++cc) {
       int dc = (cc + 1) >> 1;
       if (pro && dr <= 1 && dc <= 1) continue;  // taken above
       int col = (cc & 1) ? c0 - dc : c0 + dc;
