@@ -613,8 +613,33 @@ def gen_grow():
     np.savez_compressed(OUT / "grow.npz", **out)
 
 
+def gen_dropin():
+    """Quadrature values the reference's estimator tests compare against
+    (tests/test_subdivision.py:222-353: quadrature_radiance on the bundled scenes)."""
+    import volcache.transport as vt
+
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import circle_scene  # the reference's own test scene helper
+
+    bundled = Path("/root/reference/pkg/scenes")
+    pen = vscene.load_scene(bundled / "penumbra2d.json")
+    box = vscene.load_scene(bundled / "box3d.json")
+    circ = circle_scene(n_sides=48, sigma_s=0.5, sigma_a=0.25)
+    out = {"versions": VERSIONS}
+    out.update(scene_fields("pen_", pen))
+    out.update(scene_fields("box_", box))
+    out.update(scene_fields("circ_", circ))
+    out["q_pen"] = np.array(vt.quadrature_radiance(pen, np.array([0.15, 0.6]), n_angular=4096, n_dist=24,
+                                                   n_secondary=64))
+    out["q_circ"] = np.array(vt.quadrature_radiance(circ, np.array([0.5, 0.5]), n_angular=4096, n_dist=4,
+                                                    n_secondary=4))
+    out["q_box"] = np.array(vt.quadrature_radiance(box, np.array([0.5, 0.5, 0.5]), n_angular=3072, n_dist=6,
+                                                   n_secondary=192))
+    np.savez_compressed(OUT / "dropin.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline", "path", "grow"]
+    which = sys.argv[1:] or ["ff", "trace", "records", "make_record", "interp", "render", "populate", "io", "baseline", "path", "grow", "dropin"]
     if "ff" in which:
         gen_formfactors()
     if "trace" in which:
@@ -637,3 +662,5 @@ if __name__ == "__main__":
         gen_path()
     if "grow" in which:
         gen_grow()
+    if "dropin" in which:
+        gen_dropin()
