@@ -217,6 +217,10 @@ __device__ __forceinline__ double leaf_hit(const DevBvh& H, int k, const double*
   return hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, t_eps);
 }
 
+#ifndef VC_WHILE_WHILE
+#define VC_WHILE_WHILE 1
+#endif
+
 // Ordered BVH traversal.  mode 0: nearest hit (t_best/id_best out).  mode 1: any hit
 // that precedes (thr, id_thr) in (t, index) order — returns true on the first one.
 // Node layout (vc_bvh.cpp): per interior node the two children's boxes and references.
@@ -242,6 +246,63 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
   float stn[kBvhMaxDepth];
   int sp = 0;
   int ref = 0, cnt = 0;  // current entry: interior node `ref` (cnt = 0) or leaf [ref, ref+cnt)
+  // pop, skipping entries whose entry distance is beyond the current best
+  auto pop = [&]() -> bool {
+    while (sp > 0) {
+      --sp;
+      if (stn[sp] <= tbf) {
+        ref = sref[sp];
+        cnt = scnt[sp];
+        return true;
+      }
+    }
+    return false;
+  };
+#if VC_WHILE_WHILE
+  // while-while: descend interior nodes until a leaf, then test it — the lanes of a warp
+  // run the float64 leaf tests together instead of interleaving them with box tests
+  while (true) {
+    while (cnt == 0) {
+      const float4* N = H.nodes + 4 * (size_t)ref;
+      const float4 l0 = __ldg(N), l1 = __ldg(N + 1), r0 = __ldg(N + 2), r1 = __ldg(N + 3);
+      float tl, tr;
+      const bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
+      const bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
+      if (hl && hr) {
+        const bool lf = tl <= tr;
+        sref[sp] = __float_as_int(lf ? r0.w : l0.w);
+        scnt[sp] = __float_as_int(lf ? r1.w : l1.w);
+        stn[sp] = lf ? tr : tl;
+        ++sp;
+        ref = __float_as_int(lf ? l0.w : r0.w);
+        cnt = __float_as_int(lf ? l1.w : r1.w);
+      } else if (hl) {
+        ref = __float_as_int(l0.w);
+        cnt = __float_as_int(l1.w);
+      } else if (hr) {
+        ref = __float_as_int(r0.w);
+        cnt = __float_as_int(r1.w);
+      } else if (!pop()) {
+        return false;
+      }
+    }
+    for (int k = ref; k < ref + cnt; ++k) {
+      double t = leaf_hit<D>(H, k, o, d, t_eps);
+      if (t == INFINITY) continue;
+      int id = H.prim_id[k];
+      if (MODE == 0) {
+        if (t < t_best || (t == t_best && id < id_best)) {
+          t_best = t;
+          id_best = id;
+          tbf = tlim(t_best);
+        }
+      } else {
+        if (t < t_best || (t == t_best && id < id_best)) return true;
+      }
+    }
+    if (!pop()) return false;
+  }
+#else
   while (true) {
     if (cnt > 0) {
       for (int k = ref; k < ref + cnt; ++k) {
@@ -285,20 +346,10 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
         continue;
       }
     }
-    // pop, skipping entries whose entry distance is beyond the current best
-    bool found = false;
-    while (sp > 0) {
-      --sp;
-      if (stn[sp] <= tbf) {
-        ref = sref[sp];
-        cnt = scnt[sp];
-        found = true;
-        break;
-      }
-    }
-    if (!found) break;
+    if (!pop()) break;
   }
   return false;
+#endif
 }
 
 // Nearest hit in a primitive set; `id_best` is the original surface index.
