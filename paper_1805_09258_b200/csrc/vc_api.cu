@@ -301,6 +301,11 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
   per += (size_t)n * 16 + kAsmParts * 96 * 8;     // DirInfo + assembly partials
+  // assembly item lists: surface items ≤ 2n, media items ≤ valence × live samples; lists that
+  // outgrow their share fall back to the fused kernel
+  long long item_cap = 4LL * n + (long long)(media_per / 4) + 1024;
+  if (const char* e = getenv("VOLCACHE_ASM_ITEM_CAP")) item_cap = std::max(0LL, atoll(e));
+  per += (size_t)item_cap * 8 + kAsmParts * 8 + 4;
   if (sc->budget <= 0) {  // default scratch budget: 1/3 of HBM (B200: 60 GB), ≤ 64 GiB
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -345,6 +350,10 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.del_retry_count = (unsigned int*)alloc(39, 8);
   W.del_scratch = (double*)alloc(40, D == 3 ? (size_t)W.del_retry_cap * 48 * 3 * 8 : 16);
   W.partial = (double*)alloc(37, B * kAsmParts * 64 * 8 + B * kAsmParts * 5 * 8);  // sums + 5 counters
+  W.item_cap = item_cap;
+  W.asm_items = item_cap > 0 ? (uint2*)alloc(41, (size_t)B * item_cap * 8) : nullptr;
+  W.item_n = (int*)alloc(42, B * kAsmParts * 8);
+  W.asm_fb = (int*)alloc(43, B * 4);
   W.live_words = (P.r_ub + 63) / 64;
   W.dense_media = insp ? 1 : 0;
   W.live = (unsigned long long*)alloc(34, B * (size_t)W.live_words * n * 8);

@@ -845,6 +845,81 @@ __device__ __forceinline__ void elem_vertices(const Wave& W, const BuildParams& 
   }
 }
 
+
+// Per-record inputs of the element contributions.
+template <int D>
+struct AsmCtx {
+  const double* dirs;
+  const double* sv;
+  const int* cnt;
+  const int* pre;
+  const double* lo;
+  const float* media;
+  double x[3];
+  double step;
+};
+
+template <int D>
+__device__ __forceinline__ AsmCtx<D> asm_ctx(const BuildParams& P, const Wave& W, int rec) {
+  const size_t rb = (size_t)rec * P.n_angular;
+  AsmCtx<D> c;
+  c.dirs = W.dirs + rb * D;
+  c.sv = W.s + rb;
+  c.cnt = W.cnt + rb;
+  c.pre = W.pre + rb;
+  c.lo = W.lo + rb * 3;
+  c.media = W.media + (size_t)W.rec_base[rec] * 3;
+#pragma unroll
+  for (int a = 0; a < D; ++a) c.x[a] = W.x[rec * D + a];
+  c.step = P.march_step;
+  return c;
+}
+
+// Contribution (3·NQ components, c·NQ + t) of element v[] at `ring` with representative
+// vertex slot `rep` (src/subdivision.py:318-366); false = degenerate element (dropped).
+template <int D>
+__device__ __forceinline__ bool asm_item(const DevScene& S, const AsmCtx<D>& C, int kind, double wt, const int* v,
+                                         int ring, int rep, double (&cvec)[32]) {
+  constexpr int NQ = 1 + D + D * (D + 1) / 2;
+  double rv[D][3];
+  double dist[D];
+  const double ri = (kind == 1) ? ring_radius(ring, C.step) : 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const bool live = (kind == 1) && (ring < C.cnt[v[j]]);
+    dist[j] = live ? ri : C.sv[v[j]];
+#pragma unroll
+    for (int a = 0; a < D; ++a) rv[j][a] = dist[j] * C.dirs[(size_t)v[j] * D + a];
+  }
+  double rad[3];
+  if (kind == 0) {
+    rad[0] = C.lo[v[rep] * 3 + 0];
+    rad[1] = C.lo[v[rep] * 3 + 1];
+    rad[2] = C.lo[v[rep] * 3 + 2];
+  } else {
+    const float* m = C.media + (size_t)(C.pre[v[rep]] + ring) * 3;
+    rad[0] = m[0];
+    rad[1] = m[1];
+    rad[2] = m[2];
+  }
+  double F, gF[D], HF[D * (D + 1) / 2];
+  bool ok;
+  if constexpr (D == 3) ok = ff_triangle(rv[0], rv[1], rv[2], F, gF, HF);
+  else ok = ff_segment(rv[0], rv[1], F, gF, HF);
+  if (!ok) return false;
+  double w[D], q[NQ];
+#pragma unroll
+  for (int a = 0; a < D; ++a) w[a] = -rv[rep][a];
+  element_q<D>(w, dist[rep], S.sigma_t, F, gF, HF, q);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double f = wt * rad[c];
+#pragma unroll
+    for (int t = 0; t < NQ; ++t) cvec[c * NQ + t] = f * q[t];
+  }
+  return true;
+}
+
 // Warp transpose-reduction: every lane holds 32 values v[0..31]; afterwards lane l holds
 // Σ_lanes v[l] in v[0] (31 double shuffles; no per-lane persistent accumulators).
 __device__ __forceinline__ void warp_transpose_sum(double (&v)[32], int lane) {
@@ -860,8 +935,20 @@ __device__ __forceinline__ void warp_transpose_sum(double (&v)[32], int lane) {
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(kAsmBS, VC_ASM_MINB) k_assemble(DevScene S, BuildParams P, Wave W) {
+#ifndef VC_ASM_EVAL_MINB
+#define VC_ASM_EVAL_MINB VC_ASM_MINB
+#endif
+#ifndef VC_ASM_SCAN_MINB
+#define VC_ASM_SCAN_MINB 24  // the scan alone: ≤ 40 registers, 48 warps per SM
+#endif
+
+// EMIT = false: scan + evaluate (fused; records whose item lists overflowed).
+// EMIT = true: scan only — every warp copies its ballot-ordered item batches into its own
+// segment of W.asm_items for k_asm_eval (a light kernel at high occupancy, so the dependent
+// element → vertex → live-mask loads overlap).
+template <int D, bool EMIT>
+__global__ void __launch_bounds__(kAsmBS, EMIT ? VC_ASM_SCAN_MINB : VC_ASM_MINB)
+    k_assemble_t(DevScene S, BuildParams P, Wave W) {
   constexpr int NQ = 1 + D + D * (D + 1) / 2;
   constexpr int NW = kAsmBS / 32;
   static_assert(3 * NQ <= 32, "contribution vector must fit one warp");
@@ -875,18 +962,16 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_MINB) k_assemble(DevScene S, Bu
   double* out_part = W.partial + slot * 64;
   long long* out_cnt = (long long*)(W.partial + (size_t)W.B * kAsmParts * 64) + slot * 5;
   if (D == 3 && W.tri_status[rec] != 0) return;  // k_asm_final reports the failure
+  if (!EMIT && W.asm_items && !W.asm_fb[rec]) return;  // evaluated by k_asm_eval
+  const AsmCtx<D> ring_ctx = asm_ctx<D>(P, W, rec);
+  // EMIT: this warp's segment [seg, seg + seg_cap) and its fill
+  const long long seg_cap = W.item_cap / kAsmParts;
+  uint2* seg = EMIT ? W.asm_items + (size_t)slot * seg_cap : nullptr;
+  int fill = 0;
   const DirInfo* info = W.info + (size_t)rec * n;
   const size_t rb = (size_t)rec * n;
-  const double* dirs = W.dirs + rb * D;
-  const double* sv = W.s + rb;
   const int* idx = W.idx + rb;
   const int* cnt = W.cnt + rb;
-  const int* pre = W.pre + rb;
-  const double* lo = W.lo + rb * 3;
-  const float* media = W.media + (size_t)W.rec_base[rec] * 3;
-  double x[3];
-#pragma unroll
-  for (int a = 0; a < D; ++a) x[a] = W.x[rec * D + a];
   const double fbar = S.sigma_s / (D == 2 ? 2.0 * kPi : 4.0 * kPi);
   const double step = P.march_step;
   const bool media_on = S.sigma_s > 0.0;  // σs = 0: media rings carry zero radiance
@@ -899,56 +984,26 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_MINB) k_assemble(DevScene S, Bu
 
     // contribution of one queued item (element e at ring `ring`, representative slot rep)
     auto eval_item = [&](uint2 it, double (&cvec)[32]) {
-      int e = (int)it.x;
-      int ring = (int)(it.y >> 2);
-      int rep = (int)(it.y & 3u);
       int v[D];
-      elem_vertices<D>(W, P, rec, e, v);
-      double rv[D][3];
-      double dist[D];
-      double ri = (kind == 1) ? ring_radius(ring, step) : 0.0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        bool live = (kind == 1) && (ring < cnt[v[j]]);
-        dist[j] = live ? ri : sv[v[j]];
-#pragma unroll
-        for (int a = 0; a < D; ++a) rv[j][a] = dist[j] * dirs[(size_t)v[j] * D + a];
-      }
-      double rad[3];
-      if (kind == 0) {
-        rad[0] = lo[v[rep] * 3 + 0];
-        rad[1] = lo[v[rep] * 3 + 1];
-        rad[2] = lo[v[rep] * 3 + 2];
-      } else {
-        const float* m = media + (size_t)(pre[v[rep]] + ring) * 3;
-        rad[0] = m[0];
-        rad[1] = m[1];
-        rad[2] = m[2];
-      }
-      double F, gF[D], HF[D * (D + 1) / 2];
-      bool ok;
-      if constexpr (D == 3) ok = ff_triangle(rv[0], rv[1], rv[2], F, gF, HF);
-      else ok = ff_segment(rv[0], rv[1], F, gF, HF);
+      elem_vertices<D>(W, P, rec, (int)it.x, v);
+      const bool ok = asm_item<D>(S, ring_ctx, kind, wt, v, (int)(it.y >> 2), (int)(it.y & 3u), cvec);
       ++n_eval;
       ++ev_kind[kind];
-      if (!ok) {
-        ++n_drop;
-        return;
-      }
-      double w[D], q[NQ];
-#pragma unroll
-      for (int a = 0; a < D; ++a) w[a] = -rv[rep][a];
-      element_q<D>(w, dist[rep], S.sigma_t, F, gF, HF, q);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double f = wt * rad[c];
-#pragma unroll
-        for (int t = 0; t < NQ; ++t) cvec[c * NQ + t] = f * q[t];
-      }
+      if (!ok) ++n_drop;
     };
     // evaluate one item per lane (all lanes take part) and fold the 3·NQ components:
     // lane l accumulates component l, no per-lane 3·NQ accumulator array
     auto evaluate = [&](uint2 it, bool valid) {
+      if constexpr (EMIT) {
+        const int m = __popc(__ballot_sync(0xffffffffu, valid));
+        if (fill + m > seg_cap) {
+          if (lane == 0) W.asm_fb[rec] = 1;  // segment full: the fused kernel takes the record
+        } else if (valid) {
+          seg[fill + lane] = it;
+        }
+        fill += m;
+        return;
+      }
       double cvec[32];
 #pragma unroll
       for (int t = 0; t < 32; ++t) cvec[t] = 0.0;
@@ -1086,8 +1141,13 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_MINB) k_assemble(DevScene S, Bu
     __syncwarp();
 
     // lane l holds component l (order c·NQ + t) of this warp's sum
-    out_part[kind * 32 + lane] = acc;
+    if constexpr (EMIT) {
+      if (lane == 0) W.item_n[slot * 2 + kind] = fill;  // end of this kind's items
+    } else {
+      out_part[kind * 32 + lane] = acc;
+    }
   }
+  if constexpr (EMIT) return;
 
   // counters: evaluated / dropped / per-kind evaluated
   // star vertices: Σ_k [idx_k ≥ 0] · deg_k · (maxc − cnt_k)  (src/subdivision.py:205-207)
@@ -1100,6 +1160,79 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_MINB) k_assemble(DevScene S, Bu
     }
   }
   // counters: evaluated / dropped / per-kind evaluated / stars
+  long long cs[5] = {n_eval, n_drop, ev_kind[0], ev_kind[1], stars};
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cs[k] += __shfl_xor_sync(0xffffffffu, cs[k], o);
+  if (lane == 0)
+    for (int k = 0; k < 5; ++k) out_cnt[k] = cs[k];
+}
+
+// Evaluation of the item segments written by k_assemble_t<D, true>: warp w of a record
+// evaluates producer warp w's segment in order (a fixed summation order per record).
+template <int D>
+__global__ void __launch_bounds__(kAsmBS, VC_ASM_EVAL_MINB) k_asm_eval(DevScene S, BuildParams P, Wave W) {
+  constexpr int NW = kAsmBS / 32;
+  const int rec = blockIdx.y, part = blockIdx.x;
+  const int n = P.n_angular;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t slot = (size_t)rec * kAsmParts + (size_t)part * NW + wid;
+  double* out_part = W.partial + slot * 64;
+  long long* out_cnt = (long long*)(W.partial + (size_t)W.B * kAsmParts * 64) + slot * 5;
+  if (D == 3 && W.tri_status[rec] != 0) return;
+  if (W.asm_fb[rec]) return;  // a segment overflowed: the fused kernel takes the record
+  const AsmCtx<D> C = asm_ctx<D>(P, W, rec);
+  const long long seg_cap = W.item_cap / kAsmParts;
+  const uint2* seg = W.asm_items + (size_t)slot * seg_cap;
+  const int end0 = W.item_n[slot * 2], end1 = W.item_n[slot * 2 + 1];
+  const double fbar = S.sigma_s / (D == 2 ? 2.0 * kPi : 4.0 * kPi);
+  long long n_eval = 0, n_drop = 0, ev_kind[2] = {0, 0};
+  for (int kind = 0; kind < 2; ++kind) {
+    const double wt = fbar * (kind == 0 ? 1.0 : P.march_step);
+    const int a = kind ? end0 : 0, b = kind ? end1 : end0;
+    double acc = 0.0;
+    // the next round's item and vertex indices are fetched while this round evaluates
+    uint2 q = make_uint2(0, 0);
+    int v[D];
+    auto fetch = [&](int t) {
+      if (t < b) {
+        q = seg[t];
+        elem_vertices<D>(W, P, rec, (int)q.x, v);
+      }
+    };
+    fetch(a + lane);
+    for (int t0 = a; t0 < b; t0 += 32) {
+      const int t = t0 + lane;
+      const bool valid = t < b;
+      const uint2 qc = q;
+      int vc[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) vc[j] = v[j];
+      fetch(t + 32);
+      double cvec[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) cvec[c] = 0.0;
+      if (valid) {
+        if (!asm_item<D>(S, C, kind, wt, vc, (int)(qc.y >> 2), (int)(qc.y & 3u), cvec)) ++n_drop;
+        ++n_eval;
+        ++ev_kind[kind];
+      }
+      warp_transpose_sum(cvec, lane);
+      acc += cvec[0];
+    }
+    out_part[kind * 32 + lane] = acc;
+  }
+  // star vertices: Σ_k [idx_k ≥ 0] · deg_k · (maxc − cnt_k)  (src/subdivision.py:205-207)
+  const size_t rb = (size_t)rec * n;
+  const int maxc = W.rec_maxc[rec];
+  long long stars = 0;
+  for (int k = part * kAsmBS + threadIdx.x; k < n; k += kAsmBS * kAsmSplit) {
+    if (W.idx[rb + k] >= 0) {
+      const int dg = (D == 2) ? 2 : W.deg[rb + k];
+      stars += (long long)dg * (maxc - W.cnt[rb + k]);
+    }
+  }
   long long cs[5] = {n_eval, n_drop, ev_kind[0], ev_kind[1], stars};
 #pragma unroll
   for (int k = 0; k < 5; ++k)
@@ -1315,7 +1448,13 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   }
   prof_begin(KC_ASSEMBLE, st);
 
-  k_assemble<D><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
+  if (W.asm_items) {
+    cudaMemsetAsync(W.asm_fb, 0, sizeof(int) * W.B, st);
+    k_assemble_t<D, true><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
+    k_asm_eval<D><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
+    nl += 2;
+  }
+  k_assemble_t<D, false><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);  // overflowed records
   k_asm_final<D><<<W.B, 64, 0, st>>>(P, W);
   ++nl;
   prof_end(st);

@@ -119,6 +119,11 @@ struct Wave {
   unsigned int* del_retry_count;
   int del_retry_cap;
   double* del_scratch;   // del_retry_cap × 48 × 3 doubles of global-memory polygons
+  uint2* asm_items;      // B × item_cap assembly items (element, ring·4 + rep) in
+                         // kAsmParts per-warp segments (null: fused assembly only)
+  int* item_n;           // B × kAsmParts × 2: segment end of the surface / media items
+  int* asm_fb;           // B: 1 = a segment overflowed, the fused kernel takes the record
+  long long item_cap;    // items per record
   void* gather_q;        // two-pass gather: queued emitter-hit rays (GatherItem)
   unsigned long long* gather_q_count;
   long long gather_q_cap;

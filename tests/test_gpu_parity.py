@@ -377,6 +377,37 @@ def test_gather_queue_overflow_same_result():
     np.testing.assert_array_equal(np.load(out / "q_full.npy"), np.load(out / "q_tiny.npy"))
 
 
+def test_assembly_item_lists_match_fused():
+    """Two-kernel assembly (scan → per-warp item lists → evaluation), the fused kernel
+    (VOLCACHE_ASM_ITEM_CAP=0) and a mix (tiny lists overflow → fused fallback per record)
+    evaluate the same items; only the summation order differs."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1805_09258_b200 import configs, estimate_moments_batch, seed_words;"
+        "sc = configs.cfg3_scene(n_spheres=6, level=2); X = np.random.default_rng(9).uniform(sc.bounds_min, sc.bounds_max, (12, 3));"
+        "r = estimate_moments_batch(sc, X, seeds=seed_words(4, 401, range(12)), n_angular=4096, march_step=0.1);"
+        "np.save(sys.argv[1], r.moments); np.save(sys.argv[1] + '.stats.npy', r.stats)"
+    )
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    res = {}
+    for cap in (None, "0", "2000", "8000"):
+        env = dict(os.environ)
+        if cap is not None:
+            env["VOLCACHE_ASM_ITEM_CAP"] = cap
+        f = out / f"asm_{cap}.npy"
+        subprocess.run([sys.executable, "-c", code, str(f)], check=True, cwd=ROOT, env=env)
+        res[cap] = (np.load(f), np.load(str(f) + ".stats.npy"))
+    m0, s0 = res[None]
+    for cap in ("0", "2000", "8000"):
+        m, s = res[cap]
+        np.testing.assert_array_equal(s, s0)  # same items evaluated / dropped per kind
+        np.testing.assert_allclose(m, m0, rtol=1e-11, atol=1e-14 * np.abs(m0).max())
+
+
 def test_errors_and_edge_cases():
     from paper_1805_09258_b200 import configs, estimate_moments, estimate_moments_batch, seed_words
     from paper_1805_09258_b200.scene import Medium, Scene
