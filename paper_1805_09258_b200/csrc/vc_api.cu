@@ -235,6 +235,55 @@ void prof_end(cudaStream_t st) {
 // The record build, in waves sized by the scratch budget.
 // ---------------------------------------------------------------------------
 
+// Candidate windows of the hull triangulation, per stratum row: the smallest window
+// (rows r ± h, columns c ± w, h ≤ 3) whose border lies at least 2 mean spacings from every
+// point of the row's strata, with at most kHullK candidates.  The window only sets the
+// cost: every cell the kernel keeps passes its own security test (k_delaunay_hull).
+// VOLCACHE_DEL_HULL=0 sends every row to the clipping kernel.
+static void del_row_table(BuildParams& P) {
+  const char* env = getenv("VOLCACHE_DEL_HULL");
+  const bool on = !(env && env[0] == '0');
+  const char* ek = getenv("VOLCACHE_HULL_KMAX");
+  const int kcap = ek ? std::max(8, std::min(kHullK, atoi(ek))) : kHullK;
+  const int rows = P.rows, cols = P.cols;
+  P.del_kmax = 0;
+  const double pi = 3.141592653589793;
+  const double alpha = 2.0 * std::sqrt(4.0 * pi / P.n_angular);
+  for (int r = 0; r < std::min(rows, kDelRowsMax); ++r) {
+    const double tht = std::acos(1.0 - 2.0 * r / rows), thb = std::acos(1.0 - 2.0 * (r + 1) / rows);
+    const double smin = std::min(std::sin(tht), std::sin(thb));
+    int best = 1 << 30, code = 0;
+    for (int h = 1; on && h <= 3; ++h) {
+      if (r - h < 0 || r + h >= rows) continue;
+      const double drow = std::min(tht - std::acos(1.0 - 2.0 * (r - h) / rows),
+                                   std::acos(1.0 - 2.0 * (r + h + 1) / rows) - thb);
+      if (drow < alpha) continue;
+      for (int w = 1; w <= 15 && 2 * (2 * w + 1) < cols; ++w) {
+        const double dw = w * 2.0 * pi / cols;
+        if (dw >= 0.5 * pi) break;
+        if (std::asin(std::min(1.0, std::sin(dw) * smin)) >= alpha) {
+          const int K = (2 * h + 1) * (2 * w + 1) - 1;
+          if (K <= kcap && K < best) {
+            best = K;
+            code = (h << 6) | w;
+          }
+          break;
+        }
+      }
+    }
+    P.del_hw[r] = (unsigned char)code;
+    P.del_kmax = std::max(P.del_kmax, code ? best : 0);
+  }
+  // polar rows: candidates within δ = 2.7 spacings (2·R_cell ≤ δ holds for all but a
+  // few cells), kept in 16-bit column indices
+  P.del_zstep = 2.0 / rows;
+  const double delta = 2.7 * std::sqrt(4.0 * pi / P.n_angular);
+  P.del_cap = (on && P.del_kmax > 0 && rows >= 4 && 2 * cols <= 65535) ? 1 : 0;
+  P.del_cap_cos = (float)std::cos(delta);
+  P.del_cap_c2 = std::cos(0.5 * delta) * std::cos(0.5 * delta);
+  P.del_cap_s2 = std::sin(0.5 * delta) * std::sin(0.5 * delta);
+}
+
 int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int32_t* adjacency,
                const vc_build_params* prm, double* moments, int64_t* stats, double* records,
                cudaStream_t st, Inspect* insp) {
@@ -275,6 +324,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
       a = std::min(1.5 * a, 1.5);
     }
   }
+  if (D == 3) del_row_table(P);
   if (host) {  // ValueError before any work (src/subdivision.py:155-158)
     const double eps = 1e-12 * sc->scale;
     for (int i = 0; i < N; ++i)
@@ -349,6 +399,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.del_retry = (int*)alloc(38, (size_t)W.del_retry_cap * 4);
   W.del_retry_count = (unsigned int*)alloc(39, 8);
   W.del_scratch = (double*)alloc(40, D == 3 ? (size_t)W.del_retry_cap * 48 * 3 * 8 : 16);
+  W.del_fb = (int*)alloc(44, (D == 3 && !P.host_adjacency) ? (size_t)B * n * 4 : 16);
+  W.del_fb_count = (unsigned int*)alloc(45, 8);
   W.partial = (double*)alloc(37, B * kAsmParts * 64 * 8 + B * kAsmParts * 5 * 8);  // sums + 5 counters
   W.item_cap = item_cap;
   W.asm_items = item_cap > 0 ? (uint2*)alloc(41, (size_t)B * item_cap * 8) : nullptr;

@@ -779,6 +779,308 @@ __global__ void __launch_bounds__(128) k_delaunay_retry(BuildParams P, Wave W, i
 
 constexpr size_t kDelSmem = (size_t)kPolyV * kDelBS * (8 + 8 + 4);
 
+// Clipping kernel over the cells the hull kernel handed back (grid-stride over the list).
+__global__ void __launch_bounds__(kDelBS, VC_LB_DEL2) k_delaunay_list(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ unsigned char dsm[];
+  double* sa = (double*)dsm;
+  double* sb = sa + kPolyV * kDelBS;
+  int* sl = (int*)(sb + kPolyV * kDelBS);
+  const int n = P.n_angular;
+  const unsigned cnt = *W.del_fb_count;
+  Poly poly{sa + threadIdx.x, sb + threadIdx.x, sl + threadIdx.x};
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    const int gid = W.del_fb[t];
+    const int rec = gid / n, i = gid - rec * n;
+    if (delaunay_point(P, W, rec, i, poly, own, own_cnt) == 2) {
+      const unsigned slot = atomicAdd(W.del_retry_count, 1u);
+      if ((int)slot < W.del_retry_cap) W.del_retry[slot] = gid;
+      else atomicMax(W.tri_status + rec, 2);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stratum-window triangulation.  The Delaunay neighbours of p are the vertices of the
+// convex hull of the other directions mapped by the stereographic projection from p,
+//   u(q) = (e1·q, e2·q) / (1 − p·q),      1 − p·q = |p − q|² / 2,
+// (circles through p become lines; a point inside the circumcircle of (p, a, b) lands
+// beyond the line through u(a), u(b)), in counter-clockwise order about p.  One thread
+// per direction gift-wraps the hull of the candidates of a fixed stratum window (rows
+// r ± h, columns c ± w; uniform loop bounds across a warp, whose lanes share a row).
+// The wrap compares orientations in float32 and flags any test within its error bound
+// (|cross| ≤ 128·2⁻²⁴·max|u|²), so every decision it keeps is the exact one.  The cell is
+// kept only if it is secure: for every Voronoi vertex v (circumcentre of p and two
+// consecutive neighbours, radius R) the spherical cap of radius R about v stays inside
+// the window — rows beyond the window lie beyond the parallels of its border rows, and
+// columns beyond it in the two hemispheres cut off by its border meridians — so no
+// direction outside the window can lie in any of the star's circumcircles.  Flagged,
+// insecure or unclosed cells, and rows without a window (the polar caps), go to the
+// clipping kernel (k_delaunay_list) through a list.
+// ---------------------------------------------------------------------------
+constexpr int kHullBS = 128;
+constexpr int kHullH = 16;             // hull vertices
+constexpr int kHullSlots = kHullK + 1;  // window candidates including the centre
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Stereographic projection of q from p onto the (e1, e2) plane, in float32 (five
+// roundings relative to |u|); q = p gives NaN, which every later test ignores.
+struct Proj {
+  double px, py, pz, e1x, e1y, e1z, e2x, e2y, e2z;
+  __device__ __forceinline__ Proj(double x, double y, double z) : px(x), py(y), pz(z) {
+    double hx = 0.0, hy = 0.0, hz = 1.0;
+    if (fabs(pz) >= 0.9) { hx = 1.0; hz = 0.0; }
+    e1x = hy * pz - hz * py; e1y = hz * px - hx * pz; e1z = hx * py - hy * px;
+    const double ne = rsqrt(e1x * e1x + e1y * e1y + e1z * e1z);
+    e1x *= ne; e1y *= ne; e1z *= ne;
+    e2x = py * e1z - pz * e1y; e2y = pz * e1x - px * e1z; e2z = px * e1y - py * e1x;
+  }
+  __device__ __forceinline__ float2 operator()(const double* q) const {
+    const double d0 = px - q[0], d1 = py - q[1], d2 = pz - q[2];
+    const float inv = 2.0f * rcp_approx((float)(d0 * d0 + d1 * d1 + d2 * d2));
+    return make_float2((float)(-(e1x * d0 + e1y * d1 + e1z * d2)) * inv,
+                       (float)(-(e2x * d0 + e2y * d1 + e2z * d2)) * inv);
+  }
+};
+
+// Counter-clockwise gift wrap of the projections us[0..K) (stride kHullBS) from `start`
+// (a hull vertex).  Every orientation is compared in float32 and the smallest |cross| met
+// must exceed `margin` (the float32 error bound), else the wrap fails (returns 0).  The
+// current vertex and the initial candidate are parked as NaN during a scan, so the loop
+// body is the same for every candidate (NaN never wins and never trips the bound).
+__device__ __forceinline__ int gift_wrap(float2* us, int K, int start, float margin, unsigned char* hs) {
+  const float2 nan2 = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+  int hn = 0, cur = start;
+  float mn = FLT_MAX;
+  for (;;) {
+    hs[hn * kHullBS] = (unsigned char)cur;
+    ++hn;
+    const float2 a = us[cur * kHullBS];
+    int b0 = cur;
+    float2 b = nan2;
+    do {  // the next candidate that is not NaN (the centre) as the initial best
+      b0 = (b0 + 1 == K) ? 0 : b0 + 1;
+      b = us[b0 * kHullBS];
+    } while (b.x != b.x && b0 != cur);
+    us[cur * kHullBS] = nan2;
+    us[b0 * kHullBS] = nan2;
+    float bx = b.x - a.x, by = b.y - a.y;
+    int best = b0;
+#pragma unroll 4
+    for (int c = 0; c < K; ++c) {
+      const float2 u = us[c * kHullBS];
+      const float cx = u.x - a.x, cy = u.y - a.y;
+      const float cr = bx * cy - by * cx;
+      mn = fminf(mn, fabsf(cr));
+      if (cr < 0.0f) { best = c; bx = cx; by = cy; }
+    }
+    us[cur * kHullBS] = a;
+    us[b0 * kHullBS] = b;
+    if (best == start) break;
+    if (hn == kHullH) return 0;
+    cur = best;
+  }
+  return mn > margin ? hn : 0;
+}
+
+// float32 error bound of one orientation test over projections of norm ≤ √m2
+__device__ __forceinline__ float wrap_margin(float m2) { return 128.0f * 5.9604645e-8f * m2; }
+
+// X ≥ √Q  ⇔  X ≥ 0 ∧ X² ≥ Q
+__device__ __forceinline__ bool ge_root(double X, double Q) { return X >= 0.0 && X * X >= Q; }
+
+// Security and output of a wrapped star.  `gidx(slot)` maps a candidate slot to its
+// direction, `secure(c, cp, Q, tol)` tests one Voronoi vertex (c ∝ v; |c| cos R = c·p,
+// |c|² sin² R = Q).  Writes the valence and the owned triangles (i < both neighbours),
+// as delaunay_point; false leaves the cell to the clipping kernel.
+template <class GIdx, class Secure>
+__device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, const Proj& pr, size_t base, int i,
+                                          const unsigned char* hs, int hn, GIdx gidx, Secure secure, int* own,
+                                          int* own_cnt) {
+  if (hn < 3 || hn > kMaxV) return false;
+  const double px = pr.px, py = pr.py, pz = pr.pz;
+  const int g0 = gidx(hs[0]);
+  int gb = g0;
+  double bxd = dirs[3 * (size_t)gb] - px, byd = dirs[3 * (size_t)gb + 1] - py, bzd = dirs[3 * (size_t)gb + 2] - pz;
+  for (int t = 0; t < hn; ++t) {
+    const double ax = bxd, ay = byd, az = bzd;
+    gb = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * kHullBS]);
+    bxd = dirs[3 * (size_t)gb] - px; byd = dirs[3 * (size_t)gb + 1] - py; bzd = dirs[3 * (size_t)gb + 2] - pz;
+    const double cx = ay * bzd - az * byd, cy = az * bxd - ax * bzd, cz = ax * byd - ay * bxd;
+    const double cp = cx * px + cy * py + cz * pz;
+    const double xx = cy * pz - cz * py, xy = cz * px - cx * pz, xz = cx * py - cy * px;
+    const double Q = xx * xx + xy * xy + xz * xz;
+    const double tol = 1e-6 * (fabs(cx) + fabs(cy) + fabs(cz));
+    if (!(cp > tol && secure(cx, cy, cz, cp, Q, tol))) return false;
+  }
+  int c = 0, ga = g0;
+  for (int t = 0; t < hn; ++t) {
+    const int gn = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * kHullBS]);
+    if (i < ga && i < gn) {
+      own[(base * kMaxV + c) * 2 + 0] = ga;
+      own[(base * kMaxV + c) * 2 + 1] = gn;
+      ++c;
+    }
+    ga = gn;
+  }
+  W.deg[base] = hn;
+  own_cnt[base] = c;
+  return true;
+}
+
+__device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, int rec, int i, float2* us,
+                                          unsigned char* hs, int* own, int* own_cnt) {
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const int r0 = i / cols, c0 = i - r0 * cols;
+  const int hw = r0 < kDelRowsMax ? P.del_hw[r0] : 0;
+  if (!hw) return false;
+  const int h = hw >> 6, w = hw & 63, wc = 2 * w + 1;
+  const double* dirs = W.dirs + (size_t)rec * n * 3;
+  const Proj pr(dirs[3 * (size_t)i], dirs[3 * (size_t)i + 1], dirs[3 * (size_t)i + 2]);
+  // projected window candidates, row-major (the centre projects to NaN)
+  int col0 = c0 - w;
+  col0 += (col0 < 0) ? cols : 0;
+  int K = 0, start = 0;
+  float m2 = 0.0f;
+  for (int dr = -h; dr <= h; ++dr) {
+    const double* rowp = dirs + 3 * (size_t)(r0 + dr) * cols;
+    const double* q = rowp + 3 * col0;
+    const double* rowe = rowp + 3 * cols;
+    for (int dc = 0; dc < wc; ++dc) {
+      const float2 u = pr(q);
+      us[K * kHullBS] = u;
+      const float r2 = u.x * u.x + u.y * u.y;
+      if (r2 > m2) { m2 = r2; start = K; }
+      ++K;
+      q += 3;
+      q = (q == rowe) ? rowp : q;
+    }
+  }
+  const int hn = gift_wrap(us, K, start, wrap_margin(m2), hs);
+  // candidate k → direction index (k / wc by a 16-bit reciprocal, exact for k < 2¹⁶/wc²)
+  const unsigned rwc = (65536u + wc - 1) / wc;
+  auto gidx = [&](int k) {
+    const int a = (int)(((unsigned)k * rwc) >> 16);
+    int col = col0 + (k - a * wc);
+    col -= (col >= cols) ? cols : 0;
+    return (r0 - h + a) * cols + col;
+  };
+  // security: the cap about each Voronoi vertex stays on the window side of both border
+  // meridians (distance asin(v·n) ≥ R) and between the border parallels (|θ_v − θ| ≥ R)
+  const bool top = r0 - h > 0, bot = r0 + h < rows - 1;
+  const double zt = 1.0 - P.del_zstep * (r0 - h), zb = 1.0 - P.del_zstep * (r0 + h + 1);
+  const double st2 = fmax(0.0, 1.0 - zt * zt), sb2 = fmax(0.0, 1.0 - zb * zb);
+  double shi, chi, slo, clo;
+  sincospi(2.0 * (c0 + w + 1) / cols, &shi, &chi);
+  sincospi(2.0 * (c0 - w) / cols, &slo, &clo);
+  auto secure = [&](double cx, double cy, double cz, double cp, double Q, double tol) {
+    bool ok = ge_root(cx * shi - cy * chi - tol, Q) && ge_root(cy * clo - cx * slo - tol, Q);
+    if (top) ok &= ge_root(zt * cp - cz - tol, st2 * Q);
+    if (bot) ok &= ge_root(cz - zb * cp - tol, sb2 * Q);
+    return ok;
+  };
+  return hull_star(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
+}
+
+__global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ float2 hsm[];
+  unsigned char* hs = (unsigned char*)(hsm + (P.del_kmax + 1) * kHullBS) + threadIdx.x;
+  const int n = P.n_angular;
+  const long long gid = (long long)blockIdx.x * kHullBS + threadIdx.x;
+  bool fb = false;
+  if (gid < (long long)W.B * n) {
+    const int rec = (int)(gid / n);
+    const int i = (int)(gid - (long long)rec * n);
+    const int r0 = i / P.cols;
+    // the polar rows belong to k_delaunay_cap when it runs
+    if (!(P.del_cap && (r0 == 0 || r0 == P.rows - 1)))
+      fb = !hull_cell(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, fb);
+  if (m) {
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned slot = 0;
+    if (lane == leader) slot = atomicAdd(W.del_fb_count, (unsigned)__popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = (int)gid;
+  }
+}
+
+// The polar rows (0 and rows − 1), whose strata meet at the pole: the candidates are the
+// directions of the two cap rows within angle δ of p (a float32 dot pre-test with margin,
+// compacted into shared memory with their indices); besides the parallel below the two
+// rows, the security test asks R ≤ δ/2 of every Voronoi vertex, so no skipped direction
+// (farther than δ from p) can reach a circumcircle.
+constexpr int kCapSlots = 64;
+constexpr size_t kCapSmem = (size_t)kHullBS * (kCapSlots * (sizeof(float2) + 2) + kHullH);
+
+__global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ float2 csm[];
+  unsigned short* ix0 = (unsigned short*)(csm + kCapSlots * kHullBS);
+  unsigned short* ix = ix0 + threadIdx.x;
+  unsigned char* hs = (unsigned char*)(ix0 + kCapSlots * kHullBS) + threadIdx.x;
+  float2* us = csm + threadIdx.x;
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const long long gid = (long long)blockIdx.x * kHullBS + threadIdx.x;  // over B × 2 × cols
+  bool fb = false;
+  int cell = -1;
+  if (gid < (long long)W.B * 2 * cols) {
+    const int rec = (int)(gid / (2 * cols));
+    const int k = (int)(gid - (long long)rec * 2 * cols);
+    const bool north = k < cols;
+    const int i = north ? k : (rows - 1) * cols + (k - cols);
+    cell = rec * n + i;
+    const int rlo = north ? 0 : rows - 2;  // the two cap rows
+    const double* dirs = W.dirs + (size_t)rec * n * 3;
+    const float4* d32 = W.dirs32 + (size_t)rec * n;
+    const Proj pr(dirs[3 * (size_t)i], dirs[3 * (size_t)i + 1], dirs[3 * (size_t)i + 2]);
+    const float4 p32 = d32[i];
+    const float cutf = P.del_cap_cos - 1e-6f;
+    int K = 0, start = 0;
+    float m2 = 0.0f;
+    bool full = false;
+    for (int j = rlo * cols; j < (rlo + 2) * cols; ++j) {
+      const float4 q = d32[j];
+      if (p32.x * q.x + p32.y * q.y + p32.z * q.z > cutf) {
+        if (K == kCapSlots) { full = true; break; }
+        const float2 u = pr(dirs + 3 * (size_t)j);
+        us[K * kHullBS] = u;
+        ix[K * kHullBS] = (unsigned short)(j - rlo * cols);
+        const float r2 = u.x * u.x + u.y * u.y;
+        if (r2 > m2) { m2 = r2; start = K; }
+        ++K;
+      }
+    }
+    fb = true;
+    if (!full) {
+      const int hn = gift_wrap(us, K, start, wrap_margin(m2), hs);
+      auto gidx = [&](int s) { return rlo * cols + (int)ix[s * kHullBS]; };
+      // the parallel below (north) / above (south) the two cap rows
+      const double zb = north ? 1.0 - 2.0 * P.del_zstep : 1.0 - P.del_zstep * (rows - 2);
+      const double sb2 = fmax(0.0, 1.0 - zb * zb);
+      const double c2 = P.del_cap_c2, s2 = P.del_cap_s2;  // cos², sin² of δ/2
+      auto secure = [&](double cx, double cy, double cz, double cp, double Q, double tol) {
+        bool ok = (cp - tol) * (cp - tol) * s2 >= c2 * Q;  // R ≤ δ/2
+        ok &= north ? ge_root(cz - zb * cp - tol, sb2 * Q) : ge_root(zb * cp - cz - tol, sb2 * Q);
+        return ok;
+      };
+      fb = !hull_star(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, fb);
+  if (m) {
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned slot = 0;
+    if (lane == leader) slot = atomicAdd(W.del_fb_count, (unsigned)__popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = cell;
+  }
+}
+
 constexpr int kCompactBS = 512;
 
 __global__ void __launch_bounds__(kCompactBS) k_tri_compact(BuildParams P, Wave W, const int* own,
@@ -1426,11 +1728,36 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       static bool smem_attr = false;
       if (!smem_attr) {
         cudaFuncSetAttribute(k_delaunay_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
+        cudaFuncSetAttribute(k_delaunay_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
+        cudaFuncSetAttribute(k_delaunay_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kHullBS * (kHullSlots * sizeof(float2) + kHullH)));
+        cudaFuncSetAttribute(k_delaunay_cap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
         smem_attr = true;
       }
       prof_begin(KC_DELAUNAY, st);
       cudaMemsetAsync(W.del_retry_count, 0, sizeof(unsigned int), st);
-      k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
+      if (P.del_kmax > 0) {
+        // stratum-window hulls for most cells, the cap kernel for the polar rows, clipping
+        // for the cells either hands back
+        cudaMemsetAsync(W.del_fb_count, 0, sizeof(unsigned int), st);
+        const size_t smem = (size_t)kHullBS * ((P.del_kmax + 1) * sizeof(float2) + kHullH);
+        k_delaunay_hull<<<grid_for(nt, kHullBS), kHullBS, smem, st>>>(P, W, own, own_cnt);
+        if (P.del_cap) {
+          k_delaunay_cap<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt);
+          ++nl;
+        }
+        if (getenv("VOLCACHE_DEL_STATS")) {  // debug: cells handed to the clipping kernel
+          unsigned c = 0;
+          cudaMemcpyAsync(&c, W.del_fb_count, 4, cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fprintf(stderr, "[volcache] hull fallback cells: %u of %lld\n", c, nt);
+        }
+        k_delaunay_list<<<sm_count * VC_LB_DEL2, kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
+        nl += 2;
+      } else {
+        k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
+        ++nl;
+      }
       k_delaunay_retry<<<sm_count * 2, 128, 0, st>>>(P, W, own, own_cnt, W.del_scratch);
       ++nl;
       prof_end(st);

@@ -63,6 +63,9 @@ struct DelAngle {
   double alpha, sin_a, cos_a, tan_half;
 };
 constexpr int kDelLevels = 10;
+// Stratum-window triangulation (k_delaunay_hull): candidates per window and rows covered.
+constexpr int kHullK = 64;
+constexpr int kDelRowsMax = 512;
 
 // Per-call record-build parameters (mirrors estimate_moments' arguments).
 struct BuildParams {
@@ -77,6 +80,14 @@ struct BuildParams {
   double epsilon;        // record error budget (make_record)
   int anisotropic;
   int make_records;
+  // per stratum row: (h << 6) | w — the hull kernel's candidate window is rows r ± h,
+  // columns c ± w; 0 = the row goes to the clipping kernel (polar caps, wide rows)
+  unsigned char del_hw[kDelRowsMax];
+  int del_kmax;  // largest window in del_hw (sizes the hull kernel's shared memory)
+  double del_zstep;  // 2 / rows: stratum height in z
+  int del_cap;       // 1: the polar rows go to the cap kernel
+  float del_cap_cos;           // cos δ, the cap kernel's candidate radius
+  double del_cap_c2, del_cap_s2;  // cos²(δ/2), sin²(δ/2)
 };
 
 // Per-direction data read by the assembly scan, one 16-byte load per vertex.
@@ -119,6 +130,8 @@ struct Wave {
   unsigned int* del_retry_count;
   int del_retry_cap;
   double* del_scratch;   // del_retry_cap × 48 × 3 doubles of global-memory polygons
+  int* del_fb;           // B × n: cells the hull kernel hands to the clipping kernel
+  unsigned int* del_fb_count;
   uint2* asm_items;      // B × item_cap assembly items (element, ring·4 + rep) in
                          // kAsmParts per-warp segments (null: fused assembly only)
   int* item_n;           // B × kAsmParts × 2: segment end of the surface / media items

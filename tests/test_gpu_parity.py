@@ -120,6 +120,30 @@ def test_gpu_delaunay_equals_qhull(case):
         assert len(ins["tris"]) == 2 * int(n) - 4
 
 
+@pytest.mark.parametrize("n", [1024, 2048, 3000, 4096, 16384])
+def test_hull_triangulation_equals_clipping_and_qhull(n, monkeypatch):
+    """The stratum-window hull kernel (default) and the clipping kernel (VOLCACHE_DEL_HULL=0)
+    give the same triangle set as qhull on the reference's own directions, for grid shapes
+    with and without warp-aligned rows."""
+    from paper_1805_09258_b200 import configs, inspect_record
+    from oracle import volcache_oracle as O
+
+    sc = configs.cfg3_scene(n_spheres=2, level=1)
+    x = np.array([2.0, 1.5, 2.0])
+    for k in range(6 if n <= 4096 else 3):
+        seed = np.random.SeedSequence([5, 401, k])
+        monkeypatch.delenv("VOLCACHE_DEL_HULL", raising=False)
+        fast = inspect_record(sc, x, rng_seed=seed, n_angular=n, march_step=2.0)
+        monkeypatch.setenv("VOLCACHE_DEL_HULL", "0")
+        clip = inspect_record(sc, x, rng_seed=seed, n_angular=n, march_step=2.0)
+        assert fast["stats"][5] == 0 and clip["stats"][5] == 0
+        assert _tri_set(fast["tris"]) == _tri_set(clip["tris"])
+        _, adj = O.directions(3, n, np.random.default_rng(seed))
+        assert _tri_set(fast["tris"]) == _tri_set(adj)
+        assert len(fast["tris"]) == 2 * n - 4
+    monkeypatch.delenv("VOLCACHE_DEL_HULL", raising=False)
+
+
 @pytest.mark.parametrize("case", [c for c in REC_CASES if c.startswith(("cfg2_m01", "room", "box3d"))])
 def test_gpu_connectivity_vs_oracle(case):
     """Default path (GPU triangulation) ≡ oracle re-run with the GPU's triangles injected."""
