@@ -274,6 +274,22 @@ static void del_row_table(BuildParams& P) {
     P.del_hw[r] = (unsigned char)code;
     P.del_kmax = std::max(P.del_kmax, code ? best : 0);
   }
+  static const int kClassMax[3] = {34, 44, kHullK};
+  int nr = 0;
+  for (int k = 0; k < 3; ++k) {
+    P.del_cls[k] = nr;
+    P.del_cls_k[k] = 0;
+    for (int r = 0; r < std::min(rows, kDelRowsMax); ++r) {
+      const int code = P.del_hw[r];
+      if (!code) continue;
+      const int K = (2 * (code >> 6) + 1) * (2 * (code & 63) + 1) - 1;
+      if (K <= kClassMax[k] && (k == 0 || K > kClassMax[k - 1])) {
+        P.del_rows[nr++] = (unsigned short)r;
+        P.del_cls_k[k] = std::max(P.del_cls_k[k], K);
+      }
+    }
+  }
+  P.del_cls[3] = nr;
   // polar rows: candidates within δ = 2.7 spacings (2·R_cell ≤ δ holds for all but a
   // few cells), kept in 16-bit column indices
   P.del_zstep = 2.0 / rows;

@@ -986,19 +986,22 @@ __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, i
   return hull_star(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
 }
 
-__global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W, int* own, int* own_cnt) {
+// One launch per window class: thread → (record, row of the class, column).
+__global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W, int* own, int* own_cnt, int cls) {
   extern __shared__ float2 hsm[];
-  unsigned char* hs = (unsigned char*)(hsm + (P.del_kmax + 1) * kHullBS) + threadIdx.x;
-  const int n = P.n_angular;
+  unsigned char* hs = (unsigned char*)(hsm + (P.del_cls_k[cls] + 1) * kHullBS) + threadIdx.x;
+  const int n = P.n_angular, cols = P.cols;
+  const int nr = P.del_cls[cls + 1] - P.del_cls[cls];
   const long long gid = (long long)blockIdx.x * kHullBS + threadIdx.x;
   bool fb = false;
-  if (gid < (long long)W.B * n) {
-    const int rec = (int)(gid / n);
-    const int i = (int)(gid - (long long)rec * n);
-    const int r0 = i / P.cols;
-    // the polar rows belong to k_delaunay_cap when it runs
-    if (!(P.del_cap && (r0 == 0 || r0 == P.rows - 1)))
-      fb = !hull_cell(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
+  int cell = 0;
+  if (gid < (long long)W.B * nr * cols) {
+    const int rec = (int)(gid / ((long long)nr * cols));
+    const int rem = (int)(gid - (long long)rec * nr * cols);
+    const int rs = rem / cols;
+    const int i = (int)P.del_rows[P.del_cls[cls] + rs] * cols + (rem - rs * cols);
+    cell = rec * n + i;
+    fb = !hull_cell(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
   }
   const unsigned m = __ballot_sync(0xffffffffu, fb);
   if (m) {
@@ -1006,7 +1009,32 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W
     unsigned slot = 0;
     if (lane == leader) slot = atomicAdd(W.del_fb_count, (unsigned)__popc(m));
     slot = __shfl_sync(0xffffffffu, slot, leader);
-    if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = (int)gid;
+    if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = cell;
+  }
+}
+
+// Rows that neither the hull classes nor the cap kernel take (no window, cap kernel off)
+// go to the clipping kernel directly.
+__global__ void k_delaunay_rest(BuildParams P, Wave W) {
+  const int n = P.n_angular, cols = P.cols;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool fb = false;
+  int cell = 0;
+  if (gid < (long long)W.B * n) {
+    const int rec = (int)(gid / n);
+    const int i = (int)(gid - (long long)rec * n);
+    const int r0 = i / cols;
+    const bool cap = P.del_cap && (r0 == 0 || r0 == P.rows - 1);
+    fb = !cap && (r0 >= kDelRowsMax || P.del_hw[r0] == 0);
+    cell = rec * n + i;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, fb);
+  if (m) {
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned slot = 0;
+    if (lane == leader) slot = atomicAdd(W.del_fb_count, (unsigned)__popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = cell;
   }
 }
 
@@ -1740,8 +1768,18 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         // stratum-window hulls for most cells, the cap kernel for the polar rows, clipping
         // for the cells either hands back
         cudaMemsetAsync(W.del_fb_count, 0, sizeof(unsigned int), st);
-        const size_t smem = (size_t)kHullBS * ((P.del_kmax + 1) * sizeof(float2) + kHullH);
-        k_delaunay_hull<<<grid_for(nt, kHullBS), kHullBS, smem, st>>>(P, W, own, own_cnt);
+        for (int k = 0; k < 3; ++k) {
+          const int nr = P.del_cls[k + 1] - P.del_cls[k];
+          if (!nr) continue;
+          const size_t smem = (size_t)kHullBS * ((P.del_cls_k[k] + 1) * sizeof(float2) + kHullH);
+          k_delaunay_hull<<<grid_for((long long)W.B * nr * P.cols, kHullBS), kHullBS, smem, st>>>(P, W, own,
+                                                                                                 own_cnt, k);
+          ++nl;
+        }
+        if (P.del_cls[3] + (P.del_cap ? 2 : 0) < P.rows) {
+          k_delaunay_rest<<<grid_for(nt, 256), 256, 0, st>>>(P, W);
+          ++nl;
+        }
         if (P.del_cap) {
           k_delaunay_cap<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt);
           ++nl;
@@ -1753,7 +1791,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
           fprintf(stderr, "[volcache] hull fallback cells: %u of %lld\n", c, nt);
         }
         k_delaunay_list<<<sm_count * VC_LB_DEL2, kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
-        nl += 2;
+        ++nl;
       } else {
         k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
         ++nl;

@@ -83,7 +83,13 @@ struct BuildParams {
   // per stratum row: (h << 6) | w — the hull kernel's candidate window is rows r ± h,
   // columns c ± w; 0 = the row goes to the clipping kernel (polar caps, wide rows)
   unsigned char del_hw[kDelRowsMax];
-  int del_kmax;  // largest window in del_hw (sizes the hull kernel's shared memory)
+  int del_kmax;  // largest window in del_hw (0: no row uses the hull kernel)
+  // hull rows grouped by window size (classes ≤ 34, ≤ 44, ≤ 64 candidates: 6, 4, 3 CTAs
+  // per SM by shared memory): rows del_rows[del_cls[k] .. del_cls[k+1]) of class k, whose
+  // largest window is del_cls_k[k]
+  unsigned short del_rows[kDelRowsMax];
+  int del_cls[4];
+  int del_cls_k[3];
   double del_zstep;  // 2 / rows: stratum height in z
   int del_cap;       // 1: the polar rows go to the cap kernel
   float del_cap_cos;           // cos δ, the cap kernel's candidate radius
