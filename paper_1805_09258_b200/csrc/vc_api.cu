@@ -290,12 +290,13 @@ static void del_row_table(BuildParams& P) {
     }
   }
   P.del_cls[3] = nr;
-  // polar rows: candidates within δ = 2.7 spacings (2·R_cell ≤ δ holds for all but a
-  // few cells), kept in 16-bit column indices
+  // polar rows: candidates within δ = 3 spacings (2·R_cell ≤ δ holds for all but ~1% of
+  // the cap cells; ≤ 40 candidates), kept in 16-bit column indices
   P.del_zstep = 2.0 / rows;
-  const double delta = 2.7 * std::sqrt(4.0 * pi / P.n_angular);
+  const double delta = 3.0 * std::sqrt(4.0 * pi / P.n_angular);
   P.del_cap = (on && P.del_kmax > 0 && rows >= 4 && 2 * cols <= 65535) ? 1 : 0;
   P.del_cap_cos = (float)std::cos(delta);
+  P.del_cap_sin = (float)std::sin(delta);
   P.del_cap_c2 = std::cos(0.5 * delta) * std::cos(0.5 * delta);
   P.del_cap_s2 = std::sin(0.5 * delta) * std::sin(0.5 * delta);
 }
@@ -417,6 +418,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.del_scratch = (double*)alloc(40, D == 3 ? (size_t)W.del_retry_cap * 48 * 3 * 8 : 16);
   W.del_fb = (int*)alloc(44, (D == 3 && !P.host_adjacency) ? (size_t)B * n * 4 : 16);
   W.del_fb_count = (unsigned int*)alloc(45, 8);
+  W.del_fb2 = (int*)alloc(46, (D == 3 && !P.host_adjacency) ? (size_t)B * n * 4 : 16);
+  W.del_fb2_count = (unsigned int*)alloc(47, 8);
   W.partial = (double*)alloc(37, B * kAsmParts * 64 * 8 + B * kAsmParts * 5 * 8);  // sums + 5 counters
   W.item_cap = item_cap;
   W.asm_items = item_cap > 0 ? (uint2*)alloc(41, (size_t)B * item_cap * 8) : nullptr;

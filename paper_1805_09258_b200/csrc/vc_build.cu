@@ -16,6 +16,7 @@
 //   k_make_record thread per (record, kind): eigen + radii (src/cache.py:146-189)
 #include <cfloat>
 #include <cstdio>
+#include <vector>
 
 #include "vc_device.cuh"
 #include "vc_eigen.cuh"
@@ -786,10 +787,10 @@ __global__ void __launch_bounds__(kDelBS, VC_LB_DEL2) k_delaunay_list(BuildParam
   double* sb = sa + kPolyV * kDelBS;
   int* sl = (int*)(sb + kPolyV * kDelBS);
   const int n = P.n_angular;
-  const unsigned cnt = *W.del_fb_count;
+  const unsigned cnt = *W.del_fb2_count;
   Poly poly{sa + threadIdx.x, sb + threadIdx.x, sl + threadIdx.x};
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
-    const int gid = W.del_fb[t];
+    const int gid = W.del_fb2[t];
     const int rec = gid / n, i = gid - rec * n;
     if (delaunay_point(P, W, rec, i, poly, own, own_cnt) == 2) {
       const unsigned slot = atomicAdd(W.del_retry_count, 1u);
@@ -845,6 +846,26 @@ struct Proj {
     return make_float2((float)(-(e1x * d0 + e1y * d1 + e1z * d2)) * inv,
                        (float)(-(e2x * d0 + e2y * d1 + e2z * d2)) * inv);
   }
+  // float64 projection (the fallback wrap)
+  __device__ __forceinline__ double2 d2(const double* q) const {
+    const double d0 = px - q[0], d1 = py - q[1], d2 = pz - q[2];
+    const double inv = 2.0 / (d0 * d0 + d1 * d1 + d2 * d2);
+    return make_double2(-(e1x * d0 + e1y * d1 + e1z * d2) * inv, -(e2x * d0 + e2y * d1 + e2z * d2) * inv);
+  }
+};
+
+template <class T> struct Vec2;
+template <> struct Vec2<float> {
+  using V = float2;
+  static constexpr float kEps = 5.9604645e-8f;  // 2⁻²⁴
+  __device__ static V nan() { return make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000)); }
+  __device__ static V proj(const Proj& pr, const double* q) { return pr(q); }
+};
+template <> struct Vec2<double> {
+  using V = double2;
+  static constexpr double kEps = 1.1102230246251565e-16;  // 2⁻⁵³
+  __device__ static V nan() { return make_double2(__longlong_as_double(0x7ff8000000000000LL), __longlong_as_double(0x7ff8000000000000LL)); }
+  __device__ static V proj(const Proj& pr, const double* q) { return pr.d2(q); }
 };
 
 // Counter-clockwise gift wrap of the projections us[0..K) (stride kHullBS) from `start`
@@ -852,43 +873,47 @@ struct Proj {
 // must exceed `margin` (the float32 error bound), else the wrap fails (returns 0).  The
 // current vertex and the initial candidate are parked as NaN during a scan, so the loop
 // body is the same for every candidate (NaN never wins and never trips the bound).
-__device__ __forceinline__ int gift_wrap(float2* us, int K, int start, float margin, unsigned char* hs) {
-  const float2 nan2 = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+template <class T, int BS>
+__device__ __forceinline__ int gift_wrap(typename Vec2<T>::V* us, int K, int start, T nmax, unsigned char* hs) {
+  using V = typename Vec2<T>::V;
+  const V nan2 = Vec2<T>::nan();
   int hn = 0, cur = start;
-  float mn = FLT_MAX;
   for (;;) {
-    hs[hn * kHullBS] = (unsigned char)cur;
+    hs[hn * BS] = (unsigned char)cur;
     ++hn;
-    const float2 a = us[cur * kHullBS];
+    const V a = us[cur * BS];
+    T mn = (T)FLT_MAX;
     int b0 = cur;
-    float2 b = nan2;
+    V b = nan2;
     do {  // the next candidate that is not NaN (the centre) as the initial best
       b0 = (b0 + 1 == K) ? 0 : b0 + 1;
-      b = us[b0 * kHullBS];
+      b = us[b0 * BS];
     } while (b.x != b.x && b0 != cur);
-    us[cur * kHullBS] = nan2;
-    us[b0 * kHullBS] = nan2;
-    float bx = b.x - a.x, by = b.y - a.y;
+    us[cur * BS] = nan2;
+    us[b0 * BS] = nan2;
+    T bx = b.x - a.x, by = b.y - a.y;
     int best = b0;
 #pragma unroll 4
     for (int c = 0; c < K; ++c) {
-      const float2 u = us[c * kHullBS];
-      const float cx = u.x - a.x, cy = u.y - a.y;
-      const float cr = bx * cy - by * cx;
-      mn = fminf(mn, fabsf(cr));
-      if (cr < 0.0f) { best = c; bx = cx; by = cy; }
+      const V u = us[c * BS];
+      const T cx = u.x - a.x, cy = u.y - a.y;
+      const T cr = bx * cy - by * cx;
+      mn = fmin(mn, fabs(cr));
+      if (cr < (T)0) { best = c; bx = cx; by = cy; }
     }
-    us[cur * kHullBS] = a;
-    us[b0 * kHullBS] = b;
+    us[cur * BS] = a;
+    us[b0 * BS] = b;
+    // float32 error bound of this step's orientations: each projection carries ≤ 5
+    // roundings relative to its norm, so |err(cross)| ≤ 30·2⁻²⁴·(|a| + |b|)(|a| + |c|)
+    // ≤ 32·2⁻²⁴·(|a|₁ + max|u|₁)²
+    const T la = fabs(a.x) + fabs(a.y) + nmax;
+    if (!(mn > (T)32 * Vec2<T>::kEps * la * la)) return 0;
     if (best == start) break;
     if (hn == kHullH) return 0;
     cur = best;
   }
-  return mn > margin ? hn : 0;
+  return hn;
 }
-
-// float32 error bound of one orientation test over projections of norm ≤ √m2
-__device__ __forceinline__ float wrap_margin(float m2) { return 128.0f * 5.9604645e-8f * m2; }
 
 // X ≥ √Q  ⇔  X ≥ 0 ∧ X² ≥ Q
 __device__ __forceinline__ bool ge_root(double X, double Q) { return X >= 0.0 && X * X >= Q; }
@@ -897,7 +922,7 @@ __device__ __forceinline__ bool ge_root(double X, double Q) { return X >= 0.0 &&
 // direction, `secure(c, cp, Q, tol)` tests one Voronoi vertex (c ∝ v; |c| cos R = c·p,
 // |c|² sin² R = Q).  Writes the valence and the owned triangles (i < both neighbours),
 // as delaunay_point; false leaves the cell to the clipping kernel.
-template <class GIdx, class Secure>
+template <int BS, class GIdx, class Secure>
 __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, const Proj& pr, size_t base, int i,
                                           const unsigned char* hs, int hn, GIdx gidx, Secure secure, int* own,
                                           int* own_cnt) {
@@ -908,7 +933,7 @@ __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, con
   double bxd = dirs[3 * (size_t)gb] - px, byd = dirs[3 * (size_t)gb + 1] - py, bzd = dirs[3 * (size_t)gb + 2] - pz;
   for (int t = 0; t < hn; ++t) {
     const double ax = bxd, ay = byd, az = bzd;
-    gb = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * kHullBS]);
+    gb = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * BS]);
     bxd = dirs[3 * (size_t)gb] - px; byd = dirs[3 * (size_t)gb + 1] - py; bzd = dirs[3 * (size_t)gb + 2] - pz;
     const double cx = ay * bzd - az * byd, cy = az * bxd - ax * bzd, cz = ax * byd - ay * bxd;
     const double cp = cx * px + cy * py + cz * pz;
@@ -919,7 +944,7 @@ __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, con
   }
   int c = 0, ga = g0;
   for (int t = 0; t < hn; ++t) {
-    const int gn = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * kHullBS]);
+    const int gn = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * BS]);
     if (i < ga && i < gn) {
       own[(base * kMaxV + c) * 2 + 0] = ga;
       own[(base * kMaxV + c) * 2 + 1] = gn;
@@ -932,7 +957,8 @@ __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, con
   return true;
 }
 
-__device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, int rec, int i, float2* us,
+template <class T, int BS>
+__device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, int rec, int i, typename Vec2<T>::V* us,
                                           unsigned char* hs, int* own, int* own_cnt) {
   const int n = P.n_angular, rows = P.rows, cols = P.cols;
   const int r0 = i / cols, c0 = i - r0 * cols;
@@ -945,22 +971,23 @@ __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, i
   int col0 = c0 - w;
   col0 += (col0 < 0) ? cols : 0;
   int K = 0, start = 0;
-  float m2 = 0.0f;
+  T m2 = 0, n1 = 0;
   for (int dr = -h; dr <= h; ++dr) {
     const double* rowp = dirs + 3 * (size_t)(r0 + dr) * cols;
     const double* q = rowp + 3 * col0;
     const double* rowe = rowp + 3 * cols;
     for (int dc = 0; dc < wc; ++dc) {
-      const float2 u = pr(q);
-      us[K * kHullBS] = u;
-      const float r2 = u.x * u.x + u.y * u.y;
+      const auto u = Vec2<T>::proj(pr, q);
+      us[K * BS] = u;
+      const T r2 = u.x * u.x + u.y * u.y;
       if (r2 > m2) { m2 = r2; start = K; }
+      n1 = fmax(n1, fabs(u.x) + fabs(u.y));
       ++K;
       q += 3;
       q = (q == rowe) ? rowp : q;
     }
   }
-  const int hn = gift_wrap(us, K, start, wrap_margin(m2), hs);
+  const int hn = gift_wrap<T, BS>(us, K, start, n1, hs);
   // candidate k → direction index (k / wc by a 16-bit reciprocal, exact for k < 2¹⁶/wc²)
   const unsigned rwc = (65536u + wc - 1) / wc;
   auto gidx = [&](int k) {
@@ -983,7 +1010,7 @@ __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, i
     if (bot) ok &= ge_root(cz - zb * cp - tol, sb2 * Q);
     return ok;
   };
-  return hull_star(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
+  return hull_star<BS>(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
 }
 
 // One launch per window class: thread → (record, row of the class, column).
@@ -1001,7 +1028,7 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W
     const int rs = rem / cols;
     const int i = (int)P.del_rows[P.del_cls[cls] + rs] * cols + (rem - rs * cols);
     cell = rec * n + i;
-    fb = !hull_cell(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
+    fb = !hull_cell<float, kHullBS>(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
   }
   const unsigned m = __ballot_sync(0xffffffffu, fb);
   if (m) {
@@ -1043,15 +1070,76 @@ __global__ void k_delaunay_rest(BuildParams P, Wave W) {
 // compacted into shared memory with their indices); besides the parallel below the two
 // rows, the security test asks R ≤ δ/2 of every Voronoi vertex, so no skipped direction
 // (farther than δ from p) can reach a circumcircle.
-constexpr int kCapSlots = 64;
+constexpr int kCapSlots = 40;
 constexpr size_t kCapSmem = (size_t)kHullBS * (kCapSlots * (sizeof(float2) + 2) + kHullH);
+
+// Candidate radius δ of a cap cell: cos δ and sin δ (pre-test, column range) and
+// cos²(δ/2), sin²(δ/2) (security R ≤ δ/2).
+struct CapRadius {
+  float cos_d, sin_d;
+  double c2, s2;
+};
+
+// One polar-row cell i of record rec (see k_delaunay_cap) with up to `slots` candidates.
+// One polar-row cell i of record rec (see k_delaunay_cap) with up to `slots` candidates.
+template <class T, int BS>
+__device__ __forceinline__ bool cap_cell(const BuildParams& P, const Wave& W, int rec, int i, const CapRadius& cr,
+                                         int slots, typename Vec2<T>::V* us, unsigned short* ix, unsigned char* hs,
+                                         int* own, int* own_cnt) {
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const bool north = i < cols;
+  const int rlo = north ? 0 : rows - 2;  // the two cap rows
+  const double* dirs = W.dirs + (size_t)rec * n * 3;
+  const float4* d32 = W.dirs32 + (size_t)rec * n;
+  const Proj pr(dirs[3 * (size_t)i], dirs[3 * (size_t)i + 1], dirs[3 * (size_t)i + 2]);
+  const float4 p32 = d32[i];
+  const float cutf = cr.cos_d - 1e-6f;
+  int K = 0, start = 0;
+  T m2 = 0, n1 = 0;
+  // columns within the azimuth half-width asin(sin δ / sin θ_p) of p's stratum column
+  // (the whole row when the δ-disc holds the pole), one column of slack either side
+  const int c0 = i - (north ? 0 : (rows - 1) * cols);
+  const float stp = sqrtf(p32.x * p32.x + p32.y * p32.y);
+  int half = cols;
+  if (stp > 1.01f * cr.sin_d) half = (int)ceilf(asinf(cr.sin_d / stp) * (float)cols * 0.15915494f) + 1;
+  const int span = (2 * half + 1 >= cols) ? cols : 2 * half + 1;
+  int cstart = (span == cols) ? 0 : c0 - half;
+  cstart += (cstart < 0) ? cols : 0;
+  for (int rr = rlo; rr < rlo + 2; ++rr) {
+    int col = cstart;
+    for (int t = 0; t < span; ++t) {
+      const int j = rr * cols + col;
+      col = (col + 1 == cols) ? 0 : col + 1;
+      const float4 q = d32[j];
+      if (p32.x * q.x + p32.y * q.y + p32.z * q.z > cutf) {
+        if (K == slots) return false;
+        const auto u = Vec2<T>::proj(pr, dirs + 3 * (size_t)j);
+        us[K * BS] = u;
+        ix[K * BS] = (unsigned short)(j - rlo * cols);
+        const T r2 = u.x * u.x + u.y * u.y;
+        if (r2 > m2) { m2 = r2; start = K; }
+        n1 = fmax(n1, fabs(u.x) + fabs(u.y));
+        ++K;
+      }
+    }
+  }
+  const int hn = gift_wrap<T, BS>(us, K, start, n1, hs);
+  auto gidx = [&](int s) { return rlo * cols + (int)ix[s * BS]; };
+  // the parallel below (north) / above (south) the two cap rows
+  const double zb = north ? 1.0 - 2.0 * P.del_zstep : 1.0 - P.del_zstep * (rows - 2);
+  const double sb2 = fmax(0.0, 1.0 - zb * zb);
+  auto secure = [&](double cx, double cy, double cz, double cp, double Q, double tol) {
+    bool ok = (cp - tol) * (cp - tol) * cr.s2 >= cr.c2 * Q;  // R ≤ δ/2
+    ok &= north ? ge_root(cz - zb * cp - tol, sb2 * Q) : ge_root(zb * cp - cz - tol, sb2 * Q);
+    return ok;
+  };
+  return hull_star<BS>(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
+}
 
 __global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W, int* own, int* own_cnt) {
   extern __shared__ float2 csm[];
   unsigned short* ix0 = (unsigned short*)(csm + kCapSlots * kHullBS);
-  unsigned short* ix = ix0 + threadIdx.x;
   unsigned char* hs = (unsigned char*)(ix0 + kCapSlots * kHullBS) + threadIdx.x;
-  float2* us = csm + threadIdx.x;
   const int n = P.n_angular, rows = P.rows, cols = P.cols;
   const long long gid = (long long)blockIdx.x * kHullBS + threadIdx.x;  // over B × 2 × cols
   bool fb = false;
@@ -1059,45 +1147,11 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W,
   if (gid < (long long)W.B * 2 * cols) {
     const int rec = (int)(gid / (2 * cols));
     const int k = (int)(gid - (long long)rec * 2 * cols);
-    const bool north = k < cols;
-    const int i = north ? k : (rows - 1) * cols + (k - cols);
+    const int i = k < cols ? k : (rows - 1) * cols + (k - cols);
     cell = rec * n + i;
-    const int rlo = north ? 0 : rows - 2;  // the two cap rows
-    const double* dirs = W.dirs + (size_t)rec * n * 3;
-    const float4* d32 = W.dirs32 + (size_t)rec * n;
-    const Proj pr(dirs[3 * (size_t)i], dirs[3 * (size_t)i + 1], dirs[3 * (size_t)i + 2]);
-    const float4 p32 = d32[i];
-    const float cutf = P.del_cap_cos - 1e-6f;
-    int K = 0, start = 0;
-    float m2 = 0.0f;
-    bool full = false;
-    for (int j = rlo * cols; j < (rlo + 2) * cols; ++j) {
-      const float4 q = d32[j];
-      if (p32.x * q.x + p32.y * q.y + p32.z * q.z > cutf) {
-        if (K == kCapSlots) { full = true; break; }
-        const float2 u = pr(dirs + 3 * (size_t)j);
-        us[K * kHullBS] = u;
-        ix[K * kHullBS] = (unsigned short)(j - rlo * cols);
-        const float r2 = u.x * u.x + u.y * u.y;
-        if (r2 > m2) { m2 = r2; start = K; }
-        ++K;
-      }
-    }
-    fb = true;
-    if (!full) {
-      const int hn = gift_wrap(us, K, start, wrap_margin(m2), hs);
-      auto gidx = [&](int s) { return rlo * cols + (int)ix[s * kHullBS]; };
-      // the parallel below (north) / above (south) the two cap rows
-      const double zb = north ? 1.0 - 2.0 * P.del_zstep : 1.0 - P.del_zstep * (rows - 2);
-      const double sb2 = fmax(0.0, 1.0 - zb * zb);
-      const double c2 = P.del_cap_c2, s2 = P.del_cap_s2;  // cos², sin² of δ/2
-      auto secure = [&](double cx, double cy, double cz, double cp, double Q, double tol) {
-        bool ok = (cp - tol) * (cp - tol) * s2 >= c2 * Q;  // R ≤ δ/2
-        ok &= north ? ge_root(cz - zb * cp - tol, sb2 * Q) : ge_root(zb * cp - cz - tol, sb2 * Q);
-        return ok;
-      };
-      fb = !hull_star(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
-    }
+    const CapRadius cr{P.del_cap_cos, P.del_cap_sin, P.del_cap_c2, P.del_cap_s2};
+    fb = !cap_cell<float, kHullBS>(P, W, rec, i, cr, kCapSlots, csm + threadIdx.x, ix0 + threadIdx.x, hs, own,
+                                   own_cnt);
   }
   const unsigned m = __ballot_sync(0xffffffffu, fb);
   if (m) {
@@ -1106,6 +1160,41 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W,
     if (lane == leader) slot = atomicAdd(W.del_fb_count, (unsigned)__popc(m));
     slot = __shfl_sync(0xffffffffu, slot, leader);
     if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = cell;
+  }
+}
+
+// Cells the float32 wrap could not decide (an orientation within its error bound) or
+// certify, wrapped again with float64 projections; polar-row cells and the cells still
+// failing go on to the clipping kernel (second list).
+constexpr int kHull64BS = 64;
+
+__global__ void __launch_bounds__(kHull64BS) k_delaunay_hull64(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ double2 dsm2[];
+  unsigned char* hs = (unsigned char*)(dsm2 + kHullSlots * kHull64BS) + threadIdx.x;
+  const int n = P.n_angular;
+  const unsigned cnt = *W.del_fb_count;
+  const unsigned tot = (cnt + 31u) & ~31u;  // warp-uniform trip count for the ballot
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+    bool fb = false;
+    int cell = 0;
+    if (t < cnt) {
+      cell = W.del_fb[t];
+      const int rec = cell / n, i = cell - rec * n;
+      const int r0 = i / P.cols;
+      if (P.del_cap && (r0 == 0 || r0 == P.rows - 1)) {
+        fb = true;  // the clipping kernel takes the polar cells the cap kernel left
+      } else {
+        fb = !hull_cell<double, kHull64BS>(P, W, rec, i, dsm2 + threadIdx.x, hs, own, own_cnt);
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, fb);
+    if (m) {
+      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+      unsigned slot = 0;
+      if (lane == leader) slot = atomicAdd(W.del_fb2_count, (unsigned)__popc(m));
+      slot = __shfl_sync(0xffffffffu, slot, leader);
+      if (fb) W.del_fb2[slot + __popc(m & ((1u << lane) - 1u))] = cell;
+    }
   }
 }
 
@@ -1760,6 +1849,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         cudaFuncSetAttribute(k_delaunay_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kHullBS * (kHullSlots * sizeof(float2) + kHullH)));
         cudaFuncSetAttribute(k_delaunay_cap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
+        cudaFuncSetAttribute(k_delaunay_hull64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kHull64BS * (kHullSlots * sizeof(double2) + kHullH)));
         smem_attr = true;
       }
       prof_begin(KC_DELAUNAY, st);
@@ -1789,9 +1880,32 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
           cudaMemcpyAsync(&c, W.del_fb_count, 4, cudaMemcpyDeviceToHost, st);
           cudaStreamSynchronize(st);
           fprintf(stderr, "[volcache] hull fallback cells: %u of %lld\n", c, nt);
+          if (getenv("VOLCACHE_DEL_STATS")[0] == '3') {  // handed-back cells per stratum row
+            std::vector<int> l(c), hist(P.rows, 0);
+            cudaMemcpy(l.data(), W.del_fb, (size_t)c * 4, cudaMemcpyDeviceToHost);
+            for (int g : l) ++hist[(g % P.n_angular) / P.cols];
+            for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
+            fprintf(stderr, "\n");
+          }
+          if (getenv("VOLCACHE_DEL_STATS")[0] >= '2') {
+            k_delaunay_hull64<<<sm_count * 3, kHull64BS,
+                                (size_t)kHull64BS * (kHullSlots * sizeof(double2) + kHullH), st>>>(P, W, own,
+                                                                                                          own_cnt);
+            cudaMemcpyAsync(&c, W.del_fb2_count, 4, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "[volcache] after the float64 wrap: %u\n", c);
+            std::vector<int> l(c), hist(P.rows, 0);
+            cudaMemcpy(l.data(), W.del_fb2, (size_t)c * 4, cudaMemcpyDeviceToHost);
+            for (int g : l) ++hist[(g % P.n_angular) / P.cols];
+            for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
+            fprintf(stderr, "\n");
+          }
         }
+        cudaMemsetAsync(W.del_fb2_count, 0, sizeof(unsigned int), st);
+        k_delaunay_hull64<<<sm_count * 3, kHull64BS, (size_t)kHull64BS * (kHullSlots * sizeof(double2) + kHullH),
+                            st>>>(P, W, own, own_cnt);
         k_delaunay_list<<<sm_count * VC_LB_DEL2, kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
-        ++nl;
+        nl += 2;
       } else {
         k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
         ++nl;

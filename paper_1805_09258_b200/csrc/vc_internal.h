@@ -92,7 +92,7 @@ struct BuildParams {
   int del_cls_k[3];
   double del_zstep;  // 2 / rows: stratum height in z
   int del_cap;       // 1: the polar rows go to the cap kernel
-  float del_cap_cos;           // cos δ, the cap kernel's candidate radius
+  float del_cap_cos, del_cap_sin;  // cos δ, sin δ: the cap kernel's candidate radius
   double del_cap_c2, del_cap_s2;  // cos²(δ/2), sin²(δ/2)
 };
 
@@ -136,8 +136,10 @@ struct Wave {
   unsigned int* del_retry_count;
   int del_retry_cap;
   double* del_scratch;   // del_retry_cap × 48 × 3 doubles of global-memory polygons
-  int* del_fb;           // B × n: cells the hull kernel hands to the clipping kernel
+  int* del_fb;           // B × n: cells the float32 hull kernels hand back
   unsigned int* del_fb_count;
+  int* del_fb2;          // B × n: cells the float64 wrap hands to the clipping kernel
+  unsigned int* del_fb2_count;
   uint2* asm_items;      // B × item_cap assembly items (element, ring·4 + rep) in
                          // kAsmParts per-warp segments (null: fused assembly only)
   int* item_n;           // B × kAsmParts × 2: segment end of the surface / media items
