@@ -166,6 +166,7 @@ DevScene dev_scene(const vc_scene* sc) {
   S.K = sc->K;
   S.geo = sc->geo.dev();
   S.emit = sc->emit.dev();
+  S.ep = sc->ep;
   S.n_es = sc->n_es;
   S.reflective = sc->reflective;
   for (int a = 0; a < 3; ++a) {
@@ -365,6 +366,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
                kStats * 8 + 32 + 8;
   if (D == 3) per += (size_t)P.n_tris * 12 + (P.host_adjacency ? 0 : (size_t)n * 32 * 8);
   per += media_per / 10 * 80;                     // two-pass gather queue
+  per += (media_per / 16 + 1) * 4;                // gather run → direction table
   per += (size_t)n * 8 * ((P.r_ub + 63) / 64);  // live-sample bit masks
   per += (size_t)n * 16;                          // float32 directions
   per += (size_t)n * 16 + kAsmParts * 96 * 8;     // DirInfo + assembly partials
@@ -394,6 +396,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.idx = (int*)alloc(4, B * n * 4);
   W.cnt = (int*)alloc(5, B * n * 4);
   W.pre = (int*)alloc(6, B * n * 4);
+  W.run_stride = (int)(media_per / 16 + 1);
+  W.run_dir = (int*)alloc(48, (size_t)B * W.run_stride * 4);
   W.lo = (double*)alloc(7, B * n * 24);
   W.rec_R = (int*)alloc(8, B * 4);
   W.rec_P = (int*)alloc(9, B * 4);
@@ -558,6 +562,127 @@ int vc_profile_read(double* ms, int64_t* launches, int max_classes) {
   return KC_COUNT;
 }
 
+// Emitter plane grids (3D): triangles grouped by plane (normals and offsets equal to
+// 1e-9, every vertex within 1e-9·scale of the group plane), at most kEmitPlanes groups;
+// per group a grid of about 4 triangles' worth of area per cell over the triangles'
+// in-plane boxes, each padded by 1e-5·scale — far beyond the distance (≤ 1e-6·scale for
+// rays at ≥ 1e-3 of grazing) between the plane point a ray lands on and the point of a
+// triangle the float64 hit test accepts.  Returns false when the emitters need more planes.
+static bool build_emit_planes(const std::vector<double>& prim, const std::vector<int>& order, double scale,
+                              vc::EmitPlanes* ep, std::vector<int>* start, std::vector<int>* tri) {
+  using vc::kEmitPlanes;
+  *ep = vc::EmitPlanes{};
+  const int K = (int)order.size();
+  if (K == 0) return false;
+  std::vector<int> grp(K);
+  int ng = 0;
+  for (int k = 0; k < K; ++k) {
+    const double* P = &prim[(size_t)order[k] * 9];
+    const double* e1 = P + 3;
+    const double* e2 = P + 6;
+    double nv[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const double nn = std::sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    if (!(nn > 0.0)) return false;
+    int big = 0;
+    for (int a = 0; a < 3; ++a) {
+      nv[a] /= nn;
+      if (std::fabs(nv[a]) > std::fabs(nv[big])) big = a;
+    }
+    if (nv[big] < 0.0)
+      for (int a = 0; a < 3; ++a) nv[a] = -nv[a];
+    const double c = nv[0] * P[0] + nv[1] * P[1] + nv[2] * P[2];
+    int g = -1;
+    for (int h = 0; h < ng && g < 0; ++h) {
+      bool same = std::fabs(c - ep->c[h]) <= 1e-9 * scale;
+      for (int a = 0; a < 3; ++a) same &= std::fabs(nv[a] - ep->n[h][a]) <= 1e-9;
+      for (int v = 0; v < 3 && same; ++v) {  // every vertex on the group plane
+        double x[3];
+        for (int a = 0; a < 3; ++a) x[a] = P[a] + (v == 1 ? P[3 + a] : 0.0) + (v == 2 ? P[6 + a] : 0.0);
+        same &= std::fabs(ep->n[h][0] * x[0] + ep->n[h][1] * x[1] + ep->n[h][2] * x[2] - ep->c[h]) <= 1e-9 * scale;
+      }
+      if (same) g = h;
+    }
+    if (g < 0) {
+      if (ng == kEmitPlanes) return false;
+      g = ng++;
+      for (int a = 0; a < 3; ++a) ep->n[g][a] = nv[a];
+      ep->c[g] = c;
+      // in-plane frame: a1 ⟂ n from the axis least aligned with n, a2 = n × a1
+      double ax[3] = {0.0, 0.0, 0.0};
+      ax[(big + 1) % 3] = 1.0;
+      double d = ax[0] * nv[0] + ax[1] * nv[1] + ax[2] * nv[2];
+      double a1[3] = {ax[0] - d * nv[0], ax[1] - d * nv[1], ax[2] - d * nv[2]};
+      const double l1 = std::sqrt(a1[0] * a1[0] + a1[1] * a1[1] + a1[2] * a1[2]);
+      for (int a = 0; a < 3; ++a) ep->a1[g][a] = a1[a] / l1;
+      const double* u = ep->a1[g];
+      ep->a2[g][0] = nv[1] * u[2] - nv[2] * u[1];
+      ep->a2[g][1] = nv[2] * u[0] - nv[0] * u[2];
+      ep->a2[g][2] = nv[0] * u[1] - nv[1] * u[0];
+    }
+    grp[k] = g;
+  }
+  ep->ng = ng;
+  const double pad = 1e-5 * scale;
+  std::vector<double> box((size_t)K * 4);  // in-plane (x0, y0, x1, y1), padded
+  for (int k = 0; k < K; ++k) {
+    const double* P = &prim[(size_t)order[k] * 9];
+    const int g = grp[k];
+    double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+    for (int v = 0; v < 3; ++v) {
+      double x[3];
+      for (int a = 0; a < 3; ++a) x[a] = P[a] + (v == 1 ? P[3 + a] : 0.0) + (v == 2 ? P[6 + a] : 0.0);
+      double px = 0.0, py = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        px += ep->a1[g][a] * x[a];
+        py += ep->a2[g][a] * x[a];
+      }
+      x0 = std::min(x0, px); x1 = std::max(x1, px);
+      y0 = std::min(y0, py); y1 = std::max(y1, py);
+    }
+    box[4 * k] = x0 - pad; box[4 * k + 1] = y0 - pad;
+    box[4 * k + 2] = x1 + pad; box[4 * k + 3] = y1 + pad;
+  }
+  int ncell = 0;
+  std::vector<std::vector<int>> cells;
+  for (int g = 0; g < ng; ++g) {
+    double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY, area = 0.0;
+    int cnt = 0;
+    for (int k = 0; k < K; ++k)
+      if (grp[k] == g) {
+        x0 = std::min(x0, box[4 * k]); y0 = std::min(y0, box[4 * k + 1]);
+        x1 = std::max(x1, box[4 * k + 2]); y1 = std::max(y1, box[4 * k + 3]);
+        area += (box[4 * k + 2] - box[4 * k]) * (box[4 * k + 3] - box[4 * k + 1]);
+        ++cnt;
+      }
+    const double cs = std::sqrt(std::max(area / (4.0 * cnt), 1e-30));
+    const int gx = std::min(128, std::max(1, (int)std::ceil((x1 - x0) / cs)));
+    const int gy = std::min(128, std::max(1, (int)std::ceil((y1 - y0) / cs)));
+    ep->lo[g][0] = x0; ep->lo[g][1] = y0;
+    ep->inv[g][0] = gx / (x1 - x0); ep->inv[g][1] = gy / (y1 - y0);
+    ep->gx[g] = gx; ep->gy[g] = gy; ep->cell0[g] = ncell;
+    cells.resize((size_t)ncell + (size_t)gx * gy);
+    for (int k = 0; k < K; ++k) {
+      if (grp[k] != g) continue;
+      const int i0 = std::max(0, (int)std::floor((box[4 * k] - x0) * ep->inv[g][0]));
+      const int i1 = std::min(gx - 1, (int)std::floor((box[4 * k + 2] - x0) * ep->inv[g][0]));
+      const int j0 = std::max(0, (int)std::floor((box[4 * k + 1] - y0) * ep->inv[g][1]));
+      const int j1 = std::min(gy - 1, (int)std::floor((box[4 * k + 3] - y0) * ep->inv[g][1]));
+      for (int j = j0; j <= j1; ++j)
+        for (int i = i0; i <= i1; ++i) cells[(size_t)ncell + (size_t)j * gx + i].push_back(k);
+    }
+    ncell += gx * gy;
+  }
+  start->assign((size_t)ncell + 1, 0);
+  tri->clear();
+  for (int c = 0; c < ncell; ++c) {
+    (*start)[c] = (int)tri->size();
+    tri->insert(tri->end(), cells[c].begin(), cells[c].end());
+  }
+  (*start)[ncell] = (int)tri->size();
+  if (tri->empty()) tri->push_back(0);
+  return true;
+}
+
 int vc_scene_create(int dim, int n_surfaces, const double* vertices, const double* emission,
                     const double* albedo, const double* bounds_min, const double* bounds_max,
                     double sigma_s, double sigma_a, vc_scene** out) {
@@ -661,6 +786,20 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
   };
   make_set(all, 16, sc->geo, leaf_env("VOLCACHE_LEAF_GEO", 2));  // leaf ≤ 2: fewer float64 tests
   make_set(em, 4, sc->emit, leaf_env("VOLCACHE_LEAF_EMIT", 2));
+  if (dim == 3 && !(getenv("VOLCACHE_EMIT_PLANES") && getenv("VOLCACHE_EMIT_PLANES")[0] == '0')) {
+    // leaf order of the emitter set (as make_set laid it out)
+    std::vector<int> eorder((size_t)sc->emit.K);
+    if (sc->emit.K) cudaMemcpy(eorder.data(), sc->emit.prim_id, eorder.size() * 4, cudaMemcpyDeviceToHost);
+    std::vector<int> start, tri;
+    if (build_emit_planes(prim, eorder, sc->scale, &sc->ep, &start, &tri)) {
+      up((void**)&sc->d_ep_start, start.data(), start.size() * 4);
+      up((void**)&sc->d_ep_tri, tri.data(), tri.size() * 4);
+      sc->ep.cell_start = sc->d_ep_start;
+      sc->ep.cell_tri = sc->d_ep_tri;
+    } else {
+      sc->ep.ng = 0;
+    }
+  }
   up((void**)&sc->d_normal, K ? normal.data() : nullptr, normal.size() * 8);
   up((void**)&sc->d_emission, K ? sc->emission.data() : nullptr, sc->emission.size() * 8);
   up((void**)&sc->d_albedo, K ? sc->albedo.data() : nullptr, sc->albedo.size() * 8);

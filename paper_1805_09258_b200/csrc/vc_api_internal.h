@@ -12,7 +12,7 @@
 namespace vc {
 
 struct Workspace {
-  static constexpr int kSlots = 48;
+  static constexpr int kSlots = 56;
   void* ptr[kSlots] = {nullptr};
   size_t cap[kSlots] = {0};
   void* get(int slot, size_t bytes, cudaError_t* err);
@@ -60,6 +60,9 @@ struct vc_scene {
   int reflective = 0;
   int sm_count = 148;
   GpuBvh geo, emit;
+  vc::EmitPlanes ep{};   // device pointers owned here
+  int* d_ep_start = nullptr;
+  int* d_ep_tri = nullptr;
   double* d_normal = nullptr;
   double* d_emission = nullptr;
   double* d_albedo = nullptr;
@@ -76,6 +79,8 @@ struct vc_scene {
     cudaFree(d_es_pos);
     cudaFree(d_es_w);
     cudaFree(d_es_surf);
+    cudaFree(d_ep_start);
+    cudaFree(d_ep_tri);
   }
 };
 

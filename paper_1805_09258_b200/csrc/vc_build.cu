@@ -120,6 +120,12 @@ __device__ inline long long block_exscan(long long v, long long& total, long lon
   return pre;
 }
 
+#ifndef VC_GATHER_RUN
+#define VC_GATHER_RUN 16
+#endif
+constexpr int kGatherRun = VC_GATHER_RUN;  // consecutive samples per thread in pass 1
+static_assert(kGatherRun == 16, "run table stride (vc_api.cu)");
+
 constexpr int kRingBS = 512;
 
 __global__ void __launch_bounds__(kRingBS) k_rings(BuildParams P, Wave W) {
@@ -154,6 +160,10 @@ __global__ void __launch_bounds__(kRingBS) k_rings(BuildParams P, Wave W) {
       const size_t g = (size_t)rec * n + k;
       W.cnt[g] = c;
       W.pre[g] = (int)(run + pre);
+      // gather runs (kGatherRun consecutive samples) that start in this direction
+      const int j0 = (int)(run + pre);
+      for (int m = (j0 + kGatherRun - 1) / kGatherRun; m * kGatherRun < j0 + c; ++m)
+        W.run_dir[(size_t)rec * W.run_stride + m] = k;
       const double* lo = W.lo + g * 3;
       DirInfo di;
       di.s = s[k];
@@ -305,10 +315,6 @@ static_assert(sizeof(GatherItem) == 80, "queue entry layout (workspace sizing)")
 
 
 
-#ifndef VC_GATHER_RUN
-#define VC_GATHER_RUN 16
-#endif
-constexpr int kGatherRun = VC_GATHER_RUN;  // consecutive samples per thread in pass 1
 
 __device__ __forceinline__ void store_media(float* out, const double* v) {
 #pragma unroll
@@ -356,13 +362,8 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
     int k = 0, i = 0;
     Pcg64 g;
     if (j0 < Pr) {
-      // direction of the first sample: last k with pre[k] ≤ j0
-      int a = 0, b = n - 1;
-      while (a < b) {
-        int mid = (a + b + 1) >> 1;
-        if (pre[mid] <= j0) a = mid; else b = mid - 1;
-      }
-      k = a;
+      // direction of the first sample (run table written by k_rings)
+      k = W.run_dir[(size_t)rec * W.run_stride + j0 / kGatherRun];
       i = j0 - pre[k];
       g = pcg_load(st);
       pcg_advance(g, (unsigned long long)(draws0 + (long long)(D == 3 ? 2 : 1) * j0), jt);
@@ -387,10 +388,11 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
         } else {
           double u0 = g.next_double(), u1 = g.next_double();
           double z = sub(1.0, mul(2.0, u0));
-          double phi = mul(2.0 * kPi, u1);
           double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+          // cos, sin of φ = 2π·u1 (src/transport.py:274-285) without the range reduction of
+          // sincos(φ): equal to the reference's cos(fl(2π·u1)) within an ulp of φ
           double sp, cp;
-          sincos(phi, &sp, &cp);
+          sincospi(2.0 * u1, &sp, &cp);
           gd[0] = mul(sq, cp);
           gd[1] = mul(sq, sp);
           gd[2] = z;

@@ -401,6 +401,42 @@ __device__ bool occluded(const DevScene& S, const double* o, const double* d, do
 template <int D>
 __device__ __forceinline__ void nearest_emitter(const DevScene& S, const double* o, const double* d, double& te,
                                                 int& ie) {
+  if constexpr (D == 3) {
+    if (S.ep.ng > 0) {
+      // plane grids: the float64 hit test on the triangles of the cell the ray lands in,
+      // (t, index) minimum as the BVH; rays within 1e-3 of grazing a plane take the BVH
+      const EmitPlanes& E = S.ep;
+      te = INFINITY;
+      ie = -1;
+      bool ok = true;
+      for (int g = 0; g < E.ng && ok; ++g) {
+        const double dn = E.n[g][0] * d[0] + E.n[g][1] * d[1] + E.n[g][2] * d[2];
+        if (fabs(dn) < 1e-3) {
+          ok = false;
+          break;
+        }
+        const double tp = (E.c[g] - (E.n[g][0] * o[0] + E.n[g][1] * o[1] + E.n[g][2] * o[2])) / dn;
+        if (tp < -1e-5 * S.scale) continue;
+        const double X[3] = {o[0] + tp * d[0], o[1] + tp * d[1], o[2] + tp * d[2]};
+        const double px = E.a1[g][0] * X[0] + E.a1[g][1] * X[1] + E.a1[g][2] * X[2];
+        const double py = E.a2[g][0] * X[0] + E.a2[g][1] * X[1] + E.a2[g][2] * X[2];
+        const double fx = (px - E.lo[g][0]) * E.inv[g][0], fy = (py - E.lo[g][1]) * E.inv[g][1];
+        if (!(fx >= 0.0 && fy >= 0.0 && fx < E.gx[g] && fy < E.gy[g])) continue;
+        const int cell = E.cell0[g] + (int)fy * E.gx[g] + (int)fx;
+        for (int q = E.cell_start[cell]; q < E.cell_start[cell + 1]; ++q) {
+          const int k = E.cell_tri[q];
+          const double t = hit_tri(S.emit.prim + (size_t)k * 9, o, d, S.t_eps);
+          if (t == INFINITY) continue;
+          const int id = S.emit.prim_id[k];
+          if (t < te || (t == te && id < ie)) {
+            te = t;
+            ie = id;
+          }
+        }
+      }
+      if (ok) return;
+    }
+  }
   bvh_closest<D>(S.emit, S.t_eps, 1e-5f * (float)S.scale, o, d, te, ie);
 }
 

@@ -36,6 +36,20 @@ struct DevBvh {
   const int* prim_id;    // leaf order → original surface index
 };
 
+// Emitters grouped by plane (3D, ≤ kEmitPlanes planes), each with a 2D grid of the
+// triangles overlapping its cells: a gather ray meets each plane once and tests only the
+// triangles of the cell it lands in (vc_api.cu: build_emit_planes).
+constexpr int kEmitPlanes = 4;
+struct EmitPlanes {
+  int ng;                        // planes (0: the emitter BVH answers every query)
+  double n[kEmitPlanes][3], c[kEmitPlanes];          // unit normal, offset (n·x = c)
+  double a1[kEmitPlanes][3], a2[kEmitPlanes][3];     // in-plane frame about c·n
+  double lo[kEmitPlanes][2], inv[kEmitPlanes][2];    // grid origin and 1 / cell size
+  int gx[kEmitPlanes], gy[kEmitPlanes], cell0[kEmitPlanes];
+  const int* cell_start;         // CSR over every plane's cells
+  const int* cell_tri;           // leaf-order indices into the emitter set
+};
+
 // Scene as seen by kernels (passed by value).
 struct DevScene {
   int dim;
@@ -48,6 +62,7 @@ struct DevScene {
   double max_emission;
   DevBvh geo;            // every surface
   DevBvh emit;           // emitting surfaces only (emitter-first gather when !reflective)
+  EmitPlanes ep;         // plane grids over the emitters (gather queries)
   const double* normal;  // original order, dim doubles each
   const double* emission;// original order, 3 doubles
   const double* albedo;  // original order, 3 doubles
@@ -116,6 +131,8 @@ struct Wave {
   int* idx;              // B × n primary hit surface (−1: bounds)
   int* cnt;              // B × n live rings per direction (after clamp to R)
   int* pre;              // B × n exclusive prefix of cnt within the record
+  int* run_dir;          // B × run_stride: direction of media sample 16·m (gather runs)
+  int run_stride;
   double* lo;            // B × n × 3 surface radiance
   int* rec_R;            // B rings per record
   int* rec_P;            // B live media samples per record
