@@ -1165,38 +1165,186 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W,
   }
 }
 
-// Cells the float32 wrap could not decide (an orientation within its error bound) or
-// certify, wrapped again with float64 projections; polar-row cells and the cells still
-// failing go on to the clipping kernel (second list).
-constexpr int kHull64BS = 64;
+// Cells the float32 kernels hand back (an orientation within the float32 error bound, a
+// star not certified by its window or disc, a polar cell past the cap kernel's radius):
+// one warp per cell in float64.  Candidates are the directions within δ of p (lanes over
+// the stratum rows and columns that can hold them, ballot-compacted into the warp's
+// shared memory); each gift-wrap step is a warp reduction under the orientation order
+// (from a hull vertex every other projection lies in a half-plane, so "more clockwise" is
+// a strict order); the star is kept when every circumradius R ≤ δ/2, else δ grows to
+// 2.05·max R and the cell is redone (at most 3 radii, ≤ kWarpK candidates).  Cells still
+// open go to the clipping kernel (second list).
+constexpr int kWarpK = 192;
+constexpr int kWarpBS = 256;
+constexpr size_t kWarpSmem = (size_t)(kWarpBS / 32) * (kWarpK * (sizeof(double2) + 4) + kHullH * 4);
 
-__global__ void __launch_bounds__(kHull64BS) k_delaunay_hull64(BuildParams P, Wave W, int* own, int* own_cnt) {
-  extern __shared__ double2 dsm2[];
-  unsigned char* hs = (unsigned char*)(dsm2 + kHullSlots * kHull64BS) + threadIdx.x;
+__device__ bool warp_cell(const BuildParams& P, const Wave& W, int rec, int i, double2* us, int* ix, int* hs,
+                          int* own, int* own_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const double* dirs = W.dirs + (size_t)rec * n * 3;
+  const float4* d32 = W.dirs32 + (size_t)rec * n;
+  const double px = dirs[3 * (size_t)i], py = dirs[3 * (size_t)i + 1], pz = dirs[3 * (size_t)i + 2];
+  const Proj pr(px, py, pz);
+  const float4 p32 = d32[i];
+  const double st = sqrt(fmax(0.0, 1.0 - pz * pz));
+  double delta = P.del_warp_delta;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    const double cd = cos(delta), sd = sin(delta);
+    const float cutf = (float)cd - 1e-6f;
+    // stratum rows meeting z ∈ [cos(θ + δ), cos(θ − δ)], columns within asin(sin δ / sin θ)
+    const bool pole_n = st <= sd && pz > 0.0, pole_s = st <= sd && pz < 0.0;
+    auto row_of = [&](double z) { return min(max((int)floor((1.0 - z) * rows * 0.5), 0), rows - 1); };
+    const int ra = pole_n ? 0 : row_of(pz * cd + st * sd + 1e-9);
+    const int rb = pole_s ? rows - 1 : row_of(pz * cd - st * sd - 1e-9);
+    const int c0 = i % cols;
+    int half = cols;
+    if (!pole_n && !pole_s) half = (int)ceil(asin(fmin(1.0, sd / st)) * cols * 0.15915494309189535) + 1;
+    const int span = (2 * half + 1 >= cols) ? cols : 2 * half + 1;
+    int cstart = (span == cols) ? 0 : c0 - half;
+    cstart += (cstart < 0) ? cols : 0;
+    const int total = (rb - ra + 1) * span;
+    int K = 0;
+    for (int t0 = 0; t0 < total; t0 += 32) {
+      const int t = t0 + lane;
+      bool take = false;
+      int j = 0;
+      if (t < total) {
+        const int rr = ra + t / span;
+        int col = cstart + t % span;
+        col -= (col >= cols) ? cols : 0;
+        j = rr * cols + col;
+        const float4 q = d32[j];
+        take = p32.x * q.x + p32.y * q.y + p32.z * q.z > cutf && j != i;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, take);
+      const int pos = K + __popc(m & ((1u << lane) - 1u));
+      if (take && pos < kWarpK) {
+        us[pos] = pr.d2(dirs + 3 * (size_t)j);
+        ix[pos] = j;
+      }
+      K += __popc(m);
+    }
+    if (K > kWarpK || K < 3) return false;
+    __syncwarp();
+    // start: the largest projection (nearest direction), a hull vertex; L1 bound N
+    double best_r = -1.0, nmax = 0.0;
+    int start = -1;
+    for (int c = lane; c < K; c += 32) {
+      const double2 u = us[c];
+      const double r = u.x * u.x + u.y * u.y;
+      nmax = fmax(nmax, fabs(u.x) + fabs(u.y));
+      if (r > best_r) { best_r = r; start = c; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double r2 = __shfl_xor_sync(0xffffffffu, best_r, o);
+      const int s2 = __shfl_xor_sync(0xffffffffu, start, o);
+      if (r2 > best_r || (r2 == best_r && s2 < start)) { best_r = r2; start = s2; }
+      nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    }
+    // gift wrap, one warp reduction per step
+    int hn = 0, cur = start;
+    bool bad = false;
+    for (;;) {
+      if (lane == 0) hs[hn] = cur;
+      ++hn;
+      const double2 a = us[cur];
+      const double la = fabs(a.x) + fabs(a.y) + nmax;
+      const double margin = 32.0 * 1.1102230246251565e-16 * la * la;
+      int b = -1;
+      double bx = 0.0, by = 0.0;
+      for (int c = lane; c < K; c += 32) {
+        if (c == cur) continue;
+        const double2 u = us[c];
+        const double cx = u.x - a.x, cy = u.y - a.y;
+        if (b < 0) { b = c; bx = cx; by = cy; continue; }
+        const double cr = bx * cy - by * cx;
+        bad |= fabs(cr) <= margin;
+        if (cr < 0.0) { b = c; bx = cx; by = cy; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const int b2 = __shfl_xor_sync(0xffffffffu, b, o);
+        const double x2 = __shfl_xor_sync(0xffffffffu, bx, o), y2 = __shfl_xor_sync(0xffffffffu, by, o);
+        if (b2 >= 0) {
+          if (b < 0) { b = b2; bx = x2; by = y2; }
+          else if (b2 != b) {
+            const double cr = bx * y2 - by * x2;
+            bad |= fabs(cr) <= margin;
+            // keep the more clockwise; both lanes of a pair must agree
+            if (cr < 0.0 || (cr == 0.0 && b2 < b)) { b = b2; bx = x2; by = y2; }
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, bad)) return false;
+      if (b == start) break;
+      if (hn == kHullH) return false;
+      cur = b;
+    }
+    __syncwarp();
+    if (hn < 3 || hn > kMaxV) return false;
+    // security: every circumradius R ≤ δ/2 (c ∝ Voronoi vertex: tan² R = Q / (c·p)²)
+    const double c2 = cos(0.5 * delta) * cos(0.5 * delta), s2 = sin(0.5 * delta) * sin(0.5 * delta);
+    bool ok = true;
+    double tmax = 0.0;
+    if (lane < hn) {
+      const int ga = ix[hs[lane]], gb = ix[hs[lane + 1 == hn ? 0 : lane + 1]];
+      const double ax = dirs[3 * (size_t)ga] - px, ay = dirs[3 * (size_t)ga + 1] - py, az = dirs[3 * (size_t)ga + 2] - pz;
+      const double bx = dirs[3 * (size_t)gb] - px, by = dirs[3 * (size_t)gb + 1] - py, bz = dirs[3 * (size_t)gb + 2] - pz;
+      const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+      const double cp = cx * px + cy * py + cz * pz;
+      const double xx = cy * pz - cz * py, xy = cz * px - cx * pz, xz = cx * py - cy * px;
+      const double Q = xx * xx + xy * xy + xz * xz;
+      const double tol = 1e-6 * (fabs(cx) + fabs(cy) + fabs(cz));
+      ok = cp > tol && (cp - tol) * (cp - tol) * s2 >= c2 * Q;
+      tmax = cp > tol ? Q / (cp * cp) : INFINITY;
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    if (all_ok) {
+      if (lane == 0) {
+        const size_t base = (size_t)rec * n + i;
+        int c = 0;
+        for (int t = 0; t < hn; ++t) {
+          const int ga = ix[hs[t]], gn = ix[hs[t + 1 == hn ? 0 : t + 1]];
+          if (i < ga && i < gn) {
+            own[(base * kMaxV + c) * 2 + 0] = ga;
+            own[(base * kMaxV + c) * 2 + 1] = gn;
+            ++c;
+          }
+        }
+        W.deg[base] = hn;
+        own_cnt[base] = c;
+      }
+      __syncwarp();
+      return true;
+    }
+    if (!(tmax < INFINITY)) return false;
+    delta = fmax(delta * 1.2, 2.05 * atan(sqrt(tmax)));
+    if (delta > 1.5) return false;
+    __syncwarp();
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kWarpBS) k_delaunay_warp(BuildParams P, Wave W, int* own, int* own_cnt) {
+  extern __shared__ unsigned char wsm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* us = (double2*)wsm + wid * kWarpK;
+  int* ix = (int*)((double2*)wsm + (kWarpBS / 32) * kWarpK) + wid * kWarpK;
+  int* hs = (int*)((double2*)wsm + (kWarpBS / 32) * kWarpK) + (kWarpBS / 32) * kWarpK + wid * kHullH;
   const int n = P.n_angular;
   const unsigned cnt = *W.del_fb_count;
-  const unsigned tot = (cnt + 31u) & ~31u;  // warp-uniform trip count for the ballot
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
-    bool fb = false;
-    int cell = 0;
-    if (t < cnt) {
-      cell = W.del_fb[t];
-      const int rec = cell / n, i = cell - rec * n;
-      const int r0 = i / P.cols;
-      if (P.del_cap && (r0 == 0 || r0 == P.rows - 1)) {
-        fb = true;  // the clipping kernel takes the polar cells the cap kernel left
-      } else {
-        fb = !hull_cell<double, kHull64BS>(P, W, rec, i, dsm2 + threadIdx.x, hs, own, own_cnt);
-      }
+  for (unsigned t = blockIdx.x * (kWarpBS / 32) + wid; t < cnt; t += gridDim.x * (kWarpBS / 32)) {
+    const int cell = W.del_fb[t];
+    const int rec = cell / n, i = cell - rec * n;
+    if (!warp_cell(P, W, rec, i, us, ix, hs, own, own_cnt) && lane == 0) {
+      const unsigned slot = atomicAdd(W.del_fb2_count, 1u);
+      W.del_fb2[slot] = cell;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, fb);
-    if (m) {
-      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-      unsigned slot = 0;
-      if (lane == leader) slot = atomicAdd(W.del_fb2_count, (unsigned)__popc(m));
-      slot = __shfl_sync(0xffffffffu, slot, leader);
-      if (fb) W.del_fb2[slot + __popc(m & ((1u << lane) - 1u))] = cell;
-    }
+    __syncwarp();
   }
 }
 
@@ -1851,8 +1999,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         cudaFuncSetAttribute(k_delaunay_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kHullBS * (kHullSlots * sizeof(float2) + kHullH)));
         cudaFuncSetAttribute(k_delaunay_cap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
-        cudaFuncSetAttribute(k_delaunay_hull64, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kHull64BS * (kHullSlots * sizeof(double2) + kHullH)));
+        cudaFuncSetAttribute(k_delaunay_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWarpSmem);
         smem_attr = true;
       }
       prof_begin(KC_DELAUNAY, st);
@@ -1890,9 +2037,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
             fprintf(stderr, "\n");
           }
           if (getenv("VOLCACHE_DEL_STATS")[0] >= '2') {
-            k_delaunay_hull64<<<sm_count * 3, kHull64BS,
-                                (size_t)kHull64BS * (kHullSlots * sizeof(double2) + kHullH), st>>>(P, W, own,
-                                                                                                          own_cnt);
+            k_delaunay_warp<<<sm_count * 4, kWarpBS, kWarpSmem, st>>>(P, W, own, own_cnt);
             cudaMemcpyAsync(&c, W.del_fb2_count, 4, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             fprintf(stderr, "[volcache] after the float64 wrap: %u\n", c);
@@ -1904,8 +2049,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
           }
         }
         cudaMemsetAsync(W.del_fb2_count, 0, sizeof(unsigned int), st);
-        k_delaunay_hull64<<<sm_count * 3, kHull64BS, (size_t)kHull64BS * (kHullSlots * sizeof(double2) + kHullH),
-                            st>>>(P, W, own, own_cnt);
+        k_delaunay_warp<<<sm_count * 4, kWarpBS, kWarpSmem, st>>>(P, W, own, own_cnt);
         k_delaunay_list<<<sm_count * VC_LB_DEL2, kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
         nl += 2;
       } else {

@@ -109,6 +109,7 @@ struct BuildParams {
   int del_cap;       // 1: the polar rows go to the cap kernel
   float del_cap_cos, del_cap_sin;  // cos δ, sin δ: the cap kernel's candidate radius
   double del_cap_c2, del_cap_s2;  // cos²(δ/2), sin²(δ/2)
+  double del_warp_delta;          // first candidate radius of the one-warp fallback
 };
 
 // Per-direction data read by the assembly scan, one 16-byte load per vertex.
