@@ -31,6 +31,8 @@ def to_bytes(v, unit):
 # kernel → bench.py kernel class (vc_profile classes)
 CLASS = {"primary": "primary", "rings": "rings", "wave_scan": "wave_scan", "gather": "gather",
          "gather_emit": "gather", "gather_occl": "gather", "delaunay_smem": "delaunay", "delaunay_retry": "delaunay",
+         "delaunay_hull": "delaunay", "delaunay_cap": "delaunay", "delaunay_warp": "delaunay", "delaunay_list": "delaunay",
+         "delaunay_rest": "delaunay", "assemble_t": "assemble", "asm_eval": "assemble",
          "tri_compact": "tri_compact", "degree": "degree", "live_masks": "assemble", "assemble": "assemble",
          "asm_final": "assemble", "make_record": "make_record", "seedseq": "seedseq"}
 
@@ -52,7 +54,7 @@ def main():
         rb = to_bytes(row[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
         wb = to_bytes(row[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
         key = short.replace("vc::", "").replace("k_", "").split("<")[0]
-        traffic[key] = rb + wb
+        traffic[key] = traffic.get(key, 0.0) + rb + wb  # summed over launches (window classes)
         st = []
         for h, i in col.items():
             if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
