@@ -17,8 +17,10 @@ for r in rows[rows.index(hdr) + 1:]:
         continue
     if r[0]:  # CUDA line row
         cur = (r[0], r[1])
-        try:
-            lines[cur] = [float(r[si] or 0), float(r[ie] or 0)]
+        try:  # summed over the matching launches (window classes, repeated waves)
+            v = lines.setdefault(cur, [0.0, 0.0])
+            v[0] += float(r[si] or 0)
+            v[1] += float(r[ie] or 0)
         except ValueError:
             pass
 tot = sum(v[0] for v in lines.values()) or 1
