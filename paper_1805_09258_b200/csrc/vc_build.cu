@@ -1419,6 +1419,7 @@ __device__ __forceinline__ void elem_vertices(const Wave& W, const BuildParams& 
 template <int D>
 struct AsmCtx {
   const double* dirs;
+  const DirInfo* info;   // s and live-ring count of a direction in one 16-byte load
   const double* sv;
   const int* cnt;
   const int* pre;
@@ -1433,6 +1434,7 @@ __device__ __forceinline__ AsmCtx<D> asm_ctx(const BuildParams& P, const Wave& W
   const size_t rb = (size_t)rec * P.n_angular;
   AsmCtx<D> c;
   c.dirs = W.dirs + rb * D;
+  c.info = W.info + rb;
   c.sv = W.s + rb;
   c.cnt = W.cnt + rb;
   c.pre = W.pre + rb;
@@ -1455,8 +1457,9 @@ __device__ __forceinline__ bool asm_item(const DevScene& S, const AsmCtx<D>& C, 
   const double ri = (kind == 1) ? ring_radius(ring, C.step) : 0.0;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    const bool live = (kind == 1) && (ring < C.cnt[v[j]]);
-    dist[j] = live ? ri : C.sv[v[j]];
+    const DirInfo di = C.info[v[j]];
+    const bool live = (kind == 1) && (ring < di.cnt);
+    dist[j] = live ? ri : di.s;
 #pragma unroll
     for (int a = 0; a < D; ++a) rv[j][a] = dist[j] * C.dirs[(size_t)v[j] * D + a];
   }

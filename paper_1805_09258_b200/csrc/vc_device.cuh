@@ -566,7 +566,8 @@ __device__ inline bool ff_triangle(const double* r1v, const double* r2v, const d
   double B = r[0] * r[1] * r[2] + d12 * r[2] + d23 * r[0] + d13 * r[1];
   double aA = fabs(A);
   if (!(aA >= 1e-12 * r[0] * r[1] * r[2])) return false;
-  F = 2.0 * atan2(aA, B) / (4.0 * kPi);
+  const double k2pi = 1.0 / (2.0 * kPi);
+  F = atan2(aA, B) * k2pi;  // 2·atan2 / 4π
   // Closed forms of the reference's term-by-term chain (src/formfactor.py:199-251) with
   // unit vectors n_i = R_i/r_i, σ₂ = r₀r₁ + r₀r₂ + r₁r₂, ρ = r₀ + r₁ + r₂, m = Σn_i,
   // d = (d23, d13, d12):  ∇B = −Σ (σ₂ + d_i) n_i
@@ -592,16 +593,17 @@ __device__ inline bool ff_triangle(const double* r1v, const double* r2v, const d
     gB[c] = -((s2 + dk[0]) * n[0][c] + (s2 + dk[1]) * n[1][c] + (s2 + dk[2]) * n[2][c]);
     m[c] = n[0][c] + n[1][c] + n[2][c];
   }
-  const double den = A * A + B * B;
-  const double k2pi = 1.0 / (2.0 * kPi);
+  // one reciprocal of den = A² + B² for the gradient and Hessian (results within a few ulp
+  // of the reference's divisions)
+  const double iden = 1.0 / (A * A + B * B);
   double num[3], gD[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     num[c] = B * gU[c] - aA * gB[c];
     gD[c] = 2.0 * aA * gU[c] + 2.0 * B * gB[c];
-    g[c] = num[c] / den * k2pi;
+    g[c] = num[c] * iden * k2pi;
   }
-  const double ia = -aA / den, id2 = -0.5 / (den * den);
+  const double ia = -aA * iden, id2 = -0.5 * iden * iden;
   int e = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -657,9 +659,11 @@ __device__ inline void element_q(const double* w, double dr, double sigma_t, dou
                                  const double* HF, double* q /* 1 + D + D(D+1)/2 */) {
   constexpr int NH = D * (D + 1) / 2;
   double T = exp(-sigma_t * dr);
+  // one reciprocal of dr for ∇T and HT (within a few ulp of the reference's divisions)
+  const double idr = 1.0 / dr, idr2 = idr * idr;
   double gT[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) gT[a] = (-sigma_t * w[a]) / dr * T;
+  for (int a = 0; a < D; ++a) gT[a] = (-sigma_t * w[a]) * idr * T;
   q[0] = T * F;
 #pragma unroll
   for (int a = 0; a < D; ++a) q[1 + a] = T * gF[a] + gT[a] * F;
@@ -670,7 +674,7 @@ __device__ inline void element_q(const double* w, double dr, double sigma_t, dou
     for (int b = a; b < D; ++b) {
       double ww = w[a] * w[b];
       double I = (a == b) ? 1.0 : 0.0;
-      double HT = -sigma_t * (I / dr - ww / (dr * dr * dr) - sigma_t * ww / (dr * dr)) * T;
+      double HT = -sigma_t * (I * idr - ww * idr2 * idr - sigma_t * ww * idr2) * T;
       q[1 + D + e] = T * HF[e] + gT[a] * gF[b] + gF[a] * gT[b] + HT * F;
       ++e;
     }
