@@ -911,13 +911,31 @@ __device__ __forceinline__ int gift_wrap(typename Vec2<T>::V* us, int K, int sta
       mn = fmin(mn, fabs(cr));
       if (cr < (T)0) { best = c; bx = cx; by = cy; }
     }
-    us[cur * BS] = a;
-    us[b0 * BS] = b;
     // float32 error bound of this step's orientations: each projection carries ≤ 5
     // roundings relative to its norm, so |err(cross)| ≤ 30·2⁻²⁴·(|a| + |b|)(|a| + |c|)
     // ≤ 32·2⁻²⁴·(|a|₁ + max|u|₁)²
-    const T la = fabs(a.x) + fabs(a.y) + nmax;
-    if (!(mn > (T)32 * Vec2<T>::kEps * la * la)) return 0;
+    const T na = fabs(a.x) + fabs(a.y), la = na + nmax;
+    if (!(mn > (T)32 * Vec2<T>::kEps * la * la)) {
+      // rare: the step's tests again, each against its own bound 32·2⁻²⁴·(|a|₁+|b|₁)(|a|₁+|c|₁)
+      // (every test outside its bound decides exactly, so both scans agree)
+      T vx = b.x - a.x, vy = b.y - a.y, nb = fabs(b.x) + fabs(b.y);
+      bool bad = false;
+      for (int c = 0; c < K; ++c) {
+        const V u = us[c * BS];
+        const T cx = u.x - a.x, cy = u.y - a.y;
+        const T cr = vx * cy - vy * cx;
+        const T nc = fabs(u.x) + fabs(u.y);
+        bad |= fabs(cr) <= (T)32 * Vec2<T>::kEps * (na + nb) * (na + nc);
+        if (cr < (T)0) { vx = cx; vy = cy; nb = nc; }
+      }
+      if (bad) {
+        us[cur * BS] = a;
+        us[b0 * BS] = b;
+        return 0;
+      }
+    }
+    us[cur * BS] = a;
+    us[b0 * BS] = b;
     if (best == start) break;
     if (hn == kHullH) return 0;
     cur = best;
