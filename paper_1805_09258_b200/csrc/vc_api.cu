@@ -301,6 +301,7 @@ static void del_row_table(BuildParams& P) {
   P.del_cap_c2 = std::cos(0.5 * delta) * std::cos(0.5 * delta);
   P.del_cap_s2 = std::sin(0.5 * delta) * std::sin(0.5 * delta);
   P.del_warp_delta = 3.2 * std::sqrt(4.0 * pi / P.n_angular);
+  P.del_dbg_cell = getenv("VOLCACHE_DEL_DEBUG_CELL") ? atoi(getenv("VOLCACHE_DEL_DEBUG_CELL")) : -1;
 }
 
 int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int32_t* adjacency,

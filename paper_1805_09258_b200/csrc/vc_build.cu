@@ -1197,10 +1197,11 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W,
 // the stratum rows and columns that can hold them, ballot-compacted into the warp's
 // shared memory); each gift-wrap step is a warp reduction under the orientation order
 // (from a hull vertex every other projection lies in a half-plane, so "more clockwise" is
-// a strict order); the star is kept when every circumradius R ≤ δ/2, else δ grows to
-// 2.05·max R and the cell is redone (at most 3 radii, ≤ kWarpK candidates).  Cells still
+// a strict order); the star is kept when every circumradius R ≤ δ/2, else δ grows towards
+// 2.05·max R (by 1.2× to 1.6×) and the cell is redone (at most 5 radii, ≤ kWarpK
+// candidates).  Cells still
 // open go to the clipping kernel (second list).
-constexpr int kWarpK = 192;
+constexpr int kWarpK = 320;
 constexpr int kWarpBS = 256;
 constexpr size_t kWarpSmem = (size_t)(kWarpBS / 32) * (kWarpK * (sizeof(double2) + 4) + kHullH * 4);
 
@@ -1215,7 +1216,7 @@ __device__ bool warp_cell(const BuildParams& P, const Wave& W, int rec, int i, d
   const float4 p32 = d32[i];
   const double st = sqrt(fmax(0.0, 1.0 - pz * pz));
   double delta = P.del_warp_delta;
-  for (int attempt = 0; attempt < 3; ++attempt) {
+  for (int attempt = 0; attempt < 5; ++attempt) {
     const double cd = cos(delta), sd = sin(delta);
     const float cutf = (float)cd - 1e-6f;
     // stratum rows meeting z ∈ [cos(θ + δ), cos(θ − δ)], columns within asin(sin δ / sin θ)
@@ -1251,7 +1252,10 @@ __device__ bool warp_cell(const BuildParams& P, const Wave& W, int rec, int i, d
       }
       K += __popc(m);
     }
-    if (K > kWarpK || K < 3) return false;
+    if (K > kWarpK || K < 3) {
+      if (P.del_dbg_cell == rec * n + i && lane == 0) printf("warp_cell: K=%d delta=%g\n", K, delta);
+      return false;
+    }
     __syncwarp();
     // start: the largest projection (nearest direction), a hull vertex; L1 bound N
     double best_r = -1.0, nmax = 0.0;
@@ -1303,13 +1307,22 @@ __device__ bool warp_cell(const BuildParams& P, const Wave& W, int rec, int i, d
           }
         }
       }
-      if (__any_sync(0xffffffffu, bad)) return false;
+      if (__any_sync(0xffffffffu, bad)) {
+        if (P.del_dbg_cell == rec * n + i && lane == 0) printf("warp_cell: flagged step %d K=%d\n", hn, K);
+        return false;
+      }
       if (b == start) break;
-      if (hn == kHullH) return false;
+      if (hn == kHullH) {
+        if (P.del_dbg_cell == rec * n + i && lane == 0) printf("warp_cell: hull overflow K=%d\n", K);
+        return false;
+      }
       cur = b;
     }
     __syncwarp();
-    if (hn < 3 || hn > kMaxV) return false;
+    if (hn < 3 || hn > kMaxV) {
+      if (P.del_dbg_cell == rec * n + i && lane == 0) printf("warp_cell: hn=%d\n", hn);
+      return false;
+    }
     // security: every circumradius R ≤ δ/2 (c ∝ Voronoi vertex: tan² R = Q / (c·p)²)
     const double c2 = cos(0.5 * delta) * cos(0.5 * delta), s2 = sin(0.5 * delta) * sin(0.5 * delta);
     bool ok = true;
@@ -1347,8 +1360,10 @@ __device__ bool warp_cell(const BuildParams& P, const Wave& W, int rec, int i, d
       __syncwarp();
       return true;
     }
+    if ((P.del_dbg_cell == rec * n + i && lane == 0)) printf("warp_cell: insecure delta=%g tmax=%g hn=%d K=%d\n", delta, tmax, hn, K);
     if (!(tmax < INFINITY)) return false;
-    delta = fmax(delta * 1.2, 2.05 * atan(sqrt(tmax)));
+    // a far circumcentre usually means a neighbour beyond δ: grow by at most 1.6×
+    delta = fmin(1.6 * delta, fmax(1.2 * delta, 2.05 * atan(sqrt(tmax))));
     if (delta > 1.5) return false;
     __syncwarp();
   }
@@ -2075,6 +2090,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
             for (int g : l) ++hist[(g % P.n_angular) / P.cols];
             for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
             fprintf(stderr, "\n");
+            for (unsigned t = 0; t < c && t < 8; ++t)
+              fprintf(stderr, "[volcache] clipping cell: record %d direction %d\n", l[t] / P.n_angular, l[t] % P.n_angular);
           }
         }
         cudaMemsetAsync(W.del_fb2_count, 0, sizeof(unsigned int), st);

@@ -110,6 +110,7 @@ struct BuildParams {
   float del_cap_cos, del_cap_sin;  // cos δ, sin δ: the cap kernel's candidate radius
   double del_cap_c2, del_cap_s2;  // cos²(δ/2), sin²(δ/2)
   double del_warp_delta;          // first candidate radius of the one-warp fallback
+  int del_dbg_cell;               // VOLCACHE_DEL_DEBUG_CELL: warp_cell reports why it gives up
 };
 
 // Per-direction data read by the assembly scan, one 16-byte load per vertex.
