@@ -415,8 +415,13 @@ __device__ __forceinline__ void nearest_emitter(const DevScene& S, const double*
           ok = false;
           break;
         }
-        const double tp = (E.c[g] - (E.n[g][0] * o[0] + E.n[g][1] * o[1] + E.n[g][2] * o[2])) / dn;
-        if (tp < -1e-5 * S.scale) continue;
+        // the landing distance only picks the grid cell: a float32 reciprocal (≤ 1e-7
+        // relative) keeps it within 1e-7·scale for the distances that matter (a point of the
+        // scene lies within `scale` of the origin), far inside the cells' 1e-5·scale padding
+        float rdn;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rdn) : "f"((float)dn));
+        const double tp = (E.c[g] - (E.n[g][0] * o[0] + E.n[g][1] * o[1] + E.n[g][2] * o[2])) * (double)rdn;
+        if (tp < -1e-5 * S.scale || tp > 1.01 * S.scale) continue;
         const double X[3] = {o[0] + tp * d[0], o[1] + tp * d[1], o[2] + tp * d[2]};
         const double px = E.a1[g][0] * X[0] + E.a1[g][1] * X[1] + E.a1[g][2] * X[2];
         const double py = E.a2[g][0] * X[0] + E.a2[g][1] * X[1] + E.a2[g][2] * X[2];
