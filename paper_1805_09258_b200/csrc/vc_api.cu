@@ -566,7 +566,7 @@ int vc_profile_read(double* ms, int64_t* launches, int max_classes) {
 
 // Emitter plane grids (3D): triangles grouped by plane (normals and offsets equal to
 // 1e-9, every vertex within 1e-9·scale of the group plane), at most kEmitPlanes groups;
-// per group a grid of about 4 triangles' worth of area per cell over the triangles'
+// per group a grid of cells 1/16 of the mean triangle box over the triangles'
 // in-plane boxes, each padded by 1e-5·scale — far beyond the distance (≤ 1e-6·scale for
 // rays at ≥ 1e-3 of grazing) between the plane point a ray lands on and the point of a
 // triangle the float64 hit test accepts.  Returns false when the emitters need more planes.
@@ -624,6 +624,13 @@ static bool build_emit_planes(const std::vector<double>& prim, const std::vector
     grp[k] = g;
   }
   ep->ng = ng;
+  ep->axis_only = 1;
+  for (int g = 0; g < ng; ++g) {
+    ep->axis[g] = -1;
+    for (int a = 0; a < 3; ++a)
+      if (std::fabs(ep->n[g][a]) == 1.0 && ep->n[g][(a + 1) % 3] == 0.0 && ep->n[g][(a + 2) % 3] == 0.0) ep->axis[g] = a;
+    if (ep->axis[g] < 0) ep->axis_only = 0;
+  }
   const double pad = 1e-5 * scale;
   std::vector<double> box((size_t)K * 4);  // in-plane (x0, y0, x1, y1), padded
   for (int k = 0; k < K; ++k) {
@@ -656,7 +663,9 @@ static bool build_emit_planes(const std::vector<double>& prim, const std::vector
         area += (box[4 * k + 2] - box[4 * k]) * (box[4 * k + 3] - box[4 * k + 1]);
         ++cnt;
       }
-    const double cs = std::sqrt(std::max(area / (4.0 * cnt), 1e-30));
+    // cells of ~1/16 of a triangle's box: landings between or beside the emitters meet
+    // empty cells, a landing on one meets about its own pair of triangles
+    const double cs = std::sqrt(std::max(area / (16.0 * cnt), 1e-30));
     const int gx = std::min(128, std::max(1, (int)std::ceil((x1 - x0) / cs)));
     const int gy = std::min(128, std::max(1, (int)std::ceil((y1 - y0) / cs)));
     ep->lo[g][0] = x0; ep->lo[g][1] = y0;

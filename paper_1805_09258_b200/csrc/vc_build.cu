@@ -339,10 +339,64 @@ __device__ __forceinline__ void store_media(float* out, const double* v) {
 constexpr int kQChunk = VC_QCHUNK;  // queue slots a warp reserves with one atomic
 static_assert(kQChunk >= 32, "a step's hits (≤ 32) must fit one fresh chunk");
 
+// Could the gather ray with draws (u0, u1) from y reach an emitter?  False only when
+// every emitter plane is axis-aligned and the ray certainly moves away from each of them
+// (the sign of the direction's axis component follows from u0 or u1 alone:
+// d = (√(1−z²)·cos 2πu1, √(1−z²)·sin 2πu1, 1 − 2u0)); a hit needs the landing distance
+// (c − n·y)/(n·d) above −1e-5·scale, impossible for an origin farther than that from the
+// plane when n·d has the other sign.
+// Per-launch constants of that test (registers; no indexing by plane or axis).
+struct Toward {
+  int ng;                 // 0: every ray may reach an emitter
+  int ax[kEmitPlanes];    // plane axis
+  double nz[kEmitPlanes]; // n_axis (±1)
+  double c[kEmitPlanes];
+  __device__ __forceinline__ explicit Toward(const EmitPlanes& E) {
+    ng = E.axis_only ? E.ng : 0;
+#pragma unroll
+    for (int g = 0; g < kEmitPlanes; ++g) {
+      const int a = g < E.ng ? E.axis[g] : 0;
+      ax[g] = a;
+      nz[g] = g < E.ng ? (a == 0 ? E.n[g][0] : (a == 1 ? E.n[g][1] : E.n[g][2])) : 1.0;
+      c[g] = g < E.ng ? E.c[g] : 0.0;
+    }
+  }
+  __device__ __forceinline__ bool operator()(const double* y, double u0, double u1, double tol) const {
+    if (ng == 0) return true;
+    bool any = false;
+#pragma unroll
+    for (int g = 0; g < kEmitPlanes; ++g) {
+      if (g >= ng) break;
+      const int a = ax[g];
+      const double ya = a == 0 ? y[0] : (a == 1 ? y[1] : y[2]);
+      const double s = c[g] - nz[g] * ya;  // c − n·y with n = ±e_a
+      int sd;                              // sign of d_a (0: zero or not decided)
+      if (a == 2) sd = u0 < 0.5 ? 1 : (u0 > 0.5 ? -1 : 0);
+      else if (u0 == 0.0) sd = 0;
+      else if (a == 0) sd = (u1 < 0.25 || u1 > 0.75) ? 1 : ((u1 > 0.25 && u1 < 0.75) ? -1 : 0);
+      else sd = (u1 > 0.0 && u1 < 0.5) ? 1 : (u1 > 0.5 ? -1 : 0);
+      any |= fabs(s) <= tol || sd == 0 || (nz[g] > 0.0 ? sd : -sd) == (s > 0.0 ? 1 : -1);
+    }
+    return any;
+  }
+};
+
+// Pass 1 of the two-pass gather.  Each lane walks runs of kGatherRun consecutive samples
+// (PCG64 jumped once per run, then stepped); the draws of samples whose ray cannot reach an
+// emitter are consumed and dropped at once, the others are compacted into a per-warp queue
+// in shared memory and evaluated 32 at a time (direction, nearest emitter through the plane
+// grids), so the expensive part runs on full warps.
+struct PendSample {
+  double u0, u1;
+  int j, k, i, pad;
+};
+constexpr int kPendCap = 64;  // per warp: ≤ 31 left over + one step's 32
+
 template <int D>
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
                                                                GatherItem* q, unsigned long long* q_count,
                                                                long long q_cap) {
+  __shared__ PendSample pend_all[256 / 32][kPendCap];
   const int rec = blockIdx.y;
   const long long base = W.rec_base[rec];
   const int Pr = (int)(W.rec_base[rec + 1] - base);
@@ -351,10 +405,13 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
   const int* pre = W.pre + (size_t)rec * n;
   const int* cnt = W.cnt + (size_t)rec * n;
   const int lane = threadIdx.x & 31;
-  double x[3];
+  PendSample* pend = pend_all[threadIdx.x >> 5];
+  double x[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < D; ++c) x[c] = W.x[rec * D + c];
   const uint64_t* st = W.rng + 4 * rec;
+  const double tol = 1e-5 * S.scale;
+  const Toward toward(S.ep);
   // the warp appends emitter hits into queue chunks it reserves kQChunk slots at a time
   // (one atomic per chunk instead of one per step); unused slots are marked empty
   long long cbase = 0;
@@ -363,6 +420,85 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
     for (int t = cused + lane; t < kQChunk; t += 32)
       if (cbase + t < q_cap) q[cbase + t].slot = -1;
   };
+  auto origin = [&](int k, int i, double* y) {
+    const double ri = ring_radius(i, P.march_step);
+#pragma unroll
+    for (int c = 0; c < D; ++c) y[c] = add(x[c], mul(ri, W.dirs[((size_t)rec * n + k) * D + c]));
+  };
+  // evaluate pend[0, m) (lane l takes entry l); every lane takes part in the queue ballot
+  auto evaluate = [&](int m) {
+    const bool active = lane < m;
+    double y[3] = {0.0, 0.0, 0.0}, gd[3] = {0.0, 0.0, 0.0}, te = 0.0;
+    int ie = -1, j = 0, k = 0, i = 0;
+    if (active) {
+      const PendSample ps = pend[lane];
+      j = ps.j;
+      k = ps.k;
+      i = ps.i;
+      origin(k, i, y);
+      if constexpr (D == 2) {
+        double th = mul(2.0 * kPi, ps.u0);
+        gd[0] = cos(th);
+        gd[1] = sin(th);
+      } else {
+        double z = sub(1.0, mul(2.0, ps.u0));
+        double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+        // cos, sin of φ = 2π·u1 (src/transport.py:274-285) without the range reduction of
+        // sincos(φ): equal to the reference's cos(fl(2π·u1)) within an ulp of φ
+        double sp, cp;
+        sincospi(2.0 * ps.u1, &sp, &cp);
+        gd[0] = mul(sq, cp);
+        gd[1] = mul(sq, sp);
+        gd[2] = z;
+      }
+      nearest_emitter<D>(S, y, gd, te, ie);
+      if (ie < 0 && W.dense_media) {  // dead samples are read only by inspection
+        const double zero[3] = {0.0, 0.0, 0.0};
+        store_media(W.media + (size_t)(base + j) * 3, zero);
+      }
+    }
+    const bool hit = active && ie >= 0;
+    const unsigned hits = __ballot_sync(0xffffffffu, hit);
+    if (hits) {
+      const int nh = __popc(hits);
+      if (cused + nh > kQChunk) {  // new chunk
+        seal();
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(q_count, (unsigned long long)kQChunk);
+        cbase = (long long)__shfl_sync(0xffffffffu, nb, 0);
+        cused = 0;
+      }
+      if (hit) {
+        const long long slot = cbase + cused + __popc(hits & ((1u << lane) - 1u));
+        if (slot < q_cap) {
+          GatherItem& it = q[slot];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            it.y[c] = c < D ? y[c] : 0.0;
+            it.d[c] = c < D ? gd[c] : 0.0;
+          }
+          it.te = te;
+          it.ie = ie;
+          it.slot = base + j;
+          it.rec = rec;
+          it.k = k;
+          it.ring = i;
+        } else {  // queue full: resolve in place (same result, less coherent)
+          double v[3] = {0.0, 0.0, 0.0};
+          if (!occluded<D>(S, y, gd, te, ie)) {
+            const double* E = S.emission + (size_t)ie * 3;
+            double T = exp(-S.sigma_t * te);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
+          }
+          store_media(W.media + (size_t)(base + j) * 3, v);
+          if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, rec, k, i);
+        }
+      }
+      cused += nh;
+    }
+  };
+  int qn = 0;  // warp-uniform queue length
   const int stride = gridDim.x * blockDim.x * kGatherRun;
   // warp-uniform loop: lane runs [j0, j0 + kGatherRun) of the record's samples
   for (int j0w = (blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * kGatherRun; j0w < Pr; j0w += stride) {
@@ -379,80 +515,44 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
     for (int step = 0; step < kGatherRun; ++step) {
       const int j = j0 + step;
       const bool active = j < Pr;
-      double y[3], gd[3], te = 0.0;
-      int ie = -1;
+      bool keep = false;
+      double u0 = 0.0, u1 = 0.0;
       if (active) {
         while (i >= cnt[k]) {  // next direction with live rings
           ++k;
           i = 0;
         }
-        const double ri = ring_radius(i, P.march_step);
-#pragma unroll
-        for (int c = 0; c < D; ++c) y[c] = add(x[c], mul(ri, W.dirs[((size_t)rec * n + k) * D + c]));
-        if constexpr (D == 2) {
-          double th = mul(2.0 * kPi, g.next_double());
-          gd[0] = cos(th);
-          gd[1] = sin(th);
+        u0 = g.next_double();
+        if constexpr (D == 3) {
+          u1 = g.next_double();
+          double y[3];
+          origin(k, i, y);
+          keep = toward(y, u0, u1, tol);
+          if (!keep && W.dense_media) {
+            const double zero[3] = {0.0, 0.0, 0.0};
+            store_media(W.media + (size_t)(base + j) * 3, zero);
+          }
         } else {
-          double u0 = g.next_double(), u1 = g.next_double();
-          double z = sub(1.0, mul(2.0, u0));
-          double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
-          // cos, sin of φ = 2π·u1 (src/transport.py:274-285) without the range reduction of
-          // sincos(φ): equal to the reference's cos(fl(2π·u1)) within an ulp of φ
-          double sp, cp;
-          sincospi(2.0 * u1, &sp, &cp);
-          gd[0] = mul(sq, cp);
-          gd[1] = mul(sq, sp);
-          gd[2] = z;
-        }
-        nearest_emitter<D>(S, y, gd, te, ie);
-        if (ie < 0 && W.dense_media) {  // dead samples are read only by inspection
-          const double zero[3] = {0.0, 0.0, 0.0};
-          store_media(W.media + (size_t)(base + j) * 3, zero);
+          keep = true;
         }
       }
-      const bool hit = active && ie >= 0;
-      const unsigned hits = __ballot_sync(0xffffffffu, hit);
-      if (hits) {
-        const int nh = __popc(hits);
-        if (cused + nh > kQChunk) {  // new chunk
-          seal();
-          unsigned long long nb = 0;
-          if (lane == 0) nb = atomicAdd(q_count, (unsigned long long)kQChunk);
-          cbase = (long long)__shfl_sync(0xffffffffu, nb, 0);
-          cused = 0;
-        }
-        if (hit) {
-          const long long slot = cbase + cused + __popc(hits & ((1u << lane) - 1u));
-          if (slot < q_cap) {
-            GatherItem& it = q[slot];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              it.y[c] = c < D ? y[c] : 0.0;
-              it.d[c] = c < D ? gd[c] : 0.0;
-            }
-            it.te = te;
-            it.ie = ie;
-            it.slot = base + j;
-            it.rec = rec;
-            it.k = k;
-            it.ring = i;
-          } else {  // queue full: resolve in place (same result, less coherent)
-            double v[3] = {0.0, 0.0, 0.0};
-            if (!occluded<D>(S, y, gd, te, ie)) {
-              const double* E = S.emission + (size_t)ie * 3;
-              double T = exp(-S.sigma_t * te);
-#pragma unroll
-              for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
-            }
-            store_media(W.media + (size_t)(base + j) * 3, v);
-            if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, rec, k, i);
-          }
-        }
-        cused += nh;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) pend[qn + __popc(m & ((1u << lane) - 1u))] = PendSample{u0, u1, j, k, i, 0};
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        evaluate(32);
+        __syncwarp();
+        if (lane < qn - 32) pend[lane] = pend[32 + lane];
+        __syncwarp();
+        qn -= 32;
       }
       if (active) ++i;
     }
+  }
+  if (qn > 0) {
+    __syncwarp();
+    evaluate(qn);
   }
   seal();
 }

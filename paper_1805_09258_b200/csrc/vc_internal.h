@@ -46,6 +46,8 @@ struct EmitPlanes {
   double a1[kEmitPlanes][3], a2[kEmitPlanes][3];     // in-plane frame about c·n
   double lo[kEmitPlanes][2], inv[kEmitPlanes][2];    // grid origin and 1 / cell size
   int gx[kEmitPlanes], gy[kEmitPlanes], cell0[kEmitPlanes];
+  int axis[kEmitPlanes];         // n = ±e_axis exactly (−1: not axis-aligned)
+  int axis_only;                 // every plane axis-aligned (the gather's draw-only test)
   const int* cell_start;         // CSR over every plane's cells
   const int* cell_tri;           // leaf-order indices into the emitter set
 };
