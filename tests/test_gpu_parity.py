@@ -401,6 +401,31 @@ def test_gather_queue_overflow_same_result():
     np.testing.assert_array_equal(np.load(out / "q_full.npy"), np.load(out / "q_tiny.npy"))
 
 
+def test_emitter_plane_grids_same_result():
+    """Gather through the emitter plane grids (and the ray-away test on the draws) is
+    bit-identical to the emitter BVH (VOLCACHE_EMIT_PLANES=0): same media radiance, same
+    moments, on records of the window room at the metric's 16k directions."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1805_09258_b200 import configs, estimate_moments_batch, seed_words;"
+        "w = configs.cfg3(); X = w.points[:24];"
+        "r = estimate_moments_batch(w.scene, X, seeds=seed_words(w.seed, 401, range(24)), n_angular=16384,"
+        " march_step=w.march_step);"
+        "np.save(sys.argv[1], np.concatenate([r.moments.reshape(-1), r.stats.reshape(-1).astype(float)]))"
+    )
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    env = dict(os.environ)
+    env.pop("VOLCACHE_EMIT_PLANES", None)
+    subprocess.run([sys.executable, "-c", code, str(out / "ep_grid.npy")], check=True, cwd=ROOT, env=env)
+    env["VOLCACHE_EMIT_PLANES"] = "0"
+    subprocess.run([sys.executable, "-c", code, str(out / "ep_bvh.npy")], check=True, cwd=ROOT, env=env)
+    np.testing.assert_array_equal(np.load(out / "ep_grid.npy"), np.load(out / "ep_bvh.npy"))
+
+
 def test_assembly_item_lists_match_fused():
     """Two-kernel assembly (scan → per-warp item lists → evaluation), the fused kernel
     (VOLCACHE_ASM_ITEM_CAP=0) and a mix (tiny lists overflow → fused fallback per record)
