@@ -67,3 +67,73 @@ def build_records_sharded(scene, X, cfg_seed: int, *, builder=None, group=None, 
     else:
         local = builder(scene, np.asarray(X)[lo:hi], seeds)
     return all_gather_rows(local, group=group), (lo, hi)
+
+
+def broadcast_cache_set(cache_set, src: int = 0, group=None):
+    """Make every rank's CacheSet hold `src`'s records, in `src`'s insertion order.
+
+    Used after a populate on one rank (the reference's sequential insertion order is
+    what the lookup sums follow) before a sharded frozen render.  Records travel as
+    packed float64 rows (position, value, grad, axes, radii): counts first, then rows.
+    """
+    import torch
+    import torch.distributed as dist
+
+    dev = _coll_device(group)
+    for cache in (cache_set.single, cache_set.multiple):
+        rows = cache.packed() if dist.get_rank(group) == src else None
+        n = torch.tensor([0 if rows is None else rows.shape[0]], dtype=torch.int64, device=dev)
+        dist.broadcast(n, src, group=group)
+        from .records import record_size
+
+        buf = torch.zeros((int(n.item()), record_size(cache.dim)), dtype=torch.float64, device=dev)
+        if rows is not None:
+            buf.copy_(torch.from_numpy(rows))
+        if buf.numel():
+            dist.broadcast(buf, src, group=group)
+        if dist.get_rank(group) != src:
+            cache._records = []
+            cache._invalidate()
+            cache.extend_packed(buf.cpu().numpy())
+    return cache_set
+
+
+def render_sharded(scene, camera, settings, cache_set, *, renderer=None, group=None):
+    """Frozen-cache camera render with image rows sharded over ranks.
+
+    Every rank holds the same cache set (e.g. via `broadcast_cache_set`); rank r marches
+    rows shard_range(height, r, world), and the row slabs are all-gathered into the full
+    image (height × width × 3 float64) on every rank.  Per-pixel RNG streams depend only
+    on the global pixel index (seeds (seed, 211, k, i, m), src/renderer.py:471), so the
+    image equals the single-process render whatever the sharding.  Returns (image, stats)
+    with cache_hits / direct_evaluations summed over ranks.
+    `renderer(scene, camera, settings, cache_set, row0, rows) -> (slab, stats)` defaults to
+    the device march (`renderer.render_rows`); tests substitute a CPU stand-in.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import renderer as R
+
+    if not settings.frozen and settings.mode != "path":
+        raise ValueError("render_sharded requires frozen=True (insertion order is sequential)")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    lo, hi = shard_range(int(camera.height), rank, world)
+    fn = renderer if renderer is not None else R.render_rows
+    slab, st = fn(scene, camera, settings, cache_set, lo, hi - lo)
+    dev = _coll_device(group)
+    full = all_gather_rows(torch.as_tensor(np.ascontiguousarray(slab), dtype=torch.float64).to(dev), group=group)
+    cnt = torch.tensor([st["cache_hits"], st["direct_evaluations"]], dtype=torch.int64, device=dev)
+    dist.all_reduce(cnt, group=group)
+    image = full.cpu().numpy().reshape(int(camera.height), int(camera.width), 3)
+    return image, {"cache_hits": int(cnt[0]), "direct_evaluations": int(cnt[1]), "rows": (lo, hi)}
+
+
+def _coll_device(group=None):
+    """Tensors for a collective live on the current GPU under NCCL, on the CPU under gloo."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")

@@ -301,6 +301,56 @@ def populate_cache(scene, target, settings: RenderSettings, *, window: int = 0, 
     return cs, stats
 
 
+def _render_params(scene, settings: RenderSettings) -> "_lib.RenderParams":
+    rp = _lib.RenderParams()
+    rp.spp = int(settings.spp)
+    rp.march_step = float(settings.march_step)
+    rp.seed = int(settings.seed) & 0xFFFFFFFF
+    rp.n_angular = _n_angular(scene, settings)
+    rp.n_inner = int(settings.n_inner)
+    rp.n_light_samples = int(settings.n_light_samples)
+    rp.epsilon = float(settings.epsilon)
+    rp.estimator = _estimator(settings.mode)
+    rp.max_media_bounces = int(settings.max_media_bounces)
+    rp.path_samples = int(settings.path_samples_per_point)
+    rp.grow = 0 if settings.frozen else 1
+    rp.isotropic = 1 if settings.mode == "ours-iso" else 0
+    rp.baseline_alpha = float(settings.baseline_alpha)
+    return rp
+
+
+def render_rows(scene, camera: Camera, settings: RenderSettings, cache_set: CacheSet, row0: int, rows: int):
+    """Frozen camera render of image rows [row0, row0 + rows) → (slab (rows, width, 3), stats).
+
+    The rows equal the same rows of `render(scene, camera, settings, cache_set)`: every
+    pixel's streams depend on its global index (src/renderer.py:440-484).  The unit of the
+    row-sharded multi-GPU render (`dist.render_sharded`).
+    """
+    _check_target(scene, camera)
+    if not isinstance(camera, Camera):
+        raise TypeError("render_rows takes a Camera target")
+    if settings.mode not in DEVICE_MODES + ("path",):
+        raise _unsupported(settings.mode)
+    if settings.mode == "path":  # every point path-traced, as render() (src/renderer.py:337-346)
+        settings = RenderSettings(**{**settings.__dict__, "frozen": True})
+    if not settings.frozen:
+        raise ValueError("render_rows requires frozen=True")
+    if not 0 <= row0 <= row0 + rows <= camera.height:
+        raise ValueError("row range outside the image")
+    if settings.mode == "path":
+        cache_set = CacheSet(scene, "ours-aniso")
+    image = np.zeros((camera.height, camera.width, 3))
+    out = np.zeros(2, np.int64)
+    if rows > 0:
+        cam = camera._c()
+        cam.row0, cam.rows, cam.col0, cam.cols = int(row0), int(rows), 0, int(camera.width)
+        rp = _render_params(scene, settings)
+        hs, hm = cache_set._handles()
+        _lib.check(_lib.lib().vc_render(device_scene(scene).handle, hs, hm, _lib.C.byref(cam), _lib.C.byref(rp),
+                                        _lib.ptr(image), _lib.ptr(out), _lib.VC_MEM_HOST, None))
+    return image[row0:row0 + rows].copy(), {"cache_hits": int(out[0]), "direct_evaluations": int(out[1])}
+
+
 def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
     """Render the target; returns (image, stats) (src/renderer.py:402-422).
 
@@ -334,20 +384,7 @@ def render(scene, target, settings: RenderSettings, cache_set: CacheSet = None):
             cache_set.multiple._device_changed()
     else:
         cam = target._c()
-        rp = _lib.RenderParams()
-        rp.spp = int(settings.spp)
-        rp.march_step = float(settings.march_step)
-        rp.seed = int(settings.seed) & 0xFFFFFFFF
-        rp.n_angular = _n_angular(scene, settings)
-        rp.n_inner = int(settings.n_inner)
-        rp.n_light_samples = int(settings.n_light_samples)
-        rp.epsilon = float(settings.epsilon)
-        rp.estimator = _estimator(settings.mode)
-        rp.max_media_bounces = int(settings.max_media_bounces)
-        rp.path_samples = int(settings.path_samples_per_point)
-        rp.grow = 0 if settings.frozen else 1
-        rp.isotropic = 1 if settings.mode == "ours-iso" else 0
-        rp.baseline_alpha = float(settings.baseline_alpha)
+        rp = _render_params(scene, settings)
         image = np.zeros((target.height, target.width, 3))
         hs, hm = cache_set._handles()
         _lib.check(_lib.lib().vc_render(ds.handle, hs, hm, _lib.C.byref(cam), _lib.C.byref(rp), _lib.ptr(image),

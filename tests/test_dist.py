@@ -73,3 +73,64 @@ def test_shard_range_partitions():
             assert all(r[k][1] == r[k + 1][0] for k in range(w - 1))
             sizes = [b - a for a, b in r]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _render_worker(rank, world, port, H, W, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from types import SimpleNamespace
+
+    from paper_1805_09258_b200.dist import broadcast_cache_set, render_sharded
+    from paper_1805_09258_b200.records import record_size
+    from paper_1805_09258_b200.cache import RadianceCache
+
+    bmin, bmax = np.zeros(3), np.ones(3)
+    cs = SimpleNamespace(single=RadianceCache(bmin, bmax), multiple=RadianceCache(bmin, bmax))
+    if rank == 0:  # only rank 0 populated; the others start empty
+        rows = np.random.default_rng(5).uniform(0.1, 0.9, (7, record_size(3)))
+        cs.single.extend_packed(rows)
+        cs.multiple.extend_packed(rows[:3] * 2)
+    broadcast_cache_set(cs)
+    camera = SimpleNamespace(height=H, width=W)
+    settings = SimpleNamespace(frozen=True, mode="ours-aniso")
+
+    def fake_rows(scene, cam, st, cache_set, row0, rows):
+        """CPU stand-in for the device march: a function of the global pixel and the records."""
+        r = np.arange(row0, row0 + rows)[:, None, None]
+        c = np.arange(cam.width)[None, :, None]
+        k = cache_set.single.packed().sum() + 10 * cache_set.multiple.packed().sum()
+        slab = (r * 1000 + c) + np.arange(3)[None, None, :] * 0.25 + k
+        return slab, {"cache_hits": rows * cam.width, "direct_evaluations": rows}
+
+    img, st = render_sharded(None, camera, settings, cs, renderer=fake_rows)
+    q.put((rank, img, st, cs.single.packed(), cs.multiple.packed()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("H", [5, 1])
+def test_render_sharded_world2(H):
+    """Row-sharded frozen render: rank 0's records reach every rank, row slabs reassemble
+    into the full image in row order on every rank, and the counts sum."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    W = 4
+    procs = [ctx.Process(target=_render_worker, args=(r, 2, port, H, W, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted((q.get(timeout=120) for _ in range(2)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    from paper_1805_09258_b200.records import record_size
+
+    rows = np.random.default_rng(5).uniform(0.1, 0.9, (7, record_size(3)))
+    k = rows.sum() + 10 * (rows[:3] * 2).sum()
+    want = (np.arange(H)[:, None, None] * 1000 + np.arange(W)[None, :, None]) + np.arange(3) * 0.25 + k
+    for rank, img, st, ps, pm in got:
+        np.testing.assert_array_equal(ps, rows)
+        np.testing.assert_array_equal(pm, rows[:3] * 2)
+        np.testing.assert_allclose(img, want, rtol=0, atol=1e-9)
+        assert st["cache_hits"] == H * W and st["direct_evaluations"] == H

@@ -290,3 +290,32 @@ def test_populate_edge_cases():
     cs, stats = populate_cache(sc2, FieldGrid.for_scene(sc2, 1, 1), st2)
     assert stats["points_marched"] == 1 and stats["records_single"] == 1 and stats["records_multiple"] == 1
     np.testing.assert_array_equal(cs.single.packed()[0, :2], [0.5, 0.5])
+
+
+def test_render_rows_stitch_to_full_render():
+    """Row slabs (the unit of the row-sharded multi-GPU render) equal the full frozen render's
+    rows bit for bit, and the hit / evaluation counts add up."""
+    from paper_1805_09258_b200.renderer import RenderSettings, populate_cache, render, render_rows
+
+    z = golden("render")
+    sc = golden_scene(z)
+    eps, spp, step, n_ang, seed, n_inner, n_light = z["settings"]
+    camera = _camera(z["camera"])
+    st = RenderSettings(mode="ours-aniso", epsilon=float(eps), spp=int(spp), march_step=float(step),
+                        n_angular=int(n_ang), seed=int(seed), n_inner=int(n_inner), n_light_samples=int(n_light),
+                        frozen=True)
+    cs, _ = populate_cache(sc, camera, st)
+    full, fst = render(sc, camera, st, cs)
+    H = camera.height
+    cuts = [0, 1, H // 2, H]
+    hits = evals = 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        slab, s = render_rows(sc, camera, st, cs, a, b - a)
+        np.testing.assert_array_equal(slab, full[a:b])
+        hits += s["cache_hits"]
+        evals += s["direct_evaluations"]
+    assert (hits, evals) == (fst["cache_hits"], fst["direct_evaluations"])
+    empty, s0 = render_rows(sc, camera, st, cs, H, 0)
+    assert empty.shape == (0, camera.width, 3) and s0["cache_hits"] == 0
+    with pytest.raises(ValueError):
+        render_rows(sc, camera, st, cs, H - 1, 2)
