@@ -426,6 +426,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.del_fb_count = (unsigned int*)alloc(45, 8);
   W.del_fb2 = (int*)alloc(46, (D == 3 && !P.host_adjacency) ? (size_t)B * n * 4 : 16);
   W.del_fb2_count = (unsigned int*)alloc(47, 8);
+  W.cap_bin_stride = kCapGMax * kCapGMax + 1 + P.cols;  // bin starts + 2·cols 16-bit indices
+  W.cap_bins = (int*)alloc(49, (D == 3 && !P.host_adjacency && P.cols <= kCapGCols) ? (size_t)B * 2 * W.cap_bin_stride * 4 : 16);
   W.partial = (double*)alloc(37, B * kAsmParts * 64 * 8 + B * kAsmParts * 5 * 8);  // sums + 5 counters
   W.item_cap = item_cap;
   W.asm_items = item_cap > 0 ? (uint2*)alloc(41, (size_t)B * item_cap * 8) : nullptr;

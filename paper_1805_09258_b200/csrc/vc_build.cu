@@ -1291,6 +1291,169 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_cap(BuildParams P, Wave W,
   }
 }
 
+// Binned cap kernel.  k_cap_bin (one CTA per record and pole): the 2·cols directions of
+// the two cap rows are counting-sorted into a G × G grid over their (x, y) coordinates (cells at least
+// ρ wide, ρ ≥ the chord length of the δ pre-test), so a polar cell scans the ≤ 3 × 3 bins
+// around it instead of every column within its azimuth range — the whole two rows for the
+// ~11 % of cells whose δ-disc holds the pole, which set the pace of nearly every warp.
+// k_delaunay_capg (thread per polar cell): same candidate set (the float32 pre-test
+// decides), same wrap and security test as k_delaunay_cap.
+constexpr int kCapGBS = 128;
+constexpr size_t kCapBinSmem = sizeof(int) * (2 * kCapGMax * kCapGMax + 1) + 2 * sizeof(unsigned short) * 2 * kCapGCols;
+
+struct CapGrid {
+  int G;
+  float x0, inv, rho;
+  __device__ __forceinline__ int bin(float v) const {  // monotone in v (clamped)
+    const int b = (int)floorf((v - x0) * inv);
+    return min(max(b, 0), G - 1);
+  }
+};
+
+// Grid of the binned cap kernel (false: use the column-range kernel).  ρ bounds the
+// float32 chord |p − q| of every pair passing the pre-test p·q > cos δ − 1e-6 (with margin);
+// the grid spans the cap rows' |x|, |y| ≤ sin θ of their lower parallel.
+static bool cap_grid(const BuildParams& P, CapGrid& cg) {
+  const char* env = getenv("VOLCACHE_CAP_GRID");
+  if ((env && env[0] == '0') || P.cols > kCapGCols || P.host_adjacency) return false;
+  const double cd = (double)P.del_cap_cos;
+  const double rho = 1.001 * std::sqrt(2.0 * (1.0 - cd) + 4e-6);
+  const double zl = 1.0 - 2.0 * P.del_zstep;
+  const double gr = 1.001 * std::sqrt(std::max(0.0, 1.0 - zl * zl)) + 1e-6;
+  const int G = std::min(kCapGMax, std::max(1, (int)std::floor(2.0 * gr / rho)));
+  cg.G = G;
+  cg.x0 = (float)-gr;
+  cg.inv = (float)(G / (2.0 * gr));
+  cg.rho = (float)rho;
+  return true;
+}
+
+template <class T, int BS>
+__device__ __forceinline__ bool cap_cell_binned(const BuildParams& P, const Wave& W, int rec, int i,
+                                                const CapRadius& cr, const CapGrid& cg, const int* bstart,
+                                                const unsigned short* sorted, typename Vec2<T>::V* us,
+                                                unsigned short* ix, unsigned char* hs, int* own, int* own_cnt) {
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const bool north = i < cols;
+  const int rlo = north ? 0 : rows - 2;
+  const double* dirs = W.dirs + (size_t)rec * n * 3;
+  const float4* d32 = W.dirs32 + (size_t)rec * n;
+  const float4* c32 = d32 + (size_t)rlo * cols;
+  const Proj pr(dirs[3 * (size_t)i], dirs[3 * (size_t)i + 1], dirs[3 * (size_t)i + 2]);
+  const float4 p32 = d32[i];
+  const float cutf = cr.cos_d - 1e-6f;
+  int K = 0, start = 0;
+  T m2 = 0, n1 = 0;
+  const int bx0 = cg.bin(p32.x - cg.rho), bx1 = cg.bin(p32.x + cg.rho);
+  const int by0 = cg.bin(p32.y - cg.rho), by1 = cg.bin(p32.y + cg.rho);
+  for (int by = by0; by <= by1; ++by) {
+    // bins bx0..bx1 of one grid row are contiguous in the sorted list
+    const int a = bstart[by * cg.G + bx0], b = bstart[by * cg.G + bx1 + 1];
+    for (int t = a; t < b; ++t) {
+      const int jl = sorted[t];
+      const float4 q = c32[jl];
+      if (p32.x * q.x + p32.y * q.y + p32.z * q.z > cutf) {
+        if (K == kCapSlots) return false;
+        const auto u = Vec2<T>::proj(pr, dirs + 3 * ((size_t)rlo * cols + jl));
+        us[K * BS] = u;
+        ix[K * BS] = (unsigned short)jl;
+        const T r2 = u.x * u.x + u.y * u.y;
+        if (r2 > m2) { m2 = r2; start = K; }
+        n1 = fmax(n1, fabs(u.x) + fabs(u.y));
+        ++K;
+      }
+    }
+  }
+  const int hn = gift_wrap<T, BS>(us, K, start, n1, hs);
+  auto gidx = [&](int s) { return rlo * cols + (int)ix[s * BS]; };
+  const double zb = north ? 1.0 - 2.0 * P.del_zstep : 1.0 - P.del_zstep * (rows - 2);
+  const double sb2 = fmax(0.0, 1.0 - zb * zb);
+  auto secure = [&](double cx, double cy, double cz, double cp, double Q, double tol) {
+    bool ok = (cp - tol) * (cp - tol) * cr.s2 >= cr.c2 * Q;  // R ≤ δ/2
+    ok &= north ? ge_root(cz - zb * cp - tol, sb2 * Q) : ge_root(zb * cp - cz - tol, sb2 * Q);
+    return ok;
+  };
+  return hull_star<BS>(W, dirs, pr, (size_t)rec * n + i, i, hs, hn, gidx, secure, own, own_cnt);
+}
+
+// Counting sort of one (record, pole)'s cap-row directions by bin → W.cap_bins:
+// G² + 1 bin starts, then the 2·cols row-local indices in bin order.
+__global__ void __launch_bounds__(kCapGBS) k_cap_bin(BuildParams P, Wave W, CapGrid cg) {
+  extern __shared__ int bsm[];
+  int* bcur = bsm;                                   // G²
+  unsigned short* binof = (unsigned short*)(bsm + kCapGMax * kCapGMax);
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const int rec = blockIdx.x >> 1;
+  const bool north = !(blockIdx.x & 1);
+  const int rlo = north ? 0 : rows - 2;
+  const int np = 2 * cols, nb = cg.G * cg.G;
+  const float4* c32 = W.dirs32 + (size_t)rec * n + (size_t)rlo * cols;
+  int* out = W.cap_bins + (size_t)blockIdx.x * W.cap_bin_stride;
+  unsigned short* sorted = (unsigned short*)(out + kCapGMax * kCapGMax + 1);
+  for (int b = threadIdx.x; b < nb; b += kCapGBS) bcur[b] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < np; j += kCapGBS) {
+    const float4 q = c32[j];
+    const int b = cg.bin(q.y) * cg.G + cg.bin(q.x);
+    binof[j] = (unsigned short)b;
+    atomicAdd(&bcur[b], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the bin counts (warp 0, 32 bins per pass)
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int v = (b0 + lane < nb) ? bcur[b0 + lane] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (b0 + lane < nb) {
+        out[b0 + lane] = base + x - v;
+        bcur[b0 + lane] = base + x - v;
+      }
+      base += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) out[nb] = base;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < np; j += kCapGBS) sorted[atomicAdd(&bcur[binof[j]], 1)] = (unsigned short)j;
+}
+
+// Thread per polar cell (as k_delaunay_cap), candidates from the bins of k_cap_bin.
+__global__ void __launch_bounds__(kHullBS) k_delaunay_capg(BuildParams P, Wave W, int* own, int* own_cnt,
+                                                           CapGrid cg) {
+  extern __shared__ float2 csm[];
+  unsigned short* ix0 = (unsigned short*)(csm + kCapSlots * kHullBS);
+  unsigned char* hs = (unsigned char*)(ix0 + kCapSlots * kHullBS) + threadIdx.x;
+  const int n = P.n_angular, rows = P.rows, cols = P.cols;
+  const long long gid = (long long)blockIdx.x * kHullBS + threadIdx.x;  // over B × 2 × cols
+  bool fb = false;
+  int cell = -1;
+  if (gid < (long long)W.B * 2 * cols) {
+    const int rec = (int)(gid / (2 * cols));
+    const int k = (int)(gid - (long long)rec * 2 * cols);
+    const bool north = k < cols;
+    const int i = north ? k : (rows - 1) * cols + (k - cols);
+    cell = rec * n + i;
+    const int* bins = W.cap_bins + (size_t)(2 * rec + (north ? 0 : 1)) * W.cap_bin_stride;
+    const CapRadius cr{P.del_cap_cos, P.del_cap_sin, P.del_cap_c2, P.del_cap_s2};
+    fb = !cap_cell_binned<float, kHullBS>(P, W, rec, i, cr, cg, bins,
+                                          (const unsigned short*)(bins + kCapGMax * kCapGMax + 1),
+                                          csm + threadIdx.x, ix0 + threadIdx.x, hs, own, own_cnt);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, fb);
+  if (m) {
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned slot = 0;
+    if (lane == leader) slot = atomicAdd(W.del_fb_count, (unsigned)__popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (fb) W.del_fb[slot + __popc(m & ((1u << lane) - 1u))] = cell;
+  }
+}
+
 // Cells the float32 kernels hand back (an orientation within the float32 error bound, a
 // star not certified by its window or disc, a polar cell past the cap kernel's radius):
 // one warp per cell in float64.  Candidates are the directions within δ of p (lanes over
@@ -2143,6 +2306,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         cudaFuncSetAttribute(k_delaunay_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kHullBS * (kHullSlots * sizeof(float2) + kHullH)));
         cudaFuncSetAttribute(k_delaunay_cap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
+        cudaFuncSetAttribute(k_delaunay_capg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
         cudaFuncSetAttribute(k_delaunay_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWarpSmem);
         smem_attr = true;
       }
@@ -2165,7 +2329,14 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
           ++nl;
         }
         if (P.del_cap) {
-          k_delaunay_cap<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt);
+          CapGrid cg;
+          if (cap_grid(P, cg)) {
+            k_cap_bin<<<2 * W.B, kCapGBS, kCapBinSmem, st>>>(P, W, cg);
+            k_delaunay_capg<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt, cg);
+            ++nl;
+          } else {
+            k_delaunay_cap<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt);
+          }
           ++nl;
         }
         if (getenv("VOLCACHE_DEL_STATS")) {  // debug: cells handed to the clipping kernel

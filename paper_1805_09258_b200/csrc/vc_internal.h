@@ -16,7 +16,9 @@
 namespace vc {
 
 constexpr int kMaxDim = 3;
-constexpr int kBvhMaxDepth = 32;  // BVH depth cap = device traversal stack size
+constexpr int kBvhMaxDepth = 32;
+constexpr int kCapGMax = 32;     // binned cap kernel: bins per axis
+constexpr int kCapGCols = 1024;  // binned cap kernel: largest stratum row  // BVH depth cap = device traversal stack size
 #ifndef VC_ASM_SPLIT
 #define VC_ASM_SPLIT 16
 #endif
@@ -161,6 +163,8 @@ struct Wave {
   unsigned int* del_fb_count;
   int* del_fb2;          // B × n: cells the float64 wrap hands to the clipping kernel
   unsigned int* del_fb2_count;
+  int* cap_bins;         // B × 2 × cap_bin_stride: binned cap rows (k_cap_bin → k_delaunay_capg)
+  int cap_bin_stride;
   uint2* asm_items;      // B × item_cap assembly items (element, ring·4 + rep) in
                          // kAsmParts per-warp segments (null: fused assembly only)
   int* item_n;           // B × kAsmParts × 2: segment end of the surface / media items
