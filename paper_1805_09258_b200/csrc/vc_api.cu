@@ -573,7 +573,8 @@ int vc_profile_read(double* ms, int64_t* launches, int max_classes) {
 // rays at ≥ 1e-3 of grazing) between the plane point a ray lands on and the point of a
 // triangle the float64 hit test accepts.  Returns false when the emitters need more planes.
 static bool build_emit_planes(const std::vector<double>& prim, const std::vector<int>& order, double scale,
-                              vc::EmitPlanes* ep, std::vector<int>* start, std::vector<int>* tri) {
+                              vc::EmitPlanes* ep, std::vector<int>* start, std::vector<int>* tri,
+                              std::vector<unsigned>* occ) {
   using vc::kEmitPlanes;
   *ep = vc::EmitPlanes{};
   const int K = (int)order.size();
@@ -693,6 +694,21 @@ static bool build_emit_planes(const std::vector<double>& prim, const std::vector
   }
   (*start)[ncell] = (int)tri->size();
   if (tri->empty()) tri->push_back(0);
+  // coarse occupancy (blocks of fx × fy cells, ≤ 32 × 32 blocks per plane)
+  occ->assign((size_t)kEmitPlanes * 32, 0u);
+  for (int g = 0; g < ng; ++g) {
+    const int gx = ep->gx[g], gy = ep->gy[g];
+    const int fx = (gx + 31) / 32, fy = (gy + 31) / 32;
+    ep->occ_w[g] = (gx + fx - 1) / fx;
+    ep->occ_h[g] = (gy + fy - 1) / fy;
+    ep->occ_inv[g][0] = ep->inv[g][0] / fx;
+    ep->occ_inv[g][1] = ep->inv[g][1] / fy;
+    for (int j = 0; j < gy; ++j)
+      for (int i = 0; i < gx; ++i) {
+        const int c = ep->cell0[g] + j * gx + i;
+        if ((*start)[c + 1] > (*start)[c]) (*occ)[(size_t)g * 32 + j / fy] |= 1u << (i / fx);
+      }
+  }
   return true;
 }
 
@@ -804,11 +820,15 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     std::vector<int> eorder((size_t)sc->emit.K);
     if (sc->emit.K) cudaMemcpy(eorder.data(), sc->emit.prim_id, eorder.size() * 4, cudaMemcpyDeviceToHost);
     std::vector<int> start, tri;
-    if (build_emit_planes(prim, eorder, sc->scale, &sc->ep, &start, &tri)) {
+    std::vector<unsigned> occ;
+    if (build_emit_planes(prim, eorder, sc->scale, &sc->ep, &start, &tri, &occ)) {
       up((void**)&sc->d_ep_start, start.data(), start.size() * 4);
       up((void**)&sc->d_ep_tri, tri.data(), tri.size() * 4);
+      up((void**)&sc->d_ep_occ, occ.data(), occ.size() * 4);
       sc->ep.cell_start = sc->d_ep_start;
       sc->ep.cell_tri = sc->d_ep_tri;
+      const char* ef = getenv("VOLCACHE_EMIT_FILTER");
+      sc->ep.occ = (ef && ef[0] == '0') ? nullptr : sc->d_ep_occ;
     } else {
       sc->ep.ng = 0;
     }

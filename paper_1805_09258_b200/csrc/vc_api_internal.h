@@ -63,6 +63,7 @@ struct vc_scene {
   vc::EmitPlanes ep{};   // device pointers owned here
   int* d_ep_start = nullptr;
   int* d_ep_tri = nullptr;
+  unsigned* d_ep_occ = nullptr;
   double* d_normal = nullptr;
   double* d_emission = nullptr;
   double* d_albedo = nullptr;
@@ -81,6 +82,7 @@ struct vc_scene {
     cudaFree(d_es_surf);
     cudaFree(d_ep_start);
     cudaFree(d_ep_tri);
+    cudaFree(d_ep_occ);
   }
 };
 

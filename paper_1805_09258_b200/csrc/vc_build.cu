@@ -381,6 +381,55 @@ struct Toward {
   }
 };
 
+// Float32 pre-filter of the gather rays (3D, emitter plane grids with occupancy): could the
+// ray with draws (u0, u1) from the media sample y meet an emitter triangle?  The direction
+// and the landing point on each emitter plane are computed in float32 with a bound on
+// their error against the float64 values (y: ≤ ey = 2e-6·scale; direction components:
+// ≤ ed = 2e-6, from z = 1 − 2u0 and sin θ = 2√(u0(1 − u0)) taken from float64 and
+// sincospi of 2u1); a plane is skipped only when the landing distance is certainly
+// negative or every coarse occupancy block within the landing point's error radius is
+// empty.  A triangle the float64 test accepts holds the float64 landing point, whose fine
+// cell lists it (cells cover the triangles' padded boxes), so its block is occupied:
+// "false" is exact, the survivors take the float64 path unchanged.  Rays within 2e-3 of
+// grazing a plane are always kept.
+struct FilterPlane {
+  float n[3], c, a1[3], a2[3], lo[2], ci[2];
+  int cw, ch;
+};
+
+__device__ __forceinline__ bool emitter_may_hit(const FilterPlane* fp, const unsigned* occ, int ng,
+                                                const float* y, double u0, double u1, float ey, float mpad) {
+  const float om = (float)(1.0 - u0), z = (float)(1.0 - 2.0 * u0);
+  const float sq = sqrtf(4.0f * (float)u0 * om);
+  float sp, cp;
+  sincospif(2.0f * (float)u1, &sp, &cp);
+  const float d[3] = {sq * cp, sq * sp, z};
+  constexpr float ed = 2e-6f;
+  for (int g = 0; g < ng; ++g) {
+    const FilterPlane& E = fp[g];
+    const float dn = E.n[0] * d[0] + E.n[1] * d[1] + E.n[2] * d[2];
+    const float adn = fabsf(dn);
+    if (adn < 2e-3f) return true;
+    const float tp = (E.c - (E.n[0] * y[0] + E.n[1] * y[1] + E.n[2] * y[2])) / dn;
+    const float e = ey + fabsf(tp) * ed;
+    if (tp + 2.0f * e / adn < 0.0f) continue;  // behind the sample
+    const float X[3] = {y[0] + tp * d[0], y[1] + tp * d[1], y[2] + tp * d[2]};
+    const float px = E.a1[0] * X[0] + E.a1[1] * X[1] + E.a1[2] * X[2];
+    const float py = E.a2[0] * X[0] + E.a2[1] * X[1] + E.a2[2] * X[2];
+    const float m = 4.0f * e * (1.0f + 1.0f / adn) + mpad;
+    int i0 = (int)floorf((px - m - E.lo[0]) * E.ci[0]), i1 = (int)floorf((px + m - E.lo[0]) * E.ci[0]);
+    int j0 = (int)floorf((py - m - E.lo[1]) * E.ci[1]), j1 = (int)floorf((py + m - E.lo[1]) * E.ci[1]);
+    if (i1 < 0 || j1 < 0 || i0 >= E.cw || j0 >= E.ch) continue;  // beside every emitter
+    i0 = max(i0, 0); j0 = max(j0, 0);
+    i1 = min(i1, E.cw - 1); j1 = min(j1, E.ch - 1);
+    if (i1 - i0 > 1 || j1 - j0 > 1) return true;
+    const unsigned mask = (i1 > i0 ? 3u : 1u) << i0;
+    for (int j = j0; j <= j1; ++j)
+      if (occ[g * 32 + j] & mask) return true;
+  }
+  return false;
+}
+
 // Pass 1 of the two-pass gather.  Each lane walks runs of kGatherRun consecutive samples
 // (PCG64 jumped once per run, then stepped); the draws of samples whose ray cannot reach an
 // emitter are consumed and dropped at once, the others are compacted into a per-warp queue
@@ -397,6 +446,31 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
                                                                GatherItem* q, unsigned long long* q_count,
                                                                long long q_cap) {
   __shared__ PendSample pend_all[256 / 32][kPendCap];
+  __shared__ FilterPlane fplane[kEmitPlanes];
+  __shared__ unsigned focc[kEmitPlanes * 32];
+  const bool filt = D == 3 && S.ep.ng > 0 && S.ep.occ != nullptr;
+  if (filt) {
+    for (int t = threadIdx.x; t < kEmitPlanes * 32; t += blockDim.x) focc[t] = S.ep.occ[t];
+    if (threadIdx.x < S.ep.ng) {
+      const int g = threadIdx.x;
+      FilterPlane& F = fplane[g];
+      for (int a = 0; a < 3; ++a) {
+        F.n[a] = (float)S.ep.n[g][a];
+        F.a1[a] = (float)S.ep.a1[g][a];
+        F.a2[a] = (float)S.ep.a2[g][a];
+      }
+      F.c = (float)S.ep.c[g];
+      F.lo[0] = (float)S.ep.lo[g][0];
+      F.lo[1] = (float)S.ep.lo[g][1];
+      F.ci[0] = (float)S.ep.occ_inv[g][0];
+      F.ci[1] = (float)S.ep.occ_inv[g][1];
+      F.cw = S.ep.occ_w[g];
+      F.ch = S.ep.occ_h[g];
+    }
+    __syncthreads();
+  }
+  const float f_ey = (float)(2e-6 * S.scale), f_pad = (float)(1e-6 * S.scale);
+  const float f_step = (float)P.march_step;
   const int rec = blockIdx.y;
   const long long base = W.rec_base[rec];
   const int Pr = (int)(W.rec_base[rec + 1] - base);
@@ -525,9 +599,17 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, Bu
         u0 = g.next_double();
         if constexpr (D == 3) {
           u1 = g.next_double();
-          double y[3];
-          origin(k, i, y);
-          keep = toward(y, u0, u1, tol);
+          if (filt) {
+            // the filter's float32 sample point (error ≤ f_ey against origin())
+            const float4 dk = W.dirs32[(size_t)rec * n + k];
+            const float ri = ((float)i + 0.5f) * f_step;
+            const float y32[3] = {(float)x[0] + ri * dk.x, (float)x[1] + ri * dk.y, (float)x[2] + ri * dk.z};
+            keep = emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
+          } else {
+            double y[3];
+            origin(k, i, y);
+            keep = toward(y, u0, u1, tol);
+          }
           if (!keep && W.dense_media) {
             const double zero[3] = {0.0, 0.0, 0.0};
             store_media(W.media + (size_t)(base + j) * 3, zero);

@@ -52,6 +52,11 @@ struct EmitPlanes {
   int axis_only;                 // every plane axis-aligned (the gather's draw-only test)
   const int* cell_start;         // CSR over every plane's cells
   const int* cell_tri;           // leaf-order indices into the emitter set
+  // coarse occupancy per plane (≤ 32 × 32 blocks of cells; row j = one 32-bit word, bit i
+  // set when a cell of block (i, j) lists a triangle): the gather's float32 pre-filter
+  const unsigned* occ;           // kEmitPlanes × 32 words (nullptr: no pre-filter)
+  double occ_inv[kEmitPlanes][2];
+  int occ_w[kEmitPlanes], occ_h[kEmitPlanes];
 };
 
 // Scene as seen by kernels (passed by value).

@@ -421,9 +421,39 @@ def test_emitter_plane_grids_same_result():
     env = dict(os.environ)
     env.pop("VOLCACHE_EMIT_PLANES", None)
     subprocess.run([sys.executable, "-c", code, str(out / "ep_grid.npy")], check=True, cwd=ROOT, env=env)
+    env["VOLCACHE_EMIT_FILTER"] = "0"
+    subprocess.run([sys.executable, "-c", code, str(out / "ep_nofilt.npy")], check=True, cwd=ROOT, env=env)
     env["VOLCACHE_EMIT_PLANES"] = "0"
     subprocess.run([sys.executable, "-c", code, str(out / "ep_bvh.npy")], check=True, cwd=ROOT, env=env)
     np.testing.assert_array_equal(np.load(out / "ep_grid.npy"), np.load(out / "ep_bvh.npy"))
+    np.testing.assert_array_equal(np.load(out / "ep_nofilt.npy"), np.load(out / "ep_bvh.npy"))
+
+
+def test_gather_prefilter_same_media():
+    """The float32 emitter pre-filter of the gather drops only rays that meet no emitter:
+    per-sample media radiance (dense, every live ring sample) bit-identical with the filter
+    off (VOLCACHE_EMIT_FILTER=0), on window-room records whose samples see the windows."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1805_09258_b200 import configs, inspect_record;"
+        "w = configs.cfg3(); out = [];"
+        "[out.append(inspect_record(w.scene, w.points[i], rng_seed=np.random.SeedSequence([w.seed, 401, i]),"
+        " n_angular=4096, march_step=w.march_step)['media'].reshape(-1)) for i in range(3)];"
+        "np.save(sys.argv[1], np.concatenate(out))"
+    )
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    env = dict(os.environ)
+    env.pop("VOLCACHE_EMIT_FILTER", None)
+    subprocess.run([sys.executable, "-c", code, str(out / "pf_on.npy")], check=True, cwd=ROOT, env=env)
+    env["VOLCACHE_EMIT_FILTER"] = "0"
+    subprocess.run([sys.executable, "-c", code, str(out / "pf_off.npy")], check=True, cwd=ROOT, env=env)
+    on, off = np.load(out / "pf_on.npy"), np.load(out / "pf_off.npy")
+    assert on.size > 100000 and np.count_nonzero(on) > 1000
+    np.testing.assert_array_equal(on, off)
 
 
 def test_assembly_item_lists_match_fused():
