@@ -32,12 +32,17 @@ namespace vc {
 #define VC_LB_TRACE 3  // min resident 256-thread CTAs per SM for the ray kernels
 #endif
 // the BVH-latency-bound kernels run better at 4 CTAs (≤ 64 registers): primary 1.92 →
-// 1.64 ms, occlusion 1.70 → 1.48 ms per 512 records; the emitter pass keeps 3
+// 1.64 ms, occlusion 1.70 → 1.48 ms per 512 records
 #ifndef VC_LB_PRIMARY
 #define VC_LB_PRIMARY 4
 #endif
 #ifndef VC_LB_OCCL
 #define VC_LB_OCCL 4
+#endif
+// the emitter pass, since its float32 pre-filter: 4 CTAs (64 registers) 1.99 ms vs 3 CTAs
+// 2.05 ms vs 2 CTAs 2.43 ms per 512 records
+#ifndef VC_LB_EMIT
+#define VC_LB_EMIT 4
 #endif
 
 // Thread → direction map: each warp takes a 4-row × 8-column tile of the stratum grid
@@ -442,7 +447,7 @@ struct PendSample {
 constexpr int kPendCap = 64;  // per warp: ≤ 31 left over + one step's 32
 
 template <int D>
-__global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
+__global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
                                                                GatherItem* q, unsigned long long* q_count,
                                                                long long q_cap) {
   __shared__ PendSample pend_all[256 / 32][kPendCap];

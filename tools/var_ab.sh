@@ -6,5 +6,5 @@ for v in default paper_1805_09258_b200/lib/variants/*/libvolcache_b200.so; do
   if [ $v = default ]; then unset VOLCACHE_B200_LIB; else export VOLCACHE_B200_LIB=$PWD/$v; fi
   echo "== $v"
   ncu --clock-control none --metrics gpu__time_duration.sum -k regex:"$K" --csv python tools/ncu_target.py 512 nowarm 2>/dev/null \
-    | grep -E "$K" | awk -F'","' '{print $5, $NF}' | sed 's/(.*)//' | cut -c1-60
+    | grep -E "$K" | awk -F'","' '{print $NF, substr($5,1,40)}'
 done
