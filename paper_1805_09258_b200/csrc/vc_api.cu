@@ -414,6 +414,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   long long* dstat = (long long*)alloc(17, B * kStats * 8);
   double* drec = (double*)alloc(18, B * 2 * RS * 8);
   int* own = (int*)alloc(19, (D == 3 && !P.host_adjacency) ? B * n * 32 * 8 : 16);
+  W.own_stride = (long long)B * n;
   int* own_cnt = (int*)alloc(20, B * n * 4);
   uint32_t* dwords = (uint32_t*)alloc(21, words ? B * prm->seed_words * 4 + 4 : 16);
   W.dirs32 = (float4*)alloc(35, D == 3 ? B * n * 16 : 16);

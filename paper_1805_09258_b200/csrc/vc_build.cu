@@ -672,6 +672,13 @@ __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl(DevScene S, Wav
 
 constexpr int kMaxV = 24;
 
+// Owned triangle t of cell `base` (wave-global direction index): slot-major int2 rows
+// (stride W.own_stride cells), so the lanes of a warp (consecutive cells) write and
+// k_tri_compact reads one coalesced row per slot.
+__device__ __forceinline__ void own_put(const Wave& W, int* own, size_t base, int t, int a, int b) {
+  ((int2*)own)[(size_t)t * W.own_stride + base] = make_int2(a, b);
+}
+
 struct Line {
   double A, B, C;
 };
@@ -926,8 +933,7 @@ __device__ int delaunay_point(const BuildParams& P, const Wave& W, int rec, int 
           atomicMax(W.tri_status + rec, 2);
           break;
         }
-        own[(base * kMaxV + c) * 2 + 0] = a;
-        own[(base * kMaxV + c) * 2 + 1] = b;
+        own_put(W, own, base, c, a, b);
         ++c;
       }
     }
@@ -1161,8 +1167,7 @@ __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, con
   for (int t = 0; t < hn; ++t) {
     const int gn = (t + 1 == hn) ? g0 : gidx(hs[(t + 1) * BS]);
     if (i < ga && i < gn) {
-      own[(base * kMaxV + c) * 2 + 0] = ga;
-      own[(base * kMaxV + c) * 2 + 1] = gn;
+      own_put(W, own, base, c, ga, gn);
       ++c;
     }
     ga = gn;
@@ -1699,8 +1704,7 @@ __device__ bool warp_cell(const BuildParams& P, const Wave& W, int rec, int i, d
         for (int t = 0; t < hn; ++t) {
           const int ga = ix[hs[t]], gn = ix[hs[t + 1 == hn ? 0 : t + 1]];
           if (i < ga && i < gn) {
-            own[(base * kMaxV + c) * 2 + 0] = ga;
-            own[(base * kMaxV + c) * 2 + 1] = gn;
+            own_put(W, own, base, c, ga, gn);
             ++c;
           }
         }
@@ -1753,13 +1757,14 @@ __global__ void __launch_bounds__(kCompactBS) k_tri_compact(BuildParams P, Wave 
     long long tot;
     long long pre = block_exscan<kCompactBS>(c, tot, sm);
     if (i < n) {
-      size_t ob = ((size_t)rec * n + i) * kMaxV;
+      const int2* o2 = (const int2*)own + (size_t)rec * n + i;
       for (int t = 0; t < c; ++t) {
         long long o = run + pre + t;
         if (o < P.n_tris) {
+          const int2 ab = o2[(size_t)t * W.own_stride];
           tris[o * 3 + 0] = i;
-          tris[o * 3 + 1] = own[(ob + t) * 2 + 0];
-          tris[o * 3 + 2] = own[(ob + t) * 2 + 1];
+          tris[o * 3 + 1] = ab.x;
+          tris[o * 3 + 2] = ab.y;
         }
       }
     }

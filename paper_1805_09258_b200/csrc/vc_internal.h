@@ -168,6 +168,7 @@ struct Wave {
   unsigned int* del_fb_count;
   int* del_fb2;          // B × n: cells the float64 wrap hands to the clipping kernel
   unsigned int* del_fb2_count;
+  long long own_stride;  // cells per slot row of the owned-triangle array (wave capacity × n)
   int* cap_bins;         // B × 2 × cap_bin_stride: binned cap rows (k_cap_bin → k_delaunay_capg)
   int cap_bin_stride;
   uint2* asm_items;      // B × item_cap assembly items (element, ring·4 + rep) in
