@@ -9,7 +9,7 @@
 //                gather ray, σs·mean T·L_o  (src/transport.py:288-310)
 //   k_delaunay   thread per direction (3D): spherical Voronoi cell by half-space
 //                clipping with a security radius → canonical Delaunay triangles
-//   k_tri_compact CTA per record: owned triangles in point order → triangle list
+//   k_own_scan + k_tri_scatter: owned triangles in point order → triangle list
 //   k_assemble   CTA per record: ring elements with live representative vertex are
 //                queued per warp (ballot compaction) and evaluated 32 at a time;
 //                moments summed with shuffles + shared-memory tree, no atomics
@@ -674,7 +674,7 @@ constexpr int kMaxV = 24;
 
 // Owned triangle t of cell `base` (wave-global direction index): slot-major int2 rows
 // (stride W.own_stride cells), so the lanes of a warp (consecutive cells) write and
-// k_tri_compact reads one coalesced row per slot.
+// k_tri_scatter reads one coalesced row per slot.
 __device__ __forceinline__ void own_put(const Wave& W, int* own, size_t base, int t, int a, int b) {
   ((int2*)own)[(size_t)t * W.own_stride + base] = make_int2(a, b);
 }
@@ -1745,32 +1745,50 @@ __global__ void __launch_bounds__(kWarpBS) k_delaunay_warp(BuildParams P, Wave W
 
 constexpr int kCompactBS = 512;
 
-__global__ void __launch_bounds__(kCompactBS) k_tri_compact(BuildParams P, Wave W, const int* own,
-                                                            const int* own_cnt) {
+// Canonical triangle list in two launches: k_own_scan (CTA per record) turns the owned
+// counts into exclusive offsets (4 cells per thread, one block scan per 4·kCompactBS
+// cells), k_tri_scatter (thread per cell) copies each cell's owned triangles to its offset.
+__global__ void __launch_bounds__(kCompactBS) k_own_scan(BuildParams P, Wave W, const int* own_cnt, int* off) {
   __shared__ long long sm[kCompactBS / 32 + 1];
   const int rec = blockIdx.x, n = P.n_angular;
-  int* tris = W.tris + (size_t)rec * P.n_tris * 3;
+  const int* cnt = own_cnt + (size_t)rec * n;
+  int* o = off + (size_t)rec * n;
   long long run = 0;
-  for (int base = 0; base < n; base += kCompactBS) {
-    int i = base + threadIdx.x;
-    int c = (i < n) ? own_cnt[(size_t)rec * n + i] : 0;
+  for (int base = 0; base < n; base += 4 * kCompactBS) {
+    const int i = base + 4 * threadIdx.x;
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = (i + u < n) ? cnt[i + u] : 0;
     long long tot;
-    long long pre = block_exscan<kCompactBS>(c, tot, sm);
-    if (i < n) {
-      const int2* o2 = (const int2*)own + (size_t)rec * n + i;
-      for (int t = 0; t < c; ++t) {
-        long long o = run + pre + t;
-        if (o < P.n_tris) {
-          const int2 ab = o2[(size_t)t * W.own_stride];
-          tris[o * 3 + 0] = i;
-          tris[o * 3 + 1] = ab.x;
-          tris[o * 3 + 2] = ab.y;
-        }
-      }
+    long long pre = run + block_exscan<kCompactBS>(c[0] + c[1] + c[2] + c[3], tot, sm);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i + u < n) o[i + u] = (int)pre;
+      pre += c[u];
     }
     run += tot;
   }
   if (threadIdx.x == 0 && run != P.n_tris) atomicMax(W.tri_status + rec, 3);
+}
+
+__global__ void k_tri_scatter(BuildParams P, Wave W, const int* own, const int* own_cnt, const int* off) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = P.n_angular;
+  if (gid >= (long long)W.B * n) return;
+  const int rec = (int)(gid / n), i = (int)(gid - (long long)rec * n);
+  const int c = own_cnt[gid];
+  const int o0 = off[gid];
+  int* tris = W.tris + (size_t)rec * P.n_tris * 3;
+  const int2* o2 = (const int2*)own + gid;
+  for (int t = 0; t < c; ++t) {
+    const int o = o0 + t;
+    if (o < P.n_tris) {
+      const int2 ab = o2[(size_t)t * W.own_stride];
+      tris[o * 3 + 0] = i;
+      tris[o * 3 + 1] = ab.x;
+      tris[o * 3 + 2] = ab.y;
+    }
+  }
 }
 
 // Vertex valence of caller-supplied triangles (star counting).
@@ -2469,7 +2487,10 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       ++nl;
       prof_end(st);
       prof_begin(KC_COMPACT, st);
-  k_tri_compact<<<W.B, kCompactBS, 0, st>>>(P, W, own, own_cnt);
+  // W.del_fb (B × n ints) is free once the Delaunay kernels are done: the offsets
+  k_own_scan<<<W.B, kCompactBS, 0, st>>>(P, W, own_cnt, W.del_fb);
+  k_tri_scatter<<<grid_for(nt, 256), 256, 0, st>>>(P, W, own, own_cnt, W.del_fb);
+  ++nl;
   prof_end(st);
       nl += 2;
     } else {
