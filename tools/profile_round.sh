@@ -14,7 +14,7 @@ rm -f /tmp/prof_round.ncu-rep && timeout 2400 ncu --set full --import-source on 
   -o /tmp/prof_round python tools/ncu_target.py 2048 nowarm > gpurun_out/ncu_full.log 2>&1
 python tools/ncu_summary.py /tmp/prof_round.ncu-rep gpurun_out/ncu_full_summary.md gpurun_out/ncu_traffic.json \
   > /dev/null 2> gpurun_out/ncu_summary.err
-for k in k_delaunay_hull k_delaunay_cap k_delaunay_warp k_gather_emit k_gather_occl k_primary k_assemble_t k_asm_eval; do
+for k in k_delaunay_hull k_delaunay_capg k_delaunay_warp k_gather_emit k_gather_occl k_primary k_assemble_t k_asm_eval; do
   python tools/ncu_lines.py /tmp/prof_round.ncu-rep "$k" 25 > gpurun_out/lines_$k.txt 2>&1
 done
 tail -3 gpurun_out/ncu_full.log
