@@ -397,9 +397,11 @@ struct Toward {
 // cell lists it (cells cover the triangles' padded boxes), so its block is occupied:
 // "false" is exact, the survivors take the float64 path unchanged.  Rays within 2e-3 of
 // grazing a plane are always kept.
-struct FilterPlane {
-  float n[3], c, a1[3], a2[3], lo[2], ci[2];
-  int cw, ch;
+struct alignas(16) FilterPlane {  // four 16-byte shared-memory loads per plane
+  float4 nc;   // normal, offset
+  float4 a1;   // in-plane axis 1, grid origin x
+  float4 a2;   // in-plane axis 2, grid origin y
+  float4 cc;   // 1 / block size (x, y), blocks (x, y) as int bits
 };
 
 __device__ __forceinline__ bool emitter_may_hit(const FilterPlane* fp, const unsigned* occ, int ng,
@@ -411,22 +413,24 @@ __device__ __forceinline__ bool emitter_may_hit(const FilterPlane* fp, const uns
   const float d[3] = {sq * cp, sq * sp, z};
   constexpr float ed = 2e-6f;
   for (int g = 0; g < ng; ++g) {
-    const FilterPlane& E = fp[g];
-    const float dn = E.n[0] * d[0] + E.n[1] * d[1] + E.n[2] * d[2];
+    const float4 nc = fp[g].nc;
+    const float dn = nc.x * d[0] + nc.y * d[1] + nc.z * d[2];
     const float adn = fabsf(dn);
     if (adn < 2e-3f) return true;
-    const float tp = (E.c - (E.n[0] * y[0] + E.n[1] * y[1] + E.n[2] * y[2])) / dn;
+    const float tp = (nc.w - (nc.x * y[0] + nc.y * y[1] + nc.z * y[2])) / dn;
     const float e = ey + fabsf(tp) * ed;
     if (tp + 2.0f * e / adn < 0.0f) continue;  // behind the sample
     const float X[3] = {y[0] + tp * d[0], y[1] + tp * d[1], y[2] + tp * d[2]};
-    const float px = E.a1[0] * X[0] + E.a1[1] * X[1] + E.a1[2] * X[2];
-    const float py = E.a2[0] * X[0] + E.a2[1] * X[1] + E.a2[2] * X[2];
+    const float4 a1 = fp[g].a1, a2 = fp[g].a2, cc = fp[g].cc;
+    const int cw = __float_as_int(cc.z), ch = __float_as_int(cc.w);
+    const float px = a1.x * X[0] + a1.y * X[1] + a1.z * X[2];
+    const float py = a2.x * X[0] + a2.y * X[1] + a2.z * X[2];
     const float m = 4.0f * e * (1.0f + 1.0f / adn) + mpad;
-    int i0 = (int)floorf((px - m - E.lo[0]) * E.ci[0]), i1 = (int)floorf((px + m - E.lo[0]) * E.ci[0]);
-    int j0 = (int)floorf((py - m - E.lo[1]) * E.ci[1]), j1 = (int)floorf((py + m - E.lo[1]) * E.ci[1]);
-    if (i1 < 0 || j1 < 0 || i0 >= E.cw || j0 >= E.ch) continue;  // beside every emitter
+    int i0 = (int)floorf((px - m - a1.w) * cc.x), i1 = (int)floorf((px + m - a1.w) * cc.x);
+    int j0 = (int)floorf((py - m - a2.w) * cc.y), j1 = (int)floorf((py + m - a2.w) * cc.y);
+    if (i1 < 0 || j1 < 0 || i0 >= cw || j0 >= ch) continue;  // beside every emitter
     i0 = max(i0, 0); j0 = max(j0, 0);
-    i1 = min(i1, E.cw - 1); j1 = min(j1, E.ch - 1);
+    i1 = min(i1, cw - 1); j1 = min(j1, ch - 1);
     if (i1 - i0 > 1 || j1 - j0 > 1) return true;
     const unsigned mask = (i1 > i0 ? 3u : 1u) << i0;
     for (int j = j0; j <= j1; ++j)
@@ -458,19 +462,12 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
     for (int t = threadIdx.x; t < kEmitPlanes * 32; t += blockDim.x) focc[t] = S.ep.occ[t];
     if (threadIdx.x < S.ep.ng) {
       const int g = threadIdx.x;
-      FilterPlane& F = fplane[g];
-      for (int a = 0; a < 3; ++a) {
-        F.n[a] = (float)S.ep.n[g][a];
-        F.a1[a] = (float)S.ep.a1[g][a];
-        F.a2[a] = (float)S.ep.a2[g][a];
-      }
-      F.c = (float)S.ep.c[g];
-      F.lo[0] = (float)S.ep.lo[g][0];
-      F.lo[1] = (float)S.ep.lo[g][1];
-      F.ci[0] = (float)S.ep.occ_inv[g][0];
-      F.ci[1] = (float)S.ep.occ_inv[g][1];
-      F.cw = S.ep.occ_w[g];
-      F.ch = S.ep.occ_h[g];
+      const EmitPlanes& E = S.ep;
+      fplane[g].nc = make_float4((float)E.n[g][0], (float)E.n[g][1], (float)E.n[g][2], (float)E.c[g]);
+      fplane[g].a1 = make_float4((float)E.a1[g][0], (float)E.a1[g][1], (float)E.a1[g][2], (float)E.lo[g][0]);
+      fplane[g].a2 = make_float4((float)E.a2[g][0], (float)E.a2[g][1], (float)E.a2[g][2], (float)E.lo[g][1]);
+      fplane[g].cc = make_float4((float)E.occ_inv[g][0], (float)E.occ_inv[g][1], __int_as_float(E.occ_w[g]),
+                                 __int_as_float(E.occ_h[g]));
     }
     __syncthreads();
   }
@@ -582,7 +579,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
   // warp-uniform loop: lane runs [j0, j0 + kGatherRun) of the record's samples
   for (int j0w = (blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * kGatherRun; j0w < Pr; j0w += stride) {
     const int j0 = j0w + lane * kGatherRun;
-    int k = 0, i = 0;
+    int k = 0, i = 0, ck = 0;  // ck = cnt[k]
     Pcg64 g;
     if (j0 < Pr) {
       // direction of the first sample (run table written by k_rings)
@@ -590,6 +587,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
       i = j0 - pre[k];
       g = pcg_load(st);
       pcg_advance(g, (unsigned long long)(draws0 + (long long)(D == 3 ? 2 : 1) * j0), jt);
+      ck = cnt[k];
     }
     for (int step = 0; step < kGatherRun; ++step) {
       const int j = j0 + step;
@@ -597,9 +595,10 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
       bool keep = false;
       double u0 = 0.0, u1 = 0.0;
       if (active) {
-        while (i >= cnt[k]) {  // next direction with live rings
+        while (i >= ck) {  // next direction with live rings
           ++k;
           i = 0;
+          ck = cnt[k];
         }
         u0 = g.next_double();
         if constexpr (D == 3) {
