@@ -319,3 +319,40 @@ def test_render_rows_stitch_to_full_render():
     assert empty.shape == (0, camera.width, 3) and s0["cache_hits"] == 0
     with pytest.raises(ValueError):
         render_rows(sc, camera, st, cs, H - 1, 2)
+
+
+def test_render_sharded_nccl_world1_matches_render():
+    """dist.render_sharded + broadcast_cache_set over NCCL (one rank on this GPU): the
+    gathered image and counts equal the single-process frozen render."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = r'''
+import os, sys, socket, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+from conftest import golden, golden_scene
+from paper_1805_09258_b200.renderer import Camera, RenderSettings, populate_cache, render
+from paper_1805_09258_b200 import dist as vdist
+s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1)
+z = golden("render"); sc = golden_scene(z)
+eps, spp, step, n_ang, seed, n_inner, n_light = z["settings"]; v = z["camera"]
+cam = Camera(position=v[0:3], look_at=v[3:6], up=v[6:9], fov_degrees=float(v[9]), width=int(v[10]), height=int(v[11]))
+st = RenderSettings(mode="ours-aniso", epsilon=float(eps), spp=int(spp), march_step=float(step), n_angular=int(n_ang),
+                    seed=int(seed), n_inner=int(n_inner), n_light_samples=int(n_light), frozen=True)
+cs, _ = populate_cache(sc, cam, st)
+full, fst = render(sc, cam, st, cs)
+vdist.broadcast_cache_set(cs)
+img, s2 = vdist.render_sharded(sc, cam, st, cs)
+np.testing.assert_array_equal(img, full)
+assert (s2["cache_hits"], s2["direct_evaluations"]) == (fst["cache_hits"], fst["direct_evaluations"])
+dist.destroy_process_group()
+print("sharded ok")
+'''
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sharded ok" in r.stdout
