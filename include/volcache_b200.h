@@ -124,6 +124,9 @@ typedef struct {
   double alpha;          /* baseline_alpha: scales log_gradient_radius */
   int flags;             /* VC_MEM_HOST, VC_SEED_WORDS */
   int seed_words;
+  int64_t* draws;        /* NULL or n: PCG64 doubles each record's stream consumed, as the
+                            reference's rng (the collision loop stops at the first bounce
+                            without a collision, src/subdivision.py:480-486) */
 } vc_baseline_params;
 
 /* Occlusion-unaware baseline for n records: baseline_estimate (src/subdivision.py:416-521)
@@ -149,6 +152,10 @@ int vc_path_trace(vc_scene* scene, int m, const double* x, const void* rng, int6
 int vc_cache_create(int dim, const double* bounds_min, const double* bounds_max, int n_records,
                     const double* records, vc_cache** out);
 void vc_cache_destroy(vc_cache* cache);
+/* Append n records (rows as vc_cache_create; host memory with VC_MEM_HOST, else device,
+ * e.g. rows received over NCCL) and re-index: RadianceCache.insert (src/cache.py:298-315)
+ * for a batch, without re-uploading the records already held.  Creation tags are −1. */
+int vc_cache_insert(vc_cache* cache, int n_records, const double* records, int flags, void* stream);
 /* log_space = 1: the cache holds BaselineRecord spheres and blends with
  * log_space_interpolate (src/cache.py:363-394); 0 (default): ellipsoids, interpolate. */
 int vc_cache_set_blend(vc_cache* cache, int log_space);

@@ -51,13 +51,17 @@ def baseline_estimate(scene, x, n_angular=None, rng_seed=None, max_media_bounces
     if x.size != d:
         raise ValueError("x dimensionality does not match the scene")
     n = int(DEFAULT_N_ANGULAR[d] if n_angular is None else n_angular)
-    st, _ = pcg64_state(rng_seed)
+    st, gen = pcg64_state(rng_seed)
     p = _bparams(n, max_media_bounces, n_light_samples, 1.0, _lib.VC_MEM_HOST)
+    draws = np.zeros(1, np.int64)
+    p.draws = draws.ctypes.data
     es = 3 + 3 * d
     est = np.zeros((2, es))
     smp = np.zeros((2, 2, n))
     _lib.check(_lib.lib().vc_baseline_records(ds.handle, 1, _lib.ptr(x), _lib.ptr(st), _lib.C.byref(p),
                                               _lib.ptr(est), None, _lib.ptr(smp), None))
+    if isinstance(rng_seed, np.random.Generator):  # default_rng(gen) hands back gen itself
+        gen.bit_generator.advance(int(draws[0]))
     out = []
     for k, kind in enumerate(("single", "multiple")):
         out.append(BaselineEstimate(value=est[k, :3].copy(), grad=est[k, 3:].reshape(3, d).copy(),

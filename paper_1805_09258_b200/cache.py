@@ -16,8 +16,23 @@ from . import _lib
 from .records import CacheRecord, device_scene, record_size
 
 
+def _pack(recs, d: int) -> np.ndarray:
+    """Record objects → packed rows (N, d + 3 + 3d + d² + d)."""
+    if not recs:
+        return np.zeros((0, record_size(d)))
+    return np.ascontiguousarray(np.stack([np.concatenate([
+        np.asarray(r.position, float), np.asarray(r.value, float), np.asarray(r.grad, float).ravel(),
+        np.asarray(r.axes, float).ravel(), np.asarray(r.radii, float)]) for r in recs]))
+
+
 class RadianceCache:
-    """Records + exact point-query index (src/cache.py:262-334)."""
+    """Records + exact point-query index (src/cache.py:262-334).
+
+    Inserts are appended to the device copy lazily: the next lookup uploads only the
+    records inserted since the last one (vc_cache_insert) and re-indexes on the device,
+    so the reference's one-insert-per-miss loop (src/renderer.py:313-318) stays O(new)
+    on the host.
+    """
 
     MAX_DEPTH = 16
 
@@ -31,7 +46,8 @@ class RadianceCache:
         self.bounds_min = np.ascontiguousarray(bmin)
         self.bounds_max = np.ascontiguousarray(bmax)
         self.dim = bmin.size
-        self._records: list = []
+        self._records: list | None = []  # host record objects (None: held on the device only)
+        self._synced = 0                  # records [0, _synced) are in the device cache
         self._handle = None
         self._fin = None
 
@@ -40,25 +56,34 @@ class RadianceCache:
         """Wrap a device cache built by the library (vc_populate); records download lazily."""
         c = cls(bounds_min, bounds_max)
         c._records = None
-        c._handle = handle
-        c._fin = weakref.finalize(c, _lib.lib().vc_cache_destroy, handle)
+        c._set_handle(handle)
+        c._synced = int(_lib.lib().vc_cache_size(handle))
         return c
+
+    def _set_handle(self, h) -> None:
+        self._handle = h
+        self._fin = weakref.finalize(self, _lib.lib().vc_cache_destroy, h)
 
     def _device_changed(self) -> None:
         """The device cache grew in place (render with frozen=False): re-read lazily."""
         self._records = None
+        self._synced = int(_lib.lib().vc_cache_size(self._handle))
 
     def _host_records(self) -> list:
         if self._records is None:
-            L = _lib.lib()
-            n = int(L.vc_cache_size(self._handle))
-            rows = np.zeros((n, record_size(self.dim)))
-            if n:
-                _lib.check(L.vc_cache_records(self._handle, _lib.ptr(rows), None, _lib.VC_MEM_HOST, None))
+            rows = self._device_rows()
             from .records import unpack_record
 
             self._records = [unpack_record(r, self.dim) for r in rows]
         return self._records
+
+    def _device_rows(self) -> np.ndarray:
+        L = _lib.lib()
+        n = int(L.vc_cache_size(self._handle))
+        rows = np.zeros((n, record_size(self.dim)))
+        if n:
+            _lib.check(L.vc_cache_records(self._handle, _lib.ptr(rows), None, _lib.VC_MEM_HOST, None))
+        return rows
 
     def __len__(self) -> int:
         if self._records is None:
@@ -73,7 +98,6 @@ class RadianceCache:
         if np.asarray(record.position).size != self.dim:
             raise ValueError("record dimensionality does not match the cache")
         self._host_records().append(record)
-        self._invalidate()
 
     def extend_packed(self, packed: np.ndarray) -> None:
         """Insert many records given as packed rows (N, d + 3 + 3d + d² + d)."""
@@ -82,32 +106,55 @@ class RadianceCache:
         recs = self._host_records()
         for row in np.asarray(packed, float).reshape(-1, record_size(self.dim)):
             recs.append(unpack_record(row, self.dim))
-        self._invalidate()
 
-    def _invalidate(self):
+    def clear(self) -> None:
+        """Drop every record (host and device)."""
         if self._fin is not None:
             self._fin()
         self._handle = None
         self._fin = None
+        self._records = []
+        self._synced = 0
+
+    def device_rows(self):
+        """Packed rows as a CUDA float64 tensor (n, row) read on the device (no host copy)."""
+        import torch
+
+        h = self.handle()
+        n = int(_lib.lib().vc_cache_size(h))
+        out = torch.empty((n, record_size(self.dim)), dtype=torch.float64, device="cuda")
+        if n:
+            torch.cuda.synchronize()
+            _lib.check(_lib.lib().vc_cache_records(h, _lib.C.c_void_p(out.data_ptr()), None, 0, None))
+        return out
+
+    def insert_device_rows(self, rows, n: int) -> None:
+        """Append n packed rows that already sit in device memory (pointer or CUDA tensor),
+        e.g. records received over NCCL: no host round trip, host objects re-read lazily."""
+        h = self.handle()
+        ptr = rows.data_ptr() if hasattr(rows, "data_ptr") else int(rows)
+        _lib.check(_lib.lib().vc_cache_insert(h, int(n), _lib.C.c_void_p(ptr), 0, None))
+        self._records = None
+        self._synced += int(n)
 
     def packed(self) -> np.ndarray:
-        d = self.dim
-        recs = self._host_records()
-        if not recs:
-            return np.zeros((0, record_size(d)))
-        return np.ascontiguousarray(np.stack([np.concatenate([
-            np.asarray(r.position, float), np.asarray(r.value, float), np.asarray(r.grad, float).ravel(),
-            np.asarray(r.axes, float).ravel(), np.asarray(r.radii, float)]) for r in recs]))
+        if self._records is None:
+            return self._device_rows()
+        return _pack(self._records, self.dim)
 
     def handle(self):
+        L = _lib.lib()
         if self._handle is None:
-            L = _lib.lib()
             recs = self.packed()
             h = _lib.C.c_void_p()
             _lib.check(L.vc_cache_create(self.dim, _lib.ptr(self.bounds_min), _lib.ptr(self.bounds_max),
                                          len(recs), _lib.ptr(recs) if len(recs) else None, _lib.C.byref(h)))
-            self._handle = h
-            self._fin = weakref.finalize(self, L.vc_cache_destroy, h)
+            self._set_handle(h)
+            self._synced = len(recs)
+        elif self._records is not None and len(self._records) > self._synced:
+            rows = _pack(self._records[self._synced:], self.dim)
+            _lib.check(L.vc_cache_insert(self._handle, len(rows), _lib.ptr(rows), _lib.VC_MEM_HOST, None))
+            self._synced = len(self._records)
         return self._handle
 
     def interpolate_many(self, X, log_space: bool = False):
@@ -126,20 +173,36 @@ class RadianceCache:
         return J, cnt
 
 
-_MIRRORS: dict = {}
+# Device mirrors of reference RadianceCache objects, dropped with them.  The reference
+# cache is append-only (src/cache.py:298-315): a mirror whose last mirrored record is
+# still in place only takes the new records; anything else is re-mirrored.
+_MIRRORS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _ref_records(cache) -> list:
+    recs = getattr(cache, "_records", None)
+    return recs if isinstance(recs, list) else list(cache.records)
 
 
 def _as_device_cache(cache) -> RadianceCache:
-    """Accept a reference RadianceCache too: mirror its records on the device (re-mirrored
-    when its record count changes, i.e. after inserts)."""
+    """Accept a reference RadianceCache too: mirror its records on the device."""
     if isinstance(cache, RadianceCache):
         return cache
-    key = id(cache)
-    hit = _MIRRORS.get(key)
-    if hit is not None and hit[0] is cache and hit[1] == len(cache):
-        return hit[2]
-    dc = cache_from_records(cache.bounds_min, cache.bounds_max, cache.records)
-    _MIRRORS[key] = (cache, len(cache), dc)
+    recs = _ref_records(cache)
+    n = len(recs)
+    try:
+        hit = _MIRRORS.get(cache)
+    except TypeError:  # not weak-referenceable: no mirror kept
+        return cache_from_records(cache.bounds_min, cache.bounds_max, recs)
+    if hit is not None:
+        m, last, dc = hit
+        if n >= m and (m == 0 or recs[m - 1] is last):
+            if n > m:
+                dc._host_records().extend(cache_from_records(cache.bounds_min, cache.bounds_max, recs[m:])._records)
+                _MIRRORS[cache] = (n, recs[-1], dc)
+            return dc
+    dc = cache_from_records(cache.bounds_min, cache.bounds_max, recs)
+    _MIRRORS[cache] = (n, recs[-1] if n else None, dc)
     return dc
 
 

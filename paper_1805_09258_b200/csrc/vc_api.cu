@@ -42,6 +42,47 @@ void* Workspace::get(int slot, size_t bytes, cudaError_t* err) {
   return ptr[slot];
 }
 
+__global__ void k_outside(const double* x, long long N, int D, double3 lo, double3 hi, int* flag) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    bool out = false;
+    for (int a = 0; a < D; ++a) {
+      const double v = x[i * D + a];
+      const double l = a == 0 ? lo.x : (a == 1 ? lo.y : lo.z), h = a == 0 ? hi.x : (a == 1 ? hi.y : hi.z);
+      out |= !(v >= l && v <= h);  // NaN counts as outside, as on the host
+    }
+    if (out) atomicOr(flag, 1);
+  }
+}
+
+int check_inside(const vc_scene* sc, long long N, const double* x, bool host, const char* what,
+                 cudaStream_t st) {
+  const int D = sc->dim;
+  const double eps = 1e-12 * sc->scale;
+  if (host) {
+    for (long long i = 0; i < N; ++i)
+      for (int a = 0; a < D; ++a) {
+        const double v = x[(size_t)i * D + a];
+        if (!(v >= sc->bmin[a] - eps && v <= sc->bmax[a] + eps)) return fail(VC_EOUTSIDE, what);
+      }
+    return VC_OK;
+  }
+  static thread_local int* dflag = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (!dflag) e = cudaMalloc(&dflag, 4);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "bounds check");
+  const double3 lo = make_double3(sc->bmin[0] - eps, sc->bmin[1] - eps, sc->bmin[2] - eps);
+  const double3 hi = make_double3(sc->bmax[0] + eps, sc->bmax[1] + eps, sc->bmax[2] + eps);
+  const int grid = (int)std::min<long long>((N + 255) / 256, 4 * 148);
+  k_outside<<<grid, 256, 0, st>>>(x, N, D, lo, hi, dflag);
+  count_launches(1);
+  int h = 0;
+  e = cudaMemcpyAsync(&h, dflag, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "bounds check");
+  return h ? fail(VC_EOUTSIDE, what) : VC_OK;
+}
+
 Workspace::~Workspace() {
   for (int i = 0; i < kSlots; ++i)
     if (ptr[i]) cudaFree(ptr[i]);
@@ -345,14 +386,9 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
     }
   }
   if (D == 3) del_row_table(P);
-  if (host) {  // ValueError before any work (src/subdivision.py:155-158)
-    const double eps = 1e-12 * sc->scale;
-    for (int i = 0; i < N; ++i)
-      for (int a = 0; a < D; ++a) {
-        double v = x[(size_t)i * D + a];
-        if (!(v >= sc->bmin[a] - eps && v <= sc->bmax[a] + eps))
-          return fail(VC_EOUTSIDE, "subdivision center lies outside the medium bounds");
-      }
+  {  // ValueError before any work (src/subdivision.py:155-158), host and device inputs alike
+    const int rc = check_inside(sc, N, x, host, "subdivision center lies outside the medium bounds", st);
+    if (rc) return rc;
   }
   int rc = ensure_emitters(sc, prm->n_light_samples);
   if (rc) return rc;
@@ -572,14 +608,26 @@ int vc_profile_read(double* ms, int64_t* launches, int max_classes) {
 // per group a grid of cells 1/16 of the mean triangle box over the triangles'
 // in-plane boxes, each padded by 1e-5·scale — far beyond the distance (≤ 1e-6·scale for
 // rays at ≥ 1e-3 of grazing) between the plane point a ray lands on and the point of a
-// triangle the float64 hit test accepts.  Returns false when the emitters need more planes.
+// triangle the float64 hit test accepts.  Returns false when the emitters need more planes,
+// or when an emitter vertex lies outside the bounds padded by 0.005·scale: the grid walk
+// skips landings beyond 1.01·scale (any hit from a point of the medium on an emitter inside
+// the bounds is nearer), and the float32 gather pre-filter's error bounds assume plane
+// offsets and grid origins of magnitude ≲ scale about the bounds centre.
 static bool build_emit_planes(const std::vector<double>& prim, const std::vector<int>& order, double scale,
-                              vc::EmitPlanes* ep, std::vector<int>* start, std::vector<int>* tri,
-                              std::vector<unsigned>* occ) {
+                              const double* bmin, const double* bmax, vc::EmitPlanes* ep,
+                              std::vector<int>* start, std::vector<int>* tri, std::vector<unsigned>* occ) {
   using vc::kEmitPlanes;
   *ep = vc::EmitPlanes{};
   const int K = (int)order.size();
   if (K == 0) return false;
+  for (int k = 0; k < K; ++k) {
+    const double* P = &prim[(size_t)order[k] * 9];
+    for (int v = 0; v < 3; ++v)
+      for (int a = 0; a < 3; ++a) {
+        const double x = P[a] + (v == 1 ? P[3 + a] : 0.0) + (v == 2 ? P[6 + a] : 0.0);
+        if (!(x >= bmin[a] - 5e-3 * scale && x <= bmax[a] + 5e-3 * scale)) return false;
+      }
+  }
   std::vector<int> grp(K);
   int ng = 0;
   for (int k = 0; k < K; ++k) {
@@ -822,7 +870,7 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     if (sc->emit.K) cudaMemcpy(eorder.data(), sc->emit.prim_id, eorder.size() * 4, cudaMemcpyDeviceToHost);
     std::vector<int> start, tri;
     std::vector<unsigned> occ;
-    if (build_emit_planes(prim, eorder, sc->scale, &sc->ep, &start, &tri, &occ)) {
+    if (build_emit_planes(prim, eorder, sc->scale, sc->bmin, sc->bmax, &sc->ep, &start, &tri, &occ)) {
       up((void**)&sc->d_ep_start, start.data(), start.size() * 4);
       up((void**)&sc->d_ep_tri, tri.data(), tri.size() * 4);
       up((void**)&sc->d_ep_occ, occ.data(), occ.size() * 4);

@@ -35,6 +35,11 @@ int cuda_fail(cudaError_t e, const char* where);
 bool grid_shape_3d(int n, int* rows, int* cols);
 void count_launches(long long n);
 const unsigned long long* jump_tables(cudaError_t* err);
+// scene.contains for every point (src/scene.py:212-219): host arrays are checked on the
+// host; device arrays by one flag kernel and a 4-byte readback (synchronises `st`).
+// Returns VC_OK or VC_EOUTSIDE (with `what` as the message) / a CUDA error.
+int check_inside(const vc_scene* sc, long long N, const double* x, bool host, const char* what,
+                 cudaStream_t st);
 
 }  // namespace vc
 

@@ -94,7 +94,7 @@ __host__ __device__ constexpr int bl_comps() {
 template <int D>
 __global__ void __launch_bounds__(kBlBS) k_baseline(DevScene S, BaselineParams BP, const double* X,
                                                    const uint64_t* rng, JumpTables jt, double* partial,
-                                                   double* samples) {
+                                                   double* samples, int* max_coll) {
   constexpr int NC = bl_comps<D>();
   __shared__ double sm[NC][kBlBS + 1];
   const int rec = blockIdx.y;
@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(kBlBS) k_baseline(DevScene S, BaselineParams B
         pos[a] = x[a];
         cur_d[a] = d[a];
       }
-      for (int b = 0; b < BP.n_bounce; ++b) {
+      int b = 0;
+      for (; b < BP.n_bounce; ++b) {
         const unsigned long long base = n_dir_draws + (unsigned long long)b * per_bounce;
         Pcg64 gt = g0;
         pcg_advance(gt, base + (unsigned long long)i, jt);
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kBlBS) k_baseline(DevScene S, BaselineParams B
         for (int a = 0; a < D; ++a) cur_d[a] = nd[a];
         cur_s = s2;
       }
+      if (b > 0) atomicMax(max_coll + rec, b);  // collisions along this path
     }
     // luminance value and gradient norm per kind (src/subdivision.py:512-521)
 #pragma unroll
@@ -225,12 +227,24 @@ __global__ void __launch_bounds__(kBlBS) k_baseline(DevScene S, BaselineParams B
 // means, record rows (position, value, grad, I, radius·1) per kind
 template <int D>
 __global__ void k_baseline_final(DevScene S, BaselineParams BP, const double* X, const double* partial, int nblk,
-                                 int B, double alpha, double* est, double* records) {
+                                 int B, double alpha, double* est, double* records, const int* max_coll,
+                                 long long* draws) {
   constexpr int NC = bl_comps<D>();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 2 * B) return;
   const int rec = t >> 1, k = t & 1;
   const int o = k * (3 + 3 * D + 2);
+  if (draws && k == 0) {
+    // the reference draws n collision distances per bounce it enters and n·(d − 1) direction
+    // doubles per bounce with a collision; it leaves the loop at the first bounce without one
+    const long long n = BP.P.n_angular;
+    long long c = n * (D == 3 ? 2 : 1);
+    if (S.sigma_t > 0.0 && S.sigma_s > 0.0 && BP.n_bounce > 0) {
+      const int m = max_coll[rec];
+      c += (long long)m * n * (D == 3 ? 3 : 2) + (m < BP.n_bounce ? n : 0);
+    }
+    draws[rec] = c;
+  }
   double sum[3 + 3 * D + 2];
   for (int c = 0; c < 3 + 3 * D + 2; ++c) sum[c] = 0.0;
   for (int b = 0; b < nblk; ++b)
@@ -276,14 +290,9 @@ int baseline_impl(vc_scene* sc, int N, const double* x, const void* rng, const v
   }
   BP.n_bounce = std::max(0, prm->max_media_bounces - 1);
   BP.fb = sc->sigma_s * (1.0 / (D == 2 ? 2.0 * 3.141592653589793 : 4.0 * 3.141592653589793));
-  if (host) {
-    const double eps = 1e-12 * sc->scale;
-    for (int i = 0; i < N; ++i)
-      for (int a = 0; a < D; ++a) {
-        double v = x[(size_t)i * D + a];
-        if (!(v >= sc->bmin[a] - eps && v <= sc->bmax[a] + eps))
-          return fail(VC_EOUTSIDE, "estimate center lies outside the medium bounds");
-      }
+  {
+    const int rc = check_inside(sc, N, x, host, "estimate center lies outside the medium bounds", st);
+    if (rc) return rc;
   }
   int rc = ensure_emitters(sc, prm->n_light_samples);
   if (rc) return rc;
@@ -303,6 +312,8 @@ int baseline_impl(vc_scene* sc, int N, const double* x, const void* rng, const v
   double* dest = (double*)ws.get(4, (size_t)B * 2 * ES * 8, &err);
   double* drec = (double*)ws.get(5, (size_t)B * 2 * RS * 8, &err);
   double* dsmp = (double*)ws.get(6, samples ? (size_t)B * 4 * n * 8 : 16, &err);
+  int* dmaxc = (int*)ws.get(7, (size_t)B * 4, &err);
+  long long* ddraws = (long long*)ws.get(8, (size_t)B * 8, &err);
   if (err != cudaSuccess) return cuda_fail(err, "baseline workspace");
   long long launches = 0;
   for (int w0 = 0; w0 < N; w0 += B) {
@@ -332,13 +343,18 @@ int baseline_impl(vc_scene* sc, int N, const double* x, const void* rng, const v
     double* e_out = (host || !est) ? dest : est + (size_t)w0 * 2 * ES;
     double* r_out = (host || !records) ? drec : records + (size_t)w0 * 2 * RS;
     double* s_out = !samples ? nullptr : (host ? dsmp : samples + (size_t)w0 * 4 * n);
+    long long* d_out = !prm->draws ? nullptr : (host ? ddraws : (long long*)prm->draws + w0);
     dim3 grid(nblk, b);
+    err = cudaMemsetAsync(dmaxc, 0, (size_t)b * 4, st);
+    if (err != cudaSuccess) return cuda_fail(err, "baseline memset");
     if (D == 2) {
-      k_baseline<2><<<grid, kBlBS, 0, st>>>(S, BP, xin, rin, jt, part, s_out);
-      k_baseline_final<2><<<(2 * b + 127) / 128, 128, 0, st>>>(S, BP, xin, part, nblk, b, prm->alpha, e_out, r_out);
+      k_baseline<2><<<grid, kBlBS, 0, st>>>(S, BP, xin, rin, jt, part, s_out, dmaxc);
+      k_baseline_final<2><<<(2 * b + 127) / 128, 128, 0, st>>>(S, BP, xin, part, nblk, b, prm->alpha, e_out, r_out,
+                                                              dmaxc, d_out);
     } else {
-      k_baseline<3><<<grid, kBlBS, 0, st>>>(S, BP, xin, rin, jt, part, s_out);
-      k_baseline_final<3><<<(2 * b + 127) / 128, 128, 0, st>>>(S, BP, xin, part, nblk, b, prm->alpha, e_out, r_out);
+      k_baseline<3><<<grid, kBlBS, 0, st>>>(S, BP, xin, rin, jt, part, s_out, dmaxc);
+      k_baseline_final<3><<<(2 * b + 127) / 128, 128, 0, st>>>(S, BP, xin, part, nblk, b, prm->alpha, e_out, r_out,
+                                                              dmaxc, d_out);
     }
     launches += 2;
     err = cudaGetLastError();
@@ -349,6 +365,8 @@ int baseline_impl(vc_scene* sc, int N, const double* x, const void* rng, const v
         err = cudaMemcpyAsync(records + (size_t)w0 * 2 * RS, drec, (size_t)b * 2 * RS * 8, cudaMemcpyDeviceToHost, st);
       if (err == cudaSuccess && samples)
         err = cudaMemcpyAsync(samples + (size_t)w0 * 4 * n, dsmp, (size_t)b * 4 * n * 8, cudaMemcpyDeviceToHost, st);
+      if (err == cudaSuccess && prm->draws)
+        err = cudaMemcpyAsync((long long*)prm->draws + w0, ddraws, (size_t)b * 8, cudaMemcpyDeviceToHost, st);
       if (err == cudaSuccess) err = cudaStreamSynchronize(st);
       if (err != cudaSuccess) return cuda_fail(err, "baseline download");
     }

@@ -391,7 +391,9 @@ struct Toward {
 };
 
 // Float32 pre-filter of the gather rays (3D, emitter plane grids with occupancy): could the
-// ray with draws (u0, u1) from the media sample y meet an emitter triangle?  The direction
+// ray with draws (u0, u1) from the media sample y meet an emitter triangle?  Every position
+// (sample point, plane offsets, grid origins) is taken relative to the bounds centre in
+// float64 before rounding, so magnitudes stay ≲ scale wherever the scene sits.  The direction
 // and the landing point on each emitter plane are computed in float32 with a bound on
 // their error against the float64 values (y: ≤ ey = 2e-6·scale; direction components:
 // ≤ ed = 2e-6, from z = 1 − 2u0 and sin θ = 2√(u0(1 − u0)) taken from float64 and
@@ -467,9 +469,16 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
     if (threadIdx.x < S.ep.ng) {
       const int g = threadIdx.x;
       const EmitPlanes& E = S.ep;
-      fplane[g].nc = make_float4((float)E.n[g][0], (float)E.n[g][1], (float)E.n[g][2], (float)E.c[g]);
-      fplane[g].a1 = make_float4((float)E.a1[g][0], (float)E.a1[g][1], (float)E.a1[g][2], (float)E.lo[g][0]);
-      fplane[g].a2 = make_float4((float)E.a2[g][0], (float)E.a2[g][1], (float)E.a2[g][2], (float)E.lo[g][1]);
+      // offsets and grid origins relative to the bounds centre (float64, then rounded)
+      double ctr[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) ctr[a] = 0.5 * (S.bmin[a] + S.bmax[a]);
+      auto dotc = [&](const double* v) { return v[0] * ctr[0] + v[1] * ctr[1] + v[2] * ctr[2]; };
+      fplane[g].nc = make_float4((float)E.n[g][0], (float)E.n[g][1], (float)E.n[g][2], (float)(E.c[g] - dotc(E.n[g])));
+      fplane[g].a1 = make_float4((float)E.a1[g][0], (float)E.a1[g][1], (float)E.a1[g][2],
+                                 (float)(E.lo[g][0] - dotc(E.a1[g])));
+      fplane[g].a2 = make_float4((float)E.a2[g][0], (float)E.a2[g][1], (float)E.a2[g][2],
+                                 (float)(E.lo[g][1] - dotc(E.a2[g])));
       fplane[g].cc = make_float4((float)E.occ_inv[g][0], (float)E.occ_inv[g][1], __int_as_float(E.occ_w[g]),
                                  __int_as_float(E.occ_h[g]));
     }
@@ -487,8 +496,12 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
   const int lane = threadIdx.x & 31;
   PendSample* pend = pend_all[threadIdx.x >> 5];
   double x[3] = {0.0, 0.0, 0.0};
+  float xr[3] = {0.0f, 0.0f, 0.0f};  // the filter's sample origin relative to the bounds centre
 #pragma unroll
-  for (int c = 0; c < D; ++c) x[c] = W.x[rec * D + c];
+  for (int c = 0; c < D; ++c) {
+    x[c] = W.x[rec * D + c];
+    xr[c] = (float)(x[c] - 0.5 * (S.bmin[c] + S.bmax[c]));
+  }
   const uint64_t* st = W.rng + 4 * rec;
   const double tol = 1e-5 * S.scale;
   const Toward toward(S.ep);
@@ -611,7 +624,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
             // the filter's float32 sample point (error ≤ f_ey against origin())
             const float4 dk = W.dirs32[(size_t)rec * n + k];
             const float ri = ((float)i + 0.5f) * f_step;
-            const float y32[3] = {(float)x[0] + ri * dk.x, (float)x[1] + ri * dk.y, (float)x[2] + ri * dk.z};
+            const float y32[3] = {xr[0] + ri * dk.x, xr[1] + ri * dk.y, xr[2] + ri * dk.z};
             keep = emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
           } else {
             double y[3];

@@ -514,6 +514,26 @@ int vc_cache_create(int dim, const double* bmin, const double* bmax, int n, cons
 
 void vc_cache_destroy(vc_cache* c) { delete c; }
 
+int vc_cache_insert(vc_cache* c, int n, const double* records, int flags, void* stream) {
+  if (!c) return fail(VC_EINVAL, "null cache");
+  if (n < 0) return fail(VC_EINVAL, "negative record count");
+  if (n == 0) return VC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t RS = record_size(c->dim);
+  int rc = cache_reserve(c, (size_t)c->n + n, st);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(c->d_rec + (size_t)c->n * RS, records, (size_t)n * RS * 8,
+                                  (flags & VC_MEM_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cache insert upload");
+  k_fill_tags<<<(n + 255) / 256, 256, 0, st>>>(c->d_tag + c->n, n, -1LL);
+  count_launches(1);
+  c->n += n;
+  rc = cache_rebuild(c, st);
+  if (rc) return rc;
+  e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? VC_OK : cuda_fail(e, "cache insert");
+}
+
 int vc_cache_set_blend(vc_cache* c, int log_space) {
   if (!c) return fail(VC_EINVAL, "null cache");
   c->blend = log_space ? 1 : 0;

@@ -416,8 +416,9 @@ __device__ __forceinline__ void nearest_emitter(const DevScene& S, const double*
           break;
         }
         // the landing distance only picks the grid cell: a float32 reciprocal (≤ 1e-7
-        // relative) keeps it within 1e-7·scale for the distances that matter (a point of the
-        // scene lies within `scale` of the origin), far inside the cells' 1e-5·scale padding
+        // relative) keeps it within ~1e-7·scale for the distances that matter (|tp| ≤ 1.01·scale:
+        // the planes are built only for emitters inside the bounds, so a hit from a point of
+        // the medium is nearer), far inside the cells' 1e-5·scale padding
         float rdn;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rdn) : "f"((float)dn));
         const double tp = (E.c[g] - (E.n[g][0] * o[0] + E.n[g][1] * o[1] + E.n[g][2] * o[2])) * (double)rdn;

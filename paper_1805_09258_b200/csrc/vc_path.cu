@@ -146,14 +146,9 @@ int path_impl(vc_scene* sc, int m, const double* x, const void* rng, long long n
   const int D = sc->dim;
   const bool host = flags & VC_MEM_HOST;
   const bool words = flags & VC_SEED_WORDS;
-  if (host) {  // scene.contains (src/transport.py:337-338, src/scene.py:212-219)
-    const double eps = 1e-12 * sc->scale;
-    for (int i = 0; i < m; ++i)
-      for (int a = 0; a < D; ++a) {
-        double v = x[(size_t)i * D + a];
-        if (!(v >= sc->bmin[a] - eps && v <= sc->bmax[a] + eps))
-          return fail(VC_EOUTSIDE, "query point lies outside the medium bounds");
-      }
+  {  // scene.contains (src/transport.py:337-338, src/scene.py:212-219)
+    const int rc = check_inside(sc, m, x, host, "query point lies outside the medium bounds", st);
+    if (rc) return rc;
   }
   int rc = ensure_emitters(sc, n_light_samples);
   if (rc) return rc;

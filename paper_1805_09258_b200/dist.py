@@ -75,26 +75,35 @@ def broadcast_cache_set(cache_set, src: int = 0, group=None):
     Used after a populate on one rank (the reference's sequential insertion order is
     what the lookup sums follow) before a sharded frozen render.  Records travel as
     packed float64 rows (position, value, grad, axes, radii): counts first, then rows.
+    Under NCCL the rows never leave the device: `src` reads them out of its device cache
+    (vc_cache_records), the broadcast runs over NVLink, and receivers append them to an
+    emptied device cache (vc_cache_insert) — no host record objects on either side.
     """
     import torch
     import torch.distributed as dist
 
+    from .records import record_size
+
     dev = _coll_device(group)
+    on_gpu = dev.type == "cuda"
+    me = dist.get_rank(group)
     for cache in (cache_set.single, cache_set.multiple):
-        rows = cache.packed() if dist.get_rank(group) == src else None
+        rows = None
+        if me == src:
+            rows = cache.device_rows() if on_gpu else torch.from_numpy(cache.packed())
         n = torch.tensor([0 if rows is None else rows.shape[0]], dtype=torch.int64, device=dev)
         dist.broadcast(n, src, group=group)
-        from .records import record_size
-
-        buf = torch.zeros((int(n.item()), record_size(cache.dim)), dtype=torch.float64, device=dev)
-        if rows is not None:
-            buf.copy_(torch.from_numpy(rows))
-        if buf.numel():
+        k = int(n.item())
+        buf = rows if rows is not None else torch.zeros((k, record_size(cache.dim)), dtype=torch.float64, device=dev)
+        if k:
             dist.broadcast(buf, src, group=group)
-        if dist.get_rank(group) != src:
-            cache._records = []
-            cache._invalidate()
-            cache.extend_packed(buf.cpu().numpy())
+        if me != src:
+            cache.clear()
+            if on_gpu:
+                torch.cuda.synchronize()
+                cache.insert_device_rows(buf, k)
+            else:
+                cache.extend_packed(buf.numpy())
     return cache_set
 
 
@@ -124,6 +133,8 @@ def render_sharded(scene, camera, settings, cache_set, *, renderer=None, group=N
     dev = _coll_device(group)
     full = all_gather_rows(torch.as_tensor(np.ascontiguousarray(slab), dtype=torch.float64).to(dev), group=group)
     cnt = torch.tensor([st["cache_hits"], st["direct_evaluations"]], dtype=torch.int64, device=dev)
+    if settings.mode == "path":  # render() reports no cache statistics in path mode (src/renderer.py:409-421)
+        cnt.zero_()
     dist.all_reduce(cnt, group=group)
     image = full.cpu().numpy().reshape(int(camera.height), int(camera.width), 3)
     return image, {"cache_hits": int(cnt[0]), "direct_evaluations": int(cnt[1]), "rows": (lo, hi)}

@@ -348,6 +348,8 @@ def render_rows(scene, camera: Camera, settings: RenderSettings, cache_set: Cach
         hs, hm = cache_set._handles()
         _lib.check(_lib.lib().vc_render(device_scene(scene).handle, hs, hm, _lib.C.byref(cam), _lib.C.byref(rp),
                                         _lib.ptr(image), _lib.ptr(out), _lib.VC_MEM_HOST, None))
+    if settings.mode == "path":  # path mode keeps no cache statistics (src/renderer.py:337-346)
+        out[:] = 0
     return image[row0:row0 + rows].copy(), {"cache_hits": int(out[0]), "direct_evaluations": int(out[1])}
 
 

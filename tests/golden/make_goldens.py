@@ -546,6 +546,37 @@ def gen_baseline():
     np.savez_compressed(OUT / "baseline.npz", **out)
 
 
+def gen_baseline_rng():
+    """baseline_estimate called twice on ONE Generator (src/subdivision.py:431): the second
+    call sees the stream the first left behind, and the draw after both pins how many
+    doubles the reference consumed (its collision loop stops at the first bounce without a
+    collision, src/subdivision.py:480-486)."""
+    bundled = Path("/root/reference/pkg/scenes")
+    pen = vscene.load_scene(bundled / "penumbra2d.json")
+    box = vscene.load_scene(bundled / "box3d.json")
+    out = {"versions": VERSIONS}
+    out.update(scene_fields("pen_", pen))
+    out.update(scene_fields("box_", box))
+    cases = {  # name: (prefix, scene, points, n, max_media_bounces, generator seed)
+        "pen": ("pen_", pen, np.array([[0.15, 0.6], [0.3, 0.45]]), 256, 2, 71),
+        "pen6": ("pen_", pen, np.array([[0.5, 0.35], [0.7, 0.7]]), 64, 6, 72),
+        "box": ("box_", box, np.array([[0.5, 0.5, 0.5], [0.2, 0.7, 0.3]]), 512, 3, 73),
+        "box9": ("box_", box, np.array([[0.4, 0.3, 0.6]]), 16, 9, 74),
+    }
+    for name, (prefix, sc, pts, n, mmb, gs) in cases.items():
+        g = np.random.default_rng(gs)
+        vals = []
+        for x in pts:
+            s_, m_ = vs.baseline_estimate(sc, x, n_angular=n, rng_seed=g, max_media_bounces=mmb, n_light_samples=4)
+            vals.append([np.concatenate([s_.value, s_.grad.ravel()]), np.concatenate([m_.value, m_.grad.ravel()])])
+        out[f"{name}_prefix"] = np.array(prefix)
+        out[f"{name}_points"] = pts
+        out[f"{name}_params"] = np.array([n, mmb, gs])
+        out[f"{name}_est"] = np.array(vals)
+        out[f"{name}_next"] = np.array(g.random())
+    np.savez_compressed(OUT / "baseline_rng.npz", **out)
+
+
 def gen_path():
     """path_trace_radiance / fd_derivatives / render mode "path" through the reference
     (src/transport.py:318-391, src/renderer.py:337-346, :590-643)."""
@@ -658,6 +689,8 @@ if __name__ == "__main__":
         gen_io()
     if "baseline" in which:
         gen_baseline()
+    if "baseline_rng" in which:
+        gen_baseline_rng()
     if "path" in which:
         gen_path()
     if "grow" in which:

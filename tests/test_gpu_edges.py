@@ -1,0 +1,180 @@
+"""Edge cases of the device path that the round-1 review found unguarded.
+
+* points outside the medium bounds passed as CUDA tensors raise ValueError like the host
+  path (src/subdivision.py:155-158) instead of overrunning the ring buffers;
+* the float32 emitter pre-filter keeps exact media radiance for a scene far from the
+  origin (positions are taken relative to the bounds centre);
+* a Generator passed to baseline_estimate is advanced like the reference's
+  (golden: tests/golden/baseline_rng.npz, two calls on one Generator);
+* RadianceCache inserts reach the device incrementally (vc_cache_insert) with the same
+  lookups as a cache built in one go; reference caches are mirrored weakly and
+  incrementally.
+"""
+
+from __future__ import annotations
+
+import gc
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, golden_scene, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def test_device_tensor_outside_bounds_raises():
+    import torch
+
+    from paper_1805_09258_b200 import configs, estimate_moments_batch, seed_words
+    from paper_1805_09258_b200.baseline import baseline_records_batch
+
+    w = configs.cfg2()
+    X = np.array(w.points[:8])
+    X[5] = [0.5, 7.5, 0.5]  # far outside: would need ~70 more rings than allocated
+    Xd = torch.tensor(X, device="cuda")
+    S = torch.tensor(seed_words(w.seed, 401, range(8)).astype(np.int32), device="cuda")
+    with pytest.raises(ValueError, match="outside the medium bounds"):
+        estimate_moments_batch(w.scene, Xd, seeds=S, n_angular=256, march_step=0.1)
+    with pytest.raises(ValueError, match="outside the medium bounds"):
+        estimate_moments_batch(w.scene, X, seeds=seed_words(w.seed, 401, range(8)), n_angular=256, march_step=0.1)
+    with pytest.raises(ValueError):
+        baseline_records_batch(w.scene, X, seed_words(w.seed, 401, range(8)), n_angular=64)
+    Xd[5, 1] = float("nan")
+    with pytest.raises(ValueError):
+        estimate_moments_batch(w.scene, Xd, seeds=S, n_angular=256, march_step=0.1)
+    # on the bounds face (±1e-12·scale) is inside, on the device path too
+    Xd[5] = torch.tensor([0.5, 1.0, 0.5], dtype=torch.float64)
+    r = estimate_moments_batch(w.scene, Xd, seeds=S, n_angular=256, march_step=0.1)
+    torch.cuda.synchronize()
+    assert np.all(np.isfinite(r.moments.cpu().numpy()))
+
+
+_TRANSLATED = (
+    "import numpy as np, sys; sys.path.insert(0, '.');"
+    "from paper_1805_09258_b200 import configs, inspect_record;"
+    "from paper_1805_09258_b200.scene import Scene, Surface;"
+    "w = configs.cfg3(); T = np.array([1000.0, -2000.0, 1500.0]);"
+    "sc = Scene(tuple(Surface(s.vertices + T, s.emission, s.albedo) for s in w.scene.surfaces),"
+    " w.scene.medium, w.scene.bounds_min + T, w.scene.bounds_max + T); out = [];"
+    "[out.append(inspect_record(sc, w.points[i] + T, rng_seed=np.random.SeedSequence([w.seed, 401, i]),"
+    " n_angular=4096, march_step=w.march_step)['media'].reshape(-1)) for i in range(3)];"
+    "np.save(sys.argv[1], np.concatenate(out))"
+)
+
+
+def test_gather_prefilter_exact_far_from_origin():
+    """cfg3 translated by (1000, −2000, 1500): per-sample media radiance with the float32
+    pre-filter equals the unfiltered gather bit for bit (the filter works in coordinates
+    relative to the bounds centre, so its error radius holds wherever the scene sits)."""
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    env = dict(os.environ)
+    env.pop("VOLCACHE_EMIT_FILTER", None)
+    subprocess.run([sys.executable, "-c", _TRANSLATED, str(out / "tr_on.npy")], check=True, cwd=ROOT, env=env)
+    env["VOLCACHE_EMIT_FILTER"] = "0"
+    subprocess.run([sys.executable, "-c", _TRANSLATED, str(out / "tr_off.npy")], check=True, cwd=ROOT, env=env)
+    on, off = np.load(out / "tr_on.npy"), np.load(out / "tr_off.npy")
+    assert on.size > 100000 and np.count_nonzero(on) > 1000
+    np.testing.assert_array_equal(on, off)
+
+
+@pytest.mark.parametrize("name", ["pen", "pen6", "box", "box9"])
+def test_baseline_generator_advanced_like_reference(name):
+    from paper_1805_09258_b200.baseline import baseline_estimate
+
+    z = golden("baseline_rng")
+    sc = golden_scene(z, str(z[f"{name}_prefix"]))
+    n, mmb, gs = (int(v) for v in z[f"{name}_params"])
+    g = np.random.default_rng(gs)
+    for i, x in enumerate(z[f"{name}_points"]):
+        s, m = baseline_estimate(sc, x, n_angular=n, rng_seed=g, max_media_bounces=mmb, n_light_samples=4)
+        for k, est in enumerate((s, m)):
+            want = z[f"{name}_est"][i][k]
+            got = np.concatenate([est.value, est.grad.ravel()])
+            assert rel_l2(got, want, floor=1e-300) <= 1e-9
+    assert g.random() == float(z[f"{name}_next"])
+
+
+def _records(d, n, rng):
+    from paper_1805_09258_b200.records import CacheRecord
+
+    out = []
+    for _ in range(n):
+        q, _ = np.linalg.qr(rng.normal(size=(d, d)))
+        out.append(CacheRecord(rng.uniform(0, 1, d), rng.uniform(0, 2, 3), rng.normal(size=(3, d)), q,
+                               rng.uniform(0.05, 0.3, d)))
+    return out
+
+
+def test_incremental_insert_equals_bulk_build():
+    from paper_1805_09258_b200.cache import RadianceCache, cache_from_records
+
+    rng = np.random.default_rng(5)
+    recs = _records(3, 300, rng)
+    q = rng.uniform(0, 1, (2000, 3))
+    bulk = cache_from_records(np.zeros(3), np.ones(3), recs)
+    Jb, cb = bulk.interpolate_many(q)
+    inc = RadianceCache(np.zeros(3), np.ones(3))
+    for k, r in enumerate(recs):  # the reference's one-insert-per-miss pattern, with lookups between
+        inc.insert(r)
+        if k % 37 == 0:
+            inc.interpolate_many(q[:10])
+    h = inc.handle()
+    Ji, ci = inc.interpolate_many(q)
+    assert inc.handle() is h  # appended in place, never rebuilt from the host
+    np.testing.assert_array_equal(ci, cb)
+    np.testing.assert_array_equal(Ji, Jb)
+    np.testing.assert_array_equal(inc.packed(), bulk.packed())
+
+
+def test_reference_cache_mirror_is_incremental_and_weak():
+    from paper_1805_09258_b200 import cache as C
+
+    class RefCache:  # duck-typed reference RadianceCache (src/cache.py:262-296)
+        def __init__(self):
+            self.bounds_min, self.bounds_max, self.dim, self._records = np.zeros(3), np.ones(3), 3, []
+
+        def __len__(self):
+            return len(self._records)
+
+        @property
+        def records(self):
+            return list(self._records)
+
+    rng = np.random.default_rng(6)
+    recs = _records(3, 120, rng)
+    q = rng.uniform(0, 1, (500, 3))
+    ref = RefCache()
+    ref._records.extend(recs[:60])
+    J1 = [C.interpolate(ref, x) for x in q[:5]]
+    dc = C._as_device_cache(ref)
+    h = dc.handle()
+    ref._records.extend(recs[60:])
+    assert C._as_device_cache(ref) is dc  # same mirror, new records appended
+    J2, c2 = dc.interpolate_many(q)
+    assert dc.handle() is h
+    Jb, cb = C.cache_from_records(np.zeros(3), np.ones(3), recs).interpolate_many(q)
+    np.testing.assert_array_equal(J2, Jb)
+    np.testing.assert_array_equal(c2, cb)
+    # a record replaced in place → re-mirrored, not served stale
+    ref._records[-1] = recs[0]
+    assert C._as_device_cache(ref) is not dc
+    assert len(J1) == 5
+    n_before = len(C._MIRRORS)
+    del ref, dc
+    gc.collect()
+    assert len(C._MIRRORS) == n_before - 1
