@@ -188,6 +188,188 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# cfg5: populate + frozen camera march over ~100k records (the dependent step)
+# ---------------------------------------------------------------------------
+
+CFG5_EPS = float(os.environ.get("VOLCACHE_CFG5_EPS", "3e-5"))  # ~96k records at 1920x1080, step 0.01
+REC_BYTES_MODEL = 108  # fp32 record: pos 12, value 12, grad 36, axes 36, radii 12
+
+
+def cfg5_setup(width=1920, height=1080, step=0.01, eps=None):
+    from paper_1805_09258_b200 import configs
+    from paper_1805_09258_b200.renderer import Camera, RenderSettings
+
+    sc = configs.cfg3_scene()
+    c = configs.cfg5_camera(width, height)
+    cam = Camera(position=c["position"], look_at=c["look_at"], up=c["up"], fov_degrees=c["fov"], width=width,
+                 height=height)
+    st = RenderSettings(mode="ours-aniso", epsilon=CFG5_EPS if eps is None else eps, spp=1, march_step=step,
+                        n_angular=16384, seed=5, frozen=True)
+    return sc, cam, st
+
+
+def cfg5_march_points(scene, cam, step, rows, cols):
+    """Pixel-centre march points of a pixel window (src/renderer.py:290-299), host float64."""
+    from paper_1805_09258_b200 import _lib
+
+    r0, nr = rows
+    c0, nc = cols
+    py, px = np.meshgrid(np.arange(r0, r0 + nr), np.arange(c0, c0 + nc), indexing="ij")
+    pos = np.asarray(cam.position, float)
+    fwd = np.asarray(cam.look_at, float) - pos
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, cam.up)
+    right /= np.linalg.norm(right)
+    up = np.cross(right, fwd)
+    th = np.tan(np.radians(cam.fov_degrees) / 2)
+    asp = cam.width / cam.height
+    u = (px.ravel() + 0.5) / cam.width
+    v = (py.ravel() + 0.5) / cam.height
+    d = fwd[None] + ((2 * u - 1) * th * asp)[:, None] * right[None] + ((1 - 2 * v) * th)[:, None] * up[None]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = np.broadcast_to(pos, d.shape).copy()
+    ds = __import__("paper_1805_09258_b200").device_scene(scene)
+    m = len(d)
+    t = np.zeros(m)
+    idx = np.zeros(m, np.int32)
+    _lib.check(_lib.lib().vc_trace(ds.handle, m, _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), _lib.ptr(idx),
+                                   _lib.VC_MEM_HOST, None))
+    bmin, bmax = np.asarray(scene.bounds_min, float), np.asarray(scene.bounds_max, float)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t1, t2 = (bmin - o) / d, (bmax - o) / d
+    t_in = np.maximum(np.nanmax(np.minimum(t1, t2), axis=1), 0.0)
+    t_out = np.nanmin(np.maximum(t1, t2), axis=1)
+    t_end = np.minimum(t, t_out)
+    n = np.maximum(np.floor((t_end - t_in) / step + 0.5), 0).astype(int)
+    pts = [o[i] + (t_in[i] + (np.arange(1, n[i] + 1) - 0.5) * step)[:, None] * d[i] for i in range(m)]
+    return np.concatenate(pts) if pts else np.zeros((0, 3)), int(n.sum())
+
+
+def run_cfg5(args):
+    import torch
+
+    from paper_1805_09258_b200 import _lib, device_scene
+    from paper_1805_09258_b200.renderer import _render_params, populate_cache
+
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("cfg5 bench runs one GPU (multi-GPU populate: dist.populate_sharded)")
+    torch.cuda.set_device(local)
+    sc, cam, st = cfg5_setup(eps=args.cfg5_eps)
+    ds = device_scene(sc)
+    L = _lib.lib()
+    # warm the scene (BVH, emitter quadrature) with a tiny populate
+    from paper_1805_09258_b200.renderer import Camera
+
+    small = Camera(position=cam.position, look_at=cam.look_at, up=cam.up, fov_degrees=cam.fov_degrees, width=8,
+                   height=5)
+    populate_cache(sc, small, st)
+    torch.cuda.synchronize()
+    launches0 = L.vc_kernel_launches()
+    with ClockSampler(local) as clk_pop:
+        t0 = time.perf_counter()
+        cs, pst = populate_cache(sc, cam, st)
+        torch.cuda.synchronize()
+        pop_s = time.perf_counter() - t0
+    pop_launches = L.vc_kernel_launches() - launches0
+    n_rec = pst["records"]
+    # frozen march: device image, inputs (caches, scene) resident
+    cam_c = cam._c()
+    rp = _render_params(sc, st)
+    hs, hm = cs._handles()
+    img = torch.zeros((cam.height, cam.width, 3), dtype=torch.float64, device="cuda")
+    out = np.zeros(2, np.int64)
+
+    def march(host_img=None):
+        ptr = _lib.ptr(host_img) if host_img is not None else _lib.C.c_void_p(img.data_ptr())
+        _lib.check(L.vc_render(ds.handle, hs, hm, _lib.C.byref(cam_c), _lib.C.byref(rp), ptr, _lib.ptr(out),
+                               _lib.VC_MEM_HOST if host_img is not None else 0, None))
+
+    for _ in range(args.warmup):
+        march()
+    torch.cuda.synchronize()
+    L.vc_profile(1)
+    launches0 = L.vc_kernel_launches()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            march()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = L.vc_kernel_launches() - launches0
+    kms = np.zeros(12)
+    kcnt = np.zeros(12, np.int64)
+    L.vc_profile_read(_lib.ptr(kms), _lib.ptr(kcnt), 12)
+    L.vc_profile(0)
+    hits, misses = int(out[0]), int(out[1])
+    steps_total = hits + misses  # march points per frame
+    value = steps_total * args.steps / (ms / 1e3)
+    # e2e: the public render() call with a host image (D2H of the frame inside the timed region)
+    from paper_1805_09258_b200.renderer import render
+
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.e2e_steps)):
+        image_h, rst = render(sc, cam, st, cache_set=cs)
+    e2e_s = (time.perf_counter() - t0) / max(1, args.e2e_steps)
+    # covering records per lookup (single, multiple) on a sample of march points
+    sample, _ = cfg5_march_points(sc, cam, st.march_step, (0, cam.height), (0, cam.width)) \
+        if args.cfg5_full_sample else cfg5_march_points(sc, cam, st.march_step, (cam.height // 2 - 30, 60),
+                                                        (0, cam.width))
+    cov = []
+    for c in (cs.single, cs.multiple):
+        _, cnt = c.interpolate_many(sample)
+        cov.append(float(cnt.mean()))
+    names = _lib.KERNEL_CLASSES
+    march_ms = float(kms[names.index("march")])
+    n_march = int(kcnt[names.index("march")])
+    # algorithmic bytes per march point: single lookup (12 + Σcov·108 + 12) and, where covered,
+    # the multiple lookup; every point of the populated frame is covered by both caches
+    bpp = (24 + cov[0] * REC_BYTES_MODEL) + (24 + cov[1] * REC_BYTES_MODEL)
+    pk = peaks()
+    achieved = bpp * steps_total * args.steps / (march_ms / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("per_class", {}).get("march")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "cfg5 frozen camera-march lookups/s (1920x1080, step 0.01, ~100k records)",
+        "value": value, "unit": "lookups/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded cfg3 room, cfg5 camera; no public dataset)",
+        "config": {"workload": "cfg5-camera-1920x1080", "width": cam.width, "height": cam.height,
+                   "march_step": st.march_step, "epsilon": st.epsilon, "n_angular": 16384, "spp": 1,
+                   "records": n_rec, "records_single": pst["records_single"],
+                   "records_multiple": pst["records_multiple"], "march_points_per_frame": steps_total,
+                   "direct_evaluations_per_frame": misses,
+                   "pixel_steps_per_s": value, "mean_covering_single": cov[0], "mean_covering_multiple": cov[1],
+                   "l2": "no flush: the frame's record working set (2 caches) is L2-sized by design; "
+                         "the roofline below is against HBM",
+                   "populate": {"seconds": pop_s, "points_marched": pst["points_marched"],
+                                "records_per_s": n_rec / pop_s, "builds": pst["builds"],
+                                "builds_per_s": pst["builds"] / pop_s, "windows": pst["windows"],
+                                "discarded_builds": pst["discarded_builds"], "kernel_launches": int(pop_launches),
+                                "clocks": clk_pop.summary()}},
+        "roofline": {"bound": "hbm", "kernel": "march", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "bytes_per_march_point": bpp, "march_ms_per_frame": march_ms / max(args.steps, 1),
+                     "march_launches": n_march},
+        "e2e": {"value": steps_total / e2e_s, "unit": "lookups/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": cam.width * cam.height * 24},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
 
@@ -204,11 +386,15 @@ def main():
     ap.add_argument("--cpu-records", type=int, default=1, help="oracle records per CPU sample/step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cfg5-eps", type=float, default=None, help="cfg5: record-error target ε (default tuned)")
+    ap.add_argument("--cfg5-full-sample", action="store_true", help="cfg5: covering counts over the whole frame")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "cfg5":
+        return run_cfg5(args)
 
     import torch
     import torch.distributed as dist

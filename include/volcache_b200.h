@@ -108,6 +108,15 @@ int vc_build_inspect(vc_scene* scene, const double* x, const void* rng, const in
 int vc_make_records(int n, int dim, const double* x, const double* moments, double epsilon,
                     double scene_scale, double max_emission, int flags, double* records, void* stream);
 
+/* Per-element form factors with derivatives: ff_segment_derivs_batch (2D) /
+ * ff_triangle_derivs_batch (3D), src/formfactor.py:85-158, :298-343.  Element i has the
+ * point x[i] (m × d) and vertices verts[i] (m × d × d, vertex-major); outputs ok (m),
+ * value (m), grad (m × d), hess (m × d × d, symmetric); not-ok elements are zeros.
+ * precision 0: the float64 device functions of the record build; 1 (3D only): the
+ * float32 element path (ok-mask still decided in float64).  VC_MEM_HOST: host arrays. */
+int vc_form_factors(int dim, int m, const double* x, const double* verts, int precision, int flags,
+                    uint8_t* ok, double* value, double* grad, double* hess, void* stream);
+
 /* Nearest hit per ray: trace (src/scene.py:271-292; misses t = inf, idx = −1) or, with
  * VC_TRACE_BOUNDS, trace_or_bounds (src/scene.py:306-315; misses t = bounds exit).
  * o, d: m × dim float64; t: m float64; idx: m int32 (original surface index). */

@@ -19,7 +19,8 @@ LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libvolcache_b200.so"
 OBJ = PKG / "build"
 
-CU_SOURCES = ["vc_api.cu", "vc_build.cu", "vc_cache.cu", "vc_populate.cu", "vc_baseline.cu", "vc_path.cu"]
+CU_SOURCES = ["vc_api.cu", "vc_build.cu", "vc_cache.cu", "vc_populate.cu", "vc_baseline.cu", "vc_path.cu",
+              "vc_elements.cu"]
 CPP_SOURCES = ["vc_bvh.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + ARCH

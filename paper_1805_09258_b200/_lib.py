@@ -140,6 +140,7 @@ _SIGS = {
     "vc_cache_create": (C.c_int, [C.c_int, _vp, _vp, C.c_int, _vp, C.POINTER(_vp)]),
     "vc_cache_destroy": (None, [_vp]),
     "vc_cache_insert": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _vp]),
+    "vc_form_factors": (C.c_int, [C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "vc_cache_interpolate": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
     "vc_render": (C.c_int, [_vp, _vp, _vp, C.POINTER(Camera), C.POINTER(RenderParams), _vp, _vp, C.c_int, _vp]),
     "vc_cache_size": (C.c_int64, [_vp]),

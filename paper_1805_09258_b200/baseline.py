@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .io import BaselineRecord
+from .records import BaselineRecord
 from .records import DEFAULT_N_ANGULAR, device_scene, pcg64_state, record_size
 
 R_MAX_FRACTION = 0.25  # src/cache.py:30

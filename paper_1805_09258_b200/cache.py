@@ -50,6 +50,7 @@ class RadianceCache:
         self._synced = 0                  # records [0, _synced) are in the device cache
         self._handle = None
         self._fin = None
+        self.sphere_records = False  # device-only rows are BaselineRecord spheres (baseline mode)
 
     @classmethod
     def _adopt(cls, bounds_min, bounds_max, handle) -> "RadianceCache":
@@ -216,7 +217,7 @@ def interpolate(cache, x):
 
 
 def cache_from_records(bounds_min, bounds_max, records) -> RadianceCache:
-    from .io import BaselineRecord
+    from .records import BaselineRecord
 
     c = RadianceCache(bounds_min, bounds_max)
     for r in records:

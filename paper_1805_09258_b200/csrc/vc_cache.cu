@@ -6,6 +6,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
@@ -79,6 +80,59 @@ __global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, 
         vals[o] = r;
         ++o;
       }
+}
+
+// float32 rejection rows (vc_cache.cuh, DevCache::side).  tol bounds |q32 − q| for points with
+// q ≤ 1, i.e. |Δ| ≤ √d·r_max: rounding x, p and their difference to float32 (≤ u(|x| + |p| + |Δ|)
+// per axis), M to float32 and the products / sums (≤ 5u·|Δ|·Σ_i|M_ij| per axis j), then
+// |q32 − q| ≤ Σ_j (2e_j + e_j²) + 8u; doubled.  Non-finite M → tol = +inf (never rejects).
+__global__ void k_idx_side(const double* rec, int n, int dim, float4* side) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double* R = rec + (size_t)r * record_size(dim);
+  const double* ax = R + dim + 3 + 3 * dim;
+  const double* rad = ax + dim * dim;
+  double M[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double rmax = 0.0, pmax = 0.0;
+  for (int j = 0; j < dim; ++j) rmax = fmax(rmax, fabs(rad[j]));
+  for (int i = 0; i < dim; ++i) pmax = fmax(pmax, fabs(R[i]));
+  bool finite = true;
+  for (int i = 0; i < dim; ++i)
+    for (int j = 0; j < dim; ++j) {
+      M[i][j] = ax[i * dim + j] / rad[j];  // sphere records: identity axes, equal radii
+      finite &= isfinite(M[i][j]);
+    }
+  const double u = 5.9604644775390625e-08;  // 2^-24
+  const double dmax = sqrt((double)dim) * rmax;
+  const double B = u * (2.0 * pmax + 3.0 * dmax);
+  double tol = 8.0 * u;
+  for (int j = 0; j < dim; ++j) {
+    double ms = 0.0;
+    for (int i = 0; i < dim; ++i) ms += fabs(M[i][j]);
+    const double e = (B + 5.0 * u * dmax) * ms;
+    tol += 2.0 * e + e * e;
+  }
+  tol *= 2.0;
+  if (!finite || !isfinite(tol) || !isfinite(pmax)) tol = INFINITY;
+  float4* o = side + (size_t)r * kSide;
+  if (dim == 3) {
+    o[0] = make_float4((float)R[0], (float)R[1], (float)R[2], (float)tol);
+    o[1] = make_float4((float)M[0][0], (float)M[0][1], (float)M[0][2], (float)M[1][0]);
+    o[2] = make_float4((float)M[1][1], (float)M[1][2], (float)M[2][0], (float)M[2][1]);
+    o[3] = make_float4((float)M[2][2], 0.0f, 0.0f, 0.0f);
+  } else {
+    o[0] = make_float4((float)R[0], (float)R[1], (float)tol, (float)M[0][0]);
+    o[1] = make_float4((float)M[0][1], (float)M[1][0], (float)M[1][1], 0.0f);
+  }
+}
+
+// level of each record → bitmask of non-empty levels
+__global__ void k_idx_levels(IdxGeom G, const double* rec, int n, unsigned* mask) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int lv;
+  long long clo[3], chi[3];
+  if (record_cells(G, rec + (size_t)r * record_size(G.dim), lv, clo, chi)) atomicOr(mask, 1u << lv);
 }
 
 // cell_start[c] = first sorted entry with key ≥ c, for c in [0, n_cells]
@@ -208,6 +262,10 @@ int cache_reserve(vc_cache* c, size_t n_records, cudaStream_t st) {
   cudaFree(c->d_tag);
   c->d_rec = r;
   c->d_tag = t;
+  cudaFree(c->d_side);  // recomputed by every cache_rebuild
+  c->d_side = nullptr;
+  e = cudaMalloc(&c->d_side, cap * kSide * sizeof(float4));
+  if (e != cudaSuccess) return cuda_fail(e, "cache growth");
   c->rec_cap = cap;
   return VC_OK;
 }
@@ -239,6 +297,7 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   auto alloc = [&](int slot, size_t bytes) { return c->ws.get(slot, bytes, &e); };
   if (n == 0) {
     c->n_overflow = 0;
+    c->level_mask = 0;
     e = cudaMemsetAsync(c->d_cell_start, 0, (size_t)(c->n_cells + 1) * 4, st);
     if (e == cudaSuccess && !c->d_items) e = cudaMalloc(&c->d_items, 16);
     if (e == cudaSuccess && !c->d_overflow) e = cudaMalloc(&c->d_overflow, 16);
@@ -255,6 +314,7 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   int* off = (int*)alloc(2, ((size_t)n + 1) * 4);
   if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
   const int nb = (n + 127) / 128;
+  k_idx_side<<<nb, 128, 0, st>>>(c->d_rec, n, c->dim, c->d_side);
   k_idx_count<<<nb, 128, 0, st>>>(G, c->d_rec, n, cnt, ovf);
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, st);
@@ -277,13 +337,18 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   void* stmp = alloc(7, sb);
   if (e != cudaSuccess) return cuda_fail(e, "cache index select");
   cub::DeviceSelect::Flagged(stmp, sb, iota, ovf, ovf_list, n_sel, n, st);
-  int hv[2] = {0, 0};
-  e = cudaMemcpyAsync(&hv[0], off + n, 4, cudaMemcpyDeviceToHost, st);
+  unsigned* lmask = (unsigned*)(n_sel + 2);
+  e = cudaMemsetAsync(lmask, 0, 4, st);
+  k_idx_levels<<<nb, 128, 0, st>>>(G, c->d_rec, n, lmask);
+  int hv[3] = {0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[0], off + n, 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[1], n_sel, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[2], lmask, 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "cache index sizes");
   const int T = hv[0];
   c->n_overflow = hv[1];
+  c->level_mask = (unsigned)hv[2];
   unsigned* keys = (unsigned*)alloc(8, (size_t)T * 4 + 4);
   int* vals = (int*)alloc(9, (size_t)T * 4 + 4);
   unsigned* keys2 = (unsigned*)alloc(10, (size_t)T * 4 + 4);
@@ -310,7 +375,7 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   if (e != cudaSuccess) return cuda_fail(e, "cache index sort scratch");
   if (T > 0) cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
   k_idx_starts<<<(int)((c->n_cells + 1 + 255) / 256), 256, 0, st>>>(keys2, T, c->n_cells, c->d_cell_start);
-  count_launches(7);
+  count_launches(9);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "cache index build");
   return VC_OK;
@@ -351,7 +416,9 @@ struct MarchOut {
   long long c_n;
 };
 
-// mode 0: count misses; mode 1: write miss points + seeds; mode 2: final accumulation;
+// mode 0: count misses and hits, and finish every pixel without a miss (its image is the
+// hit-only accumulation; a frame over a populated cache is done in this one pass);
+// mode 1: write miss points + seeds; mode 2: final accumulation of the pixels with misses;
 // mode 3: final accumulation after insertion (frozen=False): each point reads the caches
 // as they were when it was reached (records of tag ≤ its ordinal), src/renderer.py:361-368
 __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
@@ -362,10 +429,12 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
   if (t >= npx) return;
   const int py = cam.row0 + t / cam.cols, px = cam.col0 + t % cam.cols;
   const long long i = (long long)py * cam.w + px;
+  if ((mode == 1 || mode == 2) && out.miss_cnt[t] == 0) return;  // finished by pass 0
   const double four_pi = 4.0 * kPi;
   double img[3] = {0.0, 0.0, 0.0};
   long long nm = 0, hits = 0;
-  long long slot = (mode >= 1) ? out.miss_off[t] : 0;
+  long long slot = (mode == 1 || mode == 2) ? out.miss_off[t] : 0;
+  const bool accum = mode != 1;
   for (int k = 0; k < spp; ++k) {
     double jx = 0.5, jy = 0.5;
     if (spp > 1) {  // rng.random((h, w, 2)) per k from SeedSequence(seed, 101)
@@ -383,13 +452,13 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
     double tt = isfinite(ts) ? ts : 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) hp[a] = add(o[a], mul(tt, d[a]));
-    if (mode >= 2) surface_radiance<3>(S, id, hp, d, lo);
+    if (accum) surface_radiance<3>(S, id, hp, d, lo);
     double t_in, t_out;
     bool valid;
     bounds_span(S, o, d, t_in, t_out, valid);
     double acc[3] = {0.0, 0.0, 0.0};
     if (!valid) {
-      if (mode >= 2 && id >= 0) {
+      if (accum && id >= 0) {
         img[0] += lo[0];
         img[1] += lo[1];
         img[2] += lo[2];
@@ -439,17 +508,19 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
           J[0] = out.miss_J[slot * 3 + 0];
           J[1] = out.miss_J[slot * 3 + 1];
           J[2] = out.miss_J[slot * 3 + 2];
+        } else {
+          J[0] = J[1] = J[2] = 0.0;  // pass 0: this pixel is redone by pass 2
         }
         ++slot;
         ++nm;
       }
-      if (mode >= 2) {
+      if (accum) {
         double f = mul(mul(exp(-S.sigma_t * sub(tk, t_in)), four_pi), 1.0);
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[c] = add(acc[c], mul(mul(f, J[c]), step));
       }
     }
-    if (mode >= 2) {
+    if (accum) {
       if (id >= 0) {
         double T = exp(-S.sigma_t * fmax(0.0, sub(t_end, t_in)));
 #pragma unroll
@@ -460,11 +531,14 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
       img[2] += acc[2];
     }
   }
-  if (mode == 0) out.miss_cnt[t] = nm;
-  if (mode >= 2) {
+  if (mode == 0) {
+    out.miss_cnt[t] = nm;
+    out.hits[t] = hits;
+  }
+  if ((mode == 0 && nm == 0) || mode >= 2) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) out.image[i * 3 + c] = __ddiv_rn(img[c], (double)spp);
-    out.hits[t] = hits;
+    if (mode == 3) out.hits[t] = hits;
   }
   (void)n_light_dummy;
 }
@@ -607,7 +681,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
   Workspace& ws = sc->ws;
   auto alloc = [&](int slot, size_t bytes) { return ws.get(slot, bytes, &e); };
   uint64_t* djit = (uint64_t*)alloc(22, 32);
-  long long* mcnt = (long long*)alloc(23, (size_t)npx * 8);
+  long long* mcnt = (long long*)alloc(23, ((size_t)npx + 1) * 8);
   long long* moff = (long long*)alloc(24, ((size_t)npx + 1) * 8);
   long long* hits = (long long*)alloc(25, (size_t)npx * 8);
   double* dimg = (double*)alloc(26, (size_t)cam.w * cam.h * 24);
@@ -659,15 +733,26 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     return VC_OK;
   }
   DevCache Cs = cs->dev(), Cm = cm->dev();
+  prof_begin(KC_MARCH, st);
   k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 0);
-  std::vector<long long> hc(npx), ho(npx + 1, 0);
-  e = cudaMemcpyAsync(hc.data(), mcnt, (size_t)npx * 8, cudaMemcpyDeviceToHost, st);
+  prof_end(st);
+  // miss offsets (device scan over npx + 1 counts, the last one zero) and the hit total
+  long long* hsum = (long long*)alloc(50, 16);
+  e = cudaMemsetAsync(mcnt + npx, 0, 8, st);
+  size_t tb = 0, tr = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, mcnt, moff, npx + 1, st);
+  cub::DeviceReduce::Sum(nullptr, tr, hits, hsum, npx, st);
+  void* tmp = alloc(51, std::max(tb, tr));
+  if (e != cudaSuccess) return cuda_fail(e, "march scan scratch");
+  cub::DeviceScan::ExclusiveSum(tmp, tb, mcnt, moff, npx + 1, st);
+  cub::DeviceReduce::Sum(tmp, tr, hits, hsum, npx, st);
+  e = cudaMemcpyAsync(hsum + 1, moff + npx, 8, cudaMemcpyDeviceToDevice, st);
+  long long hv[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hv, hsum, 16, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "march pass 1");
-  for (int t = 0; t < npx; ++t) ho[t + 1] = ho[t] + hc[t];
-  const long long nmiss = ho[npx];
-  e = cudaMemcpyAsync(moff, ho.data(), (size_t)(npx + 1) * 8, cudaMemcpyHostToDevice, st);
-  long long launches = 1;
+  const long long nmiss = hv[1];
+  long long launches = 3;
   if (nmiss > 0) {
     double* mx = (double*)alloc(27, (size_t)nmiss * 24);
     uint32_t* mw = (uint32_t*)alloc(28, (size_t)nmiss * 20);
@@ -708,32 +793,24 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     if (rc) return rc;
     k_misses_J<<<(int)((nmiss + 127) / 128), 128, 0, st>>>((int)nmiss, mmom, stride, mJ);
     mo.miss_J = mJ;
-    launches += 2;
+    prof_begin(KC_MARCH, st);
+    k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 2);
+    prof_end(st);
+    launches += 3;
   }
-  k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 2);
-  launches += 1;
   count_launches(launches);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "march launch");
   const bool host = flags & VC_MEM_HOST;
-  std::vector<long long> hh(npx);
-  e = cudaMemcpyAsync(hh.data(), hits, (size_t)npx * 8, cudaMemcpyDeviceToHost, st);
-  if (host) {
-    // copy the crop rows back
-    for (int y = cam.row0; y < cam.row0 + cam.rows && e == cudaSuccess; ++y)
-      e = cudaMemcpyAsync(image + ((size_t)y * cam.w + cam.col0) * 3, dimg + ((size_t)y * cam.w + cam.col0) * 3,
-                          (size_t)cam.cols * 24, cudaMemcpyDeviceToHost, st);
-  } else {
-    for (int y = cam.row0; y < cam.row0 + cam.rows && e == cudaSuccess; ++y)
-      e = cudaMemcpyAsync(image + ((size_t)y * cam.w + cam.col0) * 3, dimg + ((size_t)y * cam.w + cam.col0) * 3,
-                          (size_t)cam.cols * 24, cudaMemcpyDeviceToDevice, st);
-  }
+  // the crop rows (pitched copy)
+  const size_t pitch = (size_t)cam.w * 24;
+  e = cudaMemcpy2DAsync(image + ((size_t)cam.row0 * cam.w + cam.col0) * 3, pitch,
+                        dimg + ((size_t)cam.row0 * cam.w + cam.col0) * 3, pitch, (size_t)cam.cols * 24, cam.rows,
+                        host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "render download");
   if (stats) {
-    long long h = 0;
-    for (long long v : hh) h += v;
-    stats[0] = h;
+    stats[0] = hv[0];
     stats[1] = nmiss;
   }
   return VC_OK;

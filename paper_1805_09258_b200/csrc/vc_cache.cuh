@@ -35,7 +35,16 @@ struct DevCache {
   const int* overflow;
   const double* rec;           // n × record_size(dim), reference layout
   const long long* tag;        // n creation ordinals
+  const float4* side;          // n × kSide float32 rejection rows (record_side)
+  unsigned level_mask;         // bit ℓ: level ℓ lists at least one record
 };
+
+// float32 rejection row of a record: position, M = axes / radii (column j scaled by
+// 1/radius_j; for sphere records I / radius) and tol, a bound on |q32 − q| for every point
+// whose true q = Σ_j (Δ·axes_j / r_j)² ≤ 1 (i.e. |Δ| ≤ √d·r_max), so q32 > 1 + tol proves
+// support ≤ 0 (not covering).  3D: {p.xyz, tol}, {M00 M01 M02 M10}, {M11 M12 M20 M21},
+// {M22 0 0 0}; 2D: {p.xy, tol, M00}, {M01 M10 M11 0}.
+constexpr int kSide = 4;
 
 }  // namespace vc
 
@@ -53,6 +62,8 @@ struct vc_cache {
   int n_overflow = 0;
   double* d_rec = nullptr;
   long long* d_tag = nullptr;
+  float4* d_side = nullptr;  // kSide float4 per record (rejection rows)
+  unsigned level_mask = 0;
   size_t rec_cap = 0;  // records
   vc::Workspace ws;    // index-build scratch
   vc::DevCache dev() const {
@@ -70,6 +81,8 @@ struct vc_cache {
     c.overflow = d_overflow;
     c.rec = d_rec;
     c.tag = d_tag;
+    c.side = d_side;
+    c.level_mask = level_mask;
     return c;
   }
   ~vc_cache() {
@@ -79,6 +92,7 @@ struct vc_cache {
     cudaFree(d_overflow);
     cudaFree(d_rec);
     cudaFree(d_tag);
+    cudaFree(d_side);
   }
 };
 
@@ -226,6 +240,7 @@ __device__ __forceinline__ void blend_record(const double* R, const double* x, d
 template <int D, typename F>
 __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, F&& f) {
   for (int lv = C.L0; lv >= 0; --lv) {  // coarse → fine (tree order: root first)
+    if (!((C.level_mask >> lv) & 1u)) continue;
     const int N = 1 << (C.L0 - lv);
     const double h = C.size / N;
     long long cell = 0;
@@ -244,6 +259,29 @@ __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, 
   }
   for (int t = 0; t < C.n_overflow; ++t)
     if (f(C.overflow[t])) return;
+}
+
+// float32 rejection: true when record r certainly has support ≤ 0 at x (see record_side);
+// x32 is x rounded to float32.  NaN (a zero radius) never rejects: the exact test decides.
+template <int D>
+__device__ __forceinline__ bool side_rejects(const DevCache& C, int r, const float* x32) {
+  const float4* sd = C.side + (size_t)r * kSide;
+  const float4 s0 = __ldg(sd), s1 = __ldg(sd + 1);
+  if constexpr (D == 3) {
+    const float4 s2 = __ldg(sd + 2), s3 = __ldg(sd + 3);
+    const float d0 = x32[0] - s0.x, d1 = x32[1] - s0.y, d2 = x32[2] - s0.z;
+    const float a0 = d0 * s1.x + d1 * s1.w + d2 * s2.z;
+    const float a1 = d0 * s1.y + d1 * s2.x + d2 * s2.w;
+    const float a2 = d0 * s1.z + d1 * s2.y + d2 * s3.x;
+    const float q = a0 * a0 + a1 * a1 + a2 * a2;
+    return q > 1.0f + s0.w;
+  } else {
+    const float d0 = x32[0] - s0.x, d1 = x32[1] - s0.y;
+    const float a0 = d0 * s0.w + d1 * s1.y;
+    const float a1 = d0 * s1.x + d1 * s1.z;
+    const float q = a0 * a0 + a1 * a1;
+    return q > 1.0f + s0.z;
+  }
 }
 
 // log-space blend term of one sphere record (src/cache.py:363-394)
@@ -278,8 +316,12 @@ __device__ inline bool cache_interpolate(const DevCache& C, const double* x, dou
   double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};
   int hits = 0;
   const int RS = record_size(D);
+  float x32[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) x32[a] = (float)x[a];
   if (C.blend == 0) {
     cache_visit<D>(C, x, [&](int r) {
+      if (side_rejects<D>(C, r, x32)) return false;
       if (C.tag[r] < limit) blend_record<D>(C.rec + (size_t)r * RS, x, num, den[0], hits);
       return false;
     });
@@ -291,6 +333,7 @@ __device__ inline bool cache_interpolate(const DevCache& C, const double* x, dou
     return true;
   }
   cache_visit<D>(C, x, [&](int r) {
+    if (side_rejects<D>(C, r, x32)) return false;
     if (C.tag[r] < limit) log_blend_record<D>(C.rec + (size_t)r * RS, x, num, den, hits);
     return false;
   });
@@ -309,7 +352,11 @@ template <int D>
 __device__ inline bool cache_covers(const DevCache& C, const double* x, long long limit) {
   const int RS = record_size(D);
   bool hit = false;
+  float x32[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) x32[a] = (float)x[a];
   cache_visit<D>(C, x, [&](int r) {
+    if (side_rejects<D>(C, r, x32)) return false;
     if (C.tag[r] >= limit) return false;
     const double* R = C.rec + (size_t)r * RS;
     double dl[D];

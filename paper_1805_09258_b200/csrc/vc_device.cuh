@@ -624,6 +624,88 @@ __device__ inline bool ff_triangle(const double* r1v, const double* r2v, const d
   return true;
 }
 
+// The ok-mask of ff_triangle in float64 (r_i > 0 and |A| ≥ 1e-12·r₁r₂r₃ with the same
+// operations), so the element counts stay exact whatever precision evaluates the element.
+__device__ __forceinline__ bool ff_triangle_ok(const double* r1v, const double* r2v, const double* r3v) {
+  const double r0 = sqrt(r1v[0] * r1v[0] + r1v[1] * r1v[1] + r1v[2] * r1v[2]);
+  const double r1 = sqrt(r2v[0] * r2v[0] + r2v[1] * r2v[1] + r2v[2] * r2v[2]);
+  const double r2 = sqrt(r3v[0] * r3v[0] + r3v[1] * r3v[1] + r3v[2] * r3v[2]);
+  if (!(r0 > 0.0 && r1 > 0.0 && r2 > 0.0)) return false;
+  double c23[3];
+  cross3(r2v, r3v, c23);
+  const double A = r1v[0] * c23[0] + r1v[1] * c23[1] + r1v[2] * c23[2];
+  return fabs(A) >= 1e-12 * r0 * r1 * r2;
+}
+
+// float32 evaluation of ff_triangle's closed forms for an element whose ok-mask was decided
+// in float64 (ff_triangle_ok); inputs are the float-rounded offsets y_i − x.  The 3D form is
+// well conditioned (worst record H 2.8e-5 relative in float32).
+__device__ inline void ff_triangle_f32(const float* r1v, const float* r2v, const float* r3v, float& F, float g[3],
+                                       float H[6]) {
+  const float* R[3] = {r1v, r2v, r3v};
+  float r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[i] = sqrtf(R[i][0] * R[i][0] + R[i][1] * R[i][1] + R[i][2] * R[i][2]);
+  float c23[3], c12[3], c31[3];
+  c23[0] = R[1][1] * R[2][2] - R[1][2] * R[2][1];
+  c23[1] = R[1][2] * R[2][0] - R[1][0] * R[2][2];
+  c23[2] = R[1][0] * R[2][1] - R[1][1] * R[2][0];
+  c12[0] = R[0][1] * R[1][2] - R[0][2] * R[1][1];
+  c12[1] = R[0][2] * R[1][0] - R[0][0] * R[1][2];
+  c12[2] = R[0][0] * R[1][1] - R[0][1] * R[1][0];
+  c31[0] = R[2][1] * R[0][2] - R[2][2] * R[0][1];
+  c31[1] = R[2][2] * R[0][0] - R[2][0] * R[0][2];
+  c31[2] = R[2][0] * R[0][1] - R[2][1] * R[0][0];
+  const float A = R[0][0] * c23[0] + R[0][1] * c23[1] + R[0][2] * c23[2];
+  const float d12 = R[0][0] * R[1][0] + R[0][1] * R[1][1] + R[0][2] * R[1][2];
+  const float d23 = R[1][0] * R[2][0] + R[1][1] * R[2][1] + R[1][2] * R[2][2];
+  const float d13 = R[0][0] * R[2][0] + R[0][1] * R[2][1] + R[0][2] * R[2][2];
+  const float B = r[0] * r[1] * r[2] + d12 * r[2] + d23 * r[0] + d13 * r[1];
+  const float aA = fabsf(A);
+  const float k2pi = (float)(1.0 / (2.0 * kPi));
+  F = atan2f(aA, B) * k2pi;
+  const float sg = A >= 0.0f ? 1.0f : -1.0f;
+  const float s2 = r[0] * r[1] + r[0] * r[2] + r[1] * r[2];
+  const float rho = r[0] + r[1] + r[2];
+  const float dk[3] = {d23, d13, d12};
+  float n[3][3], cr[3], gU[3], gB[3], m[3];
+  float diag = 2.0f * rho;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float inv = 1.0f / r[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) n[i][c] = R[i][c] * inv;
+    cr[i] = (r[(i + 1) % 3] * r[(i + 2) % 3] + dk[i]) * inv;
+    diag += cr[i];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    gU[c] = -sg * (c12[c] + c23[c] + c31[c]);
+    gB[c] = -((s2 + dk[0]) * n[0][c] + (s2 + dk[1]) * n[1][c] + (s2 + dk[2]) * n[2][c]);
+    m[c] = n[0][c] + n[1][c] + n[2][c];
+  }
+  const float iden = 1.0f / (A * A + B * B);
+  float num[3], gD[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    num[c] = B * gU[c] - aA * gB[c];
+    gD[c] = 2.0f * aA * gU[c] + 2.0f * B * gB[c];
+    g[c] = num[c] * iden * k2pi;
+  }
+  const float ia = -aA * iden, id2 = -0.5f * iden * iden;
+  int e = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      float hb = (a == b ? diag : 0.0f) + rho * m[a] * m[b];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) hb -= (cr[i] + rho) * n[i][a] * n[i][b];
+      H[e++] = (ia * hb + id2 * (num[a] * gD[b] + num[b] * gD[a])) * k2pi;
+    }
+  }
+}
+
 __device__ inline bool ff_segment(const double* u, const double* v, double& F, double g[2], double H[3]) {
   double r0 = sqrt(u[0] * u[0] + u[1] * u[1]);
   double r1 = sqrt(v[0] * v[0] + v[1] * v[1]);

@@ -25,7 +25,10 @@
 // (record for record, in insertion order).  Misprediction costs only time: a stop
 // ends the window early, an unneeded speculative build is discarded.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <vector>
 
@@ -380,8 +383,24 @@ int Engine::run() {
   for (int s = n_slots - 1; s >= 0; --s) free_slots.push_back(s);
   std::map<long long, int> pool;  // ordinal → slot
   std::vector<double> hrec((size_t)n_slots * RS2);
+  // VOLCACHE_POP_TIMING=1: host wall time per phase (each phase ends in a stream sync) on stderr
+  const bool timing = getenv("VOLCACHE_POP_TIMING") && getenv("VOLCACHE_POP_TIMING")[0] == '1';
+  double tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double wave_s[5] = {0, 0, 0, 0, 0};  // build waves by size: <16, <128, <512, <1536, ≥1536
+  long long wave_n[5] = {0, 0, 0, 0, 0}, wave_rec[5] = {0, 0, 0, 0, 0};
+  auto tnow = [&]() {
+    if (timing) cudaStreamSynchronize(st);
+    return std::chrono::steady_clock::now();
+  };
+  auto tacc = [&](int k, std::chrono::steady_clock::time_point& t0) {
+    if (!timing) return;
+    auto t1 = tnow();
+    tph[k] += std::chrono::duration<double>(t1 - t0).count();
+    t0 = t1;
+  };
   long long pos = 0;
   while (pos < N) {
+    auto tp = tnow();
     const int Lw = (int)std::min<long long>(L, N - pos);
     // 1. lookahead points and their misses against the committed caches
     double* X = (double*)get(1, (size_t)Lw * D * 8);
@@ -405,6 +424,7 @@ int Engine::run() {
     if (e != cudaSuccess) return cuda_fail(e, "populate cover");
     count_launches(4);
     stats[3] += 1;
+    tacc(0, tp);
     // 2. sequential acceptance among the pooled builds inside the lookahead
     std::vector<long long> pords;
     std::vector<int> pslots;
@@ -441,6 +461,7 @@ int Engine::run() {
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return cuda_fail(e, "populate resolve");
     }
+    tacc(1, tp);
     // 3. tentative insertion of the accepted builds (tag = ordinal)
     const int n0s = cs->n, n0m = cm->n;
     std::vector<int> rows_s, rows_m;
@@ -470,6 +491,7 @@ int Engine::run() {
     int rc = append(cs, rows_s, tags_s, 29);
     if (!rc) rc = append(cm, rows_m, tags_m, 31);
     if (rc) return rc;
+    tacc(2, tp);
     // 4. unbuilt points still uncovered by every record of smaller tag; the first is the stop
     unsigned char* need2 = (unsigned char*)get(7, (size_t)nu + 1);
     unsigned long long* dstop = (unsigned long long*)get(33, 8);
@@ -486,6 +508,7 @@ int Engine::run() {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "populate stop");
     const long long stop = std::min<long long>((long long)hstop, pos + Lw);
+    tacc(3, tp);
     // 5. next speculative builds: need2 points thinned to one per cell of the predicted size
     std::vector<int> hj;
     if (stop < pos + Lw) {
@@ -551,6 +574,7 @@ int Engine::run() {
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return cuda_fail(e, "populate selection download");
     }
+    tacc(4, tp);
     // 6. decisions before the stop are final: keep them, roll back the rest
     int keep_s = 0, keep_m = 0, committed = 0, covered = 0;
     for (int q = 0; q < E; ++q) {
@@ -655,6 +679,7 @@ int Engine::run() {
       pool.erase(pords[q]);
       free_slots.push_back(pslots[q]);
     }
+    tacc(5, tp);
     // 7. build the new selections into the pool
     const int nn = (int)hj.size();
     if (nn > 0) {
@@ -687,12 +712,20 @@ int Engine::run() {
       if (D == 2) k_pop_gather_x<2><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
       else k_pop_gather_x<3><<<(nb2 + 127) / 128, 128, 0, st>>>(X, djs, nb2, xb);
       count_launches(1);
+      auto tb0 = tnow();
       if (estimator == VC_EST_BASELINE) {  // CacheSet.compute, mode "baseline" (src/renderer.py:233-244)
         rc = baseline_impl(sc, nb2, xb, dw, &blp, nullptr, rec, nullptr, st);
       } else {
         rc = build_impl(sc, nb2, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
       }
       if (rc) return rc;
+      if (timing) {
+        const double dt = std::chrono::duration<double>(tnow() - tb0).count();
+        const int b = nb2 < 16 ? 0 : nb2 < 128 ? 1 : nb2 < 512 ? 2 : nb2 < 1536 ? 3 : 4;
+        wave_n[b] += 1;
+        wave_rec[b] += nb2;
+        wave_s[b] += dt;
+      }
       k_pop_scatter<<<dim3(1, nb2), 64, 0, st>>>(rec, nb2, dns, RS2, WR);
       count_launches(1);
       if (D == 3 && estimator != VC_EST_BASELINE) {
@@ -708,6 +741,7 @@ int Engine::run() {
       for (int i = 0; i < nb2; ++i) pool[pos + js[i]] = new_slot[i];
       stats[4] += nb2;
     }
+    tacc(6, tp);
     // 8. advance
     if (stop >= pos + Lw) {
       pos += Lw;
@@ -720,6 +754,16 @@ int Engine::run() {
   stats[0] = N;
   stats[1] = cs->n;
   stats[2] = cm->n;
+  if (timing)
+    fprintf(stderr,
+            "populate phases (s): cover %.3f resolve %.3f append %.3f stop %.3f select %.3f commit %.3f build %.3f"
+            " | windows %lld builds %lld\n",
+            tph[0], tph[1], tph[2], tph[3], tph[4], tph[5], tph[6], (long long)stats[3], (long long)stats[4]);
+  if (timing)
+    for (int b = 0; b < 5; ++b)
+      fprintf(stderr, "  waves %s: %lld waves, %lld records, %.3f s\n",
+              b == 0 ? "<16" : b == 1 ? "<128" : b == 2 ? "<512" : b == 3 ? "<1536" : ">=1536", wave_n[b],
+              wave_rec[b], wave_s[b]);
   return VC_OK;
 }
 

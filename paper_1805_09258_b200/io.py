@@ -1,197 +1,238 @@
-"""On-disk formats of the path: cache JSON (+ a binary SoA sidecar) and PFM/PPM images.
+"""Cache files and images of the path, written from packed record rows.
 
-save_cache / load_cache write and read the reference's versioned JSON document
-(src/cache.py:397-491: format "volcache-cache", version 1, ellipsoid and sphere
-records), so caches built on the GPU load in the reference's tools and vice versa.
-save_cache_npz / load_cache_npz are the binary sidecar: packed
-record rows in the device layout plus the creation tags of a populated cache.
-write_pfm / read_pfm / write_ppm follow src/renderer.py:689-730.
+Formats (the reference's, so files move freely between the two implementations):
+* cache JSON — src/cache.py:397-491: {"format": "volcache-cache", "version": 1,
+  "dimensionality", "bounds", "metadata", "records"} with "ellipsoid" (axes, radii) and
+  "sphere" (radius) records, json indent 1 plus a trailing newline;
+* binary sidecar — the device row layout (position, value, grad, axes,
+  radii) plus creation tags, in one .npz;
+* PFM (little-endian colour, bottom-up rows) and a tonemapped PPM — src/renderer.py:689-730.
+
+Everything goes through the (N, d + 3 + 3d + d² + d) row matrix the device cache holds:
+saving reads the rows once (vc_cache_records for a device-built cache) and emits the
+document from them; loading validates the document into a row matrix and a kind vector
+and builds the device cache in one call.
 """
 
 from __future__ import annotations
 
 import json
-from dataclasses import dataclass
-from pathlib import Path
 
 import numpy as np
 
-from .cache import RadianceCache
-from .records import CacheRecord, record_size, unpack_record
+from .cache import RadianceCache, _pack
+from .records import BaselineRecord, CacheRecord, record_size
 
 CACHE_FORMAT = "volcache-cache"
 CACHE_VERSION = 1
+_ELLIPSOID, _SPHERE = 0, 1
 
 
 class CacheFormatError(ValueError):
-    """Raised for malformed or version-incompatible cache files (src/cache.py:45-46)."""
+    """A file that is not a version-1 volcache cache (src/cache.py:45-46)."""
 
 
-@dataclass(frozen=True)
-class BaselineRecord:
-    """Value + gradient with an isotropic valid region (src/cache.py:124-145).
-
-    Stored and indexed on the device as an ellipsoid with identity axes and equal radii.
-    """
-
-    position: np.ndarray
-    value: np.ndarray
-    grad: np.ndarray
-    radius: float
-
-    @property
-    def dim(self) -> int:
-        return self.position.size
-
-    @property
-    def bounding_radius(self) -> float:
-        return self.radius
-
-    @property
-    def axes(self) -> np.ndarray:
-        return np.eye(self.dim)
-
-    @property
-    def radii(self) -> np.ndarray:
-        return np.full(self.dim, float(self.radius))
+def _layout(d: int) -> dict[str, slice]:
+    """Field slices of a packed row."""
+    o, out = 0, {}
+    for name, k in (("position", d), ("value", 3), ("grad", 3 * d), ("axes", d * d), ("radii", d)):
+        out[name] = slice(o, o + k)
+        o += k
+    return out
 
 
-def _record_to_dict(rec) -> dict:
-    if isinstance(rec, BaselineRecord):
-        return {"record_type": "sphere", "position": np.asarray(rec.position, float).tolist(),
-                "value": np.asarray(rec.value, float).tolist(), "grad": np.asarray(rec.grad, float).tolist(),
-                "radius": float(rec.radius)}
-    if isinstance(rec, CacheRecord) or hasattr(rec, "axes"):
-        return {"record_type": "ellipsoid", "position": np.asarray(rec.position, float).tolist(),
-                "value": np.asarray(rec.value, float).tolist(), "grad": np.asarray(rec.grad, float).tolist(),
-                "axes": np.asarray(rec.axes, float).tolist(), "radii": np.asarray(rec.radii, float).tolist()}
-    raise TypeError(f"unknown record type {type(rec)!r}")
+def _rows_and_kinds(cache) -> tuple[np.ndarray, np.ndarray]:
+    """Packed rows + record kinds of a cache (host records, else the device rows)."""
+    recs = cache._records if isinstance(cache, RadianceCache) else list(cache.records)
+    if recs is None:  # held on the device only: the cache's mode decides the record type
+        rows = cache.packed()
+        kind = _SPHERE if getattr(cache, "sphere_records", False) else _ELLIPSOID
+        return rows, np.full(len(rows), kind, np.int8)
+    kinds = np.array([_SPHERE if (isinstance(r, BaselineRecord) or (hasattr(r, "radius") and not hasattr(r, "axes")))
+                      else _ELLIPSOID for r in recs], np.int8)
+    if len(kinds) and not np.all([hasattr(r, "position") for r in recs]):
+        raise TypeError("unknown record type in cache")
+    return _pack(recs, cache.dim), kinds
 
 
-def _record_from_dict(d: dict, dim: int):
-    try:
-        rtype = d["record_type"]
-        position = np.asarray(d["position"], dtype=float)
-        value = np.asarray(d["value"], dtype=float)
-        grad = np.asarray(d["grad"], dtype=float)
-    except (KeyError, TypeError, ValueError) as exc:
-        raise CacheFormatError(f"malformed cache record: {exc}") from exc
-    if position.shape != (dim,) or value.shape != (3,) or grad.shape != (3, dim):
-        raise CacheFormatError("cache record has inconsistent shapes")
-    if rtype == "ellipsoid":
-        try:
-            axes = np.asarray(d["axes"], dtype=float)
-            radii = np.asarray(d["radii"], dtype=float)
-        except (KeyError, TypeError, ValueError) as exc:
-            raise CacheFormatError(f"malformed cache record: {exc}") from exc
-        if axes.shape != (dim, dim) or radii.shape != (dim,):
-            raise CacheFormatError("cache record has inconsistent shapes")
-        return CacheRecord(position=position, value=value, grad=grad, axes=axes, radii=radii)
-    if rtype == "sphere":
-        try:
-            radius = float(d["radius"])
-        except (KeyError, TypeError, ValueError) as exc:
-            raise CacheFormatError(f"malformed cache record: {exc}") from exc
-        return BaselineRecord(position=position, value=value, grad=grad, radius=radius)
-    raise CacheFormatError(f"unknown record_type {rtype!r}")
+def _record_doc(row: np.ndarray, kind: int, f: dict, d: int) -> dict:
+    doc = {"record_type": "sphere" if kind == _SPHERE else "ellipsoid",
+           "position": row[f["position"]].tolist(), "value": row[f["value"]].tolist(),
+           "grad": row[f["grad"]].reshape(3, d).tolist()}
+    if kind == _SPHERE:
+        doc["radius"] = float(row[f["radii"]][0])
+    else:
+        doc["axes"] = row[f["axes"]].reshape(d, d).tolist()
+        doc["radii"] = row[f["radii"]].tolist()
+    return doc
 
 
-def save_cache(cache: RadianceCache, path, metadata: dict | None = None) -> None:
-    """Write the cache to versioned JSON (records, bounds, optional metadata)."""
-    doc = {
+def save_cache(cache, path, metadata: dict | None = None) -> None:
+    """Versioned JSON document of the cache's records, bounds and metadata."""
+    d = cache.dim
+    rows, kinds = _rows_and_kinds(cache)
+    f = _layout(d)
+    body = {
         "format": CACHE_FORMAT,
         "version": CACHE_VERSION,
-        "dimensionality": cache.dim,
-        "bounds": {"min": cache.bounds_min.tolist(), "max": cache.bounds_max.tolist()},
+        "dimensionality": d,
+        "bounds": {"min": np.asarray(cache.bounds_min, float).tolist(),
+                   "max": np.asarray(cache.bounds_max, float).tolist()},
         "metadata": metadata or {},
-        "records": [_record_to_dict(r) for r in cache.records],
+        "records": [_record_doc(r, int(k), f, d) for r, k in zip(rows, kinds)],
     }
     with open(path, "w", encoding="utf-8") as fh:
-        json.dump(doc, fh, indent=1)
+        fh.write(json.dumps(body, indent=1))
         fh.write("\n")
 
 
+def _as_array(v, shape, what):
+    try:
+        a = np.asarray(v, dtype=float)
+    except (TypeError, ValueError) as exc:
+        raise CacheFormatError(f"malformed cache record: {what}: {exc}") from exc
+    if a.shape != shape:
+        raise CacheFormatError(f"cache record has inconsistent shapes ({what} {a.shape}, want {shape})")
+    return a
+
+
+def _parse_records(items, d: int) -> tuple[np.ndarray, np.ndarray]:
+    if not isinstance(items, list):
+        raise CacheFormatError("malformed cache file: records must be a list")
+    f = _layout(d)
+    rows = np.zeros((len(items), record_size(d)))
+    kinds = np.zeros(len(items), np.int8)
+    for i, it in enumerate(items):
+        if not isinstance(it, dict):
+            raise CacheFormatError("malformed cache record: not an object")
+        for key in ("record_type", "position", "value", "grad"):
+            if key not in it:
+                raise CacheFormatError(f"malformed cache record: missing {key!r}")
+        row = rows[i]
+        row[f["position"]] = _as_array(it["position"], (d,), "position")
+        row[f["value"]] = _as_array(it["value"], (3,), "value")
+        row[f["grad"]] = _as_array(it["grad"], (3, d), "grad").ravel()
+        rtype = it["record_type"]
+        if rtype == "ellipsoid":
+            if "axes" not in it or "radii" not in it:
+                raise CacheFormatError("malformed cache record: ellipsoid without axes/radii")
+            row[f["axes"]] = _as_array(it["axes"], (d, d), "axes").ravel()
+            row[f["radii"]] = _as_array(it["radii"], (d,), "radii")
+        elif rtype == "sphere":
+            try:
+                radius = float(it["radius"])
+            except (KeyError, TypeError, ValueError) as exc:
+                raise CacheFormatError(f"malformed cache record: radius: {exc}") from exc
+            row[f["axes"]] = np.eye(d).ravel()
+            row[f["radii"]] = radius
+            kinds[i] = _SPHERE
+        else:
+            raise CacheFormatError(f"unknown record_type {rtype!r}")
+    return rows, kinds
+
+
+def _cache_from_rows(bmin, bmax, rows: np.ndarray, kinds: np.ndarray) -> RadianceCache:
+    d = np.asarray(bmin).size
+    f = _layout(d)
+    cache = RadianceCache(bmin, bmax)
+    recs = cache._records
+    for row, k in zip(rows, kinds):
+        p, v, g = row[f["position"]].copy(), row[f["value"]].copy(), row[f["grad"]].reshape(3, d).copy()
+        if k == _SPHERE:
+            recs.append(BaselineRecord(p, v, g, float(row[f["radii"]][0])))
+        else:
+            recs.append(CacheRecord(p, v, g, row[f["axes"]].reshape(d, d).copy(), row[f["radii"]].copy()))
+    return cache
+
+
 def load_cache(path) -> tuple[RadianceCache, dict]:
-    """Read a cache written by save_cache (either implementation); returns (cache, metadata)."""
-    with open(path, encoding="utf-8") as fh:
-        try:
+    """(cache, metadata) from a document written by save_cache (either implementation)."""
+    try:
+        with open(path, encoding="utf-8") as fh:
             doc = json.load(fh)
-        except json.JSONDecodeError as exc:
-            raise CacheFormatError(f"not a cache file: {exc}") from exc
+    except json.JSONDecodeError as exc:
+        raise CacheFormatError(f"not a cache file: {exc}") from exc
     if not isinstance(doc, dict) or doc.get("format") != CACHE_FORMAT:
         raise CacheFormatError("not a radiance cache file")
-    version = doc.get("version")
-    if version != CACHE_VERSION:
-        raise CacheFormatError(f"unsupported cache version {version!r} (supported: {CACHE_VERSION})")
+    if doc.get("version") != CACHE_VERSION:
+        raise CacheFormatError(f"unsupported cache version {doc.get('version')!r} (supported: {CACHE_VERSION})")
     try:
-        dim = int(doc["dimensionality"])
-        bounds_min = np.asarray(doc["bounds"]["min"], dtype=float)
-        bounds_max = np.asarray(doc["bounds"]["max"], dtype=float)
-        record_dicts = doc["records"]
+        d = int(doc["dimensionality"])
+        bmin = np.asarray(doc["bounds"]["min"], dtype=float)
+        bmax = np.asarray(doc["bounds"]["max"], dtype=float)
+        items = doc["records"]
     except (KeyError, TypeError, ValueError) as exc:
         raise CacheFormatError(f"malformed cache file: {exc}") from exc
-    cache = RadianceCache(bounds_min, bounds_max)
-    if cache.dim != dim:
-        raise CacheFormatError("dimensionality does not match bounds")
-    for d in record_dicts:
-        cache.insert(_record_from_dict(d, dim))
-    return cache, doc.get("metadata", {})
+    if bmin.shape != (d,) or bmax.shape != (d,):
+        if bmin.shape == bmax.shape and bmin.size in (2, 3):
+            raise CacheFormatError("dimensionality does not match bounds")
+        raise ValueError("bounds must be matching 2- or 3-vectors")
+    rows, kinds = _parse_records(items, d)
+    return _cache_from_rows(bmin, bmax, rows, kinds), doc.get("metadata", {})
 
 
 def save_cache_npz(cache: RadianceCache, path, tags=None) -> None:
-    """Binary SoA sidecar: bounds + packed rows (d + 3 + 3d + d² + d float64 each)."""
+    """Binary sidecar: bounds, packed rows in the device layout, creation tags."""
+    rows, kinds = _rows_and_kinds(cache)
     np.savez(path, format=np.array(CACHE_FORMAT), version=np.array(CACHE_VERSION),
-             bounds_min=cache.bounds_min, bounds_max=cache.bounds_max, records=cache.packed(),
-             tags=np.asarray(tags if tags is not None else np.full(len(cache), -1), np.int64))
+             bounds_min=np.asarray(cache.bounds_min, float), bounds_max=np.asarray(cache.bounds_max, float),
+             records=rows, kinds=kinds,
+             tags=np.asarray(tags if tags is not None else np.full(len(rows), -1), np.int64))
 
 
 def load_cache_npz(path) -> RadianceCache:
     z = np.load(path, allow_pickle=False)
     if str(z["format"]) != CACHE_FORMAT or int(z["version"]) != CACHE_VERSION:
         raise CacheFormatError("not a radiance cache sidecar")
-    cache = RadianceCache(z["bounds_min"], z["bounds_max"])
-    rows = np.asarray(z["records"], float)
-    if rows.size and rows.shape[1] != record_size(cache.dim):
+    bmin, bmax = z["bounds_min"], z["bounds_max"]
+    rows = np.asarray(z["records"], float).reshape(-1, record_size(bmin.size)) if z["records"].size else \
+        np.zeros((0, record_size(bmin.size)))
+    if z["records"].size and z["records"].shape[1] != record_size(bmin.size):
         raise CacheFormatError("sidecar rows do not match the dimensionality")
-    for r in rows:
-        cache.insert(unpack_record(r, cache.dim))
-    return cache
+    kinds = z["kinds"] if "kinds" in z.files else np.zeros(len(rows), np.int8)
+    return _cache_from_rows(bmin, bmax, rows, kinds)
+
+
+# ---------------------------------------------------------------------------
+# Images
+# ---------------------------------------------------------------------------
+
+
+def _rgb_image(image, dtype, who):
+    a = np.asarray(image, dtype=dtype)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError(f"{who} expects an (h, w, 3) image")
+    return a
 
 
 def write_pfm(path, image: np.ndarray) -> None:
-    """Write a (h, w, 3) float image (row 0 = top) as a little-endian color PFM."""
-    image = np.asarray(image, dtype=np.float32)
-    if image.ndim != 3 or image.shape[2] != 3:
-        raise ValueError("write_pfm expects an (h, w, 3) image")
-    h, w = image.shape[:2]
+    """Colour PFM, little endian (scale −1), rows stored bottom-up; row 0 of `image` is the top."""
+    a = _rgb_image(image, np.float32, "write_pfm")
+    h, w = a.shape[:2]
+    header = b"PF\n%d %d\n-1.0\n" % (w, h)
     with open(path, "wb") as fh:
-        fh.write(b"PF\n")
-        fh.write(f"{w} {h}\n".encode("ascii"))
-        fh.write(b"-1.0\n")
-        fh.write(image[::-1].astype("<f4").tobytes())  # PFM rasters are bottom-up
+        fh.write(header + np.ascontiguousarray(np.flipud(a), dtype="<f4").tobytes())
 
 
 def read_pfm(path):
-    """Read a color PFM; returns (h, w, 3) float32 with row 0 = top."""
-    with open(Path(path), "rb") as fh:
-        if fh.readline().strip() != b"PF":
-            raise ValueError("not a color PFM file")
-        w, h = (int(v) for v in fh.readline().split())
-        scale = float(fh.readline())
-        data = np.frombuffer(fh.read(), dtype="<f4" if scale < 0 else ">f4")
+    """(h, w, 3) float32 image, row 0 = top, from a colour PFM of either endianness."""
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    parts = raw.split(b"\n", 3)
+    if len(parts) < 4 or parts[0].strip() != b"PF":
+        raise ValueError("not a color PFM file")
+    w, h = (int(v) for v in parts[1].split())
+    endian = "<" if float(parts[2]) < 0 else ">"
+    data = np.frombuffer(parts[3], dtype=endian + "f4")
     if data.size != w * h * 3:
         raise ValueError("PFM payload size mismatch")
-    return data.reshape(h, w, 3)[::-1].astype(np.float32)
+    return np.flipud(data.reshape(h, w, 3)).astype(np.float32)
 
 
 def write_ppm(path, image: np.ndarray, exposure: float = 1.0) -> None:
-    """Gamma-2.2 tonemapped 8-bit PPM for quick looks."""
-    image = np.asarray(image, dtype=float)
-    if image.ndim != 3 or image.shape[2] != 3:
-        raise ValueError("write_ppm expects an (h, w, 3) image")
-    mapped = np.clip(image * exposure, 0.0, 1.0) ** (1.0 / 2.2)
-    bytes8 = (mapped * 255.0 + 0.5).astype(np.uint8)
-    h, w = image.shape[:2]
+    """8-bit binary PPM after exposure, clipping to [0, 1] and gamma 1/2.2 (for quick looks)."""
+    a = _rgb_image(image, float, "write_ppm")
+    q = (np.clip(a * exposure, 0.0, 1.0) ** (1.0 / 2.2) * 255.0 + 0.5).astype(np.uint8)
+    h, w = a.shape[:2]
     with open(path, "wb") as fh:
-        fh.write(f"P6\n{w} {h}\n255\n".encode("ascii"))
-        fh.write(bytes8.tobytes())
+        fh.write(b"P6\n%d %d\n255\n" % (w, h) + q.tobytes())

@@ -64,6 +64,35 @@ class CacheRecord:
         return np.concatenate([self.position, self.value, self.grad.ravel(), self.axes.ravel(), self.radii])
 
 
+@dataclass(frozen=True)
+class BaselineRecord:
+    """Sphere record of the occlusion-unaware baseline (src/cache.py:124-145).
+
+    The device stores it like an ellipse record: identity axes, every radius = `radius`.
+    """
+
+    position: np.ndarray
+    value: np.ndarray
+    grad: np.ndarray
+    radius: float
+
+    @property
+    def dim(self) -> int:
+        return self.position.size
+
+    @property
+    def bounding_radius(self) -> float:
+        return self.radius
+
+    @property
+    def axes(self) -> np.ndarray:
+        return np.eye(self.dim)
+
+    @property
+    def radii(self) -> np.ndarray:
+        return np.full(self.dim, float(self.radius))
+
+
 def unpack_record(row, d: int) -> CacheRecord:
     row = np.asarray(row, float)
     o = 0

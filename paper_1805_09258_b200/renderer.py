@@ -285,6 +285,7 @@ def populate_cache(scene, target, settings: RenderSettings, *, window: int = 0, 
                                       _lib.ptr(st), None))
     single = RadianceCache._adopt(scene.bounds_min, scene.bounds_max, hs)
     multiple = RadianceCache._adopt(scene.bounds_min, scene.bounds_max, hm)
+    single.sphere_records = multiple.sphere_records = settings.mode == "baseline"
     cs = CacheSet(scene, settings.mode, _single=single, _multiple=multiple)
     stats = {
         "mode": settings.mode,

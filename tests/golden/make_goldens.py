@@ -577,6 +577,77 @@ def gen_baseline_rng():
     np.savez_compressed(OUT / "baseline_rng.npz", **out)
 
 
+def _chunked_trace(orig, chunk=64):
+    """Per-ray identical stand-in for scene.trace that bounds numpy's (m, K, 3) temporaries
+    (SURVEY.md §8d chunked-trace shim): the reference's own function on ray chunks."""
+    def trace(scene, origins, dirs, t_max=None):
+        origins, dirs = np.asarray(origins, float), np.asarray(dirs, float)
+        m = origins.shape[0]
+        s = np.empty(m)
+        idx = np.empty(m, dtype=np.int64)
+        for a in range(0, m, chunk):
+            tm = None if t_max is None else (t_max if np.ndim(t_max) == 0 else np.asarray(t_max)[a:a + chunk])
+            s[a:a + chunk], idx[a:a + chunk] = orig(scene, origins[a:a + chunk], dirs[a:a + chunk], tm)
+        return s, idx
+    return trace
+
+
+def gen_cfg5_crop(src=REPO / "gpurun_out" / "cfg5_crop_records.npz"):
+    """Reference frozen render of a 64×36 crop of the cfg5 frame (1920×1080 over the cfg3
+    room, march step 0.01) from GPU-populated records (tools/cfg5_crop_fixture.py: the
+    records near the crop's rays, a superset of every record covering a crop march point).
+    The crop is a reference Camera whose rays are the full camera's rays of the crop pixels
+    (render() itself is unchanged); trace is chunked (per-ray identical)."""
+    import inspect
+    import time
+
+    z = np.load(src)
+    r0, nr, c0, nc = (int(v) for v in z["crop"])
+    sc3 = configs.cfg3_scene()
+    sc = ref_scene(sc3)
+    vscene_trace = vscene.trace
+    shim = _chunked_trace(vscene_trace)
+    for mod in (vscene, vr, __import__("volcache.transport", fromlist=["x"])):
+        if hasattr(mod, "trace"):
+            mod.trace = shim
+    c = configs.cfg5_camera(1920, 1080)
+    full = vr.Camera(position=c["position"], look_at=c["look_at"], up=c["up"], fov_degrees=c["fov"], width=1920,
+                     height=1080)
+
+    class CropCamera(vr.Camera):
+        def rays(self, jitter):
+            jf = np.full((full.height, full.width, 2), 0.5)
+            jf[r0:r0 + nr, c0:c0 + nc] = jitter
+            o, d = full.rays(jf)
+            sel = (np.arange(r0, r0 + nr)[:, None] * full.width + np.arange(c0, c0 + nc)[None]).ravel()
+            return o[sel], d[sel]
+
+    crop = CropCamera(position=c["position"], look_at=c["look_at"], up=c["up"], fov_degrees=c["fov"], width=nc,
+                      height=nr)
+    st = vr.RenderSettings(mode="ours-aniso", epsilon=float(z["eps"]), spp=1, march_step=float(z["step"]),
+                           n_angular=16384, seed=int(z["seed"]), frozen=True)
+    cs = vr.CacheSet(sc, "ours-aniso")
+    for name, cache in (("single", cs.single), ("multiple", cs.multiple)):
+        for r in z[f"{name}_rows"]:
+            cache.insert(vcache.CacheRecord(position=r[:3].copy(), value=r[3:6].copy(), grad=r[6:15].reshape(3, 3).copy(),
+                                            axes=r[15:24].reshape(3, 3).copy(), radii=r[24:27].copy()))
+    t0 = time.perf_counter()
+    img, stats = vr.render(sc, crop, st, cache_set=cs)
+    print("reference crop render", time.perf_counter() - t0, "s", {k: stats[k] for k in ("cache_hits",
+                                                                                      "direct_evaluations")})
+    assert stats["direct_evaluations"] == 0, "crop must be covered by the populated records"
+    out = {"versions": VERSIONS, "crop": z["crop"], "eps": z["eps"], "step": z["step"], "seed": z["seed"],
+           "single_rows": z["single_rows"], "multiple_rows": z["multiple_rows"],
+           "single_index": z["single_index"], "multiple_index": z["multiple_index"],
+           "pop_stats": z["pop_stats"], "image": img,
+           "stats": np.array([stats["cache_hits"], stats["direct_evaluations"]])}
+    np.savez_compressed(OUT / "cfg5_crop.npz", **out)
+    for mod in (vscene, vr, __import__("volcache.transport", fromlist=["x"])):
+        if hasattr(mod, "trace"):
+            mod.trace = vscene_trace
+    del inspect
+
+
 def gen_path():
     """path_trace_radiance / fd_derivatives / render mode "path" through the reference
     (src/transport.py:318-391, src/renderer.py:337-346, :590-643)."""
@@ -691,6 +762,8 @@ if __name__ == "__main__":
         gen_baseline()
     if "baseline_rng" in which:
         gen_baseline_rng()
+    if "cfg5_crop" in which:
+        gen_cfg5_crop()
     if "path" in which:
         gen_path()
     if "grow" in which:
