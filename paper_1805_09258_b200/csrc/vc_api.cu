@@ -54,8 +54,14 @@ __global__ void k_outside(const double* x, long long N, int D, double3 lo, doubl
   }
 }
 
-int check_inside(const vc_scene* sc, long long N, const double* x, bool host, const char* what,
-                 cudaStream_t st) {
+// Device inputs: k_outside raises a device flag (read by k_rings, which then skips every
+// ring so no kernel indexes past the r_ub-sized buffers) and copies it to pinned memory
+// behind an event; the caller enqueues its work first and waits only at check_end, so the
+// check never drains the stream ahead of the wave.
+int check_begin(const vc_scene* sc, long long N, const double* x, bool host, const char* what, cudaStream_t st,
+                InsideCheck* ck) {
+  ck->pending = false;
+  ck->dflag = nullptr;
   const int D = sc->dim;
   const double eps = 1e-12 * sc->scale;
   if (host) {
@@ -67,20 +73,43 @@ int check_inside(const vc_scene* sc, long long N, const double* x, bool host, co
     return VC_OK;
   }
   static thread_local int* dflag = nullptr;
+  static thread_local int* hflag = nullptr;
+  static thread_local cudaEvent_t ev = nullptr;
   cudaError_t e = cudaSuccess;
   if (!dflag) e = cudaMalloc(&dflag, 4);
+  if (e == cudaSuccess && !hflag) e = cudaMallocHost(&hflag, 4);
+  if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, 4, st);
   if (e != cudaSuccess) return cuda_fail(e, "bounds check");
   const double3 lo = make_double3(sc->bmin[0] - eps, sc->bmin[1] - eps, sc->bmin[2] - eps);
   const double3 hi = make_double3(sc->bmax[0] + eps, sc->bmax[1] + eps, sc->bmax[2] + eps);
-  const int grid = (int)std::min<long long>((N + 255) / 256, 4 * 148);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((N + 255) / 256, 4 * 148));
   k_outside<<<grid, 256, 0, st>>>(x, N, D, lo, hi, dflag);
   count_launches(1);
-  int h = 0;
-  e = cudaMemcpyAsync(&h, dflag, 4, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  e = cudaMemcpyAsync(hflag, dflag, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, st);
   if (e != cudaSuccess) return cuda_fail(e, "bounds check");
-  return h ? fail(VC_EOUTSIDE, what) : VC_OK;
+  ck->pending = true;
+  ck->dflag = dflag;
+  ck->hflag = hflag;
+  ck->ev = ev;
+  ck->what = what;
+  return VC_OK;
+}
+
+int check_end(InsideCheck* ck) {
+  if (!ck->pending) return VC_OK;
+  ck->pending = false;
+  const cudaError_t e = cudaEventSynchronize(ck->ev);
+  if (e != cudaSuccess) return cuda_fail(e, "bounds check");
+  return *ck->hflag ? fail(VC_EOUTSIDE, ck->what) : VC_OK;
+}
+
+int check_inside(const vc_scene* sc, long long N, const double* x, bool host, const char* what,
+                 cudaStream_t st) {
+  InsideCheck ck;
+  const int rc = check_begin(sc, N, x, host, what, st, &ck);
+  return rc ? rc : check_end(&ck);
 }
 
 Workspace::~Workspace() {
@@ -386,8 +415,12 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
     }
   }
   if (D == 3) del_row_table(P);
-  {  // ValueError before any work (src/subdivision.py:155-158), host and device inputs alike
-    const int rc = check_inside(sc, N, x, host, "subdivision center lies outside the medium bounds", st);
+  // ValueError (src/subdivision.py:155-158), host and device inputs alike: host inputs are
+  // checked before any work; device inputs by a flag kernel whose result is read after the
+  // wave is enqueued (a flagged wave does no ring work; the call then fails)
+  InsideCheck inside;
+  {
+    const int rc = check_begin(sc, N, x, host, "subdivision center lies outside the medium bounds", st, &inside);
     if (rc) return rc;
   }
   int rc = ensure_emitters(sc, prm->n_light_samples);
@@ -481,6 +514,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.gather_q_count = (unsigned long long*)alloc(33, 8);
   if (err != cudaSuccess) return cuda_fail(err, "workspace allocation");
 
+  W.outside = inside.dflag;
   KernelCounter kc;
   for (long long w0 = 0; w0 < N; w0 += B) {
     const int b = (int)std::min<long long>(B, N - w0);
@@ -549,6 +583,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
     }
   }
   g_launches += kc.launches;
+  if (const int rc = check_end(&inside)) return rc;
   if (host) {
     err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) return cuda_fail(err, "record build");

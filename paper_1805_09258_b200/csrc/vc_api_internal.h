@@ -41,6 +41,19 @@ const unsigned long long* jump_tables(cudaError_t* err);
 int check_inside(const vc_scene* sc, long long N, const double* x, bool host, const char* what,
                  cudaStream_t st);
 
+// Split form: check_begin tests host arrays at once; for device arrays it enqueues the flag
+// kernel (flag also left in ck->dflag for kernels to read) and check_end waits for it.
+struct InsideCheck {
+  bool pending = false;
+  int* dflag = nullptr;
+  int* hflag = nullptr;
+  cudaEvent_t ev = nullptr;
+  const char* what = nullptr;
+};
+int check_begin(const vc_scene* sc, long long N, const double* x, bool host, const char* what, cudaStream_t st,
+                InsideCheck* ck);
+int check_end(InsideCheck* ck);
+
 }  // namespace vc
 
 // Device copy of one primitive set (all surfaces, or the emitters) with its BVH.

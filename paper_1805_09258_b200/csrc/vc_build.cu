@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(kRingBS) k_rings(BuildParams P, Wave W) {
   }
   __syncthreads();
   const double max_s = smax[0];
-  const int R = (int)floor(__ddiv_rn(max_s, P.march_step) + 0.5);
+  // a wave whose points failed the device bounds check does no ring work (the call fails);
+  // R ≤ r_ub − 2 holds for every point inside the bounds
+  const int R = (W.outside && *W.outside) ? 0 : min((int)floor(__ddiv_rn(max_s, P.march_step) + 0.5), P.r_ub);
   long long run = 0;
   int maxc = 0;
   for (int base = 0; base < n; base += kRingBS) {

@@ -131,6 +131,7 @@ struct alignas(16) DirInfo {
 
 // Per-record scratch for one wave (device pointers).
 struct Wave {
+  const int* outside;    // device bounds-check flag (nullptr: host-checked); set → no rings
   DirInfo* info;         // B × n
   double* partial;       // B × kAsmParts × 2 × 32 assembly partial sums (+ counters)
   int B;                 // records in this wave

@@ -592,6 +592,52 @@ def _chunked_trace(orig, chunk=64):
     return trace
 
 
+CFG3_FULL_POINTS = (0, 6333, 12666, 18999)  # spread over the 19k cfg3 cache points
+
+
+def _cfg3_full_one(i):
+    """One bench-workload record (cfg3 room, n = 16384, step 0.1, n_inner 1, n_light 16) from
+    the unmodified reference: estimate_moments' build_subdivision + assemble_moments and both
+    make_record calls, with trace chunked per SURVEY.md §8d (per-ray identical)."""
+    import volcache.transport as vt
+
+    shim = _chunked_trace(vscene.trace, 16)
+    for mod in (vscene, vr, vt):
+        mod.trace = shim
+    w = configs.cfg3()
+    rs = ref_scene(w.scene)
+    x = w.points[i]
+    with Capture() as cap:
+        sub = vs.build_subdivision(rs, x, n_angular=16384, march_step=0.1, rng_seed=vr._seed(2, 401, i), n_inner=1,
+                                   n_light_samples=16)
+    single, multiple, stats = vs.assemble_moments(sub, rs.medium)
+    recs = [vcache.make_record(x, m, 0.05, rs.scale, rs.max_emission, anisotropic=True) for m in (single, multiple)]
+    return dict(L=[single.L, multiple.L], grad=[single.grad, multiple.grad], hess=[single.hess, multiple.hess],
+                stats=[stats["elements_evaluated"], stats["elements_dropped"], stats["star_vertices"]],
+                adj=np.asarray(cap.dirs.adjacency, np.int32), s=cap.s, idx=np.asarray(cap.idx, np.int32),
+                rec_value=[r.value for r in recs], rec_axes=[r.axes for r in recs], rec_radii=[r.radii for r in recs])
+
+
+def gen_cfg3_full(procs=4):
+    """Records of the bench workload itself from the reference: four cfg3
+    points spread over the 19k, full n = 16384 with qhull's adjacency captured (the GPU test
+    injects it).  ~35 min per record per core with the chunked brute-force trace."""
+    import multiprocessing as mp
+    import os
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    w = configs.cfg3()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_cfg3_full_one, CFG3_FULL_POINTS)
+    out = {k: np.array([r[k] for r in res]) for k in res[0]}
+    dim, V, E, A = scene_arrays(w.scene)
+    out.update(versions=VERSIONS, points=w.points[list(CFG3_FULL_POINTS)], index=np.array(CFG3_FULL_POINTS),
+               cfg_seed=np.array(2), params=np.array([16384, 0.1, 1, 16, 0.0]),
+               scene_digest=np.array([V.sum(), (V * V).sum(), E.sum(), float(len(V))]))
+    np.savez_compressed(OUT / "rec_cfg3_full.npz", **out)
+    print("wrote cfg3_full", flush=True)
+
+
 def gen_cfg5_crop(src=REPO / "gpurun_out" / "cfg5_crop_records.npz"):
     """Reference frozen render of a 64×36 crop of the cfg5 frame (1920×1080 over the cfg3
     room, march step 0.01) from GPU-populated records (tools/cfg5_crop_fixture.py: the
@@ -762,6 +808,8 @@ if __name__ == "__main__":
         gen_baseline()
     if "baseline_rng" in which:
         gen_baseline_rng()
+    if "cfg3_full" in which:
+        gen_cfg3_full()
     if "cfg5_crop" in which:
         gen_cfg5_crop()
     if "path" in which:
