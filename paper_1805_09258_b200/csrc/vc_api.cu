@@ -1,5 +1,6 @@
 // C ABI of libvolcache_b200: scene upload, workspace management, wave orchestration.
 #include <algorithm>
+#include <cfloat>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -865,22 +866,63 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
     if (e == cudaSuccess && src) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
   };
   // a primitive subset (original ids `ids`) → BVH (when large enough) + leaf-order prims
+  // a primitive subset (original ids `ids`) → BVH (when large enough) + leaf-order prims.
+  // Node boxes and the float32 primitive rows are taken relative to the bounds centre (in
+  // float64, then rounded), so float32 magnitudes stay ≲ scale wherever the scene sits.
+  double ctr[3] = {0, 0, 0};
+  for (int a = 0; a < dim; ++a) ctr[a] = 0.5 * (sc->bmin[a] + sc->bmax[a]);
+  auto up32 = [](double v) {  // float32 ≥ v
+    float f = (float)v;
+    return (double)f < v ? std::nextafter(f, FLT_MAX) : f;
+  };
   auto make_set = [&](const std::vector<int>& ids, int bvh_min, GpuBvh& g, int leaf_max) {
     const int Ks = (int)ids.size();
     g.K = Ks;
+    for (int a = 0; a < 3; ++a) g.ctr[a] = ctr[a];
     std::vector<int> order(ids);
+    std::vector<unsigned char> last((size_t)std::max(Ks, 1), 0);
     HostBVH bvh;
     if (Ks > bvh_min) {
       std::vector<double> vs((size_t)Ks * dim * dim);
       for (int i = 0; i < Ks; ++i)
-        std::memcpy(&vs[(size_t)i * dim * dim], &sc->verts[(size_t)ids[i] * dim * dim], dim * dim * 8);
+        for (int v = 0; v < dim; ++v)
+          for (int a = 0; a < dim; ++a)
+            vs[((size_t)i * dim + v) * dim + a] = sc->verts[((size_t)ids[i] * dim + v) * dim + a] - ctr[a];
       build_bvh(dim, Ks, vs.data(), 1e-5 * sc->scale, &bvh, leaf_max);
       for (int i = 0; i < Ks; ++i) order[i] = ids[bvh.order[i]];
+      std::memcpy(last.data(), bvh.leaf_last, (size_t)Ks);
+      g.stack_need = std::max(1, bvh.max_depth);
     }
     std::vector<double> leaf((size_t)Ks * ps);
     for (int i = 0; i < Ks; ++i) std::memcpy(&leaf[(size_t)i * ps], &prim[(size_t)order[i] * ps], ps * 8);
+    std::vector<float4> p32((size_t)std::max(Ks, 1) * 3);
+    for (int i = 0; i < Ks; ++i) {
+      const double* P = &leaf[(size_t)i * ps];
+      float4* q = &p32[(size_t)i * 3];
+      const unsigned idf = (unsigned)order[i] | (last[i] ? 0x80000000u : 0u);
+      float fid;
+      std::memcpy(&fid, &idf, 4);
+      if (dim == 3) {
+        double r[3], vb = 0.0, E = 0.0;
+        for (int a = 0; a < 3; ++a) {
+          r[a] = P[a] - ctr[a];
+          vb = std::max(vb, std::fabs(r[a]));
+          E = std::max(E, std::max(std::fabs(P[3 + a]), std::fabs(P[6 + a])));
+        }
+        // tiny or non-finite edges: no pre-test (its relative error bounds assume normal floats)
+        const bool pre = std::isfinite(E) && std::isfinite(vb) && E > 1e-9 * sc->scale && vb < 1e30;
+        q[0] = make_float4((float)r[0], (float)r[1], (float)r[2], (float)up32(vb * (1.0 + 1e-6)));
+        q[1] = make_float4((float)P[3], (float)P[4], (float)P[5], pre ? (float)up32(E * (1.0 + 1e-6)) : -1.0f);
+        q[2] = make_float4((float)P[6], (float)P[7], (float)P[8], fid);
+      } else {
+        q[0] = make_float4((float)(P[0] - ctr[0]), (float)(P[1] - ctr[1]), 0.0f, 0.0f);
+        q[1] = make_float4((float)P[2], (float)P[3], 0.0f, -1.0f);
+        q[2] = make_float4(0.0f, 0.0f, 0.0f, fid);
+      }
+    }
     up((void**)&g.prim, Ks ? leaf.data() : nullptr, leaf.size() * 8);
     up((void**)&g.prim_id, Ks ? order.data() : nullptr, order.size() * 4);
+    up((void**)&g.prim32, Ks ? p32.data() : nullptr, p32.size() * sizeof(float4));
     if (bvh.n_nodes) {
       up((void**)&g.nodes, bvh.nodes, sizeof(float4) * 4 * bvh.n_nodes);
       g.n_nodes = bvh.n_nodes;

@@ -58,15 +58,20 @@ int check_end(InsideCheck* ck);
 
 // Device copy of one primitive set (all surfaces, or the emitters) with its BVH.
 struct GpuBvh {
-  int K = 0, n_nodes = 0;
+  int K = 0, n_nodes = 0, stack_need = 0;
   double* prim = nullptr;
   int* prim_id = nullptr;
   float4* nodes = nullptr;
-  vc::DevBvh dev() const { return vc::DevBvh{K, n_nodes, nodes, prim, prim_id}; }
+  float4* prim32 = nullptr;
+  double ctr[3] = {0, 0, 0};
+  vc::DevBvh dev() const {
+    return vc::DevBvh{K, n_nodes, nodes, prim, prim_id, prim32, {ctr[0], ctr[1], ctr[2]}, stack_need};
+  }
   ~GpuBvh() {
     cudaFree(prim);
     cudaFree(prim_id);
     cudaFree(nodes);
+    cudaFree(prim32);
   }
 };
 

@@ -15,6 +15,7 @@
 //                moments summed with shuffles + shared-memory tree, no atomics
 //   k_make_record thread per (record, kind): eigen + radii (src/cache.py:146-189)
 #include <cfloat>
+#include <type_traits>
 #include <cstdio>
 #include <vector>
 
@@ -61,8 +62,25 @@ __device__ __forceinline__ int tiled_direction(int t, const BuildParams& P) {
   return (tr * TR + lane / TC) * P.cols + tc * TC + lane % TC;
 }
 
+// VC_SMEM_STACK: BVH traversal stacks in dynamic shared memory (DevBvh::stack_need entries
+// per thread) instead of per-thread local arrays.  Measured per 2048-record wave (r2): shared
+// 7.77 ms primary / 14.02 ms gather vs local 6.15 / 13.45 — the 40 KB-per-CTA carve-out
+// shrinks the L1 that caches BVH nodes and primitives, which costs more than the local
+// stack traffic it removes (the stack's live lines stay in L1 anyway)
+#ifndef VC_SMEM_STACK
+#define VC_SMEM_STACK 0
+#endif
+#if VC_SMEM_STACK
+#define VC_RAY_STACK                     \
+  extern __shared__ uint2 trav_stack[]; \
+  SharedStack<256> stk{trav_stack + threadIdx.x}
+#else
+#define VC_RAY_STACK LocalStack stk
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+  VC_RAY_STACK;
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)W.B * n) return;
@@ -75,12 +93,12 @@ __global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, Buil
   for (int a = 0; a < D; ++a) o[a] = W.x[rec * D + a];
   double s;
   int id;
-  trace_or_bounds<D>(S, o, d, s, id);
+  trace_or_bounds<D>(S, o, d, s, id, &stk);
   double hit[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) hit[a] = add(o[a], mul(s, d[a]));
   double L[3];
-  surface_radiance<D>(S, id, hit, d, L);
+  surface_radiance<D>(S, id, hit, d, L, &stk);
   size_t base = (size_t)rec * n + k;
 #pragma unroll
   for (int a = 0; a < D; ++a) W.dirs[base * D + a] = d[a];
@@ -666,13 +684,14 @@ template <int D>
 __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl(DevScene S, Wave W, int n, const GatherItem* q,
                                                                const unsigned long long* q_count, long long q_cap,
                                                                float* media) {
+  VC_RAY_STACK;
   const long long nq = min((long long)*q_count, q_cap);
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nq;
        t += (long long)gridDim.x * blockDim.x) {
     if (q[t].slot < 0) continue;  // unused tail of a warp's chunk
     const GatherItem it = q[t];
     double v[3] = {0.0, 0.0, 0.0};
-    if (!occluded<D>(S, it.y, it.d, it.te, it.ie)) {
+    if (!occluded<D>(S, it.y, it.d, it.te, it.ie, &stk)) {
       // L_o = emission (non-reflective scene); σs · T · L_o / n_inner with n_inner = 1
       const double* E = S.emission + (size_t)it.ie * 3;
       double T = exp(-S.sigma_t * it.te);
@@ -1827,6 +1846,13 @@ __global__ void k_degree(BuildParams P, Wave W) {
 // ---------------------------------------------------------------------------
 
 constexpr int kQCap = 64;
+// 3D element math in float32 (float64 ok-mask; per-round warp sums in float32, accumulated
+// over rounds in float64); 0: float64 throughout
+#ifndef VC_ASM_F32
+#define VC_ASM_F32 1
+#endif
+template <int D>
+using AsmT = typename std::conditional<D == 3 && VC_ASM_F32, float, double>::type;
 #ifndef VC_ASM_MINB
 #define VC_ASM_MINB (512 / VC_ASM_BS)  // resident CTAs per SM → ≤ 128 registers
 #endif
@@ -1883,9 +1909,9 @@ __device__ __forceinline__ AsmCtx<D> asm_ctx(const BuildParams& P, const Wave& W
 
 // Contribution (3·NQ components, c·NQ + t) of element v[] at `ring` with representative
 // vertex slot `rep` (src/subdivision.py:318-366); false = degenerate element (dropped).
-template <int D>
+template <int D, class CT>
 __device__ __forceinline__ bool asm_item(const DevScene& S, const AsmCtx<D>& C, int kind, double wt, const int* v,
-                                         int ring, int rep, double (&cvec)[32]) {
+                                         int ring, int rep, CT (&cvec)[32]) {
   constexpr int NQ = 1 + D + D * (D + 1) / 2;
   double rv[D][3];
   double dist[D];
@@ -1899,16 +1925,60 @@ __device__ __forceinline__ bool asm_item(const DevScene& S, const AsmCtx<D>& C, 
     for (int a = 0; a < D; ++a) rv[j][a] = dist[j] * C.dirs[(size_t)v[j] * D + a];
   }
   double rad[3];
+  const int vrep = rep == 0 ? v[0] : (rep == 1 || D == 2 ? v[1] : v[D - 1]);
   if (kind == 0) {
-    rad[0] = C.lo[v[rep] * 3 + 0];
-    rad[1] = C.lo[v[rep] * 3 + 1];
-    rad[2] = C.lo[v[rep] * 3 + 2];
+    rad[0] = C.lo[vrep * 3 + 0];
+    rad[1] = C.lo[vrep * 3 + 1];
+    rad[2] = C.lo[vrep * 3 + 2];
   } else {
-    const float* m = C.media + (size_t)(C.pre[v[rep]] + ring) * 3;
+    const float* m = C.media + (size_t)(C.pre[vrep] + ring) * 3;
     rad[0] = m[0];
     rad[1] = m[1];
     rad[2] = m[2];
   }
+#if VC_ASM_F32
+  if constexpr (D == 3) {
+    // float32 element math (the 3D form is fp32-safe) on lengths scaled by
+    // 1/L, L = the largest vertex distance; the ok-mask stays the float64 one: decided here
+    // when |A| clears its threshold by far more than the float32 error (≤ 12u·Πr_i against
+    // 1e-5·Πr_i), else by ff_triangle_ok.  A non-finite float32 result takes the float64 path.
+    const double L = fmax(dist[0], fmax(dist[1], dist[2]));
+    const double iL = 1.0 / L;
+    float r32[3][3], rr[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) r32[j][a] = (float)(rv[j][a] * iL);
+      rr[j] = sqrtf(r32[j][0] * r32[j][0] + r32[j][1] * r32[j][1] + r32[j][2] * r32[j][2]);
+    }
+    const float A32 = r32[0][0] * (r32[1][1] * r32[2][2] - r32[1][2] * r32[2][1]) +
+                      r32[0][1] * (r32[1][2] * r32[2][0] - r32[1][0] * r32[2][2]) +
+                      r32[0][2] * (r32[1][0] * r32[2][1] - r32[1][1] * r32[2][0]);
+    const bool sure = rr[0] > 0.0f && rr[1] > 0.0f && rr[2] > 0.0f && fabsf(A32) >= 1e-5f * rr[0] * rr[1] * rr[2];
+    if (!sure && !ff_triangle_ok(rv[0], rv[1], rv[2])) return false;
+    float F32, g32[3], H32[6], q32[10];
+    ff_triangle_f32(r32[0], r32[1], r32[2], F32, g32, H32);
+    float w32[3];  // −r32[rep] by selects (no local-memory indexing)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) w32[a] = -(rep == 0 ? r32[0][a] : (rep == 1 ? r32[1][a] : r32[2][a]));
+    const double drep = rep == 0 ? dist[0] : (rep == 1 ? dist[1] : dist[2]);
+    element_q_f32(w32, (float)(drep * iL), (float)(S.sigma_t * L), F32, g32, H32, q32);
+    bool fin = true;
+#pragma unroll
+    for (int t = 0; t < 10; ++t) fin = fin && isfinite(q32[t]);
+    if (fin) {
+      const double sc[3] = {1.0, iL, iL * iL};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double f = wt * rad[c];
+        const float fs[3] = {(float)f, (float)(f * sc[1]), (float)(f * sc[2])};
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) cvec[c * NQ + t] = (CT)(fs[t == 0 ? 0 : (t < 4 ? 1 : 2)] * q32[t]);
+      }
+      return true;
+    }
+  }
+#endif
   double F, gF[D], HF[D * (D + 1) / 2];
   bool ok;
   if constexpr (D == 3) ok = ff_triangle(rv[0], rv[1], rv[2], F, gF, HF);
@@ -1916,27 +1986,28 @@ __device__ __forceinline__ bool asm_item(const DevScene& S, const AsmCtx<D>& C, 
   if (!ok) return false;
   double w[D], q[NQ];
 #pragma unroll
-  for (int a = 0; a < D; ++a) w[a] = -rv[rep][a];
-  element_q<D>(w, dist[rep], S.sigma_t, F, gF, HF, q);
+  for (int a = 0; a < D; ++a) w[a] = -(rep == 0 ? rv[0][a] : (rep == 1 || D == 2 ? rv[1][a] : rv[D - 1][a]));
+  element_q<D>(w, rep == 0 ? dist[0] : (rep == 1 || D == 2 ? dist[1] : dist[D - 1]), S.sigma_t, F, gF, HF, q);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const double f = wt * rad[c];
 #pragma unroll
-    for (int t = 0; t < NQ; ++t) cvec[c * NQ + t] = f * q[t];
+    for (int t = 0; t < NQ; ++t) cvec[c * NQ + t] = (CT)(f * q[t]);
   }
   return true;
 }
 
 // Warp transpose-reduction: every lane holds 32 values v[0..31]; afterwards lane l holds
 // Σ_lanes v[l] in v[0] (31 double shuffles; no per-lane persistent accumulators).
-__device__ __forceinline__ void warp_transpose_sum(double (&v)[32], int lane) {
+template <class T>
+__device__ __forceinline__ void warp_transpose_sum(T (&v)[32], int lane) {
 #pragma unroll
   for (int h = 16; h >= 1; h >>= 1) {
     const bool up = lane & h;
 #pragma unroll
     for (int k = 0; k < h; ++k) {
-      double send = up ? v[k] : v[k + h];
-      double keep = up ? v[k + h] : v[k];
+      T send = up ? v[k] : v[k + h];
+      T keep = up ? v[k + h] : v[k];
       v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
     }
   }
@@ -1990,10 +2061,10 @@ __global__ void __launch_bounds__(kAsmBS, EMIT ? VC_ASM_SCAN_MINB : VC_ASM_MINB)
     int qn = 0;        // warp-uniform queue length
 
     // contribution of one queued item (element e at ring `ring`, representative slot rep)
-    auto eval_item = [&](uint2 it, double (&cvec)[32]) {
+    auto eval_item = [&](uint2 it, AsmT<D> (&cvec)[32]) {
       int v[D];
       elem_vertices<D>(W, P, rec, (int)it.x, v);
-      const bool ok = asm_item<D>(S, ring_ctx, kind, wt, v, (int)(it.y >> 2), (int)(it.y & 3u), cvec);
+      const bool ok = asm_item<D, AsmT<D>>(S, ring_ctx, kind, wt, v, (int)(it.y >> 2), (int)(it.y & 3u), cvec);
       ++n_eval;
       ++ev_kind[kind];
       if (!ok) ++n_drop;
@@ -2011,7 +2082,7 @@ __global__ void __launch_bounds__(kAsmBS, EMIT ? VC_ASM_SCAN_MINB : VC_ASM_MINB)
         fill += m;
         return;
       }
-      double cvec[32];
+      AsmT<D> cvec[32];
 #pragma unroll
       for (int t = 0; t < 32; ++t) cvec[t] = 0.0;
       if (valid) eval_item(it, cvec);
@@ -2217,11 +2288,11 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_EVAL_MINB) k_asm_eval(DevScene 
 #pragma unroll
       for (int j = 0; j < D; ++j) vc[j] = v[j];
       fetch(t + 32);
-      double cvec[32];
+      AsmT<D> cvec[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) cvec[c] = 0.0;
       if (valid) {
-        if (!asm_item<D>(S, C, kind, wt, vc, (int)(qc.y >> 2), (int)(qc.y & 3u), cvec)) ++n_drop;
+        if (!asm_item<D, AsmT<D>>(S, C, kind, wt, vc, (int)(qc.y >> 2), (int)(qc.y & 3u), cvec)) ++n_drop;
         ++n_eval;
         ++ev_kind[kind];
       }
@@ -2393,12 +2464,21 @@ void launch_trace(const DevScene& S, int m, const double* o, const double* d, do
 // Host launch sequence for one wave
 // ---------------------------------------------------------------------------
 
+// Dynamic shared memory of a 256-thread ray kernel: one traversal stack column per thread.
+template <class K>
+static size_t stack_smem(K kernel, const DevBvh& H) {
+  if (!VC_SMEM_STACK) return 0;
+  const size_t bytes = (size_t)(H.n_nodes ? H.stack_need : 0) * 256 * sizeof(uint2);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return bytes;
+}
+
 template <int D>
 static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt,
                           int* own, int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
   const long long nt = (long long)W.B * P.n_angular;
   prof_begin(KC_PRIMARY, st);
-  k_primary<D><<<grid_for(nt, 256), 256, 0, st>>>(S, P, W, jt);
+  k_primary<D><<<grid_for(nt, 256), 256, stack_smem(k_primary<D>, S.geo), st>>>(S, P, W, jt);
   prof_end(st);
   prof_begin(KC_RINGS, st);
   k_rings<<<W.B, kRingBS, 0, st>>>(P, W);
@@ -2417,7 +2497,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       cudaMemsetAsync(W.gather_q_count, 0, sizeof(unsigned long long), st);
       k_gather_emit<D><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                       W.gather_q_cap);
-      k_gather_occl<D><<<sm_count * 8, 256, 0, st>>>(S, W, P.n_angular, (const GatherItem*)W.gather_q,
+      k_gather_occl<D><<<sm_count * 8, 256, stack_smem(k_gather_occl<D>, S.geo), st>>>(
+                                                     S, W, P.n_angular, (const GatherItem*)W.gather_q,
                                                      W.gather_q_count,
                                                      W.gather_q_cap, W.media);
       nl += 2;

@@ -33,6 +33,8 @@ struct HostBVH {
   int n_nodes = 0;
   float4* nodes = nullptr;  // host array, 2*n_nodes
   int* order = nullptr;     // leaf order → original primitive
+  unsigned char* leaf_last = nullptr;  // leaf order: 1 on the last primitive of each leaf
+  int max_depth = 0;        // deepest leaf (bounds the traversal stack)
 };
 void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, int leaf_max = 0);
 void free_bvh(HostBVH* b);

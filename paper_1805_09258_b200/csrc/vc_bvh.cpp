@@ -182,9 +182,11 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, in
   out->n_nodes = n_inner;
   out->nodes = (float4*)malloc(sizeof(float4) * 4 * (size_t)n_inner);
   out->order = (int*)malloc(sizeof(int) * (size_t)std::max(K, 1));
+  // child reference: interior-node index, or the leaf's first primitive with bit 31 set
+  // (the traversal walks a leaf up to the primitive whose id carries the last-in-leaf flag)
   auto entry = [&](float4* dst, int c) {
     const Node& n = nodes[c];
-    const int ref = n.count > 0 ? n.first : inner[c];
+    const int ref = n.count > 0 ? (int)((unsigned)n.first | 0x80000000u) : inner[c];
     float fr, fc;
     std::memcpy(&fr, &ref, 4);
     std::memcpy(&fc, &n.count, 4);
@@ -203,13 +205,34 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, in
     }
   }
   std::memcpy(out->order, order.data(), sizeof(int) * K);
+  // leaf extents (leaf order) and the traversal stack bound: a push happens only below an
+  // interior node, so the stack never holds more entries than the deepest interior level
+  out->leaf_last = (unsigned char*)calloc((size_t)std::max(K, 1), 1);
+  int depth_max = 0;
+  std::vector<std::pair<int, int>> todo;  // (node, depth)
+  todo.push_back({0, 0});
+  while (!todo.empty()) {
+    auto [i, dep] = todo.back();
+    todo.pop_back();
+    const Node& n = nodes[i];
+    if (n.count > 0) {
+      out->leaf_last[n.first + n.count - 1] = 1;
+      depth_max = std::max(depth_max, dep);
+      continue;
+    }
+    todo.push_back({n.first, dep + 1});
+    todo.push_back({n.first + 1, dep + 1});
+  }
+  out->max_depth = depth_max;
 }
 
 void free_bvh(HostBVH* b) {
   free(b->nodes);
   free(b->order);
+  free(b->leaf_last);
   b->nodes = nullptr;
   b->order = nullptr;
+  b->leaf_last = nullptr;
   b->n_nodes = 0;
 }
 

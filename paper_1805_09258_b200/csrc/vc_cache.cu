@@ -20,66 +20,106 @@ namespace vc {
 // ---------------------------------------------------------------------------
 
 struct IdxGeom {
-  int dim, L0;
-  double origin[3], size;
-  const long long* level_off;
+  int dim;
+  double origin[3], size, inv_size;
 };
 
-// Level and cell box of record R; false → overflow list (box leaves the root cube).
-__device__ inline bool record_cells(const IdxGeom& G, const double* R, int& lv, long long clo[3], long long chi[3]) {
+// Level and cell range of record R; false → overflow list (box leaves the root cube or is
+// not finite).  The box is the AABB of the support ellipsoid {Δ : Σ_j (Δ·A_j / r_j)² ≤ 1}
+// with orthonormal axes A_j: half-extent e_a = √(Σ_j A_aj² r_j²) (≤ the reference tree's
+// max radius), padded for the float64 support test's rounding and the rounding of pos ± e.
+// Cell coordinates use the query's map u = (x − origin)·(1/size), floor(u·2^k): both sides
+// apply the same monotone function, so a covered point's cell lies in the record's range.
+__device__ inline bool record_cells(const IdxGeom& G, const double* R, int& lv, int clo[3], int chi[3]) {
   const int d = G.dim;
-  const double* rad = R + d + 3 + 3 * d + d * d;
-  double br = 0.0;
-  for (int a = 0; a < d; ++a) br = fmax(br, rad[a]);
-  br = br * (1.0 + 1e-9) + 1e-12 * G.size;
-  bool fits = isfinite(br);
-  double lo[3], hi[3];
+  const double* ax = R + d + 3 + 3 * d;
+  const double* rad = ax + d * d;
+  double e[3] = {0, 0, 0}, emax = 0.0;
+  bool fits = true;
   for (int a = 0; a < d; ++a) {
-    lo[a] = R[a] - br;
-    hi[a] = R[a] + br;
-    if (!(lo[a] >= G.origin[a] && hi[a] <= G.origin[a] + G.size)) fits = false;
+    double q = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double t = ax[a * d + j] * rad[j];
+      q += t * t;
+    }
+    e[a] = sqrt(q) * (1.0 + 1e-9) + 1e-12 * G.size + 1e-14 * (fabs(R[a]) + G.size);
+    fits = fits && isfinite(e[a]);
+    emax = fmax(emax, e[a]);
+  }
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  for (int a = 0; a < d && fits; ++a) {
+    lo[a] = (R[a] - e[a] - G.origin[a]) * G.inv_size;
+    hi[a] = (R[a] + e[a] - G.origin[a]) * G.inv_size;
+    if (!(lo[a] >= 0.0 && hi[a] < 1.0)) fits = false;
   }
   if (!fits) return false;
-  lv = 0;
-  while (lv < G.L0 && G.size / (double)(1LL << (G.L0 - lv)) < 2.0 * br) ++lv;
-  const long long N = 1LL << (G.L0 - lv);
-  const double h = G.size / (double)N;
+  lv = 0;  // deepest level whose cells are ≥ 2·emax
+  while (lv < kMaxLevel && G.size / (double)(1 << (lv + 1)) >= 2.0 * emax) ++lv;
+  const double s = (double)(1 << lv);
   for (int a = 0; a < 3; ++a) clo[a] = chi[a] = 0;
   for (int a = 0; a < d; ++a) {
-    clo[a] = min(max((long long)floor((lo[a] - G.origin[a]) / h), 0LL), N - 1);
-    chi[a] = min(max((long long)floor((hi[a] - G.origin[a]) / h), 0LL), N - 1);
+    clo[a] = min((int)floor(lo[a] * s), (1 << lv) - 1);
+    chi[a] = min((int)floor(hi[a] * s), (1 << lv) - 1);
   }
   return true;
 }
 
-__global__ void k_idx_count(IdxGeom G, const double* rec, int n, int* cnt, int* ovf) {
+__global__ void k_idx_count(IdxGeom G, const double* rec, int n, int* cnt, int* ovf, unsigned* lmask) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
-  int lv;
-  long long clo[3], chi[3];
+  int lv, clo[3], chi[3];
   bool fits = record_cells(G, rec + (size_t)r * record_size(G.dim), lv, clo, chi);
-  long long c = 0;
-  if (fits) c = (chi[0] - clo[0] + 1) * (chi[1] - clo[1] + 1) * (chi[2] - clo[2] + 1);
-  cnt[r] = (int)c;
+  int c = 0;
+  if (fits) {
+    c = (chi[0] - clo[0] + 1) * (chi[1] - clo[1] + 1) * (chi[2] - clo[2] + 1);
+    atomicOr(lmask, 1u << lv);
+  }
+  cnt[r] = c;
   ovf[r] = fits ? 0 : 1;
 }
 
-__global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, unsigned* keys, int* vals) {
+__global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, unsigned long long* keys, int* vals) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
-  int lv;
-  long long clo[3], chi[3];
+  int lv, clo[3], chi[3];
   if (!record_cells(G, rec + (size_t)r * record_size(G.dim), lv, clo, chi)) return;
-  const long long N = 1LL << (G.L0 - lv);
   int o = off[r];
-  for (long long z = clo[2]; z <= chi[2]; ++z)
-    for (long long y = clo[1]; y <= chi[1]; ++y)
-      for (long long x = clo[0]; x <= chi[0]; ++x) {
-        long long cell = (G.dim == 3) ? (z * N + y) * N + x : y * N + x;
-        keys[o] = (unsigned)(G.level_off[lv] + cell);
+  for (int z = clo[2]; z <= chi[2]; ++z)
+    for (int y = clo[1]; y <= chi[1]; ++y)
+      for (int x = clo[0]; x <= chi[0]; ++x) {
+        keys[o] = (unsigned long long)lv << 48 | (unsigned long long)z << 32 | (unsigned long long)y << 16 |
+                  (unsigned long long)x;
         vals[o] = r;
         ++o;
       }
+}
+
+// One thread per sorted entry: the first entry of each cell run inserts the cell into the
+// open-addressing table with its [start, end) range.
+__global__ void k_idx_hash(const unsigned long long* keys, int T, int hbits, unsigned long long* hkey,
+                           int2* hrange) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const unsigned long long k = keys[t];
+  if (t > 0 && keys[t - 1] == k) return;
+  int end = t + 1;
+  while (end < T && keys[end] == k) ++end;
+  const unsigned hm = (1u << hbits) - 1u;
+  for (unsigned h = hash_slot(k, hbits);; h = (h + 1) & hm) {
+    const unsigned long long prev = atomicCAS(hkey + h, ~0ULL, k);
+    if (prev == ~0ULL) {
+      hrange[h] = make_int2(t, end);
+      return;
+    }
+  }
+}
+
+// rows[t] = side[items[t]]: the rejection rows in entry order (contiguous scans)
+__global__ void k_idx_rows(const int* items, int T, const float4* side, float4* rows) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)T * kSide) return;
+  const long long t = i / kSide;
+  rows[i] = side[(size_t)items[t] * kSide + (i - t * kSide)];
 }
 
 // float32 rejection rows (vc_cache.cuh, DevCache::side).  tol bounds |q32 − q| for points with
@@ -124,28 +164,6 @@ __global__ void k_idx_side(const double* rec, int n, int dim, float4* side) {
     o[0] = make_float4((float)R[0], (float)R[1], (float)tol, (float)M[0][0]);
     o[1] = make_float4((float)M[0][1], (float)M[1][0], (float)M[1][1], 0.0f);
   }
-}
-
-// level of each record → bitmask of non-empty levels
-__global__ void k_idx_levels(IdxGeom G, const double* rec, int n, unsigned* mask) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  int lv;
-  long long clo[3], chi[3];
-  if (record_cells(G, rec + (size_t)r * record_size(G.dim), lv, clo, chi)) atomicOr(mask, 1u << lv);
-}
-
-// cell_start[c] = first sorted entry with key ≥ c, for c in [0, n_cells]
-__global__ void k_idx_starts(const unsigned* keys, int T, long long n_cells, int* start) {
-  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > n_cells) return;
-  int lo = 0, hi = T;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if ((long long)keys[mid] < c) lo = mid + 1;
-    else hi = mid;
-  }
-  start[c] = lo;
 }
 
 __global__ void k_cache_gather(const double* src, size_t stride, const int* sel, const long long* tags, int k, int RS,
@@ -222,22 +240,11 @@ int cache_init(vc_cache* c, int dim, const double* bmin, const double* bmax) {
   double half = 0.5 * mx + 0.25 * diag;
   for (int a = 0; a < dim; ++a) c->origin[a] = 0.5 * (bmin[a] + bmax[a]) - half;
   c->size = 2.0 * half;
-  c->L0 = dim == 3 ? 7 : 10;
-  // levels: N_ℓ = 2^(L0−ℓ) cells per axis
-  c->level_off.assign(c->L0 + 2, 0);
-  long long tot = 0;
-  for (int lv = 0; lv <= c->L0; ++lv) {
-    c->level_off[lv] = tot;
-    long long N = 1LL << (c->L0 - lv);
-    tot += (dim == 3) ? N * N * N : N * N;
-  }
-  c->level_off[c->L0 + 1] = tot;
-  c->n_cells = tot;
-  cudaError_t e = cudaMalloc(&c->d_level_off, c->level_off.size() * 8);
-  if (e == cudaSuccess)
-    e = cudaMemcpy(c->d_level_off, c->level_off.data(), c->level_off.size() * 8, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_cell_start, (size_t)(tot + 1) * 4);
-  if (e == cudaSuccess) e = cudaMemset(c->d_cell_start, 0, (size_t)(tot + 1) * 4);
+  c->hbits = 10;
+  c->hcap = 1u << c->hbits;
+  cudaError_t e = cudaMalloc(&c->d_hkey, c->hcap * 8);
+  if (e == cudaSuccess) e = cudaMemset(c->d_hkey, 0xff, c->hcap * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_hrange, c->hcap * sizeof(int2));
   if (e != cudaSuccess) return cuda_fail(e, "cache index allocation");
   return VC_OK;
 }
@@ -298,48 +305,42 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   if (n == 0) {
     c->n_overflow = 0;
     c->level_mask = 0;
-    e = cudaMemsetAsync(c->d_cell_start, 0, (size_t)(c->n_cells + 1) * 4, st);
+    e = cudaMemsetAsync(c->d_hkey, 0xff, c->hcap * 8, st);
     if (e == cudaSuccess && !c->d_items) e = cudaMalloc(&c->d_items, 16);
+    if (e == cudaSuccess && !c->d_rows) e = cudaMalloc(&c->d_rows, 16 * kSide);
     if (e == cudaSuccess && !c->d_overflow) e = cudaMalloc(&c->d_overflow, 16);
     return e == cudaSuccess ? VC_OK : cuda_fail(e, "cache index reset");
   }
   IdxGeom G{};
   G.dim = c->dim;
-  G.L0 = c->L0;
   for (int a = 0; a < 3; ++a) G.origin[a] = c->origin[a];
   G.size = c->size;
-  G.level_off = c->d_level_off;
+  G.inv_size = 1.0 / c->size;
   int* cnt = (int*)alloc(0, (size_t)n * 4);
   int* ovf = (int*)alloc(1, (size_t)n * 4);
   int* off = (int*)alloc(2, ((size_t)n + 1) * 4);
+  int* cnt1 = (int*)alloc(3, ((size_t)n + 1) * 4);
+  int* n_sel = (int*)alloc(6, 16);
+  int* ovf_list = (int*)alloc(5, (size_t)n * 4);
+  int* iota = (int*)alloc(12, (size_t)n * 4);
   if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
+  unsigned* lmask = (unsigned*)(n_sel + 2);
+  e = cudaMemsetAsync(lmask, 0, 4, st);
   const int nb = (n + 127) / 128;
   k_idx_side<<<nb, 128, 0, st>>>(c->d_rec, n, c->dim, c->d_side);
-  k_idx_count<<<nb, 128, 0, st>>>(G, c->d_rec, n, cnt, ovf);
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, st);
-  // scan n+1 entries: the last input is read past cnt[n-1]; give it a zero slot
-  int* cnt1 = (int*)alloc(3, ((size_t)n + 1) * 4);
-  if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
-  e = cudaMemcpyAsync(cnt1, cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+  k_idx_count<<<nb, 128, 0, st>>>(G, c->d_rec, n, cnt, ovf, lmask);
+  // scan n+1 entries (the last one a zero slot) → per-record entry offsets and the total
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cnt1, cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(cnt1 + n, 0, 4, st);
-  void* tmp = alloc(4, tb);
+  size_t tb = 0, sb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt1, off, n + 1, st);
+  cub::DeviceSelect::Flagged(nullptr, sb, iota, ovf, ovf_list, n_sel, n, st);
+  void* tmp = alloc(4, std::max(tb, sb));
   if (e != cudaSuccess) return cuda_fail(e, "cache index scan");
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt1, off, n + 1, st);
   // overflow list (record order) and its count
-  int* ovf_list = (int*)alloc(5, (size_t)n * 4);
-  int* n_sel = (int*)alloc(6, 16);
-  size_t sb = 0;
-  int* iota = (int*)alloc(12, (size_t)n * 4);
-  if (e != cudaSuccess) return cuda_fail(e, "cache index scratch");
   k_iota<<<nb, 128, 0, st>>>(iota, n);
-  cub::DeviceSelect::Flagged(nullptr, sb, iota, ovf, ovf_list, n_sel, n, st);
-  void* stmp = alloc(7, sb);
-  if (e != cudaSuccess) return cuda_fail(e, "cache index select");
-  cub::DeviceSelect::Flagged(stmp, sb, iota, ovf, ovf_list, n_sel, n, st);
-  unsigned* lmask = (unsigned*)(n_sel + 2);
-  e = cudaMemsetAsync(lmask, 0, 4, st);
-  k_idx_levels<<<nb, 128, 0, st>>>(G, c->d_rec, n, lmask);
+  cub::DeviceSelect::Flagged(tmp, sb, iota, ovf, ovf_list, n_sel, n, st);
   int hv[3] = {0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[0], off + n, 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[1], n_sel, 4, cudaMemcpyDeviceToHost, st);
@@ -349,32 +350,50 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   const int T = hv[0];
   c->n_overflow = hv[1];
   c->level_mask = (unsigned)hv[2];
-  unsigned* keys = (unsigned*)alloc(8, (size_t)T * 4 + 4);
+  unsigned long long* keys = (unsigned long long*)alloc(8, (size_t)T * 8 + 8);
   int* vals = (int*)alloc(9, (size_t)T * 4 + 4);
-  unsigned* keys2 = (unsigned*)alloc(10, (size_t)T * 4 + 4);
+  unsigned long long* keys2 = (unsigned long long*)alloc(10, (size_t)T * 8 + 8);
   if (c->items_cap < (size_t)T + 1) {
     cudaFree(c->d_items);
+    cudaFree(c->d_rows);
     c->d_items = nullptr;
+    c->d_rows = nullptr;
     size_t cap = std::max<size_t>((size_t)T + 1, c->items_cap * 2);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_items, cap * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_rows, cap * kSide * sizeof(float4));
     c->items_cap = e == cudaSuccess ? cap : 0;
   }
+  // hash table: ≥ 2 slots per entry (≥ 2 per occupied cell), power of two
+  int hbits = 10;
+  while (hbits < 30 && (1ULL << hbits) < 2ULL * (unsigned long long)T) ++hbits;
+  if ((1ULL << hbits) > c->hcap) {
+    cudaFree(c->d_hkey);
+    cudaFree(c->d_hrange);
+    c->d_hkey = nullptr;
+    c->d_hrange = nullptr;
+    c->hcap = 1ULL << hbits;
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_hkey, c->hcap * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_hrange, c->hcap * sizeof(int2));
+  }
+  c->hbits = hbits;
   cudaFree(c->d_overflow);
   c->d_overflow = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&c->d_overflow, (size_t)c->n_overflow * 4 + 4);
   if (e == cudaSuccess && c->n_overflow)
     e = cudaMemcpyAsync(c->d_overflow, ovf_list, (size_t)c->n_overflow * 4, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_hkey, 0xff, (1ULL << hbits) * 8, st);
   if (e != cudaSuccess) return cuda_fail(e, "cache index buffers");
   k_idx_emit<<<nb, 128, 0, st>>>(G, c->d_rec, n, off, keys, vals);
   // stable sort by cell keeps records in insertion order within a cell
-  int end_bit = 1;
-  while (end_bit < 32 && (1LL << end_bit) <= c->n_cells) ++end_bit;
   size_t rb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, c->d_items, T, 0, 53, st);
   void* rtmp = alloc(11, rb);
   if (e != cudaSuccess) return cuda_fail(e, "cache index sort scratch");
-  if (T > 0) cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
-  k_idx_starts<<<(int)((c->n_cells + 1 + 255) / 256), 256, 0, st>>>(keys2, T, c->n_cells, c->d_cell_start);
+  if (T > 0) {
+    cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, 53, st);
+    k_idx_hash<<<(T + 127) / 128, 128, 0, st>>>(keys2, T, hbits, c->d_hkey, c->d_hrange);
+    k_idx_rows<<<(int)(((long long)T * kSide + 255) / 256), 256, 0, st>>>(c->d_items, T, c->d_side, c->d_rows);
+  }
   count_launches(9);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "cache index build");

@@ -2,13 +2,18 @@
 // shared by the lookup, the camera march and the populate engine.
 //
 // Index: the reference keeps records in an MX-CIF tree whose point query returns
-// exactly the records with support > 0 (src/cache.py:262-334, ≡ linear scan).  Here a
-// record of bounding radius r lives on the coarsest-needed level ℓ of a pyramid of
-// dense grids over the same padded root cube (cell size h_ℓ ≥ 2r, so its box touches
-// ≤ 2^d cells); a query visits one cell per level plus the overflow list of records
-// whose box leaves the root cube, and applies the reference's strict support test —
-// the covering set is identical to the linear scan.  The index is rebuilt on the
-// device (counting pass → scan → stable radix sort by cell) after every insert batch.
+// exactly the records with support > 0 (src/cache.py:262-334, ≡ linear scan).  Here the
+// index is a spatial hash over a pyramid of grids on the same padded root cube: level k
+// has 2^k cells per axis (k ≤ 16, the reference tree's depth cap), and a record is listed
+// in every cell of the deepest level whose cells are at least twice its axis-aligned
+// extent (the exact AABB of its support ellipsoid, padded) — ≤ 2^d cells.  Occupied cells
+// sit in an open-addressing table (key = level and cell coordinates) mapping to their run
+// of entries; each entry carries the record's float32 rejection row inline, so a lookup
+// scans contiguous rows.  A query probes one cell per occupied level plus the overflow
+// list of records whose box leaves the root cube, and applies the reference's strict
+// support test — the covering set is identical to the linear scan.  The index is rebuilt
+// on the device (count → scan → stable radix sort by cell → hash insert) after every insert
+// batch.
 //
 // Every record carries a tag (the ordinal of the march point that created it, or −1):
 // a query with limit t sees only records with tag < t, which is how the populate
@@ -24,20 +29,7 @@
 
 namespace vc {
 
-struct DevCache {
-  int dim, n, L0, n_overflow;
-  int blend;                   // 0: ellipsoid records, linear blend; 1: sphere records, log-space blend
-  double origin[3];
-  double size;
-  const long long* level_off;  // L0+2 entries: first cell index of each level
-  const int* cell_start;       // per cell start into items (+1 sentinel)
-  const int* items;
-  const int* overflow;
-  const double* rec;           // n × record_size(dim), reference layout
-  const long long* tag;        // n creation ordinals
-  const float4* side;          // n × kSide float32 rejection rows (record_side)
-  unsigned level_mask;         // bit ℓ: level ℓ lists at least one record
-};
+constexpr int kMaxLevel = 16;  // finest grid: 2^16 cells per axis
 
 // float32 rejection row of a record: position, M = axes / radii (column j scaled by
 // 1/radius_j; for sphere records I / radius) and tol, a bound on |q32 − q| for every point
@@ -46,17 +38,39 @@ struct DevCache {
 // {M22 0 0 0}; 2D: {p.xy, tol, M00}, {M01 M10 M11 0}.
 constexpr int kSide = 4;
 
+struct DevCache {
+  int dim, n, n_overflow;
+  int blend;                   // 0: ellipsoid records, linear blend; 1: sphere records, log-space blend
+  double origin[3];
+  double size, inv_size;       // root cube
+  unsigned level_mask;         // bit k: level k lists at least one record
+  int hbits;                   // hash table: 2^hbits slots
+  const unsigned long long* hkey;  // cell key per slot (~0: empty): k << 48 | z << 32 | y << 16 | x
+  const int2* hrange;          // the cell's entries [start, end)
+  const int* items;            // record of each entry (cell order; insertion order within a cell)
+  const float4* rows;          // kSide rejection rows per entry (copies of side[items[t]])
+  const int* overflow;
+  const double* rec;           // n × record_size(dim), reference layout
+  const long long* tag;        // n creation ordinals
+  const float4* side;          // n × kSide float32 rejection rows (record_side)
+};
+
+__host__ __device__ __forceinline__ unsigned hash_slot(unsigned long long key, int hbits) {
+  return (unsigned)((key * 0x9E3779B97F4A7C15ULL) >> (64 - hbits));
+}
+
 }  // namespace vc
 
 struct vc_cache {
-  int dim = 0, n = 0, L0 = 0;
+  int dim = 0, n = 0;
   int blend = 0;  // 1: baseline cache (BaselineRecord spheres, log_space_interpolate)
   double origin[3] = {0, 0, 0}, size = 0.0;
-  long long n_cells = 0;
-  std::vector<long long> level_off;
-  long long* d_level_off = nullptr;
-  int* d_cell_start = nullptr;
+  unsigned long long* d_hkey = nullptr;
+  int2* d_hrange = nullptr;
+  int hbits = 0;
+  size_t hcap = 0;
   int* d_items = nullptr;
+  float4* d_rows = nullptr;
   size_t items_cap = 0;
   int* d_overflow = nullptr;
   int n_overflow = 0;
@@ -70,25 +84,28 @@ struct vc_cache {
     vc::DevCache c{};
     c.dim = dim;
     c.n = n;
-    c.L0 = L0;
     c.n_overflow = n_overflow;
     c.blend = blend;
     for (int a = 0; a < 3; ++a) c.origin[a] = origin[a];
     c.size = size;
-    c.level_off = d_level_off;
-    c.cell_start = d_cell_start;
+    c.inv_size = 1.0 / size;
+    c.level_mask = level_mask;
+    c.hbits = hbits;
+    c.hkey = d_hkey;
+    c.hrange = d_hrange;
     c.items = d_items;
+    c.rows = d_rows;
     c.overflow = d_overflow;
     c.rec = d_rec;
     c.tag = d_tag;
     c.side = d_side;
-    c.level_mask = level_mask;
     return c;
   }
   ~vc_cache() {
-    cudaFree(d_level_off);
-    cudaFree(d_cell_start);
+    cudaFree(d_hkey);
+    cudaFree(d_hrange);
     cudaFree(d_items);
+    cudaFree(d_rows);
     cudaFree(d_overflow);
     cudaFree(d_rec);
     cudaFree(d_tag);
@@ -235,37 +252,10 @@ __device__ __forceinline__ void blend_record(const double* R, const double* x, d
   den = add(den, w);
 }
 
-// Visit the candidate records of x in tree order (root level first, then the overflow
-// list); f(record_index) returns true to stop early.
-template <int D, typename F>
-__device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, F&& f) {
-  for (int lv = C.L0; lv >= 0; --lv) {  // coarse → fine (tree order: root first)
-    if (!((C.level_mask >> lv) & 1u)) continue;
-    const int N = 1 << (C.L0 - lv);
-    const double h = C.size / N;
-    long long cell = 0;
-    bool inside = true;
-#pragma unroll
-    for (int a = D - 1; a >= 0; --a) {
-      double fl = floor((x[a] - C.origin[a]) / h);
-      if (!(fl >= 0.0 && fl < (double)N)) inside = false;
-      cell = cell * N + (inside ? (long long)fl : 0);
-    }
-    if (!inside) continue;
-    long long ci = C.level_off[lv] + cell;
-    int b = C.cell_start[ci], e = C.cell_start[ci + 1];
-    for (int t = b; t < e; ++t)
-      if (f(C.items[t])) return;
-  }
-  for (int t = 0; t < C.n_overflow; ++t)
-    if (f(C.overflow[t])) return;
-}
-
-// float32 rejection: true when record r certainly has support ≤ 0 at x (see record_side);
-// x32 is x rounded to float32.  NaN (a zero radius) never rejects: the exact test decides.
+// float32 rejection of a row (see record_side): true when the record certainly has
+// support ≤ 0 at x; x32 is x rounded to float32.  NaN (a zero radius) never rejects.
 template <int D>
-__device__ __forceinline__ bool side_rejects(const DevCache& C, int r, const float* x32) {
-  const float4* sd = C.side + (size_t)r * kSide;
+__device__ __forceinline__ bool row_rejects(const float4* sd, const float* x32) {
   const float4 s0 = __ldg(sd), s1 = __ldg(sd + 1);
   if constexpr (D == 3) {
     const float4 s2 = __ldg(sd + 2), s3 = __ldg(sd + 3);
@@ -281,6 +271,45 @@ __device__ __forceinline__ bool side_rejects(const DevCache& C, int r, const flo
     const float a1 = d0 * s1.x + d1 * s1.z;
     const float q = a0 * a0 + a1 * a1;
     return q > 1.0f + s0.z;
+  }
+}
+
+// Visit the records of x that survive the float32 rejection, in index order (coarse level
+// first, then the overflow list); f(record_index) returns true to stop early.
+template <int D, typename F>
+__device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, F&& f) {
+  float x32[D];
+  double u[D];
+  bool in = true;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    x32[a] = (float)x[a];
+    u[a] = (x[a] - C.origin[a]) * C.inv_size;  // the same map as the registration (k_idx_*)
+    in = in && u[a] >= 0.0 && u[a] < 1.0;
+  }
+  if (in) {
+    for (unsigned m = C.level_mask; m; m &= m - 1) {
+      const int k = __ffs(m) - 1;
+      const double s = (double)(1u << k);
+      unsigned long long key = (unsigned long long)k << 48;
+#pragma unroll
+      for (int a = 0; a < D; ++a) key |= (unsigned long long)min((int)floor(u[a] * s), (1 << k) - 1) << (16 * a);
+      const unsigned hm = (1u << C.hbits) - 1u;
+      for (unsigned h = hash_slot(key, C.hbits);; h = (h + 1) & hm) {
+        const unsigned long long kk = C.hkey[h];
+        if (kk == key) {
+          const int2 r = C.hrange[h];
+          for (int t = r.x; t < r.y; ++t)
+            if (!row_rejects<D>(C.rows + (size_t)t * kSide, x32) && f(C.items[t])) return;
+          break;
+        }
+        if (kk == ~0ULL) break;
+      }
+    }
+  }
+  for (int t = 0; t < C.n_overflow; ++t) {
+    const int r = C.overflow[t];
+    if (!row_rejects<D>(C.side + (size_t)r * kSide, x32) && f(r)) return;
   }
 }
 
@@ -316,12 +345,8 @@ __device__ inline bool cache_interpolate(const DevCache& C, const double* x, dou
   double num[3] = {0.0, 0.0, 0.0}, den[3] = {0.0, 0.0, 0.0};
   int hits = 0;
   const int RS = record_size(D);
-  float x32[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) x32[a] = (float)x[a];
   if (C.blend == 0) {
     cache_visit<D>(C, x, [&](int r) {
-      if (side_rejects<D>(C, r, x32)) return false;
       if (C.tag[r] < limit) blend_record<D>(C.rec + (size_t)r * RS, x, num, den[0], hits);
       return false;
     });
@@ -333,7 +358,6 @@ __device__ inline bool cache_interpolate(const DevCache& C, const double* x, dou
     return true;
   }
   cache_visit<D>(C, x, [&](int r) {
-    if (side_rejects<D>(C, r, x32)) return false;
     if (C.tag[r] < limit) log_blend_record<D>(C.rec + (size_t)r * RS, x, num, den, hits);
     return false;
   });
@@ -352,11 +376,7 @@ template <int D>
 __device__ inline bool cache_covers(const DevCache& C, const double* x, long long limit) {
   const int RS = record_size(D);
   bool hit = false;
-  float x32[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) x32[a] = (float)x[a];
   cache_visit<D>(C, x, [&](int r) {
-    if (side_rejects<D>(C, r, x32)) return false;
     if (C.tag[r] >= limit) return false;
     const double* R = C.rec + (size_t)r * RS;
     double dl[D];

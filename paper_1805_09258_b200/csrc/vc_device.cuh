@@ -191,19 +191,21 @@ __device__ __forceinline__ double hit_prim(const double* P, const double* o, con
   else return hit_seg(P, o, d, t_eps);
 }
 
-// Conservative float32 slab test against a padded node box.
+// Conservative float32 slab test against a padded node box: t = lo·inv − of·inv as one FMA
+// per plane (the rounding it adds is far inside the 1e-5·scale box padding; an exactly zero
+// direction component gives NaN slabs, which fminf/fmaxf drop — that axis then never culls).
 template <int D>
-__device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, const float* of,
-                                        const float* inv, float t_best, float& t_near) {
-  float t0 = (lo.x - of[0]) * inv[0], t1 = (hi.x - of[0]) * inv[0];
+__device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, const float* inv, const float* noi,
+                                        float t_best, float& t_near) {
+  float t0 = fmaf(lo.x, inv[0], noi[0]), t1 = fmaf(hi.x, inv[0], noi[0]);
   float tn = fminf(t0, t1), tf = fmaxf(t0, t1);
-  t0 = (lo.y - of[1]) * inv[1];
-  t1 = (hi.y - of[1]) * inv[1];
+  t0 = fmaf(lo.y, inv[1], noi[1]);
+  t1 = fmaf(hi.y, inv[1], noi[1]);
   tn = fmaxf(tn, fminf(t0, t1));
   tf = fminf(tf, fmaxf(t0, t1));
   if constexpr (D == 3) {
-    t0 = (lo.z - of[2]) * inv[2];
-    t1 = (hi.z - of[2]) * inv[2];
+    t0 = fmaf(lo.z, inv[2], noi[2]);
+    t1 = fmaf(hi.z, inv[2], noi[2]);
     tn = fmaxf(tn, fminf(t0, t1));
     tf = fminf(tf, fmaxf(t0, t1));
   }
@@ -211,151 +213,167 @@ __device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, cons
   return tn <= tf && tf >= 0.0f && tn <= t_best;
 }
 
-// Visit one primitive of a leaf (float64 decision, src/scene.py:242-268).
-template <int D>
-__device__ __forceinline__ double leaf_hit(const DevBvh& H, int k, const double* o, const double* d, double t_eps) {
-  return hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, t_eps);
+// Certified float32 Möller–Trumbore pre-test: true only when the float64 test of
+// hit_tri (src/scene.py:242-268) certainly rejects the triangle, or certainly puts its hit
+// beyond tmax (a float32 upper bound of the current best / threshold distance).
+// With u = 2⁻²⁴, |d|∞ ≤ 1, E ≥ |e1|∞, |e2|∞ and Tb ≥ |o − v0|∞ (origin and vertex both
+// relative to the bounds centre, each rounded once), the float32 values of
+// det = e1·(d×e2), U = (o−v0)·(d×e2), V = d·((o−v0)×e1), T = e2·((o−v0)×e1) are within
+// 48u·E², 54u·Tb·E, 54u·Tb·E and 54u·Tb·E² of the exact ones (input roundings and every
+// product and sum); the margins below are 128u·(…), so a decision taken here also holds
+// for the float64 values (errors ~1e-16 relative).  NaN never rejects.
+__device__ __forceinline__ bool tri_rejects32(const float4& f0, const float4& f1, const float4& f2, const float* orl,
+                                              float Ob, const float* df, float teps, float tmax) {
+  const float E = f1.w;
+  if (!(E > 0.0f)) return false;
+  constexpr float c = 128.0f * 5.9604645e-8f;
+  const float tv0 = orl[0] - f0.x, tv1 = orl[1] - f0.y, tv2 = orl[2] - f0.z;
+  const float pv0 = df[1] * f2.z - df[2] * f2.y;
+  const float pv1 = df[2] * f2.x - df[0] * f2.z;
+  const float pv2 = df[0] * f2.y - df[1] * f2.x;
+  const float det = f1.x * pv0 + f1.y * pv1 + f1.z * pv2;
+  const float eD = c * E * E;
+  const float ad = fabsf(det);
+  if (!(ad > eD)) return false;  // sign of det (or det = 0) not decided here
+  const float sg = det > 0.0f ? 1.0f : -1.0f;
+  const float eU = c * (Ob + f0.w) * E;
+  const float su = sg * (tv0 * pv0 + tv1 * pv1 + tv2 * pv2);
+  if (su < -eU) return true;  // u < 0
+  const float qv0 = tv1 * f1.z - tv2 * f1.y;
+  const float qv1 = tv2 * f1.x - tv0 * f1.z;
+  const float qv2 = tv0 * f1.y - tv1 * f1.x;
+  const float sv = sg * (df[0] * qv0 + df[1] * qv1 + df[2] * qv2);
+  if (sv < -eU) return true;  // v < 0
+  constexpr float r4 = 4.0f * 5.9604645e-8f;
+  if (su + sv - ad > 2.0f * eU + eD + r4 * (fabsf(su) + fabsf(sv) + ad)) return true;  // u + v > 1
+  const float eT = eU * E;
+  const float st = sg * (f2.x * qv0 + f2.y * qv1 + f2.z * qv2);
+  if (st + eT < teps * (ad - eD) * (1.0f - r4)) return true;  // t ≤ t_eps
+  if (st - eT > tmax * (ad + eD) * (1.0f + r4)) return true;  // t beyond the current bound
+  return false;
 }
 
-#ifndef VC_WHILE_WHILE
-#define VC_WHILE_WHILE 1
+// Traversal stacks: entry = (child reference, entry distance bits).  LocalStack is a
+// per-thread array; SharedStack a per-thread column of a CTA's shared-memory block
+// ([entry][thread], conflict-free), sized from DevBvh::stack_need at launch.
+struct LocalStack {
+  uint2 e[kBvhMaxDepth];
+  __device__ __forceinline__ void put(int i, uint2 v) { e[i] = v; }
+  __device__ __forceinline__ uint2 get(int i) const { return e[i]; }
+};
+template <int BS>
+struct SharedStack {
+  uint2* col;  // this thread's column: smem + threadIdx.x
+  __device__ __forceinline__ void put(int i, uint2 v) { col[i * BS] = v; }
+  __device__ __forceinline__ uint2 get(int i) const { return col[i * BS]; }
+};
+
+// Float32 pre-test in the leaf loop: measured r2 per 2048-record wave, primary 6.34 vs 6.15 ms
+// and gather 13.87 vs 13.45 ms with it on — traversal (box tests, stack) dominates, the
+// float64 leaf tests are ~15% of the primary kernel's instructions — so it is off by default.
+#ifndef VC_PRETEST32
+#define VC_PRETEST32 0
 #endif
 
 // Ordered BVH traversal.  mode 0: nearest hit (t_best/id_best out).  mode 1: any hit
 // that precedes (thr, id_thr) in (t, index) order — returns true on the first one.
-// Node layout (vc_bvh.cpp): per interior node the two children's boxes and references.
-template <int D, int MODE>
+// Node layout (vc_bvh.cpp): per interior node the two children's boxes and references
+// (bit 31: leaf, walked up to the primitive flagged last-in-leaf in prim32).
+// while-while: descend interior nodes until a leaf, then test it — the lanes of a warp
+// run the leaf tests together instead of interleaving them with box tests.
+template <int D, int MODE, class Stack>
 __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const double* o, const double* d,
-                          double& t_best, int& id_best) {
-  float of[3] = {0.f, 0.f, 0.f}, inv[3] = {0.f, 0.f, 0.f};
+                          double& t_best, int& id_best, Stack& stk) {
+  float orl[3] = {0.f, 0.f, 0.f}, inv[3] = {0.f, 0.f, 0.f}, noi[3] = {0.f, 0.f, 0.f}, df[3] = {0.f, 0.f, 0.f};
+  float Ob = 0.0f;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    of[a] = (float)o[a];
-#ifndef VC_EXACT_RCP
-    // approximate reciprocal (≤ 1 ulp; ±0 → ±inf): the slab error it adds is far inside
-    // the 1e-5·scale box padding
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv[a]) : "f"((float)d[a]));
-#else
-    inv[a] = 1.0f / (float)d[a];
-#endif
+    orl[a] = (float)(o[a] - H.ctr[a]);
+    df[a] = (float)d[a];
+    // approximate reciprocal (≤ 1 ulp; ±0 → ±inf): inside the box padding
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv[a]) : "f"(df[a]));
+    noi[a] = -orl[a] * inv[a];
+    Ob = fmaxf(Ob, fabsf(orl[a]));
   }
+  Ob *= 1.0000005f;
+  const float teps = (float)t_eps;
   // slack: float32 t limit strictly above the float64 one
   auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + slack : INFINITY; };
   float tbf = tlim(t_best);
-  int sref[kBvhMaxDepth], scnt[kBvhMaxDepth];  // the builder caps the depth: pushes never overflow
-  float stn[kBvhMaxDepth];
   int sp = 0;
-  int ref = 0, cnt = 0;  // current entry: interior node `ref` (cnt = 0) or leaf [ref, ref+cnt)
-  // pop, skipping entries whose entry distance is beyond the current best
-  auto pop = [&]() -> bool {
-    while (sp > 0) {
-      --sp;
-      if (stn[sp] <= tbf) {
-        ref = sref[sp];
-        cnt = scnt[sp];
-        return true;
-      }
-    }
-    return false;
-  };
-#if VC_WHILE_WHILE
-  // while-while: descend interior nodes until a leaf, then test it — the lanes of a warp
-  // run the float64 leaf tests together instead of interleaving them with box tests
+  unsigned cur = 0;  // interior node 0 (the root)
   while (true) {
-    while (cnt == 0) {
-      const float4* N = H.nodes + 4 * (size_t)ref;
+    while (!(cur & 0x80000000u)) {
+      const float4* N = H.nodes + 4 * (size_t)cur;
       const float4 l0 = __ldg(N), l1 = __ldg(N + 1), r0 = __ldg(N + 2), r1 = __ldg(N + 3);
       float tl, tr;
-      const bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
-      const bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
+      const bool hl = box_hit<D>(l0, l1, inv, noi, tbf, tl);
+      const bool hr = box_hit<D>(r0, r1, inv, noi, tbf, tr);
       if (hl && hr) {
         const bool lf = tl <= tr;
-        sref[sp] = __float_as_int(lf ? r0.w : l0.w);
-        scnt[sp] = __float_as_int(lf ? r1.w : l1.w);
-        stn[sp] = lf ? tr : tl;
-        ++sp;
-        ref = __float_as_int(lf ? l0.w : r0.w);
-        cnt = __float_as_int(lf ? l1.w : r1.w);
-      } else if (hl) {
-        ref = __float_as_int(l0.w);
-        cnt = __float_as_int(l1.w);
-      } else if (hr) {
-        ref = __float_as_int(r0.w);
-        cnt = __float_as_int(r1.w);
-      } else if (!pop()) {
-        return false;
-      }
-    }
-    for (int k = ref; k < ref + cnt; ++k) {
-      double t = leaf_hit<D>(H, k, o, d, t_eps);
-      if (t == INFINITY) continue;
-      int id = H.prim_id[k];
-      if (MODE == 0) {
-        if (t < t_best || (t == t_best && id < id_best)) {
-          t_best = t;
-          id_best = id;
-          tbf = tlim(t_best);
-        }
+        stk.put(sp++, make_uint2(__float_as_uint(lf ? r0.w : l0.w), __float_as_uint(lf ? tr : tl)));
+        cur = __float_as_uint(lf ? l0.w : r0.w);
+      } else if (hl || hr) {
+        cur = __float_as_uint(hl ? l0.w : r0.w);
       } else {
-        if (t < t_best || (t == t_best && id < id_best)) return true;
+        bool got = false;
+        while (sp > 0) {  // pop, skipping entries whose entry distance is beyond the best
+          const uint2 e = stk.get(--sp);
+          if (__uint_as_float(e.y) <= tbf) {
+            cur = e.x;
+            got = true;
+            break;
+          }
+        }
+        if (!got) return false;
       }
     }
-    if (!pop()) return false;
-  }
-#else
-  while (true) {
-    if (cnt > 0) {
-      for (int k = ref; k < ref + cnt; ++k) {
-        double t = leaf_hit<D>(H, k, o, d, t_eps);
-        if (t == INFINITY) continue;
-        int id = H.prim_id[k];
-        if (MODE == 0) {
+    for (int k = (int)(cur & 0x7fffffffu);; ++k) {
+      const float4* Q = H.prim32 + 3 * (size_t)k;
+      const float4 f0 = __ldg(Q), f1 = __ldg(Q + 1), f2 = __ldg(Q + 2);
+      const int idf = __float_as_int(f2.w);
+      bool maybe = true;
+#if VC_PRETEST32
+      if constexpr (D == 3) maybe = !tri_rejects32(f0, f1, f2, orl, Ob, df, teps, tbf);
+#endif
+      if (maybe) {
+        const double t = hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, t_eps);
+        if (t != INFINITY) {
+          const int id = idf & 0x7fffffff;
           if (t < t_best || (t == t_best && id < id_best)) {
+            if (MODE == 1) return true;
             t_best = t;
             id_best = id;
             tbf = tlim(t_best);
           }
-        } else {
-          if (t < t_best || (t == t_best && id < id_best)) return true;
         }
       }
-    } else {
-      const float4* N = H.nodes + 4 * (size_t)ref;
-      const float4 l0 = __ldg(N), l1 = __ldg(N + 1), r0 = __ldg(N + 2), r1 = __ldg(N + 3);
-      float tl, tr;
-      const bool hl = box_hit<D>(l0, l1, of, inv, tbf, tl);
-      const bool hr = box_hit<D>(r0, r1, of, inv, tbf, tr);
-      if (hl && hr) {
-        const bool lf = tl <= tr;
-        sref[sp] = __float_as_int(lf ? r0.w : l0.w);
-        scnt[sp] = __float_as_int(lf ? r1.w : l1.w);
-        stn[sp] = lf ? tr : tl;
-        ++sp;
-        ref = __float_as_int(lf ? l0.w : r0.w);
-        cnt = __float_as_int(lf ? l1.w : r1.w);
-        continue;
-      }
-      if (hl) {
-        ref = __float_as_int(l0.w);
-        cnt = __float_as_int(l1.w);
-        continue;
-      }
-      if (hr) {
-        ref = __float_as_int(r0.w);
-        cnt = __float_as_int(r1.w);
-        continue;
+      if (idf < 0) break;
+    }
+    bool got = false;
+    while (sp > 0) {
+      const uint2 e = stk.get(--sp);
+      if (__uint_as_float(e.y) <= tbf) {
+        cur = e.x;
+        got = true;
+        break;
       }
     }
-    if (!pop()) break;
+    if (!got) return false;
   }
-  return false;
-#endif
+}
+
+template <int D, int MODE>
+__device__ __forceinline__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const double* o,
+                                          const double* d, double& t_best, int& id_best) {
+  LocalStack stk;
+  return bvh_query<D, MODE>(H, t_eps, slack, o, d, t_best, id_best, stk);
 }
 
 // Nearest hit in a primitive set; `id_best` is the original surface index.
-template <int D>
+template <int D, class Stack = LocalStack>
 __device__ void bvh_closest(const DevBvh& H, double t_eps, float slack, const double* o, const double* d,
-                            double& t_best, int& id_best) {
+                            double& t_best, int& id_best, Stack* stk = nullptr) {
   t_best = INFINITY;
   id_best = -1;
   if (H.K == 0) return;
@@ -369,20 +387,22 @@ __device__ void bvh_closest(const DevBvh& H, double t_eps, float slack, const do
     }
     return;
   }
-  bvh_query<D, 0>(H, t_eps, slack, o, d, t_best, id_best);
+  if (stk) bvh_query<D, 0>(H, t_eps, slack, o, d, t_best, id_best, *stk);
+  else bvh_query<D, 0>(H, t_eps, slack, o, d, t_best, id_best);
 }
 
 // Nearest hit over the scene (src/scene.py:271-292).
-template <int D>
+template <int D, class Stack = LocalStack>
 __device__ __forceinline__ void trace_closest(const DevScene& S, const double* o, const double* d, double& t_best,
-                                              int& id_best) {
-  bvh_closest<D>(S.geo, S.t_eps, 1e-5f * (float)S.scale, o, d, t_best, id_best);
+                                              int& id_best, Stack* stk = nullptr) {
+  bvh_closest<D, Stack>(S.geo, S.t_eps, 1e-5f * (float)S.scale, o, d, t_best, id_best, stk);
 }
 
 // Is there a valid hit preceding (thr, id_thr) in (t, index) order?  Shadow rays use
 // id_thr = −1 (visible iff nearest t ≥ thr, src/transport.py:213-214).
-template <int D>
-__device__ bool occluded(const DevScene& S, const double* o, const double* d, double thr, int id_thr = -1) {
+template <int D, class Stack = LocalStack>
+__device__ bool occluded(const DevScene& S, const double* o, const double* d, double thr, int id_thr = -1,
+                         Stack* stk = nullptr) {
   const DevBvh& H = S.geo;
   if (H.K == 0) return false;
   if (H.n_nodes == 0) {
@@ -394,6 +414,7 @@ __device__ bool occluded(const DevScene& S, const double* o, const double* d, do
   }
   double t = thr;
   int id = id_thr;
+  if (stk) return bvh_query<D, 1>(H, S.t_eps, 1e-5f * (float)S.scale, o, d, t, id, *stk);
   return bvh_query<D, 1>(H, S.t_eps, 1e-5f * (float)S.scale, o, d, t, id);
 }
 
@@ -464,8 +485,9 @@ __device__ inline double bounds_exit(const DevScene& S, const double* o, const d
 // Surface shading (src/transport.py:127-254)
 // ---------------------------------------------------------------------------
 
-template <int D>
-__device__ void direct_light(const DevScene& S, const double* p, const double* n, double acc[3]) {
+template <int D, class Stack = LocalStack>
+__device__ void direct_light(const DevScene& S, const double* p, const double* n, double acc[3],
+                             Stack* stk = nullptr) {
   acc[0] = acc[1] = acc[2] = 0.0;
   const double off = 1e-6 * S.scale;
   double org[3];
@@ -496,7 +518,7 @@ __device__ void direct_light(const DevScene& S, const double* p, const double* n
     cp = fmax(cp, 0.0);
     cq = fabs(cq);
     if (!(cp > 0.0 && cq > 0.0)) continue;
-    if (occluded<D>(S, org, dd, mul(r, 1.0 - 1e-6))) continue;
+    if (occluded<D, Stack>(S, org, dd, mul(r, 1.0 - 1e-6), -1, stk)) continue;
     double rm = fmax(r, off);
     double g = __ddiv_rn(mul(cp, cq), D == 3 ? mul(rm, rm) : rm);
     g = mul(mul(g, exp(-S.sigma_t * r)), S.es_w[j]);
@@ -512,9 +534,9 @@ __device__ void direct_light(const DevScene& S, const double* p, const double* n
 }
 
 // Outgoing radiance at a hit: emission + albedo·direct; idx < 0 → 0.
-template <int D>
+template <int D, class Stack = LocalStack>
 __device__ void surface_radiance(const DevScene& S, int idx, const double* hit, const double* dir,
-                                 double out[3]) {
+                                 double out[3], Stack* stk = nullptr) {
   out[0] = out[1] = out[2] = 0.0;
   if (idx < 0) return;
   const double* E = S.emission + (size_t)idx * 3;
@@ -533,18 +555,18 @@ __device__ void surface_radiance(const DevScene& S, int idx, const double* hit, 
 #pragma unroll
   for (int a = 0; a < D; ++a) no[a] = -(nn[a] * sg);
   double dl[3];
-  direct_light<D>(S, hit, no, dl);
+  direct_light<D, Stack>(S, hit, no, dl, stk);
   out[0] = add(out[0], mul(A[0], dl[0]));
   out[1] = add(out[1], mul(A[1], dl[1]));
   out[2] = add(out[2], mul(A[2], dl[2]));
 }
 
 // trace_or_bounds (src/scene.py:306-315)
-template <int D>
+template <int D, class Stack = LocalStack>
 __device__ __forceinline__ void trace_or_bounds(const DevScene& S, const double* o, const double* d,
-                                                double& s, int& idx) {
+                                                double& s, int& idx, Stack* stk = nullptr) {
   double t;
-  trace_closest<D>(S, o, d, t, idx);
+  trace_closest<D, Stack>(S, o, d, t, idx, stk);
   s = isfinite(t) ? t : bounds_exit<D>(S, o, d);
 }
 
@@ -738,6 +760,33 @@ __device__ inline bool ff_segment(const double* u, const double* v, double& F, d
     H[e] = -(jc / sn + (c / (sn * sn * sn)) * gc[a] * gc[b]) / (2.0 * kPi);
   }
   return true;
+}
+
+// float32 form of element_q (3D), for unit-scaled inputs (every length divided by L, σt
+// multiplied by L): the gradient part then carries 1/L and the Hessian part 1/L², which the
+// caller restores in float64.
+__device__ __forceinline__ void element_q_f32(const float* w, float dr, float sigma_t, float F, const float* gF,
+                                              const float* HF, float* q /* 10 */) {
+  const float T = __expf(-sigma_t * dr);
+  const float idr = 1.0f / dr, idr2 = idr * idr;
+  float gT[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) gT[a] = (-sigma_t * w[a]) * idr * T;
+  q[0] = T * F;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) q[1 + a] = T * gF[a] + gT[a] * F;
+  int e = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int b = a; b < 3; ++b) {
+      const float ww = w[a] * w[b];
+      const float I = (a == b) ? 1.0f : 0.0f;
+      const float HT = -sigma_t * (I * idr - ww * idr2 * idr - sigma_t * ww * idr2) * T;
+      q[4 + e] = T * HF[e] + gT[a] * gF[b] + gF[a] * gT[b] + HT * F;
+      ++e;
+    }
+  }
 }
 
 // Element contribution q = (T·F, ∇(T·F), H(T·F)) for representative offset w = x − y_rep

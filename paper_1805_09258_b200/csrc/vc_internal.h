@@ -33,9 +33,15 @@ constexpr int kAsmParts = kAsmSplit * (kAsmBS / 32);  // per-warp partial sums p
 struct DevBvh {
   int K;                 // primitives
   int n_nodes;           // nodes (0 → brute force over K in original order)
-  const float4* nodes;   // 2 float4 per node: (lo.xyz, child/first), (hi.xyz, count)
+  const float4* nodes;   // 2 float4 per child: (lo.xyz, ref), (hi.xyz, count); boxes relative to ctr
   const double* prim;    // leaf order, prim_stride(dim) doubles each
   const int* prim_id;    // leaf order → original surface index
+  // leaf order, 3 float4 per primitive (relative to ctr): (v0, |v0|∞), (e1, E), (e2, id | last);
+  // E = max(|e1|∞, |e2|∞) rounded up (−1: no float32 pre-test), last = bit 31 on the final
+  // primitive of a leaf (2D: (a, 0, 0), (e, 0, −1), (0, 0, 0, id | last))
+  const float4* prim32;
+  double ctr[3];         // bounds centre: node boxes and prim32 are relative to it
+  int stack_need;        // deepest leaf: traversal stack entries needed
 };
 
 // Emitters grouped by plane (3D, ≤ kEmitPlanes planes), each with a 2D grid of the

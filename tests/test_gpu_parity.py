@@ -380,6 +380,47 @@ def test_trace_full_cfg3_vs_oracle():
     assert np.all(np.isinf(t[~hit]))
 
 
+@pytest.mark.parametrize("shift", [0.0, 1000.0])
+def test_trace_edge_rays_vs_oracle(shift):
+    """Rays aimed at triangle vertices, edges and just inside/outside edges (the cases the
+    certified float32 Möller–Trumbore pre-test must leave to float64) in the cfg3 room, also
+    translated far from the origin: hit indices bit-exact with the brute-force oracle."""
+    from paper_1805_09258_b200 import configs
+    from paper_1805_09258_b200.records import trace
+    from paper_1805_09258_b200.scene import scene_arrays, scene_from_arrays
+    from oracle import volcache_oracle as O
+
+    base = configs.cfg3_scene()
+    dim, V, E, A = scene_arrays(base)
+    off = np.array([shift, -0.5 * shift, 2.0 * shift])
+    sc = scene_from_arrays(V + off, E, A, np.asarray(base.bounds_min) + off, np.asarray(base.bounds_max) + off,
+                           base.medium.sigma_s, base.medium.sigma_a)
+    ps = O.pack(sc)
+    O.use_c_trace(None)
+    rng = np.random.default_rng(17)
+    m = 60_000
+    tri = rng.integers(0, len(V), m)
+    v0, v1, v2 = (V[tri, j] + off for j in range(3))
+    kind = rng.integers(0, 4, m)
+    lam = rng.uniform(0, 1, (m, 1))
+    eps = rng.choice([-1e-9, 0.0, 1e-9, -1e-6, 1e-6], (m, 1))
+    tgt = np.where((kind == 0)[:, None], v0,
+                   np.where((kind == 1)[:, None], v0 + lam * (v1 - v0),
+                            np.where((kind == 2)[:, None], v1 + lam * (v2 - v1) + eps * (v0 - v1),
+                                     v2 + lam * (v0 - v2) + eps * (v1 - v2))))
+    o = rng.uniform(ps.bmin, ps.bmax, (m, 3))
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    t_ref, i_ref = O.trace(ps, o, d)
+    O.use_c_trace(0)
+    t, idx = trace(sc, o, d)
+    mism = int((idx != i_ref).sum())
+    _err(f"trace_edges_shift{shift:g}", mismatches=mism)
+    assert mism == 0
+    hit = i_ref >= 0
+    np.testing.assert_allclose(t[hit], t_ref[hit], rtol=2e-15, atol=0)
+
+
 def test_gather_queue_overflow_same_result():
     """Two-pass gather with a tiny queue (overflow → in-place resolution) is bit-identical."""
     import subprocess
