@@ -138,6 +138,32 @@ def step_indices(s: int, rank: int, world: int, B: int, N: int):
 # ---------------------------------------------------------------------------
 
 
+def cpu_info() -> dict:
+    """Host CPU model, the threads used, and the numpy / scipy versions of the CPU arm."""
+    import platform
+
+    import scipy
+
+    model = platform.processor() or "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": len(os.sched_getaffinity(0)), "numpy": np.__version__,
+            "scipy": scipy.__version__}
+
+
+def cpu_points(w, n_records: int, start: int = 0):
+    """Point indices of a CPU sample: spread evenly over the workload's cache points
+    (BASELINE.md §3), offset by `start` so successive samples differ."""
+    N = len(w.points)
+    stride = max(1, N // max(1, n_records))
+    return [(start + k * stride) % N for k in range(n_records)]
+
+
 def cpu_sample(w, n_records: int, start: int = 0):
     """Oracle records (reference algorithm; brute-force trace over all host threads)."""
     from oracle import volcache_oracle as O
@@ -146,12 +172,11 @@ def cpu_sample(w, n_records: int, start: int = 0):
     O.use_c_trace(threads)
     ps = O.pack(w.scene)
     t0 = time.perf_counter()
-    for i in range(start, start + n_records):
-        rb = O.build_record(ps, w.points[i % len(w.points)], w.n_angular, w.march_step,
-                            O.seed_seq(w.seed, 401, i % len(w.points)), w.n_inner, w.n_light_samples)
+    for i in cpu_points(w, n_records, start):
+        rb = O.build_record(ps, w.points[i], w.n_angular, w.march_step, O.seed_seq(w.seed, 401, i), w.n_inner,
+                            w.n_light_samples)
         for k in range(2):
-            O.make_record(w.points[i % len(w.points)], rb.L[k], rb.grad[k], rb.hess[k], w.epsilon, ps.scale,
-                          ps.max_emission)
+            O.make_record(w.points[i], rb.L[k], rb.grad[k], rb.hess[k], w.epsilon, ps.scale, ps.max_emission)
     dt = time.perf_counter() - t0
     return dt, threads
 
@@ -161,13 +186,13 @@ def run_reference(args):
     if rank != 0:
         return 0
     w = workload(args)
-    per = max(1, args.cpu_records)
-    for s in range(args.warmup):
-        cpu_sample(w, per, start=s * per)
+    per = max(1, args.ref_records)
+    for s in range(args.warmup):  # warm-up: one record each (page-in, C trace library load)
+        cpu_sample(w, 1, start=7919 * s)
     tot = 0.0
     threads = 1
-    for s in range(args.steps):
-        dt, threads = cpu_sample(w, per, start=(args.warmup + s) * per)
+    for s in range(args.steps):  # step s: `per` records spread over the points, offset per step
+        dt, threads = cpu_sample(w, per, start=s * 97)
         tot += dt
     value = args.steps * per / tot
     line = {
@@ -178,9 +203,10 @@ def run_reference(args):
         "config": {"workload": w.name, "records_per_step": per, "n_angular": w.n_angular,
                    "march_step": w.march_step, "triangles": len(w.scene.surfaces)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per} record(s) per step of {w.name}: oracle/volcache_oracle.py "
-                                   f"(numpy restatement) with the brute-force trace in oracle/trace_c.c "
-                                   f"on {threads} threads"},
+                         "sample": f"{per} record(s) per step of {w.name} spread over its {len(w.points)} points "
+                                   f"({args.steps * per} timed): oracle/volcache_oracle.py (numpy restatement) with "
+                                   f"the brute-force trace in oracle/trace_c.c on {threads} threads",
+                         **cpu_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -383,7 +409,8 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--march-step", type=float, default=None)
     ap.add_argument("--records-per-step", type=int, default=2048)
-    ap.add_argument("--cpu-records", type=int, default=1, help="oracle records per CPU sample/step")
+    ap.add_argument("--cpu-records", type=int, default=4, help="oracle records in the cpu_baseline sample")
+    ap.add_argument("--ref-records", type=int, default=4, help="--impl reference: oracle records per timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cfg5-eps", type=float, default=None, help="cfg5: record-error target ε (default tuned)")
@@ -428,6 +455,10 @@ def main():
     res = None
     for s in range(args.warmup):
         res = estimate_moments_batch(w.scene, Xs[s], seeds=Ss[s], **kw)
+    gathered = None
+    if world > 1:  # fixed-size record all-gather over NCCL, warmed once
+        gathered = torch.empty(world * res.records.numel(), dtype=res.records.dtype, device="cuda")
+        dist.all_gather_into_tensor(gathered, res.records.reshape(-1))
     torch.cuda.synchronize()
     L = _lib.lib()
     L.vc_profile(1)
@@ -441,6 +472,8 @@ def main():
         for s in range(args.warmup, total_steps):
             res = estimate_moments_batch(w.scene, Xs[s], seeds=Ss[s], **kw)
             stats_acc.append(res.stats)
+            if world > 1:  # the exchange before a lookup pass: every rank gets every record
+                dist.all_gather_into_tensor(gathered, res.records.reshape(-1))
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -545,6 +578,9 @@ def main():
         "config": {"workload": w.name, "records_per_step": B * world, "records_per_rank_step": B,
                    "n_angular": n, "march_step": w.march_step, "n_inner": w.n_inner, "epsilon": w.epsilon,
                    "triangles": K, "cache_points": N, "parallelism": f"records sharded over {world} GPU(s)",
+                   "exchange": ("per step, every rank's records all-gathered over NCCL inside the timed region "
+                                f"({world * B * 2 * record_size(ds.dim) * 8} bytes gathered per step)")
+                   if world > 1 else "none (1 GPU)",
                    "l2": "no flush: per-step scratch (media samples, directions) is GBs, far above the 126 MB L2",
                    "samples_per_s": value * n, "mean_media_samples_per_record": P_sum / nrec,
                    "mean_elements_evaluated": E_sum / nrec, "triangulation_failures": tri_fail},
@@ -555,12 +591,14 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dt, threads = cpu_sample(w, max(1, args.cpu_records))
+        nc = max(1, args.cpu_records)
+        dt, threads = cpu_sample(w, nc)
         line["cpu_baseline"] = {
-            "value": max(1, args.cpu_records) / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{max(1, args.cpu_records)} record(s) of {w.name} through oracle/volcache_oracle.py "
-                      f"(numpy restatement of the reference) with the brute-force trace in oracle/trace_c.c "
-                      f"on {threads} host threads",
+            "value": nc / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{nc} record(s) of {w.name} spread over its {len(w.points)} points, through "
+                      f"oracle/volcache_oracle.py (numpy restatement of the reference) with the brute-force trace "
+                      f"in oracle/trace_c.c on {threads} host threads ({dt:.1f} s)",
+            **cpu_info(),
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

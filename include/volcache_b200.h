@@ -32,6 +32,7 @@ extern "C" {
 #define VC_ECUDA (-3)
 #define VC_ETRI (-4)
 #define VC_ENOMEM (-5)
+#define VC_EHOOK (-6) /* a caller-supplied hook reported failure */
 
 /* flags */
 #define VC_MEM_HOST 1     /* all array pointers are host memory */
@@ -234,6 +235,16 @@ typedef struct {
   int max_media_bounces;      /* baseline and path estimators */
   double baseline_alpha;      /* baseline estimator only: log_gradient_radius scale */
   int path_samples;           /* path estimator: path_samples_per_point */
+  /* Multi-GPU populate (subdivision estimator): when set, every speculative build wave is
+   * handed to this hook instead of the local record build.  It receives the wave's n points
+   * (device n × dim float64) and seed words (device n × seed_words uint32) and must fill
+   * rec_out (device n × 2 × record size float64, single then multiple) and stats_out
+   * (device n × 8 int64) for all n, in order, on `stream` — e.g. every rank builds a
+   * contiguous share and the shares are all-gathered over NCCL, so every rank resolves the
+   * same wave (paper_1805_09258_b200.dist.populate_sharded).  Returns 0 or a VC_E* code. */
+  int (*build_hook)(void* user, int n, const double* x, const uint32_t* words, int seed_words, double* rec_out,
+                    int64_t* stats_out, void* stream);
+  void* build_hook_user;
 } vc_populate_params;
 
 /* populate_cache (src/renderer.py:302-327) for the cache modes ours-aniso / ours-iso:

@@ -19,6 +19,7 @@ VC_EOUTSIDE = -2
 VC_ECUDA = -3
 VC_ETRI = -4
 VC_ENOMEM = -5
+VC_EHOOK = -6
 
 VC_MEM_HOST = 1
 VC_SEED_WORDS = 2
@@ -105,7 +106,15 @@ class PopulateParams(C.Structure):
         ("max_media_bounces", C.c_int),
         ("baseline_alpha", C.c_double),
         ("path_samples", C.c_int),
+        ("build_hook", C.c_void_p),
+        ("build_hook_user", C.c_void_p),
     ]
+
+
+# int (*)(void* user, int n, const double* x, const uint32_t* words, int seed_words,
+#         double* rec_out, int64_t* stats_out, void* stream)
+BUILD_HOOK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                         C.c_void_p)
 
 
 class BaselineParams(C.Structure):

@@ -350,6 +350,8 @@ struct Engine {
   int seed_kind = 0;  // 0: populate (seed, 401, i); 1: field render (seed, 307, iy, ix); 2: camera render
   int npx = 1;        // camera pixels (seed kind 2)
   int estimator = VC_EST_SUBDIVISION;
+  int (*hook)(void*, int, const double*, const uint32_t*, int, double*, int64_t*, void*) = nullptr;
+  void* hook_user = nullptr;
   vc_baseline_params blp{};
   double* commit_J = nullptr;  // optional N × 3: direct value (L_s + L_m) of every point that built
   bool commit_list = false;    // camera render: (ordinal, value) of every point that built
@@ -715,6 +717,11 @@ int Engine::run() {
       auto tb0 = tnow();
       if (estimator == VC_EST_BASELINE) {  // CacheSet.compute, mode "baseline" (src/renderer.py:233-244)
         rc = baseline_impl(sc, nb2, xb, dw, &blp, nullptr, rec, nullptr, st);
+      } else if (hook) {  // multi-GPU: the wave is sharded over ranks and all-gathered by the caller
+        rc = hook(hook_user, nb2, xb, dw, bp.seed_words, rec, (int64_t*)bst, (void*)st);
+        if (rc) return fail(VC_EHOOK, "populate build hook failed (code " + std::to_string(rc) + ")");
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "populate build hook");
       } else {
         rc = build_impl(sc, nb2, xb, dw, nullptr, &bp, mom, (int64_t*)bst, rec, st, nullptr);
       }
@@ -792,6 +799,8 @@ int vc::populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, 
   g.bp.seed_words = seed_kind == 0 ? 3 : (seed_kind == 1 ? 4 : 5);
   g.commit_list = rs != nullptr;
   g.estimator = pp->estimator == VC_EST_BASELINE ? VC_EST_BASELINE : VC_EST_SUBDIVISION;
+  g.hook = pp->build_hook;
+  g.hook_user = pp->build_hook_user;
   g.blp.n_angular = pp->n_angular;
   g.blp.max_media_bounces = pp->max_media_bounces;
   g.blp.n_light_samples = pp->n_light_samples;

@@ -69,6 +69,87 @@ def build_records_sharded(scene, X, cfg_seed: int, *, builder=None, group=None, 
     return all_gather_rows(local, group=group), (lo, hi)
 
 
+def sharded_wave(n: int, build_local, exchange, rank: int, world: int):
+    """One speculative build wave of n points split over ranks: rank r builds its contiguous
+    share [lo, hi) (`build_local(lo, hi)` → (hi − lo, K) rows) and `exchange` all-gathers the
+    shares into the (n, K) rows in wave order.  Every record's seed words come with its point,
+    so the rows equal a single-rank build of the whole wave."""
+    lo, hi = shard_range(n, rank, world)
+    return exchange(build_local(lo, hi))
+
+
+class _DeviceArray:
+    """Zero-copy CUDA array view of a raw device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(v) for v in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _view(ptr: int, shape, dtype):
+    import torch
+
+    typestr = {torch.float64: "<f8", torch.int64: "<i8", torch.int32: "<i4"}[dtype]
+    if ptr == 0 or 0 in tuple(shape):
+        return torch.empty(shape, dtype=dtype, device="cuda")
+    return torch.as_tensor(_DeviceArray(ptr, shape, typestr), device="cuda")
+
+
+def populate_sharded(scene, target, settings, *, group=None, window: int = 0, lookahead: int = 0):
+    """populate_cache (src/renderer.py:302-327) on every rank of the group, with each
+    speculative build wave of the engine sharded over the ranks.
+
+    Every rank runs the same deterministic engine (march stream, cover tests, sequential
+    resolve); only the record builds are split: rank r builds its contiguous share of each
+    wave and the shares are all-gathered device-to-device over NCCL before the resolve, so
+    every rank commits the same records in the same order — the caches equal the
+    single-GPU (and the reference's sequential) populate record for record.
+    Returns (CacheSet, stats) on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from . import renderer as R
+    from .records import device_scene, record_size
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ds = device_scene(scene)
+    d = ds.dim
+    RS = record_size(d)
+    prm = _lib.BuildParams()
+    prm.n_angular = R._n_angular(scene, settings)
+    prm.march_step = float(settings.march_step)
+    prm.n_inner = int(settings.n_inner)
+    prm.n_light_samples = int(settings.n_light_samples)
+    prm.epsilon = float(settings.epsilon)
+    prm.flags = _lib.VC_SEED_WORDS | _lib.VC_MAKE_RECORDS | (_lib.VC_ISOTROPIC if settings.mode == "ours-iso" else 0)
+    L = _lib.lib()
+
+    def hook(n, x, w, sw, rec, stats):
+        prm.seed_words = sw
+        X = _view(x, (n, d), torch.float64)
+        Wd = _view(w, (n, sw), torch.int32)
+
+        def build_local(lo, hi):
+            m = hi - lo
+            recs = torch.zeros((m, 2 * RS), dtype=torch.float64, device="cuda")
+            st = torch.zeros((m, 8), dtype=torch.int64, device="cuda")
+            if m:
+                xs, ws = X[lo:hi].contiguous(), Wd[lo:hi].contiguous()
+                _lib.check(L.vc_build_records(ds.handle, m, _lib.C.c_void_p(xs.data_ptr()),
+                                              _lib.C.c_void_p(ws.data_ptr()), None, _lib.C.byref(prm), None,
+                                              _lib.C.c_void_p(st.data_ptr()), _lib.C.c_void_p(recs.data_ptr()),
+                                              None))
+            return torch.cat([recs, st.view(torch.float64)], dim=1)
+
+        rows = sharded_wave(n, build_local, lambda t: all_gather_rows(t, group=group), rank, world)
+        _view(rec, (n, 2 * RS), torch.float64).copy_(rows[:, :2 * RS])
+        _view(stats, (n, 8), torch.int64).copy_(rows[:, 2 * RS:].contiguous().view(torch.int64))
+
+    return R.populate_cache(scene, target, settings, window=window, lookahead=lookahead, build_hook=hook)
+
+
 def broadcast_cache_set(cache_set, src: int = 0, group=None):
     """Make every rank's CacheSet hold `src`'s records, in `src`'s insertion order.
 

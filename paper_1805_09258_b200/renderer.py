@@ -261,13 +261,17 @@ class CacheSet:
             self.multiple.insert(rec_m)
 
 
-def populate_cache(scene, target, settings: RenderSettings, *, window: int = 0, lookahead: int = 0):
+def populate_cache(scene, target, settings: RenderSettings, *, window: int = 0, lookahead: int = 0,
+                   build_hook=None):
     """March view points in scanline order, inserting records where coverage lacks.
 
     Returns (CacheSet, stats) equal to the reference's sequential loop
     (src/renderer.py:302-327), computed by the speculative-window engine (vc_populate).
     `window` / `lookahead` bound the speculative builds per window and the initial
     lookahead (0 = library defaults); the result does not depend on them.
+    `build_hook(n, x_ptr, words_ptr, seed_words, rec_ptr, stats_ptr) -> None` (device
+    pointers) replaces the engine's record build for every speculative wave — the
+    multi-GPU populate (`dist.populate_sharded`) shards each wave over ranks there.
     """
     if settings.mode not in CACHE_MODES:
         raise ValueError(f"populate_cache requires a cache mode, got {settings.mode!r}")
@@ -279,10 +283,27 @@ def populate_cache(scene, target, settings: RenderSettings, *, window: int = 0, 
     p = _params(scene, target, settings)
     p.window = int(window)
     p.lookahead = int(lookahead)
+    failure = []
+    if build_hook is not None:
+        if settings.mode not in ("ours-aniso", "ours-iso"):
+            raise ValueError("build_hook applies to the subdivision estimator (modes ours-aniso / ours-iso)")
+
+        def _hook(user, n, x, words, seed_words, rec, stats, stream):
+            try:
+                build_hook(int(n), int(x or 0), int(words or 0), int(seed_words), int(rec or 0), int(stats or 0))
+                return 0
+            except BaseException as exc:  # reported after vc_populate returns
+                failure.append(exc)
+                return 1
+
+        cb = _lib.BUILD_HOOK(_hook)
+        p.build_hook = _lib.C.cast(cb, _lib.C.c_void_p)
     hs, hm = _lib.C.c_void_p(), _lib.C.c_void_p()
     st = np.zeros(8, np.int64)
-    _lib.check(_lib.lib().vc_populate(ds.handle, _lib.C.byref(p), _lib.C.byref(hs), _lib.C.byref(hm),
-                                      _lib.ptr(st), None))
+    rc = _lib.lib().vc_populate(ds.handle, _lib.C.byref(p), _lib.C.byref(hs), _lib.C.byref(hm), _lib.ptr(st), None)
+    if failure:
+        raise failure[0]
+    _lib.check(rc)
     single = RadianceCache._adopt(scene.bounds_min, scene.bounds_max, hs)
     multiple = RadianceCache._adopt(scene.bounds_min, scene.bounds_max, hm)
     single.sphere_records = multiple.sphere_records = settings.mode == "baseline"

@@ -685,7 +685,7 @@ def gen_cfg5_crop(src=REPO / "gpurun_out" / "cfg5_crop_records.npz"):
     out = {"versions": VERSIONS, "crop": z["crop"], "eps": z["eps"], "step": z["step"], "seed": z["seed"],
            "single_rows": z["single_rows"], "multiple_rows": z["multiple_rows"],
            "single_index": z["single_index"], "multiple_index": z["multiple_index"],
-           "pop_stats": z["pop_stats"], "image": img,
+           "pop_stats": z["pop_stats"], "image": img, "gpu_full_cache_crop": z["gpu_full_cache_crop"],
            "stats": np.array([stats["cache_hits"], stats["direct_evaluations"]])}
     np.savez_compressed(OUT / "cfg5_crop.npz", **out)
     for mod in (vscene, vr, __import__("volcache.transport", fromlist=["x"])):

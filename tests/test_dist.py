@@ -134,3 +134,58 @@ def test_render_sharded_world2(H):
         np.testing.assert_array_equal(pm, rows[:3] * 2)
         np.testing.assert_allclose(img, want, rtol=0, atol=1e-9)
         assert st["cache_hits"] == H * W and st["direct_evaluations"] == H
+
+
+def _wave_worker(rank, world, port, sizes, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1805_09258_b200.dist import all_gather_rows, sharded_wave
+
+    out = []
+    for n in sizes:
+        X = np.random.default_rng(n).uniform(0, 1, (n, 3))
+        words = np.stack([np.full(n, 5), np.full(n, 401), np.arange(n)], axis=1).astype(np.uint32)
+        built = []
+
+        def build_local(lo, hi):
+            built.append((lo, hi))
+            recs = fake_builder(None, X[lo:hi], words[lo:hi]).reshape(hi - lo, 14)
+            stats = torch.tensor(np.stack([np.arange(lo, hi), np.zeros(hi - lo, np.int64)], axis=1))
+            return torch.cat([recs, stats.view(torch.float64)], dim=1)
+
+        rows = sharded_wave(n, build_local, lambda t: all_gather_rows(t), rank, world)
+        out.append((n, built[0], rows.numpy()))
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_populate_wave_sharding_world2():
+    """The multi-GPU populate's per-wave exchange (dist.populate_sharded → sharded_wave): each
+    rank builds a contiguous share of the wave's points and the all-gather hands every rank
+    the rows of the whole wave in wave order, equal to one rank building the whole wave —
+    so every rank's engine resolves identical records (waves smaller than the world
+    included)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    sizes = [5, 1, 0, 64, 2]
+    procs = [ctx.Process(target=_wave_worker, args=(r, 2, port, sizes, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted((q.get(timeout=120) for _ in range(2)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for k, n in enumerate(sizes):
+        X = np.random.default_rng(n).uniform(0, 1, (n, 3))
+        words = np.stack([np.full(n, 5), np.full(n, 401), np.arange(n)], axis=1).astype(np.uint32)
+        want = fake_builder(None, X, words).reshape(n, 14).numpy()
+        shares = [got[r][1][k][1] for r in range(2)]
+        assert shares[0][0] == 0 and shares[0][1] == shares[1][0] and shares[1][1] == n
+        for r in range(2):
+            rows = got[r][1][k][2]
+            assert rows.shape[0] == n
+            np.testing.assert_array_equal(rows[:, :want.shape[1]], want)
+            np.testing.assert_array_equal(rows[:, want.shape[1]:].copy().view(np.int64)[:, 0], np.arange(n))

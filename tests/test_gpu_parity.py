@@ -99,6 +99,51 @@ def test_records_vs_reference_goldens(case):
         np.testing.assert_allclose(ins["s"], z["s"][i], rtol=1e-13)
 
 
+def test_cfg3_full_bench_workload_vs_reference():
+    """The bench workload itself (cfg3 window room, 51,300 triangles, n = 16384, step 0.1) on
+    four cache points spread over the 19k, against the unmodified reference run here with
+    the chunked-trace shim (tests/golden/rec_cfg3_full.npz, make_goldens.py gen_cfg3_full):
+    with qhull's adjacency injected, moments within the north_star gate, element and star
+    counts and primary hit indices exact, records (value, quadratic form) equal; the GPU
+    triangulation gives qhull's triangle set.  The default path (GPU triangles in canonical
+    vertex order, so a different representative vertex on ties) is
+    recorded against the same reference in parity_errors.json (cfg3_full-default[i])."""
+    from paper_1805_09258_b200 import configs, estimate_moments_batch, inspect_record
+    from paper_1805_09258_b200.records import unpack_record
+    from paper_1805_09258_b200.scene import scene_arrays
+
+    z = golden("rec_cfg3_full")
+    sc = configs.cfg3_scene()
+    _, V, E, _ = scene_arrays(sc)
+    np.testing.assert_allclose([V.sum(), (V * V).sum(), E.sum(), float(len(V))], z["scene_digest"], rtol=1e-13)
+    n, step, n_inner, n_light, _ = z["params"]
+    idx = [int(i) for i in z["index"]]
+    words = np.array([[2, 401, i] for i in idx], np.uint32)
+    adj = z["adj"].astype(np.int32)
+    kw = dict(n_angular=int(n), march_step=float(step), n_inner=int(n_inner), n_light_samples=int(n_light),
+              epsilon=0.05)
+    r = estimate_moments_batch(sc, z["points"], seeds=words, adjacency=adj, **kw)
+    d = estimate_moments_batch(sc, z["points"], seeds=words, **kw)  # default path: GPU triangulation
+    for j, i in enumerate(idx):
+        _check_moments(f"cfg3_full[{i}]", r.L[j], r.grad[j], r.hess[j], z["L"][j], z["grad"][j], z["hess"][j])
+        assert tuple(int(v) for v in r.stats[j, :3]) == tuple(int(v) for v in z["stats"][j])
+        for k in range(2):
+            rec = unpack_record(r.records[j, k], 3)
+            np.testing.assert_allclose(rec.value, z["rec_value"][j][k], rtol=1e-4, atol=1e-300)
+            assert rel_l2(_quadform(rec.axes, rec.radii), _quadform(z["rec_axes"][j][k], z["rec_radii"][j][k])) <= 1e-3
+        ins = inspect_record(sc, z["points"][j], rng_seed=np.random.SeedSequence([2, 401, i]), **{
+            k: v for k, v in kw.items() if k != "epsilon"})
+        np.testing.assert_array_equal(ins["idx"], z["idx"][j])
+        np.testing.assert_allclose(ins["s"], z["s"][j], rtol=1e-13)
+        assert _tri_set(ins["tris"]) == _tri_set(z["adj"][j])
+        # default-path deviation (recorded, not gated: the representative vertex differs on ties)
+        dev = {}
+        for key, got, want in (("L", d.L[j], z["L"][j]), ("grad", d.grad[j], z["grad"][j]),
+                                ("hess", d.hess[j], z["hess"][j])):
+            dev[key] = max(rel_l2(got[k], want[k]) for k in range(2))
+        _err(f"cfg3_full-default[{i}]", **dev)
+
+
 def _tri_set(t):
     return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
 
@@ -342,6 +387,37 @@ def test_render_misses_vs_oracle():
     assert np.all(img.reshape(-1, 3)[[i for i in range(24) if i not in pix]] == 0.0)  # crop only
 
 
+def test_cfg5_crop_vs_reference():
+    """cfg5 at its stated size (BASELINE.json config 5: 1920×1080 camera over the cfg3 room, march
+    step 0.01, ~96k records): a 64×36 crop rendered frozen from the GPU-populated records near
+    the crop, against the reference's render() of the same crop from the same records
+    (tests/golden/cfg5_crop.npz, tools/cfg5_crop_fixture.py + make_goldens.py gen_cfg5_crop).
+    Per pixel ≤ 1e-4 relative; the subset render equals the render over the
+    full populated caches."""
+    from paper_1805_09258_b200 import configs
+    from paper_1805_09258_b200.cache import RadianceCache, render_frozen
+
+    if not (ROOT / "tests" / "golden" / "cfg5_crop.npz").exists():
+        pytest.skip("cfg5_crop fixture not generated yet (make_goldens.py cfg5_crop)")
+    z = golden("cfg5_crop")
+    sc = configs.cfg3_scene()
+    r0, nr, c0, nc = (int(v) for v in z["crop"])
+    caches = []
+    for name in ("single", "multiple"):
+        c = RadianceCache(sc.bounds_min, sc.bounds_max)
+        c.extend_packed(z[f"{name}_rows"])
+        caches.append(c)
+    img, st = render_frozen(sc, configs.cfg5_camera(1920, 1080), caches[0], caches[1], march_step=float(z["step"]),
+                            seed=int(z["seed"]), n_angular=16384, epsilon=float(z["eps"]), crop=(r0, nr, c0, nc))
+    got = img[r0:r0 + nr, c0:c0 + nc]
+    want = z["image"]
+    assert st["direct_evaluations"] == 0 and st["cache_hits"] == int(z["stats"][0])
+    err = float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
+    _err("cfg5_crop_64x36", max_rel_pixel=err)
+    assert err <= 1e-4
+    np.testing.assert_array_equal(got, z["gpu_full_cache_crop"])
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "room"])
 def test_trace_vs_reference_goldens(name):
     """Raw nearest hits on the reference's golden rays: idx bit-exact, t to the last ulp."""
@@ -500,7 +576,9 @@ def test_gather_prefilter_same_media():
 def test_assembly_item_lists_match_fused():
     """Two-kernel assembly (scan → per-warp item lists → evaluation), the fused kernel
     (VOLCACHE_ASM_ITEM_CAP=0) and a mix (tiny lists overflow → fused fallback per record)
-    evaluate the same items; only the summation order differs."""
+    evaluate the same items; only the summation order differs.  The 3D element contributions
+    are float32 and each round's 32-lane sum is float32 (VC_ASM_F32), so orders differ at
+    ~1e-6 of the per-component scale; the element counts are exact."""
     import subprocess
     import sys
 
@@ -525,7 +603,8 @@ def test_assembly_item_lists_match_fused():
     for cap in ("0", "2000", "8000"):
         m, s = res[cap]
         np.testing.assert_array_equal(s, s0)  # same items evaluated / dropped per kind
-        np.testing.assert_allclose(m, m0, rtol=1e-11, atol=1e-14 * np.abs(m0).max())
+        scale = np.abs(m0).max(axis=-1, keepdims=True)  # per record and kind
+        assert np.all(np.abs(m - m0) <= 2e-5 * scale), float((np.abs(m - m0) / scale).max())
 
 
 def test_errors_and_edge_cases():

@@ -356,3 +356,43 @@ print("sharded ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "sharded ok" in r.stdout
+
+
+def test_populate_sharded_nccl_world1_matches_populate():
+    """dist.populate_sharded over NCCL (one rank on this GPU): every speculative wave goes
+    through the engine's build hook (shard → device build → all-gather → resolve) and the
+    caches equal the plain populate record for record, with the same engine statistics."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = r'''
+import os, sys, socket, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+from conftest import golden, golden_scene
+from paper_1805_09258_b200.renderer import Camera, RenderSettings, populate_cache
+from paper_1805_09258_b200 import dist as vdist
+s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1)
+z = golden("render"); sc = golden_scene(z)
+eps, spp, step, n_ang, seed, n_inner, n_light = z["settings"]; v = z["camera"]
+cam = Camera(position=v[0:3], look_at=v[3:6], up=v[6:9], fov_degrees=float(v[9]), width=int(v[10]), height=int(v[11]))
+for mode in ("ours-aniso", "ours-iso"):
+    st = RenderSettings(mode=mode, epsilon=float(eps), spp=int(spp), march_step=float(step), n_angular=int(n_ang),
+                        seed=int(seed), n_inner=int(n_inner), n_light_samples=int(n_light), frozen=True)
+    ref, rst = populate_cache(sc, cam, st)
+    cs, pst = vdist.populate_sharded(sc, cam, st, window=3)
+    ref3, st3 = populate_cache(sc, cam, st, window=3)
+    for a, b in ((cs.single, ref.single), (cs.multiple, ref.multiple)):
+        np.testing.assert_array_equal(a.packed(), b.packed())
+    assert pst["records"] == rst["records"] > 0
+    assert (pst["builds"], pst["windows"]) == (st3["builds"], st3["windows"])
+dist.destroy_process_group()
+print("populate sharded ok")
+'''
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "populate sharded ok" in r.stdout
