@@ -1219,7 +1219,7 @@ __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, con
 
 template <class T, int BS>
 __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, int rec, int i, typename Vec2<T>::V* us,
-                                          unsigned char* hs, int* own, int* own_cnt) {
+                                          unsigned char* hs, int* own, int* own_cnt, bool cull = false) {
   const int n = P.n_angular, rows = P.rows, cols = P.cols;
   const int r0 = i / cols, c0 = i - r0 * cols;
   const int hw = r0 < kDelRowsMax ? P.del_hw[r0] : 0;
@@ -1247,10 +1247,47 @@ __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, i
       q = (q == rowe) ? rowp : q;
     }
   }
-  const int hn = gift_wrap<T, BS>(us, K, start, n1, hs);
+  // Culling: the projections of directions farther than the cull chord (|u| < u_c,
+  // u_c = 2 / chord) are dropped before the wrap and the survivors compacted (their window
+  // slots kept as a 64-bit mask in registers); the hull of the survivors is the hull of all candidates iff it
+  // contains the disk |u| ≤ u_c, checked per hull edge with the float32 error margins —
+  // else the cell goes to the clipping kernel.
+  int Kw = K, startw = start;
+  const T thr2 = (T)P.del_cull_u2;
+  unsigned keep_lo = 0u, keep_hi = 0u;  // survivors' window slots (K ≤ 64)
+  if (cull && thr2 > (T)0) {
+    int Kc = 0;
+    n1 = 0;
+    for (int k = 0; k < K; ++k) {
+      const auto u = us[k * BS];
+      if (u.x * u.x + u.y * u.y >= thr2) {  // NaN (the centre) is dropped
+        if (k == start) startw = Kc;
+        us[Kc * BS] = u;
+        if (k < 32) keep_lo |= 1u << k;
+        else keep_hi |= 1u << (k - 32);
+        n1 = fmax(n1, fabs(u.x) + fabs(u.y));
+        ++Kc;
+      }
+    }
+    if (Kc < 3) return false;
+    Kw = Kc;
+  }
+  const int hn = gift_wrap<T, BS>(us, Kw, startw, n1, hs);
+  if (Kw < K && hn >= 3) {
+    for (int t = 0; t < hn; ++t) {
+      const auto a = us[hs[t * BS] * BS];
+      const auto b = us[hs[(t + 1 == hn ? 0 : t + 1) * BS] * BS];
+      const T na = fabs(a.x) + fabs(a.y), nb = fabs(b.x) + fabs(b.y);
+      const T cr = a.x * b.y - a.y * b.x - (T)64 * Vec2<T>::kEps * (na + nb) * (na + nb);
+      const T ex = b.x - a.x, ey = b.y - a.y;
+      if (!(cr > (T)0 && cr * cr >= thr2 * (T)1.002 * (ex * ex + ey * ey))) return false;
+    }
+  }
   // candidate k → direction index (k / wc by a 16-bit reciprocal, exact for k < 2¹⁶/wc²)
   const unsigned rwc = (65536u + wc - 1) / wc;
-  auto gidx = [&](int k) {
+  const int nlo = __popc(keep_lo);
+  auto gidx = [&](int kw) {  // survivor kw → its window slot: the kw-th set bit of the mask
+    const int k = (Kw == K) ? kw : (kw < nlo ? (int)__fns(keep_lo, 0, kw + 1) : 32 + (int)__fns(keep_hi, 0, kw - nlo + 1));
     const int a = (int)(((unsigned)k * rwc) >> 16);
     int col = col0 + (k - a * wc);
     col -= (col >= cols) ? cols : 0;
@@ -1288,7 +1325,7 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W
     const int rs = rem / cols;
     const int i = (int)P.del_rows[P.del_cls[cls] + rs] * cols + (rem - rs * cols);
     cell = rec * n + i;
-    fb = !hull_cell<float, kHullBS>(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
+    fb = !hull_cell<float, kHullBS>(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt, true);
   }
   const unsigned m = __ballot_sync(0xffffffffu, fb);
   if (m) {

@@ -42,6 +42,17 @@ class Moments:
         return self.grad.shape[1]
 
 
+# Result class of estimate_moments: a host that rebinds the reference's names can have the
+# drop-in return the reference's own Moments dataclass (same fields), so isinstance checks
+# on the reference side hold (tools/rebind_plugin.py).
+_RESULT_TYPES = {"moments": Moments}
+
+
+def use_result_types(moments=None) -> None:
+    """Return `moments(L=, grad=, hess=, kind=)` instances from estimate_moments (None: ours)."""
+    _RESULT_TYPES["moments"] = moments if moments is not None else Moments
+
+
 @dataclass(frozen=True)
 class CacheRecord:
     """Value + gradient with an ellipsoidal valid region (src/cache.py:94-121)."""
@@ -219,7 +230,7 @@ def estimate_moments(scene, x, n_angular=None, march_step=0.1, rng_seed=None, n_
     out = []
     for k, kind in enumerate(("single", "multiple")):
         L, g, h = split_moments(mom[k], d)
-        out.append(Moments(L=L, grad=g, hess=h, kind=kind))
+        out.append(_RESULT_TYPES["moments"](L=L, grad=g, hess=h, kind=kind))
     return out[0], out[1]
 
 

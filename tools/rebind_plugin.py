@@ -39,6 +39,8 @@ REBOUND = {
 for (mod, name), fn in REBOUND.items():
     if hasattr(mod, name):
         setattr(mod, name, fn)
+# results come back as the reference's own Moments dataclass (same fields)
+_b200.records.use_result_types(moments=_vs.Moments)
 
 
 def pytest_report_header(config):
