@@ -362,14 +362,6 @@ static void del_row_table(BuildParams& P) {
     }
   }
   P.del_cls[3] = nr;
-  // hull-kernel culling: keep window candidates within κ mean spacings (chord); the projection
-  // of a direction at chord c has |u| ≤ 2/c, so |u|² < (2/(κ·s))² drops only farther ones
-  {
-    const char* ec = getenv("VOLCACHE_HULL_CULL");
-    const double kappa = ec ? atof(ec) : 2.5;
-    const double sp = std::sqrt(4.0 * pi / P.n_angular);
-    P.del_cull_u2 = kappa > 0.0 ? 4.0 / (kappa * sp * kappa * sp) : 0.0;
-  }
   // polar rows: candidates within δ = 3 spacings (2·R_cell ≤ δ holds for all but ~1% of
   // the cap cells; ≤ 40 candidates), kept in 16-bit column indices
   P.del_zstep = 2.0 / rows;

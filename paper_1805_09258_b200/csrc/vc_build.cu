@@ -365,6 +365,10 @@ __device__ __forceinline__ void store_media(float* out, const double* v) {
 #ifndef VC_QCHUNK
 #define VC_QCHUNK 32
 #endif
+// first-stage direction-sign test of the emitter pre-filter (emitter_ahead); 0: off
+#ifndef VC_EMIT_AHEAD
+#define VC_EMIT_AHEAD 1
+#endif
 constexpr int kQChunk = VC_QCHUNK;  // queue slots a warp reserves with one atomic
 static_assert(kQChunk >= 32, "a step's hits (≤ 32) must fit one fresh chunk");
 
@@ -430,6 +434,37 @@ struct alignas(16) FilterPlane {  // four 16-byte shared-memory loads per plane
   float4 cc;   // 1 / block size (x, y), blocks (x, y) as int bits
 };
 
+// Sign of the gather direction's axis-a component from the draws alone, d = (sinθ·cos 2πu1,
+// sinθ·sin 2πu1, 1 − 2u0) (src/transport.py:274-285), or 0 when not certain: u1 and u0 must
+// clear the sign changes by 1e-6 (sin(2π·1e-6) ≫ the float64 rounding of cos/sin), and
+// sinθ = 2√(u0(1 − u0)) vanishes only at u0 ∈ {0, 1}.
+__device__ __forceinline__ int draw_sign(int a, double u0, double u1) {
+  constexpr double m = 1e-6;
+  if (a == 2) return u0 < 0.5 - m ? 1 : (u0 > 0.5 + m ? -1 : 0);
+  if (!(u0 > 0.0 && u0 < 1.0)) return 0;
+  if (a == 0) return (u1 < 0.25 - m || u1 > 0.75 + m) ? 1 : ((u1 > 0.25 + m && u1 < 0.75 - m) ? -1 : 0);
+  return (u1 > m && u1 < 0.5 - m) ? 1 : ((u1 > 0.5 + m && u1 < 1.0 - m) ? -1 : 0);
+}
+
+// Cheap first stage for axis-aligned emitter planes (pax[g] = axis, −1 otherwise): a plane
+// can be met only if the ray moves toward it, i.e. sign(n·d) = sign(c − n·y) whenever the
+// sample is farther than `tol` from the plane (a hit needs a landing distance > 0).  False
+// only when every plane is certainly behind the ray; the survivors take the full test.
+__device__ __forceinline__ bool emitter_ahead(const FilterPlane* fp, const int* pax, int ng, const float* y,
+                                             double u0, double u1, float tol) {
+  for (int g = 0; g < ng; ++g) {
+    const int a = pax[g];
+    if (a < 0) return true;
+    const float4 nc = fp[g].nc;
+    const float sgn = a == 0 ? nc.x : (a == 1 ? nc.y : nc.z);  // ±1
+    const float s = nc.w - sgn * (a == 0 ? y[0] : (a == 1 ? y[1] : y[2]));
+    if (!(fabsf(s) > tol)) return true;
+    const int sd = draw_sign(a, u0, u1);
+    if (sd == 0 || ((sgn * (float)sd > 0.0f) == (s > 0.0f))) return true;
+  }
+  return false;
+}
+
 __device__ __forceinline__ bool emitter_may_hit(const FilterPlane* fp, const unsigned* occ, int ng,
                                                 const float* y, double u0, double u1, float ey, float mpad) {
   const float om = (float)(1.0 - u0), z = (float)(1.0 - 2.0 * u0);
@@ -483,6 +518,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
   __shared__ PendSample pend_all[256 / 32][kPendCap];
   __shared__ FilterPlane fplane[kEmitPlanes];
   __shared__ unsigned focc[kEmitPlanes * 32];
+  __shared__ int fpax[kEmitPlanes];
   const bool filt = D == 3 && S.ep.ng > 0 && S.ep.occ != nullptr;
   if (filt) {
     for (int t = threadIdx.x; t < kEmitPlanes * 32; t += blockDim.x) focc[t] = S.ep.occ[t];
@@ -501,6 +537,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
                                  (float)(E.lo[g][1] - dotc(E.a2[g])));
       fplane[g].cc = make_float4((float)E.occ_inv[g][0], (float)E.occ_inv[g][1], __int_as_float(E.occ_w[g]),
                                  __int_as_float(E.occ_h[g]));
+      fpax[g] = VC_EMIT_AHEAD ? E.axis[g] : -1;
     }
     __syncthreads();
   }
@@ -645,7 +682,8 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
             const float4 dk = W.dirs32[(size_t)rec * n + k];
             const float ri = ((float)i + 0.5f) * f_step;
             const float y32[3] = {xr[0] + ri * dk.x, xr[1] + ri * dk.y, xr[2] + ri * dk.z};
-            keep = emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
+            keep = emitter_ahead(fplane, fpax, S.ep.ng, y32, u0, u1, 2.0f * f_ey + f_pad) &&
+                   emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
           } else {
             double y[3];
             origin(k, i, y);
@@ -1219,7 +1257,7 @@ __device__ __forceinline__ bool hull_star(const Wave& W, const double* dirs, con
 
 template <class T, int BS>
 __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, int rec, int i, typename Vec2<T>::V* us,
-                                          unsigned char* hs, int* own, int* own_cnt, bool cull = false) {
+                                          unsigned char* hs, int* own, int* own_cnt) {
   const int n = P.n_angular, rows = P.rows, cols = P.cols;
   const int r0 = i / cols, c0 = i - r0 * cols;
   const int hw = r0 < kDelRowsMax ? P.del_hw[r0] : 0;
@@ -1247,47 +1285,10 @@ __device__ __forceinline__ bool hull_cell(const BuildParams& P, const Wave& W, i
       q = (q == rowe) ? rowp : q;
     }
   }
-  // Culling: the projections of directions farther than the cull chord (|u| < u_c,
-  // u_c = 2 / chord) are dropped before the wrap and the survivors compacted (their window
-  // slots kept as a 64-bit mask in registers); the hull of the survivors is the hull of all candidates iff it
-  // contains the disk |u| ≤ u_c, checked per hull edge with the float32 error margins —
-  // else the cell goes to the clipping kernel.
-  int Kw = K, startw = start;
-  const T thr2 = (T)P.del_cull_u2;
-  unsigned keep_lo = 0u, keep_hi = 0u;  // survivors' window slots (K ≤ 64)
-  if (cull && thr2 > (T)0) {
-    int Kc = 0;
-    n1 = 0;
-    for (int k = 0; k < K; ++k) {
-      const auto u = us[k * BS];
-      if (u.x * u.x + u.y * u.y >= thr2) {  // NaN (the centre) is dropped
-        if (k == start) startw = Kc;
-        us[Kc * BS] = u;
-        if (k < 32) keep_lo |= 1u << k;
-        else keep_hi |= 1u << (k - 32);
-        n1 = fmax(n1, fabs(u.x) + fabs(u.y));
-        ++Kc;
-      }
-    }
-    if (Kc < 3) return false;
-    Kw = Kc;
-  }
-  const int hn = gift_wrap<T, BS>(us, Kw, startw, n1, hs);
-  if (Kw < K && hn >= 3) {
-    for (int t = 0; t < hn; ++t) {
-      const auto a = us[hs[t * BS] * BS];
-      const auto b = us[hs[(t + 1 == hn ? 0 : t + 1) * BS] * BS];
-      const T na = fabs(a.x) + fabs(a.y), nb = fabs(b.x) + fabs(b.y);
-      const T cr = a.x * b.y - a.y * b.x - (T)64 * Vec2<T>::kEps * (na + nb) * (na + nb);
-      const T ex = b.x - a.x, ey = b.y - a.y;
-      if (!(cr > (T)0 && cr * cr >= thr2 * (T)1.002 * (ex * ex + ey * ey))) return false;
-    }
-  }
+  const int hn = gift_wrap<T, BS>(us, K, start, n1, hs);
   // candidate k → direction index (k / wc by a 16-bit reciprocal, exact for k < 2¹⁶/wc²)
   const unsigned rwc = (65536u + wc - 1) / wc;
-  const int nlo = __popc(keep_lo);
-  auto gidx = [&](int kw) {  // survivor kw → its window slot: the kw-th set bit of the mask
-    const int k = (Kw == K) ? kw : (kw < nlo ? (int)__fns(keep_lo, 0, kw + 1) : 32 + (int)__fns(keep_hi, 0, kw - nlo + 1));
+  auto gidx = [&](int k) {
     const int a = (int)(((unsigned)k * rwc) >> 16);
     int col = col0 + (k - a * wc);
     col -= (col >= cols) ? cols : 0;
@@ -1325,7 +1326,7 @@ __global__ void __launch_bounds__(kHullBS) k_delaunay_hull(BuildParams P, Wave W
     const int rs = rem / cols;
     const int i = (int)P.del_rows[P.del_cls[cls] + rs] * cols + (rem - rs * cols);
     cell = rec * n + i;
-    fb = !hull_cell<float, kHullBS>(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt, true);
+    fb = !hull_cell<float, kHullBS>(P, W, rec, i, hsm + threadIdx.x, hs, own, own_cnt);
   }
   const unsigned m = __ballot_sync(0xffffffffu, fb);
   if (m) {

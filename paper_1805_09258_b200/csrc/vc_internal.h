@@ -121,7 +121,6 @@ struct BuildParams {
   int del_cls[4];
   int del_cls_k[3];
   double del_zstep;  // 2 / rows: stratum height in z
-  double del_cull_u2;  // hull kernel: window candidates with |u|² below this are culled (0: off)
   int del_cap;       // 1: the polar rows go to the cap kernel
   float del_cap_cos, del_cap_sin;  // cos δ, sin δ: the cap kernel's candidate radius
   double del_cap_c2, del_cap_s2;  // cos²(δ/2), sin²(δ/2)
