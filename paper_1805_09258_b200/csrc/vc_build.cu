@@ -365,10 +365,6 @@ __device__ __forceinline__ void store_media(float* out, const double* v) {
 #ifndef VC_QCHUNK
 #define VC_QCHUNK 32
 #endif
-// first-stage direction-sign test of the emitter pre-filter (emitter_ahead); 0: off
-#ifndef VC_EMIT_AHEAD
-#define VC_EMIT_AHEAD 1
-#endif
 constexpr int kQChunk = VC_QCHUNK;  // queue slots a warp reserves with one atomic
 static_assert(kQChunk >= 32, "a step's hits (≤ 32) must fit one fresh chunk");
 
@@ -434,37 +430,6 @@ struct alignas(16) FilterPlane {  // four 16-byte shared-memory loads per plane
   float4 cc;   // 1 / block size (x, y), blocks (x, y) as int bits
 };
 
-// Sign of the gather direction's axis-a component from the draws alone, d = (sinθ·cos 2πu1,
-// sinθ·sin 2πu1, 1 − 2u0) (src/transport.py:274-285), or 0 when not certain: u1 and u0 must
-// clear the sign changes by 1e-6 (sin(2π·1e-6) ≫ the float64 rounding of cos/sin), and
-// sinθ = 2√(u0(1 − u0)) vanishes only at u0 ∈ {0, 1}.
-__device__ __forceinline__ int draw_sign(int a, double u0, double u1) {
-  constexpr double m = 1e-6;
-  if (a == 2) return u0 < 0.5 - m ? 1 : (u0 > 0.5 + m ? -1 : 0);
-  if (!(u0 > 0.0 && u0 < 1.0)) return 0;
-  if (a == 0) return (u1 < 0.25 - m || u1 > 0.75 + m) ? 1 : ((u1 > 0.25 + m && u1 < 0.75 - m) ? -1 : 0);
-  return (u1 > m && u1 < 0.5 - m) ? 1 : ((u1 > 0.5 + m && u1 < 1.0 - m) ? -1 : 0);
-}
-
-// Cheap first stage for axis-aligned emitter planes (pax[g] = axis, −1 otherwise): a plane
-// can be met only if the ray moves toward it, i.e. sign(n·d) = sign(c − n·y) whenever the
-// sample is farther than `tol` from the plane (a hit needs a landing distance > 0).  False
-// only when every plane is certainly behind the ray; the survivors take the full test.
-__device__ __forceinline__ bool emitter_ahead(const FilterPlane* fp, const int* pax, int ng, const float* y,
-                                             double u0, double u1, float tol) {
-  for (int g = 0; g < ng; ++g) {
-    const int a = pax[g];
-    if (a < 0) return true;
-    const float4 nc = fp[g].nc;
-    const float sgn = a == 0 ? nc.x : (a == 1 ? nc.y : nc.z);  // ±1
-    const float s = nc.w - sgn * (a == 0 ? y[0] : (a == 1 ? y[1] : y[2]));
-    if (!(fabsf(s) > tol)) return true;
-    const int sd = draw_sign(a, u0, u1);
-    if (sd == 0 || ((sgn * (float)sd > 0.0f) == (s > 0.0f))) return true;
-  }
-  return false;
-}
-
 __device__ __forceinline__ bool emitter_may_hit(const FilterPlane* fp, const unsigned* occ, int ng,
                                                 const float* y, double u0, double u1, float ey, float mpad) {
   const float om = (float)(1.0 - u0), z = (float)(1.0 - 2.0 * u0);
@@ -518,7 +483,6 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
   __shared__ PendSample pend_all[256 / 32][kPendCap];
   __shared__ FilterPlane fplane[kEmitPlanes];
   __shared__ unsigned focc[kEmitPlanes * 32];
-  __shared__ int fpax[kEmitPlanes];
   const bool filt = D == 3 && S.ep.ng > 0 && S.ep.occ != nullptr;
   if (filt) {
     for (int t = threadIdx.x; t < kEmitPlanes * 32; t += blockDim.x) focc[t] = S.ep.occ[t];
@@ -537,7 +501,6 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
                                  (float)(E.lo[g][1] - dotc(E.a2[g])));
       fplane[g].cc = make_float4((float)E.occ_inv[g][0], (float)E.occ_inv[g][1], __int_as_float(E.occ_w[g]),
                                  __int_as_float(E.occ_h[g]));
-      fpax[g] = VC_EMIT_AHEAD ? E.axis[g] : -1;
     }
     __syncthreads();
   }
@@ -682,8 +645,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
             const float4 dk = W.dirs32[(size_t)rec * n + k];
             const float ri = ((float)i + 0.5f) * f_step;
             const float y32[3] = {xr[0] + ri * dk.x, xr[1] + ri * dk.y, xr[2] + ri * dk.z};
-            keep = emitter_ahead(fplane, fpax, S.ep.ng, y32, u0, u1, 2.0f * f_ey + f_pad) &&
-                   emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
+            keep = emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
           } else {
             double y[3];
             origin(k, i, y);

@@ -78,7 +78,11 @@ __global__ void k_idx_count(IdxGeom G, const double* rec, int n, int* cnt, int* 
   ovf[r] = fits ? 0 : 1;
 }
 
-__global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, unsigned long long* keys, int* vals) {
+// Cell key: level k above key_shift = d·(deepest occupied level), then the cell's linear
+// index (z·2^k + y)·2^k + x — as short as the occupied levels allow, so the radix sort runs
+// over key_shift + 5 bits.
+__global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, int key_shift,
+                           unsigned long long* keys, int* vals) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int lv, clo[3], chi[3];
@@ -87,8 +91,8 @@ __global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, 
   for (int z = clo[2]; z <= chi[2]; ++z)
     for (int y = clo[1]; y <= chi[1]; ++y)
       for (int x = clo[0]; x <= chi[0]; ++x) {
-        keys[o] = (unsigned long long)lv << 48 | (unsigned long long)z << 32 | (unsigned long long)y << 16 |
-                  (unsigned long long)x;
+        const unsigned long long cell = (((unsigned long long)z << lv | (unsigned long long)y) << lv) | x;
+        keys[o] = (unsigned long long)lv << key_shift | cell;
         vals[o] = r;
         ++o;
       }
@@ -376,21 +380,29 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_hrange, c->hcap * sizeof(int2));
   }
   c->hbits = hbits;
-  cudaFree(c->d_overflow);
-  c->d_overflow = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_overflow, (size_t)c->n_overflow * 4 + 4);
+  if (!c->d_overflow || c->ovf_cap < (size_t)c->n_overflow + 1) {  // grows only (no per-rebuild free)
+    cudaFree(c->d_overflow);
+    c->d_overflow = nullptr;
+    c->ovf_cap = std::max<size_t>((size_t)c->n_overflow + 1, 2 * c->ovf_cap);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_overflow, c->ovf_cap * 4);
+  }
   if (e == cudaSuccess && c->n_overflow)
     e = cudaMemcpyAsync(c->d_overflow, ovf_list, (size_t)c->n_overflow * 4, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->d_hkey, 0xff, (1ULL << hbits) * 8, st);
   if (e != cudaSuccess) return cuda_fail(e, "cache index buffers");
-  k_idx_emit<<<nb, 128, 0, st>>>(G, c->d_rec, n, off, keys, vals);
+  int kmax = 0;
+  for (int k = 0; k <= kMaxLevel; ++k)
+    if ((c->level_mask >> k) & 1u) kmax = k;
+  c->key_shift = c->dim * kmax;
+  const int end_bit = c->key_shift + 5;
+  k_idx_emit<<<nb, 128, 0, st>>>(G, c->d_rec, n, off, c->key_shift, keys, vals);
   // stable sort by cell keeps records in insertion order within a cell
   size_t rb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, c->d_items, T, 0, 53, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
   void* rtmp = alloc(11, rb);
   if (e != cudaSuccess) return cuda_fail(e, "cache index sort scratch");
   if (T > 0) {
-    cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, 53, st);
+    cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
     k_idx_hash<<<(T + 127) / 128, 128, 0, st>>>(keys2, T, hbits, c->d_hkey, c->d_hrange);
     k_idx_rows<<<(int)(((long long)T * kSide + 255) / 256), 256, 0, st>>>(c->d_items, T, c->d_side, c->d_rows);
   }

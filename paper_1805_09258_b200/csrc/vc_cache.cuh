@@ -45,7 +45,8 @@ struct DevCache {
   double size, inv_size;       // root cube
   unsigned level_mask;         // bit k: level k lists at least one record
   int hbits;                   // hash table: 2^hbits slots
-  const unsigned long long* hkey;  // cell key per slot (~0: empty): k << 48 | z << 32 | y << 16 | x
+  int key_shift;               // d · (deepest occupied level): cell keys are k << key_shift | cell
+  const unsigned long long* hkey;  // cell key per slot (~0: empty); cell = (z·2^k + y)·2^k + x
   const int2* hrange;          // the cell's entries [start, end)
   const int* items;            // record of each entry (cell order; insertion order within a cell)
   const float4* rows;          // kSide rejection rows per entry (copies of side[items[t]])
@@ -67,8 +68,8 @@ struct vc_cache {
   double origin[3] = {0, 0, 0}, size = 0.0;
   unsigned long long* d_hkey = nullptr;
   int2* d_hrange = nullptr;
-  int hbits = 0;
-  size_t hcap = 0;
+  int hbits = 0, key_shift = 0;
+  size_t hcap = 0, ovf_cap = 0;
   int* d_items = nullptr;
   float4* d_rows = nullptr;
   size_t items_cap = 0;
@@ -91,6 +92,7 @@ struct vc_cache {
     c.inv_size = 1.0 / size;
     c.level_mask = level_mask;
     c.hbits = hbits;
+    c.key_shift = key_shift;
     c.hkey = d_hkey;
     c.hrange = d_hrange;
     c.items = d_items;
@@ -291,9 +293,10 @@ __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, 
     for (unsigned m = C.level_mask; m; m &= m - 1) {
       const int k = __ffs(m) - 1;
       const double s = (double)(1u << k);
-      unsigned long long key = (unsigned long long)k << 48;
+      unsigned long long cell = 0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) key |= (unsigned long long)min((int)floor(u[a] * s), (1 << k) - 1) << (16 * a);
+      for (int a = D - 1; a >= 0; --a) cell = (cell << k) | (unsigned long long)min((int)floor(u[a] * s), (1 << k) - 1);
+      const unsigned long long key = (unsigned long long)k << C.key_shift | cell;
       const unsigned hm = (1u << C.hbits) - 1u;
       for (unsigned h = hash_slot(key, C.hbits);; h = (h + 1) & hm) {
         const unsigned long long kk = C.hkey[h];

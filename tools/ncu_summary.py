@@ -34,7 +34,8 @@ CLASS = {"primary": "primary", "rings": "rings", "wave_scan": "wave_scan", "gath
          "delaunay_hull": "delaunay", "delaunay_cap": "delaunay", "delaunay_capg": "delaunay", "cap_bin": "delaunay", "delaunay_warp": "delaunay", "delaunay_list": "delaunay",
          "delaunay_rest": "delaunay", "assemble_t": "assemble", "asm_eval": "assemble",
          "tri_compact": "tri_compact", "own_scan": "tri_compact", "tri_scatter": "tri_compact", "degree": "degree", "live_masks": "assemble", "assemble": "assemble",
-         "asm_final": "assemble", "make_record": "make_record", "seedseq": "seedseq"}
+         "asm_final": "assemble", "make_record": "make_record", "seedseq": "seedseq", "march": "march",
+         "interpolate": "interpolate"}
 
 
 def main():
