@@ -34,7 +34,7 @@ MEASURED = ROOT / "MEASURED_PEAKS.json"
 
 # Algorithmic flop model: divides/sqrt/exp/atan2 count 1.
 F_DIR3, F_REC, F_X3, F_LVL3, F_BOX3, F_ELEM3 = 20, 150, 45, 24, 12, 640
-F_TRI_POINT = 300  # spherical-Delaunay cell per direction (added: SURVEY's W omits qhull)
+ISSUE_PEAK = 4.0  # warp instructions per cycle per SM (4 SMSPs × 1 issue/cycle)
 
 
 def f_ray(K: int) -> int:
@@ -534,9 +534,8 @@ def main():
         "gather": P_sum * (6 + w.n_inner * (f_ray(K) + 10)),
         "primary": nrec * n * (F_DIR3 + f_ray(K)),
         "assemble": E_sum * F_ELEM3,
-        "delaunay": nrec * n * F_TRI_POINT,
         "make_record": nrec * 2 * F_REC,
-    }
+    }  # SURVEY.md §8d's W; the triangulation has no flop term there — it is rated on issue below
     names = _lib.KERNEL_CLASSES
     shares = {names[i]: float(kms[i]) for i in range(12) if kcnt[i] > 0}
     dom = max(shares, key=shares.get)
@@ -559,6 +558,22 @@ def main():
         if k in shares and shares[k] > 0:
             a = w_k / (shares[k] / 1e3) / 1e12
             per_kernel[k] = {"achieved_tflops": a, "frac": a / pk["fp32_tflops"], "ms": shares[k]}
+    # issue-rate bound per kernel class: warp instructions of one 2048-record wave (ncu capture,
+    # profiles/ncu_traffic.json "inst_per_class") scaled to the records timed here, over the
+    # live CUDA-event time → achieved warp instructions per SM-cycle, against 4
+    inst_model = {}
+    if tf.exists():
+        try:
+            inst_model = json.loads(tf.read_text()).get("inst_per_class", {})
+        except Exception:
+            inst_model = {}
+    f_sm = (clk.summary().get("sm_mhz") or pk["sm_max_mhz"]) * 1e6
+    for k, inst in inst_model.items():
+        if k in shares and shares[k] > 0:
+            ipc = inst * (nrec / 2048.0) / (shares[k] / 1e3) / (148 * f_sm)
+            per_kernel.setdefault(k, {"ms": shares[k]})
+            per_kernel[k]["issue_ipc_per_sm"] = ipc
+            per_kernel[k]["issue_frac"] = ipc / ISSUE_PEAK
     w_path = sum(work.values())
     path_achieved = w_path / (ms / 1e3) / 1e12
     roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",

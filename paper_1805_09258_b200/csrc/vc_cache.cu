@@ -19,6 +19,10 @@ namespace vc {
 // Index build on the device
 // ---------------------------------------------------------------------------
 
+#ifndef VC_CELL_SPAN
+#define VC_CELL_SPAN 2.0
+#endif
+
 struct IdxGeom {
   int dim;
   double origin[3], size, inv_size;
@@ -53,8 +57,8 @@ __device__ inline bool record_cells(const IdxGeom& G, const double* R, int& lv, 
     if (!(lo[a] >= 0.0 && hi[a] < 1.0)) fits = false;
   }
   if (!fits) return false;
-  lv = 0;  // deepest level whose cells are ≥ 2·emax
-  while (lv < kMaxLevel && G.size / (double)(1 << (lv + 1)) >= 2.0 * emax) ++lv;
+  lv = 0;  // deepest level whose cells are ≥ VC_CELL_SPAN·emax (2: ≤ 2 cells per axis; 1: ≤ 3)
+  while (lv < kMaxLevel && G.size / (double)(1 << (lv + 1)) >= VC_CELL_SPAN * emax) ++lv;
   const double s = (double)(1 << lv);
   for (int a = 0; a < 3; ++a) clo[a] = chi[a] = 0;
   for (int a = 0; a < d; ++a) {

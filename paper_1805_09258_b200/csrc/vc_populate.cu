@@ -367,6 +367,7 @@ struct Engine {
   int C = 2048;
   long long L = 65536, Lmax = 1LL << 24;
   double kappa = 1.0, h_sel = INFINITY;
+  double waste_ratio = 1.0;  // VOLCACHE_POP_WASTE: target discarded / committed builds per window
   int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaError_t e = cudaSuccess;
 
@@ -671,7 +672,9 @@ int Engine::run() {
         }
       if (!rmin.empty()) {
         std::nth_element(rmin.begin(), rmin.begin() + rmin.size() / 2, rmin.end());
-        if (covered > committed) kappa *= 1.25;
+        // controller: grow the selection cell while speculative builds that turned out
+        // covered exceed waste_ratio × committed ones, shrink it otherwise
+        if (covered > waste_ratio * committed) kappa *= 1.25;
         else kappa *= 0.9;
         kappa = std::min(8.0, std::max(0.1, kappa));
         h_sel = kappa * rmin[rmin.size() / 2];
@@ -800,6 +803,7 @@ int vc::populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, 
   g.commit_list = rs != nullptr;
   g.estimator = pp->estimator == VC_EST_BASELINE ? VC_EST_BASELINE : VC_EST_SUBDIVISION;
   g.hook = pp->build_hook;
+  if (const char* ew = getenv("VOLCACHE_POP_WASTE")) g.waste_ratio = std::max(0.05, atof(ew));
   g.hook_user = pp->build_hook_user;
   g.blp.n_angular = pp->n_angular;
   g.blp.max_media_bounces = pp->max_media_bounces;

@@ -13,6 +13,7 @@ METRICS = [
     "sm__inst_executed.avg.per_cycle_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "lts__t_bytes.sum", "l1tex__t_bytes.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "local_load_bytes", "smsp__sass_inst_executed_op_local_ld.sum",
+    "sm__inst_executed.sum",
 ]
 
 
@@ -78,7 +79,17 @@ def main():
             c = CLASS.get(k)
             if c:
                 per_class[c] = per_class.get(c, 0.0) + v
-        json.dump({"report": rep, "per_kernel": traffic, "per_class": per_class}, open(traffic_out, "w"), indent=1)
+        inst = defaultdict(float)  # warp instructions per class over the captured launches
+        for row in rows:
+            short = row[col["Kernel Name"]].split("(")[0].replace("void ", "")
+            key = short.replace("vc::", "").replace("k_", "").split("<")[0]
+            c = CLASS.get(key)
+            for m in ("sm__inst_executed.sum", "smsp__inst_executed.sum"):
+                if c and m in col and row[col[m]] not in ("", "n/a"):
+                    inst[c] += float(row[col[m]].replace(",", ""))
+                    break
+        json.dump({"report": rep, "per_kernel": traffic, "per_class": per_class, "inst_per_class": dict(inst)},
+                  open(traffic_out, "w"), indent=1)
     print(open(md).read())
 
 
