@@ -120,7 +120,13 @@ def workload(args):
     from paper_1805_09258_b200 import configs
 
     if args.config == "cfg3":
-        return configs.cfg3()
+        w = configs.cfg3()
+        if getattr(args, "media_bounces", 1) > 1:  # extension: BASELINE cfg3's multi-bounce media radiance
+            import dataclasses
+
+            w = dataclasses.replace(w, name=f"{w.name}+{args.media_bounces}-bounce-media",
+                                    media_bounces=args.media_bounces)
+        return w
     if args.config == "cfg2":
         return configs.cfg2(march_step=args.march_step or 4.0)
     if args.config == "cfg1":
@@ -174,7 +180,7 @@ def cpu_sample(w, n_records: int, start: int = 0):
     t0 = time.perf_counter()
     for i in cpu_points(w, n_records, start):
         rb = O.build_record(ps, w.points[i], w.n_angular, w.march_step, O.seed_seq(w.seed, 401, i), w.n_inner,
-                            w.n_light_samples)
+                            w.n_light_samples, media_bounces=w.media_bounces)
         for k in range(2):
             O.make_record(w.points[i], rb.L[k], rb.grad[k], rb.hess[k], w.epsilon, ps.scale, ps.max_emission)
     dt = time.perf_counter() - t0
@@ -338,9 +344,10 @@ def run_cfg5(args):
     from paper_1805_09258_b200.renderer import render
 
     t0 = time.perf_counter()
-    for _ in range(max(1, args.e2e_steps)):
+    e2e_n = max(1, args.e2e_steps if args.e2e_steps is not None else 3)  # cfg5: whole frames
+    for _ in range(e2e_n):
         image_h, rst = render(sc, cam, st, cache_set=cs)
-    e2e_s = (time.perf_counter() - t0) / max(1, args.e2e_steps)
+    e2e_s = (time.perf_counter() - t0) / e2e_n
     # covering records per lookup (single, multiple) on a sample of march points
     sample, _ = cfg5_march_points(sc, cam, st.march_step, (0, cam.height), (0, cam.width)) \
         if args.cfg5_full_sample else cfg5_march_points(sc, cam, st.march_step, (cam.height // 2 - 30, 60),
@@ -411,8 +418,10 @@ def main():
     ap.add_argument("--records-per-step", type=int, default=2048)
     ap.add_argument("--cpu-records", type=int, default=4, help="oracle records in the cpu_baseline sample")
     ap.add_argument("--ref-records", type=int, default=4, help="--impl reference: oracle records per timed step")
+    ap.add_argument("--media-bounces", type=int, default=1,
+                    help="cfg3 extension: media events per gather path (1 = the reference's estimator)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="e2e timed steps (default: --steps)")
     ap.add_argument("--cfg5-eps", type=float, default=None, help="cfg5: record-error target ε (default tuned)")
     ap.add_argument("--cfg5-full-sample", action="store_true", help="cfg5: covering counts over the whole frame")
     args = ap.parse_args()
@@ -438,7 +447,7 @@ def main():
     B = args.records_per_step
     ds = device_scene(w.scene)
     kw = dict(n_angular=w.n_angular, march_step=w.march_step, n_inner=w.n_inner,
-              n_light_samples=w.n_light_samples, epsilon=w.epsilon)
+              n_light_samples=w.n_light_samples, epsilon=w.epsilon, media_bounces=args.media_bounces)
     total_steps = args.warmup + args.steps
     # inputs resident in HBM before timing
     Xs, Ss = [], []
@@ -494,7 +503,7 @@ def main():
     value = records / (ms_max / 1e3)
 
     # ---- e2e: public API with pinned host buffers, H2D + D2H inside the timed region ----
-    e2e_steps = max(1, args.e2e_steps)
+    e2e_steps = max(1, args.e2e_steps if args.e2e_steps is not None else args.steps)
     Xh = [torch.tensor(w.points[step_indices(s, rank, world, B, N)]).pin_memory().numpy() for s in range(e2e_steps)]
     Sh = [torch.tensor(seed_words(w.seed, 401, step_indices(s, rank, world, B, N)).astype(np.int32))
           .pin_memory().numpy().view(np.uint32) for s in range(e2e_steps)]
@@ -507,6 +516,7 @@ def main():
     prm.n_angular, prm.march_step, prm.n_inner = w.n_angular, w.march_step, w.n_inner
     prm.n_light_samples, prm.epsilon = w.n_light_samples, w.epsilon
     prm.flags = _lib.VC_MEM_HOST | _lib.VC_SEED_WORDS | _lib.VC_MAKE_RECORDS
+    prm.media_bounces = args.media_bounces
     prm.seed_words = 3
     barrier()
     torch.cuda.synchronize()

@@ -74,6 +74,10 @@ typedef struct {
   double epsilon;      /* make_record error budget */
   int flags;           /* VC_* flags */
   int seed_words;      /* entropy words per record when VC_SEED_WORDS */
+  int media_bounces;   /* extension: media scattering events per gather path (0/1 = the
+                          reference's one-bounce gather; ≤ 8): the multiple-scattering loop of
+                          path_trace_radiance continued from each media sample, its draws taken
+                          from the record's stream after every draw the reference makes */
 } vc_build_params;
 
 /* Batch estimate_moments (+ make_record for both kinds).

@@ -437,6 +437,43 @@ def gather_mean(ps, points, dirs_pp, n_light):  # src/transport.py:288-310
     return tot.reshape(m, n, 3).mean(axis=1)
 
 
+def gather_mean_bounces(ps, points, dirs_pp, n_light, extras, bounces):
+    """Extension (BASELINE.json cfg3 "multiple scattering up to 4 bounces"; the reference
+    stops at one extra bounce): the media-sample gather continued by up to `bounces` − 1
+    further media scattering events per gather path, restating the multiple-scattering loop
+    of path_trace_radiance (src/transport.py:362-388) — collision distance
+    −log1p(−u)/σt against the current segment, weight σs/σt per collision, a uniform new
+    direction, T·L_o at its surface hit added with the path weight.  `extras` (m, n, B−1, d')
+    holds per path and bounce (u_dist, direction draws): the record's PCG64 stream continued
+    after every draw the reference makes (build_record).  bounces = 1 → gather_mean."""
+    m, n, dim = dirs_pp.shape
+    org = np.repeat(points, n, axis=0)
+    dd = dirs_pp.reshape(-1, dim)
+    s, idx = trace_or_bounds(ps, org, dd)
+    tot = np.exp(-ps.sigma_t * s)[:, None] * surface_radiance(ps, idx, org + s[:, None] * dd, dd, n_light)
+    if bounces > 1 and ps.sigma_t > 0.0:
+        ex = extras.reshape(m * n, bounces - 1, -1)
+        w = np.ones(m * n)
+        alive = np.ones(m * n, bool)
+        pos, cur_d, cur_s = org, dd, s
+        for b in range(bounces - 1):
+            t = -np.log1p(-ex[:, b, 0]) / ps.sigma_t
+            col = alive & (t < cur_s)
+            if not np.any(col):
+                break
+            pos = pos + np.where(col, t, 0.0)[:, None] * cur_d
+            w = w * np.where(col, ps.sigma_s / ps.sigma_t, 1.0)
+            nd = uniform_dirs(dim, ex[:, b, 1] if dim == 2 else ex[:, b, 1:3])
+            s2 = np.zeros(m * n)
+            s2[col], idx2 = trace_or_bounds(ps, pos[col], nd[col])
+            lo2 = surface_radiance(ps, idx2, pos[col] + s2[col, None] * nd[col], nd[col], n_light)
+            tot[col] += w[col, None] * np.exp(-ps.sigma_t * s2[col])[:, None] * lo2
+            alive = col
+            cur_d = nd
+            cur_s = s2
+    return tot.reshape(m, n, 3).mean(axis=1)
+
+
 # ---------------------------------------------------------------------------
 # Form factors with derivatives (src/formfactor.py:85-343)
 # ---------------------------------------------------------------------------
@@ -565,6 +602,7 @@ def build_record(
     n_inner: int = 1,
     n_light_samples: int = 16,
     adjacency=None,
+    media_bounces: int = 1,
 ) -> RecordBuild:
     """One cache point: `estimate_moments` (src/subdivision.py:373-393) in one pass.
 
@@ -604,7 +642,12 @@ def build_record(
         else:
             u = rng.random((p.shape[0], n_inner, 2))
             gd = uniform_dirs(3, u.reshape(-1, 2)).reshape(p.shape[0], n_inner, 3)
-        media_rad.reshape(-1, 3)[flat] = ps.sigma_s * gather_mean(ps, p, gd, n_light_samples)
+        if media_bounces > 1:  # extension: the stream continues after the reference's draws
+            ex = rng.random((p.shape[0], n_inner, media_bounces - 1, 2 if dim == 2 else 3))
+            media_rad.reshape(-1, 3)[flat] = ps.sigma_s * gather_mean_bounces(ps, p, gd, n_light_samples, ex,
+                                                                            media_bounces)
+        else:
+            media_rad.reshape(-1, 3)[flat] = ps.sigma_s * gather_mean(ps, p, gd, n_light_samples)
 
     fbar = ps.sigma_s / (2.0 * np.pi if dim == 2 else 4.0 * np.pi)
     sig = ps.sigma_t

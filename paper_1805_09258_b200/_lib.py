@@ -42,6 +42,7 @@ class BuildParams(C.Structure):
         ("epsilon", C.c_double),
         ("flags", C.c_int),
         ("seed_words", C.c_int),
+        ("media_bounces", C.c_int),
     ]
 
 

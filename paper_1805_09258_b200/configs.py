@@ -31,6 +31,7 @@ class Workload:
     n_inner: int = 1
     n_light_samples: int = 16
     epsilon: float = 0.05
+    media_bounces: int = 1  # extension: media events per gather path (1 = the reference)
 
     @property
     def dim(self) -> int:

@@ -255,7 +255,9 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
   const int n = P.n_angular;
   const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
   const int per = (D == 3 ? 2 : 1) * P.n_inner;
-  const bool emitter_first = !S.reflective && 2 * S.emit.K <= S.geo.K;
+  const int nb = P.media_bounces - 1;  // extension: further media events per gather path
+  const bool emitter_first = !S.reflective && 2 * S.emit.K <= S.geo.K && nb == 0;
+  const double albedo = S.sigma_t > 0.0 ? __ddiv_rn(S.sigma_s, S.sigma_t) : 0.0;
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total;
        j += (long long)gridDim.x * blockDim.x) {
     // record: last r with base[r] ≤ j
@@ -310,16 +312,64 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
       } else {
         trace_or_bounds<D>(S, y, gd, s2, id2);
       }
+      double path[3] = {0.0, 0.0, 0.0};
       if (id2 >= 0) {
         double hp[3], L[3];
 #pragma unroll
         for (int c = 0; c < D; ++c) hp[c] = add(y[c], mul(s2, gd[c]));
         surface_radiance<D>(S, id2, hp, gd, L);
         double T = exp(-S.sigma_t * s2);
-        acc[0] = add(acc[0], mul(T, L[0]));
-        acc[1] = add(acc[1], mul(T, L[1]));
-        acc[2] = add(acc[2], mul(T, L[2]));
+        path[0] = mul(T, L[0]);
+        path[1] = mul(T, L[1]);
+        path[2] = mul(T, L[2]);
       }
+      if (nb > 0 && S.sigma_t > 0.0) {
+        // Extension: the multiple-scattering loop of path_trace_radiance (src/transport.py:
+        // 362-388) from y along the gather ray — collision at −log1p(−u)/σt inside the current
+        // segment, weight σs/σt, uniform new direction, T·L_o at its hit — with this path's
+        // draws from the record stream after every reference draw (oracle: gather_mean_bounces)
+        constexpr int pb = (D == 3) ? 3 : 2;
+        Pcg64 gx = pcg_load(W.rng + 4 * rec);
+        pcg_advance(gx, (unsigned long long)(draws0 + (long long)per * W.rec_P[rec] +
+                                             ((long long)jl * P.n_inner + t) * nb * pb), jt);
+        double pos[3] = {y[0], y[1], y[2]}, cd[3] = {gd[0], gd[1], gd[2]}, cs = s2, w = 1.0;
+        for (int bb = 0; bb < nb; ++bb) {
+          const double ud = gx.next_double();
+          const double ua = gx.next_double();
+          const double ub = (D == 3) ? gx.next_double() : 0.0;
+          const double tc = __ddiv_rn(-log1p(-ud), S.sigma_t);
+          if (!(tc < cs)) break;  // the path leaves this segment through its surface / bounds
+#pragma unroll
+          for (int c = 0; c < D; ++c) pos[c] = add(pos[c], mul(tc, cd[c]));
+          w = mul(w, albedo);
+          if constexpr (D == 2) {
+            const double th = mul(2.0 * kPi, ua);
+            cd[0] = cos(th);
+            cd[1] = sin(th);
+          } else {
+            const double z = sub(1.0, mul(2.0, ua));
+            const double phi = mul(2.0 * kPi, ub);
+            const double sq = sqrt(fmax(sub(1.0, mul(z, z)), 0.0));
+            cd[0] = mul(sq, cos(phi));
+            cd[1] = mul(sq, sin(phi));
+            cd[2] = z;
+          }
+          int id3;
+          trace_or_bounds<D>(S, pos, cd, cs, id3);
+          if (id3 >= 0) {
+            double hp[3], L[3];
+#pragma unroll
+            for (int c = 0; c < D; ++c) hp[c] = add(pos[c], mul(cs, cd[c]));
+            surface_radiance<D>(S, id3, hp, cd, L);
+            const double wT = mul(w, exp(-S.sigma_t * cs));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) path[c] = add(path[c], mul(wT, L[c]));
+          }
+        }
+      }
+      acc[0] = add(acc[0], path[0]);
+      acc[1] = add(acc[1], path[1]);
+      acc[2] = add(acc[2], path[2]);
     }
     float* out = W.media + (size_t)(W.rec_base[rec] + jl) * 3;
     bool pos = false;
@@ -2490,8 +2540,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   // live-sample masks are set by the gather itself (mark_live)
   cudaMemsetAsync(W.live, 0, sizeof(unsigned long long) * (size_t)W.live_words * nt, st);
   if (S.sigma_s > 0.0) {
-    const bool two_pass =
-        !S.reflective && 2 * S.emit.K <= S.geo.K && P.n_inner == 1 && W.gather_q_cap > 0;
+    const bool two_pass = !S.reflective && 2 * S.emit.K <= S.geo.K && P.n_inner == 1 && W.gather_q_cap > 0 &&
+                          P.media_bounces <= 1;
     prof_begin(KC_GATHER, st);
     if (two_pass) {
       cudaMemsetAsync(W.gather_q_count, 0, sizeof(unsigned long long), st);

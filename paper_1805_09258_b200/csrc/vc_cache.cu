@@ -19,13 +19,10 @@ namespace vc {
 // Index build on the device
 // ---------------------------------------------------------------------------
 
-#ifndef VC_CELL_SPAN
-#define VC_CELL_SPAN 2.0
-#endif
-
 struct IdxGeom {
   int dim;
   double origin[3], size, inv_size;
+  double span;  // cells of a record's level are ≥ span × its largest AABB extent
 };
 
 // Level and cell range of record R; false → overflow list (box leaves the root cube or is
@@ -57,8 +54,8 @@ __device__ inline bool record_cells(const IdxGeom& G, const double* R, int& lv, 
     if (!(lo[a] >= 0.0 && hi[a] < 1.0)) fits = false;
   }
   if (!fits) return false;
-  lv = 0;  // deepest level whose cells are ≥ VC_CELL_SPAN·emax (2: ≤ 2 cells per axis; 1: ≤ 3)
-  while (lv < kMaxLevel && G.size / (double)(1 << (lv + 1)) >= VC_CELL_SPAN * emax) ++lv;
+  lv = 0;  // deepest level whose cells are ≥ span·emax (span 2: ≤ 2 cells per axis; 1: ≤ 3)
+  while (lv < kMaxLevel && G.size / (double)(1 << (lv + 1)) >= G.span * emax) ++lv;
   const double s = (double)(1 << lv);
   for (int a = 0; a < 3; ++a) clo[a] = chi[a] = 0;
   for (int a = 0; a < d; ++a) {
@@ -324,6 +321,7 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   for (int a = 0; a < 3; ++a) G.origin[a] = c->origin[a];
   G.size = c->size;
   G.inv_size = 1.0 / c->size;
+  G.span = c->cell_span;
   int* cnt = (int*)alloc(0, (size_t)n * 4);
   int* ovf = (int*)alloc(1, (size_t)n * 4);
   int* off = (int*)alloc(2, ((size_t)n + 1) * 4);

@@ -103,6 +103,7 @@ struct BuildParams {
   int n_angular;
   double march_step;
   int n_inner;
+  int media_bounces;     // media events per gather path (1: the reference; extension > 1)
   int rows, cols;        // 3D stratum grid (src/scene.py:370-385); 2D: rows = 1, cols = n
   int n_tris;            // elements per ring: n (2D) or 2n-4 (3D)
   int r_ub;              // upper bound on rings per record (allocation)

@@ -782,8 +782,25 @@ int Engine::run() {
 // Stream setup + engine run on existing caches (records with tag −1 pre-exist).
 // seed_kind 2 (camera render with insertion) marches spp jittered passes and hands the
 // ray prefix and the committed direct values to the caller through `rs`.
+static int populate_run_impl(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
+                             int64_t* stats, cudaStream_t st, double* commit_J, int spp, RenderStream* rs);
+
+// The engine rebuilds the indexes after every window with the coarser cell span; the
+// finished caches are re-indexed at the lookup span (vc_cache::cell_span).
 int vc::populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
                      int64_t* stats, cudaStream_t st, double* commit_J, int spp, RenderStream* rs) {
+  const double span_s = cs->cell_span, span_m = cm->cell_span;
+  cs->cell_span = cm->cell_span = 2.0;
+  int rc = populate_run_impl(sc, pp, seed_kind, cs, cm, stats, st, commit_J, spp, rs);
+  cs->cell_span = span_s;
+  cm->cell_span = span_m;
+  if (!rc) rc = cache_rebuild(cs, st);
+  if (!rc) rc = cache_rebuild(cm, st);
+  return rc;
+}
+
+static int populate_run_impl(vc_scene* sc, const vc_populate_params* pp, int seed_kind, vc_cache* cs, vc_cache* cm,
+                             int64_t* stats, cudaStream_t st, double* commit_J, int spp, RenderStream* rs) {
   if (!(pp->march_step > 0.0)) return fail(VC_EINVAL, "march_step must be positive");
   if (!(pp->epsilon > 0.0)) return fail(VC_EINVAL, "epsilon must be positive");
   Engine g;

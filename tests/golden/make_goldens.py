@@ -592,6 +592,83 @@ def _chunked_trace(orig, chunk=64):
     return trace
 
 
+def _gather_bounces_shim(seed_box, bounces):
+    """Extension oracle written with the reference's own primitives: mean_surface_gather
+    (src/transport.py:288-310) continued by up to `bounces` − 1 media scattering events per
+    gather path, exactly the multiple-scattering loop of path_trace_radiance
+    (src/transport.py:362-388); per path and bounce the draws (u_dist, u0, u1) come from the
+    record's stream continued after every draw build_subdivision makes (2·n directions,
+    then 2·n_inner per media sample)."""
+    import volcache.transport as vt
+
+    def gather(scene, points, dirs_per_point, n_light_samples=16):
+        m, n, dim = dirs_per_point.shape
+        per_dir = 2 if dim == 3 else 1  # draws per stratum jitter and per gather direction
+        g = np.random.default_rng(seed_box["seed"])
+        g.bit_generator.advance(per_dir * seed_box["n_dirs"] + per_dir * m * n)
+        ex = g.random((m * n, bounces - 1, 3 if dim == 3 else 2))
+        origins = np.repeat(points, n, axis=0)
+        dirs = dirs_per_point.reshape(-1, dim)
+        s, idx = vscene.trace_or_bounds(scene, origins, dirs)
+        tot = np.exp(-scene.medium.sigma_t * s)[:, None] * vt.surface_radiance_batch(
+            scene, idx, origins + s[:, None] * dirs, dirs, n_light_samples)
+        sig_t, sig_s = scene.medium.sigma_t, scene.medium.sigma_s
+        w = np.ones(m * n)
+        alive = np.ones(m * n, dtype=bool)
+        pos, cur_d, cur_s = origins, dirs, s
+        for b in range(bounces - 1):
+            t = -np.log1p(-ex[:, b, 0]) / sig_t
+            collide = alive & (t < cur_s)
+            if not np.any(collide):
+                break
+            pos = pos + np.where(collide, t, 0.0)[:, None] * cur_d
+            w = w * np.where(collide, sig_s / sig_t, 1.0)
+            nd = vt.uniform_directions(dim, ex[:, b, 1] if dim == 2 else ex[:, b, 1:3])
+            s2 = np.zeros(m * n)
+            s2[collide], idx2 = vscene.trace_or_bounds(scene, pos[collide], nd[collide])
+            lo2 = vt.surface_radiance_batch(scene, idx2, pos[collide] + s2[collide, None] * nd[collide],
+                                            nd[collide], n_light_samples)
+            tot[collide] += w[collide, None] * np.exp(-sig_t * s2[collide])[:, None] * lo2
+            alive = collide
+            cur_d = nd
+            cur_s = s2
+        return tot.reshape(m, n, 3).mean(axis=1)
+
+    return gather
+
+
+def gen_media_bounces():
+    """Records with the ≤ B-bounce media-radiance extension (BASELINE cfg3 asks for up to 4;
+    the reference has one extra bounce): the reference's build_subdivision + assemble_moments
+    with mean_surface_gather replaced by _gather_bounces_shim (reference primitives only)."""
+    room = configs.cfg3_scene(n_spheres=4, level=1)
+    rs = ref_scene(room)
+    pts = np.random.default_rng(21).uniform(room.bounds_min + 0.3, room.bounds_max - 0.3, (3, 3))
+    n, step, B = 1024, 0.2, 4
+    box = {}
+    orig = vs.mean_surface_gather
+    vs.mean_surface_gather = _gather_bounces_shim(box, B)
+    res = {k: [] for k in ("L", "grad", "hess", "stats", "adj")}
+    try:
+        for i, x in enumerate(pts):
+            box.update(seed=vr._seed(3, 401, i), n_dirs=n)
+            with Capture() as cap:
+                sub = vs.build_subdivision(rs, x, n_angular=n, march_step=step, rng_seed=vr._seed(3, 401, i))
+            single, multiple, stats = vs.assemble_moments(sub, rs.medium)
+            res["L"].append([single.L, multiple.L])
+            res["grad"].append([single.grad, multiple.grad])
+            res["hess"].append([single.hess, multiple.hess])
+            res["stats"].append([stats["elements_evaluated"], stats["elements_dropped"], stats["star_vertices"]])
+            res["adj"].append(np.asarray(cap.dirs.adjacency, np.int32))
+    finally:
+        vs.mean_surface_gather = orig
+    out = {k: np.array(v) for k, v in res.items()}
+    out.update(scene_fields("", rs))
+    out.update(versions=VERSIONS, points=pts, cfg_seed=np.array(3), params=np.array([n, step, 1, 16, float(B)]))
+    np.savez_compressed(OUT / "rec_media_bounces.npz", **out)
+    print("wrote media_bounces", flush=True)
+
+
 CFG3_FULL_POINTS = (0, 6333, 12666, 18999)  # spread over the 19k cfg3 cache points
 
 
@@ -810,6 +887,8 @@ if __name__ == "__main__":
         gen_baseline_rng()
     if "cfg3_full" in which:
         gen_cfg3_full()
+    if "media_bounces" in which:
+        gen_media_bounces()
     if "cfg5_crop" in which:
         gen_cfg5_crop()
     if "path" in which:

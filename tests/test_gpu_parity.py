@@ -144,6 +144,40 @@ def test_cfg3_full_bench_workload_vs_reference():
         _err(f"cfg3_full-default[{i}]", **dev)
 
 
+def test_media_bounces_extension_vs_reference_shim():
+    """Extension (BASELINE cfg3: multiple scattering up to 4 bounces; the reference gathers
+    one extra bounce): media samples continue their gather path through up to 3 further
+    media events (media_bounces = 4).  Device vs the reference's build_subdivision +
+    assemble_moments with a gather written from the reference's primitives
+    (tests/golden/rec_media_bounces.npz; the oracle is pinned to the same fixture), qhull
+    adjacency injected; the north_star gate on the moments, element counts exact, and the
+    Generator advanced by every draw the build consumed."""
+    from paper_1805_09258_b200 import estimate_moments, estimate_moments_batch
+
+    z = golden("rec_media_bounces")
+    sc = golden_scene(z)
+    n, step, n_inner, n_light, B = z["params"]
+    N = len(z["points"])
+    seed = int(z["cfg_seed"])
+    words = np.array([[seed, 401, i] for i in range(N)], np.uint32)
+    adj = z["adj"].astype(np.int32)
+    r = estimate_moments_batch(sc, z["points"], seeds=words, n_angular=int(n), march_step=float(step),
+                               n_inner=int(n_inner), n_light_samples=int(n_light), adjacency=adj,
+                               media_bounces=int(B))
+    for i in range(N):
+        _check_moments(f"media_bounces{int(B)}[{i}]", r.L[i], r.grad[i], r.hess[i], z["L"][i], z["grad"][i],
+                       z["hess"][i])
+        assert tuple(int(v) for v in r.stats[i, :3]) == tuple(int(v) for v in z["stats"][i])
+    g = np.random.default_rng(np.random.SeedSequence([seed, 401, 0]))
+    estimate_moments(sc, z["points"][0], n_angular=int(n), march_step=float(step), rng_seed=g, adjacency=adj[0],
+                     media_bounces=int(B))
+    from oracle import volcache_oracle as O
+
+    g2 = np.random.default_rng(np.random.SeedSequence([seed, 401, 0]))
+    O.build_record(O.pack(sc), z["points"][0], int(n), float(step), g2, adjacency=adj[0], media_bounces=int(B))
+    assert g.random() == g2.random()  # same number of draws consumed
+
+
 def _tri_set(t):
     return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
 

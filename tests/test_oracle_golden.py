@@ -65,6 +65,28 @@ def test_records_match_reference(case):
             assert rel_l2(q, qz) <= 1e-8
 
 
+def test_media_bounces_oracle_matches_reference_shim():
+    """The ≤ B-bounce media-radiance extension in the oracle (gather_mean_bounces) against
+    the reference's build_subdivision + assemble_moments run with a gather written from the
+    reference's own primitives (make_goldens.py gen_media_bounces, B = 4)."""
+    z = golden("rec_media_bounces")
+    ps = O.pack(golden_scene(z))
+    n, step, n_inner, n_light, B = z["params"]
+    for i, x in enumerate(z["points"]):
+        rb = O.build_record(ps, x, int(n), float(step), O.seed_seq(int(z["cfg_seed"]), 401, i), int(n_inner),
+                            int(n_light), adjacency=z["adj"][i], media_bounces=int(B))
+        st = rb.stats
+        assert [st["elements_evaluated"], st["elements_dropped"], st["star_vertices"]] == z["stats"][i].tolist()
+        for k in range(2):
+            assert rel_l2(rb.L[k], z["L"][i][k]) <= 1e-12
+            assert rel_l2(rb.grad[k], z["grad"][i][k]) <= 1e-11
+            assert rel_l2(rb.hess[k], z["hess"][i][k]) <= 1e-10
+    # the extension changes only the multiple-scattering moments
+    rb1 = O.build_record(ps, z["points"][0], int(n), float(step), O.seed_seq(int(z["cfg_seed"]), 401, 0),
+                         adjacency=z["adj"][0])
+    assert rel_l2(rb1.L[0], z["L"][0][0]) <= 1e-12 and rel_l2(rb1.L[1], z["L"][0][1]) > 1e-3
+
+
 def test_make_record_edge_cases():
     z = golden("make_record")
     for j in range(int(z["n_cases"])):
