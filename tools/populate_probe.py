@@ -28,9 +28,20 @@ def main():
     # warm (scene upload, BVH, emitter quadrature)
     populate_cache(sc, Camera(position=c["position"], look_at=c["look_at"], up=c["up"], fov_degrees=c["fov"],
                               width=4, height=3), st)
+    import numpy as np
+
+    from paper_1805_09258_b200 import _lib
+
+    L = _lib.lib()
+    L.vc_profile(1)
     t0 = time.perf_counter()
     cs, stats = populate_cache(sc, cam, st, window=window)
     dt = time.perf_counter() - t0
+    ms = np.zeros(12)
+    cnt = np.zeros(12, np.int64)
+    L.vc_profile_read(_lib.ptr(ms), _lib.ptr(cnt), 12)
+    L.vc_profile(0)
+    stats["kernel_ms"] = {k: round(float(m), 1) for k, m in zip(_lib.KERNEL_CLASSES, ms) if m > 0}
     stats["wall_s"] = dt
     stats["records_per_s"] = stats["builds"] / dt
     stats["config"] = dict(w=w, h=h, step=step, eps=eps, n=n, window=window)
