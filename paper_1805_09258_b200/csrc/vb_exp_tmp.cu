@@ -86,9 +86,8 @@ __global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, Buil
   if (gid >= (long long)W.B * n) return;
   int rec = (int)(gid / n);
   int k = tiled_direction((int)(gid - (long long)rec * n), P);
-  Pcg64 g0 = pcg_load(W.rng + 4 * rec);
   double d[3], o[3];
-  stratum_direction<D>(k, P, g0, jt, d);
+  for (int a = 0; a < D; ++a) d[a] = W.dirs[((size_t)rec * n + k) * D + a];
 #pragma unroll
   for (int a = 0; a < D; ++a) o[a] = W.x[rec * D + a];
   double s;

@@ -139,6 +139,8 @@ struct alignas(16) DirInfo {
 // Per-record scratch for one wave (device pointers).
 struct Wave {
   const int* outside;    // device bounds-check flag (nullptr: host-checked); set → no rings
+  int* surv_cnt;         // B: survivors of the gather filter per record; redo = surv_cnt + B
+  int* redo;             // B: 1 → the record's survivor evaluation found the queue full
   DirInfo* info;         // B × n
   double* partial;       // B × kAsmParts × 2 × 32 assembly partial sums (+ counters)
   int B;                 // records in this wave
