@@ -78,7 +78,10 @@ __device__ __forceinline__ int tiled_direction(int t, const BuildParams& P) {
 #define VC_RAY_STACK LocalStack stk
 #endif
 
-template <int D>
+// REFL = false (no surface reflects): L_o is the emission, so the direct-lighting code —
+// shadow rays through a second inlined BVH traversal — is not compiled into the kernel
+// (its register demand made the traversal spill: 308 → 16 bytes of spill stores).
+template <int D, bool REFL>
 __global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   VC_RAY_STACK;
   const int n = P.n_angular;
@@ -98,7 +101,17 @@ __global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, Buil
 #pragma unroll
   for (int a = 0; a < D; ++a) hit[a] = add(o[a], mul(s, d[a]));
   double L[3];
-  surface_radiance<D>(S, id, hit, d, L, &stk);
+  if constexpr (REFL) {
+    surface_radiance<D>(S, id, hit, d, L, &stk);
+  } else {  // surface_radiance of a non-reflective scene (src/transport.py:240-254)
+    L[0] = L[1] = L[2] = 0.0;
+    if (id >= 0) {
+      const double* E = S.emission + (size_t)id * 3;
+      L[0] = E[0];
+      L[1] = E[1];
+      L[2] = E[2];
+    }
+  }
   size_t base = (size_t)rec * n + k;
 #pragma unroll
   for (int a = 0; a < D; ++a) W.dirs[base * D + a] = d[a];
@@ -2637,7 +2650,8 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
                           int* own, int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
   const long long nt = (long long)W.B * P.n_angular;
   prof_begin(KC_PRIMARY, st);
-  k_primary<D><<<grid_for(nt, 256), 256, stack_smem(k_primary<D>, S.geo), st>>>(S, P, W, jt);
+  if (S.reflective) k_primary<D, true><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, true>, S.geo), st>>>(S, P, W, jt);
+  else k_primary<D, false><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, false>, S.geo), st>>>(S, P, W, jt);
   prof_end(st);
   prof_begin(KC_RINGS, st);
   k_rings<<<W.B, kRingBS, 0, st>>>(P, W);
@@ -2658,7 +2672,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         cudaMemsetAsync(W.surv_cnt, 0, sizeof(int) * 2 * (size_t)W.B, st);  // surv_cnt and redo
         k_gather_emit<D, 1><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
-        k_gather_eval<D><<<dim3(4, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_eval<D><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                       W.gather_q_cap);
         k_gather_emit<D, 2><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);

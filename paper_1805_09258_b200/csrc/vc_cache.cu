@@ -454,6 +454,8 @@ struct MarchOut {
 // mode 1: write miss points + seeds; mode 2: final accumulation of the pixels with misses;
 // mode 3: final accumulation after insertion (frozen=False): each point reads the caches
 // as they were when it was reached (records of tag ≤ its ordinal), src/renderer.py:361-368
+// REFL = false: the hit's L_o is its emission (no direct-lighting code in the kernel, as k_primary)
+template <bool REFL>
 __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
                                                double step, int seed, const uint64_t* jit_state, JumpTables jt,
                                                int n_light_dummy, MarchOut out, int mode) {
@@ -485,7 +487,15 @@ __global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache
     double tt = isfinite(ts) ? ts : 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) hp[a] = add(o[a], mul(tt, d[a]));
-    if (accum) surface_radiance<3>(S, id, hp, d, lo);
+    if (accum) {
+      if constexpr (REFL) {
+        surface_radiance<3>(S, id, hp, d, lo);
+      } else {
+        lo[0] = lo[1] = lo[2] = 0.0;
+        if (id >= 0)
+          for (int c = 0; c < 3; ++c) lo[c] = S.emission[(size_t)id * 3 + c];
+      }
+    }
     double t_in, t_out;
     bool valid;
     bounds_span(S, o, d, t_in, t_out, valid);
@@ -689,6 +699,8 @@ int vc_cache_interpolate(vc_cache* c, int m, const double* xq, double* J, int32_
   return VC_OK;
 }
 
+#define VC_MARCH(refl) ((refl) ? k_march<true> : k_march<false>)
+
 int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, const vc_render_params* rp,
               double* image, int64_t* stats, int flags, void* stream) {
   if (!sc || !cs || !cm || !camp || !rp || !image) return fail(VC_EINVAL, "null argument");
@@ -750,7 +762,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     mo.c_ord = rs.c_ord;
     mo.c_val = rs.c_val;
     mo.c_n = rs.c_n;
-    k_march<<<grid, 128, 0, st>>>(S, cs->dev(), cm->dev(), cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo,
+    VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, cs->dev(), cm->dev(), cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo,
                                   3);
     count_launches(1);
     e = cudaGetLastError();
@@ -767,7 +779,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
   }
   DevCache Cs = cs->dev(), Cm = cm->dev();
   prof_begin(KC_MARCH, st);
-  k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 0);
+  VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 0);
   prof_end(st);
   // miss offsets (device scan over npx + 1 counts, the last one zero) and the hit total
   long long* hsum = (long long*)alloc(50, 16);
@@ -795,7 +807,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     if (e != cudaSuccess) return cuda_fail(e, "miss workspace");
     mo.miss_x = mx;
     mo.miss_words = mw;
-    k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 1);
+    VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 1);
     vc_build_params bp{};
     bp.n_angular = rp->n_angular;
     bp.march_step = rp->march_step;
@@ -827,7 +839,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     k_misses_J<<<(int)((nmiss + 127) / 128), 128, 0, st>>>((int)nmiss, mmom, stride, mJ);
     mo.miss_J = mJ;
     prof_begin(KC_MARCH, st);
-    k_march<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 2);
+    VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 2);
     prof_end(st);
     launches += 3;
   }
