@@ -455,8 +455,11 @@ struct MarchOut {
 // mode 3: final accumulation after insertion (frozen=False): each point reads the caches
 // as they were when it was reached (records of tag ≤ its ordinal), src/renderer.py:361-368
 // REFL = false: the hit's L_o is its emission (no direct-lighting code in the kernel, as k_primary)
+#ifndef VC_MARCH_MINB
+#define VC_MARCH_MINB 5  // resident 128-thread CTAs per SM (≤ 102 registers)
+#endif
 template <bool REFL>
-__global__ void __launch_bounds__(128) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
+__global__ void __launch_bounds__(128, VC_MARCH_MINB) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
                                                double step, int seed, const uint64_t* jit_state, JumpTables jt,
                                                int n_light_dummy, MarchOut out, int mode) {
   const int npx = cam.rows * cam.cols;
