@@ -170,9 +170,11 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, in
     stack.push_back({left, t.begin, mid, t.depth + 1});
   }
   // Device layout: one 64-byte record per interior node holding its two children's boxes
-  // and references — (lo.xyz, ref), (hi.xyz, count) per child, ref = first primitive of a
-  // leaf (count > 0) or the child's interior-node index (count = 0).  A visit loads one
-  // cache line and tests both children; leaves need no node of their own.
+  // and references, the boxes interleaved by child so every float4 half is a (left, right)
+  // pair for the packed FFMA2 slab tests: (lo.x l r, lo.y l r), (lo.z l r, hi.x l r),
+  // (hi.y l r, hi.z l r), (ref l, count l, ref r, count r); ref = first primitive of a leaf
+  // with bit 31 set (the traversal walks it to the primitive flagged last-in-leaf), or the
+  // child's interior-node index.  A visit loads one cache line and tests both children.
   std::vector<int> inner(nodes.size(), -1);
   int n_inner = 0;
   for (size_t i = 0; i < nodes.size(); ++i)
@@ -182,26 +184,27 @@ void build_bvh(int dim, int K, const double* verts, double pad, HostBVH* out, in
   out->n_nodes = n_inner;
   out->nodes = (float4*)malloc(sizeof(float4) * 4 * (size_t)n_inner);
   out->order = (int*)malloc(sizeof(int) * (size_t)std::max(K, 1));
-  // child reference: interior-node index, or the leaf's first primitive with bit 31 set
-  // (the traversal walks a leaf up to the primitive whose id carries the last-in-leaf flag)
-  auto entry = [&](float4* dst, int c) {
-    const Node& n = nodes[c];
-    const int ref = n.count > 0 ? (int)((unsigned)n.first | 0x80000000u) : inner[c];
-    float fr, fc;
-    std::memcpy(&fr, &ref, 4);
-    std::memcpy(&fc, &n.count, 4);
-    dst[0] = make_float4(n.b.lo[0], n.b.lo[1], n.b.lo[2], fr);
-    dst[1] = make_float4(n.b.hi[0], n.b.hi[1], n.b.hi[2], fc);
+  auto bits = [](int v) {
+    float f;
+    std::memcpy(&f, &v, 4);
+    return f;
+  };
+  auto pair = [&](float4* dst, int cl, int cr) {
+    const Node& l = nodes[cl];
+    const Node& r = nodes[cr];
+    const int rl = l.count > 0 ? (int)((unsigned)l.first | 0x80000000u) : inner[cl];
+    const int rr = r.count > 0 ? (int)((unsigned)r.first | 0x80000000u) : inner[cr];
+    dst[0] = make_float4(l.b.lo[0], r.b.lo[0], l.b.lo[1], r.b.lo[1]);
+    dst[1] = make_float4(l.b.lo[2], r.b.lo[2], l.b.hi[0], r.b.hi[0]);
+    dst[2] = make_float4(l.b.hi[1], r.b.hi[1], l.b.hi[2], r.b.hi[2]);
+    dst[3] = make_float4(bits(rl), bits(l.count), bits(rr), bits(r.count));
   };
   if (root_leaf) {  // both children the same leaf (tested twice: same result)
-    entry(out->nodes, 0);
-    entry(out->nodes + 2, 0);
+    pair(out->nodes, 0, 0);
   } else {
     for (size_t i = 0; i < nodes.size(); ++i) {
       if (inner[i] < 0) continue;
-      float4* dst = out->nodes + 4 * (size_t)inner[i];
-      entry(dst, nodes[i].first);
-      entry(dst + 2, nodes[i].first + 1);
+      pair(out->nodes + 4 * (size_t)inner[i], nodes[i].first, nodes[i].first + 1);
     }
   }
   std::memcpy(out->order, order.data(), sizeof(int) * K);

@@ -456,7 +456,7 @@ struct MarchOut {
 // as they were when it was reached (records of tag ≤ its ordinal), src/renderer.py:361-368
 // REFL = false: the hit's L_o is its emission (no direct-lighting code in the kernel, as k_primary)
 #ifndef VC_MARCH_MINB
-#define VC_MARCH_MINB 5  // resident 128-thread CTAs per SM (≤ 102 registers)
+#define VC_MARCH_MINB 8  // resident 128-thread CTAs per SM (≤ 64 registers): cfg5 frame 235 / 230 / 216 / 190 ms at 4 / 5 / 6 / 8
 #endif
 template <bool REFL>
 __global__ void __launch_bounds__(128, VC_MARCH_MINB) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,

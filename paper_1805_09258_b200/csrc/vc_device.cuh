@@ -191,26 +191,42 @@ __device__ __forceinline__ double hit_prim(const double* P, const double* o, con
   else return hit_seg(P, o, d, t_eps);
 }
 
-// Conservative float32 slab test against a padded node box: t = lo·inv − of·inv as one FMA
-// per plane (the rounding it adds is far inside the 1e-5·scale box padding; an exactly zero
-// direction component gives NaN slabs, which fminf/fmaxf drop — that axis then never culls).
+// Packed float32 FMA on (left, right) pairs (sm_100a FFMA2): one instruction per slab plane
+// for both children of a node.  Same rounding as two fmaf.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+// Conservative float32 slab tests of both children of a node (layout: vc_bvh.cpp):
+// t = lo·inv − of·inv as one packed FMA per plane (the rounding it adds is far inside the
+// 1e-5·scale box padding; an exactly zero direction component gives NaN slabs, which
+// fminf/fmaxf drop — that axis then never culls).
 template <int D>
-__device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, const float* inv, const float* noi,
-                                        float t_best, float& t_near) {
-  float t0 = fmaf(lo.x, inv[0], noi[0]), t1 = fmaf(hi.x, inv[0], noi[0]);
-  float tn = fminf(t0, t1), tf = fmaxf(t0, t1);
-  t0 = fmaf(lo.y, inv[1], noi[1]);
-  t1 = fmaf(hi.y, inv[1], noi[1]);
-  tn = fmaxf(tn, fminf(t0, t1));
-  tf = fminf(tf, fmaxf(t0, t1));
+__device__ __forceinline__ void box_hit2(const float4& A, const float4& B, const float4& C, const float2* inv2,
+                                         const float2* noi2, float t_best, bool& hl, bool& hr, float& tl, float& tr) {
+  const float2 lx = ffma2(make_float2(A.x, A.y), inv2[0], noi2[0]);
+  const float2 ly = ffma2(make_float2(A.z, A.w), inv2[1], noi2[1]);
+  const float2 hx = ffma2(make_float2(B.z, B.w), inv2[0], noi2[0]);
+  const float2 hy = ffma2(make_float2(C.x, C.y), inv2[1], noi2[1]);
+  float nl = fmaxf(fminf(lx.x, hx.x), fminf(ly.x, hy.x)), fl = fminf(fmaxf(lx.x, hx.x), fmaxf(ly.x, hy.x));
+  float nr = fmaxf(fminf(lx.y, hx.y), fminf(ly.y, hy.y)), fr = fminf(fmaxf(lx.y, hx.y), fmaxf(ly.y, hy.y));
   if constexpr (D == 3) {
-    t0 = fmaf(lo.z, inv[2], noi[2]);
-    t1 = fmaf(hi.z, inv[2], noi[2]);
-    tn = fmaxf(tn, fminf(t0, t1));
-    tf = fminf(tf, fmaxf(t0, t1));
+    const float2 lz = ffma2(make_float2(B.x, B.y), inv2[2], noi2[2]);
+    const float2 hz = ffma2(make_float2(C.z, C.w), inv2[2], noi2[2]);
+    nl = fmaxf(nl, fminf(lz.x, hz.x));
+    fl = fminf(fl, fmaxf(lz.x, hz.x));
+    nr = fmaxf(nr, fminf(lz.y, hz.y));
+    fr = fminf(fr, fmaxf(lz.y, hz.y));
   }
-  t_near = tn;
-  return tn <= tf && tf >= 0.0f && tn <= t_best;
+  tl = nl;
+  tr = nr;
+  hl = nl <= fl && fl >= 0.0f && nl <= t_best;
+  hr = nr <= fr && fr >= 0.0f && nr <= t_best;
 }
 
 // Certified float32 Möller–Trumbore pre-test: true only when the float64 test of
@@ -284,16 +300,22 @@ struct SharedStack {
 template <int D, int MODE, class Stack>
 __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const double* o, const double* d,
                           double& t_best, int& id_best, Stack& stk) {
-  float orl[3] = {0.f, 0.f, 0.f}, inv[3] = {0.f, 0.f, 0.f}, noi[3] = {0.f, 0.f, 0.f}, df[3] = {0.f, 0.f, 0.f};
+  float orl[3] = {0.f, 0.f, 0.f}, df[3] = {0.f, 0.f, 0.f};
+  float2 inv2[3], noi2[3];  // (inv, inv) and (−of·inv, −of·inv) per axis, for the packed slabs
   float Ob = 0.0f;
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    orl[a] = (float)(o[a] - H.ctr[a]);
-    df[a] = (float)d[a];
-    // approximate reciprocal (≤ 1 ulp; ±0 → ±inf): inside the box padding
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv[a]) : "f"(df[a]));
-    noi[a] = -orl[a] * inv[a];
-    Ob = fmaxf(Ob, fabsf(orl[a]));
+  for (int a = 0; a < 3; ++a) {
+    float inv = 0.0f, noi = 0.0f;
+    if (a < D) {
+      orl[a] = (float)(o[a] - H.ctr[a]);
+      df[a] = (float)d[a];
+      // approximate reciprocal (≤ 1 ulp; ±0 → ±inf): inside the box padding
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(df[a]));
+      noi = -orl[a] * inv;
+      Ob = fmaxf(Ob, fabsf(orl[a]));
+    }
+    inv2[a] = make_float2(inv, inv);
+    noi2[a] = make_float2(noi, noi);
   }
   Ob *= 1.0000005f;
   const float teps = (float)t_eps;
@@ -305,16 +327,16 @@ __device__ bool bvh_query(const DevBvh& H, double t_eps, float slack, const doub
   while (true) {
     while (!(cur & 0x80000000u)) {
       const float4* N = H.nodes + 4 * (size_t)cur;
-      const float4 l0 = __ldg(N), l1 = __ldg(N + 1), r0 = __ldg(N + 2), r1 = __ldg(N + 3);
+      const float4 A = __ldg(N), B = __ldg(N + 1), C = __ldg(N + 2), R = __ldg(N + 3);
       float tl, tr;
-      const bool hl = box_hit<D>(l0, l1, inv, noi, tbf, tl);
-      const bool hr = box_hit<D>(r0, r1, inv, noi, tbf, tr);
+      bool hl, hr;
+      box_hit2<D>(A, B, C, inv2, noi2, tbf, hl, hr, tl, tr);
       if (hl && hr) {
         const bool lf = tl <= tr;
-        stk.put(sp++, make_uint2(__float_as_uint(lf ? r0.w : l0.w), __float_as_uint(lf ? tr : tl)));
-        cur = __float_as_uint(lf ? l0.w : r0.w);
+        stk.put(sp++, make_uint2(__float_as_uint(lf ? R.z : R.x), __float_as_uint(lf ? tr : tl)));
+        cur = __float_as_uint(lf ? R.x : R.z);
       } else if (hl || hr) {
-        cur = __float_as_uint(hl ? l0.w : r0.w);
+        cur = __float_as_uint(hl ? R.x : R.z);
       } else {
         bool got = false;
         while (sp > 0) {  // pop, skipping entries whose entry distance is beyond the best

@@ -33,7 +33,7 @@ constexpr int kAsmParts = kAsmSplit * (kAsmBS / 32);  // per-warp partial sums p
 struct DevBvh {
   int K;                 // primitives
   int n_nodes;           // nodes (0 → brute force over K in original order)
-  const float4* nodes;   // 2 float4 per child: (lo.xyz, ref), (hi.xyz, count); boxes relative to ctr
+  const float4* nodes;   // 4 float4 per interior node, children interleaved (vc_bvh.cpp); boxes relative to ctr
   const double* prim;    // leaf order, prim_stride(dim) doubles each
   const int* prim_id;    // leaf order → original surface index
   // leaf order, 3 float4 per primitive (relative to ctr): (v0, |v0|∞), (e1, E), (e2, id | last);
