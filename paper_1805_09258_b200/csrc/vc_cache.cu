@@ -83,7 +83,7 @@ __global__ void k_idx_count(IdxGeom G, const double* rec, int n, int* cnt, int* 
 // index (z·2^k + y)·2^k + x — as short as the occupied levels allow, so the radix sort runs
 // over key_shift + 5 bits.
 __global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, int key_shift,
-                           unsigned long long* keys, int* vals) {
+                           unsigned long long* keys, int* vals, int r0) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int lv, clo[3], chi[3];
@@ -94,7 +94,7 @@ __global__ void k_idx_emit(IdxGeom G, const double* rec, int n, const int* off, 
       for (int x = clo[0]; x <= chi[0]; ++x) {
         const unsigned long long cell = (((unsigned long long)z << lv | (unsigned long long)y) << lv) | x;
         keys[o] = (unsigned long long)lv << key_shift | cell;
-        vals[o] = r;
+        vals[o] = r0 + r;
         ++o;
       }
 }
@@ -180,9 +180,9 @@ __global__ void k_cache_gather(const double* src, size_t stride, const int* sel,
   if (threadIdx.x == 0) dtag[j] = tags ? tags[j] : -1;
 }
 
-__global__ void k_iota(int* v, int n) {
+__global__ void k_iota(int* v, int n, int first = 0) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = i;
+  if (i < n) v[i] = first + i;
 }
 
 __global__ void k_fill_tags(long long* tag, int n, long long v) {
@@ -245,11 +245,19 @@ int cache_init(vc_cache* c, int dim, const double* bmin, const double* bmax) {
   double half = 0.5 * mx + 0.25 * diag;
   for (int a = 0; a < dim; ++a) c->origin[a] = 0.5 * (bmin[a] + bmax[a]) - half;
   c->size = 2.0 * half;
-  c->hbits = 10;
-  c->hcap = 1u << c->hbits;
-  cudaError_t e = cudaMalloc(&c->d_hkey, c->hcap * 8);
-  if (e == cudaSuccess) e = cudaMemset(c->d_hkey, 0xff, c->hcap * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_hrange, c->hcap * sizeof(int2));
+  cudaError_t e = cudaSuccess;
+  for (CacheIndex& X : c->ix) {
+    X.hbits = 10;
+    X.hcap = 1u << X.hbits;
+    if (e == cudaSuccess) e = cudaMalloc(&X.hkey, X.hcap * 8);
+    if (e == cudaSuccess) e = cudaMemset(X.hkey, 0xff, X.hcap * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&X.hrange, X.hcap * sizeof(int2));
+    if (e == cudaSuccess) e = cudaMalloc(&X.items, 16);
+    if (e == cudaSuccess) e = cudaMalloc(&X.rows, 16 * kSide);
+    if (e == cudaSuccess) e = cudaMalloc(&X.overflow, 16);
+    X.items_cap = 1;
+    X.ovf_cap = 4;
+  }
   if (e != cudaSuccess) return cuda_fail(e, "cache index allocation");
   return VC_OK;
 }
@@ -274,10 +282,18 @@ int cache_reserve(vc_cache* c, size_t n_records, cudaStream_t st) {
   cudaFree(c->d_tag);
   c->d_rec = r;
   c->d_tag = t;
-  cudaFree(c->d_side);  // recomputed by every cache_rebuild
-  c->d_side = nullptr;
-  e = cudaMalloc(&c->d_side, cap * kSide * sizeof(float4));
-  if (e != cudaSuccess) return cuda_fail(e, "cache growth");
+  // rejection rows: an incremental rebuild recomputes only the appended records' rows
+  float4* sd = nullptr;
+  e = cudaMalloc(&sd, cap * kSide * sizeof(float4));
+  if (e == cudaSuccess && c->n && c->d_side)
+    e = cudaMemcpyAsync(sd, c->d_side, (size_t)c->n * kSide * sizeof(float4), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(sd);
+    return cuda_fail(e, "cache growth");
+  }
+  cudaFree(c->d_side);
+  c->d_side = sd;
   c->rec_cap = cap;
   return VC_OK;
 }
@@ -303,25 +319,21 @@ int cache_truncate(vc_cache* c, int n, cudaStream_t st) {
   return VC_OK;
 }
 
-int cache_rebuild(vc_cache* c, cudaStream_t st) {
-  const int n = c->n;
+// Index records [r0, r0 + nr) into X (scratch in c->ws; the index arrays grow only).
+static int index_build(vc_cache* c, CacheIndex& X, int r0, int nr, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   auto alloc = [&](int slot, size_t bytes) { return c->ws.get(slot, bytes, &e); };
-  if (n == 0) {
-    c->n_overflow = 0;
-    c->level_mask = 0;
-    e = cudaMemsetAsync(c->d_hkey, 0xff, c->hcap * 8, st);
-    if (e == cudaSuccess && !c->d_items) e = cudaMalloc(&c->d_items, 16);
-    if (e == cudaSuccess && !c->d_rows) e = cudaMalloc(&c->d_rows, 16 * kSide);
-    if (e == cudaSuccess && !c->d_overflow) e = cudaMalloc(&c->d_overflow, 16);
-    return e == cudaSuccess ? VC_OK : cuda_fail(e, "cache index reset");
-  }
+  X.clear();
+  if (nr == 0) return VC_OK;
+  const int RS = record_size(c->dim);
+  const double* rec = c->d_rec + (size_t)r0 * RS;
   IdxGeom G{};
   G.dim = c->dim;
   for (int a = 0; a < 3; ++a) G.origin[a] = c->origin[a];
   G.size = c->size;
   G.inv_size = 1.0 / c->size;
   G.span = c->cell_span;
+  const int n = nr;
   int* cnt = (int*)alloc(0, (size_t)n * 4);
   int* ovf = (int*)alloc(1, (size_t)n * 4);
   int* off = (int*)alloc(2, ((size_t)n + 1) * 4);
@@ -333,8 +345,8 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   unsigned* lmask = (unsigned*)(n_sel + 2);
   e = cudaMemsetAsync(lmask, 0, 4, st);
   const int nb = (n + 127) / 128;
-  k_idx_side<<<nb, 128, 0, st>>>(c->d_rec, n, c->dim, c->d_side);
-  k_idx_count<<<nb, 128, 0, st>>>(G, c->d_rec, n, cnt, ovf, lmask);
+  k_idx_side<<<nb, 128, 0, st>>>(rec, n, c->dim, c->d_side + (size_t)r0 * kSide);
+  k_idx_count<<<nb, 128, 0, st>>>(G, rec, n, cnt, ovf, lmask);
   // scan n+1 entries (the last one a zero slot) → per-record entry offsets and the total
   if (e == cudaSuccess) e = cudaMemcpyAsync(cnt1, cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(cnt1 + n, 0, 4, st);
@@ -345,7 +357,7 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   if (e != cudaSuccess) return cuda_fail(e, "cache index scan");
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt1, off, n + 1, st);
   // overflow list (record order) and its count
-  k_iota<<<nb, 128, 0, st>>>(iota, n);
+  k_iota<<<nb, 128, 0, st>>>(iota, n, r0);
   cub::DeviceSelect::Flagged(tmp, sb, iota, ovf, ovf_list, n_sel, n, st);
   int hv[3] = {0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(&hv[0], off + n, 4, cudaMemcpyDeviceToHost, st);
@@ -354,64 +366,86 @@ int cache_rebuild(vc_cache* c, cudaStream_t st) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "cache index sizes");
   const int T = hv[0];
-  c->n_overflow = hv[1];
-  c->level_mask = (unsigned)hv[2];
+  X.n_overflow = hv[1];
+  X.level_mask = (unsigned)hv[2];
   unsigned long long* keys = (unsigned long long*)alloc(8, (size_t)T * 8 + 8);
   int* vals = (int*)alloc(9, (size_t)T * 4 + 4);
   unsigned long long* keys2 = (unsigned long long*)alloc(10, (size_t)T * 8 + 8);
-  if (c->items_cap < (size_t)T + 1) {
-    cudaFree(c->d_items);
-    cudaFree(c->d_rows);
-    c->d_items = nullptr;
-    c->d_rows = nullptr;
-    size_t cap = std::max<size_t>((size_t)T + 1, c->items_cap * 2);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_items, cap * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_rows, cap * kSide * sizeof(float4));
-    c->items_cap = e == cudaSuccess ? cap : 0;
+  if (X.items_cap < (size_t)T + 1) {
+    cudaFree(X.items);
+    cudaFree(X.rows);
+    X.items = nullptr;
+    X.rows = nullptr;
+    size_t cap = std::max<size_t>((size_t)T + 1, X.items_cap * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&X.items, cap * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&X.rows, cap * kSide * sizeof(float4));
+    X.items_cap = e == cudaSuccess ? cap : 0;
   }
   // hash table: ≥ 2 slots per entry (≥ 2 per occupied cell), power of two
   int hbits = 10;
   while (hbits < 30 && (1ULL << hbits) < 2ULL * (unsigned long long)T) ++hbits;
-  if ((1ULL << hbits) > c->hcap) {
-    cudaFree(c->d_hkey);
-    cudaFree(c->d_hrange);
-    c->d_hkey = nullptr;
-    c->d_hrange = nullptr;
-    c->hcap = 1ULL << hbits;
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_hkey, c->hcap * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_hrange, c->hcap * sizeof(int2));
+  if ((1ULL << hbits) > X.hcap) {
+    cudaFree(X.hkey);
+    cudaFree(X.hrange);
+    X.hkey = nullptr;
+    X.hrange = nullptr;
+    X.hcap = 1ULL << hbits;
+    if (e == cudaSuccess) e = cudaMalloc(&X.hkey, X.hcap * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&X.hrange, X.hcap * sizeof(int2));
   }
-  c->hbits = hbits;
-  if (!c->d_overflow || c->ovf_cap < (size_t)c->n_overflow + 1) {  // grows only (no per-rebuild free)
-    cudaFree(c->d_overflow);
-    c->d_overflow = nullptr;
-    c->ovf_cap = std::max<size_t>((size_t)c->n_overflow + 1, 2 * c->ovf_cap);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_overflow, c->ovf_cap * 4);
+  X.hbits = hbits;
+  if (X.ovf_cap < (size_t)X.n_overflow + 1) {  // grows only (no per-rebuild free)
+    cudaFree(X.overflow);
+    X.overflow = nullptr;
+    X.ovf_cap = std::max<size_t>((size_t)X.n_overflow + 1, 2 * X.ovf_cap);
+    if (e == cudaSuccess) e = cudaMalloc(&X.overflow, X.ovf_cap * 4);
   }
-  if (e == cudaSuccess && c->n_overflow)
-    e = cudaMemcpyAsync(c->d_overflow, ovf_list, (size_t)c->n_overflow * 4, cudaMemcpyDeviceToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_hkey, 0xff, (1ULL << hbits) * 8, st);
+  if (e == cudaSuccess && X.n_overflow)
+    e = cudaMemcpyAsync(X.overflow, ovf_list, (size_t)X.n_overflow * 4, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(X.hkey, 0xff, (1ULL << hbits) * 8, st);
   if (e != cudaSuccess) return cuda_fail(e, "cache index buffers");
   int kmax = 0;
   for (int k = 0; k <= kMaxLevel; ++k)
-    if ((c->level_mask >> k) & 1u) kmax = k;
-  c->key_shift = c->dim * kmax;
-  const int end_bit = c->key_shift + 5;
-  k_idx_emit<<<nb, 128, 0, st>>>(G, c->d_rec, n, off, c->key_shift, keys, vals);
+    if ((X.level_mask >> k) & 1u) kmax = k;
+  X.key_shift = c->dim * kmax;
+  const int end_bit = X.key_shift + 5;
+  k_idx_emit<<<nb, 128, 0, st>>>(G, rec, n, off, X.key_shift, keys, vals, r0);
   // stable sort by cell keeps records in insertion order within a cell
   size_t rb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, rb, keys, keys2, vals, X.items, T, 0, end_bit, st);
   void* rtmp = alloc(11, rb);
   if (e != cudaSuccess) return cuda_fail(e, "cache index sort scratch");
   if (T > 0) {
-    cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, c->d_items, T, 0, end_bit, st);
-    k_idx_hash<<<(T + 127) / 128, 128, 0, st>>>(keys2, T, hbits, c->d_hkey, c->d_hrange);
-    k_idx_rows<<<(int)(((long long)T * kSide + 255) / 256), 256, 0, st>>>(c->d_items, T, c->d_side, c->d_rows);
+    cub::DeviceRadixSort::SortPairs(rtmp, rb, keys, keys2, vals, X.items, T, 0, end_bit, st);
+    k_idx_hash<<<(T + 127) / 128, 128, 0, st>>>(keys2, T, hbits, X.hkey, X.hrange);
+    k_idx_rows<<<(int)(((long long)T * kSide + 255) / 256), 256, 0, st>>>(X.items, T, c->d_side, X.rows);
   }
   count_launches(9);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "cache index build");
   return VC_OK;
+}
+
+// Index after an append / truncation: the records since the last full index go to ix[1]
+// alone while they number ≤ max(4096, n_main / 4); otherwise (or after a truncation below
+// n_main) everything is re-indexed into ix[0].  Either way a query sees every record, in
+// the order of one index over all of them (vc_cache.cuh, DevCache).
+int cache_rebuild(vc_cache* c, cudaStream_t st) {
+  const int n = c->n;
+  const int delta = n - c->n_main;
+  if (delta >= 0 && delta <= std::max(4096, c->n_main / 4) && c->n_main > 0) {
+    return index_build(c, c->ix[1], c->n_main, delta, st);
+  }
+  c->n_main = n;
+  c->ix[1].clear();
+  return index_build(c, c->ix[0], 0, n, st);
+}
+
+// Both parts re-indexed as one (after a populate run: lookups then scan a single index).
+int cache_rebuild_full(vc_cache* c, cudaStream_t st) {
+  c->n_main = c->n;
+  c->ix[1].clear();
+  return index_build(c, c->ix[0], 0, c->n, st);
 }
 
 template <int D>

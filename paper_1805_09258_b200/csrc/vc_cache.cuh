@@ -38,19 +38,28 @@ constexpr int kMaxLevel = 16;  // finest grid: 2^16 cells per axis
 // {M22 0 0 0}; 2D: {p.xy, tol, M00}, {M01 M10 M11 0}.
 constexpr int kSide = 4;
 
-struct DevCache {
-  int dim, n, n_overflow;
-  int blend;                   // 0: ellipsoid records, linear blend; 1: sphere records, log-space blend
-  double origin[3];
-  double size, inv_size;       // root cube
+// One spatial-hash index over a contiguous range of a cache's records.
+struct DevIndex {
   unsigned level_mask;         // bit k: level k lists at least one record
   int hbits;                   // hash table: 2^hbits slots
   int key_shift;               // d · (deepest occupied level): cell keys are k << key_shift | cell
+  int n_overflow;
   const unsigned long long* hkey;  // cell key per slot (~0: empty); cell = (z·2^k + y)·2^k + x
   const int2* hrange;          // the cell's entries [start, end)
   const int* items;            // record of each entry (cell order; insertion order within a cell)
   const float4* rows;          // kSide rejection rows per entry (copies of side[items[t]])
-  const int* overflow;
+  const int* overflow;         // records whose box leaves the root cube (record order)
+};
+
+// ix[0] indexes records [0, n_main), ix[1] the records appended since (the populate engine
+// re-indexes only those after each window); a query visits, per level, ix[0]'s cell then
+// ix[1]'s, then both overflow lists — record for record the order of one index over all.
+struct DevCache {
+  int dim, n;
+  int blend;                   // 0: ellipsoid records, linear blend; 1: sphere records, log-space blend
+  double origin[3];
+  double size, inv_size;       // root cube
+  DevIndex ix[2];
   const double* rec;           // n × record_size(dim), reference layout
   const long long* tag;        // n creation ordinals
   const float4* side;          // n × kSide float32 rejection rows (record_side)
@@ -62,59 +71,70 @@ __host__ __device__ __forceinline__ unsigned hash_slot(unsigned long long key, i
 
 }  // namespace vc
 
+// Host side of one DevIndex (device arrays grow only).
+struct CacheIndex {
+  unsigned long long* hkey = nullptr;
+  int2* hrange = nullptr;
+  int hbits = 10, key_shift = 0;
+  size_t hcap = 0;
+  int* items = nullptr;
+  float4* rows = nullptr;
+  size_t items_cap = 0;
+  int* overflow = nullptr;
+  int n_overflow = 0;
+  size_t ovf_cap = 0;
+  unsigned level_mask = 0;
+  vc::DevIndex dev() const {
+    return vc::DevIndex{level_mask, hbits, key_shift, n_overflow, hkey, hrange, items, rows, overflow};
+  }
+  void clear() {
+    level_mask = 0;
+    n_overflow = 0;
+  }
+  ~CacheIndex() {
+    cudaFree(hkey);
+    cudaFree(hrange);
+    cudaFree(items);
+    cudaFree(rows);
+    cudaFree(overflow);
+  }
+};
+
 struct vc_cache {
   int dim = 0, n = 0;
   int blend = 0;  // 1: baseline cache (BaselineRecord spheres, log_space_interpolate)
   double origin[3] = {0, 0, 0}, size = 0.0;
-  unsigned long long* d_hkey = nullptr;
-  int2* d_hrange = nullptr;
-  int hbits = 0, key_shift = 0;
-  size_t hcap = 0, ovf_cap = 0;
-  // Level choice: a record's cells are ≥ cell_span × its largest AABB half-extent... span 1
+  // Level choice: a record's cells are ≥ cell_span × its largest AABB half-extent; span 1
   // (≤ 3 cells per axis, ~3× fewer candidates per lookup) for lookups and marches; the
   // populate engine, which rebuilds after every window, runs with 2 (≤ 2 per axis, fewer
   // entries to sort) and rebuilds at 1 when it finishes.  cfg5: march 377 → 224 ms per
   // frame at span 1; populate 31.7 s at span 2 vs 42.8 s at 1.
   double cell_span = 1.0;
-  int* d_items = nullptr;
-  float4* d_rows = nullptr;
-  size_t items_cap = 0;
-  int* d_overflow = nullptr;
-  int n_overflow = 0;
+  // ix[0] covers records [0, n_main); appends up to max(4096, n_main / 4) records are indexed
+  // in ix[1] alone, then everything is re-indexed into ix[0] (cache_rebuild)
+  CacheIndex ix[2];
+  int n_main = 0;
   double* d_rec = nullptr;
   long long* d_tag = nullptr;
   float4* d_side = nullptr;  // kSide float4 per record (rejection rows)
-  unsigned level_mask = 0;
   size_t rec_cap = 0;  // records
   vc::Workspace ws;    // index-build scratch
   vc::DevCache dev() const {
     vc::DevCache c{};
     c.dim = dim;
     c.n = n;
-    c.n_overflow = n_overflow;
     c.blend = blend;
     for (int a = 0; a < 3; ++a) c.origin[a] = origin[a];
     c.size = size;
     c.inv_size = 1.0 / size;
-    c.level_mask = level_mask;
-    c.hbits = hbits;
-    c.key_shift = key_shift;
-    c.hkey = d_hkey;
-    c.hrange = d_hrange;
-    c.items = d_items;
-    c.rows = d_rows;
-    c.overflow = d_overflow;
+    c.ix[0] = ix[0].dev();
+    c.ix[1] = ix[1].dev();
     c.rec = d_rec;
     c.tag = d_tag;
     c.side = d_side;
     return c;
   }
   ~vc_cache() {
-    cudaFree(d_hkey);
-    cudaFree(d_hrange);
-    cudaFree(d_items);
-    cudaFree(d_rows);
-    cudaFree(d_overflow);
     cudaFree(d_rec);
     cudaFree(d_tag);
     cudaFree(d_side);
@@ -196,7 +216,8 @@ int cache_reserve(vc_cache* c, size_t n_records, cudaStream_t st);
 int cache_append(vc_cache* c, const double* src, size_t stride, const int* d_sel, const long long* d_tags,
                  int k, cudaStream_t st);
 int cache_truncate(vc_cache* c, int n, cudaStream_t st);
-int cache_rebuild(vc_cache* c, cudaStream_t st);
+int cache_rebuild(vc_cache* c, cudaStream_t st);       // incremental (appended records in ix[1])
+int cache_rebuild_full(vc_cache* c, cudaStream_t st);  // every record in ix[0]
 
 // support coordinate 1 − ‖(Δ·A)/r‖ (src/cache.py:112-116)
 template <int D>
@@ -285,6 +306,23 @@ __device__ __forceinline__ bool row_rejects(const float4* sd, const float* x32) 
 // Visit the records of x that survive the float32 rejection, in index order (coarse level
 // first, then the overflow list); f(record_index) returns true to stop early.
 template <int D, typename F>
+__device__ __forceinline__ bool index_cell(const DevIndex& X, int k, unsigned long long cell, const float* x32, F& f) {
+  if (!((X.level_mask >> k) & 1u)) return false;
+  const unsigned long long key = (unsigned long long)k << X.key_shift | cell;
+  const unsigned hm = (1u << X.hbits) - 1u;
+  for (unsigned h = hash_slot(key, X.hbits);; h = (h + 1) & hm) {
+    const unsigned long long kk = X.hkey[h];
+    if (kk == key) {
+      const int2 r = X.hrange[h];
+      for (int t = r.x; t < r.y; ++t)
+        if (!row_rejects<D>(X.rows + (size_t)t * kSide, x32) && f(X.items[t])) return true;
+      return false;
+    }
+    if (kk == ~0ULL) return false;
+  }
+}
+
+template <int D, typename F>
 __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, F&& f) {
   float x32[D];
   double u[D];
@@ -296,30 +334,21 @@ __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, 
     in = in && u[a] >= 0.0 && u[a] < 1.0;
   }
   if (in) {
-    for (unsigned m = C.level_mask; m; m &= m - 1) {
+    for (unsigned m = C.ix[0].level_mask | C.ix[1].level_mask; m; m &= m - 1) {
       const int k = __ffs(m) - 1;
       const double s = (double)(1u << k);
       unsigned long long cell = 0;
 #pragma unroll
       for (int a = D - 1; a >= 0; --a) cell = (cell << k) | (unsigned long long)min((int)floor(u[a] * s), (1 << k) - 1);
-      const unsigned long long key = (unsigned long long)k << C.key_shift | cell;
-      const unsigned hm = (1u << C.hbits) - 1u;
-      for (unsigned h = hash_slot(key, C.hbits);; h = (h + 1) & hm) {
-        const unsigned long long kk = C.hkey[h];
-        if (kk == key) {
-          const int2 r = C.hrange[h];
-          for (int t = r.x; t < r.y; ++t)
-            if (!row_rejects<D>(C.rows + (size_t)t * kSide, x32) && f(C.items[t])) return;
-          break;
-        }
-        if (kk == ~0ULL) break;
-      }
+      if (index_cell<D>(C.ix[0], k, cell, x32, f)) return;
+      if (index_cell<D>(C.ix[1], k, cell, x32, f)) return;
     }
   }
-  for (int t = 0; t < C.n_overflow; ++t) {
-    const int r = C.overflow[t];
-    if (!row_rejects<D>(C.side + (size_t)r * kSide, x32) && f(r)) return;
-  }
+  for (int p = 0; p < 2; ++p)
+    for (int t = 0; t < C.ix[p].n_overflow; ++t) {
+      const int r = C.ix[p].overflow[t];
+      if (!row_rejects<D>(C.side + (size_t)r * kSide, x32) && f(r)) return;
+    }
 }
 
 // log-space blend term of one sphere record (src/cache.py:363-394)

@@ -794,8 +794,8 @@ int vc::populate_run(vc_scene* sc, const vc_populate_params* pp, int seed_kind, 
   int rc = populate_run_impl(sc, pp, seed_kind, cs, cm, stats, st, commit_J, spp, rs);
   cs->cell_span = span_s;
   cm->cell_span = span_m;
-  if (!rc) rc = cache_rebuild(cs, st);
-  if (!rc) rc = cache_rebuild(cm, st);
+  if (!rc) rc = cache_rebuild_full(cs, st);
+  if (!rc) rc = cache_rebuild_full(cm, st);
   return rc;
 }
 
