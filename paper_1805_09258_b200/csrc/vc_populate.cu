@@ -367,7 +367,7 @@ struct Engine {
   int C = 2048;
   long long L = 65536, Lmax = 1LL << 24;
   double kappa = 1.0, h_sel = INFINITY;
-  double waste_ratio = 1.0;  // VOLCACHE_POP_WASTE: target discarded / committed builds per window
+  double waste_ratio = 0.3;  // VOLCACHE_POP_WASTE: target discarded / committed builds per window
   int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaError_t e = cudaSuccess;
 
