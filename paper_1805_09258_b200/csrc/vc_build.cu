@@ -493,12 +493,47 @@ struct alignas(16) FilterPlane {  // four 16-byte shared-memory loads per plane
   float4 cc;   // 1 / block size (x, y), blocks (x, y) as int bits
 };
 
+// Direction inputs of the filter: u0f = (float)u0, om = (float)(1 − u0), z = (float)(1 − 2u0)
+// (each the correctly rounded float of the exact float64 value) and (cos, sin)(2π·u1) to
+// within 1e-6.
+struct FilterDir {
+  float u0f, om, z, cp, sp;
+};
+
+// From the float64 draws (the fused pass): sincospif of 2·(float)u1.
+__device__ __forceinline__ FilterDir filter_dir(double u0, double u1) {
+  FilterDir f;
+  f.u0f = (float)u0;
+  f.om = (float)(1.0 - u0);
+  f.z = (float)(1.0 - 2.0 * u0);
+  sincospif(2.0f * (float)u1, &f.sp, &f.cp);
+  return f;
+}
+
+// From the raw 53-bit draw mantissas m (u = m·2⁻⁵³, numpy's double): the same u0f / om / z
+// by integer → float conversions of the exact values (bit-identical to filter_dir), and
+// MUFU sine / cosine of φ = 2π(u1 − ½) ∈ [−π, π) with (cos, sin)(φ + π) = −(cos, sin)φ:
+// argument error ≤ 2π·2⁻²⁴ (u1 rounded to float, u1 − ½ exact or within 2⁻²⁵), MUFU error
+// ≤ 2⁻²¹·⁴¹ on [−π, π] — ≤ 1e-6 in all, inside the filter's ed = 2e-6.
+__device__ __forceinline__ FilterDir filter_dir_raw(unsigned long long m0, unsigned long long m1) {
+  constexpr float k53 = 1.1102230246251565e-16f;  // 2⁻⁵³
+  FilterDir f;
+  f.u0f = __ull2float_rn(m0) * k53;
+  f.om = __ull2float_rn((1ULL << 53) - m0) * k53;
+  f.z = __ll2float_rn((long long)(1ULL << 53) - 2LL * (long long)m0) * k53;
+  const float phi = 6.283185307179586f * (__ull2float_rn(m1) * k53 - 0.5f);
+  float s, c;
+  __sincosf(phi, &s, &c);
+  f.sp = -s;
+  f.cp = -c;
+  return f;
+}
+
 __device__ __forceinline__ bool emitter_may_hit(const FilterPlane* fp, const unsigned* occ, int ng,
-                                                const float* y, double u0, double u1, float ey, float mpad) {
-  const float om = (float)(1.0 - u0), z = (float)(1.0 - 2.0 * u0);
-  const float sq = sqrtf(4.0f * (float)u0 * om);
-  float sp, cp;
-  sincospif(2.0f * (float)u1, &sp, &cp);
+                                                const float* y, const FilterDir& fd, float ey, float mpad) {
+  const float z = fd.z;
+  const float sq = sqrtf(4.0f * fd.u0f * fd.om);
+  const float sp = fd.sp, cp = fd.cp;
   const float d[3] = {sq * cp, sq * sp, z};
   constexpr float ed = 2e-6f;
   for (int g = 0; g < ng; ++g) {
@@ -719,15 +754,24 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
           i = 0;
           ck = cnt[k];
         }
-        u0 = g.next_double();
+        FilterDir fd{};
+        if (MODE == 1 && D == 3 && filt) {  // the survivors redraw their doubles (k_gather_eval)
+          const unsigned long long m0 = g.next64() >> 11, m1 = g.next64() >> 11;
+          fd = filter_dir_raw(m0, m1);
+        } else {
+          u0 = g.next_double();
+          if constexpr (D == 3) {
+            u1 = g.next_double();
+            if (filt) fd = filter_dir(u0, u1);
+          }
+        }
         if constexpr (D == 3) {
-          u1 = g.next_double();
           if (filt) {
             // the filter's float32 sample point (error ≤ f_ey against origin())
             const float4 dk = W.dirs32[(size_t)rec * n + k];
             const float ri = ((float)i + 0.5f) * f_step;
             const float y32[3] = {xr[0] + ri * dk.x, xr[1] + ri * dk.y, xr[2] + ri * dk.z};
-            keep = emitter_may_hit(fplane, focc, S.ep.ng, y32, u0, u1, f_ey, f_pad);
+            keep = emitter_may_hit(fplane, focc, S.ep.ng, y32, fd, f_ey, f_pad);
           } else {
             double y[3];
             origin(k, i, y);
