@@ -128,6 +128,13 @@ int vc_form_factors(int dim, int m, const double* x, const double* verts, int pr
 int vc_trace(vc_scene* scene, int m, const double* o, const double* d, double* t, int32_t* idx, int flags,
              void* stream);
 
+/* Outgoing surface radiance per hit: surface_radiance_batch(scene, idx, points, dirs,
+ * n_light_samples) (src/transport.py:240-254) — emission (two-sided) + albedo · direct
+ * lighting by the emitter quadrature with one shadow ray per sample; idx < 0 → 0.
+ * points, dirs: m × dim float64; idx: m int32; out: m × 3 float64. */
+int vc_surface_radiance(vc_scene* scene, int m, const double* points, const double* dirs, const int32_t* idx,
+                        int n_light_samples, double* out, int flags, void* stream);
+
 /* numpy SeedSequence(words) → PCG64 state (host), for n records of nw words each. */
 int vc_seed_states(int n, const uint32_t* words, int nw, uint64_t* states);
 

@@ -21,6 +21,7 @@ from .records import (
     make_record,
     make_records,
     seed_words,
+    surface_radiance_batch,
 )
 from .io import (CACHE_FORMAT, CACHE_VERSION, BaselineRecord, CacheFormatError, load_cache, load_cache_npz, read_pfm,
                  save_cache, save_cache_npz, write_pfm, write_ppm)
@@ -40,5 +41,5 @@ __all__ = [
     "DEFAULT_N_ANGULAR", "BatchResult", "CacheRecord", "DeviceScene", "Moments", "RadianceCache",
     "Medium", "Scene", "Surface", "cache_from_records", "device_scene", "estimate_moments",
     "estimate_moments_batch", "inspect_record", "interpolate", "load_scene", "make_record",
-    "make_records", "render_frozen", "save_scene", "seed_words",
+    "make_records", "render_frozen", "save_scene", "seed_words", "surface_radiance_batch",
 ]

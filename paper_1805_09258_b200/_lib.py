@@ -146,6 +146,7 @@ _SIGS = {
     "vc_make_records": (C.c_int, [C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, C.c_double, C.c_int,
                                   _vp, _vp]),
     "vc_trace": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]),
+    "vc_surface_radiance": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp]),
     "vc_seed_states": (C.c_int, [C.c_int, _vp, C.c_int, _vp]),
     "vc_cache_create": (C.c_int, [C.c_int, _vp, _vp, C.c_int, _vp, C.POINTER(_vp)]),
     "vc_cache_destroy": (None, [_vp]),

@@ -1088,6 +1088,48 @@ int vc_trace(vc_scene* sc, int m, const double* o, const double* d, double* t, i
   return VC_OK;
 }
 
+int vc_surface_radiance(vc_scene* sc, int m, const double* points, const double* dirs, const int32_t* idx,
+                        int n_light_samples, double* out, int flags, void* stream) {
+  if (!sc) return fail(VC_EINVAL, "null scene");
+  if (n_light_samples < 1) return fail(VC_EINVAL, "n_light_samples must be >= 1");
+  if (m <= 0) return VC_OK;
+  int rc = ensure_emitters(sc, n_light_samples);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool host = flags & VC_MEM_HOST;
+  const int D = sc->dim;
+  const double *dp = points, *dd = dirs;
+  const int* di = idx;
+  double* dout = out;
+  void* buf = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (host) {
+    e = cudaMalloc(&buf, (size_t)m * (2 * D * 8 + 24 + 8));
+    if (e != cudaSuccess) return cuda_fail(e, "surface radiance staging");
+    double* b = (double*)buf;
+    dp = b;
+    dd = b + (size_t)m * D;
+    dout = b + (size_t)2 * m * D;
+    di = (const int*)(b + (size_t)2 * m * D + 3 * (size_t)m);
+    e = cudaMemcpyAsync((void*)dp, points, (size_t)m * D * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((void*)dd, dirs, (size_t)m * D * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((void*)di, idx, (size_t)m * 4, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+      cudaFree(buf);
+      return cuda_fail(e, "surface radiance upload");
+    }
+  }
+  launch_surface_radiance(dev_scene(sc), m, dp, dd, di, dout, st);
+  g_launches += 1;
+  e = cudaGetLastError();
+  if (e == cudaSuccess && host) {
+    e = cudaMemcpyAsync(out, dout, (size_t)m * 24, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  cudaFree(buf);
+  return e == cudaSuccess ? VC_OK : cuda_fail(e, "surface radiance");
+}
+
 int vc_seed_states(int n, const uint32_t* words, int nw, uint64_t* states) {
   if (n < 0 || nw < 1 || nw > 16) return fail(VC_EINVAL, "seed words per record must be in [1, 16]");
   for (int i = 0; i < n; ++i) seedseq_pcg64(words + (size_t)i * nw, nw, states + (size_t)i * 4);

@@ -2670,6 +2670,30 @@ __global__ void k_trace(DevScene S, int m, const double* org, const double* dir,
   idx_out[i] = id;
 }
 
+// surface_radiance_batch (src/transport.py:240-254) per hit: emission + albedo · direct
+// lighting with shadow rays, float64 in the reference's order (surface_radiance).
+template <int D>
+__global__ void __launch_bounds__(128) k_surface_radiance(DevScene S, int m, const double* pts, const double* dirs,
+                                                          const int* idx, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double p[3] = {0.0, 0.0, 0.0}, d[3] = {0.0, 0.0, 0.0}, L[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    p[a] = pts[(size_t)i * D + a];
+    d[a] = dirs[(size_t)i * D + a];
+  }
+  surface_radiance<D>(S, idx[i], p, d, L);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[(size_t)i * 3 + c] = L[c];
+}
+
+void launch_surface_radiance(const DevScene& S, int m, const double* pts, const double* dirs, const int* idx,
+                             double* out, cudaStream_t st) {
+  if (S.dim == 2) k_surface_radiance<2><<<grid_for(m, 128), 128, 0, st>>>(S, m, pts, dirs, idx, out);
+  else k_surface_radiance<3><<<grid_for(m, 128), 128, 0, st>>>(S, m, pts, dirs, idx, out);
+}
+
 void launch_trace(const DevScene& S, int m, const double* o, const double* d, double* t, int* idx, int with_bounds,
                   cudaStream_t st) {
   if (S.dim == 2) k_trace<2><<<grid_for(m, 128), 128, 0, st>>>(S, m, o, d, t, idx, with_bounds);

@@ -22,6 +22,8 @@ void prof_end(cudaStream_t st);
 
 void launch_wave(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt, int* own,
                  int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc);
+void launch_surface_radiance(const DevScene& S, int m, const double* pts, const double* dirs, const int* idx,
+                             double* out, cudaStream_t st);
 void launch_trace(const DevScene& S, int m, const double* o, const double* d, double* t, int* idx, int with_bounds,
                   cudaStream_t st);
 void launch_make_records(const DevScene& S, const BuildParams& P, const Wave& W, cudaStream_t st);

@@ -362,6 +362,23 @@ def inspect_record(scene, x, rng_seed=None, n_angular=None, march_step=0.1, n_in
     }
 
 
+def surface_radiance_batch(scene, idx, points, dirs, n_light_samples=16):
+    """Outgoing radiance at surface hits — drop-in for src/transport.py:240-254: emission
+    (two-sided) + albedo · direct lighting (emitter quadrature, one shadow ray per sample);
+    idx < 0 → 0.  Returns (m, 3) float64."""
+    ds = device_scene(scene)
+    d = ds.dim
+    idx = np.ascontiguousarray(np.asarray(idx).reshape(-1), np.int32)
+    m = idx.size
+    pts = np.ascontiguousarray(np.asarray(points, float).reshape(m, d))
+    drs = np.ascontiguousarray(np.asarray(dirs, float).reshape(m, d))
+    out = np.zeros((m, 3))
+    if m:
+        _lib.check(_lib.lib().vc_surface_radiance(ds.handle, m, _lib.ptr(pts), _lib.ptr(drs), _lib.ptr(idx),
+                                                  int(n_light_samples), _lib.ptr(out), _lib.VC_MEM_HOST, None))
+    return out
+
+
 def make_records(X, moments, epsilon, scene_scale, max_emission, anisotropic=True):
     """Batch make_record: X (N, d), moments (N, 2, M) → packed records (N, 2, RS)."""
     X = np.ascontiguousarray(np.asarray(X, float))

@@ -23,7 +23,7 @@ def golden(name: str):
 
 
 REC_CASES = ["cfg1_surf", "cfg1_m01", "pen2d", "refl2d", "cfg2_surf", "cfg2_m01",
-             "cfg2_m01_canon", "box3d_refl", "room_small"]
+             "cfg2_m01_canon", "box3d_refl", "room_small", "room_refl"]
 
 
 def golden_scene(z, prefix=""):

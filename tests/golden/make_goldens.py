@@ -146,7 +146,7 @@ def canonical_rotation(adj):
     return np.stack([adj[np.arange(len(adj)), (k + j) % 3] for j in range(3)], axis=1)
 
 
-def gen_records():
+def gen_records(only=None):
     bundled = Path("/root/reference/pkg/scenes")
     pen = vscene.load_scene(bundled / "penumbra2d.json")
     box = vscene.load_scene(bundled / "box3d.json")
@@ -180,8 +180,13 @@ def gen_records():
         "cfg2_m01_canon": (c2.scene, c2.points[:3], 1, 4096, 0.1, 1, 16, True),
         "box3d_refl": (box_refl, np.array([[0.5, 0.5, 0.5], [0.2, 0.7, 0.3]]), 5, 256, 0.25, 2, 4, False),
         "room_small": (room, room_pts, 2, 1024, 0.2, 1, 16, False),
+        # reflective walls: surface and media-gather hits lit by shadow rays (a3)
+        "room_refl": (configs.cfg3_scene(n_spheres=4, level=1, wall_albedo=0.5), room_pts, 2, 1024, 0.2, 1, 4,
+                      False),
     }
     for name, (sc, pts, cseed, n, step, n_inner, n_light, canon) in cases.items():
+        if only and name not in only:
+            continue
         rs = sc if isinstance(sc, vscene.Scene) else ref_scene(sc)
         N, d = pts.shape
         res = {k: [] for k in ("L", "grad", "hess", "stats", "dirs", "adj", "s", "idx",
@@ -669,6 +674,39 @@ def gen_media_bounces():
     print("wrote media_bounces", flush=True)
 
 
+def gen_surface():
+    """Per-hit outgoing radiance surface_radiance_batch (src/transport.py:240-254) on
+    reflective rooms (walls albedo 0.5): the small room on 4096 random rays, the full cfg3
+    room (51,300 triangles; chunked trace) on 48 rays; the hits from the reference's trace."""
+    import volcache.transport as vt
+
+    out = {"versions": VERSIONS}
+    shim = _chunked_trace(vscene.trace, 16)
+    saved = {m: m.trace for m in (vscene, vr, vt)}
+    try:
+        for mod in saved:
+            mod.trace = shim
+        for name, sc, m, seed in (("small", configs.cfg3_scene(n_spheres=4, level=1, wall_albedo=0.5), 4096, 31),
+                                  ("full", configs.cfg3_scene(wall_albedo=0.5), 48, 32)):
+            rs = ref_scene(sc)
+            rng = np.random.default_rng(seed)
+            o = rng.uniform(rs.bounds_min, rs.bounds_max, (m, 3))
+            d = rng.normal(size=(m, 3))
+            d /= np.linalg.norm(d, axis=1, keepdims=True)
+            s_, idx = vscene.trace(rs, o, d)
+            hit = o + np.where(np.isfinite(s_), s_, 0.0)[:, None] * d
+            lo = vt.surface_radiance_batch(rs, idx, hit, d, 16)
+            out[f"{name}_points"] = hit
+            out[f"{name}_dirs"] = d
+            out[f"{name}_idx"] = idx
+            out[f"{name}_lo"] = lo
+            print("surface", name, int((idx >= 0).sum()), "hits", flush=True)
+    finally:
+        for mod, f in saved.items():
+            mod.trace = f
+    np.savez_compressed(OUT / "surface.npz", **out)
+
+
 CFG3_FULL_POINTS = (0, 6333, 12666, 18999)  # spread over the 19k cfg3 cache points
 
 
@@ -871,6 +909,9 @@ if __name__ == "__main__":
         gen_trace()
     if "records" in which:
         gen_records()
+    for w in which:
+        if w.startswith("records:"):  # e.g. records:room_refl
+            gen_records(only=w.split(":", 1)[1].split(","))
     if "make_record" in which:
         gen_make_record()
     if "interp" in which:
@@ -887,6 +928,8 @@ if __name__ == "__main__":
         gen_baseline_rng()
     if "cfg3_full" in which:
         gen_cfg3_full()
+    if "surface" in which:
+        gen_surface()
     if "media_bounces" in which:
         gen_media_bounces()
     if "cfg5_crop" in which:

@@ -178,6 +178,26 @@ def test_media_bounces_extension_vs_reference_shim():
     assert g.random() == g2.random()  # same number of draws consumed
 
 
+@pytest.mark.parametrize("name", ["small", "full"])
+def test_surface_radiance_vs_reference(name):
+    """Per-hit outgoing radiance (a3: emission + albedo · direct lighting with shadow rays)
+    on reflective rooms — the small room on 4096 rays and the full cfg3 room (51,300
+    triangles) on 48 — against the reference's surface_radiance_batch
+    (tests/golden/surface.npz)."""
+    from paper_1805_09258_b200 import configs
+    from paper_1805_09258_b200.records import surface_radiance_batch
+
+    z = golden("surface")
+    sc = (configs.cfg3_scene(n_spheres=4, level=1, wall_albedo=0.5) if name == "small"
+          else configs.cfg3_scene(wall_albedo=0.5))
+    lo = surface_radiance_batch(sc, z[f"{name}_idx"], z[f"{name}_points"], z[f"{name}_dirs"], 16)
+    want = z[f"{name}_lo"]
+    assert np.count_nonzero(want.sum(axis=1)) > 10
+    err = float(np.max(np.abs(lo - want) / np.maximum(np.abs(want), 1e-300)))
+    _err(f"surface_radiance_{name}", max_rel=err)
+    np.testing.assert_allclose(lo, want, rtol=1e-12, atol=1e-15)
+
+
 def _tri_set(t):
     return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
 

@@ -87,6 +87,17 @@ def test_media_bounces_oracle_matches_reference_shim():
     assert rel_l2(rb1.L[0], z["L"][0][0]) <= 1e-12 and rel_l2(rb1.L[1], z["L"][0][1]) > 1e-3
 
 
+def test_surface_radiance_matches_reference():
+    """The oracle's surface_radiance (direct lighting with shadow rays) on the reflective
+    small room against the reference's surface_radiance_batch (tests/golden/surface.npz)."""
+    from paper_1805_09258_b200 import configs
+
+    z = golden("surface")
+    ps = O.pack(configs.cfg3_scene(n_spheres=4, level=1, wall_albedo=0.5))
+    lo = O.surface_radiance(ps, z["small_idx"], z["small_points"], z["small_dirs"], 16)
+    np.testing.assert_allclose(lo, z["small_lo"], rtol=1e-12, atol=1e-15)
+
+
 def test_make_record_edge_cases():
     z = golden("make_record")
     for j in range(int(z["n_cases"])):
