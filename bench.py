@@ -121,11 +121,12 @@ def workload(args):
 
     if args.config == "cfg3":
         w = configs.cfg3()
-        if getattr(args, "media_bounces", 1) > 1:  # extension: BASELINE cfg3's multi-bounce media radiance
+        B, g = getattr(args, "media_bounces", 1), getattr(args, "hg_g", 0.0)
+        if B > 1 or g != 0.0:  # extension: BASELINE cfg3's HG media / multi-bounce media radiance
             import dataclasses
 
-            w = dataclasses.replace(w, name=f"{w.name}+{args.media_bounces}-bounce-media",
-                                    media_bounces=args.media_bounces)
+            tag = (f"+hg{g:g}" if g != 0.0 else "") + (f"+{B}-bounce-media" if B > 1 else "")
+            w = dataclasses.replace(w, name=f"{w.name}{tag}", media_bounces=B, hg_g=g)
         return w
     if args.config == "cfg2":
         return configs.cfg2(march_step=args.march_step or 4.0)
@@ -180,7 +181,7 @@ def cpu_sample(w, n_records: int, start: int = 0):
     t0 = time.perf_counter()
     for i in cpu_points(w, n_records, start):
         rb = O.build_record(ps, w.points[i], w.n_angular, w.march_step, O.seed_seq(w.seed, 401, i), w.n_inner,
-                            w.n_light_samples, media_bounces=w.media_bounces)
+                            w.n_light_samples, media_bounces=w.media_bounces, hg_g=w.hg_g)
         for k in range(2):
             O.make_record(w.points[i], rb.L[k], rb.grad[k], rb.hess[k], w.epsilon, ps.scale, ps.max_emission)
     dt = time.perf_counter() - t0
@@ -420,6 +421,8 @@ def main():
     ap.add_argument("--ref-records", type=int, default=4, help="--impl reference: oracle records per timed step")
     ap.add_argument("--media-bounces", type=int, default=1,
                     help="cfg3 extension: media events per gather path (1 = the reference's estimator)")
+    ap.add_argument("--hg-g", type=float, default=0.0,
+                    help="cfg3 extension: Henyey-Greenstein g of the media scattering events (0 = the reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e timed steps (default: --steps)")
     ap.add_argument("--cfg5-eps", type=float, default=None, help="cfg5: record-error target ε (default tuned)")
@@ -447,7 +450,8 @@ def main():
     B = args.records_per_step
     ds = device_scene(w.scene)
     kw = dict(n_angular=w.n_angular, march_step=w.march_step, n_inner=w.n_inner,
-              n_light_samples=w.n_light_samples, epsilon=w.epsilon, media_bounces=args.media_bounces)
+              n_light_samples=w.n_light_samples, epsilon=w.epsilon, media_bounces=args.media_bounces,
+              hg_g=args.hg_g)
     total_steps = args.warmup + args.steps
     # inputs resident in HBM before timing
     Xs, Ss = [], []
@@ -517,6 +521,7 @@ def main():
     prm.n_light_samples, prm.epsilon = w.n_light_samples, w.epsilon
     prm.flags = _lib.VC_MEM_HOST | _lib.VC_SEED_WORDS | _lib.VC_MAKE_RECORDS
     prm.media_bounces = args.media_bounces
+    prm.hg_g = args.hg_g
     prm.seed_words = 3
     barrier()
     torch.cuda.synchronize()

@@ -78,6 +78,9 @@ typedef struct {
                           reference's one-bounce gather; ≤ 8): the multiple-scattering loop of
                           path_trace_radiance continued from each media sample, its draws taken
                           from the record's stream after every draw the reference makes */
+  double hg_g;         /* extension: Henyey–Greenstein g of the media (0 = the reference's isotropic
+                          medium; 3D): scattering at each media sample toward the cache point weighs
+                          its gather paths by 4π·p_g, further media events sample HG directions */
 } vc_build_params;
 
 /* Batch estimate_moments (+ make_record for both kinds).

@@ -437,7 +437,28 @@ def gather_mean(ps, points, dirs_pp, n_light):  # src/transport.py:288-310
     return tot.reshape(m, n, 3).mean(axis=1)
 
 
-def gather_mean_bounces(ps, points, dirs_pp, n_light, extras, bounces):
+def hg_phase(g, c):
+    """Henyey–Greenstein phase p(cos θ), normalised over the sphere (extension)."""
+    return (1.0 - g * g) / (4.0 * np.pi * (1.0 + g * g - 2.0 * g * c) ** 1.5)
+
+
+def hg_sample(g, cur, u0, u1):
+    """Extension: a direction about the unit vectors `cur` (m, 3) with cos θ ~ HG(g) (g ≠ 0)
+    from u0 and azimuth 2π·u1, in the branchless orthonormal basis of Duff et al. (2017)."""
+    s = (1.0 - g * g) / (1.0 - g + 2.0 * g * u0)
+    ct = (1.0 + g * g - s * s) / (2.0 * g)
+    st = np.sqrt(np.maximum(0.0, 1.0 - ct * ct))
+    phi = 2.0 * np.pi * u1
+    x, y, z = cur[:, 0], cur[:, 1], cur[:, 2]
+    sign = np.copysign(1.0, z)
+    a = -1.0 / (sign + z)
+    b = x * y * a
+    t1 = np.stack([1.0 + sign * x * x * a, sign * b, -sign * x], axis=1)
+    t2 = np.stack([b, sign + y * y * a, -y], axis=1)
+    return (st * np.cos(phi))[:, None] * t1 + (st * np.sin(phi))[:, None] * t2 + ct[:, None] * cur
+
+
+def gather_mean_bounces(ps, points, dirs_pp, n_light, extras, bounces, g=0.0, x=None):
     """Extension (BASELINE.json cfg3 "multiple scattering up to 4 bounces"; the reference
     stops at one extra bounce): the media-sample gather continued by up to `bounces` − 1
     further media scattering events per gather path, restating the multiple-scattering loop
@@ -445,15 +466,26 @@ def gather_mean_bounces(ps, points, dirs_pp, n_light, extras, bounces):
     −log1p(−u)/σt against the current segment, weight σs/σt per collision, a uniform new
     direction, T·L_o at its surface hit added with the path weight.  `extras` (m, n, B−1, d')
     holds per path and bounce (u_dist, direction draws): the record's PCG64 stream continued
-    after every draw the reference makes (build_record).  bounces = 1 → gather_mean."""
+    after every draw the reference makes (build_record).  bounces = 1 → gather_mean.
+
+    Extension g ≠ 0 (3D; BASELINE cfg2/cfg3's Henyey–Greenstein media): scattering at the media
+    sample y toward the cache point x weighs each gather path by 4π·p_g(ω·w), w = (y − x)/|y − x|
+    (light arriving along −ω leaves toward x), and every further media event samples its new
+    direction from HG(g) about the current one (hg_sample; the σs/σt weight is unchanged)."""
     m, n, dim = dirs_pp.shape
     org = np.repeat(points, n, axis=0)
     dd = dirs_pp.reshape(-1, dim)
     s, idx = trace_or_bounds(ps, org, dd)
     tot = np.exp(-ps.sigma_t * s)[:, None] * surface_radiance(ps, idx, org + s[:, None] * dd, dd, n_light)
+    w0 = np.ones(m * n)
+    if g != 0.0:
+        dx = org - np.asarray(x, float)[None]
+        wk = dx / np.sqrt((dx * dx).sum(axis=1))[:, None]
+        w0 = 4.0 * np.pi * hg_phase(g, (dd * wk).sum(axis=1))
+        tot = tot * w0[:, None]
     if bounces > 1 and ps.sigma_t > 0.0:
         ex = extras.reshape(m * n, bounces - 1, -1)
-        w = np.ones(m * n)
+        w = w0.copy()
         alive = np.ones(m * n, bool)
         pos, cur_d, cur_s = org, dd, s
         for b in range(bounces - 1):
@@ -463,7 +495,10 @@ def gather_mean_bounces(ps, points, dirs_pp, n_light, extras, bounces):
                 break
             pos = pos + np.where(col, t, 0.0)[:, None] * cur_d
             w = w * np.where(col, ps.sigma_s / ps.sigma_t, 1.0)
-            nd = uniform_dirs(dim, ex[:, b, 1] if dim == 2 else ex[:, b, 1:3])
+            if g != 0.0:
+                nd = hg_sample(g, cur_d, ex[:, b, 1], ex[:, b, 2])
+            else:
+                nd = uniform_dirs(dim, ex[:, b, 1] if dim == 2 else ex[:, b, 1:3])
             s2 = np.zeros(m * n)
             s2[col], idx2 = trace_or_bounds(ps, pos[col], nd[col])
             lo2 = surface_radiance(ps, idx2, pos[col] + s2[col, None] * nd[col], nd[col], n_light)
@@ -603,6 +638,7 @@ def build_record(
     n_light_samples: int = 16,
     adjacency=None,
     media_bounces: int = 1,
+    hg_g: float = 0.0,
 ) -> RecordBuild:
     """One cache point: `estimate_moments` (src/subdivision.py:373-393) in one pass.
 
@@ -642,10 +678,10 @@ def build_record(
         else:
             u = rng.random((p.shape[0], n_inner, 2))
             gd = uniform_dirs(3, u.reshape(-1, 2)).reshape(p.shape[0], n_inner, 3)
-        if media_bounces > 1:  # extension: the stream continues after the reference's draws
+        if media_bounces > 1 or hg_g != 0.0:  # extension: the stream continues after the reference's draws
             ex = rng.random((p.shape[0], n_inner, media_bounces - 1, 2 if dim == 2 else 3))
             media_rad.reshape(-1, 3)[flat] = ps.sigma_s * gather_mean_bounces(ps, p, gd, n_light_samples, ex,
-                                                                            media_bounces)
+                                                                            media_bounces, hg_g, x)
         else:
             media_rad.reshape(-1, 3)[flat] = ps.sigma_s * gather_mean(ps, p, gd, n_light_samples)
 

@@ -43,6 +43,7 @@ class BuildParams(C.Structure):
         ("flags", C.c_int),
         ("seed_words", C.c_int),
         ("media_bounces", C.c_int),
+        ("hg_g", C.c_double),
     ]
 
 

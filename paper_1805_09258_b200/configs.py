@@ -32,6 +32,7 @@ class Workload:
     n_light_samples: int = 16
     epsilon: float = 0.05
     media_bounces: int = 1  # extension: media events per gather path (1 = the reference)
+    hg_g: float = 0.0  # extension: Henyey-Greenstein g of the media scattering events (0 = the reference)
 
     @property
     def dim(self) -> int:

@@ -394,6 +394,8 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   P.n_inner = prm->n_inner;
   if (prm->media_bounces < 0 || prm->media_bounces > 8) return fail(VC_EINVAL, "media_bounces must be in [0, 8]");
   P.media_bounces = std::max(1, prm->media_bounces);
+  if (!(prm->hg_g > -1.0 && prm->hg_g < 1.0)) return fail(VC_EINVAL, "hg_g must lie in (-1, 1)");
+  P.hg_g = D == 3 ? prm->hg_g : 0.0;
   P.epsilon = prm->epsilon;
   P.anisotropic = (prm->flags & VC_ISOTROPIC) ? 0 : 1;
   P.make_records = (records != nullptr) || (prm->flags & VC_MAKE_RECORDS);

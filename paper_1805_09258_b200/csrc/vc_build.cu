@@ -262,6 +262,30 @@ __device__ __forceinline__ void mark_live(const Wave& W, int n, int rec, int k, 
   atomicOr(w, 1ULL << (ring & 63));
 }
 
+// Extension helpers (oracle hg_phase / hg_sample, same float64 operation order).
+__device__ __forceinline__ double hg_phase(double g, double c) {
+  const double num = sub(1.0, mul(g, g));
+  const double b = sub(add(1.0, mul(g, g)), mul(mul(2.0, g), c));
+  return __ddiv_rn(num, mul(4.0 * kPi, pow(b, 1.5)));
+}
+
+// cd ← a direction about cd with cos θ ~ HG(g) from u0, azimuth 2π·u1 (Duff et al. basis)
+__device__ __forceinline__ void hg_sample(double g, double* cd, double u0, double u1) {
+  const double s = __ddiv_rn(sub(1.0, mul(g, g)), add(sub(1.0, g), mul(mul(2.0, g), u0)));
+  const double ct = __ddiv_rn(sub(add(1.0, mul(g, g)), mul(s, s)), mul(2.0, g));
+  const double st = sqrt(fmax(0.0, sub(1.0, mul(ct, ct))));
+  const double phi = mul(2.0 * kPi, u1);
+  const double x = cd[0], y = cd[1], z = cd[2];
+  const double sg = copysign(1.0, z);
+  const double a = __ddiv_rn(-1.0, add(sg, z));
+  const double b = mul(mul(x, y), a);
+  const double t1[3] = {add(1.0, mul(mul(mul(sg, x), x), a)), mul(sg, b), mul(-sg, x)};
+  const double t2[3] = {b, add(sg, mul(mul(y, y), a)), -y};
+  const double ca = mul(st, cos(phi)), sa = mul(st, sin(phi));
+#pragma unroll
+  for (int c = 0; c < 3; ++c) cd[c] = add(add(mul(ca, t1[c]), mul(sa, t2[c])), mul(ct, cd[c]));
+}
+
 template <int D>
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const long long total = W.rec_base[W.B];
@@ -269,7 +293,8 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
   const long long draws0 = (D == 3) ? 2LL * P.rows * P.cols : (long long)n;
   const int per = (D == 3 ? 2 : 1) * P.n_inner;
   const int nb = P.media_bounces - 1;  // extension: further media events per gather path
-  const bool emitter_first = !S.reflective && 2 * S.emit.K <= S.geo.K && nb == 0;
+  const double hg = (D == 3) ? P.hg_g : 0.0;  // extension: Henyey–Greenstein media
+  const bool emitter_first = !S.reflective && 2 * S.emit.K <= S.geo.K && nb == 0 && hg == 0.0;
   const double albedo = S.sigma_t > 0.0 ? __ddiv_rn(S.sigma_s, S.sigma_t) : 0.0;
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total;
        j += (long long)gridDim.x * blockDim.x) {
@@ -336,6 +361,18 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
         path[1] = mul(T, L[1]);
         path[2] = mul(T, L[2]);
       }
+      double w0 = 1.0;
+      if (hg != 0.0) {  // extension: HG scattering at y toward x (oracle gather_mean_bounces)
+        double dx[3], wk[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dx[c] = sub(y[c], W.x[rec * D + c]);
+        const double nrm = sqrt(add(add(mul(dx[0], dx[0]), mul(dx[1], dx[1])), mul(dx[2], dx[2])));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) wk[c] = __ddiv_rn(dx[c], nrm);
+        w0 = mul(4.0 * kPi, hg_phase(hg, add(add(mul(gd[0], wk[0]), mul(gd[1], wk[1])), mul(gd[2], wk[2]))));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) path[c] = mul(path[c], w0);
+      }
       if (nb > 0 && S.sigma_t > 0.0) {
         // Extension: the multiple-scattering loop of path_trace_radiance (src/transport.py:
         // 362-388) from y along the gather ray — collision at −log1p(−u)/σt inside the current
@@ -345,7 +382,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
         Pcg64 gx = pcg_load(W.rng + 4 * rec);
         pcg_advance(gx, (unsigned long long)(draws0 + (long long)per * W.rec_P[rec] +
                                              ((long long)jl * P.n_inner + t) * nb * pb), jt);
-        double pos[3] = {y[0], y[1], y[2]}, cd[3] = {gd[0], gd[1], gd[2]}, cs = s2, w = 1.0;
+        double pos[3] = {y[0], y[1], y[2]}, cd[3] = {gd[0], gd[1], gd[2]}, cs = s2, w = w0;
         for (int bb = 0; bb < nb; ++bb) {
           const double ud = gx.next_double();
           const double ua = gx.next_double();
@@ -359,6 +396,8 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
             const double th = mul(2.0 * kPi, ua);
             cd[0] = cos(th);
             cd[1] = sin(th);
+          } else if (hg != 0.0) {
+            hg_sample(hg, cd, ua, ub);
           } else {
             const double z = sub(1.0, mul(2.0, ua));
             const double phi = mul(2.0 * kPi, ub);
@@ -2732,7 +2771,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   cudaMemsetAsync(W.live, 0, sizeof(unsigned long long) * (size_t)W.live_words * nt, st);
   if (S.sigma_s > 0.0) {
     const bool two_pass = !S.reflective && 2 * S.emit.K <= S.geo.K && P.n_inner == 1 && W.gather_q_cap > 0 &&
-                          P.media_bounces <= 1;
+                          P.media_bounces <= 1 && P.hg_g == 0.0;
     prof_begin(KC_GATHER, st);
     if (two_pass) {
       cudaMemsetAsync(W.gather_q_count, 0, sizeof(unsigned long long), st);

@@ -104,6 +104,7 @@ struct BuildParams {
   double march_step;
   int n_inner;
   int media_bounces;     // media events per gather path (1: the reference; extension > 1)
+  double hg_g;           // extension: Henyey–Greenstein g of the media (0: the reference)
   int rows, cols;        // 3D stratum grid (src/scene.py:370-385); 2D: rows = 1, cols = n
   int n_tris;            // elements per ring: n (2D) or 2n-4 (3D)
   int r_ub;              // upper bound on rings per record (allocation)

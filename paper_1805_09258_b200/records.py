@@ -183,9 +183,11 @@ def pcg64_state(rng_seed) -> tuple[np.ndarray, np.random.Generator]:
     return np.array([s >> 64, s & m, inc >> 64, inc & m], dtype=np.uint64), g
 
 
-def _params(dim, n_angular, march_step, n_inner, n_light_samples, epsilon, flags, seed_words=0, media_bounces=1):
+def _params(dim, n_angular, march_step, n_inner, n_light_samples, epsilon, flags, seed_words=0, media_bounces=1,
+            hg_g=0.0):
     p = _lib.BuildParams()
     p.media_bounces = int(media_bounces)
+    p.hg_g = float(hg_g)
     p.n_angular = int(DEFAULT_N_ANGULAR[dim] if n_angular is None else n_angular)
     p.march_step = float(march_step)
     p.n_inner = int(n_inner)
@@ -202,14 +204,15 @@ def _draws(dim, n, P, n_inner, media_bounces=1):
 
 
 def estimate_moments(scene, x, n_angular=None, march_step=0.1, rng_seed=None, n_inner=1,
-                     n_light_samples=16, adjacency=None, media_bounces=1):
+                     n_light_samples=16, adjacency=None, media_bounces=1, hg_g=0.0):
     """(single, multiple) Moments at x — drop-in for src/subdivision.py:373-393.
 
     `adjacency` optionally injects the 3D triangle list (e.g. qhull's simplices) instead
     of the GPU spherical Delaunay.  A Generator passed as rng_seed is advanced by the
     draws the build consumed, exactly as the reference would.  `media_bounces` > 1 is an
     extension (not in the reference): each media sample's gather path continues through up
-    to media_bounces − 1 further media scattering events.
+    to media_bounces − 1 further media scattering events, and `hg_g` ≠ 0 makes those media
+    scattering events Henyey–Greenstein.
     """
     ds = device_scene(scene)
     x = np.ascontiguousarray(np.asarray(x, float).reshape(-1))
@@ -221,7 +224,7 @@ def estimate_moments(scene, x, n_angular=None, march_step=0.1, rng_seed=None, n_
         raise ValueError("subdivision center lies outside the medium bounds")
     st, gen = pcg64_state(rng_seed)
     p = _params(ds.dim, n_angular, march_step, n_inner, n_light_samples, None, _lib.VC_MEM_HOST,
-                media_bounces=media_bounces)
+                media_bounces=media_bounces, hg_g=hg_g)
     d = ds.dim
     mom = np.zeros((2, moment_size(d)))
     stats = np.zeros(8, np.int64)
@@ -273,7 +276,7 @@ class BatchResult:
 
 def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None, march_step=0.1,
                            n_inner=1, n_light_samples=16, adjacency=None, epsilon=None,
-                           anisotropic=True, stream=None, media_bounces=1) -> BatchResult:
+                           anisotropic=True, stream=None, media_bounces=1, hg_g=0.0) -> BatchResult:
     """Batch record build: N cache points in one call (moments, stats, optional records).
 
     X is (N, d) host numpy or a CUDA torch tensor (then every output is a CUDA tensor
@@ -325,7 +328,7 @@ def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None
         recs = np.zeros((N, 2, record_size(d))) if epsilon else None
         adj = np.ascontiguousarray(np.asarray(adjacency, np.int32)) if (adjacency is not None and d == 3) else None
     p = _params(d, n_angular, march_step, n_inner, n_light_samples, epsilon, flags,
-                seed_words=(rng.shape[1] if seeds is not None else 0), media_bounces=media_bounces)
+                seed_words=(rng.shape[1] if seeds is not None else 0), media_bounces=media_bounces, hg_g=hg_g)
     _lib.check(_lib.lib().vc_build_records(ds.handle, N, _lib.ptr(Xc), _lib.ptr(rng), _lib.ptr(adj),
                                            _lib.C.byref(p), _lib.ptr(mom), _lib.ptr(stats), _lib.ptr(recs),
                                            stream))
@@ -333,14 +336,14 @@ def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None
 
 
 def inspect_record(scene, x, rng_seed=None, n_angular=None, march_step=0.1, n_inner=1,
-                   n_light_samples=16, adjacency=None, media_cap=1 << 22, media_bounces=1):
+                   n_light_samples=16, adjacency=None, media_cap=1 << 22, media_bounces=1, hg_g=0.0):
     """One record with its per-direction internals (dirs, s, idx, counts, triangles, media)."""
     ds = device_scene(scene)
     d = ds.dim
     x = np.ascontiguousarray(np.asarray(x, float).reshape(-1))
     st, _ = pcg64_state(rng_seed)
     p = _params(d, n_angular, march_step, n_inner, n_light_samples, None, _lib.VC_MEM_HOST,
-                media_bounces=media_bounces)
+                media_bounces=media_bounces, hg_g=hg_g)
     n = p.n_angular
     dirs = np.zeros((n, d))
     s = np.zeros(n)

@@ -597,7 +597,22 @@ def _chunked_trace(orig, chunk=64):
     return trace
 
 
-def _gather_bounces_shim(seed_box, bounces):
+def _hg_sample_ref(g, cur, u0, u1):
+    """HG direction sampling about `cur` (the extension's convention)."""
+    s = (1.0 - g * g) / (1.0 - g + 2.0 * g * u0)
+    ct = (1.0 + g * g - s * s) / (2.0 * g)
+    st = np.sqrt(np.maximum(0.0, 1.0 - ct * ct))
+    phi = 2.0 * np.pi * u1
+    x, y, z = cur[:, 0], cur[:, 1], cur[:, 2]
+    sign = np.copysign(1.0, z)
+    a = -1.0 / (sign + z)
+    b = x * y * a
+    t1 = np.stack([1.0 + sign * x * x * a, sign * b, -sign * x], axis=1)
+    t2 = np.stack([b, sign + y * y * a, -y], axis=1)
+    return (st * np.cos(phi))[:, None] * t1 + (st * np.sin(phi))[:, None] * t2 + ct[:, None] * cur
+
+
+def _gather_bounces_shim(seed_box, bounces, hg=0.0):
     """Extension oracle written with the reference's own primitives: mean_surface_gather
     (src/transport.py:288-310) continued by up to `bounces` − 1 media scattering events per
     gather path, exactly the multiple-scattering loop of path_trace_radiance
@@ -618,7 +633,14 @@ def _gather_bounces_shim(seed_box, bounces):
         tot = np.exp(-scene.medium.sigma_t * s)[:, None] * vt.surface_radiance_batch(
             scene, idx, origins + s[:, None] * dirs, dirs, n_light_samples)
         sig_t, sig_s = scene.medium.sigma_t, scene.medium.sigma_s
-        w = np.ones(m * n)
+        w0 = np.ones(m * n)
+        if hg != 0.0:  # HG scattering at the media sample toward the cache point
+            dx = origins - seed_box["x"][None]
+            wk = dx / np.sqrt((dx * dx).sum(axis=1))[:, None]
+            c = (dirs * wk).sum(axis=1)
+            w0 = 4.0 * np.pi * ((1.0 - hg * hg) / (4.0 * np.pi * (1.0 + hg * hg - 2.0 * hg * c) ** 1.5))
+            tot = tot * w0[:, None]
+        w = w0.copy()
         alive = np.ones(m * n, dtype=bool)
         pos, cur_d, cur_s = origins, dirs, s
         for b in range(bounces - 1):
@@ -628,7 +650,10 @@ def _gather_bounces_shim(seed_box, bounces):
                 break
             pos = pos + np.where(collide, t, 0.0)[:, None] * cur_d
             w = w * np.where(collide, sig_s / sig_t, 1.0)
-            nd = vt.uniform_directions(dim, ex[:, b, 1] if dim == 2 else ex[:, b, 1:3])
+            if hg != 0.0:
+                nd = _hg_sample_ref(hg, cur_d, ex[:, b, 1], ex[:, b, 2])
+            else:
+                nd = vt.uniform_directions(dim, ex[:, b, 1] if dim == 2 else ex[:, b, 1:3])
             s2 = np.zeros(m * n)
             s2[collide], idx2 = vscene.trace_or_bounds(scene, pos[collide], nd[collide])
             lo2 = vt.surface_radiance_batch(scene, idx2, pos[collide] + s2[collide, None] * nd[collide],
@@ -640,6 +665,38 @@ def _gather_bounces_shim(seed_box, bounces):
         return tot.reshape(m, n, 3).mean(axis=1)
 
     return gather
+
+
+def gen_media_hg():
+    """Extension records with Henyey–Greenstein media (g = 0.5, BASELINE cfg3) and 4 media
+    events per gather path: the reference's build_subdivision + assemble_moments with the
+    gather rebuilt from its primitives (_gather_bounces_shim)."""
+    room = configs.cfg3_scene(n_spheres=4, level=1)
+    rs = ref_scene(room)
+    pts = np.random.default_rng(23).uniform(room.bounds_min + 0.3, room.bounds_max - 0.3, (3, 3))
+    n, step, B, g = 1024, 0.2, 4, 0.5
+    box = {}
+    orig = vs.mean_surface_gather
+    vs.mean_surface_gather = _gather_bounces_shim(box, B, g)
+    res = {k: [] for k in ("L", "grad", "hess", "stats", "adj")}
+    try:
+        for i, x in enumerate(pts):
+            box.update(seed=vr._seed(4, 401, i), n_dirs=n, x=np.asarray(x, float))
+            with Capture() as cap:
+                sub = vs.build_subdivision(rs, x, n_angular=n, march_step=step, rng_seed=vr._seed(4, 401, i))
+            single, multiple, stats = vs.assemble_moments(sub, rs.medium)
+            res["L"].append([single.L, multiple.L])
+            res["grad"].append([single.grad, multiple.grad])
+            res["hess"].append([single.hess, multiple.hess])
+            res["stats"].append([stats["elements_evaluated"], stats["elements_dropped"], stats["star_vertices"]])
+            res["adj"].append(np.asarray(cap.dirs.adjacency, np.int32))
+    finally:
+        vs.mean_surface_gather = orig
+    out = {k: np.array(v) for k, v in res.items()}
+    out.update(scene_fields("", rs))
+    out.update(versions=VERSIONS, points=pts, cfg_seed=np.array(4), params=np.array([n, step, 1, 16, float(B), g]))
+    np.savez_compressed(OUT / "rec_media_hg.npz", **out)
+    print("wrote media_hg", flush=True)
 
 
 def gen_media_bounces():
@@ -932,6 +989,8 @@ if __name__ == "__main__":
         gen_surface()
     if "media_bounces" in which:
         gen_media_bounces()
+    if "media_hg" in which:
+        gen_media_hg()
     if "cfg5_crop" in which:
         gen_cfg5_crop()
     if "path" in which:

@@ -198,6 +198,28 @@ def test_surface_radiance_vs_reference(name):
     np.testing.assert_allclose(lo, want, rtol=1e-12, atol=1e-15)
 
 
+def test_media_hg_extension_vs_reference_shim():
+    """Extension (BASELINE cfg3: Henyey–Greenstein g = 0.5, up to 4 bounces): HG scattering at
+    every media sample toward the cache point and at every further media event.  Device vs
+    the reference's build_subdivision + assemble_moments with the gather rebuilt from its
+    primitives (tests/golden/rec_media_hg.npz; the oracle is pinned to it), qhull adjacency
+    injected; the north_star gate, element counts exact."""
+    from paper_1805_09258_b200 import estimate_moments_batch
+
+    z = golden("rec_media_hg")
+    sc = golden_scene(z)
+    n, step, n_inner, n_light, B, g = z["params"]
+    N = len(z["points"])
+    seed = int(z["cfg_seed"])
+    words = np.array([[seed, 401, i] for i in range(N)], np.uint32)
+    r = estimate_moments_batch(sc, z["points"], seeds=words, n_angular=int(n), march_step=float(step),
+                               n_inner=int(n_inner), n_light_samples=int(n_light), adjacency=z["adj"].astype(np.int32),
+                               media_bounces=int(B), hg_g=float(g))
+    for i in range(N):
+        _check_moments(f"media_hg{g}[{i}]", r.L[i], r.grad[i], r.hess[i], z["L"][i], z["grad"][i], z["hess"][i])
+        assert tuple(int(v) for v in r.stats[i, :3]) == tuple(int(v) for v in z["stats"][i])
+
+
 def _tri_set(t):
     return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
 

@@ -84,6 +84,6 @@ def test_build_params_layout():
     from paper_1805_09258_b200 import _lib
 
     # matches vc_build_params in include/volcache_b200.h (x86-64 SysV layout)
-    assert C.sizeof(_lib.BuildParams) == 48  # include/volcache_b200.h vc_build_params (incl. media_bounces)
+    assert C.sizeof(_lib.BuildParams) == 56  # include/volcache_b200.h vc_build_params (incl. media_bounces, hg_g)
     assert _lib.BuildParams.epsilon.offset == 24
     assert C.sizeof(_lib.Camera) == 10 * 8 + 6 * 4 + 4 * 0 or C.sizeof(_lib.Camera) == 104

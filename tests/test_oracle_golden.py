@@ -98,6 +98,24 @@ def test_surface_radiance_matches_reference():
     np.testing.assert_allclose(lo, z["small_lo"], rtol=1e-12, atol=1e-15)
 
 
+def test_media_hg_oracle_matches_reference_shim():
+    """The Henyey–Greenstein extension (g = 0.5 at the media sample and at every further media
+    event, 4 events per gather path) in the oracle against the reference's build_subdivision +
+    assemble_moments with the gather rebuilt from its primitives (gen_media_hg)."""
+    z = golden("rec_media_hg")
+    ps = O.pack(golden_scene(z))
+    n, step, n_inner, n_light, B, g = z["params"]
+    for i, x in enumerate(z["points"]):
+        rb = O.build_record(ps, x, int(n), float(step), O.seed_seq(int(z["cfg_seed"]), 401, i), int(n_inner),
+                            int(n_light), adjacency=z["adj"][i], media_bounces=int(B), hg_g=float(g))
+        assert [rb.stats["elements_evaluated"], rb.stats["elements_dropped"], rb.stats["star_vertices"]] == \
+            z["stats"][i].tolist()
+        for k in range(2):
+            assert rel_l2(rb.L[k], z["L"][i][k]) <= 1e-12
+            assert rel_l2(rb.grad[k], z["grad"][i][k]) <= 1e-11
+            assert rel_l2(rb.hess[k], z["hess"][i][k]) <= 1e-10
+
+
 def test_make_record_edge_cases():
     z = golden("make_record")
     for j in range(int(z["n_cases"])):
