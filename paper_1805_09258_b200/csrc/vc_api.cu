@@ -516,7 +516,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.gather_q_cap = std::min<long long>(W.media_cap, std::max<long long>(1LL << 24, W.media_cap / 10));
   if (const char* e = getenv("VOLCACHE_GATHER_QCAP")) W.gather_q_cap = std::min<long long>(W.gather_q_cap, atoll(e));
   W.gather_q = alloc(32, (size_t)W.gather_q_cap * 80);
-  W.gather_q_count = (unsigned long long*)alloc(33, 8);
+  W.gather_q_count = (unsigned long long*)alloc(33, 16);  // [1]: the occlusion pass's fetch cursor
   W.surv_cnt = (int*)alloc(52, (size_t)B * 8);  // slots 22-30, 50-51: vc_render around its miss builds
   W.redo = W.surv_cnt + B;
   if (err != cudaSuccess) return cuda_fail(err, "workspace allocation");

@@ -958,6 +958,143 @@ __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl(DevScene S, Wav
   }
 }
 
+// Occlusion pass with persistent lanes: every lane owns one queued ray at a time and advances
+// its traversal leaf by leaf; a lane whose ray is decided writes the result and fetches the
+// next ray (warp-aggregated atomic cursor) at the next step, so lanes no longer idle until
+// the slowest ray of a grid-stride batch finishes (k_gather_occl: 9 of 32 lanes active per
+// instruction).  The traversal is bvh_query's any-hit mode, resumable: the same node order,
+// culling and (t, index) decision per ray.
+#ifndef VC_OCCL_PT
+#define VC_OCCL_PT 1
+#endif
+template <int D>
+__global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl_pt(DevScene S, Wave W, int n, const GatherItem* q,
+                                                                  unsigned long long* q_count, long long q_cap,
+                                                                  float* media) {
+  const long long nq = min((long long)q_count[0], q_cap);
+  unsigned long long* cursor = q_count + 1;
+  const DevBvh& H = S.geo;
+  const int lane = threadIdx.x & 31;
+  const float slack = 1e-5f * (float)S.scale;
+  LocalStack stk;
+  long long cur_item = -1;
+  bool exhausted = false;
+  double o[3] = {0, 0, 0}, d[3] = {0, 0, 0}, thr = 0.0;
+  int id_thr = 0;
+  float2 inv2[3], noi2[3];
+  float tbf = 0.0f;
+  int sp = 0;
+  unsigned cur = 0;
+  auto finish = [&](bool occl) {
+    const GatherItem& it = q[cur_item];
+    double v[3] = {0.0, 0.0, 0.0};
+    if (!occl) {  // L_o = emission (non-reflective scene); σs · T · L_o / n_inner with n_inner = 1
+      const double* E = S.emission + (size_t)it.ie * 3;
+      const double T = exp(-S.sigma_t * it.te);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
+    }
+    store_media(media + (size_t)it.slot * 3, v);
+    if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, it.rec, it.k, it.ring);
+    cur_item = -1;
+  };
+  auto pop = [&]() -> bool {
+    while (sp > 0) {
+      const uint2 e = stk.get(--sp);
+      if (__uint_as_float(e.y) <= tbf) {
+        cur = e.x;
+        return true;
+      }
+    }
+    return false;
+  };
+  while (true) {
+    // lanes without a ray fetch the next ones
+    const bool need = cur_item < 0 && !exhausted;
+    const unsigned mneed = __ballot_sync(0xffffffffu, need);
+    if (mneed) {
+      const int leader = __ffs(mneed) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(cursor, (unsigned long long)__popc(mneed));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const long long t = (long long)base + __popc(mneed & ((1u << lane) - 1u));
+        if (t >= nq) {
+          exhausted = true;
+        } else if (q[t].slot >= 0) {  // (negative: an unused tail slot of a producer's chunk)
+          cur_item = t;
+          const GatherItem& it = q[t];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            o[a] = it.y[a];
+            d[a] = it.d[a];
+          }
+          thr = it.te;
+          id_thr = it.ie;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            float inv = 0.0f, noi = 0.0f;
+            if (a < D) {
+              const float orl = (float)(o[a] - H.ctr[a]);
+              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)d[a]));
+              noi = -orl * inv;
+            }
+            inv2[a] = make_float2(inv, inv);
+            noi2[a] = make_float2(noi, noi);
+          }
+          tbf = __double2float_ru(thr) * 1.0001f + slack;  // thr finite: an emitter hit distance
+          sp = 0;
+          cur = 0;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, cur_item >= 0)) {
+      if (__all_sync(0xffffffffu, exhausted)) break;
+      continue;
+    }
+    if (cur_item >= 0) {
+      // one step: descend to the next leaf, test it
+      bool alive = true;
+      while (!(cur & 0x80000000u)) {
+        const float4* N = H.nodes + 4 * (size_t)cur;
+        const float4 A = __ldg(N), B = __ldg(N + 1), C = __ldg(N + 2), R = __ldg(N + 3);
+        float tl, tr;
+        bool hl, hr;
+        box_hit2<D>(A, B, C, inv2, noi2, tbf, hl, hr, tl, tr);
+        if (hl && hr) {
+          const bool lf = tl <= tr;
+          stk.put(sp++, make_uint2(__float_as_uint(lf ? R.z : R.x), __float_as_uint(lf ? tr : tl)));
+          cur = __float_as_uint(lf ? R.x : R.z);
+        } else if (hl || hr) {
+          cur = __float_as_uint(hl ? R.x : R.z);
+        } else if (!pop()) {
+          alive = false;
+          break;
+        }
+      }
+      if (!alive) {
+        finish(false);
+      } else {
+        bool occl = false;
+        for (int k = (int)(cur & 0x7fffffffu);; ++k) {
+          const int idf = __float_as_int(__ldg(&H.prim32[3 * (size_t)k + 2].w));
+          const double t = hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+          if (t != INFINITY) {
+            const int id = idf & 0x7fffffff;
+            if (t < thr || (t == thr && id < id_thr)) {
+              occl = true;
+              break;
+            }
+          }
+          if (idf < 0) break;
+        }
+        if (occl) finish(true);
+        else if (!pop()) finish(false);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Spherical Delaunay (3D connectivity, src/scene.py:388-399)
 // ---------------------------------------------------------------------------
@@ -2774,7 +2911,7 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
                           P.media_bounces <= 1 && P.hg_g == 0.0;
     prof_begin(KC_GATHER, st);
     if (two_pass) {
-      cudaMemsetAsync(W.gather_q_count, 0, sizeof(unsigned long long), st);
+      cudaMemsetAsync(W.gather_q_count, 0, 2 * sizeof(unsigned long long), st);
       if (VC_GATHER_SPLIT && !W.dense_media) {  // filter → survivor evaluation → redo pass
         cudaMemsetAsync(W.surv_cnt, 0, sizeof(int) * 2 * (size_t)W.B, st);  // surv_cnt and redo
         k_gather_emit<D, 1><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
@@ -2788,10 +2925,12 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         k_gather_emit<D, 0><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
       }
-      k_gather_occl<D><<<sm_count * 8, 256, stack_smem(k_gather_occl<D>, S.geo), st>>>(
-                                                     S, W, P.n_angular, (const GatherItem*)W.gather_q,
-                                                     W.gather_q_count,
-                                                     W.gather_q_cap, W.media);
+      if (VC_OCCL_PT && S.geo.n_nodes > 0)
+        k_gather_occl_pt<D><<<sm_count * 8, 256, 0, st>>>(S, W, P.n_angular, (const GatherItem*)W.gather_q,
+                                                          W.gather_q_count, W.gather_q_cap, W.media);
+      else
+        k_gather_occl<D><<<sm_count * 8, 256, stack_smem(k_gather_occl<D>, S.geo), st>>>(
+            S, W, P.n_angular, (const GatherItem*)W.gather_q, W.gather_q_count, W.gather_q_cap, W.media);
       nl += 2;
     } else {
       k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
