@@ -519,6 +519,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.gather_q_count = (unsigned long long*)alloc(33, 16);  // [1]: the occlusion pass's fetch cursor
   W.surv_cnt = (int*)alloc(52, (size_t)B * 8);  // slots 22-30, 50-51: vc_render around its miss builds
   W.redo = W.surv_cnt + B;
+  W.ray_cursor = (unsigned long long*)alloc(53, 16);
   if (err != cudaSuccess) return cuda_fail(err, "workspace allocation");
 
   W.outside = inside.dflag;

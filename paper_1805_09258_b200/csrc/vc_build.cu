@@ -123,6 +123,160 @@ __global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, Buil
   W.lo[base * 3 + 2] = L[2];
 }
 
+// Persistent-lane primary pass (non-reflective scenes with a BVH; VC_PRIMARY_PT): the
+// directions first (thread per direction), then every lane owns one primary ray at a time
+// and advances its nearest-hit traversal leaf by leaf, fetching the next ray index (tile
+// order) through a warp-aggregated cursor when its ray is done.  Same traversal, culling
+// and (t, index) decision per ray as trace_or_bounds; the results do not depend on the
+// schedule.  Off: 6.03 ms vs 5.77 ms per 2048 records for the thread-per-direction kernel
+// (lane efficiency 15.4/32 — the tiled primary rays are coherent, fetching breaks that).
+#ifndef VC_PRIMARY_PT
+#define VC_PRIMARY_PT 0
+#endif
+template <int D>
+__global__ void __launch_bounds__(256) k_directions(BuildParams P, Wave W, JumpTables jt) {
+  const int n = P.n_angular;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)W.B * n) return;
+  const int rec = (int)(gid / n);
+  const int k = (int)(gid - (long long)rec * n);
+  Pcg64 g0 = pcg_load(W.rng + 4 * rec);
+  double d[3];
+  stratum_direction<D>(k, P, g0, jt, d);
+  const size_t base = (size_t)rec * n + k;
+#pragma unroll
+  for (int a = 0; a < D; ++a) W.dirs[base * D + a] = d[a];
+  if constexpr (D == 3) W.dirs32[base] = make_float4((float)d[0], (float)d[1], (float)d[2], 0.0f);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary_pt(DevScene S, BuildParams P, Wave W,
+                                                                 unsigned long long* cursor) {
+  const int n = P.n_angular;
+  const long long total = (long long)W.B * n;
+  const DevBvh& H = S.geo;
+  const int lane = threadIdx.x & 31;
+  const float slack = 1e-5f * (float)S.scale;
+  auto tlim = [&](double t) { return isfinite(t) ? __double2float_ru(t) * 1.0001f + slack : INFINITY; };
+  LocalStack stk;
+  long long ray = -1;
+  bool exhausted = false;
+  double o[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_best = INFINITY;
+  int id_best = -1;
+  float2 inv2[3], noi2[3];
+  float tbf = INFINITY;
+  int sp = 0;
+  unsigned cur = 0;
+  size_t base = 0;
+  auto finish = [&]() {
+    double s = isfinite(t_best) ? t_best : bounds_exit<D>(S, o, d);
+    W.s[base] = s;
+    W.idx[base] = id_best;
+    double L[3] = {0.0, 0.0, 0.0};  // surface_radiance of a non-reflective scene: the emission
+    if (id_best >= 0) {
+      const double* E = S.emission + (size_t)id_best * 3;
+      L[0] = E[0];
+      L[1] = E[1];
+      L[2] = E[2];
+    }
+    W.lo[base * 3 + 0] = L[0];
+    W.lo[base * 3 + 1] = L[1];
+    W.lo[base * 3 + 2] = L[2];
+    ray = -1;
+  };
+  auto pop = [&]() -> bool {
+    while (sp > 0) {
+      const uint2 e = stk.get(--sp);
+      if (__uint_as_float(e.y) <= tbf) {
+        cur = e.x;
+        return true;
+      }
+    }
+    return false;
+  };
+  while (true) {
+    const bool need = ray < 0 && !exhausted;
+    const unsigned mneed = __ballot_sync(0xffffffffu, need);
+    if (mneed) {
+      const int leader = __ffs(mneed) - 1;
+      unsigned long long b0 = 0;
+      if (lane == leader) b0 = atomicAdd(cursor, (unsigned long long)__popc(mneed));
+      b0 = __shfl_sync(0xffffffffu, b0, leader);
+      if (need) {
+        const long long g = (long long)b0 + __popc(mneed & ((1u << lane) - 1u));
+        if (g >= total) {
+          exhausted = true;
+        } else {
+          ray = g;
+          const int rec = (int)(g / n);
+          const int k = tiled_direction((int)(g - (long long)rec * n), P);
+          base = (size_t)rec * n + k;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            o[a] = a < D ? W.x[rec * D + a] : 0.0;
+            d[a] = a < D ? W.dirs[base * D + a] : 0.0;
+            float inv = 0.0f, noi = 0.0f;
+            if (a < D) {
+              const float orl = (float)(o[a] - H.ctr[a]);
+              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)d[a]));
+              noi = -orl * inv;
+            }
+            inv2[a] = make_float2(inv, inv);
+            noi2[a] = make_float2(noi, noi);
+          }
+          t_best = INFINITY;
+          id_best = -1;
+          tbf = INFINITY;
+          sp = 0;
+          cur = 0;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, ray >= 0)) {
+      if (__all_sync(0xffffffffu, exhausted)) break;
+      continue;
+    }
+    if (ray >= 0) {  // one step: descend to the next leaf, test it
+      bool alive = true;
+      while (!(cur & 0x80000000u)) {
+        const float4* N = H.nodes + 4 * (size_t)cur;
+        const float4 A = __ldg(N), B = __ldg(N + 1), C = __ldg(N + 2), R = __ldg(N + 3);
+        float tl, tr;
+        bool hl, hr;
+        box_hit2<D>(A, B, C, inv2, noi2, tbf, hl, hr, tl, tr);
+        if (hl && hr) {
+          const bool lf = tl <= tr;
+          stk.put(sp++, make_uint2(__float_as_uint(lf ? R.z : R.x), __float_as_uint(lf ? tr : tl)));
+          cur = __float_as_uint(lf ? R.x : R.z);
+        } else if (hl || hr) {
+          cur = __float_as_uint(hl ? R.x : R.z);
+        } else if (!pop()) {
+          alive = false;
+          break;
+        }
+      }
+      if (alive) {
+        for (int k = (int)(cur & 0x7fffffffu);; ++k) {
+          const int idf = __float_as_int(__ldg(&H.prim32[3 * (size_t)k + 2].w));
+          const double t = hit_prim<D>(H.prim + (size_t)k * prim_stride(D), o, d, S.t_eps);
+          if (t != INFINITY) {
+            const int id = idf & 0x7fffffff;
+            if (t < t_best || (t == t_best && id < id_best)) {
+              t_best = t;
+              id_best = id;
+              tbf = tlim(t_best);
+            }
+          }
+          if (idf < 0) break;
+        }
+        if (!pop()) finish();
+      } else {
+        finish();
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Ring counts (src/subdivision.py:172-176)
 // ---------------------------------------------------------------------------
@@ -2894,8 +3048,16 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
                           int* own, int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
   const long long nt = (long long)W.B * P.n_angular;
   prof_begin(KC_PRIMARY, st);
-  if (S.reflective) k_primary<D, true><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, true>, S.geo), st>>>(S, P, W, jt);
-  else k_primary<D, false><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, false>, S.geo), st>>>(S, P, W, jt);
+  if (S.reflective) {
+    k_primary<D, true><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, true>, S.geo), st>>>(S, P, W, jt);
+  } else if (VC_PRIMARY_PT && D == 3 && S.geo.n_nodes > 0 && W.ray_cursor) {
+    k_directions<D><<<grid_for(nt, 256), 256, 0, st>>>(P, W, jt);
+    cudaMemsetAsync(W.ray_cursor, 0, sizeof(unsigned long long), st);
+    k_primary_pt<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, W.ray_cursor);
+    if (kc) kc->launches += 1;
+  } else {
+    k_primary<D, false><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, false>, S.geo), st>>>(S, P, W, jt);
+  }
   prof_end(st);
   prof_begin(KC_RINGS, st);
   k_rings<<<W.B, kRingBS, 0, st>>>(P, W);

@@ -142,6 +142,7 @@ struct Wave {
   const int* outside;    // device bounds-check flag (nullptr: host-checked); set → no rings
   int* surv_cnt;         // B: survivors of the gather filter per record; redo = surv_cnt + B
   int* redo;             // B: 1 → the record's survivor evaluation found the queue full
+  unsigned long long* ray_cursor;  // persistent-lane primary pass: next ray index
   DirInfo* info;         // B × n
   double* partial;       // B × kAsmParts × 2 × 32 assembly partial sums (+ counters)
   int B;                 // records in this wave
