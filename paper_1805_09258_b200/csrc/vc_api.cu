@@ -272,8 +272,12 @@ struct Profiler {
   bool on = false;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
-  int open_kc = -1;
-  cudaEvent_t open_ev = nullptr;
+  struct Open {
+    cudaStream_t st;
+    int kc;
+    cudaEvent_t ev;
+  };
+  std::vector<Open> open;  // one open interval per stream (the wave forks the triangulation)
   cudaEvent_t get() {
     if (!pool.empty()) {
       cudaEvent_t e = pool.back();
@@ -290,17 +294,27 @@ Profiler g_prof;
 
 void prof_begin(int kc, cudaStream_t st) {
   if (!g_prof.on) return;
-  g_prof.open_kc = kc;
-  g_prof.open_ev = g_prof.get();
-  cudaEventRecord(g_prof.open_ev, st);
+  cudaEvent_t a = g_prof.get();
+  cudaEventRecord(a, st);
+  for (auto& o : g_prof.open)
+    if (o.st == st) {
+      o.kc = kc;
+      o.ev = a;
+      return;
+    }
+  g_prof.open.push_back({st, kc, a});
 }
 
 void prof_end(cudaStream_t st) {
-  if (!g_prof.on || g_prof.open_kc < 0) return;
-  cudaEvent_t b = g_prof.get();
-  cudaEventRecord(b, st);
-  g_prof.recs.push_back({g_prof.open_kc, g_prof.open_ev, b});
-  g_prof.open_kc = -1;
+  if (!g_prof.on) return;
+  for (size_t i = 0; i < g_prof.open.size(); ++i)
+    if (g_prof.open[i].st == st) {
+      cudaEvent_t b = g_prof.get();
+      cudaEventRecord(b, st);
+      g_prof.recs.push_back({g_prof.open[i].kc, g_prof.open[i].ev, b});
+      g_prof.open.erase(g_prof.open.begin() + i);
+      return;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -623,6 +637,7 @@ int vc_profile(int on) {
     g_prof.pool.push_back(r.b);
   }
   g_prof.recs.clear();
+  g_prof.open.clear();
   g_prof.on = on != 0;
   return VC_OK;
 }

@@ -18,6 +18,7 @@
 #include <type_traits>
 #include <cstdio>
 #include <vector>
+#include <mutex>
 
 #include "vc_device.cuh"
 #include "vc_eigen.cuh"
@@ -3043,6 +3044,42 @@ static size_t stack_smem(K kernel, const DevBvh& H) {
   return bytes;
 }
 
+// Off: forking the triangulation beside the gather chain gave 36.25 ms (side stream at the
+// greatest priority) vs 36.56 ms per 2048 records — both chains fill the SMs on their own —
+// and overlapped kernels make the per-class event times (the roofline's denominators)
+// meaningless.
+#ifndef VC_WAVE_FORK
+#define VC_WAVE_FORK 0
+#endif
+#ifndef VC_FORK_PRIO
+#define VC_FORK_PRIO 0  // side-stream priority: 0 default, 1 the greatest
+#endif
+// One side stream per device, created on first use; fork/join events are per call, so
+// concurrent callers (on their own streams) cannot pick up each other's fork points.
+static cudaStream_t side_stream() {
+  static cudaStream_t per_dev[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  cudaStream_t& s = per_dev[dev & 63];
+  if (!s) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, VC_FORK_PRIO ? hi : lo);
+  }
+  return s;
+}
+
+// a waits for everything enqueued on b so far
+static void stream_after(cudaStream_t a, cudaStream_t b) {
+  cudaEvent_t e;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEventRecord(e, b);
+  cudaStreamWaitEvent(a, e, 0);
+  cudaEventDestroy(e);  // released once recorded work completes
+}
+
 template <int D>
 static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W, const JumpTables& jt,
                           int* own, int* own_cnt, int sm_count, cudaStream_t st, KernelCounter* kc) {
@@ -3059,13 +3096,119 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
     k_primary<D, false><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, false>, S.geo), st>>>(S, P, W, jt);
   }
   prof_end(st);
+  int nl = 3;
+  // Spherical Delaunay (depends only on the directions): on a forked side stream it runs
+  // beside the rings + gather chain (VC_WAVE_FORK).
+  auto triangulate = [&](cudaStream_t ts) {
+  if constexpr (D == 3) {
+    cudaMemsetAsync(W.tri_status, 0, sizeof(int) * W.B, ts);
+    if (!P.host_adjacency) {
+      static bool smem_attr = false;
+      if (!smem_attr) {
+        cudaFuncSetAttribute(k_delaunay_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
+        cudaFuncSetAttribute(k_delaunay_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
+        cudaFuncSetAttribute(k_delaunay_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kHullBS * (kHullSlots * sizeof(float2) + kHullH)));
+        cudaFuncSetAttribute(k_delaunay_cap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
+        cudaFuncSetAttribute(k_delaunay_capg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
+        cudaFuncSetAttribute(k_delaunay_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWarpSmem);
+        smem_attr = true;
+      }
+      prof_begin(KC_DELAUNAY, ts);
+      cudaMemsetAsync(W.del_retry_count, 0, sizeof(unsigned int), ts);
+      if (P.del_kmax > 0) {
+        // stratum-window hulls for most cells, the cap kernel for the polar rows, clipping
+        // for the cells either hands back
+        cudaMemsetAsync(W.del_fb_count, 0, sizeof(unsigned int), ts);
+        for (int k = 0; k < 3; ++k) {
+          const int nr = P.del_cls[k + 1] - P.del_cls[k];
+          if (!nr) continue;
+          const size_t smem = (size_t)kHullBS * ((P.del_cls_k[k] + 1) * sizeof(float2) + kHullH);
+          k_delaunay_hull<<<grid_for((long long)W.B * nr * P.cols, kHullBS), kHullBS, smem, ts>>>(P, W, own,
+                                                                                                 own_cnt, k);
+          ++nl;
+        }
+        if (P.del_cls[3] + (P.del_cap ? 2 : 0) < P.rows) {
+          k_delaunay_rest<<<grid_for(nt, 256), 256, 0, ts>>>(P, W);
+          ++nl;
+        }
+        if (P.del_cap) {
+          CapGrid cg;
+          if (cap_grid(P, cg)) {
+            k_cap_bin<<<2 * W.B, kCapGBS, kCapBinSmem, ts>>>(P, W, cg);
+            k_delaunay_capg<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, ts>>>(P, W, own, own_cnt, cg);
+            ++nl;
+          } else {
+            k_delaunay_cap<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, ts>>>(P, W, own, own_cnt);
+          }
+          ++nl;
+        }
+        if (getenv("VOLCACHE_DEL_STATS")) {  // debug: cells handed to the clipping kernel
+          unsigned c = 0;
+          cudaMemcpyAsync(&c, W.del_fb_count, 4, cudaMemcpyDeviceToHost, ts);
+          cudaStreamSynchronize(ts);
+          fprintf(stderr, "[volcache] hull fallback cells: %u of %lld\n", c, nt);
+          if (getenv("VOLCACHE_DEL_STATS")[0] == '3') {  // handed-back cells per stratum row
+            std::vector<int> l(c), hist(P.rows, 0);
+            cudaMemcpy(l.data(), W.del_fb, (size_t)c * 4, cudaMemcpyDeviceToHost);
+            for (int g : l) ++hist[(g % P.n_angular) / P.cols];
+            for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
+            fprintf(stderr, "\n");
+          }
+          if (getenv("VOLCACHE_DEL_STATS")[0] >= '2') {
+            k_delaunay_warp<<<sm_count * 4, kWarpBS, kWarpSmem, ts>>>(P, W, own, own_cnt);
+            cudaMemcpyAsync(&c, W.del_fb2_count, 4, cudaMemcpyDeviceToHost, ts);
+            cudaStreamSynchronize(ts);
+            fprintf(stderr, "[volcache] after the float64 wrap: %u\n", c);
+            std::vector<int> l(c), hist(P.rows, 0);
+            cudaMemcpy(l.data(), W.del_fb2, (size_t)c * 4, cudaMemcpyDeviceToHost);
+            for (int g : l) ++hist[(g % P.n_angular) / P.cols];
+            for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
+            fprintf(stderr, "\n");
+            for (unsigned t = 0; t < c && t < 8; ++t)
+              fprintf(stderr, "[volcache] clipping cell: record %d direction %d\n", l[t] / P.n_angular, l[t] % P.n_angular);
+          }
+        }
+        cudaMemsetAsync(W.del_fb2_count, 0, sizeof(unsigned int), ts);
+        k_delaunay_warp<<<sm_count * 4, kWarpBS, kWarpSmem, ts>>>(P, W, own, own_cnt);
+        k_delaunay_list<<<sm_count * VC_LB_DEL2, kDelBS, kDelSmem, ts>>>(P, W, own, own_cnt);
+        nl += 2;
+      } else {
+        k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, ts>>>(P, W, own, own_cnt);
+        ++nl;
+      }
+      k_delaunay_retry<<<sm_count * 2, 128, 0, ts>>>(P, W, own, own_cnt, W.del_scratch);
+      ++nl;
+      prof_end(ts);
+      prof_begin(KC_COMPACT, ts);
+  // W.del_fb (B × n ints) is free once the Delaunay kernels are done: the offsets
+  k_own_scan<<<W.B, kCompactBS, 0, ts>>>(P, W, own_cnt, W.del_fb);
+  k_tri_scatter<<<grid_for(nt, 256), 256, 0, ts>>>(P, W, own, own_cnt, W.del_fb);
+  ++nl;
+  prof_end(ts);
+      nl += 2;
+    } else {
+      cudaMemsetAsync(W.deg, 0, sizeof(int) * nt, ts);
+      prof_begin(KC_DEGREE, ts);
+  k_degree<<<grid_for((long long)W.B * P.n_tris, 256), 256, 0, ts>>>(P, W);
+  prof_end(ts);
+      ++nl;
+    }
+  }
+  };
+  const bool fork = VC_WAVE_FORK && D == 3;
+  cudaStream_t side = nullptr;
+  if (fork) {
+    side = side_stream();
+    stream_after(side, st);
+    triangulate(side);
+  }
   prof_begin(KC_RINGS, st);
   k_rings<<<W.B, kRingBS, 0, st>>>(P, W);
   prof_end(st);
   prof_begin(KC_WAVESCAN, st);
   k_wave_scan<<<1, 1024, 0, st>>>(W, S.sigma_s > 0.0 ? 1 : 0);
   prof_end(st);
-  int nl = 3;
   // live-sample masks are set by the gather itself (mark_live)
   cudaMemsetAsync(W.live, 0, sizeof(unsigned long long) * (size_t)W.live_words * nt, st);
   if (S.sigma_s > 0.0) {
@@ -3100,100 +3243,10 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
     }
     prof_end(st);
   }
-  if constexpr (D == 3) {
-    cudaMemsetAsync(W.tri_status, 0, sizeof(int) * W.B, st);
-    if (!P.host_adjacency) {
-      static bool smem_attr = false;
-      if (!smem_attr) {
-        cudaFuncSetAttribute(k_delaunay_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
-        cudaFuncSetAttribute(k_delaunay_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDelSmem);
-        cudaFuncSetAttribute(k_delaunay_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kHullBS * (kHullSlots * sizeof(float2) + kHullH)));
-        cudaFuncSetAttribute(k_delaunay_cap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
-        cudaFuncSetAttribute(k_delaunay_capg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCapSmem);
-        cudaFuncSetAttribute(k_delaunay_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWarpSmem);
-        smem_attr = true;
-      }
-      prof_begin(KC_DELAUNAY, st);
-      cudaMemsetAsync(W.del_retry_count, 0, sizeof(unsigned int), st);
-      if (P.del_kmax > 0) {
-        // stratum-window hulls for most cells, the cap kernel for the polar rows, clipping
-        // for the cells either hands back
-        cudaMemsetAsync(W.del_fb_count, 0, sizeof(unsigned int), st);
-        for (int k = 0; k < 3; ++k) {
-          const int nr = P.del_cls[k + 1] - P.del_cls[k];
-          if (!nr) continue;
-          const size_t smem = (size_t)kHullBS * ((P.del_cls_k[k] + 1) * sizeof(float2) + kHullH);
-          k_delaunay_hull<<<grid_for((long long)W.B * nr * P.cols, kHullBS), kHullBS, smem, st>>>(P, W, own,
-                                                                                                 own_cnt, k);
-          ++nl;
-        }
-        if (P.del_cls[3] + (P.del_cap ? 2 : 0) < P.rows) {
-          k_delaunay_rest<<<grid_for(nt, 256), 256, 0, st>>>(P, W);
-          ++nl;
-        }
-        if (P.del_cap) {
-          CapGrid cg;
-          if (cap_grid(P, cg)) {
-            k_cap_bin<<<2 * W.B, kCapGBS, kCapBinSmem, st>>>(P, W, cg);
-            k_delaunay_capg<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt, cg);
-            ++nl;
-          } else {
-            k_delaunay_cap<<<grid_for(2LL * W.B * P.cols, kHullBS), kHullBS, kCapSmem, st>>>(P, W, own, own_cnt);
-          }
-          ++nl;
-        }
-        if (getenv("VOLCACHE_DEL_STATS")) {  // debug: cells handed to the clipping kernel
-          unsigned c = 0;
-          cudaMemcpyAsync(&c, W.del_fb_count, 4, cudaMemcpyDeviceToHost, st);
-          cudaStreamSynchronize(st);
-          fprintf(stderr, "[volcache] hull fallback cells: %u of %lld\n", c, nt);
-          if (getenv("VOLCACHE_DEL_STATS")[0] == '3') {  // handed-back cells per stratum row
-            std::vector<int> l(c), hist(P.rows, 0);
-            cudaMemcpy(l.data(), W.del_fb, (size_t)c * 4, cudaMemcpyDeviceToHost);
-            for (int g : l) ++hist[(g % P.n_angular) / P.cols];
-            for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
-            fprintf(stderr, "\n");
-          }
-          if (getenv("VOLCACHE_DEL_STATS")[0] >= '2') {
-            k_delaunay_warp<<<sm_count * 4, kWarpBS, kWarpSmem, st>>>(P, W, own, own_cnt);
-            cudaMemcpyAsync(&c, W.del_fb2_count, 4, cudaMemcpyDeviceToHost, st);
-            cudaStreamSynchronize(st);
-            fprintf(stderr, "[volcache] after the float64 wrap: %u\n", c);
-            std::vector<int> l(c), hist(P.rows, 0);
-            cudaMemcpy(l.data(), W.del_fb2, (size_t)c * 4, cudaMemcpyDeviceToHost);
-            for (int g : l) ++hist[(g % P.n_angular) / P.cols];
-            for (int r = 0; r < P.rows; ++r) fprintf(stderr, "%d:%d ", r, hist[r]);
-            fprintf(stderr, "\n");
-            for (unsigned t = 0; t < c && t < 8; ++t)
-              fprintf(stderr, "[volcache] clipping cell: record %d direction %d\n", l[t] / P.n_angular, l[t] % P.n_angular);
-          }
-        }
-        cudaMemsetAsync(W.del_fb2_count, 0, sizeof(unsigned int), st);
-        k_delaunay_warp<<<sm_count * 4, kWarpBS, kWarpSmem, st>>>(P, W, own, own_cnt);
-        k_delaunay_list<<<sm_count * VC_LB_DEL2, kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
-        nl += 2;
-      } else {
-        k_delaunay_smem<<<grid_for(nt, kDelBS), kDelBS, kDelSmem, st>>>(P, W, own, own_cnt);
-        ++nl;
-      }
-      k_delaunay_retry<<<sm_count * 2, 128, 0, st>>>(P, W, own, own_cnt, W.del_scratch);
-      ++nl;
-      prof_end(st);
-      prof_begin(KC_COMPACT, st);
-  // W.del_fb (B × n ints) is free once the Delaunay kernels are done: the offsets
-  k_own_scan<<<W.B, kCompactBS, 0, st>>>(P, W, own_cnt, W.del_fb);
-  k_tri_scatter<<<grid_for(nt, 256), 256, 0, st>>>(P, W, own, own_cnt, W.del_fb);
-  ++nl;
-  prof_end(st);
-      nl += 2;
-    } else {
-      cudaMemsetAsync(W.deg, 0, sizeof(int) * nt, st);
-      prof_begin(KC_DEGREE, st);
-  k_degree<<<grid_for((long long)W.B * P.n_tris, 256), 256, 0, st>>>(P, W);
-  prof_end(st);
-      ++nl;
-    }
+  if (fork) {  // join: the assembly needs both the media and the triangles
+    stream_after(st, side);
+  } else {
+    triangulate(st);
   }
   prof_begin(KC_ASSEMBLE, st);
 

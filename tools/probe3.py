@@ -11,7 +11,16 @@ X = torch.tensor(w.points[idx], device="cuda")
 S = torch.tensor(seed_words(w.seed, 401, idx).astype(np.int32), device="cuda")
 kw = dict(n_angular=w.n_angular, march_step=w.march_step, epsilon=0.05)
 r = estimate_moments_batch(w.scene, X, seeds=S, **kw); torch.cuda.synchronize()
-L = _lib.lib(); L.vc_profile(1)
+L = _lib.lib()
+if "noprof" in sys.argv:  # device time of 5 batches without the per-class events
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        r = estimate_moments_batch(w.scene, X, seeds=S, **kw)
+    e1.record(); torch.cuda.synchronize()
+    print(json.dumps({"B": B, "noprof_ms": round(e0.elapsed_time(e1) / 5, 3), "rec_per_s": round(5000 * B / e0.elapsed_time(e1), 1)}))
+    sys.exit(0)
+L.vc_profile(1)
 t = time.perf_counter()
 r = estimate_moments_batch(w.scene, X, seeds=S, **kw); torch.cuda.synchronize()
 dt = time.perf_counter() - t
