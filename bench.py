@@ -553,7 +553,11 @@ def main():
     }  # SURVEY.md §8d's W; the triangulation has no flop term there — it is rated on issue below
     names = _lib.KERNEL_CLASSES
     shares = {names[i]: float(kms[i]) for i in range(12) if kcnt[i] > 0}
-    dom = max(shares, key=shares.get)
+    # the roofline's kernel is the largest class SURVEY §8d's W has a term for; the triangulation
+    # (no flop term in W, ~equal in time to the gather) is rated on its issue rate in per_kernel
+    # and named in "largest_by_time" when it leads
+    top = max(shares, key=shares.get)
+    dom = max((k for k in shares if k in work), key=shares.get)
     dom_i = names.index(dom)
     launches_dom = int(kcnt[dom_i])
     avg_ms = float(kms[dom_i]) / max(launches_dom, 1)
@@ -596,6 +600,8 @@ def main():
                 "peak_source": f"148 SMs x 128 FP32 lanes x 2 x sm_max_mhz ({pk['source']} clocks)",
                 "kernel_ms_share": {k: round(v / sum(shares.values()), 4) for k, v in shares.items()},
                 "algorithmic_flops_per_launch": flops_per_launch,
+                "largest_by_time": {"kernel": top, "ms": shares[top],
+                                    "issue_frac": per_kernel.get(top, {}).get("issue_frac")},
                 "per_kernel": per_kernel,
                 "path": {"algorithmic_flops_per_record": w_path / nrec, "achieved": path_achieved,
                          "frac": path_achieved / pk["fp32_tflops"]}}
