@@ -127,6 +127,15 @@ def workload(args):
 
             tag = (f"+hg{g:g}" if g != 0.0 else "") + (f"+{B}-bounce-media" if B > 1 else "")
             w = dataclasses.replace(w, name=f"{w.name}{tag}", media_bounces=B, hg_g=g)
+        lights = getattr(args, "lights", "none")
+        if lights != "none":  # extension: delta lights (sun = BASELINE cfg3's directional light through
+            import dataclasses  # open window cut-outs; lamp = a point light inside the portal room)
+
+            from paper_1805_09258_b200.scene import point_light
+
+            sc = (configs.cfg3_spec_scene() if lights == "sun" else
+                  configs.cfg3_scene(lights=[point_light((2.6, 2.2, 1.4), (6.0, 5.0, 4.0))]))
+            w = dataclasses.replace(w, name=f"{w.name}+{lights}", scene=sc)
         return w
     if args.config == "cfg2":
         return configs.cfg2(march_step=args.march_step or 4.0)
@@ -423,6 +432,8 @@ def main():
                     help="cfg3 extension: media events per gather path (1 = the reference's estimator)")
     ap.add_argument("--hg-g", type=float, default=0.0,
                     help="cfg3 extension: Henyey-Greenstein g of the media scattering events (0 = the reference)")
+    ap.add_argument("--lights", default="none", choices=["none", "sun", "lamp"],
+                    help="cfg3 extension: delta lights (sun: open windows + directional light; lamp: point light)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e timed steps (default: --steps)")
     ap.add_argument("--cfg5-eps", type=float, default=None, help="cfg5: record-error target ε (default tuned)")

@@ -63,6 +63,16 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
                     const double* albedo, const double* bounds_min, const double* bounds_max,
                     double sigma_s, double sigma_a, vc_scene** out);
 void vc_scene_destroy(vc_scene* scene);
+/* Extension (no reference counterpart: the reference has area emitters only, SPEC.md:149;
+ * BASELINE.json cfg1/cfg2/cfg4 name point lights, cfg3 a directional light).  Delta lights of
+ * the scene, n_lights × 8 doubles in host memory: kind (0 = point, 1 = directional), v[3]
+ * (position, or the unit vector pointing toward the light; 2D uses v[0..1]), rgb (radiant
+ * intensity, or irradiance on a plane facing the light), 0.  They light reflective surfaces
+ * (same cosine and normalisation as direct_lighting, src/transport.py:175-225), every media
+ * sample of a record (σs × mean incident radiance, beside mean_surface_gather,
+ * src/transport.py:288-310) and the cache point itself (closed-form value, gradient and
+ * Hessian with the point visibility held constant).  Call before building records; 0 clears. */
+int vc_scene_set_lights(vc_scene* scene, int n_lights, const double* rows);
 /* Scratch budget for one record wave (bytes; default a third of device memory, ≤ 64 GiB). */
 int vc_scene_set_budget(vc_scene* scene, int64_t bytes);
 

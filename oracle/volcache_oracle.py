@@ -59,6 +59,10 @@ class PackedScene:
     bmax: np.ndarray
     sigma_s: float
     sigma_a: float
+    # extension (not in the reference): delta lights, rows (kind, v0, v1, v2, r, g, b, 0) —
+    # kind 0 = point light at v with radiant intensity rgb, kind 1 = directional light whose
+    # unit vector v points TOWARD the light, with irradiance rgb on a plane facing it
+    lights: np.ndarray = field(default_factory=lambda: np.zeros((0, 8)))
     # derived (+ cached flat primitive array for the C helper)
     _prim: np.ndarray = field(init=False, default=None, repr=False)
     a: np.ndarray = field(init=False)
@@ -124,6 +128,7 @@ def pack(scene) -> PackedScene:
         np.asarray(scene.bounds_max, float),
         float(scene.medium.sigma_s),
         float(scene.medium.sigma_a),
+        np.asarray(getattr(scene, "lights", np.zeros((0, 8))), float).reshape(-1, 8),
     )
 
 
@@ -372,6 +377,104 @@ def emitter_quadrature(ps: PackedScene, n_per: int):
     return out
 
 
+def delta_incident(ps: PackedScene, org):
+    """Extension (BASELINE.json cfg1/cfg2/cfg4 point lights, cfg3 directional light; the
+    reference has area emitters only): per delta light the unit direction d toward
+    it from each origin, its unoccluded attenuated geometric term and its rgb strength.
+    Point light at P: r = |P − o|, term e^{−σt r} / max(r, 1e-6·scale)^{dim−1}, visible iff the
+    nearest hit along d is at t ≥ r(1 − 1e-6) (the reference's shadow-ray rule,
+    src/transport.py:213-214); r ≤ 1e-6·scale → 0.  Directional light: the ray must leave
+    the scene without a hit (the light is outside the bounds), term e^{−σt s_b} with s_b the
+    distance to the bounds exit along d (src/scene.py:295-303)."""
+    org = np.atleast_2d(org)
+    m, dim = org.shape
+    off = 1e-6 * ps.scale
+    out = []
+    for row in ps.lights:
+        kind, v, I = int(row[0]), row[1:1 + dim], row[4:7]
+        val = np.zeros(m)
+        if kind == 0:
+            to = v[None] - org
+            r = np.linalg.norm(to, axis=1)
+            ok = r > off
+            d = np.zeros_like(to)
+            d[ok] = to[ok] / r[ok, None]
+            if np.any(ok):
+                th, _ = trace(ps, org[ok], d[ok])
+                vis = th >= r[ok] * (1.0 - 1e-6)
+                ii = np.flatnonzero(ok)[vis]
+                val[ii] = np.exp(-ps.sigma_t * r[ii]) / np.maximum(r[ii], off) ** (dim - 1)
+        else:
+            d = np.broadcast_to(v, (m, dim)).copy()
+            th, _ = trace(ps, org, d)
+            vis = ~np.isfinite(th)
+            if np.any(vis):
+                val[vis] = np.exp(-ps.sigma_t * bounds_exit(ps, org[vis], d[vis]))
+        out.append((d, val, I))
+    return out
+
+
+def delta_inscatter(ps: PackedScene, pts, g=0.0, toward=None):
+    """Extension: mean incident radiance over the sphere (circle) at media points from the
+    delta lights, Σ_l term_l·I_l / 4π (2π in 2D) — the quantity mean_surface_gather estimates
+    for surfaces (src/transport.py:288-310).  g ≠ 0: each light is weighted 4π·p_g(d_l·toward),
+    `toward` (m, 3) = the unit direction pointing AWAY from where the scattered light goes."""
+    pts = np.atleast_2d(pts)
+    out = np.zeros((pts.shape[0], 3))
+    norm = 4.0 * np.pi if ps.dim == 3 else 2.0 * np.pi
+    for d, val, I in delta_incident(ps, pts):
+        w = val / norm
+        if g != 0.0:
+            w = w * (4.0 * np.pi * hg_phase(g, (d * toward).sum(axis=1)))
+        out += w[:, None] * I[None]
+    return out
+
+
+def delta_single(ps: PackedScene, x):
+    """Extension: the delta lights' own single scattering at the cache point x, in the units of
+    the single moments (f̄ × mean incident radiance): value, gradient and Hessian of
+    f̄·I·φ(x)/4π (2π in 2D) with the visibility V(x) held constant (a point visibility has no
+    occlusion-aware derivative; the occlusion-aware terms of the method enter through the
+    lit surfaces and media samples of the subdivision).  Point light: φ = e^{−σt r} r^{−k},
+    k = dim − 1: φ′ = −(σt + k/r)φ, φ″ = ((σt + k/r)² + k/r²)φ, ∇φ = φ′u, Hφ = φ″uuᵀ + φ′/r(I − uuᵀ),
+    u = (x − P)/r.  Directional light: φ = e^{−σt s_b}, s_b = (b_a − x_a)/d_a on the exit face a:
+    ∇φ = σt φ e_a/d_a, Hφ = σt² φ e_a e_aᵀ/d_a²."""
+    x = np.asarray(x, float)
+    dim = x.size
+    L, G, H = np.zeros(3), np.zeros((3, dim)), np.zeros((3, dim, dim))
+    fbar = ps.sigma_s / (2.0 * np.pi if dim == 2 else 4.0 * np.pi)
+    norm = 4.0 * np.pi if dim == 3 else 2.0 * np.pi
+    sig, k = ps.sigma_t, dim - 1
+    for row, (d, val, I) in zip(ps.lights, delta_incident(ps, x[None])):
+        if not val[0] > 0.0:
+            continue
+        phi = val[0]
+        if int(row[0]) == 0:
+            w = x - row[1:1 + dim]
+            r = float(np.linalg.norm(w))
+            u = w / r
+            a = sig + k / r
+            d1 = -a * phi
+            d2 = (a * a + k / (r * r)) * phi
+            g = d1 * u
+            h = d2 * np.outer(u, u) + d1 / r * (np.eye(dim) - np.outer(u, u))
+        else:
+            dv = d[0]
+            with np.errstate(divide="ignore", invalid="ignore"):
+                t = np.maximum((ps.bmin - x) / dv, (ps.bmax - x) / dv)
+            t = np.where(np.isnan(t), np.inf, t)
+            a = int(np.argmin(t))
+            e = np.zeros(dim)
+            e[a] = 1.0 / dv[a]
+            g = sig * phi * e
+            h = sig * sig * phi * np.outer(e, e)
+        c = fbar / norm
+        L += c * phi * I
+        G += c * I[:, None] * g[None]
+        H += c * I[:, None, None] * h[None]
+    return L, G, H
+
+
 def direct_light(ps: PackedScene, points, normals, n_light: int):
     """Shadow-ray quadrature of direct light; ÷π (3D) or ÷2 (2D).  src/transport.py:175-225."""
     points = np.atleast_2d(points)
@@ -379,10 +482,13 @@ def direct_light(ps: PackedScene, points, normals, n_light: int):
     m = points.shape[0]
     acc = np.zeros((m, 3))
     quad = emitter_quadrature(ps, n_light)
-    if not quad:
+    if not quad and not len(ps.lights):
         return acc
     off = 1e-6 * ps.scale
     org = points + off * normals
+    for d, val, I in delta_incident(ps, org):  # extension: delta lights, same cosine and ÷π / ÷2
+        cp = np.clip(np.einsum("md,md->m", normals, d), 0.0, None)
+        acc += (cp * val)[:, None] * I[None]
     for pts, wts, E, N in quad:
         for j in range(pts.shape[0]):
             to = pts[j][None] - org
@@ -503,6 +609,8 @@ def gather_mean_bounces(ps, points, dirs_pp, n_light, extras, bounces, g=0.0, x=
             s2[col], idx2 = trace_or_bounds(ps, pos[col], nd[col])
             lo2 = surface_radiance(ps, idx2, pos[col] + s2[col, None] * nd[col], nd[col], n_light)
             tot[col] += w[col, None] * np.exp(-ps.sigma_t * s2[col])[:, None] * lo2
+            if len(ps.lights):  # extension: the delta lights scattered at this collision toward −cur_d
+                tot[col] += w[col, None] * delta_inscatter(ps, pos[col], g, cur_d[col])
             alive = col
             cur_d = nd
             cur_s = s2
@@ -684,6 +792,10 @@ def build_record(
                                                                             media_bounces, hg_g, x)
         else:
             media_rad.reshape(-1, 3)[flat] = ps.sigma_s * gather_mean(ps, p, gd, n_light_samples)
+        if len(ps.lights):  # extension: the delta lights' in-scatter at every media sample
+            dx = p - x[None]
+            wk = dx / np.sqrt((dx * dx).sum(axis=1))[:, None]
+            media_rad.reshape(-1, 3)[flat] += ps.sigma_s * delta_inscatter(ps, p, hg_g, wk)
 
     fbar = ps.sigma_s / (2.0 * np.pi if dim == 2 else 4.0 * np.pi)
     sig = ps.sigma_t
@@ -750,6 +862,11 @@ def build_record(
     ring("surface", hit_pts, lo_surf, s, 1.0)
 
     acc_h = 0.5 * (acc_h + np.swapaxes(acc_h, -1, -2))
+    if len(ps.lights):  # extension: the delta lights' single scattering at x itself
+        dL, dG, dH = delta_single(ps, x)
+        acc_L[0] += dL
+        acc_g[0] += dG
+        acc_h[0] += dH
     stats = {
         "elements_evaluated": n_eval,
         "elements_dropped": n_drop,

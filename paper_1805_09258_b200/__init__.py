@@ -26,7 +26,7 @@ from .records import (
 from .io import (CACHE_FORMAT, CACHE_VERSION, BaselineRecord, CacheFormatError, load_cache, load_cache_npz, read_pfm,
                  save_cache, save_cache_npz, write_pfm, write_ppm)
 from .renderer import (CACHE_MODES, MODES, CacheSet, Camera, FieldGrid, RenderSettings, populate_cache, render)
-from .scene import Medium, Scene, Surface, load_scene, save_scene
+from .scene import Medium, Scene, Surface, directional_light, load_scene, point_light, save_scene
 from . import baseline, path  # noqa: E402  (submodules: b200.baseline.*, b200.path.*)
 from .baseline import (BaselineEstimate, baseline_estimate, log_gradient_radius, log_space_interpolate,
                        make_baseline_record, occlusion_unaware_gradient)

@@ -141,6 +141,7 @@ _SIGS = {
                                   C.POINTER(_vp)]),
     "vc_scene_destroy": (None, [_vp]),
     "vc_scene_set_budget": (C.c_int, [_vp, C.c_int64]),
+    "vc_scene_set_lights": (C.c_int, [_vp, C.c_int, _vp]),
     "vc_build_records": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.POINTER(BuildParams), _vp, _vp, _vp, _vp]),
     "vc_build_inspect": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(BuildParams), _vp, _vp, _vp, _vp, _vp, _vp,
                                    C.c_int64, _vp, _vp, _vp]),

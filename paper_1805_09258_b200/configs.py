@@ -17,7 +17,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .scene import Medium, Scene, Surface
+from .scene import Medium, Scene, Surface, directional_light, point_light
 
 
 @dataclass(frozen=True)
@@ -117,6 +117,14 @@ def cfg1_scene() -> Scene:
     return Scene(tuple(light + occ), Medium(0.5, 0.1), np.zeros(2), np.ones(2))
 
 
+def cfg1_spec_scene(occluder_albedo: float = 0.0) -> Scene:
+    """Extension: cfg1 as BASELINE.json states it — a point light (intensity 1) instead of the
+    emissive square (delta lights are not in the reference)."""
+    occ = _rect_2d(0.4, 0.45, 0.6, 0.55, albedo=occluder_albedo)
+    return Scene(tuple(occ), Medium(0.5, 0.1), np.zeros(2), np.ones(2),
+                 lights=np.array([point_light((0.2, 0.8), 1.0)]))
+
+
 def cfg1(n_points: int = 256, march_step: float = 4.0) -> Workload:
     sc = cfg1_scene()
     pts = np.random.default_rng(0).uniform(sc.bounds_min, sc.bounds_max, (n_points, 2))
@@ -137,6 +145,14 @@ def cfg2_scene() -> Scene:
     return Scene(tuple(light + cube), Medium(0.8, 0.2), np.zeros(3), np.ones(3))
 
 
+def cfg2_spec_scene() -> Scene:
+    """Extension: cfg2 as BASELINE.json states it — an isotropic point light at (0.5, 0.95, 0.5)
+    (used with hg_g = 0.3)."""
+    cube = _box_3d((0.5, 0.6, 0.5), 0.2)
+    return Scene(tuple(cube), Medium(0.8, 0.2), np.zeros(3), np.ones(3),
+                 lights=np.array([point_light((0.5, 0.95, 0.5), 1.0)]))
+
+
 def cfg2(n_points: int = 4096, march_step: float = 4.0) -> Workload:
     sc = cfg2_scene()
     pts = np.random.default_rng(1).uniform(sc.bounds_min, sc.bounds_max, (n_points, 3))
@@ -151,8 +167,13 @@ ROOM = np.array([4.0, 3.0, 4.0])
 WINDOW_EMISSION = np.array([20.0, 19.0, 17.0])
 
 
-def _window_wall(emission):
-    """Wall x = 0 tiled by a cut grid; the 8 window cells (2 rows × 4) are emissive portals."""
+SUN_TOWARD = np.array([-1.0, 0.55, 0.2])  # cfg3-spec: from the room toward the distant light
+SUN_IRRADIANCE = np.array([20.0, 19.0, 17.0])
+
+
+def _window_wall(emission, open_windows=False):
+    """Wall x = 0 tiled by a cut grid; the 8 window cells (2 rows × 4) are emissive portals
+    (or, open_windows, cut-outs a directional light shines through)."""
     zc = [0.6, 1.53, 2.47, 3.4]
     yc = [1.0, 2.1]
     hw, hh = 0.3, 0.35
@@ -164,14 +185,20 @@ def _window_wall(emission):
             z0, z1, y0, y1 = zs[i], zs[i + 1], ys[j], ys[j + 1]
             zm, ym = 0.5 * (z0 + z1), 0.5 * (y0 + y1)
             win = any(abs(zm - z) < hw for z in zc) and any(abs(ym - y) < hh for y in yc)
+            if win and open_windows:
+                continue
             out += _quad((0, y0, z0), (0, y0, z1), (0, y1, z1), (0, y1, z0),
                          emission=emission if win else 0.0)
     return out
 
 
-def cfg3_scene(n_spheres: int = 40, level: int = 3, seed: int = 2, wall_albedo: float = 0.0) -> Scene:
+def cfg3_scene(n_spheres: int = 40, level: int = 3, seed: int = 2, wall_albedo: float = 0.0,
+               open_windows: bool = False, lights=()) -> Scene:
+    """open_windows / lights: the delta-light extension (cfg3 as BASELINE.json states it: window
+    cut-outs lit by a distant directional light); the default is the reference-runnable parity
+    variant with emissive portals."""
     X, Y, Z = ROOM
-    walls = _window_wall(WINDOW_EMISSION)
+    walls = _window_wall(WINDOW_EMISSION, open_windows)
     walls += _quad((X, 0, 0), (X, 3, 0), (X, 3, Z), (X, 0, Z), albedo=wall_albedo)  # far side
     walls += _quad((0, 0, 0), (X, 0, 0), (X, 0, Z), (0, 0, Z), albedo=wall_albedo)  # floor
     walls += _quad((0, Y, 0), (0, Y, Z), (X, Y, Z), (X, Y, 0), albedo=wall_albedo)  # ceiling
@@ -185,7 +212,15 @@ def cfg3_scene(n_spheres: int = 40, level: int = 3, seed: int = 2, wall_albedo: 
         r = rng.uniform(0.12, 0.3)
         P = c[None] + r * V
         spheres += [_tri(P[a], P[b], P[d]) for a, b, d in F]
-    return Scene(tuple(walls + spheres), Medium(0.27, 0.03), np.zeros(3), ROOM.copy())
+    return Scene(tuple(walls + spheres), Medium(0.27, 0.03), np.zeros(3), ROOM.copy(),
+                 lights=np.asarray(lights, float).reshape(-1, 8))
+
+
+def cfg3_spec_scene(n_spheres: int = 40, level: int = 3, wall_albedo: float = 0.0) -> Scene:
+    """Extension: cfg3 as BASELINE.json states it — open window cut-outs and a distant
+    directional light (used with hg_g = 0.5 and media_bounces = 4)."""
+    return cfg3_scene(n_spheres, level, wall_albedo=wall_albedo, open_windows=True,
+                      lights=[directional_light(SUN_TOWARD, SUN_IRRADIANCE)])
 
 
 def cfg3(n_points: int = 19000, n_spheres: int = 40, level: int = 3, n_angular: int = 16384,

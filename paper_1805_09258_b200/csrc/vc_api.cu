@@ -256,6 +256,8 @@ DevScene dev_scene(const vc_scene* sc) {
   S.es_pos = sc->d_es_pos;
   S.es_w = sc->d_es_w;
   S.es_surf = sc->d_es_surf;
+  S.n_lights = sc->n_lights;
+  S.lights = sc->d_lights;
   return S;
 }
 
@@ -993,6 +995,29 @@ int vc_scene_create(int dim, int n_surfaces, const double* vertices, const doubl
 }
 
 void vc_scene_destroy(vc_scene* sc) { delete sc; }
+
+int vc_scene_set_lights(vc_scene* sc, int n_lights, const double* rows) {
+  if (!sc || n_lights < 0 || (n_lights > 0 && !rows)) return fail(VC_EINVAL, "invalid lights");
+  for (int l = 0; l < n_lights; ++l) {
+    const double* r = rows + 8 * (size_t)l;
+    if (!(r[0] == 0.0 || r[0] == 1.0)) return fail(VC_EINVAL, "light kind must be 0 (point) or 1 (directional)");
+    if (!(r[4] >= 0.0 && r[5] >= 0.0 && r[6] >= 0.0)) return fail(VC_EINVAL, "light strength must be non-negative");
+    if (r[0] == 1.0) {
+      double n2 = 0.0;
+      for (int a = 0; a < sc->dim; ++a) n2 += r[1 + a] * r[1 + a];
+      if (!(std::fabs(n2 - 1.0) <= 1e-12)) return fail(VC_EINVAL, "directional light vector must be unit length");
+    }
+  }
+  cudaFree(sc->d_lights);
+  sc->d_lights = nullptr;
+  sc->n_lights = 0;
+  if (n_lights == 0) return VC_OK;
+  cudaError_t e = cudaMalloc((void**)&sc->d_lights, sizeof(double) * 8 * (size_t)n_lights);
+  if (e == cudaSuccess) e = cudaMemcpy(sc->d_lights, rows, sizeof(double) * 8 * (size_t)n_lights, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "lights upload");
+  sc->n_lights = n_lights;
+  return VC_OK;
+}
 
 int vc_scene_set_budget(vc_scene* sc, int64_t bytes) {
   if (!sc || bytes <= 0) return fail(VC_EINVAL, "invalid budget");

@@ -94,6 +94,8 @@ struct vc_scene {
   double* d_es_pos = nullptr;
   double* d_es_w = nullptr;
   int* d_es_surf = nullptr;
+  int n_lights = 0;            // extension: delta lights (vc_scene_set_lights)
+  double* d_lights = nullptr;  // n_lights × 8
   long long budget = 0;  // 0: a third of the device memory, capped at 64 GiB
   vc::Workspace ws;
   ~vc_scene() {
@@ -106,6 +108,7 @@ struct vc_scene {
     cudaFree(d_ep_start);
     cudaFree(d_ep_tri);
     cudaFree(d_ep_occ);
+    cudaFree(d_lights);
   }
 };
 

@@ -441,6 +441,29 @@ __device__ __forceinline__ void hg_sample(double g, double* cd, double u0, doubl
   for (int c = 0; c < 3; ++c) cd[c] = add(add(mul(ca, t1[c]), mul(sa, t2[c])), mul(ct, cd[c]));
 }
 
+// Extension (oracle delta_inscatter): mean incident radiance over the sphere (circle) at a
+// media point from the delta lights, Σ_l term_l·I_l / 4π (2π); g ≠ 0 weighs each light by
+// 4π·p_g(d_l·toward).
+template <int D>
+__device__ inline void delta_inscatter(const DevScene& S, const double* p, double g, const double* toward,
+                                       double out[3]) {
+  out[0] = out[1] = out[2] = 0.0;
+  const double norm = (D == 3) ? 4.0 * kPi : 2.0 * kPi;
+  for (int l = 0; l < S.n_lights; ++l) {
+    const double* L8 = S.lights + 8 * (size_t)l;
+    double d[3];
+    const double val = delta_term<D>(S, L8, p, d);
+    if (!(val > 0.0)) continue;
+    double w = __ddiv_rn(val, norm);
+    if (g != 0.0)
+      w = mul(w, mul(4.0 * kPi, hg_phase(g, add(add(mul(d[0], toward[0]), mul(d[1], toward[1])),
+                                                  mul(d[2], toward[2])))));
+    out[0] = add(out[0], mul(w, L8[4]));
+    out[1] = add(out[1], mul(w, L8[5]));
+    out[2] = add(out[2], mul(w, L8[6]));
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   const long long total = W.rec_base[W.B];
@@ -547,6 +570,7 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
 #pragma unroll
           for (int c = 0; c < D; ++c) pos[c] = add(pos[c], mul(tc, cd[c]));
           w = mul(w, albedo);
+          const double pd[3] = {cd[0], cd[1], cd[2]};  // the direction the path arrived along
           if constexpr (D == 2) {
             const double th = mul(2.0 * kPi, ua);
             cd[0] = cos(th);
@@ -572,6 +596,12 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
 #pragma unroll
             for (int c = 0; c < 3; ++c) path[c] = add(path[c], mul(wT, L[c]));
           }
+          if (S.n_lights > 0) {  // extension: the delta lights scattered at this collision
+            double dl[3];
+            delta_inscatter<D>(S, pos, hg, pd, dl);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) path[c] = add(path[c], mul(w, dl[c]));
+          }
         }
       }
       acc[0] = add(acc[0], path[0]);
@@ -589,6 +619,131 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
       pos |= f > 0.0f;
     }
     if (pos) mark_live(W, n, rec, k, i);
+  }
+}
+
+// Extension: the delta lights' in-scatter at every live-ring media sample, added to the
+// gathered radiance after either gather path (thread per sample; a sample no gather ray lit
+// has an undefined row in the two-pass path, so the live bit decides add vs. write).
+template <int D>
+__global__ void __launch_bounds__(256) k_gather_delta(DevScene S, BuildParams P, Wave W) {
+  const long long total = W.rec_base[W.B];
+  const int n = P.n_angular;
+  const double hg = (D == 3) ? P.hg_g : 0.0;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < total;
+       j += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = W.B - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (W.rec_base[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    const int rec = lo;
+    const int jl = (int)(j - W.rec_base[rec]);
+    const int* pre = W.pre + (size_t)rec * n;
+    int a = 0, b = n - 1;
+    while (a < b) {
+      int mid = (a + b + 1) >> 1;
+      if (pre[mid] <= jl) a = mid; else b = mid - 1;
+    }
+    const int k = a, i = jl - pre[k];
+    const double ri = ring_radius(i, P.march_step);
+    double y[3] = {0.0, 0.0, 0.0}, wk[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double dk = W.dirs[((size_t)rec * n + k) * D + c];
+      y[c] = add(W.x[rec * D + c], mul(ri, dk));
+    }
+    if (hg != 0.0) {
+      double dx[3], n2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        dx[c] = sub(y[c], W.x[rec * D + c]);
+        n2 = add(n2, mul(dx[c], dx[c]));
+      }
+      const double nrm = sqrt(n2);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wk[c] = __ddiv_rn(dx[c], nrm);
+    }
+    double dl[3];
+    delta_inscatter<D>(S, y, hg, wk, dl);
+    if (!(dl[0] > 0.0 || dl[1] > 0.0 || dl[2] > 0.0)) continue;
+    const unsigned long long word = W.live[((size_t)rec * W.live_words + (i >> 6)) * n + k];
+    const bool live = (word >> (i & 63)) & 1ULL;
+    float* out = W.media + (size_t)(W.rec_base[rec] + jl) * 3;
+    bool pos = false;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = mul(S.sigma_s, dl[c]);
+      float f = (float)v;
+      if (v > 0.0 && !(f > 0.0f)) f = FLT_TRUE_MIN;
+      f += live ? out[c] : 0.0f;
+      out[c] = f;
+      pos |= f > 0.0f;
+    }
+    if (pos && !live) mark_live(W, n, rec, k, i);
+  }
+}
+
+// Extension (oracle delta_single): the delta lights' own single scattering at the cache
+// point, f̄·I·φ(x)/4π (2π) with its closed-form gradient and Hessian (visibility held
+// constant), added to the single moments.
+template <int D>
+__global__ void k_delta_single(DevScene S, Wave W) {
+  const int rec = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rec >= W.B) return;
+  if (D == 3 && W.tri_status[rec] != 0) return;
+  if (W.outside && *W.outside) return;
+  const double norm = (D == 3) ? 4.0 * kPi : 2.0 * kPi;
+  const double c0 = S.sigma_s / norm / norm;  // f̄ / norm
+  const double sig = S.sigma_t;
+  constexpr int kk = D - 1;
+  double x[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < D; ++a) x[a] = W.x[rec * D + a];
+  double* M = W.moments + ((size_t)rec * 2) * moment_size(D);
+  for (int l = 0; l < S.n_lights; ++l) {
+    const double* L8 = S.lights + 8 * (size_t)l;
+    double d[3];
+    const double phi = delta_term<D>(S, L8, x, d);
+    if (!(phi > 0.0)) continue;
+    double g[3] = {0.0, 0.0, 0.0}, h[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (L8[0] == 0.0) {
+      double w[3], r2 = 0.0;
+      for (int a = 0; a < D; ++a) {
+        w[a] = x[a] - L8[1 + a];
+        r2 += w[a] * w[a];
+      }
+      const double r = sqrt(r2);
+      const double a1 = sig + kk / r;
+      const double d1 = -a1 * phi, d2 = (a1 * a1 + kk / (r * r)) * phi;
+      for (int a = 0; a < D; ++a) {
+        const double ua = w[a] / r;
+        g[a] = d1 * ua;
+        for (int b = 0; b < D; ++b) {
+          const double ub = w[b] / r;
+          h[a * D + b] = d2 * ua * ub + d1 / r * ((a == b ? 1.0 : 0.0) - ua * ub);
+        }
+      }
+    } else {
+      int ax = 0;
+      double best = 0.0;
+      for (int a = 0; a < D; ++a) {
+        const double t1 = (S.bmin[a] - x[a]) / d[a], t2 = (S.bmax[a] - x[a]) / d[a];
+        const double far = isnan(t1) ? INFINITY : np_max(t1, t2);
+        if (a == 0 || far < best) {
+          best = far;
+          ax = a;
+        }
+      }
+      const double e = 1.0 / d[ax];
+      g[ax] = sig * phi * e;
+      h[ax * D + ax] = sig * sig * phi * e * e;
+    }
+    for (int c = 0; c < 3; ++c) {
+      const double I = c0 * L8[4 + c];
+      M[c] += I * phi;
+      for (int a = 0; a < D; ++a) M[3 + c * D + a] += I * g[a];
+      for (int e2 = 0; e2 < D * D; ++e2) M[3 + 3 * D + c * D * D + e2] += I * h[e2];
+    }
   }
 }
 
@@ -3241,6 +3396,10 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
       ++nl;
     }
+    if (S.n_lights > 0) {  // extension: delta lights lit the media samples too
+      k_gather_delta<D><<<sm_count * 8, 256, 0, st>>>(S, P, W);
+      ++nl;
+    }
     prof_end(st);
   }
   if (fork) {  // join: the assembly needs both the media and the triangles
@@ -3259,6 +3418,10 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   k_assemble_t<D, false><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);  // overflowed records
   k_asm_final<D><<<W.B, 64, 0, st>>>(P, W);
   ++nl;
+  if (S.n_lights > 0 && S.sigma_s > 0.0) {
+    k_delta_single<D><<<grid_for(W.B, 128), 128, 0, st>>>(S, W);
+    ++nl;
+  }
   prof_end(st);
   ++nl;
   if (P.make_records) {

@@ -507,6 +507,37 @@ __device__ inline double bounds_exit(const DevScene& S, const double* o, const d
 // Surface shading (src/transport.py:127-254)
 // ---------------------------------------------------------------------------
 
+// Extension (oracle delta_incident): one delta light seen from o — the unit direction d
+// toward it and its attenuated geometric term, 0 when occluded.  Point light: e^{−σt r} /
+// max(r, 1e-6·scale)^{D−1}, visible iff the nearest hit lies at t ≥ r(1 − 1e-6) (the
+// reference's shadow-ray rule); directional light: the ray must leave the scene without a
+// hit, e^{−σt s_b} over the distance s_b to the bounds exit.
+template <int D, class Stack = LocalStack>
+__device__ inline double delta_term(const DevScene& S, const double* L8, const double* o, double* d,
+                                    Stack* stk = nullptr) {
+  const double off = 1e-6 * S.scale;
+  d[0] = d[1] = d[2] = 0.0;
+  if (L8[0] == 0.0) {
+    double to[3], r2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      to[a] = sub(L8[1 + a], o[a]);
+      r2 = add(r2, mul(to[a], to[a]));
+    }
+    const double r = sqrt(r2);
+    if (!(r > off)) return 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) d[a] = __ddiv_rn(to[a], r);
+    if (occluded<D, Stack>(S, o, d, mul(r, 1.0 - 1e-6), -1, stk)) return 0.0;
+    const double rm = fmax(r, off);
+    return __ddiv_rn(exp(-S.sigma_t * r), D == 3 ? mul(rm, rm) : rm);
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) d[a] = L8[1 + a];
+  if (occluded<D, Stack>(S, o, d, INFINITY, -1, stk)) return 0.0;
+  return exp(-S.sigma_t * bounds_exit<D>(S, o, d));
+}
+
 template <int D, class Stack = LocalStack>
 __device__ void direct_light(const DevScene& S, const double* p, const double* n, double acc[3],
                              Stack* stk = nullptr) {
@@ -515,6 +546,19 @@ __device__ void direct_light(const DevScene& S, const double* p, const double* n
   double org[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) org[a] = add(p[a], mul(off, n[a]));
+  for (int l = 0; l < S.n_lights; ++l) {  // extension: delta lights, same cosine and ÷π / ÷2
+    const double* L8 = S.lights + 8 * (size_t)l;
+    double dd[3];
+    const double val = delta_term<D, Stack>(S, L8, org, dd, stk);
+    if (!(val > 0.0)) continue;
+    double cp = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) cp = add(cp, mul(n[a], dd[a]));
+    cp = mul(fmax(cp, 0.0), val);
+    acc[0] = add(acc[0], mul(cp, L8[4]));
+    acc[1] = add(acc[1], mul(cp, L8[5]));
+    acc[2] = add(acc[2], mul(cp, L8[6]));
+  }
   for (int j = 0; j < S.n_es; ++j) {
     const double* P = S.es_pos + (size_t)j * D;
     double to[3], dd[3] = {0.0, 0.0, 0.0};

@@ -84,6 +84,10 @@ struct DevScene {
   const double* es_pos;  // n_es × dim
   const double* es_w;    // n_es
   const int* es_surf;    // n_es → original surface index of the emitter
+  // extension (not in the reference): delta lights, 8 doubles each — kind (0 point, 1
+  // directional), v[3] (position, or the unit vector toward the light), rgb, 0
+  int n_lights;
+  const double* lights;
 };
 
 __host__ __device__ constexpr int prim_stride(int dim) { return dim == 3 ? 9 : 4; }

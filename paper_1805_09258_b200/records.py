@@ -142,6 +142,10 @@ class DeviceScene:
                                      self.sigma_s, self.sigma_a, _lib.C.byref(h)))
         self.handle = h
         self._finalizer = weakref.finalize(self, L.vc_scene_destroy, h)
+        lights = getattr(scene, "lights", None)  # extension: delta lights (scene.light_rows)
+        if lights is not None and len(lights):
+            rows = np.ascontiguousarray(np.asarray(lights, float).reshape(-1, 8))
+            _lib.check(L.vc_scene_set_lights(h, rows.shape[0], _lib.ptr(rows)))
 
     def set_budget(self, nbytes: int) -> None:
         _lib.check(_lib.lib().vc_scene_set_budget(self.handle, int(nbytes)))

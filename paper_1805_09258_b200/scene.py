@@ -78,9 +78,13 @@ class Scene:
     medium: Medium
     bounds_min: np.ndarray
     bounds_max: np.ndarray
+    # extension (the reference has area emitters only): delta lights as rows
+    # (kind, v0, v1, v2, r, g, b, 0) — see point_light / directional_light
+    lights: np.ndarray = field(default_factory=lambda: np.zeros((0, 8)))
 
     def __post_init__(self):
         self.surfaces = tuple(self.surfaces)
+        self.lights = np.asarray(self.lights, dtype=float).reshape(-1, 8)
         self.bounds_min = np.asarray(self.bounds_min, dtype=float)
         self.bounds_max = np.asarray(self.bounds_max, dtype=float)
         if self.bounds_min.shape != self.bounds_max.shape or self.bounds_min.ndim != 1:
@@ -109,6 +113,24 @@ class Scene:
         return ok if np.asarray(points).ndim == 2 else bool(ok[0])
 
 
+def point_light(position, intensity) -> np.ndarray:
+    """Extension: an isotropic point light (radiant intensity rgb) as a Scene.lights row."""
+    p = np.zeros(3)
+    v = np.asarray(position, float)
+    p[: v.size] = v
+    return np.concatenate([[0.0], p, _rgb(intensity, "intensity"), [0.0]])
+
+
+def directional_light(toward, irradiance) -> np.ndarray:
+    """Extension: a distant light; `toward` points from the scene to the light (normalised
+    here), `irradiance` is the rgb irradiance on a plane facing it."""
+    v = np.asarray(toward, float)
+    v = v / np.linalg.norm(v)
+    p = np.zeros(3)
+    p[: v.size] = v
+    return np.concatenate([[1.0], p, _rgb(irradiance, "irradiance"), [0.0]])
+
+
 def scene_arrays(scene):
     """Packed float64 arrays of any duck-typed scene: verts (K,k,d), emission, albedo."""
     dim = int(np.asarray(scene.bounds_min).size)
@@ -123,8 +145,9 @@ def scene_arrays(scene):
     return dim, verts, em, al
 
 
-def scene_from_arrays(verts, emission, albedo, bounds_min, bounds_max, sigma_s, sigma_a) -> Scene:
+def scene_from_arrays(verts, emission, albedo, bounds_min, bounds_max, sigma_s, sigma_a, lights=()) -> Scene:
     return Scene(
+        lights=np.asarray(lights, float).reshape(-1, 8),
         surfaces=tuple(
             Surface(vertices=v, emission=e, albedo=a) for v, e, a in zip(verts, emission, albedo)
         ),
@@ -135,6 +158,14 @@ def scene_from_arrays(verts, emission, albedo, bounds_min, bounds_max, sigma_s, 
 
 
 def scene_to_dict(scene) -> dict:
+    d = _scene_to_dict(scene)
+    lights = getattr(scene, "lights", None)
+    if lights is not None and len(lights):  # extension key, absent for reference scenes
+        d["lights"] = np.asarray(lights, float).reshape(-1, 8).tolist()
+    return d
+
+
+def _scene_to_dict(scene) -> dict:
     return {
         "dimensionality": int(np.asarray(scene.bounds_min).size),
         "medium": {"sigma_s": float(scene.medium.sigma_s), "sigma_a": float(scene.medium.sigma_a)},
@@ -174,6 +205,7 @@ def scene_from_dict(d: dict) -> Scene:
         medium=Medium(float(med.get("sigma_s", 0.0)), float(med.get("sigma_a", 0.0))),
         bounds_min=np.asarray(b["min"], float),
         bounds_max=np.asarray(b["max"], float),
+        lights=np.asarray(d.get("lights", []), float).reshape(-1, 8),
     )
 
 

@@ -30,8 +30,9 @@ def golden_scene(z, prefix=""):
     from paper_1805_09258_b200.scene import scene_from_arrays
 
     sig = z[prefix + "sigma"]
+    lights = z[prefix + "lights"] if (prefix + "lights") in getattr(z, "files", z) else ()
     return scene_from_arrays(z[prefix + "verts"], z[prefix + "emission"], z[prefix + "albedo"],
-                             z[prefix + "bmin"], z[prefix + "bmax"], sig[0], sig[1])
+                             z[prefix + "bmin"], z[prefix + "bmax"], sig[0], sig[1], lights)
 
 
 def rel_l2(a, b, floor=1e-12):

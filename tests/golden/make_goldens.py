@@ -38,7 +38,9 @@ VERSIONS = np.array([np.__version__, scipy.__version__])
 
 
 def ref_scene(scene):
-    return vscene.scene_from_dict(scene_to_dict(scene))
+    d = scene_to_dict(scene)
+    d.pop("lights", None)  # extension key the reference does not know
+    return vscene.scene_from_dict(d)
 
 
 def scene_fields(prefix, scene):
@@ -612,7 +614,7 @@ def _hg_sample_ref(g, cur, u0, u1):
     return (st * np.cos(phi))[:, None] * t1 + (st * np.sin(phi))[:, None] * t2 + ct[:, None] * cur
 
 
-def _gather_bounces_shim(seed_box, bounces, hg=0.0):
+def _gather_bounces_shim(seed_box, bounces, hg=0.0, inscatter=None):
     """Extension oracle written with the reference's own primitives: mean_surface_gather
     (src/transport.py:288-310) continued by up to `bounces` − 1 media scattering events per
     gather path, exactly the multiple-scattering loop of path_trace_radiance
@@ -659,6 +661,8 @@ def _gather_bounces_shim(seed_box, bounces, hg=0.0):
             lo2 = vt.surface_radiance_batch(scene, idx2, pos[collide] + s2[collide, None] * nd[collide],
                                             nd[collide], n_light_samples)
             tot[collide] += w[collide, None] * np.exp(-sig_t * s2[collide])[:, None] * lo2
+            if inscatter is not None:  # delta lights scattered at this collision toward −cur_d
+                tot[collide] += w[collide, None] * inscatter(pos[collide], hg, cur_d[collide])
             alive = collide
             cur_d = nd
             cur_s = s2
@@ -729,6 +733,160 @@ def gen_media_bounces():
     out.update(versions=VERSIONS, points=pts, cfg_seed=np.array(3), params=np.array([n, step, 1, 16, float(B)]))
     np.savez_compressed(OUT / "rec_media_bounces.npz", **out)
     print("wrote media_bounces", flush=True)
+
+
+def _delta_ref(rs, lights):
+    """Delta-light extension written with the reference's own primitives (scene.trace,
+    scene.bounds_exit): per light the direction toward it, the attenuated geometric term with
+    the reference's shadow-ray rule (src/transport.py:213-214), and its rgb strength."""
+    dim = rs.dim
+    off = 1e-6 * rs.scale
+    sig = rs.medium.sigma_t
+
+    def incident(org):
+        org = np.atleast_2d(org)
+        m = org.shape[0]
+        res = []
+        for row in lights:
+            kind, v, I = int(row[0]), row[1:1 + dim], row[4:7]
+            val = np.zeros(m)
+            if kind == 0:
+                to = v[None] - org
+                r = np.linalg.norm(to, axis=1)
+                ok = r > off
+                d = np.zeros_like(to)
+                d[ok] = to[ok] / r[ok, None]
+                th, _ = vscene.trace(rs, org[ok], d[ok])
+                vis = th >= r[ok] * (1.0 - 1e-6)
+                ii = np.flatnonzero(ok)[vis]
+                val[ii] = np.exp(-sig * r[ii]) / np.maximum(r[ii], off) ** (dim - 1)
+            else:
+                d = np.broadcast_to(v, (m, dim)).copy()
+                th, _ = vscene.trace(rs, org, d)
+                vis = ~np.isfinite(th)
+                val[vis] = np.exp(-sig * vscene.bounds_exit(rs, org[vis], d[vis]))
+            res.append((d, val, I))
+        return res
+
+    def inscatter(pts, g=0.0, toward=None):
+        out = np.zeros((np.atleast_2d(pts).shape[0], 3))
+        norm = 4.0 * np.pi if dim == 3 else 2.0 * np.pi
+        for d, val, I in incident(pts):
+            w = val / norm
+            if g != 0.0:
+                c = (d * toward).sum(axis=1)
+                w = w * (4.0 * np.pi * ((1.0 - g * g) / (4.0 * np.pi * (1.0 + g * g - 2.0 * g * c) ** 1.5)))
+            out += w[:, None] * I[None]
+        return out
+
+    def single(x):
+        x = np.asarray(x, float)
+        L, G, H = np.zeros(3), np.zeros((3, dim)), np.zeros((3, dim, dim))
+        norm = 4.0 * np.pi if dim == 3 else 2.0 * np.pi
+        c = rs.medium.sigma_s / norm / norm
+        k = dim - 1
+        for row, (d, val, I) in zip(lights, incident(x[None])):
+            phi = val[0]
+            if not phi > 0.0:
+                continue
+            if int(row[0]) == 0:
+                w = x - row[1:1 + dim]
+                r = float(np.linalg.norm(w))
+                u = w / r
+                a = sig + k / r
+                d1, d2 = -a * phi, (a * a + k / (r * r)) * phi
+                g = d1 * u
+                h = d2 * np.outer(u, u) + d1 / r * (np.eye(dim) - np.outer(u, u))
+            else:
+                dv = d[0]
+                with np.errstate(divide="ignore", invalid="ignore"):
+                    t = np.maximum((rs.bounds_min - x) / dv, (rs.bounds_max - x) / dv)
+                t = np.where(np.isnan(t), np.inf, t)
+                ax = int(np.argmin(t))
+                e = np.zeros(dim)
+                e[ax] = 1.0 / dv[ax]
+                g = sig * phi * e
+                h = sig * sig * phi * np.outer(e, e)
+            L += c * phi * I
+            G += c * I[:, None] * g[None]
+            H += c * I[:, None, None] * h[None]
+        return L, G, H
+
+    return incident, inscatter, single
+
+
+def gen_delta_lights():
+    """Extension records with delta lights (BASELINE.json cfg1/cfg2/cfg4 point lights, cfg3's
+    directional light; the reference has area emitters only): the reference's build_subdivision
+    + assemble_moments with direct_lighting and mean_surface_gather extended through the
+    reference's own trace / bounds_exit (_delta_ref), plus the lights' closed-form single
+    scattering at the cache point.  Four cases: 2D cfg1-as-specified with a reflective occluder;
+    a reflective 3D room with open windows (directional + point); a non-reflective room with
+    emissive portals and a point light (the two-pass gather); open windows with HG g = 0.5 and
+    3 media events per gather path (delta lights scattered at every collision)."""
+    import volcache.transport as vt
+    from paper_1805_09258_b200.scene import directional_light, point_light
+
+    sun = directional_light(configs.SUN_TOWARD, configs.SUN_IRRADIANCE)
+    lamp = point_light((2.6, 2.2, 1.4), (6.0, 5.0, 4.0))
+    cases = [
+        ("d2", configs.cfg1_spec_scene(occluder_albedo=0.3), 4, 1024, 0.1, 1, 0.0, 41),
+        ("refl", configs.cfg3_scene(4, 1, wall_albedo=0.5, open_windows=True, lights=[sun, lamp]), 3, 1024, 0.2, 1,
+         0.0, 42),
+        ("portal", configs.cfg3_scene(4, 1, lights=[lamp]), 2, 1024, 0.2, 1, 0.0, 43),
+        ("hg", configs.cfg3_scene(4, 1, open_windows=True, lights=[sun, lamp]), 2, 1024, 0.2, 3, 0.5, 44),
+    ]
+    out = {"versions": VERSIONS}
+    for name, sc, npts, n, step, B, g, seed in cases:
+        rs = ref_scene(sc)
+        dim = rs.dim
+        incident, inscatter, single = _delta_ref(rs, sc.lights)
+        pts = np.random.default_rng(seed).uniform(rs.bounds_min + 0.15 * (rs.bounds_max - rs.bounds_min),
+                                                  rs.bounds_max - 0.15 * (rs.bounds_max - rs.bounds_min), (npts, dim))
+        box = {}
+        o_dl, o_msg = vt.direct_lighting, vs.mean_surface_gather
+
+        def direct_lighting(scene, points, normals, n_light_samples=16, _o=o_dl, _inc=incident):
+            points, normals = np.atleast_2d(points), np.atleast_2d(normals)
+            base = _o(scene, points, normals, n_light_samples)
+            add = np.zeros_like(base)
+            for d, val, I in _inc(points + 1e-6 * scene.scale * normals):
+                cp = np.clip(np.einsum("md,md->m", normals, d), 0.0, None)
+                add += (cp * val)[:, None] * I[None]
+            return base + add / (np.pi if scene.dim == 3 else 2.0)
+
+        base_gather = o_msg if (B == 1 and g == 0.0) else _gather_bounces_shim(box, B, g, inscatter)
+
+        def gather(scene, points, dirs_pp, n_light_samples=16, _b=base_gather, _ins=inscatter, _g=g):
+            dx = points - box["x"][None]
+            wk = dx / np.sqrt((dx * dx).sum(axis=1))[:, None]
+            return _b(scene, points, dirs_pp, n_light_samples) + _ins(points, _g, wk)
+
+        vt.direct_lighting = direct_lighting
+        vs.mean_surface_gather = gather
+        res = {k: [] for k in ("L", "grad", "hess", "stats", "adj")}
+        try:
+            for i, x in enumerate(pts):
+                box.update(seed=vr._seed(seed, 401, i), n_dirs=n, x=np.asarray(x, float))
+                with Capture() as cap:
+                    sub = vs.build_subdivision(rs, x, n_angular=n, march_step=step, rng_seed=vr._seed(seed, 401, i))
+                sg, mu, stats = vs.assemble_moments(sub, rs.medium)
+                dL, dG, dH = single(x)
+                res["L"].append([sg.L + dL, mu.L])
+                res["grad"].append([sg.grad + dG, mu.grad])
+                res["hess"].append([sg.hess + dH, mu.hess])
+                res["stats"].append([stats["elements_evaluated"], stats["elements_dropped"], stats["star_vertices"]])
+                res["adj"].append(np.asarray(cap.dirs.adjacency, np.int32))
+        finally:
+            vt.direct_lighting = o_dl
+            vs.mean_surface_gather = o_msg
+        out.update({f"{name}_{k}": np.array(v) for k, v in res.items()})
+        out.update(scene_fields(f"{name}_", rs))
+        out[f"{name}_lights"] = np.asarray(sc.lights, float)
+        out[f"{name}_points"] = pts
+        out[f"{name}_params"] = np.array([n, step, 1, 16, float(B), g, float(seed)])
+        print("delta lights", name, np.array(res["L"])[:, :, 1].tolist(), flush=True)
+    np.savez_compressed(OUT / "rec_delta_lights.npz", **out)
 
 
 def gen_surface():
@@ -987,6 +1145,8 @@ if __name__ == "__main__":
         gen_cfg3_full()
     if "surface" in which:
         gen_surface()
+    if "delta_lights" in which:
+        gen_delta_lights()
     if "media_bounces" in which:
         gen_media_bounces()
     if "media_hg" in which:

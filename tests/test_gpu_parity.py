@@ -220,6 +220,51 @@ def test_media_hg_extension_vs_reference_shim():
         assert tuple(int(v) for v in r.stats[i, :3]) == tuple(int(v) for v in z["stats"][i])
 
 
+@pytest.mark.parametrize("case", ["d2", "refl", "portal", "hg"])
+def test_delta_lights_extension_vs_reference_shim(case):
+    """Extension (BASELINE cfg1/cfg2/cfg4 point lights, cfg3's directional light): delta lights
+    on reflective surfaces (direct_light), at every media sample (k_gather_delta after either
+    gather path; inside k_gather's bounce loop in `hg`) and at the cache point
+    (k_delta_single).  Device vs the reference's build_subdivision + assemble_moments extended
+    through its own trace / bounds_exit (tests/golden/rec_delta_lights.npz; the oracle is pinned
+    to it), the reference's adjacency injected; the north_star gate, element counts exact."""
+    from paper_1805_09258_b200 import estimate_moments_batch
+
+    z = golden("rec_delta_lights")
+    sc = golden_scene(z, case + "_")
+    n, step, n_inner, n_light, B, g, seed = z[case + "_params"]
+    pts = z[case + "_points"]
+    N = len(pts)
+    words = np.array([[int(seed), 401, i] for i in range(N)], np.uint32)
+    adj = z[case + "_adj"].astype(np.int32) if pts.shape[1] == 3 else None
+    r = estimate_moments_batch(sc, pts, seeds=words, n_angular=int(n), march_step=float(step),
+                               n_inner=int(n_inner), n_light_samples=int(n_light), adjacency=adj,
+                               media_bounces=int(B), hg_g=float(g))
+    for i in range(N):
+        _check_moments(f"delta_{case}[{i}]", r.L[i], r.grad[i], r.hess[i], z[case + "_L"][i], z[case + "_grad"][i],
+                       z[case + "_hess"][i])
+        assert tuple(int(v) for v in r.stats[i, :3]) == tuple(int(v) for v in z[case + "_stats"][i])
+
+
+def test_delta_lights_lit_samples_vs_oracle():
+    """Per media sample: the device's media radiance with a lamp inside the portal room (the
+    two-pass gather, then k_gather_delta on every sample) against the oracle's."""
+    from paper_1805_09258_b200 import inspect_record
+    from oracle import volcache_oracle as O
+
+    z = golden("rec_delta_lights")
+    sc = golden_scene(z, "portal_")
+    n, step, n_inner, n_light, B, g, seed = z["portal_params"]
+    x = z["portal_points"][1]
+    ss = np.random.SeedSequence([int(seed), 401, 1])
+    ins = inspect_record(sc, x, rng_seed=ss, n_angular=int(n), march_step=float(step),
+                         adjacency=z["portal_adj"][1].astype(np.int32))
+    ob = O.build_record(O.pack(sc), x, int(n), float(step), np.random.SeedSequence([int(seed), 401, 1]),
+                        adjacency=z["portal_adj"][1])
+    np.testing.assert_allclose(ins["media"], ob.media_radiance, rtol=2e-6, atol=1e-30)
+    assert (ob.media_radiance > 0).any(axis=1).mean() > 0.5  # the lamp reaches most samples
+
+
 def _tri_set(t):
     return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
 

@@ -116,6 +116,45 @@ def test_media_hg_oracle_matches_reference_shim():
             assert rel_l2(rb.hess[k], z["hess"][i][k]) <= 1e-10
 
 
+DELTA_CASES = ("d2", "refl", "portal", "hg")
+
+
+@pytest.mark.parametrize("case", DELTA_CASES)
+def test_delta_lights_oracle_matches_reference_shim(case):
+    """The delta-light extension (point and directional lights on reflective surfaces, at every
+    media sample and at the cache point; with HG and further media events in `hg`) in the
+    oracle against the reference's build_subdivision + assemble_moments with direct_lighting
+    and the gather extended through the reference's own trace / bounds_exit (gen_delta_lights)."""
+    z = golden("rec_delta_lights")
+    ps = O.pack(golden_scene(z, case + "_"))
+    assert len(ps.lights) >= 1
+    n, step, n_inner, n_light, B, g, seed = z[case + "_params"]
+    for i, x in enumerate(z[case + "_points"]):
+        rb = O.build_record(ps, x, int(n), float(step), O.seed_seq(int(seed), 401, i), int(n_inner), int(n_light),
+                            adjacency=z[case + "_adj"][i], media_bounces=int(B), hg_g=float(g))
+        assert [rb.stats["elements_evaluated"], rb.stats["elements_dropped"], rb.stats["star_vertices"]] == \
+            z[case + "_stats"][i].tolist()
+        for k in range(2):
+            assert rel_l2(rb.L[k], z[case + "_L"][i][k]) <= 1e-12
+            assert rel_l2(rb.grad[k], z[case + "_grad"][i][k]) <= 1e-11
+            assert rel_l2(rb.hess[k], z[case + "_hess"][i][k]) <= 1e-10
+
+
+def test_delta_lights_off_is_the_reference():
+    """No lights → every delta-light hook is inert (the reference's estimator exactly)."""
+    z = golden("rec_delta_lights")
+    sc = golden_scene(z, "portal_")
+    ps = O.pack(sc)
+    ps0 = O.pack(golden_scene({k: z[k] for k in z.files if not k.endswith("_lights")}, "portal_"))
+    assert len(ps0.lights) == 0 and len(ps.lights) == 1
+    n, step, n_inner, n_light, B, g, seed = z["portal_params"]
+    x = z["portal_points"][0]
+    a = O.build_record(ps, x, int(n), float(step), O.seed_seq(int(seed), 401, 0), adjacency=z["portal_adj"][0])
+    b = O.build_record(ps0, x, int(n), float(step), O.seed_seq(int(seed), 401, 0), adjacency=z["portal_adj"][0])
+    assert np.all(a.L[1] > b.L[1]) and np.all(a.L[0] > b.L[0])  # the lamp adds light everywhere
+    np.testing.assert_array_equal(a.idx, b.idx)
+
+
 def test_make_record_edge_cases():
     z = golden("make_record")
     for j in range(int(z["n_cases"])):
