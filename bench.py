@@ -141,6 +141,15 @@ def workload(args):
         return configs.cfg2(march_step=args.march_step or 4.0)
     if args.config == "cfg1":
         return configs.cfg1(march_step=args.march_step or 4.0)
+    if args.config in ("cfg1-spec", "cfg2-spec"):  # extension: the configs as BASELINE.json states them
+        import dataclasses
+
+        if args.config == "cfg1-spec":  # point light instead of the emissive square
+            w = configs.cfg1(march_step=args.march_step or 0.1)
+            return dataclasses.replace(w, name="cfg1-flatland-2d+point-light", scene=configs.cfg1_spec_scene())
+        w = configs.cfg2(march_step=args.march_step or 0.1)  # point light, Henyey-Greenstein g = 0.3
+        return dataclasses.replace(w, name="cfg2-single-occluder-3d+point-light+hg0.3",
+                                   scene=configs.cfg2_spec_scene(), hg_g=0.3)
     raise SystemExit(f"unknown config {args.config}")
 
 
@@ -461,8 +470,8 @@ def main():
     B = args.records_per_step
     ds = device_scene(w.scene)
     kw = dict(n_angular=w.n_angular, march_step=w.march_step, n_inner=w.n_inner,
-              n_light_samples=w.n_light_samples, epsilon=w.epsilon, media_bounces=args.media_bounces,
-              hg_g=args.hg_g)
+              n_light_samples=w.n_light_samples, epsilon=w.epsilon, media_bounces=w.media_bounces,
+              hg_g=w.hg_g)
     total_steps = args.warmup + args.steps
     # inputs resident in HBM before timing
     Xs, Ss = [], []
@@ -531,8 +540,8 @@ def main():
     prm.n_angular, prm.march_step, prm.n_inner = w.n_angular, w.march_step, w.n_inner
     prm.n_light_samples, prm.epsilon = w.n_light_samples, w.epsilon
     prm.flags = _lib.VC_MEM_HOST | _lib.VC_SEED_WORDS | _lib.VC_MAKE_RECORDS
-    prm.media_bounces = args.media_bounces
-    prm.hg_g = args.hg_g
+    prm.media_bounces = w.media_bounces
+    prm.hg_g = w.hg_g
     prm.seed_words = 3
     barrier()
     torch.cuda.synchronize()

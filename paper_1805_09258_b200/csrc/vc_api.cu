@@ -336,7 +336,8 @@ static void del_row_table(BuildParams& P) {
   const int rows = P.rows, cols = P.cols;
   P.del_kmax = 0;
   const double pi = 3.141592653589793;
-  const double alpha = 2.0 * std::sqrt(4.0 * pi / P.n_angular);
+  const char* ea = getenv("VOLCACHE_HULL_ALPHA");  // window margin in mean spacings (default 2)
+  const double alpha = (ea ? std::max(0.5, std::min(4.0, atof(ea))) : 2.0) * std::sqrt(4.0 * pi / P.n_angular);
   for (int r = 0; r < std::min(rows, kDelRowsMax); ++r) {
     const double tht = std::acos(1.0 - 2.0 * r / rows), thb = std::acos(1.0 - 2.0 * (r + 1) / rows);
     const double smin = std::min(std::sin(tht), std::sin(thb));
