@@ -622,6 +622,10 @@ __global__ void __launch_bounds__(256, VC_LB_TRACE) k_gather(DevScene S, BuildPa
   }
 }
 
+#ifndef VC_DELTA_PT
+#define VC_DELTA_PT 0  // persistent-lane shadow rays for the delta lights: measured slower (221 vs 194 ms per
+                       // 2048 lamp-lit cfg3 records) — the shadow rays of consecutive samples are coherent
+#endif
 // Extension: the delta lights' in-scatter at every live-ring media sample, added to the
 // gathered radiance after either gather path (thread per sample; a sample no gather ray lit
 // has an undefined row in the two-pass path, so the live bit decides add vs. write).
@@ -772,6 +776,32 @@ __device__ __forceinline__ void store_media(float* out, const double* v) {
     if (v[c] > 0.0 && !(f > 0.0f)) f = FLT_TRUE_MIN;  // keep the liveness bit exact
     out[c] = f;
   }
+}
+
+// Media radiance of an unoccluded emitter hit in the two-pass gather: σs · T · L_o / n_inner
+// with n_inner = 1 and L_o = emission (non-reflective scene); extension hg ≠ 0: the path is
+// weighted 4π·p_g(d·w), w = (y − x)/|y − x| (k_gather's first-event weight).
+template <int D>
+__device__ __forceinline__ void emitter_radiance(const DevScene& S, const Wave& W, double hg, int rec,
+                                                 const double* y, const double* d, double te, int ie, double* v) {
+  const double* E = S.emission + (size_t)ie * 3;
+  const double T = exp(-S.sigma_t * te);
+  double w0 = 1.0;
+  if (D == 3 && hg != 0.0) {
+    double dx[3], n2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      dx[c] = sub(y[c], W.x[rec * D + c]);
+      n2 = add(n2, mul(dx[c], dx[c]));
+    }
+    const double nrm = sqrt(n2);
+    double cs = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cs = add(cs, mul(d[c], __ddiv_rn(dx[c], nrm)));
+    w0 = mul(4.0 * kPi, hg_phase(hg, cs));
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(mul(T, E[c]), w0));
 }
 
 #ifndef VC_QCHUNK
@@ -1064,12 +1094,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
           it.ring = i;
         } else {  // queue full: resolve in place (same result, less coherent)
           double v[3] = {0.0, 0.0, 0.0};
-          if (!occluded<D>(S, y, gd, te, ie)) {
-            const double* E = S.emission + (size_t)ie * 3;
-            double T = exp(-S.sigma_t * te);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
-          }
+          if (!occluded<D>(S, y, gd, te, ie)) emitter_radiance<D>(S, W, P.hg_g, rec, y, gd, te, ie, v);
           store_media(W.media + (size_t)(base + j) * 3, v);
           if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, rec, k, i);
         }
@@ -1245,10 +1270,10 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_eval(DevScene S, Bui
     if (cbase + u < q_cap) q[cbase + u].slot = -1;
 }
 
-template <int D>
+template <int D, bool HG = false>
 __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl(DevScene S, Wave W, int n, const GatherItem* q,
                                                                const unsigned long long* q_count, long long q_cap,
-                                                               float* media) {
+                                                               float* media, double hg) {
   VC_RAY_STACK;
   const long long nq = min((long long)*q_count, q_cap);
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nq;
@@ -1256,13 +1281,8 @@ __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl(DevScene S, Wav
     if (q[t].slot < 0) continue;  // unused tail of a warp's chunk
     const GatherItem it = q[t];
     double v[3] = {0.0, 0.0, 0.0};
-    if (!occluded<D>(S, it.y, it.d, it.te, it.ie, &stk)) {
-      // L_o = emission (non-reflective scene); σs · T · L_o / n_inner with n_inner = 1
-      const double* E = S.emission + (size_t)it.ie * 3;
-      double T = exp(-S.sigma_t * it.te);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
-    }
+    if (!occluded<D>(S, it.y, it.d, it.te, it.ie, &stk))
+      emitter_radiance<D>(S, W, HG ? hg : 0.0, it.rec, it.y, it.d, it.te, it.ie, v);
     store_media(media + (size_t)it.slot * 3, v);
     if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, it.rec, it.k, it.ring);
   }
@@ -1277,10 +1297,10 @@ __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl(DevScene S, Wav
 #ifndef VC_OCCL_PT
 #define VC_OCCL_PT 1
 #endif
-template <int D>
+template <int D, bool HG = false>
 __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl_pt(DevScene S, Wave W, int n, const GatherItem* q,
                                                                   unsigned long long* q_count, long long q_cap,
-                                                                  float* media) {
+                                                                  float* media, double hg) {
   const long long nq = min((long long)q_count[0], q_cap);
   unsigned long long* cursor = q_count + 1;
   const DevBvh& H = S.geo;
@@ -1298,12 +1318,7 @@ __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl_pt(DevScene S, 
   auto finish = [&](bool occl) {
     const GatherItem& it = q[cur_item];
     double v[3] = {0.0, 0.0, 0.0};
-    if (!occl) {  // L_o = emission (non-reflective scene); σs · T · L_o / n_inner with n_inner = 1
-      const double* E = S.emission + (size_t)it.ie * 3;
-      const double T = exp(-S.sigma_t * it.te);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) v[c] = mul(S.sigma_s, mul(T, E[c]));
-    }
+    if (!occl) emitter_radiance<D>(S, W, HG ? hg : 0.0, it.rec, it.y, it.d, it.te, it.ie, v);
     store_media(media + (size_t)it.slot * 3, v);
     if (v[0] > 0.0 || v[1] > 0.0 || v[2] > 0.0) mark_live(W, n, it.rec, it.k, it.ring);
     cur_item = -1;
@@ -1400,6 +1415,218 @@ __global__ void __launch_bounds__(256, VC_LB_OCCL) k_gather_occl_pt(DevScene S, 
         }
         if (occl) finish(true);
         else if (!pop()) finish(false);
+      }
+    }
+  }
+}
+
+// k_gather_delta with persistent lanes (scenes with a BVH): a lane owns one media sample at
+// a time, walks its lights one shadow ray after the other — each advanced leaf by leaf, as
+// k_gather_occl_pt — and fetches the next sample through a warp-aggregated cursor once the
+// last light is decided.  Same per-sample arithmetic and light order as k_gather_delta.
+template <int D>
+__global__ void __launch_bounds__(256, 3) k_gather_delta_pt(DevScene S, BuildParams P, Wave W,
+                                                            unsigned long long* cursor) {
+  const long long total = W.rec_base[W.B];
+  const int n = P.n_angular;
+  const double hg = (D == 3) ? P.hg_g : 0.0;
+  const DevBvh& H = S.geo;
+  const int lane = threadIdx.x & 31;
+  const float slack = 1e-5f * (float)S.scale;
+  const double off = 1e-6 * S.scale;
+  const double norm = (D == 3) ? 4.0 * kPi : 2.0 * kPi;
+  LocalStack stk;
+  long long j = -1;  // the lane's sample (−1: none)
+  bool exhausted = false, ray = false;
+  int rec = 0, k = 0, i = 0, l = 0;
+  double y[3] = {0.0, 0.0, 0.0}, dl[3] = {0.0, 0.0, 0.0};
+  double d[3] = {0.0, 0.0, 0.0}, thr = 0.0, rr = 0.0;  // rr: distance to a point light
+  float2 inv2[3], noi2[3];
+  float tbf = 0.0f;
+  int sp = 0;
+  unsigned cur = 0;
+  auto pop = [&]() -> bool {
+    while (sp > 0) {
+      const uint2 e = stk.get(--sp);
+      if (__uint_as_float(e.y) <= tbf) {
+        cur = e.x;
+        return true;
+      }
+    }
+    return false;
+  };
+  auto decided = [&](bool occl) {
+    if (!occl) {
+      const double* L8 = S.lights + 8 * (size_t)l;
+      double val;
+      if (L8[0] == 0.0) {
+        const double rm = fmax(rr, off);
+        val = __ddiv_rn(exp(-S.sigma_t * rr), D == 3 ? mul(rm, rm) : rm);
+      } else {
+        val = exp(-S.sigma_t * bounds_exit<D>(S, y, d));
+      }
+      if (val > 0.0) {
+        double w = __ddiv_rn(val, norm);
+        if (hg != 0.0) {
+          double dx[3], n2 = 0.0;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            dx[c] = sub(y[c], W.x[rec * D + c]);
+            n2 = add(n2, mul(dx[c], dx[c]));
+          }
+          const double nrm = sqrt(n2);
+          double cs = 0.0;  // d·w in delta_inscatter's order
+#pragma unroll
+          for (int c = 0; c < 3; ++c) cs = add(cs, mul(d[c], __ddiv_rn(dx[c], nrm)));
+          w = mul(w, mul(4.0 * kPi, hg_phase(hg, cs)));
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dl[c] = add(dl[c], mul(w, L8[4 + c]));
+      }
+    }
+    ray = false;
+    ++l;
+  };
+  while (true) {
+    const bool need = j < 0 && !exhausted;
+    const unsigned mneed = __ballot_sync(0xffffffffu, need);
+    if (mneed) {
+      const int leader = __ffs(mneed) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(cursor, (unsigned long long)__popc(mneed));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const long long t = (long long)base + __popc(mneed & ((1u << lane) - 1u));
+        if (t >= total) {
+          exhausted = true;
+        } else {
+          j = t;
+          int lo = 0, hi = W.B - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (W.rec_base[mid] <= j) lo = mid; else hi = mid - 1;
+          }
+          rec = lo;
+          const int jl = (int)(j - W.rec_base[rec]);
+          const int* pre = W.pre + (size_t)rec * n;
+          int a = 0, b = n - 1;
+          while (a < b) {
+            const int mid = (a + b + 1) >> 1;
+            if (pre[mid] <= jl) a = mid; else b = mid - 1;
+          }
+          k = a;
+          i = jl - pre[k];
+          const double ri = ring_radius(i, P.march_step);
+#pragma unroll
+          for (int c = 0; c < D; ++c) y[c] = add(W.x[rec * D + c], mul(ri, W.dirs[((size_t)rec * n + k) * D + c]));
+          l = 0;
+          dl[0] = dl[1] = dl[2] = 0.0;
+        }
+      }
+    }
+    if (j >= 0 && !ray) {
+      while (l < S.n_lights) {  // the sample's next shadow ray
+        const double* L8 = S.lights + 8 * (size_t)l;
+        bool ok = true;
+        if (L8[0] == 0.0) {
+          double to[3], r2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            to[a] = sub(L8[1 + a], y[a]);
+            r2 = add(r2, mul(to[a], to[a]));
+          }
+          const double r = sqrt(r2);
+          ok = r > off;
+          if (ok) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) d[a] = __ddiv_rn(to[a], r);
+            thr = mul(r, 1.0 - 1e-6);
+            rr = r;
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < D; ++a) d[a] = L8[1 + a];
+          thr = INFINITY;
+          rr = 0.0;
+        }
+        if (ok) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            float inv = 0.0f, noi = 0.0f;
+            if (a < D) {
+              const float orl = (float)(y[a] - H.ctr[a]);
+              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"((float)d[a]));
+              noi = -orl * inv;
+            }
+            inv2[a] = make_float2(inv, inv);
+            noi2[a] = make_float2(noi, noi);
+          }
+          tbf = isfinite(thr) ? __double2float_ru(thr) * 1.0001f + slack : INFINITY;
+          sp = 0;
+          cur = 0;
+          ray = true;
+          break;
+        }
+        ++l;
+      }
+      if (!ray) {  // every light decided: merge into the sample's media row
+        if (dl[0] > 0.0 || dl[1] > 0.0 || dl[2] > 0.0) {
+          const unsigned long long word = W.live[((size_t)rec * W.live_words + (i >> 6)) * n + k];
+          const bool live = (word >> (i & 63)) & 1ULL;
+          float* out = W.media + (size_t)j * 3;
+          bool pos = false;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double v = mul(S.sigma_s, dl[c]);
+            float f = (float)v;
+            if (v > 0.0 && !(f > 0.0f)) f = FLT_TRUE_MIN;
+            f += live ? out[c] : 0.0f;
+            out[c] = f;
+            pos |= f > 0.0f;
+          }
+          if (pos && !live) mark_live(W, n, rec, k, i);
+        }
+        j = -1;
+      }
+    }
+    if (!__any_sync(0xffffffffu, ray)) {
+      if (__all_sync(0xffffffffu, exhausted && j < 0)) break;
+      continue;
+    }
+    if (ray) {  // one step: descend to the next leaf, test it
+      bool alive = true;
+      while (!(cur & 0x80000000u)) {
+        const float4* N = H.nodes + 4 * (size_t)cur;
+        const float4 A = __ldg(N), B = __ldg(N + 1), C = __ldg(N + 2), R = __ldg(N + 3);
+        float tl, tr;
+        bool hl, hr;
+        box_hit2<D>(A, B, C, inv2, noi2, tbf, hl, hr, tl, tr);
+        if (hl && hr) {
+          const bool lf = tl <= tr;
+          stk.put(sp++, make_uint2(__float_as_uint(lf ? R.z : R.x), __float_as_uint(lf ? tr : tl)));
+          cur = __float_as_uint(lf ? R.x : R.z);
+        } else if (hl || hr) {
+          cur = __float_as_uint(hl ? R.x : R.z);
+        } else if (!pop()) {
+          alive = false;
+          break;
+        }
+      }
+      if (!alive) {
+        decided(false);
+      } else {
+        bool occl = false;
+        for (int kk = (int)(cur & 0x7fffffffu);; ++kk) {
+          const int idf = __float_as_int(__ldg(&H.prim32[3 * (size_t)kk + 2].w));
+          const double t = hit_prim<D>(H.prim + (size_t)kk * prim_stride(D), y, d, S.t_eps);
+          if (t < thr) {  // (id_thr = −1: no tie clause)
+            occl = true;
+            break;
+          }
+          if (idf < 0) break;
+        }
+        if (occl) decided(true);
+        else if (!pop()) decided(false);
       }
     }
   }
@@ -3367,10 +3594,17 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   // live-sample masks are set by the gather itself (mark_live)
   cudaMemsetAsync(W.live, 0, sizeof(unsigned long long) * (size_t)W.live_words * nt, st);
   if (S.sigma_s > 0.0) {
+    // (the HG extension with one media event only weighs the emitter hits: still two passes)
     const bool two_pass = !S.reflective && 2 * S.emit.K <= S.geo.K && P.n_inner == 1 && W.gather_q_cap > 0 &&
-                          P.media_bounces <= 1 && P.hg_g == 0.0;
+                          P.media_bounces <= 1;
+    // nothing emits and nothing reflects: every gather path carries zero radiance (only the
+    // delta lights, extension, light the media — k_gather_delta below, or inside k_gather's
+    // bounce loop when further media events are on)
+    const bool dark = S.emit.K == 0 && !S.reflective && (P.media_bounces <= 1 || S.n_lights == 0);
     prof_begin(KC_GATHER, st);
-    if (two_pass) {
+    if (dark) {
+      if (W.dense_media) cudaMemsetAsync(W.media, 0, sizeof(float) * 3 * (size_t)W.media_cap, st);
+    } else if (two_pass) {
       cudaMemsetAsync(W.gather_q_count, 0, 2 * sizeof(unsigned long long), st);
       if (VC_GATHER_SPLIT && !W.dense_media) {  // filter → survivor evaluation → redo pass
         cudaMemsetAsync(W.surv_cnt, 0, sizeof(int) * 2 * (size_t)W.B, st);  // surv_cnt and redo
@@ -3385,19 +3619,28 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
         k_gather_emit<D, 0><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
       }
-      if (VC_OCCL_PT && S.geo.n_nodes > 0)
-        k_gather_occl_pt<D><<<sm_count * 8, 256, 0, st>>>(S, W, P.n_angular, (const GatherItem*)W.gather_q,
-                                                          W.gather_q_count, W.gather_q_cap, W.media);
-      else
-        k_gather_occl<D><<<sm_count * 8, 256, stack_smem(k_gather_occl<D>, S.geo), st>>>(
-            S, W, P.n_angular, (const GatherItem*)W.gather_q, W.gather_q_count, W.gather_q_cap, W.media);
+      const bool hg_on = D == 3 && P.hg_g != 0.0;
+      if (VC_OCCL_PT && S.geo.n_nodes > 0) {
+        auto kern = hg_on ? k_gather_occl_pt<D, true> : k_gather_occl_pt<D, false>;
+        kern<<<sm_count * 8, 256, 0, st>>>(S, W, P.n_angular, (const GatherItem*)W.gather_q, W.gather_q_count,
+                                           W.gather_q_cap, W.media, P.hg_g);
+      } else {
+        auto kern = hg_on ? k_gather_occl<D, true> : k_gather_occl<D, false>;
+        kern<<<sm_count * 8, 256, stack_smem(k_gather_occl<D, false>, S.geo), st>>>(
+            S, W, P.n_angular, (const GatherItem*)W.gather_q, W.gather_q_count, W.gather_q_cap, W.media, P.hg_g);
+      }
       nl += 2;
     } else {
       k_gather<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, jt);
       ++nl;
     }
     if (S.n_lights > 0) {  // extension: delta lights lit the media samples too
-      k_gather_delta<D><<<sm_count * 8, 256, 0, st>>>(S, P, W);
+      if (VC_DELTA_PT && S.geo.n_nodes > 0 && W.ray_cursor) {
+        cudaMemsetAsync(W.ray_cursor, 0, sizeof(unsigned long long), st);
+        k_gather_delta_pt<D><<<sm_count * 6, 256, 0, st>>>(S, P, W, W.ray_cursor);
+      } else {
+        k_gather_delta<D><<<sm_count * 8, 256, 0, st>>>(S, P, W);
+      }
       ++nl;
     }
     prof_end(st);

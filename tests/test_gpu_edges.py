@@ -178,3 +178,33 @@ def test_reference_cache_mirror_is_incremental_and_weak():
     del ref, dc
     gc.collect()
     assert len(C._MIRRORS) == n_before - 1
+
+
+@pytest.mark.gpu
+def test_light_rows_validated_and_inert_when_empty():
+    """vc_scene_set_lights rejects malformed rows with the ValueError of the other argument
+    checks; a scene without lights builds the reference's records bit for bit."""
+    from paper_1805_09258_b200 import Scene, configs, device_scene, estimate_moments_batch
+    from paper_1805_09258_b200.scene import directional_light, point_light
+
+    base = configs.cfg3_scene(n_spheres=2, level=1)
+
+    def with_lights(rows):
+        return Scene(base.surfaces, base.medium, base.bounds_min, base.bounds_max, lights=np.array(rows))
+
+    bad_dir = directional_light((1.0, 0.0, 0.0), 1.0)
+    bad_dir[1] = 2.0  # not unit length
+    bad_kind = point_light((1.0, 1.0, 1.0), 1.0)
+    bad_kind[0] = 3.0
+    neg = point_light((1.0, 1.0, 1.0), (1.0, -1.0, 1.0))
+    for rows in ([bad_dir], [bad_kind], [neg]):
+        with pytest.raises(ValueError):
+            device_scene(with_lights(rows))
+    x = np.array([[1.3, 1.1, 2.2]])
+    kw = dict(seeds=np.array([[3, 401, 0]], np.uint32), n_angular=1024, march_step=0.25)
+    a = estimate_moments_batch(base, x, **kw)
+    b = estimate_moments_batch(with_lights(np.zeros((0, 8))), x, **kw)
+    np.testing.assert_array_equal(a.L, b.L)
+    np.testing.assert_array_equal(a.hess, b.hess)
+    c = estimate_moments_batch(with_lights([point_light((2.0, 1.5, 2.0), 5.0)]), x, **kw)
+    assert np.all(c.L > a.L)

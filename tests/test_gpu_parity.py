@@ -265,6 +265,49 @@ def test_delta_lights_lit_samples_vs_oracle():
     assert (ob.media_radiance > 0).any(axis=1).mean() > 0.5  # the lamp reaches most samples
 
 
+def test_hg_single_event_two_pass_vs_oracle():
+    """HG media with one media event per gather path keeps the two-pass gather (the emitter
+    hits are weighted 4π·p_g in the occlusion pass): per-sample media radiance and moments vs
+    the oracle (whose HG restatement is pinned to rec_media_hg.npz)."""
+    from paper_1805_09258_b200 import estimate_moments_batch, inspect_record
+    from oracle import volcache_oracle as O
+
+    z = golden("rec_delta_lights")
+    sc = golden_scene({k: z[k] for k in z.files if not k.endswith("_lights")}, "portal_")
+    n, step = 1024, 0.2
+    x = z["portal_points"][0]
+    ins = inspect_record(sc, x, rng_seed=np.random.SeedSequence([9, 401, 0]), n_angular=n, march_step=step, hg_g=0.5)
+    ob = O.build_record(O.pack(sc), x, n, step, np.random.SeedSequence([9, 401, 0]), adjacency=ins["tris"], hg_g=0.5)
+    np.testing.assert_allclose(ins["media"], ob.media_radiance, rtol=2e-6, atol=1e-30)
+    assert (ob.media_radiance > 0).any()
+    r = estimate_moments_batch(sc, x[None], seeds=np.array([[9, 401, 0]], np.uint32), n_angular=n, march_step=step,
+                               adjacency=ins["tris"][None].astype(np.int32), hg_g=0.5)
+    _check_moments("hg_two_pass", r.L[0], r.grad[0], r.hess[0], ob.L, ob.grad, ob.hess)
+
+
+def test_dark_scene_point_light_vs_oracle():
+    """cfg2 as BASELINE.json states it (no emitter, an isotropic point light, HG g = 0.3): the
+    gather is skipped (nothing emits or reflects) and the media are lit by k_gather_delta
+    alone; moments and element counts vs the oracle with the device's triangles."""
+    from paper_1805_09258_b200 import configs, estimate_moments_batch, inspect_record
+    from oracle import volcache_oracle as O
+
+    sc = configs.cfg2_spec_scene()
+    ps = O.pack(sc)
+    pts = np.array([[0.2, 0.8, 0.3], [0.5, 0.3, 0.5]])  # lit from the side; in the cube's shadow
+    n, step = 1024, 0.1
+    for i, x in enumerate(pts):
+        ins = inspect_record(sc, x, rng_seed=np.random.SeedSequence([17, 401, i]), n_angular=n, march_step=step,
+                             hg_g=0.3)
+        ob = O.build_record(ps, x, n, step, np.random.SeedSequence([17, 401, i]), adjacency=ins["tris"], hg_g=0.3)
+        np.testing.assert_allclose(ins["media"], ob.media_radiance, rtol=2e-6, atol=1e-30)
+        r = estimate_moments_batch(sc, x[None], seeds=np.array([[17, 401, i]], np.uint32), n_angular=n,
+                                   march_step=step, adjacency=ins["tris"][None].astype(np.int32), hg_g=0.3)
+        _check_moments(f"dark_point_light[{i}]", r.L[0], r.grad[0], r.hess[0], ob.L, ob.grad, ob.hess)
+        assert int(r.stats[0, 0]) == ob.stats["elements_evaluated"]
+        assert ob.L[1].min() > 0 and (ob.L[0].min() > 0) == (i == 0)
+
+
 def _tri_set(t):
     return {tuple(sorted(map(int, r))) for r in np.asarray(t)}
 

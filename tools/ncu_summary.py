@@ -31,7 +31,9 @@ def to_bytes(v, unit):
 
 # kernel → bench.py kernel class (vc_profile classes)
 CLASS = {"primary": "primary", "rings": "rings", "wave_scan": "wave_scan", "gather": "gather",
-         "gather_emit": "gather", "gather_occl": "gather", "delaunay_smem": "delaunay", "delaunay_retry": "delaunay",
+         "gather_emit": "gather", "gather_occl": "gather", "gather_eval": "gather", "gather_occl_pt": "gather",
+         "gather_delta": "gather", "gather_delta_pt": "gather", "delta_single": "assemble", "primary_pt": "primary",
+         "directions": "primary", "delaunay_smem": "delaunay", "delaunay_retry": "delaunay",
          "delaunay_hull": "delaunay", "delaunay_cap": "delaunay", "delaunay_capg": "delaunay", "cap_bin": "delaunay", "delaunay_warp": "delaunay", "delaunay_list": "delaunay",
          "delaunay_rest": "delaunay", "assemble_t": "assemble", "asm_eval": "assemble",
          "tri_compact": "tri_compact", "own_scan": "tri_compact", "tri_scatter": "tri_compact", "degree": "degree", "live_masks": "assemble", "assemble": "assemble",
