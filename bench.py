@@ -150,6 +150,8 @@ def workload(args):
         w = configs.cfg2(march_step=args.march_step or 0.1)  # point light, Henyey-Greenstein g = 0.3
         return dataclasses.replace(w, name="cfg2-single-occluder-3d+point-light+hg0.3",
                                    scene=configs.cfg2_spec_scene(), hg_g=0.3)
+    if args.config == "cfg4-standin":  # extension stand-in: cfg4's lights and occluders, homogeneous medium
+        return configs.cfg4_standin(march_step=args.march_step or 0.1)
     raise SystemExit(f"unknown config {args.config}")
 
 

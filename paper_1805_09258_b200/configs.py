@@ -193,12 +193,13 @@ def _window_wall(emission, open_windows=False):
 
 
 def cfg3_scene(n_spheres: int = 40, level: int = 3, seed: int = 2, wall_albedo: float = 0.0,
-               open_windows: bool = False, lights=()) -> Scene:
+               open_windows: bool = False, lights=(), window_emission=WINDOW_EMISSION,
+               medium: Medium | None = None) -> Scene:
     """open_windows / lights: the delta-light extension (cfg3 as BASELINE.json states it: window
     cut-outs lit by a distant directional light); the default is the reference-runnable parity
     variant with emissive portals."""
     X, Y, Z = ROOM
-    walls = _window_wall(WINDOW_EMISSION, open_windows)
+    walls = _window_wall(window_emission, open_windows)
     walls += _quad((X, 0, 0), (X, 3, 0), (X, 3, Z), (X, 0, Z), albedo=wall_albedo)  # far side
     walls += _quad((0, 0, 0), (X, 0, 0), (X, 0, Z), (0, 0, Z), albedo=wall_albedo)  # floor
     walls += _quad((0, Y, 0), (0, Y, Z), (X, Y, Z), (X, Y, 0), albedo=wall_albedo)  # ceiling
@@ -212,7 +213,7 @@ def cfg3_scene(n_spheres: int = 40, level: int = 3, seed: int = 2, wall_albedo: 
         r = rng.uniform(0.12, 0.3)
         P = c[None] + r * V
         spheres += [_tri(P[a], P[b], P[d]) for a, b, d in F]
-    return Scene(tuple(walls + spheres), Medium(0.27, 0.03), np.zeros(3), ROOM.copy(),
+    return Scene(tuple(walls + spheres), medium or Medium(0.27, 0.03), np.zeros(3), ROOM.copy(),
                  lights=np.asarray(lights, float).reshape(-1, 8))
 
 
@@ -228,6 +229,30 @@ def cfg3(n_points: int = 19000, n_spheres: int = 40, level: int = 3, n_angular: 
     sc = cfg3_scene(n_spheres, level)
     pts = np.random.default_rng(2).uniform(sc.bounds_min, sc.bounds_max, (n_points, 3))
     return Workload("cfg3-window-room-3d", sc, pts, 2, n_angular, march_step)
+
+
+# ---------------------------------------------------------------------------
+# Config 4 stand-in: cfg3's occluders, 8 seeded point lights, homogeneous medium
+# ---------------------------------------------------------------------------
+
+
+def cfg4_standin_scene(n_spheres: int = 40, level: int = 3) -> Scene:
+    """Extension, and only a stand-in: BASELINE.json's cfg4 is a heterogeneous Perlin medium
+    with ratio tracking, which the method does not cover (its ∇T, HT assume a constant σt;
+    PAPER.md:603 lists heterogeneous media as future work).  This keeps cfg4's geometry
+    (cfg3's occluder set, no emissive windows) and its 8 seeded point lights (seed 3) in a
+    homogeneous medium at the grid's nominal mean density: σt = 2 (max 4 × mean 0.5),
+    albedo 0.85."""
+    rng = np.random.default_rng(3)
+    pos = rng.uniform([0.4, 0.4, 0.4], ROOM - 0.4, (8, 3))
+    lights = [point_light(p, (3.0, 3.0, 3.0)) for p in pos]
+    return cfg3_scene(n_spheres, level, lights=lights, window_emission=0.0, medium=Medium(1.7, 0.3))
+
+
+def cfg4_standin(n_points: int = 32000, n_angular: int = 16384, march_step: float = 0.1) -> Workload:
+    sc = cfg4_standin_scene()
+    pts = np.random.default_rng(3).uniform(sc.bounds_min, sc.bounds_max, (n_points, 3))
+    return Workload("cfg4-standin-homogeneous+8-point-lights", sc, pts, 3, n_angular, march_step)
 
 
 # ---------------------------------------------------------------------------
