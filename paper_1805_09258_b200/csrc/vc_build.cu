@@ -35,6 +35,9 @@ namespace vc {
 #endif
 // the BVH-latency-bound kernels run better at 4 CTAs (≤ 64 registers): primary 1.92 →
 // 1.64 ms, occlusion 1.70 → 1.48 ms per 512 records
+#ifndef VC_PRIMARY_BS
+#define VC_PRIMARY_BS 128  // threads per k_primary CTA: 5.44 ms per 2048 records vs 5.77 at 256 (a CTA frees its slots when its slowest warp ends; 64: 5.43, 32: 5.50)
+#endif
 #ifndef VC_LB_PRIMARY
 #define VC_LB_PRIMARY 4
 #endif
@@ -83,7 +86,8 @@ __device__ __forceinline__ int tiled_direction(int t, const BuildParams& P) {
 // shadow rays through a second inlined BVH traversal — is not compiled into the kernel
 // (its register demand made the traversal spill: 308 → 16 bytes of spill stores).
 template <int D, bool REFL>
-__global__ void __launch_bounds__(256, VC_LB_PRIMARY) k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
+__global__ void __launch_bounds__(VC_PRIMARY_BS, VC_LB_PRIMARY * 256 / VC_PRIMARY_BS)
+    k_primary(DevScene S, BuildParams P, Wave W, JumpTables jt) {
   VC_RAY_STACK;
   const int n = P.n_angular;
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -3468,14 +3472,16 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   const long long nt = (long long)W.B * P.n_angular;
   prof_begin(KC_PRIMARY, st);
   if (S.reflective) {
-    k_primary<D, true><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, true>, S.geo), st>>>(S, P, W, jt);
+    k_primary<D, true><<<grid_for(nt, VC_PRIMARY_BS), VC_PRIMARY_BS, stack_smem(k_primary<D, true>, S.geo), st>>>(
+        S, P, W, jt);
   } else if (VC_PRIMARY_PT && D == 3 && S.geo.n_nodes > 0 && W.ray_cursor) {
     k_directions<D><<<grid_for(nt, 256), 256, 0, st>>>(P, W, jt);
     cudaMemsetAsync(W.ray_cursor, 0, sizeof(unsigned long long), st);
     k_primary_pt<D><<<sm_count * 8, 256, 0, st>>>(S, P, W, W.ray_cursor);
     if (kc) kc->launches += 1;
   } else {
-    k_primary<D, false><<<grid_for(nt, 256), 256, stack_smem(k_primary<D, false>, S.geo), st>>>(S, P, W, jt);
+    k_primary<D, false><<<grid_for(nt, VC_PRIMARY_BS), VC_PRIMARY_BS, stack_smem(k_primary<D, false>, S.geo), st>>>(
+        S, P, W, jt);
   }
   prof_end(st);
   int nl = 3;

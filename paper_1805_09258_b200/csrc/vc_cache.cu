@@ -489,17 +489,35 @@ struct MarchOut {
 // mode 3: final accumulation after insertion (frozen=False): each point reads the caches
 // as they were when it was reached (records of tag ≤ its ordinal), src/renderer.py:361-368
 // REFL = false: the hit's L_o is its emission (no direct-lighting code in the kernel, as k_primary)
+#ifndef VC_MARCH_BS
+#define VC_MARCH_BS 128
+#endif
+#ifndef VC_MARCH_TILE
+#define VC_MARCH_TILE 0
+#endif
 #ifndef VC_MARCH_MINB
 #define VC_MARCH_MINB 8  // resident 128-thread CTAs per SM (≤ 64 registers): cfg5 frame 235 / 230 / 216 / 190 ms at 4 / 5 / 6 / 8
 #endif
 template <bool REFL>
-__global__ void __launch_bounds__(128, VC_MARCH_MINB) k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp,
-                                               double step, int seed, const uint64_t* jit_state, JumpTables jt,
-                                               int n_light_dummy, MarchOut out, int mode) {
+__global__ void __launch_bounds__(VC_MARCH_BS, VC_MARCH_MINB * 128 / VC_MARCH_BS)
+    k_march(DevScene S, DevCache Cs, DevCache Cm, DevCamera cam, int spp, double step, int seed,
+            const uint64_t* jit_state, JumpTables jt, int n_light_dummy, MarchOut out, int mode) {
+#if VC_MARCH_TILE
+  // a warp marches an 8 × 4 pixel tile: its rays stay within a few cells of one another, so the
+  // lanes probe the same index cells and scan similar candidate lists
+  const int tiles_x = (cam.cols + 7) >> 3;
+  const int tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+  const int ry = ty * 4 + (lane >> 3), rx = tx * 8 + (lane & 7);
+  if (ry >= cam.rows || rx >= cam.cols) return;
+  const int t = ry * cam.cols + rx;
+  const int py = cam.row0 + ry, px = cam.col0 + rx;
+#else
   const int npx = cam.rows * cam.cols;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= npx) return;
   const int py = cam.row0 + t / cam.cols, px = cam.col0 + t % cam.cols;
+#endif
   const long long i = (long long)py * cam.w + px;
   if ((mode == 1 || mode == 2) && out.miss_cnt[t] == 0) return;  // finished by pass 0
   const double four_pi = 4.0 * kPi;
@@ -774,7 +792,11 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
   mo.miss_cnt = mcnt;
   mo.miss_off = moff;
   mo.hits = hits;
-  const int grid = (npx + 127) / 128;
+#if VC_MARCH_TILE
+  const int grid = (int)(((long long)((cam.rows + 3) / 4) * ((cam.cols + 7) / 8) * 32 + VC_MARCH_BS - 1) / VC_MARCH_BS);
+#else
+  const int grid = (npx + VC_MARCH_BS - 1) / VC_MARCH_BS;
+#endif
   if (rp->grow) {  // frozen = False: misses insert in (pass, pixel, step) order (src/renderer.py:361-368)
     if (rp->estimator == VC_EST_PATH) return fail(VC_EINVAL, "the path mode has no cache to grow");
     if (cam.rows != cam.h || cam.cols != cam.w) return fail(VC_EINVAL, "frozen=False renders the full image (no crop)");
@@ -799,7 +821,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     mo.c_ord = rs.c_ord;
     mo.c_val = rs.c_val;
     mo.c_n = rs.c_n;
-    VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, cs->dev(), cm->dev(), cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo,
+    VC_MARCH(S.reflective)<<<grid, VC_MARCH_BS, 0, st>>>(S, cs->dev(), cm->dev(), cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo,
                                   3);
     count_launches(1);
     e = cudaGetLastError();
@@ -816,7 +838,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
   }
   DevCache Cs = cs->dev(), Cm = cm->dev();
   prof_begin(KC_MARCH, st);
-  VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 0);
+  VC_MARCH(S.reflective)<<<grid, VC_MARCH_BS, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 0);
   prof_end(st);
   // miss offsets (device scan over npx + 1 counts, the last one zero) and the hit total
   long long* hsum = (long long*)alloc(50, 16);
@@ -844,7 +866,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     if (e != cudaSuccess) return cuda_fail(e, "miss workspace");
     mo.miss_x = mx;
     mo.miss_words = mw;
-    VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 1);
+    VC_MARCH(S.reflective)<<<grid, VC_MARCH_BS, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 1);
     vc_build_params bp{};
     bp.n_angular = rp->n_angular;
     bp.march_step = rp->march_step;
@@ -876,7 +898,7 @@ int vc_render(vc_scene* sc, vc_cache* cs, vc_cache* cm, const vc_camera* camp, c
     k_misses_J<<<(int)((nmiss + 127) / 128), 128, 0, st>>>((int)nmiss, mmom, stride, mJ);
     mo.miss_J = mJ;
     prof_begin(KC_MARCH, st);
-    VC_MARCH(S.reflective)<<<grid, 128, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 2);
+    VC_MARCH(S.reflective)<<<grid, VC_MARCH_BS, 0, st>>>(S, Cs, Cm, cam, rp->spp, rp->march_step, rp->seed, djit, jt, 0, mo, 2);
     prof_end(st);
     launches += 3;
   }
