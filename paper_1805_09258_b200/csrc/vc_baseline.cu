@@ -273,6 +273,8 @@ int baseline_impl(vc_scene* sc, int N, const double* x, const void* rng, const v
                   double* est, double* records, double* samples, cudaStream_t st) {
   if (!sc || !prm) return fail(VC_EINVAL, "null scene or params");
   if (N < 0) return fail(VC_EINVAL, "n_records must be non-negative");
+  if (sc->n_lights > 0)  // the extension covers the record build and its callers only
+    return fail(VC_EINVAL, "delta lights (vc_scene_set_lights) are not supported by the baseline estimator");
   if (N == 0) return VC_OK;
   const int D = sc->dim;
   const int n = prm->n_angular;

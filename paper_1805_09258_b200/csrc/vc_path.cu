@@ -142,6 +142,8 @@ int path_impl(vc_scene* sc, int m, const double* x, const void* rng, long long n
   if (m < 0) return fail(VC_EINVAL, "negative point count");
   if (n_samples < 1) return fail(VC_EINVAL, "n_samples must be positive");
   if (n_light_samples < 1) return fail(VC_EINVAL, "n_light_samples must be >= 1");
+  if (sc->n_lights > 0)  // the extension covers the record build and its callers only
+    return fail(VC_EINVAL, "delta lights (vc_scene_set_lights) are not supported by the path tracer");
   if (m == 0) return VC_OK;
   const int D = sc->dim;
   const bool host = flags & VC_MEM_HOST;

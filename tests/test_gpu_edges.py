@@ -206,5 +206,13 @@ def test_light_rows_validated_and_inert_when_empty():
     b = estimate_moments_batch(with_lights(np.zeros((0, 8))), x, **kw)
     np.testing.assert_array_equal(a.L, b.L)
     np.testing.assert_array_equal(a.hess, b.hess)
-    c = estimate_moments_batch(with_lights([point_light((2.0, 1.5, 2.0), 5.0)]), x, **kw)
+    lit = with_lights([point_light((2.0, 1.5, 2.0), 5.0)])
+    c = estimate_moments_batch(lit, x, **kw)
     assert np.all(c.L > a.L)
+    # the extension covers the record build and its callers; the other estimators refuse the scene
+    from paper_1805_09258_b200 import baseline_estimate, path_trace_radiance
+
+    with pytest.raises(ValueError):
+        baseline_estimate(lit, x[0], n_angular=256, rng_seed=1)
+    with pytest.raises(ValueError):
+        path_trace_radiance(lit, x[0], 64, rng_seed=1)
