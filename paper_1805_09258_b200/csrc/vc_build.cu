@@ -46,6 +46,12 @@ namespace vc {
 #endif
 // the emitter pass, since its float32 pre-filter: 4 CTAs (64 registers) 1.99 ms vs 3 CTAs
 // 2.05 ms vs 2 CTAs 2.43 ms per 512 records
+#ifndef VC_EMIT_BS
+#define VC_EMIT_BS 128  // threads per CTA of the emitter filter / fused pass (gather 11.56 vs 11.60 ms at 256)
+#endif
+#ifndef VC_EVAL_BS
+#define VC_EVAL_BS 128  // threads per CTA of the survivor evaluation (gather 11.55 vs 11.60 ms at 256)
+#endif
 #ifndef VC_LB_EMIT
 #define VC_LB_EMIT 4
 #endif
@@ -968,11 +974,11 @@ constexpr int kPendCap = 64;  // per warp: ≤ 31 left over + one step's 32
 // without spills.  MODE 2: the fused pass again for records whose evaluation found the
 // queue full (W.redo) — the others exit at once.
 template <int D, int MODE>
-__global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
+__global__ void __launch_bounds__(VC_EMIT_BS, VC_LB_EMIT * 256 / VC_EMIT_BS) k_gather_emit(DevScene S, BuildParams P, Wave W, JumpTables jt,
                                                                GatherItem* q, unsigned long long* q_count,
                                                                long long q_cap) {
   if (MODE == 2 && !W.redo[blockIdx.y]) return;
-  __shared__ PendSample pend_all[256 / 32][kPendCap];
+  __shared__ PendSample pend_all[VC_EMIT_BS / 32][kPendCap];
   __shared__ FilterPlane fplane[kEmitPlanes];
   __shared__ unsigned focc[kEmitPlanes * 32];
   const bool filt = D == 3 && S.ep.ng > 0 && S.ep.occ != nullptr;
@@ -1189,7 +1195,7 @@ __global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_emit(DevScene S, Bui
 // draws), the nearest emitter through the plane grids, emitter hits appended to the
 // occlusion queue in warp chunks.  A full queue flags the record for the fused redo pass.
 template <int D>
-__global__ void __launch_bounds__(256, VC_LB_EMIT) k_gather_eval(DevScene S, BuildParams P, Wave W, JumpTables jt,
+__global__ void __launch_bounds__(VC_EVAL_BS, VC_LB_EMIT * 256 / VC_EVAL_BS) k_gather_eval(DevScene S, BuildParams P, Wave W, JumpTables jt,
                                                                GatherItem* q, unsigned long long* q_count,
                                                                long long q_cap) {
   const int rec = blockIdx.y;
@@ -3644,15 +3650,15 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       cudaMemsetAsync(W.gather_q_count, 0, 2 * sizeof(unsigned long long), st);
       if (VC_GATHER_SPLIT && !W.dense_media) {  // filter → survivor evaluation → redo pass
         cudaMemsetAsync(W.surv_cnt, 0, sizeof(int) * 2 * (size_t)W.B, st);  // surv_cnt and redo
-        k_gather_emit<D, 1><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_emit<D, 1><<<dim3(16 * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
-        k_gather_eval<D><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_eval<D><<<dim3(16 * 256 / VC_EVAL_BS, W.B), VC_EVAL_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                       W.gather_q_cap);
-        k_gather_emit<D, 2><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_emit<D, 2><<<dim3(16 * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
         nl += 2;
       } else {
-        k_gather_emit<D, 0><<<dim3(16, W.B), 256, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_emit<D, 0><<<dim3(16 * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
       }
       const bool hg_on = D == 3 && P.hg_g != 0.0;
