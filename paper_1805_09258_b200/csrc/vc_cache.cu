@@ -54,7 +54,7 @@ __device__ inline bool record_cells(const IdxGeom& G, const double* R, int& lv, 
     if (!(lo[a] >= 0.0 && hi[a] < 1.0)) fits = false;
   }
   if (!fits) return false;
-  lv = 0;  // deepest level whose cells are ≥ span·emax (span 2: ≤ 2 cells per axis; 1: ≤ 3)
+  lv = 0;  // deepest level whose cells are ≥ span·emax (span 2: ≤ 2 cells per axis; 1: ≤ 3; 0.35: ≤ 7)
   while (lv < kMaxLevel && G.size / (double)(1 << (lv + 1)) >= G.span * emax) ++lv;
   const double s = (double)(1 << lv);
   for (int a = 0; a < 3; ++a) clo[a] = chi[a] = 0;
@@ -333,6 +333,8 @@ static int index_build(vc_cache* c, CacheIndex& X, int r0, int nr, cudaStream_t 
   G.size = c->size;
   G.inv_size = 1.0 / c->size;
   G.span = c->cell_span;
+  if (const char* es = getenv("VOLCACHE_IDX_SPAN"))  // tuning knob: the lookup span (the engine's 2 stays)
+    if (c->cell_span < 2.0) G.span = atof(es);
   const int n = nr;
   int* cnt = (int*)alloc(0, (size_t)n * 4);
   int* ovf = (int*)alloc(1, (size_t)n * 4);

@@ -104,12 +104,13 @@ struct vc_cache {
   int dim = 0, n = 0;
   int blend = 0;  // 1: baseline cache (BaselineRecord spheres, log_space_interpolate)
   double origin[3] = {0, 0, 0}, size = 0.0;
-  // Level choice: a record's cells are ≥ cell_span × its largest AABB half-extent; span 1
-  // (≤ 3 cells per axis, ~3× fewer candidates per lookup) for lookups and marches; the
-  // populate engine, which rebuilds after every window, runs with 2 (≤ 2 per axis, fewer
-  // entries to sort) and rebuilds at 1 when it finishes.  cfg5: march 377 → 224 ms per
-  // frame at span 1; populate 31.7 s at span 2 vs 42.8 s at 1.
-  double cell_span = 1.0;
+  // Level choice: a record's cells are ≥ cell_span × its largest AABB half-extent.  Lookups and
+  // marches run at 0.35 (≤ 7 cells per axis: small cells list few records that do not cover the
+  // query — cfg5 frame 377 ms at span 2, 224 at 1 on pixel strips; with the tiled march 172.5
+  // at 1, 142.0 at 0.5, 134.1 at 0.35, 142.7 at 0.25); the populate engine, which rebuilds
+  // after every window, runs with 2 (≤ 2 per axis, fewer entries to sort) and re-indexes at the
+  // lookup span when it finishes.
+  double cell_span = 0.35;
   // ix[0] covers records [0, n_main); appends up to max(4096, n_main / 4) records are indexed
   // in ix[1] alone, then everything is re-indexed into ix[0] (cache_rebuild)
   CacheIndex ix[2];
