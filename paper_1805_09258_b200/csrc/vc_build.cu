@@ -3062,7 +3062,7 @@ __global__ void __launch_bounds__(kAsmBS, EMIT ? VC_ASM_SCAN_MINB : VC_ASM_MINB)
     // lane cursor over (element, ring); liveness of media samples comes from the per-direction
     // bit masks, so the scan itself touches memory once per element (and per 64 rings)
     const unsigned long long* live = W.live + (size_t)rec * W.live_words * n;
-    constexpr int kStride = kAsmBS * kAsmSplit;  // elements interleaved across the record's CTAs
+    const int kStride = kAsmBS * (int)gridDim.x;  // elements interleaved across the record's CTAs
     int e = part * kAsmBS + threadIdx.x;
     int ring = 0;
     int vv[D];
@@ -3200,7 +3200,7 @@ __global__ void __launch_bounds__(kAsmBS, EMIT ? VC_ASM_SCAN_MINB : VC_ASM_MINB)
   // star vertices: Σ_k [idx_k ≥ 0] · deg_k · (maxc − cnt_k)  (src/subdivision.py:205-207)
   const int maxc = W.rec_maxc[rec];
   long long stars = 0;
-  for (int k = part * kAsmBS + threadIdx.x; k < n; k += kAsmBS * kAsmSplit) {
+  for (int k = part * kAsmBS + threadIdx.x; k < n; k += kAsmBS * (int)gridDim.x) {
     if (idx[k] >= 0) {
       int dg = (D == 2) ? 2 : W.deg[rb + k];
       stars += (long long)dg * (maxc - cnt[k]);
@@ -3274,7 +3274,7 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_EVAL_MINB) k_asm_eval(DevScene 
   const size_t rb = (size_t)rec * n;
   const int maxc = W.rec_maxc[rec];
   long long stars = 0;
-  for (int k = part * kAsmBS + threadIdx.x; k < n; k += kAsmBS * kAsmSplit) {
+  for (int k = part * kAsmBS + threadIdx.x; k < n; k += kAsmBS * (int)gridDim.x) {
     if (W.idx[rb + k] >= 0) {
       const int dg = (D == 2) ? 2 : W.deg[rb + k];
       stars += (long long)dg * (maxc - W.cnt[rb + k]);
@@ -3292,7 +3292,7 @@ __global__ void __launch_bounds__(kAsmBS, VC_ASM_EVAL_MINB) k_asm_eval(DevScene 
 // Fixed-order sum of the kAsmSplit partials per record (deterministic), scattered into
 // the reference layout L(3), grad(3, D), hess(3, D, D); stats.
 template <int D>
-__global__ void k_asm_final(BuildParams P, Wave W) {
+__global__ void k_asm_final(BuildParams P, Wave W, int parts) {  // parts: per-warp partials written per record
   constexpr int NQ = 1 + D + D * (D + 1) / 2;
   const int rec = blockIdx.x;
   const int tid = threadIdx.x;  // 64 threads: kind · 32 + component
@@ -3301,7 +3301,7 @@ __global__ void k_asm_final(BuildParams P, Wave W) {
   if (comp < 3 * NQ) {
     double v = 0.0;
     if (!failed)
-      for (int p = 0; p < kAsmParts; ++p) v += W.partial[((size_t)rec * kAsmParts + p) * 64 + kind * 32 + comp];
+      for (int p = 0; p < parts; ++p) v += W.partial[((size_t)rec * kAsmParts + p) * 64 + kind * 32 + comp];
     const int c = comp / NQ, t = comp - c * NQ;
     double* M = W.moments + ((size_t)rec * 2 + kind) * moment_size(D);
     if (t == 0) {
@@ -3320,7 +3320,7 @@ __global__ void k_asm_final(BuildParams P, Wave W) {
     const long long* cnt = (const long long*)(W.partial + (size_t)W.B * kAsmParts * 64);
     long long t[5] = {0, 0, 0, 0, 0};
     if (!failed)
-      for (int p = 0; p < kAsmParts; ++p)
+      for (int p = 0; p < parts; ++p)
         for (int k = 0; k < 5; ++k) t[k] += cnt[((size_t)rec * kAsmParts + p) * 5 + k];
     long long* o = W.stats + (size_t)rec * kStats;
     o[0] = t[0];
@@ -3694,14 +3694,22 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
   }
   prof_begin(KC_ASSEMBLE, st);
 
+  // CTAs per record: kAsmSplit for the 3D sizes (n ≥ 8192), fewer for short element lists — the
+  // small 2D records pay for idle CTAs otherwise (cfg1: 4.5 M records/s at 16, 3.0 M at 32)
+  int split = kAsmSplit;
+  {
+    const int E = (D == 2) ? P.n_angular : P.n_tris;
+    while (split > 2 && (long long)split * kAsmBS * 8 > E) split >>= 1;
+    if (const char* es = getenv("VOLCACHE_ASM_SPLIT")) split = std::max(1, std::min(kAsmSplit, atoi(es)));
+  }
   if (W.asm_items) {
     cudaMemsetAsync(W.asm_fb, 0, sizeof(int) * W.B, st);
-    k_assemble_t<D, true><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
-    k_asm_eval<D><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);
+    k_assemble_t<D, true><<<dim3(split, W.B), kAsmBS, 0, st>>>(S, P, W);
+    k_asm_eval<D><<<dim3(split, W.B), kAsmBS, 0, st>>>(S, P, W);
     nl += 2;
   }
-  k_assemble_t<D, false><<<dim3(kAsmSplit, W.B), kAsmBS, 0, st>>>(S, P, W);  // overflowed records
-  k_asm_final<D><<<W.B, 64, 0, st>>>(P, W);
+  k_assemble_t<D, false><<<dim3(split, W.B), kAsmBS, 0, st>>>(S, P, W);  // overflowed records
+  k_asm_final<D><<<W.B, 64, 0, st>>>(P, W, split * (kAsmBS / 32));
   ++nl;
   if (S.n_lights > 0 && S.sigma_s > 0.0) {
     k_delta_single<D><<<grid_for(W.B, 128), 128, 0, st>>>(S, W);

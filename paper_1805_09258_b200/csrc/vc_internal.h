@@ -20,12 +20,13 @@ constexpr int kBvhMaxDepth = 32;
 constexpr int kCapGMax = 32;     // binned cap kernel: bins per axis
 constexpr int kCapGCols = 1024;  // binned cap kernel: largest stratum row  // BVH depth cap = device traversal stack size
 #ifndef VC_ASM_SPLIT
-#define VC_ASM_SPLIT 16
+#define VC_ASM_SPLIT 32
 #endif
 #ifndef VC_ASM_BS
 #define VC_ASM_BS 64
 #endif
-constexpr int kAsmSplit = VC_ASM_SPLIT;  // CTAs per record in the moment assembly
+constexpr int kAsmSplit = VC_ASM_SPLIT;  // CTAs per record in the moment assembly (32: 5.21 ms per 2048 cfg3
+                                         // records; 16: 5.62, 48: 5.29, 64: 5.34, 8: 6.33)
 constexpr int kAsmBS = VC_ASM_BS;        // threads per assembly CTA
 constexpr int kAsmParts = kAsmSplit * (kAsmBS / 32);  // per-warp partial sums per record
 
