@@ -52,6 +52,12 @@ namespace vc {
 #ifndef VC_EVAL_BS
 #define VC_EVAL_BS 128  // threads per CTA of the survivor evaluation (gather 11.55 vs 11.60 ms at 256)
 #endif
+#ifndef VC_EMIT_CTAS
+#define VC_EMIT_CTAS 16  // 256-thread CTA equivalents per record in the emitter filter
+#endif
+#ifndef VC_EVAL_CTAS
+#define VC_EVAL_CTAS 16  // ... and in the survivor evaluation
+#endif
 #ifndef VC_LB_EMIT
 #define VC_LB_EMIT 4
 #endif
@@ -3650,15 +3656,15 @@ static void launch_wave_t(const DevScene& S, const BuildParams& P, const Wave& W
       cudaMemsetAsync(W.gather_q_count, 0, 2 * sizeof(unsigned long long), st);
       if (VC_GATHER_SPLIT && !W.dense_media) {  // filter → survivor evaluation → redo pass
         cudaMemsetAsync(W.surv_cnt, 0, sizeof(int) * 2 * (size_t)W.B, st);  // surv_cnt and redo
-        k_gather_emit<D, 1><<<dim3(16 * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_emit<D, 1><<<dim3(VC_EMIT_CTAS * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
-        k_gather_eval<D><<<dim3(16 * 256 / VC_EVAL_BS, W.B), VC_EVAL_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_eval<D><<<dim3(VC_EVAL_CTAS * 256 / VC_EVAL_BS, W.B), VC_EVAL_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                       W.gather_q_cap);
-        k_gather_emit<D, 2><<<dim3(16 * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_emit<D, 2><<<dim3(VC_EMIT_CTAS * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
         nl += 2;
       } else {
-        k_gather_emit<D, 0><<<dim3(16 * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
+        k_gather_emit<D, 0><<<dim3(VC_EMIT_CTAS * 256 / VC_EMIT_BS, W.B), VC_EMIT_BS, 0, st>>>(S, P, W, jt, (GatherItem*)W.gather_q, W.gather_q_count,
                                                            W.gather_q_cap);
       }
       const bool hg_on = D == 3 && P.hg_g != 0.0;
