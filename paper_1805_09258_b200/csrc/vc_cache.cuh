@@ -27,10 +27,6 @@
 #include "vc_api_internal.h"
 #include "vc_device.cuh"
 
-#ifndef VC_PROBE_PREFETCH
-#define VC_PROBE_PREFETCH 0
-#endif
-
 namespace vc {
 
 constexpr int kMaxLevel = 16;  // finest grid: 2^16 cells per axis
@@ -339,20 +335,6 @@ __device__ __forceinline__ void cache_visit(const DevCache& C, const double* x, 
     in = in && u[a] >= 0.0 && u[a] < 1.0;
   }
   if (in) {
-#if VC_PROBE_PREFETCH
-    // the hash slots of every occupied level first, as prefetches: the probes below then find
-    // their keys in cache instead of paying one DRAM / L2 round trip per level in sequence
-    for (unsigned m = C.ix[0].level_mask; m; m &= m - 1) {
-      const int k = __ffs(m) - 1;
-      const double s = (double)(1u << k);
-      unsigned long long cell = 0;
-#pragma unroll
-      for (int a = D - 1; a >= 0; --a) cell = (cell << k) | (unsigned long long)min((int)floor(u[a] * s), (1 << k) - 1);
-      const unsigned long long key = (unsigned long long)k << C.ix[0].key_shift | cell;
-      const unsigned long long* slot = C.ix[0].hkey + hash_slot(key, C.ix[0].hbits);
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(slot));
-    }
-#endif
     for (unsigned m = C.ix[0].level_mask | C.ix[1].level_mask; m; m &= m - 1) {
       const int k = __ffs(m) - 1;
       const double s = (double)(1u << k);
