@@ -492,6 +492,7 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
   W.run_stride = (int)(media_per / 16 + 1);
   W.run_dir = (int*)alloc(48, (size_t)B * W.run_stride * 4);
   W.lo = (double*)alloc(7, B * n * 24);
+  W.emit_tab = sc->reflective ? nullptr : sc->d_emission;  // non-reflective: L_o = emission[idx], lo unused
   W.rec_R = (int*)alloc(8, B * 4);
   W.rec_P = (int*)alloc(9, B * 4);
   W.rec_maxc = (int*)alloc(10, B * 4);

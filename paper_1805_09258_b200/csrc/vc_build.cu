@@ -135,9 +135,11 @@ __global__ void __launch_bounds__(VC_PRIMARY_BS, VC_LB_PRIMARY * 256 / VC_PRIMAR
   if constexpr (D == 3) W.dirs32[base] = make_float4((float)d[0], (float)d[1], (float)d[2], 0.0f);
   W.s[base] = s;
   W.idx[base] = id;
-  W.lo[base * 3 + 0] = L[0];
-  W.lo[base * 3 + 1] = L[1];
-  W.lo[base * 3 + 2] = L[2];
+  if (REFL || !W.emit_tab) {  // (non-reflective: the readers take emission[idx] themselves)
+    W.lo[base * 3 + 0] = L[0];
+    W.lo[base * 3 + 1] = L[1];
+    W.lo[base * 3 + 2] = L[2];
+  }
 }
 
 // Persistent-lane primary pass (non-reflective scenes with a BVH; VC_PRIMARY_PT): the
@@ -386,10 +388,14 @@ __global__ void __launch_bounds__(kRingBS) k_rings(BuildParams P, Wave W) {
       for (int m = (j0 + kGatherRun - 1) / kGatherRun; m * kGatherRun < j0 + c; ++m)
         W.run_dir[(size_t)rec * W.run_stride + m] = k;
       const double* lo = W.lo + g * 3;
+      if (W.emit_tab) {  // non-reflective scene: the surface radiance is the hit's emission
+        const int id = W.idx[g];
+        lo = id >= 0 ? W.emit_tab + (size_t)id * 3 : nullptr;
+      }
       DirInfo di;
       di.s = s[k];
       di.cnt = c;
-      di.surf_live = (lo[0] > 0.0 || lo[1] > 0.0 || lo[2] > 0.0) ? 1 : 0;
+      di.surf_live = (lo && (lo[0] > 0.0 || lo[1] > 0.0 || lo[2] > 0.0)) ? 1 : 0;
       W.info[g] = di;
     }
     run += tot;
@@ -2860,6 +2866,8 @@ struct AsmCtx {
   const int* cnt;
   const int* pre;
   const double* lo;
+  const int* idx;          // with emit: surface radiance = emit[idx[v]] (non-reflective scenes)
+  const double* emit;
   const float* media;
   double x[3];
   double step;
@@ -2875,6 +2883,8 @@ __device__ __forceinline__ AsmCtx<D> asm_ctx(const BuildParams& P, const Wave& W
   c.cnt = W.cnt + rb;
   c.pre = W.pre + rb;
   c.lo = W.lo + rb * 3;
+  c.idx = W.idx + rb;
+  c.emit = W.emit_tab;
   c.media = W.media + (size_t)W.rec_base[rec] * 3;
 #pragma unroll
   for (int a = 0; a < D; ++a) c.x[a] = W.x[rec * D + a];
@@ -2902,9 +2912,14 @@ __device__ __forceinline__ bool asm_item(const DevScene& S, const AsmCtx<D>& C, 
   double rad[3];
   const int vrep = rep == 0 ? v[0] : (rep == 1 || D == 2 ? v[1] : v[D - 1]);
   if (kind == 0) {
-    rad[0] = C.lo[vrep * 3 + 0];
-    rad[1] = C.lo[vrep * 3 + 1];
-    rad[2] = C.lo[vrep * 3 + 2];
+    const double* lo = C.lo + (size_t)vrep * 3;
+    if (C.emit) {
+      const int id = C.idx[vrep];
+      lo = C.emit + (size_t)(id >= 0 ? id : 0) * 3;  // (a surface item's representative is live: id ≥ 0)
+    }
+    rad[0] = lo[0];
+    rad[1] = lo[1];
+    rad[2] = lo[2];
   } else {
     const float* m = C.media + (size_t)(C.pre[vrep] + ring) * 3;
     rad[0] = m[0];

@@ -161,7 +161,9 @@ struct Wave {
   int* pre;              // B × n exclusive prefix of cnt within the record
   int* run_dir;          // B × run_stride: direction of media sample 16·m (gather runs)
   int run_stride;
-  double* lo;            // B × n × 3 surface radiance
+  double* lo;            // B × n × 3 surface radiance (reflective scenes)
+  const double* emit_tab;  // non-reflective scenes: L_o = emission[idx] (DevScene::emission), lo is not
+                           // written or read (nullptr: read lo)
   int* rec_R;            // B rings per record
   int* rec_P;            // B live media samples per record
   int* rec_maxc;         // B max cnt (rings that carry any live sample)
