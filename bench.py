@@ -69,6 +69,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # first calls outside the timed region: NVML's lazy set-up inside it stalled the launching
+            # thread for ~70 ms in 2 of 10 runs (GPU idle between steps, per-kernel sums unchanged)
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         except Exception:
             self.nv = None
         self.period = period
@@ -80,7 +84,7 @@ class ClockSampler:
             "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
             "hw_power_brake_slowdown": 0x80,
         }
-        while not self._stop.is_set():
+        while not self._stop.wait(self.period):  # samples at period, 2·period, … into the timed region
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
@@ -89,7 +93,6 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            self._stop.wait(self.period)
 
     def __enter__(self):
         if self.nv is not None:
@@ -101,6 +104,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join()
+        if self.nv is not None and not self.samples:  # a timed region shorter than one period
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
@@ -504,9 +512,14 @@ def main():
         barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
+        step_ev = []
         for s in range(args.warmup, total_steps):
             res = estimate_moments_batch(w.scene, Xs[s], seeds=Ss[s], **kw)
             stats_acc.append(res.stats)
+            if os.environ.get("BENCH_STEP_EVENTS"):  # debug: where inside the region the time goes
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                step_ev.append((e, time.perf_counter()))
             if world > 1:  # the exchange before a lookup pass: every rank gets every record
                 dist.all_gather_into_tensor(gathered, res.records.reshape(-1))
         ev1.record(stream)
@@ -514,6 +527,9 @@ def main():
         barrier()
     launches = L.vc_kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1)
+    if step_ev:
+        print("step end (ms, device | host):", [(round(ev0.elapsed_time(e), 2), round((t - step_ev[0][1]) * 1e3, 2))
+                                               for e, t in step_ev], file=sys.stderr)
     kms = np.zeros(12)
     kcnt = np.zeros(12, np.int64)
     L.vc_profile_read(_lib.ptr(kms), _lib.ptr(kcnt), 12)
