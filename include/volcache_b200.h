@@ -40,6 +40,7 @@ extern "C" {
 #define VC_MAKE_RECORDS 4 /* also finalize records (make_record) into `records` */
 #define VC_ISOTROPIC 8    /* make_record(..., anisotropic=False) */
 #define VC_TRACE_BOUNDS 16 /* vc_trace: trace_or_bounds semantics */
+#define VC_DEFER_CHECK 32 /* vc_build_records with device arrays: do not wait for the bounds check */
 
 typedef struct vc_scene vc_scene;
 typedef struct vc_cache vc_cache;
@@ -73,6 +74,13 @@ void vc_scene_destroy(vc_scene* scene);
  * src/transport.py:288-310) and the cache point itself (closed-form value, gradient and
  * Hessian with the point visibility held constant).  Call before building records; 0 clears. */
 int vc_scene_set_lights(vc_scene* scene, int n_lights, const double* rows);
+/* Deferred bounds check.  vc_build_records raises the reference's ValueError for a point outside
+ * the medium bounds (src/subdivision.py:155-158); with device arrays that needs one host read of
+ * a device flag per call.  With VC_DEFER_CHECK in params->flags the call returns as soon as its
+ * work is enqueued (a flagged wave still builds no rings) and the flag is OR-ed into a word
+ * that this function reads and clears: VC_EOUTSIDE if any deferred call of this host thread since
+ * the last read saw a point outside the bounds.  Synchronises `stream`. */
+int vc_check_deferred(void* stream);
 /* Scratch budget for one record wave (bytes; default a third of device memory, ≤ 64 GiB). */
 int vc_scene_set_budget(vc_scene* scene, int64_t bytes);
 

@@ -14,6 +14,7 @@ from .records import (
     CacheRecord,
     DeviceScene,
     Moments,
+    check_deferred,
     device_scene,
     estimate_moments,
     estimate_moments_batch,
@@ -39,7 +40,7 @@ __all__ = [
     "BaselineEstimate", "TransportDerivativeEstimate", "baseline_estimate", "fd_derivatives", "log_gradient_radius",
     "log_space_interpolate", "make_baseline_record", "occlusion_unaware_gradient", "path_trace_radiance",
     "DEFAULT_N_ANGULAR", "BatchResult", "CacheRecord", "DeviceScene", "Moments", "RadianceCache",
-    "Medium", "Scene", "Surface", "cache_from_records", "device_scene", "estimate_moments",
+    "Medium", "Scene", "Surface", "cache_from_records", "check_deferred", "device_scene", "estimate_moments",
     "estimate_moments_batch", "inspect_record", "interpolate", "load_scene", "make_record",
     "make_records", "render_frozen", "save_scene", "seed_words", "surface_radiance_batch",
 ]

@@ -25,6 +25,7 @@ VC_MEM_HOST = 1
 VC_SEED_WORDS = 2
 VC_MAKE_RECORDS = 4
 VC_ISOTROPIC = 8
+VC_DEFER_CHECK = 32
 VC_TRACE_BOUNDS = 16
 
 _dp = C.POINTER(C.c_double)
@@ -141,6 +142,7 @@ _SIGS = {
                                   C.POINTER(_vp)]),
     "vc_scene_destroy": (None, [_vp]),
     "vc_scene_set_budget": (C.c_int, [_vp, C.c_int64]),
+    "vc_check_deferred": (C.c_int, [_vp]),
     "vc_scene_set_lights": (C.c_int, [_vp, C.c_int, _vp]),
     "vc_build_records": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.POINTER(BuildParams), _vp, _vp, _vp, _vp]),
     "vc_build_inspect": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(BuildParams), _vp, _vp, _vp, _vp, _vp, _vp,

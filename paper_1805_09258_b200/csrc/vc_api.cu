@@ -98,6 +98,39 @@ int check_begin(const vc_scene* sc, long long N, const double* x, bool host, con
   return VC_OK;
 }
 
+// Deferred form (VC_DEFER_CHECK): the wave's flag is OR-ed into a sticky per-thread device word on
+// the stream and the call returns without waiting; vc_check_deferred reads and clears the word.
+__global__ void k_flag_or(int* sticky, const int* flag) {
+  if (*flag) atomicOr(sticky, 1);
+}
+
+static int* sticky_flag() {
+  static thread_local int* d = nullptr;
+  if (!d && cudaMalloc(&d, 4) == cudaSuccess) cudaMemset(d, 0, 4);
+  return d;
+}
+
+int check_defer(InsideCheck* ck, cudaStream_t st) {
+  if (!ck->pending) return VC_OK;
+  ck->pending = false;
+  int* sticky = sticky_flag();
+  if (!sticky) return fail(VC_ECUDA, "bounds check (deferred flag allocation)");
+  k_flag_or<<<1, 1, 0, st>>>(sticky, ck->dflag);
+  count_launches(1);
+  return VC_OK;
+}
+
+int check_deferred_read(cudaStream_t st) {
+  int* sticky = sticky_flag();
+  if (!sticky) return fail(VC_ECUDA, "bounds check (deferred flag allocation)");
+  int h = 0;
+  cudaError_t e = cudaMemcpyAsync(&h, sticky, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(sticky, 0, 4, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "bounds check");
+  return h ? fail(VC_EOUTSIDE, "subdivision center lies outside the medium bounds (deferred check)") : VC_OK;
+}
+
 int check_end(InsideCheck* ck) {
   if (!ck->pending) return VC_OK;
   ck->pending = false;
@@ -609,7 +642,11 @@ int build_impl(vc_scene* sc, int N, const double* x, const void* rng, const int3
     }
   }
   g_launches += kc.launches;
-  if (const int rc = check_end(&inside)) return rc;
+  if (!host && (prm->flags & VC_DEFER_CHECK)) {
+    if (const int rc = check_defer(&inside, st)) return rc;
+  } else if (const int rc = check_end(&inside)) {
+    return rc;
+  }
   if (host) {
     err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) return cuda_fail(err, "record build");
@@ -1020,6 +1057,8 @@ int vc_scene_set_lights(vc_scene* sc, int n_lights, const double* rows) {
   sc->n_lights = n_lights;
   return VC_OK;
 }
+
+int vc_check_deferred(void* stream) { return check_deferred_read((cudaStream_t)stream); }
 
 int vc_scene_set_budget(vc_scene* sc, int64_t bytes) {
   if (!sc || bytes <= 0) return fail(VC_EINVAL, "invalid budget");

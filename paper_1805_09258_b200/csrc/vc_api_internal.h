@@ -53,6 +53,8 @@ struct InsideCheck {
 int check_begin(const vc_scene* sc, long long N, const double* x, bool host, const char* what, cudaStream_t st,
                 InsideCheck* ck);
 int check_end(InsideCheck* ck);
+int check_defer(InsideCheck* ck, cudaStream_t st);
+int check_deferred_read(cudaStream_t st);
 
 }  // namespace vc
 

@@ -280,13 +280,17 @@ class BatchResult:
 
 def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None, march_step=0.1,
                            n_inner=1, n_light_samples=16, adjacency=None, epsilon=None,
-                           anisotropic=True, stream=None, media_bounces=1, hg_g=0.0) -> BatchResult:
+                           anisotropic=True, stream=None, media_bounces=1, hg_g=0.0,
+                           defer_check=False) -> BatchResult:
     """Batch record build: N cache points in one call (moments, stats, optional records).
 
     X is (N, d) host numpy or a CUDA torch tensor (then every output is a CUDA tensor
     and the call is asynchronous on `stream`).  Per-record RNG: `seeds` (N, w) uint32
     SeedSequence entropy words — e.g. rows (cfg_seed, 401, i), src/renderer.py:317 —
     or `rng_states` (N, 4) uint64 PCG64 states.  `epsilon` set → also make_record.
+    With CUDA inputs the reference's ValueError for a point outside the bounds needs one host
+    read of a device flag per call; `defer_check=True` returns without it (successive calls
+    then queue back to back) and `check_deferred()` raises for all of them at once.
     """
     ds = device_scene(scene)
     d = ds.dim
@@ -298,6 +302,8 @@ def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None
         flags |= _lib.VC_MAKE_RECORDS
     if not anisotropic:
         flags |= _lib.VC_ISOTROPIC
+    if on_dev and defer_check:
+        flags |= _lib.VC_DEFER_CHECK
     N = int(X.shape[0])
     if N == 0:
         return BatchResult(d, np.zeros((0, 2, moment_size(d))), np.zeros((0, 8), np.int64),
@@ -337,6 +343,16 @@ def estimate_moments_batch(scene, X, seeds=None, rng_states=None, n_angular=None
                                            _lib.C.byref(p), _lib.ptr(mom), _lib.ptr(stats), _lib.ptr(recs),
                                            stream))
     return BatchResult(d, mom, stats, recs)
+
+
+def check_deferred(stream=None) -> None:
+    """Raise the ValueError of every `defer_check=True` build since the last call whose points
+    left the medium bounds (vc_check_deferred); synchronises the stream."""
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().vc_check_deferred(stream))
 
 
 def inspect_record(scene, x, rng_seed=None, n_angular=None, march_step=0.1, n_inner=1,

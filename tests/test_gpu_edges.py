@@ -63,6 +63,34 @@ def test_device_tensor_outside_bounds_raises():
     assert np.all(np.isfinite(r.moments.cpu().numpy()))
 
 
+def test_deferred_bounds_check():
+    """defer_check=True queues device-resident builds without the per-call host read of the
+    bounds flag; check_deferred() raises once for any of them (and clears the flag), the
+    results of the in-bounds calls equal the checked calls'."""
+    import torch
+
+    from paper_1805_09258_b200 import check_deferred, configs, estimate_moments_batch, seed_words
+
+    w = configs.cfg2()
+    X = np.array(w.points[:8])
+    Xd = torch.tensor(X, device="cuda")
+    S = torch.tensor(seed_words(w.seed, 401, range(8)).astype(np.int32), device="cuda")
+    kw = dict(seeds=S, n_angular=256, march_step=0.1)
+    a = estimate_moments_batch(w.scene, Xd, **kw)
+    b = estimate_moments_batch(w.scene, Xd, defer_check=True, **kw)
+    c = estimate_moments_batch(w.scene, Xd, defer_check=True, **kw)
+    check_deferred()  # nothing outside: no error
+    torch.testing.assert_close(a.moments, b.moments, rtol=0, atol=0)
+    torch.testing.assert_close(a.moments, c.moments, rtol=0, atol=0)
+    bad = Xd.clone()
+    bad[5] = torch.tensor([0.5, 7.5, 0.5], dtype=torch.float64)
+    estimate_moments_batch(w.scene, bad, defer_check=True, **kw)  # returns: the check is pending
+    estimate_moments_batch(w.scene, Xd, defer_check=True, **kw)   # a later good call does not clear it
+    with pytest.raises(ValueError, match="outside the medium bounds"):
+        check_deferred()
+    check_deferred()  # cleared by the read
+
+
 _TRANSLATED = (
     "import numpy as np, sys; sys.path.insert(0, '.');"
     "from paper_1805_09258_b200 import configs, inspect_record;"
